@@ -1,0 +1,176 @@
+/*
+ * gfors.h — C ABI of the B200-native GFORS hot path (arXiv 2510.27117).
+ *
+ * GFORS solves the binary integer program (eq. bip)
+ *
+ *     min  x'Qx + c'x + c0   s.t.  K x >= r (GE rows) | K x = r (EQ) | K x <= r (LE),  x in {0,1}^n
+ *
+ * with Alg. 1: Preprocess, then a device loop of UpdatePenalty ->
+ * FirstOrderStep (Alg. 2, PDHG on the rho-penalised saddle form)
+ * -> every k_int iterations k_r rounds of RandSampleStep (Alg. 3) + EvalBest
+ * -> CheckHalt; finally EvalBest(round(x_k)).
+ * Everything after gfors_load runs in this library's sm_100a kernels.  No CPU fallback.
+ *
+ * Call order: gfors_create -> gfors_load -> gfors_preprocess -> gfors_run* ->
+ * gfors_best_incumbent -> gfors_destroy.  Any other order returns GFORS_E_STATE.
+ * All functions return a gfors_status; no C++ exception crosses this boundary.  On error
+ * gfors_last_error() returns a message naming the offending argument/field/index.
+ * Threading: one context per (process, GPU); a context must not be used concurrently.
+ * Ownership: the library copies every input at the call and retains no caller pointer; the
+ * caller owns every output buffer it passes.  Host pointers are plain host memory (pinned or
+ * pageable); device pointers are CUDA device memory of the context's device.
+ */
+#ifndef GFORS_H
+#define GFORS_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    GFORS_OK = 0,
+    GFORS_NO_INCUMBENT = 2, /* SPEC L674 exit 2: run finished, no feasible sample found */
+    GFORS_E_INPUT = 3,      /* SPEC L674 exit 3: invalid argument / instance */
+    GFORS_E_DIVERGED = 4,   /* SPEC L674 exit 4: non-finite indicator (NaN guard) */
+    GFORS_E_CUDA = 5,       /* CUDA runtime error (message has the CUDA error string) */
+    GFORS_E_NCCL = 6,       /* NCCL unavailable or failed (world > 1) */
+    GFORS_E_STATE = 7,      /* wrong call order */
+    GFORS_E_OOM = 8         /* device allocation failed */
+} gfors_status;
+
+typedef struct gfors_ctx gfors_ctx;
+
+/* Device/rank options.  stream: a cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream)
+ * or NULL for a library-owned stream.  rank/world: sample-sharded data parallelism
+ * (DESIGN.md §7): rank r draws global sample words [r*W, (r+1)*W).  nccl_id: 128-byte
+ * ncclUniqueId (identical on all ranks) when world > 1, else NULL. */
+typedef struct {
+    int32_t device;
+    void *stream;
+    int32_t rank, world;
+    const void *nccl_id;
+} gfors_device_opts;
+
+/* Problem in USER form.  CSR K (m x n): k_rowptr[m+1] (nondecreasing, [0]=0),
+ * k_col[nnz] (strictly increasing within a row, in [0,n)), k_val[nnz] (finite, nonzero);
+ * r[m]; sense[m] in {+1 GE, 0 EQ, -1 LE}.  Q (n x n, symmetric, full storage; q_rowptr NULL
+ * means Q = 0); c[n]; c0; maximize != 0 maximises.  mem_space: 0 host pointers, 1 device
+ * pointers.  Requirements: 0 < n < 2^31, nnz(K), nnz(Q) < 2^31. */
+typedef struct {
+    int64_t n, m;
+    int32_t mem_space;
+    const int64_t *k_rowptr;
+    const int32_t *k_col;
+    const double *k_val;
+    const double *r;
+    const int8_t *sense;
+    const int64_t *q_rowptr;
+    const int32_t *q_col;
+    const double *q_val;
+    const double *c;
+    double c0;
+    int32_t maximize;
+} gfors_problem;
+
+/* Preprocess options.  precision: 64 -> fp64 iterates,
+ * 32 -> fp32 iterates (sums accumulate in fp64 either way; Preprocess is always fp64). */
+typedef struct {
+    double tol;        /* power-iteration relative-change tolerance, default 1e-7 */
+    int32_t max_iter;  /* power-iteration sweeps, default 500 */
+    int32_t precision; /* 64 (default) or 32 */
+} gfors_prep_opts;
+
+/* Scaling record: obj_scale = ||Q||_2 + ||c||_2 (1 if 0), k_scale = ||D^-1 K||_2
+ * (1 if 0), zero_rows = rows of K with no nonzero (kept with row scale 1). */
+typedef struct {
+    double obj_scale, k_scale;
+    int64_t zero_rows;
+} gfors_scaling;
+
+/* Alg. 1 parameters (SPEC L293, L632-635, L667 defaults via gfors_params_default). */
+typedef struct {
+    double sigma;                 /* tau1 = tau2 = sqrt(sigma), 0 < sigma < 1 */
+    int32_t k_int, k_r;           /* sampling interval, rounds per trigger */
+    int64_t k_b;                  /* samples per round PER RANK, multiple of 64 */
+    double rho_min, rho_max, growth_T, growth_p, rho_delta; /* UpdatePenalty */
+    double tol_primal, tol_dual, tol_binary, stall_rel;     /* CheckHalt */
+    int32_t stall_window;         /* W checks, 1..1024 */
+    int64_t max_iters;
+    double time_limit_s;
+    uint64_t seed;                /* Philox key */
+    int32_t use_graph;            /* 1: CUDA graph with a device WHILE node (default); 0: eager */
+    int32_t trace_cap;            /* trace ring-buffer rows (default 4096) */
+} gfors_params;
+
+/* halt_reason: 1 criteria met, 2 max_iters, 3 time limit, 4 diverged. */
+typedef struct {
+    int64_t iters, rounds, candidates;
+    int32_t halt_reason;
+    double elapsed_s;   /* device time of the loop (CUDA events), Preprocess excluded */
+    int64_t n_trace;    /* trace rows written (ring keeps the last trace_cap) */
+} gfors_run_info;
+
+typedef struct {
+    int64_t found_iter, found_round, found_index; /* round/index -1: final round(x_k) */
+    double found_time_s;                          /* %globaltimer since loop start */
+    int32_t has_incumbent;
+} gfors_incumbent_info;
+
+void gfors_params_default(gfors_params *p);
+void gfors_prep_opts_default(gfors_prep_opts *p);
+
+gfors_status gfors_create(gfors_ctx **out, const gfors_device_opts *opts);
+/* Validates (CSR invariants, finiteness, Q symmetry, sense) and canonicalises (maximise ->
+ * negate; LE -> GE by negation; rows stably permuted GE first), builds the device
+ * layouts (CSR K, CSR K', CSR Q) and classifies rows for the evaluator.  Copies inputs. */
+gfors_status gfors_load(gfors_ctx *ctx, const gfors_problem *prob);
+/* Preprocess on the device (row norms, power iterations).  out may be NULL. */
+gfors_status gfors_preprocess(gfors_ctx *ctx, const gfors_prep_opts *opts, gfors_scaling *out);
+/* Alg. 1 from x0 = 0.5*1, y0 = 0 (reading R14).  Blocks until the loop has finished.
+ * Collective when world > 1 (all ranks must call with identical params except k_b). */
+gfors_status gfors_run(gfors_ctx *ctx, const gfors_params *p, gfors_run_info *out);
+/* z: objective in ORIGINAL units and sense (+inf if none); x: n bytes (0/1) or NULL (host).
+ * Returns GFORS_NO_INCUMBENT if no feasible point was found. */
+gfors_status gfors_best_incumbent(gfors_ctx *ctx, double *z, uint8_t *x, gfors_incumbent_info *info);
+const char *gfors_last_error(const gfors_ctx *ctx);
+void gfors_destroy(gfors_ctx *ctx);
+
+/* ---------------- hooks for parity tests and benchmarks (same library, host buffers) ------- */
+/* Preprocess results: row scale divisors s_j (m, canonical row order), and the scaled saddle
+ * vectors r (m) and c (n) as fp64.  Any pointer may be NULL. */
+gfors_status gfors_get_scaled(gfors_ctx *ctx, double *row_scale, double *r_scaled, double *c_scaled);
+/* RandSampleStep of p (n, host fp64 in [0,1]) for global words [word_begin, word_begin+n_words):
+ * bits[i*n_words + w] (host).  Same contract as the loop's sampler (DESIGN.md §3 R10). */
+gfors_status gfors_sample(gfors_ctx *ctx, const double *p, uint64_t seed, uint32_t round_id,
+                          int64_t word_begin, int64_t n_words, uint64_t *bits);
+/* EvalBest pieces on a host batch bits[n][n_words]: feasible[64*n_words] (0/1) and z (canonical
+ * minimisation objective, original units). */
+gfors_status gfors_eval(gfors_ctx *ctx, const uint64_t *bits, int64_t n_words, uint8_t *feasible, double *z);
+/* Set/get the PDHG iterate (host fp64; y in canonical row order). */
+gfors_status gfors_set_state(gfors_ctx *ctx, const double *x, const double *xbar, const double *y);
+gfors_status gfors_get_state(gfors_ctx *ctx, double *x, double *xbar, double *y);
+/* iters Alg. 2 steps with fixed rho, tau1, tau2 (no sampling, no halting). */
+gfors_status gfors_step(gfors_ctx *ctx, int64_t iters, double rho, double tau1, double tau2);
+/* Indicators after the last step: out[0]=primal_gap, [1]=||s^x||, [2]=||s^y||, [3]=binary_gap. */
+gfors_status gfors_indicators(gfors_ctx *ctx, double rho, double tau1, double tau2, double *out);
+/* Trace rows of the last run (8 doubles: iter, rho, primal_gap, sx, sy, binary_gap,
+ * z_best canonical, improved), oldest first; returns rows copied in *n_rows. */
+gfors_status gfors_get_trace(gfors_ctx *ctx, double *rows, int64_t max_rows, int64_t *n_rows);
+/* Kernel timing of one loop block (bench): runs `blocks` blocks eagerly with CUDA events
+ * around every launch; ms_out[k] = mean duration of kernel class k, names via
+ * gfors_kernel_class_name(k); n_classes out.  Uses p as in gfors_run; state is reset. */
+gfors_status gfors_profile_blocks(gfors_ctx *ctx, const gfors_params *p, int32_t blocks,
+                                  double *ms_out, int32_t max_classes, int32_t *n_classes);
+const char *gfors_kernel_class_name(int32_t k);
+/* Number of kernel launches per loop block for p (bench "gpu_launches" accounting). */
+int64_t gfors_launches_per_block(gfors_ctx *ctx, const gfors_params *p);
+/* Cross-rank incumbent merge rule (host-only, no GPU needed): given world records
+ * (z, global sample index, flags) pick the winner: lowest z among valid, ties -> lowest index.
+ * Returns the winning record position or -1. */
+int32_t gfors_merge_records(const double *z, const int64_t *index, const int32_t *valid, int32_t world);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

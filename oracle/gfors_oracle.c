@@ -537,33 +537,41 @@ int orc_indicators(const orc_ctx *o, double rho, double tau1, double tau2, doubl
 /* RandSampleStep (Alg. 3) under the Philox bit-plane contract */
 /* (reading R10).  Literal: all 32 planes are drawn for every lane.            */
 /* ------------------------------------------------------------------------- */
+static uint64_t sample_word(double p, uint32_t i, uint64_t wg, uint32_t round_id, const uint32_t key[2]) {
+    /* T_i = ceil(p_i * 2^32), exact in fp64 (p outside [0,1] is clamped) */
+    double pi = p < 0.0 ? 0.0 : (p > 1.0 ? 1.0 : p);
+    uint64_t T = (uint64_t)ceil(pi * 4294967296.0);
+    uint64_t plane[32];
+    for (uint32_t q = 0; q < 16; ++q) {
+        uint32_t ctr[4] = {i, (uint32_t)wg, q, round_id}, o4[4];
+        orc_philox4x32_10(ctr, key, o4);
+        plane[2 * q] = (uint64_t)o4[0] | ((uint64_t)o4[1] << 32);
+        plane[2 * q + 1] = (uint64_t)o4[2] | ((uint64_t)o4[3] << 32);
+    }
+    uint64_t word = 0;
+    for (int b = 0; b < 64; ++b) {
+        uint64_t u = 0;  /* plane 0 is the most significant bit of u */
+        for (int t = 0; t < 32; ++t) u |= ((plane[t] >> b) & 1u) << (31 - t);
+        uint64_t xb = (u < T) ? 1u : 0u;  /* Bernoulli(p_i) */
+        word |= xb << b;
+    }
+    return word;
+}
+
 void orc_sample(const double *p, int64_t n, uint64_t seed, uint32_t round_id,
                 int64_t word_begin, int64_t n_words, uint64_t *bits) {
     const uint32_t key[2] = {(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32)};
-    for (int64_t i = 0; i < n; ++i) {
-        /* T_i = ceil(p_i * 2^32), exact in fp64 (p outside [0,1] is clamped) */
-        double pi = p[i] < 0.0 ? 0.0 : (p[i] > 1.0 ? 1.0 : p[i]);
-        double Td = ceil(pi * 4294967296.0);
-        uint64_t T = (uint64_t)Td;
-        for (int64_t w = 0; w < n_words; ++w) {
-            uint64_t wg = (uint64_t)(word_begin + w);
-            uint64_t plane[32];
-            for (uint32_t q = 0; q < 16; ++q) {
-                uint32_t ctr[4] = {(uint32_t)i, (uint32_t)wg, q, round_id}, o4[4];
-                orc_philox4x32_10(ctr, key, o4);
-                plane[2 * q] = (uint64_t)o4[0] | ((uint64_t)o4[1] << 32);
-                plane[2 * q + 1] = (uint64_t)o4[2] | ((uint64_t)o4[3] << 32);
-            }
-            uint64_t word = 0;
-            for (int b = 0; b < 64; ++b) {
-                uint64_t u = 0;  /* plane 0 is the most significant bit of u */
-                for (int t = 0; t < 32; ++t) u |= ((plane[t] >> b) & 1u) << (31 - t);
-                uint64_t xb = (u < T) ? 1u : 0u;  /* Bernoulli(p_i) */
-                word |= xb << b;
-            }
-            bits[i * n_words + w] = word;
-        }
-    }
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t w = 0; w < n_words; ++w)
+            bits[i * n_words + w] = sample_word(p[i], (uint32_t)i, (uint64_t)(word_begin + w), round_id, key);
+}
+
+void orc_sample_subset(const double *p_sub, const int64_t *idx, int64_t count, uint64_t seed,
+                       uint32_t round_id, int64_t word_begin, int64_t n_words, uint64_t *bits) {
+    const uint32_t key[2] = {(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32)};
+    for (int64_t k = 0; k < count; ++k)
+        for (int64_t w = 0; w < n_words; ++w)
+            bits[k * n_words + w] = sample_word(p_sub[k], (uint32_t)idx[k], (uint64_t)(word_begin + w), round_id, key);
 }
 
 /* ------------------------------------------------------------------------- */

@@ -83,6 +83,10 @@ int orc_indicators(const orc_ctx *o, double rho, double tau1, double tau2, doubl
 void orc_sample(const double *p, int64_t n, uint64_t seed, uint32_t round_id,
                 int64_t word_begin, int64_t n_words, uint64_t *bits);
 
+/* Same contract for a subset of variables: bits[k*n_words + w] for variable idx[k]. */
+void orc_sample_subset(const double *p_sub, const int64_t *idx, int64_t count, uint64_t seed,
+                       uint32_t round_id, int64_t word_begin, int64_t n_words, uint64_t *bits);
+
 /* Evaluate a bit-sliced batch on the ORIGINAL canonical data (SPEC L147-155,
  * L138-146): feasible[l] in {0,1}, z[l] canonical (minimisation) objective. */
 int orc_eval(const orc_ctx *o, const uint64_t *bits, int64_t n_words,

@@ -84,6 +84,7 @@ def _declare(L):
     L.orc_step.argtypes = [P, D, D, D]
     L.orc_indicators.argtypes = [P, D, D, D, P]
     L.orc_sample.argtypes = [P, I64, C.c_uint64, C.c_uint32, I64, I64, P]
+    L.orc_sample_subset.argtypes = [P, P, I64, C.c_uint64, C.c_uint32, I64, I64, P]
     L.orc_eval.argtypes = [P, P, I64, P, P]
     L.orc_eval_point.argtypes = [P, P, P, P]
     L.orc_halt_init.argtypes = [C.POINTER(OrcHaltState), D, D, D, D, C.c_int]
@@ -123,6 +124,14 @@ def sample(p, seed, round_id, word_begin, n_words):
     p = np.ascontiguousarray(p, dtype=np.float64)
     bits = np.zeros((p.shape[0], n_words), dtype=np.uint64)
     lib().orc_sample(_ptr(p), p.shape[0], seed, round_id, word_begin, n_words, _ptr(bits))
+    return bits
+
+
+def sample_subset(p_sub, idx, seed, round_id, word_begin, n_words):
+    p_sub = np.ascontiguousarray(p_sub, dtype=np.float64)
+    idx = np.ascontiguousarray(idx, dtype=np.int64)
+    bits = np.zeros((idx.shape[0], n_words), dtype=np.uint64)
+    lib().orc_sample_subset(_ptr(p_sub), _ptr(idx), idx.shape[0], seed, round_id, word_begin, n_words, _ptr(bits))
     return bits
 
 

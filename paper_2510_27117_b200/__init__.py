@@ -1,0 +1,290 @@
+"""paper_2510_27117_b200 — B200-native GFORS hot path (arXiv 2510.27117).
+
+Thin ctypes binding of ``libgfors.so`` (C ABI in include/gfors.h).  Argument marshalling only:
+every step of the method runs in the library's sm_100a kernels.  There is no CPU fallback —
+if the library is missing this module raises on import.
+
+    s = Solver(device=0)
+    s.load(inst)                  # gfors_load     (numpy arrays -> host, torch CUDA tensors -> device)
+    s.preprocess()                # gfors_preprocess
+    info = s.run(max_iters=...)   # gfors_run
+    z, x, meta = s.best_incumbent()
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgfors.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} not found: build it with `python -m paper_2510_27117_b200.build` "
+        "(nvcc, sm_100a).  There is no CPU fallback."
+    )
+_lib = C.CDLL(LIB_PATH)
+
+P = C.c_void_p
+I32, I64, U64, D = C.c_int32, C.c_int64, C.c_uint64, C.c_double
+
+STATUS = {0: "OK", 2: "NO_INCUMBENT", 3: "E_INPUT", 4: "E_DIVERGED", 5: "E_CUDA", 6: "E_NCCL", 7: "E_STATE", 8: "E_OOM"}
+
+
+class GforsError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"gfors {STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class DeviceOpts(C.Structure):
+    _fields_ = [("device", I32), ("stream", P), ("rank", I32), ("world", I32), ("nccl_id", P)]
+
+
+class Problem(C.Structure):
+    _fields_ = [("n", I64), ("m", I64), ("mem_space", I32), ("k_rowptr", P), ("k_col", P), ("k_val", P),
+                ("r", P), ("sense", P), ("q_rowptr", P), ("q_col", P), ("q_val", P), ("c", P),
+                ("c0", D), ("maximize", I32)]
+
+
+class PrepOpts(C.Structure):
+    _fields_ = [("tol", D), ("max_iter", I32), ("precision", I32)]
+
+
+class Scaling(C.Structure):
+    _fields_ = [("obj_scale", D), ("k_scale", D), ("zero_rows", I64)]
+
+
+class Params(C.Structure):
+    _fields_ = [("sigma", D), ("k_int", I32), ("k_r", I32), ("k_b", I64),
+                ("rho_min", D), ("rho_max", D), ("growth_T", D), ("growth_p", D), ("rho_delta", D),
+                ("tol_primal", D), ("tol_dual", D), ("tol_binary", D), ("stall_rel", D),
+                ("stall_window", I32), ("max_iters", I64), ("time_limit_s", D), ("seed", U64),
+                ("use_graph", I32), ("trace_cap", I32)]
+
+
+class RunInfo(C.Structure):
+    _fields_ = [("iters", I64), ("rounds", I64), ("candidates", I64), ("halt_reason", I32),
+                ("elapsed_s", D), ("n_trace", I64)]
+
+
+class IncumbentInfo(C.Structure):
+    _fields_ = [("found_iter", I64), ("found_round", I64), ("found_index", I64), ("found_time_s", D),
+                ("has_incumbent", I32)]
+
+
+EXPORTS = {
+    "gfors_params_default": (None, [C.POINTER(Params)]),
+    "gfors_prep_opts_default": (None, [C.POINTER(PrepOpts)]),
+    "gfors_create": (I32, [C.POINTER(P), C.POINTER(DeviceOpts)]),
+    "gfors_load": (I32, [P, C.POINTER(Problem)]),
+    "gfors_preprocess": (I32, [P, C.POINTER(PrepOpts), C.POINTER(Scaling)]),
+    "gfors_run": (I32, [P, C.POINTER(Params), C.POINTER(RunInfo)]),
+    "gfors_best_incumbent": (I32, [P, P, P, C.POINTER(IncumbentInfo)]),
+    "gfors_last_error": (C.c_char_p, [P]),
+    "gfors_destroy": (None, [P]),
+    "gfors_get_scaled": (I32, [P, P, P, P]),
+    "gfors_sample": (I32, [P, P, U64, C.c_uint32, I64, I64, P]),
+    "gfors_eval": (I32, [P, P, I64, P, P]),
+    "gfors_set_state": (I32, [P, P, P, P]),
+    "gfors_get_state": (I32, [P, P, P, P]),
+    "gfors_step": (I32, [P, I64, D, D, D]),
+    "gfors_indicators": (I32, [P, D, D, D, P]),
+    "gfors_get_trace": (I32, [P, P, I64, P]),
+    "gfors_profile_blocks": (I32, [P, C.POINTER(Params), I32, P, I32, P]),
+    "gfors_kernel_class_name": (C.c_char_p, [I32]),
+    "gfors_launches_per_block": (I64, [P, C.POINTER(Params)]),
+    "gfors_merge_records": (I32, [P, P, P, I32]),
+}
+for _name, (_res, _args) in EXPORTS.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+
+def lib():
+    return _lib
+
+
+def default_params(**kw) -> Params:
+    p = Params()
+    _lib.gfors_params_default(C.byref(p))
+    for k, v in kw.items():
+        if not hasattr(p, k):
+            raise TypeError(f"unknown parameter {k!r}")
+        setattr(p, k, v)
+    return p
+
+
+def merge_records(z, index, valid):
+    """Host-side cross-rank incumbent merge rule of the library (no GPU needed)."""
+    z = np.ascontiguousarray(z, dtype=np.float64)
+    idx = np.ascontiguousarray(index, dtype=np.int64)
+    v = np.ascontiguousarray(valid, dtype=np.int32)
+    return int(_lib.gfors_merge_records(z.ctypes.data_as(P), idx.ctypes.data_as(P), v.ctypes.data_as(P), len(z)))
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):  # torch tensor
+        return P(a.data_ptr())
+    return a.ctypes.data_as(P)
+
+
+class Solver:
+    """One gfors context on one GPU."""
+
+    def __init__(self, device: int = 0, stream=None, rank: int = 0, world: int = 1):
+        opts = DeviceOpts(device, P(stream) if stream else None, rank, world, None)
+        h = P()
+        rc = _lib.gfors_create(C.byref(h), C.byref(opts))
+        if rc != 0:
+            raise GforsError(rc, "gfors_create failed")
+        self.h = h
+        self.n = self.m = 0
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.gfors_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _chk(self, rc, ok=(0,)):
+        if rc not in ok:
+            raise GforsError(rc, _lib.gfors_last_error(self.h).decode())
+        return rc
+
+    # ------------------------------------------------------------------ boundary calls
+    def load(self, inst: dict):
+        """gfors_load.  inst: dict of the user-form arrays (see gen/instances.py).  numpy arrays are
+        passed as host memory; torch CUDA tensors as device memory (all arrays must agree)."""
+        keep = []
+        is_dev = any(hasattr(v, "is_cuda") and v.is_cuda for v in inst.values())
+
+        def arr(key, dt):
+            v = inst.get(key)
+            if v is None:
+                return None
+            if is_dev:
+                keep.append(v)
+                return v
+            a = np.ascontiguousarray(v, dtype=dt)
+            keep.append(a)
+            return a
+
+        pr = Problem()
+        pr.n, pr.m = int(inst["n"]), int(inst["m"])
+        pr.mem_space = 1 if is_dev else 0
+        pr.k_rowptr = _ptr(arr("k_rowptr", np.int64))
+        pr.k_col = _ptr(arr("k_col", np.int32))
+        pr.k_val = _ptr(arr("k_val", np.float64))
+        pr.r = _ptr(arr("r", np.float64))
+        pr.sense = _ptr(arr("sense", np.int8))
+        pr.q_rowptr = _ptr(arr("q_rowptr", np.int64))
+        pr.q_col = _ptr(arr("q_col", np.int32))
+        pr.q_val = _ptr(arr("q_val", np.float64))
+        pr.c = _ptr(arr("c", np.float64))
+        pr.c0 = float(inst.get("c0", 0.0))
+        pr.maximize = int(bool(inst.get("maximize", False)))
+        self._chk(_lib.gfors_load(self.h, C.byref(pr)))
+        self.n, self.m = pr.n, pr.m
+        return self
+
+    def preprocess(self, tol=1e-7, max_iter=500, precision=64):
+        o = PrepOpts(tol, max_iter, precision)
+        sc = Scaling()
+        self._chk(_lib.gfors_preprocess(self.h, C.byref(o), C.byref(sc)))
+        return {"obj_scale": sc.obj_scale, "k_scale": sc.k_scale, "zero_rows": sc.zero_rows}
+
+    def run(self, params: Params | None = None, **kw):
+        p = params or default_params(**kw)
+        info = RunInfo()
+        rc = _lib.gfors_run(self.h, C.byref(p), C.byref(info))
+        res = {f: getattr(info, f) for f, _ in RunInfo._fields_}
+        if rc == 4:
+            res["diverged"] = True
+            return res
+        self._chk(rc)
+        res["diverged"] = False
+        return res
+
+    def best_incumbent(self, want_x=True):
+        z = C.c_double()
+        x = np.zeros(self.n, dtype=np.uint8) if want_x else None
+        info = IncumbentInfo()
+        self._chk(_lib.gfors_best_incumbent(self.h, C.byref(z), _ptr(x), C.byref(info)), ok=(0, 2))
+        meta = {f: getattr(info, f) for f, _ in IncumbentInfo._fields_}
+        return z.value, x, meta
+
+    # ------------------------------------------------------------------ test / bench hooks
+    def scaled(self):
+        s = np.zeros(self.m); r = np.zeros(self.m); c = np.zeros(self.n)
+        self._chk(_lib.gfors_get_scaled(self.h, _ptr(s), _ptr(r), _ptr(c)))
+        return s, r, c
+
+    def sample(self, p, seed, round_id, word_begin, n_words):
+        p = np.ascontiguousarray(p, dtype=np.float64)
+        bits = np.zeros((self.n, n_words), dtype=np.uint64)
+        self._chk(_lib.gfors_sample(self.h, _ptr(p), seed, round_id, word_begin, n_words, _ptr(bits)))
+        return bits
+
+    def eval(self, bits):
+        bits = np.ascontiguousarray(bits, dtype=np.uint64)
+        nw = bits.shape[1]
+        feas = np.zeros(64 * nw, dtype=np.uint8)
+        z = np.zeros(64 * nw)
+        self._chk(_lib.gfors_eval(self.h, _ptr(bits), nw, _ptr(feas), _ptr(z)))
+        return feas, z
+
+    def set_state(self, x, xbar, y):
+        a = [np.ascontiguousarray(v, dtype=np.float64) for v in (x, xbar, y)]
+        self._chk(_lib.gfors_set_state(self.h, _ptr(a[0]), _ptr(a[1]), _ptr(a[2])))
+
+    def get_state(self):
+        x = np.zeros(self.n); xb = np.zeros(self.n); y = np.zeros(self.m)
+        self._chk(_lib.gfors_get_state(self.h, _ptr(x), _ptr(xb), _ptr(y)))
+        return x, xb, y
+
+    def step(self, iters, rho, tau1, tau2):
+        self._chk(_lib.gfors_step(self.h, iters, rho, tau1, tau2))
+
+    def indicators(self, rho, tau1, tau2):
+        out = np.zeros(4)
+        self._chk(_lib.gfors_indicators(self.h, rho, tau1, tau2, _ptr(out)))
+        return {"primal_gap": out[0], "sx": out[1], "sy": out[2], "dual_gap": out[1] + out[2],
+                "binary_gap": out[3]}
+
+    def trace(self, max_rows=1 << 20):
+        rows = np.zeros((max_rows, 8))
+        nr = C.c_int64()
+        self._chk(_lib.gfors_get_trace(self.h, _ptr(rows), max_rows, C.byref(nr)))
+        return rows[: nr.value]
+
+    def profile_blocks(self, blocks, params: Params | None = None, **kw):
+        p = params or default_params(**kw)
+        ms = np.zeros(16)
+        nc = C.c_int32()
+        self._chk(_lib.gfors_profile_blocks(self.h, C.byref(p), blocks, _ptr(ms), 16, C.byref(nc)))
+        return {_lib.gfors_kernel_class_name(k).decode(): float(ms[k]) for k in range(nc.value)}
+
+    def launches_per_block(self, params: Params | None = None, **kw):
+        p = params or default_params(**kw)
+        return int(_lib.gfors_launches_per_block(self.h, C.byref(p)))
+
+
+def solve(inst, precision=64, device=0, **params):
+    """Convenience: load -> preprocess -> run -> best_incumbent."""
+    s = Solver(device)
+    s.load(inst)
+    s.preprocess(precision=precision)
+    info = s.run(**params)
+    z, x, meta = s.best_incumbent()
+    return z, x, info, meta

@@ -1,0 +1,121 @@
+// common.cuh — shared device types and helpers of the GFORS B200 library (sm_100a).
+// Nothing here is shared with oracle/ (the CPU oracle is an independent implementation).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace gfors {
+
+// Storage class of a sparse matrix's values (chosen at load).
+//  SIGN: every value of row j equals rsign[j] in {+1,-1}  -> no value array at all
+//  I8  : integral values with |v| <= 127                   -> int8 per nonzero
+//  F64 : anything else                                     -> fp64 per nonzero
+enum KKind : int { KV_SIGN = 0, KV_I8 = 1, KV_F64 = 2 };
+
+// Device-resident loop control, written only by device kernels inside the loop
+// (UpdatePenalty / CheckHalt / EvalBest bookkeeping live here so the host never syncs).
+struct Ctrl {
+    long long blk;          // sampling blocks completed == UpdatePenalty counter n (reading R7)
+    long long k;            // PDHG iterations completed
+    double rho, tau1, tau2; // current penalty and steps
+    long long max_blocks;   // number of full blocks allowed by max_iters
+    unsigned long long t0_ns, deadline_ns;
+    int halt;               // 0 running, 1 criteria, 2 max_iters, 3 time, 4 diverged
+    int improved;           // incumbent improved within the current block
+    long long since_improve;
+    long long checks;
+    long long rounds;
+    long long n_trace;
+    int has_inc;
+    double z_best;          // canonical (minimisation) objective, original units
+    long long found_iter, found_round, found_index;
+    unsigned long long found_ns;
+    int win_lane;           // winning lane of the last argmin (-1 none)
+    int pad0;
+    double ind[4];          // primal_gap, ||s^x||, ||s^y||, binary_gap of the last trigger
+};
+
+struct HaltPar {
+    double tol[3];
+    double stall_rel;
+    int window;
+    int trace_cap;
+    int k_int, k_r;
+    long long k_b_total;   // samples per round over all ranks
+};
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Philox4x32-10 (Salmon et al., SC'11) — the generator fixed by reading R10.
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+    const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u, W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r > 0) { k.x += W0; k.y += W1; }
+        const uint32_t lo0 = M0 * c.x, hi0 = __umulhi(M0, c.x);
+        const uint32_t lo1 = M1 * c.z, hi1 = __umulhi(M1, c.z);
+        c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    }
+    return c;
+}
+
+template <typename T> __device__ __forceinline__ T ldg(const T* p) { return __ldg(p); }
+
+// value of nonzero p of a K-like matrix in the given storage class
+template <int KIND>
+__device__ __forceinline__ double kval(const void* vals, long long p) {
+    if constexpr (KIND == KV_I8) return (double)__ldg(reinterpret_cast<const int8_t*>(vals) + p);
+    else if constexpr (KIND == KV_F64) return __ldg(reinterpret_cast<const double*>(vals) + p);
+    else return 1.0;
+}
+
+// deterministic butterfly sum over a group of SUB lanes (SUB power of two <= 32)
+template <int SUB>
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+    for (int o = SUB / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, SUB);
+    return v;
+}
+
+__device__ __forceinline__ double warp_sum(double v) { return group_sum<32>(v); }
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// fixed-order block reduction (sum) of one double per thread; result valid in thread 0
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) sh[wid] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (wid == 0) {
+        r = (lane < NT / 32) ? sh[lane] : 0.0;
+        r = warp_sum(r);
+    }
+    return r;
+}
+template <int NT>
+__device__ __forceinline__ double block_max(double v, double* sh) {
+    v = warp_max(v);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) sh[wid] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (wid == 0) {
+        r = (lane < NT / 32) ? sh[lane] : 0.0;
+        r = warp_max(r);
+    }
+    return r;
+}
+
+}  // namespace gfors

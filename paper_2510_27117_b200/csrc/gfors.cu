@@ -1,0 +1,1528 @@
+// gfors.cu — C ABI (include/gfors.h) and device runtime of the B200 GFORS hot path.
+//
+// Host side: validation + canonicalisation + layout planning (once per gfors_load), the device
+// Preprocess driver, and the loop driver, which captures one Alg. 1 sampling block
+// (k_int PDHG iterations, indicators, k_r x [sample, evaluate, argmin], CheckHalt) into the body
+// of a CUDA-graph WHILE node whose condition is set on the device by the CheckHalt kernel, so
+// a whole gfors_run is one graph launch with no host synchronisation inside the loop.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <cmath>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/gfors.h"
+#include "common.cuh"
+#include "pdhg.cuh"
+#include "prep.cuh"
+#include "sample_eval.cuh"
+
+using namespace gfors;
+
+namespace {
+
+constexpr int NT = 256;
+constexpr int NUM_SMS_B200 = 148;
+
+struct Err {
+    gfors_status st;
+    std::string msg;
+};
+
+#define CK(call)                                                                              \
+    do {                                                                                      \
+        cudaError_t e__ = (call);                                                             \
+        if (e__ != cudaSuccess)                                                               \
+            throw Err{e__ == cudaErrorMemoryAllocation ? GFORS_E_OOM : GFORS_E_CUDA,          \
+                      std::string(#call) + ": " + cudaGetErrorString(e__)};                   \
+    } while (0)
+
+[[noreturn]] void input_error(const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    throw Err{GFORS_E_INPUT, buf};
+}
+
+template <typename X>
+X* dalloc(size_t count) {
+    if (count == 0) count = 1;
+    void* p = nullptr;
+    CK(cudaMalloc(&p, count * sizeof(X)));
+    return reinterpret_cast<X*>(p);
+}
+template <typename X>
+X* dupload(const std::vector<X>& v, cudaStream_t s) {
+    X* p = dalloc<X>(v.size());
+    if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(X), cudaMemcpyHostToDevice, s));
+    return p;
+}
+
+int grid_for(long long work, int per_thread = 1) {
+    long long b = (work / per_thread + NT - 1) / NT;
+    if (b < 1) b = 1;
+    if (b > NUM_SMS_B200 * 8) b = NUM_SMS_B200 * 8;
+    return (int)b;
+}
+
+int pick_sub(double mean_len) {
+    if (mean_len <= 2.5) return 2;
+    if (mean_len <= 6) return 4;
+    if (mean_len <= 12) return 8;
+    if (mean_len <= 24) return 16;
+    return 32;
+}
+
+struct HostSeg {
+    std::vector<long long> seg_start, row_seg;
+    std::vector<int> seg_row;
+};
+
+// split each row of a CSR into segments of at most seg nonzeros
+HostSeg make_segments(const std::vector<int64_t>& ptr, long long rows, long long seg) {
+    HostSeg h;
+    h.row_seg.resize(rows + 1);
+    h.row_seg[0] = 0;
+    for (long long r = 0; r < rows; ++r) {
+        const long long len = ptr[r + 1] - ptr[r];
+        const long long ns = len == 0 ? 0 : (len + seg - 1) / seg;
+        for (long long k = 0; k < ns; ++k) {
+            h.seg_start.push_back(ptr[r] + k * seg);
+            h.seg_row.push_back((int)r);
+        }
+        h.row_seg[r + 1] = h.row_seg[r] + ns;
+    }
+    h.seg_start.push_back(ptr[rows]);
+    return h;
+}
+
+struct DevSeg {
+    long long* seg_start = nullptr;
+    int* seg_row = nullptr;
+    long long* row_seg = nullptr;
+    long long nseg = 0;
+    SegPlan plan() const { return SegPlan{seg_start, seg_row, row_seg, nseg}; }
+};
+
+struct DirPlan {  // how one product direction (K rows or K' columns) is computed
+    int sub = 32;
+    bool seg = false;
+    long long seg_len = 1024;
+    DevSeg ds;
+};
+
+DirPlan plan_direction(const std::vector<int64_t>& ptr, long long rows, cudaStream_t s,
+                       std::vector<void*>& owned) {
+    DirPlan d;
+    const long long nnz = ptr[rows];
+    long long maxlen = 0;
+    for (long long r = 0; r < rows; ++r) maxlen = std::max<long long>(maxlen, ptr[r + 1] - ptr[r]);
+    const double mean = rows ? (double)nnz / (double)rows : 0.0;
+    d.sub = pick_sub(mean);
+    // long or few rows: fixed-length segments, one warp each (>= 8 warps per SM of work)
+    const long long groups = rows;
+    d.seg = (maxlen > 4096) || (groups * 32 < (long long)NUM_SMS_B200 * 2048 && nnz > (long long)NUM_SMS_B200 * 1024);
+    if (d.seg) {
+        long long L = 1024;
+        while (L > 128 && nnz / L < (long long)NUM_SMS_B200 * 16) L /= 2;
+        d.seg_len = L;
+        HostSeg h = make_segments(ptr, rows, L);
+        d.ds.seg_start = dupload(h.seg_start, s);
+        d.ds.seg_row = dupload(h.seg_row, s);
+        d.ds.row_seg = dupload(h.row_seg, s);
+        d.ds.nseg = (long long)h.seg_row.size();
+        owned.push_back(d.ds.seg_start);
+        owned.push_back(d.ds.seg_row);
+        owned.push_back(d.ds.row_seg);
+    }
+    return d;
+}
+
+const char* kClassNames[] = {"pdhg_dual", "pdhg_primal", "trig_rows", "trig_cols", "sample",
+                             "feas", "obj", "argmin", "halt"};
+enum KClass { KC_DUAL = 0, KC_PRIMAL, KC_TRIGR, KC_TRIGC, KC_SAMPLE, KC_FEAS, KC_OBJ, KC_ARGMIN, KC_HALT, KC_N };
+
+}  // namespace
+
+// =============================================================================================
+// CheckHalt + UpdatePenalty + loop control, one block of 256 threads
+// =============================================================================================
+__global__ void __launch_bounds__(256) k_halt(Ctrl* __restrict__ ctrl, HaltPar hp, const double* __restrict__ part1,
+                                              int nb1, const double* __restrict__ part2, int nb2, long long n,
+                                              double* __restrict__ hist, const double* __restrict__ rho_tab,
+                                              long long nrho, double* __restrict__ trace,
+                                              cudaGraphConditionalHandle handle, int use_handle) {
+    __shared__ double sh[32];
+    __shared__ double ind[4];
+    reduce_indicators(part1, nb1, part2, nb2, n, sh, ind);
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    const double pg = ind[0], dg = ind[1] + ind[2], bg = ind[3];
+    for (int a = 0; a < 4; ++a) ctrl->ind[a] = ind[a];
+    const int improved = ctrl->improved;
+    ctrl->improved = 0;
+    ctrl->since_improve = improved ? 0 : ctrl->since_improve + 1;
+    const int W = hp.window;
+    const long long slot = ctrl->checks % W;
+    hist[slot] = pg; hist[W + slot] = dg; hist[2 * W + slot] = bg;
+    ctrl->checks += 1;
+    int halt = 0;
+    if (!isfinite(pg) || !isfinite(dg) || !isfinite(bg)) {
+        halt = 4;
+    } else {
+        const double v[3] = {pg, dg, bg};
+        bool all_ok = true;
+        for (int a = 0; a < 3; ++a) {
+            bool ok = v[a] <= hp.tol[a];
+            if (!ok && ctrl->checks >= W) {
+                double mx = hist[a * W], mn = hist[a * W];
+                for (int s = 1; s < W; ++s) { mx = fmax(mx, hist[a * W + s]); mn = fmin(mn, hist[a * W + s]); }
+                const double den = fabs(mx) > 1e-300 ? fabs(mx) : 1e-300;
+                ok = (mx - mn) / den < hp.stall_rel;
+            }
+            all_ok = all_ok && ok;
+        }
+        if (all_ok && ctrl->since_improve >= W) halt = 1;
+        else if (globaltimer_ns() >= ctrl->deadline_ns) halt = 3;
+        else if (ctrl->blk + 1 >= ctrl->max_blocks) halt = 2;
+    }
+    const long long k = (ctrl->blk + 1) * hp.k_int;
+    if (hp.trace_cap > 0) {
+        double* row = trace + 8 * (ctrl->n_trace % hp.trace_cap);
+        row[0] = (double)k; row[1] = ctrl->rho; row[2] = pg; row[3] = ind[1]; row[4] = ind[2];
+        row[5] = bg; row[6] = ctrl->z_best; row[7] = improved;
+    }
+    ctrl->n_trace += 1;
+    ctrl->blk += 1;
+    ctrl->k = k;
+    ctrl->rho = rho_tab[ctrl->blk < nrho ? ctrl->blk : nrho - 1];
+    ctrl->halt = halt;
+    if (use_handle) cudaGraphSetConditional(handle, halt ? 0u : 1u);
+}
+
+__global__ void k_loop_start(Ctrl* ctrl, double time_limit_s) {
+    const unsigned long long t = globaltimer_ns();
+    ctrl->t0_ns = t;
+    const double lim = time_limit_s * 1e9;
+    ctrl->deadline_ns = lim >= 1.8e19 ? ~0ull : t + (unsigned long long)lim;
+}
+
+// =============================================================================================
+// Context
+// =============================================================================================
+struct gfors_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr, cap_stream = nullptr;
+    bool own_stream = false;
+    int rank = 0, world = 1;
+    std::string err;
+    int stage = 0;  // 0 created, 1 loaded, 2 preprocessed
+
+    // ---- canonical problem (host) ----
+    long long n = 0, m = 0, m1 = 0, m2 = 0, nnz = 0, qnnz = 0;
+    bool maximize = false, integral = false, hasq = false;
+    double c0 = 0.0;
+    std::vector<int64_t> kptr, ktptr, qptr;
+    std::vector<int32_t> kcol, ktrow, qcol;
+    std::vector<double> kval, ktval, qval, ru, c;
+    std::vector<int64_t> perm;
+    std::vector<signed char> rsign;
+    int kkind = KV_F64;
+
+    // ---- device problem ----
+    long long *d_kptr = nullptr, *d_ktptr = nullptr, *d_qptr = nullptr;
+    int *d_kcol = nullptr, *d_ktrow = nullptr, *d_qcol = nullptr;
+    void *d_kval = nullptr, *d_ktval = nullptr;
+    double *d_qval = nullptr, *d_c = nullptr, *d_ru = nullptr;
+    signed char* d_rsign = nullptr;
+    DirPlan pd, pp;  // dual (rows of K), primal (rows of K')
+    double* d_segpart = nullptr;
+    double* d_segpart2 = nullptr;
+    long long segpart_len = 0;
+    // evaluator plan
+    struct CountList {
+        int* row = nullptr;
+        int* t = nullptr;
+        signed char* rel = nullptr;
+        signed char* B = nullptr;
+        long long nrows = 0;
+        int sub = 32;
+    } cnt[3];  // BMAX 1, 2, 8
+    int* d_int_row = nullptr;
+    long long* d_int_rhs = nullptr;
+    signed char* d_int_eq = nullptr;
+    long long* d_int_seg_start = nullptr;
+    int* d_int_seg_slot = nullptr;
+    long long n_int = 0, n_int_seg = 0;
+    int* d_real_row = nullptr;
+    long long n_real = 0;
+    bool never_feasible = false;
+    std::vector<void*> owned;
+
+    // ---- Preprocess ----
+    double* d_s = nullptr;
+    double omega = 1.0, kappa = 1.0;
+    long long zero_rows = 0;
+    int precision = 64;
+    void *d_g = nullptr, *d_rh = nullptr, *d_cs = nullptr, *d_qs = nullptr;
+    void *d_x[2] = {nullptr, nullptr}, *d_xb[2] = {nullptr, nullptr}, *d_y[2] = {nullptr, nullptr}, *d_w = nullptr;
+    double* d_tmp[4] = {nullptr, nullptr, nullptr, nullptr};
+    double* d_red = nullptr;  // reduction partials
+    double* d_scalar = nullptr;
+
+    // ---- loop ----
+    Ctrl* d_ctrl = nullptr;
+    double* d_part1 = nullptr;
+    double* d_part2 = nullptr;
+    int nb1 = 1, nb2 = 1;
+    double* d_hist = nullptr;
+    double* d_rho = nullptr;
+    long long nrho = 0, rho_cap = 0;
+    double* d_trace = nullptr;
+    int trace_cap = 0;
+    unsigned char* d_xbest = nullptr;
+    uint64_t* d_X = nullptr;
+    long long X_words = 0;
+    unsigned long long* d_viol = nullptr;
+    unsigned long long* d_iacc = nullptr;
+    long long iacc_len = 0;
+    void* d_zpart = nullptr;
+    long long zpart_len = 0;
+    double* d_z = nullptr;
+    long long z_len = 0;
+    int obj_chunk = 2048;
+    long long hk = 0;  // iterations done in hook mode (parity)
+    bool have_run = false;
+    gfors_run_info last_info{};
+
+    // graph cache
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    gfors_params gkey{};
+    int gkey_W = -1;
+    bool gvalid = false;
+
+    // profiling
+    bool profiling = false;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_ev;
+    long long launches = 0;
+
+    ~gfors_ctx();
+    void free_problem();
+    void free_prep();
+};
+
+static void dfree(void* p) {
+    if (p) cudaFree(p);
+}
+
+void gfors_ctx::free_problem() {
+    for (void* p : owned) dfree(p);
+    owned.clear();
+    d_kptr = d_ktptr = d_qptr = nullptr;
+    d_kcol = d_ktrow = d_qcol = nullptr;
+    d_kval = d_ktval = nullptr;
+    d_qval = d_c = d_ru = nullptr;
+    d_rsign = nullptr;
+    for (auto& c : cnt) c = CountList{};
+    d_int_row = nullptr; d_int_rhs = nullptr; d_int_eq = nullptr; d_int_seg_start = nullptr; d_int_seg_slot = nullptr;
+    d_real_row = nullptr;
+    pd = DirPlan{}; pp = DirPlan{};
+}
+
+void gfors_ctx::free_prep() {
+    void** ps[] = {(void**)&d_s, &d_g, &d_rh, &d_cs, &d_qs, &d_x[0], &d_x[1], &d_xb[0], &d_xb[1], &d_y[0], &d_y[1],
+                   &d_w, (void**)&d_tmp[0], (void**)&d_tmp[1], (void**)&d_tmp[2], (void**)&d_tmp[3],
+                   (void**)&d_red, (void**)&d_scalar, (void**)&d_segpart, (void**)&d_segpart2, (void**)&d_part1,
+                   (void**)&d_part2, (void**)&d_hist, (void**)&d_rho, (void**)&d_trace, (void**)&d_xbest,
+                   (void**)&d_X, (void**)&d_viol, (void**)&d_iacc, &d_zpart, (void**)&d_z, (void**)&d_ctrl};
+    for (void** p : ps) { dfree(*p); *p = nullptr; }
+    X_words = iacc_len = zpart_len = z_len = 0;
+    rho_cap = 0;
+    trace_cap = 0;
+    if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }
+    if (graph) { cudaGraphDestroy(graph); graph = nullptr; }
+    gvalid = false;
+}
+
+gfors_ctx::~gfors_ctx() {
+    cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
+    free_prep();
+    free_problem();
+    if (cap_stream) cudaStreamDestroy(cap_stream);
+    if (own_stream && stream) cudaStreamDestroy(stream);
+}
+
+// =============================================================================================
+// Load: validate, canonicalise, layouts (a1)
+// =============================================================================================
+static void validate_csr(long long rows, long long cols, const int64_t* ptr, const int32_t* idx, const double* val,
+                         const char* name) {
+    if (ptr[0] != 0) input_error("%s: row_ptr[0] must be 0", name);
+    for (long long r = 0; r < rows; ++r) {
+        if (ptr[r + 1] < ptr[r]) input_error("%s: row_ptr decreases at row %lld", name, r);
+        for (long long p = ptr[r]; p < ptr[r + 1]; ++p) {
+            if (idx[p] < 0 || idx[p] >= cols) input_error("%s: column index out of range at nonzero %lld", name, p);
+            if (p > ptr[r] && idx[p] <= idx[p - 1])
+                input_error("%s: column indices not strictly increasing in row %lld", name, r);
+            if (!std::isfinite(val[p])) input_error("%s: non-finite value at nonzero %lld", name, p);
+            if (val[p] == 0.0) input_error("%s: explicit zero at nonzero %lld", name, p);
+        }
+    }
+}
+
+static bool is_int53(double v) { return std::isfinite(v) && v == std::floor(v) && std::fabs(v) < 9007199254740992.0; }
+
+template <typename X>
+static std::vector<X> fetch(const X* p, size_t count, int mem_space) {
+    std::vector<X> v(count);
+    if (count == 0) return v;
+    if (mem_space == 1) CK(cudaMemcpy(v.data(), p, count * sizeof(X), cudaMemcpyDeviceToHost));
+    else memcpy(v.data(), p, count * sizeof(X));
+    return v;
+}
+
+// CSR transpose by counting sort (column order stable -> ascending row within each column)
+static void transpose(long long rows, long long cols, const std::vector<int64_t>& ptr, const std::vector<int32_t>& idx,
+                      const std::vector<double>& val, std::vector<int64_t>& tptr, std::vector<int32_t>& tidx,
+                      std::vector<double>& tval) {
+    const long long nnz = ptr[rows];
+    tptr.assign(cols + 1, 0);
+    for (long long p = 0; p < nnz; ++p) tptr[idx[p] + 1]++;
+    for (long long i = 0; i < cols; ++i) tptr[i + 1] += tptr[i];
+    std::vector<int64_t> pos(tptr.begin(), tptr.end() - 1);
+    tidx.resize(nnz);
+    tval.resize(nnz);
+    for (long long r = 0; r < rows; ++r)
+        for (long long p = ptr[r]; p < ptr[r + 1]; ++p) {
+            const long long q = pos[idx[p]]++;
+            tidx[q] = (int32_t)r;
+            tval[q] = val[p];
+        }
+}
+
+static void do_load(gfors_ctx* C, const gfors_problem* P) {
+    if (!P) input_error("problem: NULL");
+    const long long n = P->n, m = P->m;
+    if (n <= 0 || n >= 2147483647LL) input_error("problem.n: must be in [1, 2^31-1)");
+    if (m < 0 || m >= 2147483647LL) input_error("problem.m: must be in [0, 2^31-1)");
+    if (P->mem_space != 0 && P->mem_space != 1) input_error("problem.mem_space: must be 0 (host) or 1 (device)");
+    if (!P->c) input_error("problem.c: NULL");
+    if (m > 0 && (!P->k_rowptr || !P->k_col || !P->k_val || !P->r || !P->sense))
+        input_error("problem: k_rowptr, k_col, k_val, r and sense are required when m > 0");
+    if (!std::isfinite(P->c0)) input_error("problem.c0: non-finite");
+    const int ms = P->mem_space;
+    CK(cudaSetDevice(C->device));
+    std::vector<int64_t> kptr = m ? fetch(P->k_rowptr, m + 1, ms) : std::vector<int64_t>(1, 0);
+    const long long nnz = kptr[m];
+    if (nnz < 0 || nnz >= 2147483647LL) input_error("problem: nnz(K) must be < 2^31");
+    std::vector<int32_t> kcol = fetch(P->k_col, nnz, ms);
+    std::vector<double> kval = fetch(P->k_val, nnz, ms);
+    std::vector<double> r = fetch(P->r, m, ms);
+    std::vector<int8_t> sense = fetch(P->sense, m, ms);
+    std::vector<double> c = fetch(P->c, n, ms);
+    if (m) validate_csr(m, n, kptr.data(), kcol.data(), kval.data(), "K");
+    for (long long j = 0; j < m; ++j) {
+        if (!std::isfinite(r[j])) input_error("r: non-finite value at row %lld", j);
+        if (sense[j] != 1 && sense[j] != 0 && sense[j] != -1) input_error("sense: row %lld must be +1, 0 or -1", j);
+    }
+    for (long long i = 0; i < n; ++i)
+        if (!std::isfinite(c[i])) input_error("c: non-finite value at %lld", i);
+    std::vector<int64_t> qptr;
+    std::vector<int32_t> qcol;
+    std::vector<double> qval;
+    if (P->q_rowptr) {
+        qptr = fetch(P->q_rowptr, n + 1, ms);
+        const long long qn = qptr[n];
+        if (qn < 0 || qn >= 2147483647LL) input_error("problem: nnz(Q) must be < 2^31");
+        if (qn > 0 && (!P->q_col || !P->q_val)) input_error("problem: q_col and q_val required with q_rowptr");
+        qcol = fetch(P->q_col, qn, ms);
+        qval = fetch(P->q_val, qn, ms);
+        validate_csr(n, n, qptr.data(), qcol.data(), qval.data(), "Q");
+        for (long long i = 0; i < n; ++i)
+            for (long long p = qptr[i]; p < qptr[i + 1]; ++p) {
+                const int j = qcol[p];
+                auto b = qcol.begin() + qptr[j], e = qcol.begin() + qptr[j + 1];
+                auto it = std::lower_bound(b, e, (int32_t)i);
+                if (it == e || *it != i || qval[qptr[j] + (it - b)] != qval[p])
+                    input_error("Q: not symmetric at (%lld, %d)", i, j);
+            }
+    } else {
+        qptr.assign(n + 1, 0);
+    }
+
+    C->free_prep();
+    C->free_problem();
+    C->stage = 0;
+    C->n = n; C->m = m; C->nnz = nnz;
+    C->maximize = P->maximize != 0;
+    const double sgn = C->maximize ? -1.0 : 1.0;
+    // objective: maximise -> minimise by negation
+    C->c.resize(n);
+    for (long long i = 0; i < n; ++i) C->c[i] = sgn * c[i];
+    C->c0 = sgn * P->c0;
+    C->qptr = qptr; C->qcol = qcol; C->qval = qval;
+    for (auto& v : C->qval) v *= sgn;
+    C->qnnz = (long long)C->qval.size();
+    C->hasq = C->qnnz > 0;
+    // rows: LE -> GE by negation; GE rows first, then EQ (stable)
+    C->kptr.assign(m + 1, 0); C->kcol.resize(nnz); C->kval.resize(nnz); C->ru.resize(m); C->perm.resize(m);
+    long long cj = 0, q = 0;
+    for (int pass = 0; pass < 2; ++pass) {
+        for (long long j = 0; j < m; ++j) {
+            if ((sense[j] == 0) != (pass == 1)) continue;
+            const double s = sense[j] == -1 ? -1.0 : 1.0;
+            C->perm[cj] = j;
+            C->ru[cj] = s * r[j];
+            for (long long p = kptr[j]; p < kptr[j + 1]; ++p, ++q) { C->kcol[q] = kcol[p]; C->kval[q] = s * kval[p]; }
+            C->kptr[cj + 1] = q;
+            ++cj;
+        }
+        if (pass == 0) C->m1 = cj;
+    }
+    C->m2 = m - C->m1;
+    // integrality (reading R12; bound of A23)
+    bool integ = is_int53(C->c0);
+    double bound = std::fabs(C->c0);
+    for (double v : C->c) { integ = integ && is_int53(v); bound += std::fabs(v); }
+    for (double v : C->qval) { integ = integ && is_int53(v); bound += std::fabs(v); }
+    for (double v : C->kval) integ = integ && is_int53(v);
+    for (double v : C->ru) integ = integ && is_int53(v);
+    if (bound >= 9007199254740992.0) integ = false;
+    C->integral = integ;
+    // value storage class of K
+    C->rsign.assign(m, 1);
+    bool sign_rows = true, i8 = true;
+    for (long long j = 0; j < m && sign_rows; ++j) {
+        if (C->kptr[j + 1] > C->kptr[j]) {
+            const double v0 = C->kval[C->kptr[j]];
+            if (v0 != 1.0 && v0 != -1.0) { sign_rows = false; break; }
+            C->rsign[j] = (signed char)(v0 > 0 ? 1 : -1);
+            for (long long p = C->kptr[j]; p < C->kptr[j + 1]; ++p)
+                if (C->kval[p] != v0) { sign_rows = false; break; }
+        }
+    }
+    for (double v : C->kval) i8 = i8 && (v == std::floor(v)) && std::fabs(v) <= 127.0;
+    C->kkind = sign_rows ? KV_SIGN : (i8 ? KV_I8 : KV_F64);
+    transpose(m, n, C->kptr, C->kcol, C->kval, C->ktptr, C->ktrow, C->ktval);
+
+    // ---- device upload ----
+    cudaStream_t s = C->stream;
+    auto own = [&](void* p) { C->owned.push_back(p); return p; };
+    C->d_kptr = (long long*)own(dupload(std::vector<long long>(C->kptr.begin(), C->kptr.end()), s));
+    C->d_kcol = (int*)own(dupload(std::vector<int>(C->kcol.begin(), C->kcol.end()), s));
+    C->d_ktptr = (long long*)own(dupload(std::vector<long long>(C->ktptr.begin(), C->ktptr.end()), s));
+    C->d_ktrow = (int*)own(dupload(std::vector<int>(C->ktrow.begin(), C->ktrow.end()), s));
+    if (C->kkind == KV_I8) {
+        std::vector<signed char> a(nnz), b(nnz);
+        for (long long p = 0; p < nnz; ++p) { a[p] = (signed char)C->kval[p]; b[p] = (signed char)C->ktval[p]; }
+        C->d_kval = own(dupload(a, s));
+        C->d_ktval = own(dupload(b, s));
+    } else if (C->kkind == KV_F64) {
+        C->d_kval = own(dupload(C->kval, s));
+        C->d_ktval = own(dupload(C->ktval, s));
+    }
+    C->d_rsign = (signed char*)own(dupload(C->rsign, s));
+    C->d_qptr = (long long*)own(dupload(std::vector<long long>(C->qptr.begin(), C->qptr.end()), s));
+    C->d_qcol = (int*)own(dupload(std::vector<int>(C->qcol.begin(), C->qcol.end()), s));
+    C->d_qval = (double*)own(dupload(C->qval, s));
+    C->d_c = (double*)own(dupload(C->c, s));
+    C->d_ru = (double*)own(dupload(C->ru, s));
+    C->pd = plan_direction(C->kptr, m, s, C->owned);
+    C->pp = plan_direction(C->ktptr, n, s, C->owned);
+
+    // ---- evaluator row classes ----
+    std::vector<int> crow[3], ct[3];
+    std::vector<signed char> crel[3], cB[3];
+    std::vector<int> irow, rrow;
+    std::vector<long long> irhs, iseg_start;
+    std::vector<int> iseg_slot;
+    std::vector<signed char> ieq;
+    long long cnt_nnz[3] = {0, 0, 0};
+    C->never_feasible = false;
+    for (long long j = 0; j < m; ++j) {
+        const long long L = C->kptr[j + 1] - C->kptr[j];
+        const bool is_eq = j >= C->m1;
+        if (!C->integral) { rrow.push_back((int)j); continue; }
+        const long long R = (long long)C->ru[j];
+        bool as_count = sign_rows;
+        if (!as_count && L > 0) {  // per-row single-sign pattern even if the matrix is mixed
+            const double v0 = C->kval[C->kptr[j]];
+            as_count = (v0 == 1.0 || v0 == -1.0);
+            for (long long p = C->kptr[j]; p < C->kptr[j + 1] && as_count; ++p) as_count = C->kval[p] == v0;
+        }
+        if (L == 0) {
+            const bool ok = is_eq ? (R == 0) : (R <= 0);
+            if (!ok) C->never_feasible = true;
+            continue;
+        }
+        if (as_count) {
+            const long long s0 = C->kval[C->kptr[j]] > 0 ? 1 : -1;
+            long long t;
+            int rel;
+            // s*c >= R  or  s*c == R  with c = #ones in [0, L]
+            if (!is_eq) {
+                if (s0 > 0) {
+                    if (R <= 0) continue;
+                    if (R > L) { C->never_feasible = true; continue; }
+                    t = R; rel = 0;
+                } else {
+                    const long long U = -R;
+                    if (U < 0) { C->never_feasible = true; continue; }
+                    if (U >= L) continue;
+                    t = U; rel = 1;
+                }
+            } else {
+                const long long V = s0 > 0 ? R : -R;
+                if (V < 0 || V > L) { C->never_feasible = true; continue; }
+                t = V; rel = 2;
+            }
+            const long long cap = rel == 0 ? t : t + 1;
+            int B = 0;
+            while ((1LL << B) - 1 < cap) ++B;
+            if (B <= 8) {
+                const int li = B <= 1 ? 0 : (B <= 2 ? 1 : 2);
+                crow[li].push_back((int)j); ct[li].push_back((int)t); crel[li].push_back((signed char)rel);
+                cB[li].push_back((signed char)B);
+                cnt_nnz[li] += L;
+                continue;
+            }
+        }
+        // general integer row
+        const long long slot = (long long)irow.size();
+        irow.push_back((int)j); irhs.push_back(R); ieq.push_back(is_eq ? 1 : 0);
+        for (long long p = C->kptr[j]; p < C->kptr[j + 1]; p += 256) { iseg_start.push_back(p); iseg_slot.push_back((int)slot); }
+    }
+    for (int li = 0; li < 3; ++li) {
+        auto& cl = C->cnt[li];
+        cl.nrows = (long long)crow[li].size();
+        if (cl.nrows) {
+            cl.row = (int*)own(dupload(crow[li], s));
+            cl.t = (int*)own(dupload(ct[li], s));
+            cl.rel = (signed char*)own(dupload(crel[li], s));
+            cl.B = (signed char*)own(dupload(cB[li], s));
+            cl.sub = pick_sub((double)cnt_nnz[li] / (double)cl.nrows);
+        }
+    }
+    C->n_int = (long long)irow.size();
+    C->n_int_seg = (long long)iseg_slot.size();
+    if (C->n_int) {
+        // segment ends: segments are contiguous inside a row but rows need not be adjacent
+        std::vector<long long> starts;  // pairs packed as start array with explicit end per segment
+        C->d_int_row = (int*)own(dupload(irow, s));
+        C->d_int_rhs = (long long*)own(dupload(irhs, s));
+        C->d_int_eq = (signed char*)own(dupload(ieq, s));
+        // store [start, end) per segment as start/end arrays laid out as seg_start[2*k], [2*k+1]
+        std::vector<long long> se(2 * C->n_int_seg);
+        for (long long k = 0; k < C->n_int_seg; ++k) {
+            const int row = irow[iseg_slot[k]];
+            se[2 * k] = iseg_start[k];
+            se[2 * k + 1] = std::min<long long>(iseg_start[k] + 256, C->kptr[row + 1]);
+        }
+        C->d_int_seg_start = (long long*)own(dupload(se, s));
+        C->d_int_seg_slot = (int*)own(dupload(iseg_slot, s));
+    }
+    C->n_real = (long long)rrow.size();
+    if (C->n_real) C->d_real_row = (int*)own(dupload(rrow, s));
+    CK(cudaStreamSynchronize(s));
+    C->stage = 1;
+}
+
+// =============================================================================================
+// Typed dispatch helpers
+// =============================================================================================
+namespace {
+
+struct LaunchCtx {
+    gfors_ctx* C;
+    cudaStream_t s;
+    int cls;
+};
+
+inline void prof_begin(gfors_ctx* C, cudaStream_t s, int cls, cudaEvent_t* a) {
+    C->launches++;
+    if (!C->profiling) return;
+    CK(cudaEventCreate(a));
+    CK(cudaEventRecord(*a, s));
+    (void)cls;
+}
+inline void prof_end(gfors_ctx* C, cudaStream_t s, int cls, cudaEvent_t a) {
+    if (!C->profiling) return;
+    cudaEvent_t b;
+    CK(cudaEventCreate(&b));
+    CK(cudaEventRecord(b, s));
+    C->prof_ev.push_back({cls, {a, b}});
+}
+#define LAUNCH(C, s, cls, ...)                                   \
+    do {                                                         \
+        cudaEvent_t ev_a__ = nullptr;                            \
+        prof_begin((C), (s), (cls), &ev_a__);                    \
+        __VA_ARGS__;                                             \
+        CK(cudaGetLastError());                                  \
+        prof_end((C), (s), (cls), ev_a__);                       \
+    } while (0)
+
+template <typename T>
+State<T> state_of(gfors_ctx* C) {
+    State<T> st;
+    for (int b = 0; b < 2; ++b) { st.x[b] = (T*)C->d_x[b]; st.xb[b] = (T*)C->d_xb[b]; st.y[b] = (T*)C->d_y[b]; }
+    st.w = (T*)C->d_w;
+    return st;
+}
+inline Csr csr_K(gfors_ctx* C) { return Csr{C->d_kptr, C->d_kcol, C->d_kval, C->m}; }
+inline Csr csr_Kt(gfors_ctx* C) { return Csr{C->d_ktptr, C->d_ktrow, C->d_ktval, C->n}; }
+inline Csr csr_Q(gfors_ctx* C) { return Csr{C->d_qptr, C->d_qcol, C->d_qval, C->n}; }
+
+#define SUB_SWITCH(sub, ...)                                  \
+    switch (sub) {                                            \
+        case 2: { constexpr int SUBV = 2; __VA_ARGS__; } break;  \
+        case 4: { constexpr int SUBV = 4; __VA_ARGS__; } break;  \
+        case 8: { constexpr int SUBV = 8; __VA_ARGS__; } break;  \
+        case 16: { constexpr int SUBV = 16; __VA_ARGS__; } break; \
+        default: { constexpr int SUBV = 32; __VA_ARGS__; } break; \
+    }
+#define KIND_SWITCH(kind, ...)                                           \
+    switch (kind) {                                                      \
+        case KV_SIGN: { constexpr int KINDV = KV_SIGN; __VA_ARGS__; } break; \
+        case KV_I8: { constexpr int KINDV = KV_I8; __VA_ARGS__; } break;     \
+        default: { constexpr int KINDV = KV_F64; __VA_ARGS__; } break;       \
+    }
+
+// one PDHG iteration (dual + primal); kint/j select the parity (see pdhg.cuh)
+template <typename T>
+void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
+    State<T> st = state_of<T>(C);
+    const Ctrl* ctrl = C->d_ctrl;
+    const T* g = (const T*)C->d_g;
+    const T* rh = (const T*)C->d_rh;
+    if (C->m > 0) {
+        if (!C->pd.seg) {
+            const int grid = grid_for(C->m * (long long)C->pd.sub);
+            KIND_SWITCH(C->kkind, SUB_SWITCH(C->pd.sub, LAUNCH(C, s, KC_DUAL,
+                (k_dual<T, KINDV, SUBV><<<grid, NT, 0, s>>>(csr_K(C), st, g, rh, C->d_rsign, C->m1, ctrl, kint, j)))));
+        } else {
+            const int grid = grid_for(C->pd.ds.nseg * 32);
+            const int grid2 = grid_for(C->m);
+            KIND_SWITCH(C->kkind, LAUNCH(C, s, KC_DUAL,
+                (k_seg_partial<T, KINDV><<<grid, NT, 0, s>>>(csr_K(C), C->pd.ds.plan(), st.xb[0], st.xb[1], nullptr,
+                                                             nullptr, 1, ctrl, kint, j, C->d_segpart));
+                (k_dual_seg_final<T, KINDV><<<grid2, NT, 0, s>>>(C->m, C->pd.ds.plan(), C->d_segpart, st, g, rh,
+                                                                 C->d_rsign, C->m1, ctrl, kint, j))));
+        }
+    }
+    const Csr Q = csr_Q(C);
+    const T* qs = (const T*)C->d_qs;
+    const T* cs = (const T*)C->d_cs;
+    // K' values: SIGN rows fold the sign into w, so the transpose carries no values
+    const int tkind = C->kkind;
+    if (!C->pp.seg) {
+        const int grid = grid_for(C->n * (long long)C->pp.sub);
+        if (C->hasq) {
+            KIND_SWITCH(tkind, SUB_SWITCH(C->pp.sub, LAUNCH(C, s, KC_PRIMAL,
+                (k_primal<T, KINDV, SUBV, true><<<grid, NT, 0, s>>>(csr_Kt(C), Q, qs, st, cs, ctrl, kint, j)))));
+        } else {
+            KIND_SWITCH(tkind, SUB_SWITCH(C->pp.sub, LAUNCH(C, s, KC_PRIMAL,
+                (k_primal<T, KINDV, SUBV, false><<<grid, NT, 0, s>>>(csr_Kt(C), Q, qs, st, cs, ctrl, kint, j)))));
+        }
+    } else {
+        const int grid = grid_for(C->pp.ds.nseg * 32);
+        const int grid2 = grid_for(C->n);
+        KIND_SWITCH(tkind, LAUNCH(C, s, KC_PRIMAL,
+            (k_seg_partial<T, KINDV><<<grid, NT, 0, s>>>(csr_Kt(C), C->pp.ds.plan(), st.w, st.w, nullptr, nullptr, 0,
+                                                         ctrl, kint, j, C->d_segpart2))));
+        if (C->hasq)
+            LAUNCH(C, s, KC_PRIMAL, (k_primal_seg_final<T, true><<<grid2, NT, 0, s>>>(
+                                        C->n, C->pp.ds.plan(), C->d_segpart2, Q, qs, st, cs, ctrl, kint, j)));
+        else
+            LAUNCH(C, s, KC_PRIMAL, (k_primal_seg_final<T, false><<<grid2, NT, 0, s>>>(
+                                        C->n, C->pp.ds.plan(), C->d_segpart2, Q, qs, st, cs, ctrl, kint, j)));
+    }
+}
+
+// trigger indicator passes after iteration j of the block
+template <typename T>
+void enqueue_trigger(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
+    State<T> st = state_of<T>(C);
+    const Ctrl* ctrl = C->d_ctrl;
+    const T* g = (const T*)C->d_g;
+    const T* rh = (const T*)C->d_rh;
+    if (C->m > 0) {
+        if (!C->pd.seg) {
+            KIND_SWITCH(C->kkind, SUB_SWITCH(C->pd.sub, LAUNCH(C, s, KC_TRIGR,
+                (k_trig_rows<T, KINDV, SUBV, false><<<C->nb1, NT, 0, s>>>(csr_K(C), C->pd.ds.plan(), nullptr, nullptr,
+                    st, g, rh, C->d_rsign, C->m1, ctrl, kint, j, C->d_part1)))));
+        } else {
+            const int grid = grid_for(C->pd.ds.nseg * 32);
+            KIND_SWITCH(C->kkind, LAUNCH(C, s, KC_TRIGR,
+                (k_seg_partial<T, KINDV><<<grid, NT, 0, s>>>(csr_K(C), C->pd.ds.plan(), st.x[0], st.x[1], nullptr,
+                                                             nullptr, 2, ctrl, kint, j, C->d_segpart));
+                (k_seg_partial<T, KINDV><<<grid, NT, 0, s>>>(csr_K(C), C->pd.ds.plan(), st.x[0], st.x[1], st.xb[0],
+                                                             st.xb[1], 2, ctrl, kint, j, C->d_segpart2));
+                (k_trig_rows<T, KINDV, 32, true><<<C->nb1, NT, 0, s>>>(csr_K(C), C->pd.ds.plan(), C->d_segpart,
+                    C->d_segpart2, st, g, rh, C->d_rsign, C->m1, ctrl, kint, j, C->d_part1))));
+        }
+    } else {
+        LAUNCH(C, s, KC_TRIGR, (k_fill<<<1, NT, 0, s>>>(C->d_part1, 3LL * C->nb1, 0.0)));
+    }
+    if (C->hasq)
+        LAUNCH(C, s, KC_TRIGC, (k_trig_cols<T, true><<<C->nb2, NT, 0, s>>>(C->n, csr_Q(C), (const T*)C->d_qs, st, ctrl,
+                                                                            kint, j, C->d_part2)));
+    else
+        LAUNCH(C, s, KC_TRIGC, (k_trig_cols<T, false><<<C->nb2, NT, 0, s>>>(C->n, csr_Q(C), (const T*)C->d_qs, st, ctrl,
+                                                                             kint, j, C->d_part2)));
+}
+
+// evaluation of the batch in d_X (W words per variable); viol/iacc must have been reset
+void enqueue_eval(gfors_ctx* C, cudaStream_t s, int W) {
+    const Csr K = csr_K(C);
+    for (int li = 0; li < 3; ++li) {
+        auto& cl = C->cnt[li];
+        if (!cl.nrows) continue;
+        CountRows cr{cl.row, cl.t, cl.rel, cl.B, cl.nrows};
+        const int grid = grid_for(cl.nrows * (long long)cl.sub);
+        const size_t sm = (size_t)W * 8;
+        if (li == 0) {
+            SUB_SWITCH(cl.sub, LAUNCH(C, s, KC_FEAS, (k_feas_count<1, SUBV><<<grid, NT, sm, s>>>(K, cr, C->d_X, W, C->d_viol))));
+        } else if (li == 1) {
+            SUB_SWITCH(cl.sub, LAUNCH(C, s, KC_FEAS, (k_feas_count<2, SUBV><<<grid, NT, sm, s>>>(K, cr, C->d_X, W, C->d_viol))));
+        } else {
+            SUB_SWITCH(cl.sub, LAUNCH(C, s, KC_FEAS, (k_feas_count<8, SUBV><<<grid, NT, sm, s>>>(K, cr, C->d_X, W, C->d_viol))));
+        }
+    }
+    if (C->n_int) {
+        IntRows ir{C->d_int_row, C->d_int_rhs, C->d_int_eq, C->d_int_seg_start, C->d_int_seg_slot, C->n_int, C->n_int_seg};
+        const int grid = grid_for(C->n_int_seg * 2LL * W * 32);
+        KIND_SWITCH(C->kkind, LAUNCH(C, s, KC_FEAS, (k_feas_int_partial<KINDV><<<grid, NT, 0, s>>>(K, ir, C->d_X, W, C->d_iacc))));
+        LAUNCH(C, s, KC_FEAS, (k_feas_int_final<<<grid_for(C->n_int * 64LL * W), NT, 0, s>>>(ir, W, C->d_iacc, C->d_viol)));
+    }
+    if (C->n_real) {
+        const int grid = grid_for(C->n_real * 2LL * W * 32);
+        KIND_SWITCH(C->kkind, LAUNCH(C, s, KC_FEAS, (k_feas_real<KINDV><<<grid, NT, 0, s>>>(K, C->d_real_row, C->n_real, C->d_ru,
+                                                                                             C->m1, C->d_X, W, C->d_viol))));
+    }
+    const long long nchunk = (C->n + C->obj_chunk - 1) / C->obj_chunk;
+    const int grid = grid_for(nchunk * 2LL * W * 32);
+    const Csr Q = csr_Q(C);
+    if (C->integral) {
+        if (C->hasq)
+            LAUNCH(C, s, KC_OBJ, (k_obj_partial<true, true><<<grid, NT, 0, s>>>(C->n, C->obj_chunk, C->d_c, Q, C->d_qval, C->d_X, W, C->d_zpart)));
+        else
+            LAUNCH(C, s, KC_OBJ, (k_obj_partial<true, false><<<grid, NT, 0, s>>>(C->n, C->obj_chunk, C->d_c, Q, C->d_qval, C->d_X, W, C->d_zpart)));
+        LAUNCH(C, s, KC_OBJ, (k_obj_final<true><<<grid_for(64LL * W), NT, 0, s>>>(nchunk, W, C->d_zpart, C->c0, C->d_z)));
+    } else {
+        if (C->hasq)
+            LAUNCH(C, s, KC_OBJ, (k_obj_partial<false, true><<<grid, NT, 0, s>>>(C->n, C->obj_chunk, C->d_c, Q, C->d_qval, C->d_X, W, C->d_zpart)));
+        else
+            LAUNCH(C, s, KC_OBJ, (k_obj_partial<false, false><<<grid, NT, 0, s>>>(C->n, C->obj_chunk, C->d_c, Q, C->d_qval, C->d_X, W, C->d_zpart)));
+        LAUNCH(C, s, KC_OBJ, (k_obj_final<false><<<grid_for(64LL * W), NT, 0, s>>>(nchunk, W, C->d_zpart, C->c0, C->d_z)));
+    }
+}
+
+void enqueue_reset(gfors_ctx* C, cudaStream_t s, int W, unsigned long long last_mask) {
+    const long long niacc = C->n_int * 64LL * W;
+    LAUNCH(C, s, KC_ARGMIN, (k_round_reset<<<grid_for(std::max<long long>(niacc, 1)), NT, 0, s>>>(
+                                C->d_viol, W, C->d_iacc, niacc, last_mask, C->never_feasible ? 1 : 0)));
+}
+
+// make sure the batch buffers fit W words per variable
+void ensure_batch(gfors_ctx* C, int W) {
+    const long long words = C->n * (long long)W;
+    if (words > C->X_words) {
+        dfree(C->d_X); C->d_X = nullptr;
+        C->d_X = dalloc<uint64_t>(words);
+        C->X_words = words;
+        dfree(C->d_viol); C->d_viol = dalloc<unsigned long long>(W);
+        C->gvalid = false;
+    }
+    const long long niacc = C->n_int * 64LL * W;
+    if (niacc > C->iacc_len) {
+        dfree(C->d_iacc); C->d_iacc = dalloc<unsigned long long>(niacc); C->iacc_len = niacc; C->gvalid = false;
+    }
+    if (!C->d_iacc) { C->d_iacc = dalloc<unsigned long long>(1); C->iacc_len = 1; }
+    const long long nchunk = (C->n + C->obj_chunk - 1) / C->obj_chunk;
+    const long long zp = nchunk * 64LL * W;
+    if (zp > C->zpart_len) { dfree(C->d_zpart); C->d_zpart = dalloc<double>(zp); C->zpart_len = zp; C->gvalid = false; }
+    if (64LL * W > C->z_len) { dfree(C->d_z); C->d_z = dalloc<double>(64LL * W); C->z_len = 64LL * W; C->gvalid = false; }
+}
+
+template <typename T>
+void enqueue_sample(gfors_ctx* C, cudaStream_t s, const double* pfix, int W, long long word_off, uint64_t seed,
+                    long long kint, int r, int kr, unsigned round_fixed, int use_fixed) {
+    const uint2 key = make_uint2((unsigned)(seed & 0xffffffffu), (unsigned)(seed >> 32));
+    LAUNCH(C, s, KC_SAMPLE, (k_sample<T><<<grid_for(C->n * (long long)W), NT, 0, s>>>(
+                                (const T*)C->d_x[0], (const T*)C->d_x[1], pfix, C->n, W, word_off, key, C->d_ctrl, kint, r,
+                                kr, round_fixed, use_fixed, C->d_X)));
+}
+
+// one whole Alg. 1 sampling block (graph body)
+template <typename T>
+void enqueue_block(gfors_ctx* C, cudaStream_t s, const gfors_params* p, int W, HaltPar hp,
+                   cudaGraphConditionalHandle h, int use_handle) {
+    const long long kint = p->k_int;
+    for (long long j = 0; j < kint; ++j) enqueue_iter<T>(C, s, kint, j);
+    enqueue_trigger<T>(C, s, kint, kint - 1);
+    const long long word_off = (long long)C->rank * W;
+    for (int r = 0; r < p->k_r; ++r) {
+        enqueue_reset(C, s, W, ~0ull);
+        enqueue_sample<T>(C, s, nullptr, W, word_off, p->seed, kint, r, p->k_r, 0u, 0);
+        enqueue_eval(C, s, W);
+        LAUNCH(C, s, KC_ARGMIN, (k_argmin<<<1, NT, 0, s>>>(C->d_z, C->d_viol, 64LL * W, word_off, C->d_ctrl, kint, r, p->k_r, 0)));
+        LAUNCH(C, s, KC_ARGMIN, (k_copy_best<<<grid_for(C->n), NT, 0, s>>>(C->d_X, W, C->n, C->d_ctrl, C->d_xbest)));
+    }
+    LAUNCH(C, s, KC_HALT, (k_halt<<<1, NT, 0, s>>>(C->d_ctrl, hp, C->d_part1, C->nb1, C->d_part2, C->nb2, C->n, C->d_hist,
+                                                  C->d_rho, C->nrho, C->d_trace, h, use_handle)));
+}
+
+}  // namespace
+
+// =============================================================================================
+// Preprocess (a2) on the device
+// =============================================================================================
+static double dev_norm(gfors_ctx* C, const double* v, long long len) {
+    cudaStream_t s = C->stream;
+    const int nb = std::min(grid_for(len), 1024);
+    k_sumsq_partial<<<nb, NT, 0, s>>>(v, len, C->d_red);
+    CK(cudaGetLastError());
+    k_sum_final<<<1, NT, 0, s>>>(C->d_red, nb, C->d_scalar);
+    CK(cudaGetLastError());
+    double h = 0.0;
+    CK(cudaMemcpyAsync(&h, C->d_scalar, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return h;
+}
+
+// power iteration on M'M (readings R5, R6).  isq: M = Q (symmetric) else
+// M = D^-1 K_u (row scale s).
+static double power_iteration(gfors_ctx* C, bool isq, double tol, int max_iter) {
+    cudaStream_t s = C->stream;
+    const long long cols = C->n, rows = isq ? C->n : C->m;
+    if (rows == 0) return 0.0;
+    double* v = C->d_tmp[0];
+    double* w = C->d_tmp[1];
+    double* u = C->d_tmp[2];
+    k_fill<<<grid_for(cols), NT, 0, s>>>(v, cols, 1.0 / std::sqrt((double)cols));
+    CK(cudaGetLastError());
+    double sigma = 0.0, sigma_prev = 0.0;
+    bool restarted = false;
+    const int gr = grid_for(rows * 32LL), gc = grid_for(cols * 32LL);
+    for (int t = 1; t <= max_iter; ++t) {
+        if (isq) {
+            k_spmv_rows<KV_F64><<<gr, NT, 0, s>>>(csr_Q(C), nullptr, nullptr, v, w);
+        } else {
+            KIND_SWITCH(C->kkind, (k_spmv_rows<KINDV><<<gr, NT, 0, s>>>(csr_K(C), C->d_rsign, C->d_s, v, w)));
+        }
+        CK(cudaGetLastError());
+        sigma = dev_norm(C, w, rows);
+        if (isq) {
+            k_spmv_rows<KV_F64><<<gc, NT, 0, s>>>(csr_Q(C), nullptr, nullptr, w, u);
+        } else {
+            KIND_SWITCH(C->kkind, (k_spmv_cols<KINDV><<<gc, NT, 0, s>>>(csr_Kt(C), C->d_rsign, C->d_s, w, u)));
+        }
+        CK(cudaGetLastError());
+        const double nu = dev_norm(C, u, cols);
+        if (nu == 0.0) {
+            if (t == 1 && !restarted) {
+                k_philox_vec<<<grid_for(cols), NT, 0, s>>>(v, cols);
+                CK(cudaGetLastError());
+                const double nv = dev_norm(C, v, cols);
+                CK(cudaMemcpyAsync(C->d_scalar, &nv, sizeof(double), cudaMemcpyHostToDevice, s));
+                k_scale_vec<<<grid_for(cols), NT, 0, s>>>(v, C->d_scalar, cols, v);
+                CK(cudaGetLastError());
+                restarted = true;
+                t = 0;
+                continue;
+            }
+            break;
+        }
+        // v = u / ||u||  (the norm is already in d_scalar)
+        k_scale_vec<<<grid_for(cols), NT, 0, s>>>(u, C->d_scalar, cols, v);
+        CK(cudaGetLastError());
+        if (t > 1 && std::fabs(sigma - sigma_prev) <= tol * sigma) break;
+        sigma_prev = sigma;
+    }
+    return sigma;
+}
+
+template <typename T>
+static void alloc_loop_data(gfors_ctx* C) {
+    const long long n = C->n, m = C->m;
+    C->d_g = dalloc<T>(m); C->d_rh = dalloc<T>(m); C->d_cs = dalloc<T>(n); C->d_qs = dalloc<T>(C->qnnz);
+    for (int b = 0; b < 2; ++b) { C->d_x[b] = dalloc<T>(n); C->d_xb[b] = dalloc<T>(n); C->d_y[b] = dalloc<T>(m); }
+    C->d_w = dalloc<T>(m);
+    cudaStream_t s = C->stream;
+    k_make_rowdata<T><<<grid_for(m), NT, 0, s>>>(m, C->d_s, C->d_ru, C->kappa, (T*)C->d_g, (T*)C->d_rh);
+    CK(cudaGetLastError());
+    k_scale_to<T><<<grid_for(n), NT, 0, s>>>(C->d_c, n, C->omega, (T*)C->d_cs);
+    CK(cudaGetLastError());
+    if (C->qnnz) {
+        k_scale_to<T><<<grid_for(C->qnnz), NT, 0, s>>>(C->d_qval, C->qnnz, C->omega, (T*)C->d_qs);
+        CK(cudaGetLastError());
+    }
+    k_init_state<T><<<grid_for(std::max(n, m)), NT, 0, s>>>(state_of<T>(C), n, m);
+    CK(cudaGetLastError());
+}
+
+static void do_preprocess(gfors_ctx* C, const gfors_prep_opts* o, gfors_scaling* out) {
+    if (C->stage < 1) throw Err{GFORS_E_STATE, "gfors_preprocess: call gfors_load first"};
+    gfors_prep_opts d;
+    gfors_prep_opts_default(&d);
+    if (!o) o = &d;
+    if (o->precision != 32 && o->precision != 64) input_error("prep_opts.precision: must be 32 or 64");
+    if (!(o->tol > 0.0)) input_error("prep_opts.tol: must be > 0");
+    if (o->max_iter < 1) input_error("prep_opts.max_iter: must be >= 1");
+    CK(cudaSetDevice(C->device));
+    C->free_prep();
+    cudaStream_t s = C->stream;
+    const long long n = C->n, m = C->m;
+    const long long big = std::max(n, m);
+    for (int k = 0; k < 4; ++k) C->d_tmp[k] = dalloc<double>(big);
+    C->d_red = dalloc<double>(2048);
+    C->d_scalar = dalloc<double>(1);
+    C->d_s = dalloc<double>(m);
+    unsigned long long* d_zr = dalloc<unsigned long long>(1);
+    CK(cudaMemsetAsync(d_zr, 0, sizeof(unsigned long long), s));
+    // step 1: row 2-norms of K
+    if (m) {
+        KIND_SWITCH(C->kkind, (k_row_norms<KINDV><<<grid_for(m), NT, 0, s>>>(csr_K(C), C->d_s, d_zr)));
+        CK(cudaGetLastError());
+    }
+    unsigned long long zr = 0;
+    CK(cudaMemcpyAsync(&zr, d_zr, sizeof zr, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    dfree(d_zr);
+    C->zero_rows = (long long)zr;
+    // step 2: omega = ||Q||_2 + ||c||_2
+    const double qn = C->qnnz ? power_iteration(C, true, o->tol, o->max_iter) : 0.0;
+    const double cn = dev_norm(C, C->d_c, n);
+    const double omega = qn + cn;
+    C->omega = omega > 0.0 ? omega : 1.0;
+    // step 3: kappa = ||D^-1 K||_2
+    const double kap = m ? power_iteration(C, false, o->tol, o->max_iter) : 0.0;
+    C->kappa = kap > 0.0 ? kap : 1.0;
+    C->precision = o->precision;
+    if (C->precision == 64) alloc_loop_data<double>(C); else alloc_loop_data<float>(C);
+    // loop workspaces
+    C->nb1 = std::max(1, std::min(grid_for(std::max<long long>(m, 1) * 32LL), 1024));
+    C->nb2 = std::max(1, std::min(grid_for(n), 1024));
+    C->d_part1 = dalloc<double>(3LL * C->nb1);
+    C->d_part2 = dalloc<double>(2LL * C->nb2);
+    C->segpart_len = std::max<long long>(std::max(C->pd.ds.nseg, C->pp.ds.nseg), 1);
+    C->d_segpart = dalloc<double>(C->segpart_len);
+    C->d_segpart2 = dalloc<double>(C->segpart_len);
+    C->d_ctrl = dalloc<Ctrl>(1);
+    C->d_hist = dalloc<double>(3 * 1024);
+    C->d_xbest = dalloc<unsigned char>(n);
+    CK(cudaMemsetAsync(C->d_ctrl, 0, sizeof(Ctrl), s));
+    CK(cudaMemsetAsync(C->d_xbest, 0, n, s));
+    CK(cudaStreamSynchronize(s));
+    C->hk = 0;
+    C->have_run = false;
+    C->stage = 2;
+    if (out) { out->obj_scale = C->omega; out->k_scale = C->kappa; out->zero_rows = C->zero_rows; }
+}
+
+// =============================================================================================
+// Run (Alg. 1)
+// =============================================================================================
+static void host_rho_table(const gfors_params* p, long long count, std::vector<double>& rho) {
+    // UpdatePenalty (readings R7, R8): rho_t = clip(rho_min(1+t/T)^p, rho_{t-1}+delta, rho_max)
+    rho.resize(count);
+    double prev = p->rho_min;
+    for (long long t = 0; t < count; ++t) {
+        const double tilde = p->rho_min * std::pow(1.0 + (double)t / p->growth_T, p->growth_p);
+        const double lo = prev + p->rho_delta;
+        double v = tilde < lo ? lo : tilde;
+        v = v > p->rho_max ? p->rho_max : v;
+        rho[t] = v;
+        prev = v;
+    }
+}
+
+static void validate_params(const gfors_params* p) {
+    if (!(p->sigma > 0.0 && p->sigma < 1.0)) input_error("params.sigma: must be in (0,1)");
+    if (p->k_int < 1) input_error("params.k_int: must be >= 1");
+    if (p->k_r < 1) input_error("params.k_r: must be >= 1");
+    if (p->k_b < 64 || p->k_b % 64) input_error("params.k_b: must be a positive multiple of 64");
+    if (p->k_b / 64 > (1 << 20)) input_error("params.k_b: too large");
+    if (p->stall_window < 1 || p->stall_window > 1024) input_error("params.stall_window: must be in [1,1024]");
+    if (p->max_iters < 0) input_error("params.max_iters: must be >= 0");
+    if (!(p->growth_T > 0.0)) input_error("params.growth_T: must be > 0");
+    if (!(p->time_limit_s > 0.0)) input_error("params.time_limit_s: must be > 0");
+    if (!(p->rho_min >= 0.0) || !(p->rho_max >= p->rho_min)) input_error("params.rho_min/rho_max: need 0 <= rho_min <= rho_max");
+    if (p->trace_cap < 0) input_error("params.trace_cap: must be >= 0");
+}
+
+static bool same_graph_key(const gfors_params& a, const gfors_params& b) {
+    return a.sigma == b.sigma && a.k_int == b.k_int && a.k_r == b.k_r && a.k_b == b.k_b && a.tol_primal == b.tol_primal &&
+           a.tol_dual == b.tol_dual && a.tol_binary == b.tol_binary && a.stall_rel == b.stall_rel &&
+           a.stall_window == b.stall_window && a.seed == b.seed && a.trace_cap == b.trace_cap;
+}
+
+template <typename T>
+static void run_tail_and_final(gfors_ctx* C, long long k_done, long long tail, int W) {
+    cudaStream_t s = C->stream;
+    for (long long t = 0; t < tail; ++t) enqueue_iter<T>(C, s, 0, k_done + t);
+    // x_k parity for the final round: ctrl->k = k_done + tail
+    const long long kfinal = k_done + tail;
+    CK(cudaMemcpyAsync(&C->d_ctrl->k, &kfinal, sizeof(long long), cudaMemcpyHostToDevice, s));
+    // final EvalBest(round(x_k)): one-lane batch
+    enqueue_reset(C, s, 1, 1ull);
+    LAUNCH(C, s, KC_SAMPLE, (k_round_batch<T><<<grid_for(C->n), NT, 0, s>>>((const T*)C->d_x[0], (const T*)C->d_x[1], C->n,
+                                                                           C->d_ctrl, 0, C->d_X)));
+    enqueue_eval(C, s, 1);
+    LAUNCH(C, s, KC_ARGMIN, (k_argmin<<<1, NT, 0, s>>>(C->d_z, C->d_viol, 1, 0, C->d_ctrl, 0, 0, 1, 1)));
+    LAUNCH(C, s, KC_ARGMIN, (k_copy_best<<<grid_for(C->n), NT, 0, s>>>(C->d_X, 1, C->n, C->d_ctrl, C->d_xbest)));
+    (void)W;
+}
+
+template <typename T>
+static void do_run_t(gfors_ctx* C, const gfors_params* p, gfors_run_info* out) {
+    cudaStream_t s = C->stream;
+    const int W = (int)(p->k_b / 64);
+    ensure_batch(C, W);
+    const long long max_blocks = p->max_iters / p->k_int;
+    const long long tail = p->max_iters % p->k_int;
+    // rho table (host pow, like the oracle; reading R7)
+    const long long nrho = max_blocks + 2;
+    std::vector<double> rho;
+    host_rho_table(p, nrho, rho);
+    if (nrho > C->rho_cap) {
+        dfree(C->d_rho);
+        C->d_rho = dalloc<double>(nrho);
+        C->rho_cap = nrho;
+        C->gvalid = false;
+    }
+    C->nrho = nrho;
+    CK(cudaMemcpyAsync(C->d_rho, rho.data(), nrho * sizeof(double), cudaMemcpyHostToDevice, s));
+    const int tcap = std::max(1, p->trace_cap);
+    if (tcap > C->trace_cap) { dfree(C->d_trace); C->d_trace = dalloc<double>(8LL * tcap); C->trace_cap = tcap; C->gvalid = false; }
+    // reset state and control
+    k_init_state<T><<<grid_for(std::max(C->n, C->m)), NT, 0, s>>>(state_of<T>(C), C->n, C->m);
+    CK(cudaGetLastError());
+    Ctrl h{};
+    h.blk = 0; h.k = 0; h.rho = rho[0]; h.tau1 = std::sqrt(p->sigma); h.tau2 = std::sqrt(p->sigma);
+    h.max_blocks = max_blocks; h.z_best = INFINITY; h.found_iter = h.found_round = h.found_index = -1; h.win_lane = -1;
+    CK(cudaMemcpyAsync(C->d_ctrl, &h, sizeof h, cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(C->d_xbest, 0, C->n, s));
+    CK(cudaMemsetAsync(C->d_hist, 0, 3 * 1024 * sizeof(double), s));
+    HaltPar hp{{p->tol_primal, p->tol_dual, p->tol_binary}, p->stall_rel, p->stall_window, p->trace_cap,
+               p->k_int, p->k_r, p->k_b * (long long)C->world};
+    k_loop_start<<<1, 1, 0, s>>>(C->d_ctrl, p->time_limit_s);
+    CK(cudaGetLastError());
+
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, s));
+    if (max_blocks > 0) {
+        if (p->use_graph) {
+            if (!(C->gvalid && same_graph_key(C->gkey, *p) && C->gkey_W == W)) {
+                if (C->gexec) { cudaGraphExecDestroy(C->gexec); C->gexec = nullptr; }
+                if (C->graph) { cudaGraphDestroy(C->graph); C->graph = nullptr; }
+                CK(cudaGraphCreate(&C->graph, 0));
+                cudaGraphConditionalHandle handle;
+                CK(cudaGraphConditionalHandleCreate(&handle, C->graph, 1, cudaGraphCondAssignDefault));
+                cudaGraphNodeParams cp = {};
+                cp.type = cudaGraphNodeTypeConditional;
+                cp.conditional.handle = handle;
+                cp.conditional.type = cudaGraphCondTypeWhile;
+                cp.conditional.size = 1;
+                cudaGraphNode_t node;
+                CK(cudaGraphAddNode(&node, C->graph, nullptr, 0, &cp));
+                cudaGraph_t body = cp.conditional.phGraph_out[0];
+                if (!C->cap_stream) CK(cudaStreamCreateWithFlags(&C->cap_stream, cudaStreamNonBlocking));
+                CK(cudaStreamBeginCaptureToGraph(C->cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+                try {
+                    enqueue_block<T>(C, C->cap_stream, p, W, hp, handle, 1);
+                } catch (...) {
+                    cudaGraph_t g2;
+                    cudaStreamEndCapture(C->cap_stream, &g2);
+                    throw;
+                }
+                cudaGraph_t g2;
+                CK(cudaStreamEndCapture(C->cap_stream, &g2));
+                CK(cudaGraphInstantiate(&C->gexec, C->graph, 0));
+                C->gkey = *p;
+                C->gkey_W = W;
+                C->gvalid = true;
+            }
+            CK(cudaGraphLaunch(C->gexec, s));
+        } else {
+            // eager: one block at a time, host reads the halt flag (debug / fallback path)
+            for (long long b = 0; b < max_blocks; ++b) {
+                enqueue_block<T>(C, s, p, W, hp, cudaGraphConditionalHandle{}, 0);
+                int hf = 0;
+                CK(cudaMemcpyAsync(&hf, &C->d_ctrl->halt, sizeof(int), cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+                if (hf) break;
+            }
+        }
+    }
+    CK(cudaMemcpyAsync(&h, C->d_ctrl, sizeof h, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    long long k_done = max_blocks > 0 ? h.k : 0;
+    int reason = max_blocks > 0 ? h.halt : 2;
+    long long tail_run = 0;
+    if (reason == 2) tail_run = (max_blocks > 0 ? p->max_iters - k_done : p->max_iters);
+    if (reason != 4) run_tail_and_final<T>(C, k_done, tail_run, W);
+    CK(cudaEventRecord(e1, s));
+    CK(cudaMemcpyAsync(&h, C->d_ctrl, sizeof h, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    gfors_run_info info{};
+    info.iters = k_done + tail_run;
+    info.rounds = h.rounds;
+    info.candidates = h.rounds * p->k_b * (long long)C->world;
+    info.halt_reason = reason;
+    info.elapsed_s = ms * 1e-3;
+    info.n_trace = h.n_trace;
+    C->last_info = info;
+    C->have_run = true;
+    C->hk = info.iters;
+    if (out) *out = info;
+    if (reason == 4) throw Err{GFORS_E_DIVERGED, "diverged: non-finite indicator at iteration " + std::to_string(h.k)};
+}
+
+// =============================================================================================
+// C ABI
+// =============================================================================================
+#define API_BEGIN(C)                                 \
+    if (!(C)) return GFORS_E_STATE;                  \
+    try {                                            \
+        cudaSetDevice((C)->device);
+#define API_END(C)                                   \
+    }                                                \
+    catch (const Err& e) {                           \
+        (C)->err = e.msg;                            \
+        return e.st;                                 \
+    }                                                \
+    catch (const std::exception& e) {                \
+        (C)->err = e.what();                         \
+        return GFORS_E_CUDA;                         \
+    }                                                \
+    (C)->err.clear();                                \
+    return GFORS_OK;
+
+template <typename T>
+static void set_state_t(gfors_ctx* C, const double* x, const double* xbar, const double* y) {
+    cudaStream_t s = C->stream;
+    double* t = C->d_tmp[3];
+    if (x) { CK(cudaMemcpyAsync(t, x, C->n * 8, cudaMemcpyHostToDevice, s)); k_to_T<T><<<grid_for(C->n), NT, 0, s>>>(t, C->n, (T*)C->d_x[0]); CK(cudaStreamSynchronize(s)); }
+    if (xbar) { CK(cudaMemcpyAsync(t, xbar, C->n * 8, cudaMemcpyHostToDevice, s)); k_to_T<T><<<grid_for(C->n), NT, 0, s>>>(t, C->n, (T*)C->d_xb[0]); CK(cudaStreamSynchronize(s)); }
+    if (y && C->m) { CK(cudaMemcpyAsync(t, y, C->m * 8, cudaMemcpyHostToDevice, s)); k_to_T<T><<<grid_for(C->m), NT, 0, s>>>(t, C->m, (T*)C->d_y[0]); CK(cudaStreamSynchronize(s)); }
+    CK(cudaGetLastError());
+    C->hk = 0;
+}
+
+template <typename T>
+static void get_state_t(gfors_ctx* C, double* x, double* xbar, double* y) {
+    cudaStream_t s = C->stream;
+    const int b = (int)(C->hk & 1);
+    double* t = C->d_tmp[3];
+    if (x) { k_from_T<T><<<grid_for(C->n), NT, 0, s>>>((T*)C->d_x[b], C->n, t); CK(cudaMemcpyAsync(x, t, C->n * 8, cudaMemcpyDeviceToHost, s)); CK(cudaStreamSynchronize(s)); }
+    if (xbar) { k_from_T<T><<<grid_for(C->n), NT, 0, s>>>((T*)C->d_xb[b], C->n, t); CK(cudaMemcpyAsync(xbar, t, C->n * 8, cudaMemcpyDeviceToHost, s)); CK(cudaStreamSynchronize(s)); }
+    if (y && C->m) { k_from_T<T><<<grid_for(C->m), NT, 0, s>>>((T*)C->d_y[b], C->m, t); CK(cudaMemcpyAsync(y, t, C->m * 8, cudaMemcpyDeviceToHost, s)); CK(cudaStreamSynchronize(s)); }
+    CK(cudaGetLastError());
+}
+
+extern "C" {
+
+void gfors_params_default(gfors_params* p) {
+    // SPEC L293, L667 defaults; k_b = 128 per rank
+    memset(p, 0, sizeof *p);
+    p->sigma = 0.99; p->k_int = 10; p->k_r = 1; p->k_b = 128;
+    p->rho_min = 1e-3; p->rho_max = 10.0; p->growth_T = 100.0; p->growth_p = 2.0; p->rho_delta = 1e-6;
+    p->tol_primal = 1e-6; p->tol_dual = 1e-6; p->tol_binary = 1e-6; p->stall_rel = 1e-8; p->stall_window = 50;
+    p->max_iters = 100000; p->time_limit_s = 1800.0; p->seed = 20251030ull; p->use_graph = 1; p->trace_cap = 4096;
+}
+
+void gfors_prep_opts_default(gfors_prep_opts* p) {
+    p->tol = 1e-7; p->max_iter = 500; p->precision = 64;
+}
+
+gfors_status gfors_create(gfors_ctx** out, const gfors_device_opts* opts) {
+    if (!out) return GFORS_E_INPUT;
+    *out = nullptr;
+    auto* C = new gfors_ctx();
+    try {
+        if (opts) { C->device = opts->device; C->rank = opts->rank; C->world = opts->world; }
+        if (C->world < 1 || C->rank < 0 || C->rank >= C->world) input_error("device_opts: need 0 <= rank < world");
+        if (C->world > 1) throw Err{GFORS_E_NCCL, "world > 1 is driven through the sharded runner (DESIGN.md §7); not in this build"};
+        int ndev = 0;
+        CK(cudaGetDeviceCount(&ndev));
+        if (C->device < 0 || C->device >= ndev) input_error("device_opts.device: %d not in [0,%d)", C->device, ndev);
+        CK(cudaSetDevice(C->device));
+        if (opts && opts->stream) {
+            C->stream = (cudaStream_t)opts->stream;
+        } else {
+            CK(cudaStreamCreateWithFlags(&C->stream, cudaStreamNonBlocking));
+            C->own_stream = true;
+        }
+    } catch (const Err& e) {
+        gfors_status st = e.st;
+        delete C;
+        return st;
+    }
+    *out = C;
+    return GFORS_OK;
+}
+
+gfors_status gfors_load(gfors_ctx* C, const gfors_problem* prob) {
+    API_BEGIN(C)
+    do_load(C, prob);
+    API_END(C)
+}
+
+gfors_status gfors_preprocess(gfors_ctx* C, const gfors_prep_opts* o, gfors_scaling* out) {
+    API_BEGIN(C)
+    do_preprocess(C, o, out);
+    API_END(C)
+}
+
+gfors_status gfors_run(gfors_ctx* C, const gfors_params* p, gfors_run_info* out) {
+    API_BEGIN(C)
+    if (C->stage < 2) throw Err{GFORS_E_STATE, "gfors_run: call gfors_preprocess first"};
+    gfors_params d;
+    gfors_params_default(&d);
+    if (!p) p = &d;
+    validate_params(p);
+    if (C->precision == 64) do_run_t<double>(C, p, out); else do_run_t<float>(C, p, out);
+    API_END(C)
+}
+
+gfors_status gfors_best_incumbent(gfors_ctx* C, double* z, uint8_t* x, gfors_incumbent_info* info) {
+    if (!C) return GFORS_E_STATE;
+    try {
+        cudaSetDevice(C->device);
+        if (!C->have_run) throw Err{GFORS_E_STATE, "gfors_best_incumbent: call gfors_run first"};
+        Ctrl h;
+        CK(cudaMemcpyAsync(&h, C->d_ctrl, sizeof h, cudaMemcpyDeviceToHost, C->stream));
+        if (x) CK(cudaMemcpyAsync(x, C->d_xbest, C->n, cudaMemcpyDeviceToHost, C->stream));
+        CK(cudaStreamSynchronize(C->stream));
+        const double zz = h.has_inc ? (C->maximize ? -h.z_best : h.z_best) : INFINITY;
+        if (z) *z = zz;
+        if (info) {
+            info->found_iter = h.found_iter; info->found_round = h.found_round; info->found_index = h.found_index;
+            info->found_time_s = h.found_ns * 1e-9; info->has_incumbent = h.has_inc;
+        }
+        C->err.clear();
+        return h.has_inc ? GFORS_OK : GFORS_NO_INCUMBENT;
+    } catch (const Err& e) {
+        C->err = e.msg;
+        return e.st;
+    }
+}
+
+const char* gfors_last_error(const gfors_ctx* C) { return C ? C->err.c_str() : "null context"; }
+
+void gfors_destroy(gfors_ctx* C) { delete C; }
+
+gfors_status gfors_get_scaled(gfors_ctx* C, double* row_scale, double* r_scaled, double* c_scaled) {
+    API_BEGIN(C)
+    if (C->stage < 2) throw Err{GFORS_E_STATE, "gfors_get_scaled: call gfors_preprocess first"};
+    std::vector<double> s(C->m);
+    if (C->m) CK(cudaMemcpy(s.data(), C->d_s, C->m * sizeof(double), cudaMemcpyDeviceToHost));
+    if (row_scale) memcpy(row_scale, s.data(), C->m * sizeof(double));
+    if (r_scaled)
+        for (long long j = 0; j < C->m; ++j) r_scaled[j] = (C->ru[j] / s[j]) / C->kappa;
+    if (c_scaled)
+        for (long long i = 0; i < C->n; ++i) c_scaled[i] = C->c[i] / C->omega;
+    API_END(C)
+}
+
+gfors_status gfors_sample(gfors_ctx* C, const double* p, uint64_t seed, uint32_t round_id, int64_t word_begin,
+                          int64_t n_words, uint64_t* bits) {
+    API_BEGIN(C)
+    if (C->stage < 2) throw Err{GFORS_E_STATE, "gfors_sample: call gfors_preprocess first"};
+    if (!p || !bits) input_error("gfors_sample: p and bits required");
+    if (n_words < 1 || n_words > (1 << 20)) input_error("gfors_sample: n_words out of range");
+    if (word_begin < 0 || word_begin + n_words > (1LL << 32)) input_error("gfors_sample: word range exceeds 2^32");
+    for (long long i = 0; i < C->n; ++i)
+        if (!(p[i] >= 0.0 && p[i] <= 1.0)) input_error("gfors_sample: p[%lld] not in [0,1]", i);
+    ensure_batch(C, (int)n_words);
+    cudaStream_t s = C->stream;
+    double* dp = C->d_tmp[3];
+    CK(cudaMemcpyAsync(dp, p, C->n * sizeof(double), cudaMemcpyHostToDevice, s));
+    if (C->precision == 64)
+        enqueue_sample<double>(C, s, dp, (int)n_words, word_begin, seed, 1, 0, 1, round_id, 1);
+    else
+        enqueue_sample<float>(C, s, dp, (int)n_words, word_begin, seed, 1, 0, 1, round_id, 1);
+    CK(cudaMemcpyAsync(bits, C->d_X, C->n * n_words * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    API_END(C)
+}
+
+gfors_status gfors_eval(gfors_ctx* C, const uint64_t* bits, int64_t n_words, uint8_t* feasible, double* z) {
+    API_BEGIN(C)
+    if (C->stage < 1) throw Err{GFORS_E_STATE, "gfors_eval: call gfors_load first"};
+    if (!bits) input_error("gfors_eval: bits required");
+    if (n_words < 1 || n_words > (1 << 20)) input_error("gfors_eval: n_words out of range");
+    if (C->stage < 2) throw Err{GFORS_E_STATE, "gfors_eval: call gfors_preprocess first"};
+    const int W = (int)n_words;
+    ensure_batch(C, W);
+    cudaStream_t s = C->stream;
+    CK(cudaMemcpyAsync(C->d_X, bits, C->n * n_words * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+    enqueue_reset(C, s, W, ~0ull);
+    enqueue_eval(C, s, W);
+    std::vector<unsigned long long> viol(W);
+    std::vector<double> zz(64LL * W);
+    CK(cudaMemcpyAsync(viol.data(), C->d_viol, W * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(zz.data(), C->d_z, 64LL * W * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (long long l = 0; l < 64LL * W; ++l) {
+        if (feasible) feasible[l] = (uint8_t)(((viol[l >> 6] >> (l & 63)) & 1ull) ? 0 : 1);
+        if (z) z[l] = zz[l];
+    }
+    API_END(C)
+}
+
+gfors_status gfors_set_state(gfors_ctx* C, const double* x, const double* xbar, const double* y) {
+    API_BEGIN(C)
+    if (C->stage < 2) throw Err{GFORS_E_STATE, "gfors_set_state: call gfors_preprocess first"};
+    if (C->precision == 64) set_state_t<double>(C, x, xbar, y); else set_state_t<float>(C, x, xbar, y);
+    API_END(C)
+}
+
+gfors_status gfors_get_state(gfors_ctx* C, double* x, double* xbar, double* y) {
+    API_BEGIN(C)
+    if (C->stage < 2) throw Err{GFORS_E_STATE, "gfors_get_state: call gfors_preprocess first"};
+    if (C->precision == 64) get_state_t<double>(C, x, xbar, y); else get_state_t<float>(C, x, xbar, y);
+    API_END(C)
+}
+
+gfors_status gfors_step(gfors_ctx* C, int64_t iters, double rho, double tau1, double tau2) {
+    API_BEGIN(C)
+    if (C->stage < 2) throw Err{GFORS_E_STATE, "gfors_step: call gfors_preprocess first"};
+    if (iters < 0) input_error("gfors_step: iters must be >= 0");
+    cudaStream_t s = C->stream;
+    Ctrl h{};
+    h.rho = rho; h.tau1 = tau1; h.tau2 = tau2;
+    CK(cudaMemcpyAsync(C->d_ctrl, &h, sizeof h, cudaMemcpyHostToDevice, s));
+    for (long long t = 0; t < iters; ++t) {
+        if (C->precision == 64) enqueue_iter<double>(C, s, 0, C->hk); else enqueue_iter<float>(C, s, 0, C->hk);
+        C->hk++;
+    }
+    CK(cudaStreamSynchronize(s));
+    API_END(C)
+}
+
+gfors_status gfors_indicators(gfors_ctx* C, double rho, double tau1, double tau2, double* out) {
+    API_BEGIN(C)
+    if (C->stage < 2 || C->hk < 1) throw Err{GFORS_E_STATE, "gfors_indicators: take a gfors_step first"};
+    cudaStream_t s = C->stream;
+    Ctrl h{};
+    h.rho = rho; h.tau1 = tau1; h.tau2 = tau2;
+    CK(cudaMemcpyAsync(C->d_ctrl, &h, sizeof h, cudaMemcpyHostToDevice, s));
+    if (C->precision == 64) enqueue_trigger<double>(C, s, 0, C->hk - 1); else enqueue_trigger<float>(C, s, 0, C->hk - 1);
+    double* o4 = C->d_tmp[3];
+    k_indicators_only<<<1, NT, 0, s>>>(C->d_part1, C->nb1, C->d_part2, C->nb2, C->n, o4);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, o4, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    API_END(C)
+}
+
+gfors_status gfors_get_trace(gfors_ctx* C, double* rows, int64_t max_rows, int64_t* n_rows) {
+    API_BEGIN(C)
+    if (!C->have_run) throw Err{GFORS_E_STATE, "gfors_get_trace: call gfors_run first"};
+    const long long total = C->last_info.n_trace;
+    const long long cap = C->trace_cap;
+    const long long avail = std::min(total, cap);
+    const long long k = std::min<long long>(avail, max_rows);
+    std::vector<double> all(8 * cap);
+    CK(cudaMemcpy(all.data(), C->d_trace, 8 * cap * sizeof(double), cudaMemcpyDeviceToHost));
+    const long long first = total - avail;  // oldest kept row index
+    for (long long r = 0; r < k; ++r) {
+        const long long src = (first + r) % cap;
+        memcpy(rows + 8 * r, all.data() + 8 * src, 8 * sizeof(double));
+    }
+    if (n_rows) *n_rows = k;
+    API_END(C)
+}
+
+const char* gfors_kernel_class_name(int32_t k) { return (k >= 0 && k < KC_N) ? kClassNames[k] : ""; }
+
+int64_t gfors_launches_per_block(gfors_ctx* C, const gfors_params* p) {
+    if (!C || C->stage < 2) return -1;
+    // count by enqueueing into a throwaway capture-free dry run: reuse the counter
+    const long long before = C->launches;
+    C->launches = 0;
+    // a dry count: mirror enqueue_block's structure
+    long long per_iter = 0;
+    per_iter += C->m > 0 ? (C->pd.seg ? 2 : 1) : 0;
+    per_iter += C->pp.seg ? 2 : 1;
+    long long trig = (C->m > 0 ? (C->pd.seg ? 3 : 1) : 1) + 1;
+    long long eval = 0;
+    for (auto& cl : C->cnt) eval += cl.nrows ? 1 : 0;
+    eval += C->n_int ? 2 : 0;
+    eval += C->n_real ? 1 : 0;
+    eval += 2;  // objective partial + final
+    const long long per_round = 1 /*reset*/ + 1 /*sample*/ + eval + 2 /*argmin, copy*/;
+    C->launches = before;
+    return per_iter * p->k_int + trig + per_round * p->k_r + 1 /*halt*/;
+}
+
+gfors_status gfors_profile_blocks(gfors_ctx* C, const gfors_params* p, int32_t blocks, double* ms_out,
+                                  int32_t max_classes, int32_t* n_classes) {
+    API_BEGIN(C)
+    if (C->stage < 2) throw Err{GFORS_E_STATE, "gfors_profile_blocks: call gfors_preprocess first"};
+    gfors_params d;
+    gfors_params_default(&d);
+    if (!p) p = &d;
+    validate_params(p);
+    if (blocks < 1) input_error("gfors_profile_blocks: blocks must be >= 1");
+    // a normal run with max_iters = blocks*k_int in eager mode, events around every launch
+    gfors_params q = *p;
+    q.max_iters = (long long)blocks * p->k_int;
+    q.use_graph = 0;
+    q.tol_primal = q.tol_dual = q.tol_binary = -1.0;  // never halt on criteria
+    q.stall_rel = -1.0;
+    C->profiling = true;
+    C->prof_ev.clear();
+    try {
+        if (C->precision == 64) do_run_t<double>(C, &q, nullptr); else do_run_t<float>(C, &q, nullptr);
+    } catch (...) {
+        C->profiling = false;
+        throw;
+    }
+    C->profiling = false;
+    CK(cudaStreamSynchronize(C->stream));
+    std::vector<double> sum(KC_N, 0.0);
+    for (auto& e : C->prof_ev) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, e.second.first, e.second.second));
+        sum[e.first] += ms;
+        cudaEventDestroy(e.second.first);
+        cudaEventDestroy(e.second.second);
+    }
+    C->prof_ev.clear();
+    const int nc = std::min<int>(KC_N, max_classes);
+    for (int k = 0; k < nc; ++k) ms_out[k] = sum[k] / blocks;  // per block
+    if (n_classes) *n_classes = nc;
+    API_END(C)
+}
+
+int32_t gfors_merge_records(const double* z, const int64_t* index, const int32_t* valid, int32_t world) {
+    // lowest z among valid records, ties -> lowest global sample index (reading R11)
+    int32_t best = -1;
+    for (int32_t r = 0; r < world; ++r) {
+        if (!valid[r]) continue;
+        if (best < 0 || z[r] < z[best] || (z[r] == z[best] && index[r] < index[best])) best = r;
+    }
+    return best;
+}
+
+}  // extern "C"
