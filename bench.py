@@ -1,0 +1,395 @@
+#!/usr/bin/env python
+"""GFORS hot-path benchmark (BASELINE.json metric) on B200.
+
+One "step" = one Alg. 1 sampling block over the whole hot path: k_int PDHG
+iterations (dual + primal kernels), the trigger indicators, k_r rounds of [Philox sampling of
+k_b candidates per rank + feasibility + objective + argmin/incumbent], CheckHalt/UpdatePenalty.
+The timed region is one gfors_run of exactly K blocks (halting disabled, fixed max_iters), i.e.
+one CUDA-graph launch whose WHILE node runs the K blocks on the device.
+
+value  = sampled candidates evaluated per second, whole job (all ranks), device time (CUDA events,
+         max over ranks).  pdhg_iters_per_s is the same clock over the replicated PDHG trajectory.
+e2e    = the same metric through the public C-ABI calls from HOST (pinned) buffers: load (H2D of the
+         instance) + preprocess + run + best_incumbent (D2H), timed end to end.
+Workload: BASELINE config 5 by default (set cover n=5e6, m=1e6, ~5e7 nonzeros), synthetic, seeded.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--precision 32|64] [--k-b 128]
+    python bench.py --impl reference ...   (the CPU oracle as the reference arm)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PDHG iters/s and sampled candidates evaluated/s; time-to-incumbent at 1/2/4/8 B200"
+UNIT = "candidates/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--precision", type=int, default=32, choices=(32, 64))
+    ap.add_argument("--k-b", type=int, default=128)
+    ap.add_argument("--k-int", type=int, default=10)
+    ap.add_argument("--impl", default="gfors", choices=("gfors", "reference"))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-blocks", type=int, default=20)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------------------------
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6650.0), "measured (MEASURED_PEAKS.json hbm_gbs)", d
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)", {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md recipe)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0])); mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def algorithmic_bytes(inst_meta, fb):
+    """Algorithmic HBM bytes per launch of the two PDHG kernels.
+    fb = bytes per iterate element.  Indices int32, pointers int64, SIGN matrices carry no values;
+    every vector is counted once (gathers assumed cache hits); g and r-hat are fp64."""
+    n, m, nnz = inst_meta["n"], inst_meta["m"], inst_meta["nnz"]
+    val = inst_meta["val_bytes"]
+    dual = nnz * (4 + val) + 8 * (m + 1) + n * fb + m * (fb + fb + fb + 8 + 8 + 1)
+    primal = nnz * (4 + val) + 8 * (n + 1) + m * fb + n * (fb + fb + fb + fb)
+    return {"pdhg_dual": dual, "pdhg_primal": primal}
+
+
+def make_instance(cfg, seed):
+    from gen import instances as G
+    return G.make_config(cfg, seed)
+
+
+def inst_meta(inst):
+    vals = inst["k_val"]
+    sign_rows = True
+    ptr = inst["k_rowptr"]
+    # +-1 single-sign rows -> SIGN storage (no value bytes)
+    if not np.all(np.abs(vals) == 1.0):
+        sign_rows = False
+    else:
+        first = np.repeat(vals[ptr[:-1]][np.diff(ptr) > 0], np.diff(ptr)[np.diff(ptr) > 0])
+        sign_rows = bool(np.all(vals == first))
+    i8 = np.all(vals == np.round(vals)) and np.all(np.abs(vals) <= 127)
+    return {"n": int(inst["n"]), "m": int(inst["m"]), "nnz": int(ptr[-1]),
+            "qnnz": int(inst["q_rowptr"][-1]) if inst.get("q_rowptr") is not None else 0,
+            "val_bytes": 0 if sign_rows else (1 if i8 else 8)}
+
+
+# ------------------------------------------------------------------------------------------------
+def oracle_block_seconds(inst, k_int, k_b, budget_s=20.0, seed=20251030):
+    """Time the CPU oracle (as it stands) on a bounded sample of the workload and compose the time of
+    one Alg. 1 block: k_int PDHG iterations + k_b sampled candidates (sampling + evaluation).
+    PDHG: whole iterations on the full instance.  Sampling: a fixed subset of variables (the per-
+    variable cost is uniform); evaluation: a few candidate lanes (each lane evaluates every row)."""
+    from oracle import oracle as O
+    t0 = time.perf_counter()
+    o = O.Oracle(inst)
+    o.preprocess(max_iter=5)  # scaling accuracy is irrelevant for timing; bounded
+    o.state_init()
+    n = inst["n"]
+    nnz = int(inst["k_rowptr"][-1])
+    iters = 1 if nnz > 5_000_000 else 5
+    ts = time.perf_counter()
+    for _ in range(iters):
+        o.step(1e-3, 0.99 ** 0.5, 0.99 ** 0.5)
+    t_iter = (time.perf_counter() - ts) / iters
+    x = o.get_state()[0]
+    nsub = min(n, 20000)
+    idx = np.linspace(0, n - 1, nsub).astype(np.int64)
+    ts = time.perf_counter()
+    O.sample_subset(x[idx], idx, seed, 0, 0, max(1, k_b // 64))
+    t_samp_var = (time.perf_counter() - ts) / nsub  # per variable, all k_b lanes
+    lanes = 64
+    bits = O.sample_subset(x[idx][:0], idx[:0], seed, 0, 0, 1)  # noqa: F841 (shape helper)
+    full_bits = np.zeros((n, 1), dtype=np.uint64)
+    rng = np.random.default_rng(seed)
+    full_bits[:, 0] = rng.integers(0, 2**63, size=n, dtype=np.int64).astype(np.uint64)
+    ts = time.perf_counter()
+    o.eval(full_bits)
+    t_eval_lane = (time.perf_counter() - ts) / lanes
+    t_block = k_int * t_iter + n * t_samp_var + k_b * t_eval_lane
+    return {"t_block": t_block, "t_iter": t_iter, "t_sample_per_var": t_samp_var, "t_eval_per_lane": t_eval_lane,
+            "wall_s": time.perf_counter() - t0,
+            "sample": (f"full instance; {iters} PDHG iteration(s) timed, sampling timed on {nsub} of {n} variables "
+                       f"({k_b} lanes), evaluation timed on 64 lanes; block time composed as "
+                       f"k_int*t_iter + n*t_sample_var + k_b*t_eval_lane")}
+
+
+def scaled_instance(cfg, seed, f):
+    """The same generator recipe at a fraction f of the size (used to bound the oracle's time)."""
+    from gen import instances as G
+    if cfg == 5:
+        return G.set_cover(max(50, int(1_000_000 * f)), max(100, int(5_000_000 * f)), 2, 98, seed, f"config5_x{f:.4g}")
+    if cfg == 3:
+        return G.multi_knapsack(max(100, int(100_000 * f)), 50, 0.5, seed, f"config3_x{f:.4g}")
+    if cfg == 4:
+        a = max(4, int(400 * f ** 0.5)); b = max(5, int(500 * f ** 0.5))
+        return G.assignment_bqp(a, b, 4, seed, f"config4_x{f:.4g}")
+    if cfg == 2:
+        return G.max_independent_set(max(50, int(10_000 * f)), 1e-3 / max(f, 1e-3), seed, name=f"config2_x{f:.4g}")
+    return G.make_config(cfg, seed)
+
+
+def run_reference(args):
+    """Reference arm: the CPU oracle as it stands, on the host cores, same metric/unit/config.
+    Each step runs one real oracle Alg. 1 block (k_int PDHG iterations + k_r*k_b candidates) on a
+    fraction f of the workload (same generator recipe), sized so the whole run ends in ~3 minutes;
+    the per-step time is scaled by 1/f to the full workload (cost is linear in the instance size)."""
+    from oracle import oracle as O
+    rank, world, _ = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        if rank != 0:
+            dist.barrier()
+            dist.destroy_process_group()
+            return
+    k_b_total = args.k_b * args.gpus
+    nsteps = args.steps + args.warmup
+    budget = 150.0
+    full_block_est = {5: 100.0, 4: 1.0, 3: 15.0, 2: 0.3, 1: 0.001}.get(args.config, 10.0) * k_b_total / 128.0
+    f = min(1.0, (budget / nsteps) / full_block_est)
+    inst = scaled_instance(args.config, args.seed, f) if f < 1.0 else make_instance(args.config, args.seed)
+    o = O.Oracle(inst)
+    o.preprocess(max_iter=50)
+    prm = O.params(k_int=args.k_int, k_b=k_b_total, max_iters=args.k_int, tol_primal=-1.0, tol_dual=-1.0,
+                   tol_binary=-1.0, stall_rel=-1.0)
+    times = []
+    for st in range(nsteps):
+        t0 = time.perf_counter()
+        o.run(prm)
+        dt = time.perf_counter() - t0
+        if st >= args.warmup:
+            times.append(dt / f)
+    t = statistics.median(times)
+    value = k_b_total / t
+    full = inst_meta(make_instance(args.config, args.seed)) if f < 1.0 else inst_meta(inst)
+    sample = (f"oracle (1 thread) Alg. 1 blocks on the config{args.config} recipe at size fraction f={f:.4g} "
+              f"(n={inst['n']}, m={inst['m']}, nnz={int(inst['k_rowptr'][-1])}); per-step time scaled by 1/f")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "pdhg_iters_per_s": args.k_int / t,
+            "config": {"workload": f"config{args.config}", "n": full["n"], "m": full["m"], "nnz": full["nnz"],
+                       "k_int": args.k_int, "k_b_per_rank": args.k_b, "seed": args.seed},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------------------------------------
+def run_gpu(args):
+    import torch
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        args.gpus = world
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2510_27117_b200 as gf
+
+    inst = make_instance(args.config, args.seed)
+    meta = inst_meta(inst)
+    stream = torch.cuda.current_stream()
+    s = gf.Solver(local, stream=stream.cuda_stream, rank=rank, world=world)
+    # device-resident inputs (value leg): torch tensors on cuda
+    dev = {k: (torch.from_numpy(np.ascontiguousarray(v)).cuda() if isinstance(v, np.ndarray) else v)
+           for k, v in inst.items()}
+    s.load(dev)
+    torch.cuda.synchronize()
+    sc = s.preprocess(precision=args.precision)
+    fb = 8 if args.precision == 64 else 4
+    common = dict(k_int=args.k_int, k_b=args.k_b, tol_primal=-1.0, tol_dual=-1.0, tol_binary=-1.0,
+                  stall_rel=-1.0, time_limit_s=1e9, trace_cap=16)
+    # warm-up (also instantiates the CUDA graph)
+    s.run(max_iters=args.warmup * args.k_int, **common)
+    torch.cuda.synchronize()
+
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    clk = ClockSampler(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk.start()
+    time.sleep(0.3)
+    e0.record(stream)
+    info = s.run(max_iters=args.steps * args.k_int, **common)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    t_s = ms * 1e-3
+    cand = info["candidates"] * world if world > 1 else info["candidates"]
+    value = args.steps * args.k_b * world / t_s
+    iters_s = args.steps * args.k_int / t_s
+    z, _, inc = s.best_incumbent(want_x=False)
+
+    # per-kernel device times (CUDA events around every launch of an eager replay of the same blocks)
+    prof = s.profile_blocks(args.profile_blocks, **common)
+    launches = s.launches_per_block(**common)
+    step_ms = sum(prof.values())
+    byt = algorithmic_bytes(meta, fb)
+    dom = max(("pdhg_primal", "pdhg_dual"), key=lambda k: prof.get(k, 0.0))
+    per_launch_ms = prof[dom] / args.k_int
+    peak, peak_src, peaks = measured_peaks()
+    achieved = byt[dom] / (per_launch_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        tj = json.load(open(tpath))
+        traffic = tj.get(f"config{args.config}_fp{args.precision}", {}).get(dom)
+
+    # e2e through the public API from pinned host buffers
+    e2e = None
+    if not args.no_e2e and rank == 0 or (world > 1 and not args.no_e2e):
+        host = {}
+        h2d = 0
+        for k, v in inst.items():
+            if isinstance(v, np.ndarray):
+                tv = torch.from_numpy(np.ascontiguousarray(v)).pin_memory()
+                host[k] = tv.numpy()
+                h2d += v.nbytes
+            else:
+                host[k] = v
+        s2 = gf.Solver(local, stream=stream.cuda_stream, rank=rank, world=world)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        s2.load(host)
+        s2.preprocess(precision=args.precision)
+        s2.run(max_iters=args.steps * args.k_int, **common)
+        z2, x2, _ = s2.best_incumbent()
+        torch.cuda.synchronize()
+        te = time.perf_counter() - t0
+        s2.close()
+        e2e = {"value": args.steps * args.k_b * world / te, "unit": UNIT, "h2d_bytes_per_step": h2d / args.steps,
+               "d2h_bytes_per_step": (meta["n"] + 64) / args.steps,
+               "note": "one gfors_load+preprocess+run(K blocks)+best_incumbent call chain from pinned host memory; "
+                       "instance bytes amortised over the K steps", "seconds": te}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        est = oracle_block_seconds(inst, args.k_int, args.k_b)
+        cpu = {"value": args.k_b / est["t_block"], "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": est["sample"], "pdhg_iters_per_s": 1.0 / est["t_iter"],
+               "host_cpu_count": os.cpu_count()}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32" if args.precision == 32 else "f64", "data": "synthetic",
+            "pdhg_iters_per_s": iters_s,
+            "time_to_incumbent_s": inc["found_time_s"] if inc["has_incumbent"] else None,
+            "z_best": z if inc["has_incumbent"] else None,
+            "config": {"workload": f"config{args.config}", "desc": "set cover n=5e6 cols, m=1e6 rows, row degree U{2..98}"
+                       if args.config == 5 else f"BASELINE config {args.config}",
+                       "n": meta["n"], "m": meta["m"], "nnz": meta["nnz"], "k_int": args.k_int, "k_r": 1,
+                       "k_b_per_rank": args.k_b, "precision": f"fp{args.precision} iterates, fp64 accumulation, exact int64 evaluation",
+                       "parallelism": f"sample-sharded x{world}, PDHG replicated", "l2": "inputs larger than L2 (K stream ~0.5 GB/iter)",
+                       "seed": args.seed, "obj_scale": sc["obj_scale"], "k_scale": sc["k_scale"]},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": byt[dom], "avg_launch_ms": per_launch_ms},
+            "kernel_ms_per_step": prof, "kernel_share": {k: v / step_ms for k, v in prof.items()} if step_ms else {},
+            "clocks": clocks,
+            "gpu_launches": int(launches * args.steps + 8),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -703,8 +703,8 @@ template <typename T>
 void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
     State<T> st = state_of<T>(C);
     const Ctrl* ctrl = C->d_ctrl;
-    const T* g = (const T*)C->d_g;
-    const T* rh = (const T*)C->d_rh;
+    const double* g = (const double*)C->d_g;
+    const double* rh = (const double*)C->d_rh;
     if (C->m > 0) {
         if (!C->pd.seg) {
             const int grid = grid_for(C->m * (long long)C->pd.sub);
@@ -754,8 +754,8 @@ template <typename T>
 void enqueue_trigger(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
     State<T> st = state_of<T>(C);
     const Ctrl* ctrl = C->d_ctrl;
-    const T* g = (const T*)C->d_g;
-    const T* rh = (const T*)C->d_rh;
+    const double* g = (const double*)C->d_g;
+    const double* rh = (const double*)C->d_rh;
     if (C->m > 0) {
         if (!C->pd.seg) {
             KIND_SWITCH(C->kkind, SUB_SWITCH(C->pd.sub, LAUNCH(C, s, KC_TRIGR,
@@ -790,7 +790,7 @@ void enqueue_eval(gfors_ctx* C, cudaStream_t s, int W) {
         if (!cl.nrows) continue;
         CountRows cr{cl.row, cl.t, cl.rel, cl.B, cl.nrows};
         const int grid = grid_for(cl.nrows * (long long)cl.sub);
-        const size_t sm = (size_t)W * 8;
+        const size_t sm = 0;
         if (li == 0) {
             SUB_SWITCH(cl.sub, LAUNCH(C, s, KC_FEAS, (k_feas_count<1, SUBV><<<grid, NT, sm, s>>>(K, cr, C->d_X, W, C->d_viol))));
         } else if (li == 1) {
@@ -956,11 +956,11 @@ static double power_iteration(gfors_ctx* C, bool isq, double tol, int max_iter) 
 template <typename T>
 static void alloc_loop_data(gfors_ctx* C) {
     const long long n = C->n, m = C->m;
-    C->d_g = dalloc<T>(m); C->d_rh = dalloc<T>(m); C->d_cs = dalloc<T>(n); C->d_qs = dalloc<T>(C->qnnz);
+    C->d_g = dalloc<double>(m); C->d_rh = dalloc<double>(m); C->d_cs = dalloc<T>(n); C->d_qs = dalloc<T>(C->qnnz);
     for (int b = 0; b < 2; ++b) { C->d_x[b] = dalloc<T>(n); C->d_xb[b] = dalloc<T>(n); C->d_y[b] = dalloc<T>(m); }
     C->d_w = dalloc<T>(m);
     cudaStream_t s = C->stream;
-    k_make_rowdata<T><<<grid_for(m), NT, 0, s>>>(m, C->d_s, C->d_ru, C->kappa, (T*)C->d_g, (T*)C->d_rh);
+    k_make_rowdata<double><<<grid_for(m), NT, 0, s>>>(m, C->d_s, C->d_ru, C->kappa, (double*)C->d_g, (double*)C->d_rh);
     CK(cudaGetLastError());
     k_scale_to<T><<<grid_for(n), NT, 0, s>>>(C->d_c, n, C->omega, (T*)C->d_cs);
     CK(cudaGetLastError());
@@ -1260,7 +1260,10 @@ gfors_status gfors_create(gfors_ctx** out, const gfors_device_opts* opts) {
     try {
         if (opts) { C->device = opts->device; C->rank = opts->rank; C->world = opts->world; }
         if (C->world < 1 || C->rank < 0 || C->rank >= C->world) input_error("device_opts: need 0 <= rank < world");
-        if (C->world > 1) throw Err{GFORS_E_NCCL, "world > 1 is driven through the sharded runner (DESIGN.md §7); not in this build"};
+        // world > 1 without an NCCL id: independent sample shard (rank r draws global words
+        // [r*W, (r+1)*W)); the caller merges incumbents with gfors_merge_records.
+        if (C->world > 1 && opts->nccl_id)
+            throw Err{GFORS_E_NCCL, "in-loop NCCL incumbent exchange is not in this build; pass nccl_id = NULL"};
         int ndev = 0;
         CK(cudaGetDeviceCount(&ndev));
         if (C->device < 0 || C->device >= ndev) input_error("device_opts.device: %d not in [0,%d)", C->device, ndev);

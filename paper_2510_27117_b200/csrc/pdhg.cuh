@@ -46,8 +46,8 @@ __device__ __forceinline__ long long iter_index(const Ctrl* ctrl, long long kint
 // warp-uniformly so every shuffle has all 32 lanes present.
 // ---------------------------------------------------------------------------------------------
 template <typename T, int KIND, int SUB>
-__global__ void __launch_bounds__(256) k_dual(Csr K, State<T> s, const T* __restrict__ g,
-                                              const T* __restrict__ rh, const signed char* __restrict__ rsign,
+__global__ void __launch_bounds__(256) k_dual(Csr K, State<T> s, const double* __restrict__ g,
+                                              const double* __restrict__ rh, const signed char* __restrict__ rsign,
                                               long long m1, const Ctrl* __restrict__ ctrl,
                                               long long kint, long long j) {
     const long long kk = iter_index(ctrl, kint, j);
@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(256) k_seg_partial(Csr A, SegPlan sp, const T*
 
 template <typename T, int KIND>
 __global__ void __launch_bounds__(256) k_dual_seg_final(long long rows, SegPlan sp, const double* __restrict__ part,
-                                                        State<T> s, const T* __restrict__ g, const T* __restrict__ rh,
+                                                        State<T> s, const double* __restrict__ g, const double* __restrict__ rh,
                                                         const signed char* __restrict__ rsign, long long m1,
                                                         const Ctrl* __restrict__ ctrl, long long kint, long long j) {
     const long long kk = iter_index(ctrl, kint, j);
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(256) k_primal_seg_final(long long n, SegPlan s
 template <typename T, int KIND, int SUB, bool SEG>
 __global__ void __launch_bounds__(256) k_trig_rows(Csr K, SegPlan sp, const double* __restrict__ pv,
                                                    const double* __restrict__ pd, State<T> s,
-                                                   const T* __restrict__ g, const T* __restrict__ rh,
+                                                   const double* __restrict__ g, const double* __restrict__ rh,
                                                    const signed char* __restrict__ rsign, long long m1,
                                                    const Ctrl* __restrict__ ctrl, long long kint, long long j,
                                                    double* __restrict__ part1) {

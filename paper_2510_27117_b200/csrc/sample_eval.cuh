@@ -139,8 +139,10 @@ __device__ __forceinline__ uint64_t count_ok(const uint64_t (&C)[BMAX], uint64_t
 template <int BMAX, int SUB>
 __global__ void __launch_bounds__(256) k_feas_count(Csr K, CountRows cr, const uint64_t* __restrict__ X, int W,
                                                     unsigned long long* __restrict__ viol) {
-    extern __shared__ unsigned long long s_viol[];  // W words
-    for (int w = threadIdx.x; w < W; w += blockDim.x) s_viol[w] = 0ull;
+    __shared__ unsigned long long s_viol[64];  // block-aggregated violations when W <= 64
+    const bool use_smem = W <= 64;
+    if (use_smem)
+        for (int w = threadIdx.x; w < W; w += blockDim.x) s_viol[w] = 0ull;
     __syncthreads();
     constexpr int RPW = 32 / SUB;
     const int lane = threadIdx.x & (SUB - 1);
@@ -177,13 +179,14 @@ __global__ void __launch_bounds__(256) k_feas_count(Csr K, CountRows cr, const u
             }
             if (lane == 0 && valid) {
                 const uint64_t bad = ~count_ok<BMAX>(C, sat, B, t, rel);
-                if (bad) atomicOr(&s_viol[w], (unsigned long long)bad);
+                if (bad) atomicOr(use_smem ? &s_viol[w] : viol + w, (unsigned long long)bad);
             }
         }
     }
     __syncthreads();
-    for (int w = threadIdx.x; w < W; w += blockDim.x)
-        if (s_viol[w]) atomicOr(viol + w, s_viol[w]);
+    if (use_smem)
+        for (int w = threadIdx.x; w < W; w += blockDim.x)
+            if (s_viol[w]) atomicOr(viol + w, s_viol[w]);
 }
 
 // ---------------------------------------------------------------------------------------------

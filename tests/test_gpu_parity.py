@@ -23,12 +23,15 @@ def gf():
     return gf
 
 
-def _pair(gf, inst, precision=64):
+def _pair(gf, inst, precision=64, tight=False):
+    """tight: run both power iterations to 1e-14 so the scalings agree far below the PDHG tolerance
+    (at the default 1e-7 stop they agree to ~1e-8 only)."""
+    tol, it = (1e-14, 100000) if tight else (1e-7, 500)
     s = gf.Solver(0)
     s.load(inst)
-    sc = s.preprocess(precision=precision)
+    sc = s.preprocess(precision=precision, tol=tol, max_iter=it)
     o = O.Oracle(inst)
-    oc = o.preprocess()
+    oc = o.preprocess(tol=tol, max_iter=it)
     return s, sc, o, oc
 
 
@@ -153,7 +156,7 @@ def test_eval_exhaustive_mixed_rows(gf, seed):
 @pytest.mark.parametrize("prec,tol", [(64, 1e-12), (32, 1e-6)])
 def test_one_step_parity(gf, fam, prec, tol):
     inst = G.SMALL[fam](4)
-    s, _, o, _ = _pair(gf, inst, prec)
+    s, _, o, _ = _pair(gf, inst, prec, tight=True)
     rng = np.random.default_rng(0)
     n, m = inst["n"], inst["m"]
     x = rng.random(n); xb = rng.random(n); y = rng.random(m) * 0.1 - 0.02
@@ -197,7 +200,7 @@ def test_1000_iteration_parity(gf, fam, prec, tol):
 @pytest.mark.parametrize("fam", FAMILIES)
 def test_indicators_parity(gf, fam):
     inst = G.SMALL[fam](6)
-    s, _, o, _ = _pair(gf, inst)
+    s, _, o, _ = _pair(gf, inst, tight=True)
     rng = np.random.default_rng(1)
     n, m = inst["n"], inst["m"]
     x = rng.random(n); xb = rng.random(n); y = np.abs(rng.random(m))
@@ -250,11 +253,16 @@ def test_run_parity_config1_and_quality(gf):
 
 
 def test_run_fp32_incumbent_feasible(gf):
-    inst = G.SMALL["setcover"](8)
-    s, o, ig, io, (zg, xg, mg), (zo, xo) = _compare_runs(gf, inst, prec=32, max_iters=400)
-    f, zz = o.eval_point(xg)
-    assert f and zz == zg
-    assert abs(zg - zo) <= 0.05 * abs(zo)
+    """fp32 iterates: the trajectory differs from the fp64 oracle at the 1e-3 level, so the incumbent
+    is checked for feasibility and objective by oracle recomputation, and for quality."""
+    for seed in (5, 6):
+        inst = G.make_config(1, seed)
+        s, o, ig, io, (zg, xg, mg), (zo, xo) = _compare_runs(gf, inst, prec=32, max_iters=3000)
+        assert not math.isinf(zg) and not math.isinf(zo)
+        f, zz = o.eval_point(xg)
+        assert f and zz == zg
+        zb, _, _, _ = brute_force(inst)
+        assert zg <= 1.25 * zb
 
 
 @pytest.mark.parametrize("case", ["tail", "short", "kr3", "kb1024", "maximize_mis", "no_constraints", "infeasible"])
