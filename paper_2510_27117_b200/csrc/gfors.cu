@@ -23,6 +23,8 @@
 #include "pdhg.cuh"
 #include "prep.cuh"
 #include "sample_eval.cuh"
+#include "rowblock.cuh"
+#include <cstdlib>
 
 using namespace gfors;
 
@@ -30,6 +32,7 @@ namespace {
 
 constexpr int NT = 256;
 constexpr int NUM_SMS_B200 = 148;
+constexpr int RB_GRID = NUM_SMS_B200 * 8;
 
 struct Err {
     gfors_status st;
@@ -115,10 +118,28 @@ struct DevSeg {
 
 struct DirPlan {  // how one product direction (K rows or K' columns) is computed
     int sub = 32;
-    bool seg = false;
+    bool seg = false;        // long rows: fixed-length segments + ordered combine
+    bool rb = false;         // row blocks of <= RB_NNZ nonzeros (default for short rows)
     long long seg_len = 1024;
     DevSeg ds;
+    long long* blk_row = nullptr;
+    long long nblk = 0;
 };
+
+// greedy nonzero-balanced row blocks: consecutive rows, <= cap nonzeros each (rows <= cap long)
+static std::vector<long long> make_rowblocks(const std::vector<int64_t>& ptr, long long rows, long long cap) {
+    std::vector<long long> b;
+    b.push_back(0);
+    long long r = 0;
+    while (r < rows) {
+        long long e = r;
+        while (e < rows && ptr[e + 1] - ptr[r] <= cap) ++e;
+        if (e == r) e = r + 1;  // (not reached when every row is <= cap)
+        b.push_back(e);
+        r = e;
+    }
+    return b;
+}
 
 DirPlan plan_direction(const std::vector<int64_t>& ptr, long long rows, cudaStream_t s,
                        std::vector<void*>& owned) {
@@ -131,6 +152,22 @@ DirPlan plan_direction(const std::vector<int64_t>& ptr, long long rows, cudaStre
     // long or few rows: fixed-length segments, one warp each (>= 8 warps per SM of work)
     const long long groups = rows;
     d.seg = (maxlen > 4096) || (groups * 32 < (long long)NUM_SMS_B200 * 2048 && nnz > (long long)NUM_SMS_B200 * 1024);
+    const char* force = getenv("GFORS_SPMV");
+    const std::string fm = force ? force : "";
+    if (maxlen <= RB_NNZ && fm != "short" && fm != "seg") {
+        d.seg = false;
+        d.rb = true;
+    } else if (fm == "short" && maxlen <= 4096) {
+        d.seg = false;
+    } else if (fm == "seg") {
+        d.seg = true;
+    }
+    if (d.rb) {
+        std::vector<long long> b = make_rowblocks(ptr, rows, RB_NNZ);
+        d.nblk = (long long)b.size() - 1;
+        d.blk_row = dupload(b, s);
+        owned.push_back(d.blk_row);
+    }
     if (d.seg) {
         long long L = 1024;
         while (L > 128 && nnz / L < (long long)NUM_SMS_B200 * 16) L /= 2;
@@ -706,7 +743,12 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
     const double* g = (const double*)C->d_g;
     const double* rh = (const double*)C->d_rh;
     if (C->m > 0) {
-        if (!C->pd.seg) {
+        if (C->pd.rb) {
+            const int grid = (int)std::min<long long>(C->pd.nblk, RB_GRID);
+            KIND_SWITCH(C->kkind, LAUNCH(C, s, KC_DUAL,
+                (k_dual_rb<T, KINDV><<<grid, RB_NT, 0, s>>>(csr_K(C), C->pd.blk_row, C->pd.nblk, st, g, rh, C->d_rsign,
+                                                            C->m1, ctrl, kint, j))));
+        } else if (!C->pd.seg) {
             const int grid = grid_for(C->m * (long long)C->pd.sub);
             KIND_SWITCH(C->kkind, SUB_SWITCH(C->pd.sub, LAUNCH(C, s, KC_DUAL,
                 (k_dual<T, KINDV, SUBV><<<grid, NT, 0, s>>>(csr_K(C), st, g, rh, C->d_rsign, C->m1, ctrl, kint, j)))));
@@ -725,7 +767,18 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
     const T* cs = (const T*)C->d_cs;
     // K' values: SIGN rows fold the sign into w, so the transpose carries no values
     const int tkind = C->kkind;
-    if (!C->pp.seg) {
+    if (C->pp.rb) {
+        const int grid = (int)std::min<long long>(C->pp.nblk, RB_GRID);
+        if (C->hasq) {
+            KIND_SWITCH(tkind, LAUNCH(C, s, KC_PRIMAL,
+                (k_primal_rb<T, KINDV, true><<<grid, RB_NT, 0, s>>>(csr_Kt(C), C->pp.blk_row, C->pp.nblk, Q, qs, st, cs,
+                                                                    ctrl, kint, j))));
+        } else {
+            KIND_SWITCH(tkind, LAUNCH(C, s, KC_PRIMAL,
+                (k_primal_rb<T, KINDV, false><<<grid, RB_NT, 0, s>>>(csr_Kt(C), C->pp.blk_row, C->pp.nblk, Q, qs, st, cs,
+                                                                     ctrl, kint, j))));
+        }
+    } else if (!C->pp.seg) {
         const int grid = grid_for(C->n * (long long)C->pp.sub);
         if (C->hasq) {
             KIND_SWITCH(tkind, SUB_SWITCH(C->pp.sub, LAUNCH(C, s, KC_PRIMAL,
@@ -757,7 +810,14 @@ void enqueue_trigger(gfors_ctx* C, cudaStream_t s, long long kint, long long j) 
     const double* g = (const double*)C->d_g;
     const double* rh = (const double*)C->d_rh;
     if (C->m > 0) {
-        if (!C->pd.seg) {
+        if (C->pd.rb) {
+            const int grid = (int)std::min<long long>(C->pd.nblk, (long long)C->nb1);
+            KIND_SWITCH(C->kkind, LAUNCH(C, s, KC_TRIGR,
+                (k_trig_rows_rb<T, KINDV><<<grid, RB_NT, 0, s>>>(csr_K(C), C->pd.blk_row, C->pd.nblk, st, g, rh,
+                                                                 C->d_rsign, C->m1, ctrl, kint, j, C->d_part1))));
+            if (grid < C->nb1)
+                LAUNCH(C, s, KC_TRIGR, (k_fill<<<1, NT, 0, s>>>(C->d_part1 + 3LL * grid, 3LL * (C->nb1 - grid), 0.0)));
+        } else if (!C->pd.seg) {
             KIND_SWITCH(C->kkind, SUB_SWITCH(C->pd.sub, LAUNCH(C, s, KC_TRIGR,
                 (k_trig_rows<T, KINDV, SUBV, false><<<C->nb1, NT, 0, s>>>(csr_K(C), C->pd.ds.plan(), nullptr, nullptr,
                     st, g, rh, C->d_rsign, C->m1, ctrl, kint, j, C->d_part1)))));
@@ -1012,7 +1072,7 @@ static void do_preprocess(gfors_ctx* C, const gfors_prep_opts* o, gfors_scaling*
     C->precision = o->precision;
     if (C->precision == 64) alloc_loop_data<double>(C); else alloc_loop_data<float>(C);
     // loop workspaces
-    C->nb1 = std::max(1, std::min(grid_for(std::max<long long>(m, 1) * 32LL), 1024));
+    C->nb1 = 1024;
     C->nb2 = std::max(1, std::min(grid_for(n), 1024));
     C->d_part1 = dalloc<double>(3LL * C->nb1);
     C->d_part2 = dalloc<double>(2LL * C->nb2);
@@ -1467,7 +1527,7 @@ int64_t gfors_launches_per_block(gfors_ctx* C, const gfors_params* p) {
     long long per_iter = 0;
     per_iter += C->m > 0 ? (C->pd.seg ? 2 : 1) : 0;
     per_iter += C->pp.seg ? 2 : 1;
-    long long trig = (C->m > 0 ? (C->pd.seg ? 3 : 1) : 1) + 1;
+    long long trig = (C->m > 0 ? (C->pd.seg ? 3 : (C->pd.rb ? 1 + (C->pd.nblk < C->nb1 ? 1 : 0) : 1)) : 1) + 1;
     long long eval = 0;
     for (auto& cl : C->cnt) eval += cl.nrows ? 1 : 0;
     eval += C->n_int ? 2 : 0;

@@ -52,9 +52,9 @@ __global__ void __launch_bounds__(256) k_dual(Csr K, State<T> s, const double* _
                                               long long kint, long long j) {
     const long long kk = iter_index(ctrl, kint, j);
     const int par = (int)(kk & 1);
-    const T* __restrict__ xb = s.xb[par];
-    const T* __restrict__ yin = s.y[par];
-    T* __restrict__ yout = s.y[par ^ 1];
+    const T* __restrict__ xb = (par ? s.xb[1] : s.xb[0]);
+    const T* __restrict__ yin = (par ? s.y[1] : s.y[0]);
+    T* __restrict__ yout = (par ? s.y[0] : s.y[1]);
     const double tau2 = ctrl->tau2;
     constexpr int RPW = 32 / SUB;  // rows per warp
     const int lane = threadIdx.x & (SUB - 1);
@@ -102,9 +102,9 @@ __global__ void __launch_bounds__(256) k_primal(Csr Kt, Csr Q, const T* __restri
                                                 long long kint, long long j) {
     const long long kk = iter_index(ctrl, kint, j);
     const int par = (int)(kk & 1);
-    const T* __restrict__ xin = s.x[par];
-    T* __restrict__ xout = s.x[par ^ 1];
-    T* __restrict__ xbout = s.xb[par ^ 1];
+    const T* __restrict__ xin = (par ? s.x[1] : s.x[0]);
+    T* __restrict__ xout = (par ? s.x[0] : s.x[1]);
+    T* __restrict__ xbout = (par ? s.xb[0] : s.xb[1]);
     const T* __restrict__ w = s.w;
     const double rho = ctrl->rho, tau1 = ctrl->tau1;
     constexpr int RPW = 32 / SUB;
@@ -210,9 +210,9 @@ __global__ void __launch_bounds__(256) k_dual_seg_final(long long rows, SegPlan 
         for (long long q = sp.row_seg[row]; q < sp.row_seg[row + 1]; ++q) acc += part[q];
         const double sg = (KIND == KV_SIGN) ? (double)rsign[row] : 1.0;
         const double gj = (double)g[row];
-        double yn = (double)s.y[par][row] + tau2 * ((double)rh[row] - gj * (sg * acc));
+        double yn = (double)(par ? s.y[1] : s.y[0])[row] + tau2 * ((double)rh[row] - gj * (sg * acc));
         if (row < m1 && yn < 0.0) yn = 0.0;
-        s.y[par ^ 1][row] = (T)yn;
+        (par ? s.y[0] : s.y[1])[row] = (T)yn;
         s.w[row] = (T)(gj * sg * yn);
     }
 }
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(256) k_primal_seg_final(long long n, SegPlan s
     const long long kk = iter_index(ctrl, kint, j);
     const int par = (int)(kk & 1);
     const double rho = ctrl->rho, tau1 = ctrl->tau1;
-    const T* __restrict__ xin = s.x[par];
+    const T* __restrict__ xin = (par ? s.x[1] : s.x[0]);
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += gridDim.x * (long long)blockDim.x) {
         double a = 0.0, b = 0.0;
         for (long long q = sp.row_seg[i]; q < sp.row_seg[i + 1]; ++q) a += part[q];
@@ -235,8 +235,8 @@ __global__ void __launch_bounds__(256) k_primal_seg_final(long long n, SegPlan s
         const double delta = (((double)cs[i] + rho) - a) + 2.0 * b - 2.0 * rho * xi;
         double xn = xi - tau1 * delta;
         xn = xn < 0.0 ? 0.0 : (xn > 1.0 ? 1.0 : xn);
-        s.x[par ^ 1][i] = (T)xn;
-        s.xb[par ^ 1][i] = (T)(2.0 * xn - xi);
+        (par ? s.x[0] : s.x[1])[i] = (T)xn;
+        (par ? s.xb[0] : s.xb[1])[i] = (T)(2.0 * xn - xi);
     }
 }
 
@@ -257,8 +257,8 @@ __global__ void __launch_bounds__(256) k_trig_rows(Csr K, SegPlan sp, const doub
     __shared__ double sh[32];
     const long long kk = iter_index(ctrl, kint, j);
     const int par = (int)(kk & 1);
-    const T* __restrict__ xk = s.x[par ^ 1];
-    const T* __restrict__ xbp = s.xb[par];
+    const T* __restrict__ xk = (par ? s.x[0] : s.x[1]);
+    const T* __restrict__ xbp = (par ? s.xb[1] : s.xb[0]);
     const double tau2 = ctrl->tau2;
     constexpr int RPW = 32 / SUB;
     const int lane = threadIdx.x & (SUB - 1);
@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(256) k_trig_rows(Csr K, SegPlan sp, const doub
             const double gj = (double)g[row];
             const double gap = (double)rh[row] - gj * (sg * v);
             if (row < m1) ge = fmax(ge, fmax(gap, 0.0)); else eq = fmax(eq, fabs(gap));
-            const double sy = ((double)s.y[par][row] - (double)s.y[par ^ 1][row]) / tau2 + gj * (sg * d);
+            const double sy = ((double)(par ? s.y[1] : s.y[0])[row] - (double)(par ? s.y[0] : s.y[1])[row]) / tau2 + gj * (sg * d);
             sy2 += sy * sy;
         }
     }
@@ -308,8 +308,8 @@ __global__ void __launch_bounds__(256) k_trig_cols(long long n, Csr Q, const T* 
     __shared__ double sh[32];
     const long long kk = iter_index(ctrl, kint, j);
     const int par = (int)(kk & 1);
-    const T* __restrict__ xk = s.x[par ^ 1];
-    const T* __restrict__ xp = s.x[par];
+    const T* __restrict__ xk = (par ? s.x[0] : s.x[1]);
+    const T* __restrict__ xp = (par ? s.x[1] : s.x[0]);
     const double rho = ctrl->rho, tau1 = ctrl->tau1;
     double sx2 = 0.0, bg = 0.0;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += gridDim.x * (long long)blockDim.x) {

@@ -1,0 +1,257 @@
+// rowblock.cuh — nonzero-balanced "row-block" SpMV kernels for the PDHG step (B200 design).
+//
+// The PDHG products K xbar (rows of K_u) and K' w (rows of the transposed CSR) have short rows
+// (2..98 and ~10 nonzeros on config 5) and random column indices, so each iteration is a stream of
+// int32 indices from HBM plus one random L2 gather per nonzero.  Measured on B200, random 4-8 byte
+// gathers saturate at ~0.9 per cycle per SM (one L1TEX wavefront each) whatever the cache policy,
+// so the kernels are built to keep that pipe full:
+//   * one CTA owns a contiguous range of rows holding <= RB_NNZ nonzeros (planned on the host);
+//   * phase 1 streams the block's indices (coalesced, evict-first) and issues one cp.async (LDGSTS)
+//     gather per nonzero straight into shared memory — no registers held by in-flight loads, so
+//     occupancy stays at 2048 threads/SM — double-buffered: the gathers of the CTA's next row block
+//     are in flight while the current one is reduced;
+//   * phase 2 reduces rows from shared memory with groups of G threads (G = 32..1 from the block's
+//     row count, fixed order => deterministic) and runs the fused epilogue (dual clamp, or primal
+//     box projection + extrapolation) with coalesced vector traffic.
+#pragma once
+#include "common.cuh"
+#include "pdhg.cuh"
+
+namespace gfors {
+
+constexpr int RB_NNZ = 2048;  // nonzeros per row block (8 per thread)
+constexpr int RB_NT = 256;
+constexpr int RB_U = RB_NNZ / RB_NT;
+
+__device__ __forceinline__ int ldcs_i32(const int* p) { return __ldcs(p); }
+
+template <typename T>
+__device__ __forceinline__ void cp_async_elem(T* smem, const T* g) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    if constexpr (sizeof(T) == 8) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(g));
+    else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(g));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;"); }
+
+// phase 1 of row block b: sv[t] = v[idx_t] for its nonzeros (values applied in phase 2)
+template <typename T>
+__device__ __forceinline__ void rb_issue(const Csr& A, const long long* __restrict__ blk_row, long long b,
+                                         long long nblk, const T* __restrict__ v, T* sv) {
+    if (b < nblk) {
+        const long long p0 = __ldg(A.ptr + blk_row[b]);
+        const int cnt = (int)(__ldg(A.ptr + blk_row[b + 1]) - p0);
+        int cols[RB_U];
+#pragma unroll
+        for (int u = 0; u < RB_U; ++u) {
+            const int t = u * RB_NT + threadIdx.x;
+            cols[u] = t < cnt ? ldcs_i32(A.idx + p0 + t) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < RB_U; ++u)
+            if (cols[u] >= 0) cp_async_elem(sv + u * RB_NT + threadIdx.x, v + cols[u]);
+    }
+    cp_async_commit();
+}
+
+__device__ __forceinline__ int rb_group_size(int nr) {
+    int G = 32;
+    while (G > 1 && G * nr > RB_NT) G >>= 1;
+    return G;
+}
+
+__device__ __forceinline__ double rb_group_sum(double v, int G) {
+    for (int o = G >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, G);
+    return v;
+}
+
+// sum of val_q * sv[q - p0] over the row's nonzeros [q0, q1) by the G lanes of a group
+template <typename T, int KIND>
+__device__ __forceinline__ double rb_row_sum(const Csr& A, const T* sv, long long p0, long long q0, long long q1,
+                                             int lane, int G) {
+    double acc = 0.0;
+    for (long long q = q0 + lane; q < q1; q += G) {
+        const double a = (double)sv[q - p0];
+        if constexpr (KIND == KV_SIGN) acc += a;
+        else acc += kval<KIND>(A.val, q) * a;
+    }
+    return acc;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Dual half-step on row blocks of K_u:
+//   y_k = Pi( y_{k-1} + tau2 (K xbar_{k-1} + r) ),  K = -diag(g) K_u,  w = g rsign y_k
+// ---------------------------------------------------------------------------------------------
+template <typename T, int KIND>
+__global__ void __launch_bounds__(RB_NT) k_dual_rb(Csr K, const long long* __restrict__ blk_row, long long nblk,
+                                                   State<T> s, const double* __restrict__ g,
+                                                   const double* __restrict__ rh, const signed char* __restrict__ rsign,
+                                                   long long m1, const Ctrl* __restrict__ ctrl, long long kint,
+                                                   long long j) {
+    __shared__ __align__(16) T sv[2][RB_NNZ];
+    const long long kk = iter_index(ctrl, kint, j);
+    const int par = (int)(kk & 1);
+    const T* __restrict__ xb = par ? s.xb[1] : s.xb[0];
+    const T* __restrict__ yin = par ? s.y[1] : s.y[0];
+    T* __restrict__ yout = par ? s.y[0] : s.y[1];
+    const double tau2 = ctrl->tau2;
+    int st = 0;
+    rb_issue<T>(K, blk_row, blockIdx.x, nblk, xb, sv[0]);
+    for (long long b = blockIdx.x; b < nblk; b += gridDim.x) {
+        rb_issue<T>(K, blk_row, b + gridDim.x, nblk, xb, sv[st ^ 1]);
+        cp_async_wait1();
+        __syncthreads();
+        const long long r0 = blk_row[b], r1 = blk_row[b + 1];
+        const long long p0 = __ldg(K.ptr + r0);
+        const int nr = (int)(r1 - r0);
+        const int G = rb_group_size(nr);
+        const int lane = threadIdx.x & (G - 1), grp = threadIdx.x / G, ngr = RB_NT / G;
+        for (int rb = 0; rb < nr; rb += ngr) {
+            const int rr = rb + grp;
+            const long long row = r0 + rr;
+            double acc = 0.0;
+            if (rr < nr) acc = rb_row_sum<T, KIND>(K, sv[st], p0, __ldg(K.ptr + row), __ldg(K.ptr + row + 1), lane, G);
+            acc = rb_group_sum(acc, G);
+            if (lane == 0 && rr < nr) {
+                const double sg = (KIND == KV_SIGN) ? (double)rsign[row] : 1.0;
+                const double gj = g[row];
+                double yn = (double)yin[row] + tau2 * (rh[row] - gj * (sg * acc));
+                if (row < m1 && yn < 0.0) yn = 0.0;
+                yout[row] = (T)yn;
+                s.w[row] = (T)(gj * sg * yn);
+            }
+        }
+        __syncthreads();
+        st ^= 1;
+    }
+    asm volatile("cp.async.wait_all;");
+}
+
+// ---------------------------------------------------------------------------------------------
+// Primal half-step on row blocks of K_u' (one "row" = one variable i):
+//   delta = c + rho + K'y_k + 2Q x_{k-1} - 2 rho x_{k-1};  x_k = Pi_[0,1](x_{k-1} - tau1 delta);
+//   xbar_k = 2 x_k - x_{k-1}
+// ---------------------------------------------------------------------------------------------
+template <typename T, int KIND, bool HASQ>
+__global__ void __launch_bounds__(RB_NT) k_primal_rb(Csr Kt, const long long* __restrict__ blk_row, long long nblk,
+                                                     Csr Q, const T* __restrict__ qs, State<T> s,
+                                                     const T* __restrict__ cs, const Ctrl* __restrict__ ctrl,
+                                                     long long kint, long long j) {
+    __shared__ __align__(16) T sv[2][RB_NNZ];
+    const long long kk = iter_index(ctrl, kint, j);
+    const int par = (int)(kk & 1);
+    const T* __restrict__ xin = par ? s.x[1] : s.x[0];
+    T* __restrict__ xout = par ? s.x[0] : s.x[1];
+    T* __restrict__ xbout = par ? s.xb[0] : s.xb[1];
+    const double rho = ctrl->rho, tau1 = ctrl->tau1;
+    int st = 0;
+    rb_issue<T>(Kt, blk_row, blockIdx.x, nblk, s.w, sv[0]);
+    for (long long b = blockIdx.x; b < nblk; b += gridDim.x) {
+        rb_issue<T>(Kt, blk_row, b + gridDim.x, nblk, s.w, sv[st ^ 1]);
+        cp_async_wait1();
+        __syncthreads();
+        const long long r0 = blk_row[b], r1 = blk_row[b + 1];
+        const long long p0 = __ldg(Kt.ptr + r0);
+        const int nr = (int)(r1 - r0);
+        const int G = rb_group_size(nr);
+        const int lane = threadIdx.x & (G - 1), grp = threadIdx.x / G, ngr = RB_NT / G;
+        for (int rb = 0; rb < nr; rb += ngr) {
+            const int rr = rb + grp;
+            const long long i = r0 + rr;
+            double a = 0.0, bq = 0.0;
+            if (rr < nr) {
+                a = rb_row_sum<T, KIND>(Kt, sv[st], p0, __ldg(Kt.ptr + i), __ldg(Kt.ptr + i + 1), lane, G);
+                if constexpr (HASQ)
+                    for (long long q = __ldg(Q.ptr + i) + lane; q < __ldg(Q.ptr + i + 1); q += G)
+                        bq += (double)__ldg(qs + q) * (double)__ldg(xin + __ldg(Q.idx + q));
+            }
+            a = rb_group_sum(a, G);
+            if constexpr (HASQ) bq = rb_group_sum(bq, G);
+            if (lane == 0 && rr < nr) {
+                const double xi = (double)xin[i];
+                const double delta = (((double)cs[i] + rho) - a) + 2.0 * bq - 2.0 * rho * xi;
+                double xn = xi - tau1 * delta;
+                xn = xn < 0.0 ? 0.0 : (xn > 1.0 ? 1.0 : xn);
+                xout[i] = (T)xn;
+                xbout[i] = (T)(2.0 * xn - xi);
+            }
+        }
+        __syncthreads();
+        st ^= 1;
+    }
+    asm volatile("cp.async.wait_all;");
+}
+
+// ---------------------------------------------------------------------------------------------
+// Trigger row pass on row blocks: v = K_u x_k, d = K_u (x_k - xbar_{k-1}).
+// Once per k_int iterations; register gathers (two vectors per nonzero).
+// ---------------------------------------------------------------------------------------------
+template <typename T, int KIND>
+__global__ void __launch_bounds__(RB_NT) k_trig_rows_rb(Csr K, const long long* __restrict__ blk_row, long long nblk,
+                                                        State<T> s, const double* __restrict__ g,
+                                                        const double* __restrict__ rh,
+                                                        const signed char* __restrict__ rsign, long long m1,
+                                                        const Ctrl* __restrict__ ctrl, long long kint, long long j,
+                                                        double* __restrict__ part1) {
+    __shared__ double sv[RB_NNZ];
+    __shared__ double sd[RB_NNZ];
+    __shared__ double sh[32];
+    const long long kk = iter_index(ctrl, kint, j);
+    const int par = (int)(kk & 1);
+    const T* __restrict__ xk = par ? s.x[0] : s.x[1];
+    const T* __restrict__ xbp = par ? s.xb[1] : s.xb[0];
+    const T* __restrict__ yprev = par ? s.y[1] : s.y[0];
+    const T* __restrict__ ynew = par ? s.y[0] : s.y[1];
+    const double tau2 = ctrl->tau2;
+    double ge = 0.0, eq = 0.0, sy2 = 0.0;
+    for (long long b = blockIdx.x; b < nblk; b += gridDim.x) {
+        const long long r0 = blk_row[b], r1 = blk_row[b + 1];
+        const long long p0 = __ldg(K.ptr + r0);
+        const int cnt = (int)(__ldg(K.ptr + r1) - p0);
+        int cols[RB_U];
+#pragma unroll
+        for (int u = 0; u < RB_U; ++u) {
+            const int t = u * RB_NT + threadIdx.x;
+            cols[u] = t < cnt ? ldcs_i32(K.idx + p0 + t) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < RB_U; ++u) {
+            const int t = u * RB_NT + threadIdx.x;
+            if (t < cnt) {
+                const double a = (double)__ldg(xk + cols[u]);
+                sv[t] = a;
+                sd[t] = a - (double)__ldg(xbp + cols[u]);
+            }
+        }
+        __syncthreads();
+        const int nr = (int)(r1 - r0);
+        const int G = rb_group_size(nr);
+        const int lane = threadIdx.x & (G - 1), grp = threadIdx.x / G, ngr = RB_NT / G;
+        for (int rb = 0; rb < nr; rb += ngr) {
+            const int rr = rb + grp;
+            const long long row = r0 + rr;
+            double v = 0.0, d = 0.0;
+            if (rr < nr) {
+                v = rb_row_sum<double, KIND>(K, sv, p0, __ldg(K.ptr + row), __ldg(K.ptr + row + 1), lane, G);
+                d = rb_row_sum<double, KIND>(K, sd, p0, __ldg(K.ptr + row), __ldg(K.ptr + row + 1), lane, G);
+            }
+            v = rb_group_sum(v, G);
+            d = rb_group_sum(d, G);
+            if (lane == 0 && rr < nr) {
+                const double sg = (KIND == KV_SIGN) ? (double)rsign[row] : 1.0;
+                const double gj = g[row];
+                const double gap = rh[row] - gj * (sg * v);
+                if (row < m1) ge = fmax(ge, fmax(gap, 0.0)); else eq = fmax(eq, fabs(gap));
+                const double sy = ((double)yprev[row] - (double)ynew[row]) / tau2 + gj * (sg * d);
+                sy2 += sy * sy;
+            }
+        }
+        __syncthreads();
+    }
+    const double a = block_max<RB_NT>(ge, sh);
+    const double bb = block_max<RB_NT>(eq, sh);
+    const double c = block_sum<RB_NT>(sy2, sh);
+    if (threadIdx.x == 0) { part1[3 * blockIdx.x] = a; part1[3 * blockIdx.x + 1] = bb; part1[3 * blockIdx.x + 2] = c; }
+}
+
+}  // namespace gfors
