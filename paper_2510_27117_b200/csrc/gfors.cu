@@ -337,6 +337,10 @@ struct gfors_ctx {
     double* d_z = nullptr;
     long long z_len = 0;
     int obj_chunk = 2048;
+    bool obj_bits = false;        // integral c with a small range: bit-plane objective kernel
+    unsigned* d_planes = nullptr;  // [ceil(n/32)][obj_nb] coefficient bit planes of c - cmin
+    int obj_nb = 0;
+    long long obj_cmin = 0;
     long long hk = 0;  // iterations done in hook mode (parity)
     bool have_run = false;
     gfors_run_info last_info{};
@@ -373,6 +377,8 @@ void gfors_ctx::free_problem() {
     for (auto& c : cnt) c = CountList{};
     d_int_row = nullptr; d_int_rhs = nullptr; d_int_eq = nullptr; d_int_seg_start = nullptr; d_int_seg_slot = nullptr;
     d_real_row = nullptr;
+    d_planes = nullptr;
+    obj_bits = false;
     pd = DirPlan{}; pp = DirPlan{};
 }
 
@@ -648,7 +654,7 @@ static void do_load(gfors_ctx* C, const gfors_problem* P) {
             cl.t = (int*)own(dupload(ct[li], s));
             cl.rel = (signed char*)own(dupload(crel[li], s));
             cl.B = (signed char*)own(dupload(cB[li], s));
-            cl.sub = pick_sub((double)cnt_nnz[li] / (double)cl.nrows);
+            cl.sub = pick_sub((double)cnt_nnz[li] / (double)cl.nrows / 6.0);  // ~6 gathers per lane
         }
     }
     C->n_int = (long long)irow.size();
@@ -668,6 +674,29 @@ static void do_load(gfors_ctx* C, const gfors_problem* P) {
         }
         C->d_int_seg_start = (long long*)own(dupload(se, s));
         C->d_int_seg_slot = (int*)own(dupload(iseg_slot, s));
+    }
+    // coefficient bit planes for the objective kernel (integral c with max - min < 2^20)
+    C->obj_bits = false;
+    if (C->integral) {
+        double cmin = C->c[0], cmax = C->c[0];
+        for (double v : C->c) { cmin = std::min(cmin, v); cmax = std::max(cmax, v); }
+        const long long range = (long long)(cmax - cmin);
+        if (range < (1LL << 20)) {
+            int nb = 0;
+            while ((1LL << nb) <= range) ++nb;
+            if (nb == 0) nb = 1;
+            const long long nch = (n + 31) / 32;
+            std::vector<unsigned> planes(nch * nb, 0u);
+            for (long long i = 0; i < n; ++i) {
+                const long long cp = (long long)(C->c[i] - cmin);
+                for (int b = 0; b < nb; ++b)
+                    if ((cp >> b) & 1) planes[(i / 32) * nb + b] |= 1u << (i % 32);
+            }
+            C->d_planes = (unsigned*)own(dupload(planes, s));
+            C->obj_nb = nb;
+            C->obj_cmin = (long long)cmin;
+            C->obj_bits = getenv("GFORS_OBJ_SIMPLE") == nullptr;
+        }
     }
     C->n_real = (long long)rrow.size();
     if (C->n_real) C->d_real_row = (int*)own(dupload(rrow, s));
@@ -842,6 +871,13 @@ void enqueue_trigger(gfors_ctx* C, cudaStream_t s, long long kint, long long j) 
                                                                              kint, j, C->d_part2)));
 }
 
+// 32-variable chunks per warp job of k_obj_bits: enough jobs for ~64 warps per SM
+int obj_vpj(const gfors_ctx* C, int W) {
+    const long long nchunk32 = (C->n + 31) / 32;
+    long long v = nchunk32 * W / ((long long)NUM_SMS_B200 * 64);
+    return (int)std::max<long long>(1, std::min<long long>(64, v));
+}
+
 // evaluation of the batch in d_X (W words per variable); viol/iacc must have been reset
 void enqueue_eval(gfors_ctx* C, cudaStream_t s, int W) {
     const Csr K = csr_K(C);
@@ -851,13 +887,19 @@ void enqueue_eval(gfors_ctx* C, cudaStream_t s, int W) {
         CountRows cr{cl.row, cl.t, cl.rel, cl.B, cl.nrows};
         const int grid = grid_for(cl.nrows * (long long)cl.sub);
         const size_t sm = 0;
+        const int wv = (W % 4 == 0) ? 4 : ((W % 2 == 0) ? 2 : 1);
+#define FEAS_WV(BM)                                                                                                \
+    if (wv == 4) { SUB_SWITCH(cl.sub, LAUNCH(C, s, KC_FEAS, (k_feas_count<BM, SUBV, 4><<<grid, NT, sm, s>>>(K, cr, C->d_X, W, C->d_viol)))); } \
+    else if (wv == 2) { SUB_SWITCH(cl.sub, LAUNCH(C, s, KC_FEAS, (k_feas_count<BM, SUBV, 2><<<grid, NT, sm, s>>>(K, cr, C->d_X, W, C->d_viol)))); } \
+    else { SUB_SWITCH(cl.sub, LAUNCH(C, s, KC_FEAS, (k_feas_count<BM, SUBV, 1><<<grid, NT, sm, s>>>(K, cr, C->d_X, W, C->d_viol)))); }
         if (li == 0) {
-            SUB_SWITCH(cl.sub, LAUNCH(C, s, KC_FEAS, (k_feas_count<1, SUBV><<<grid, NT, sm, s>>>(K, cr, C->d_X, W, C->d_viol))));
+            FEAS_WV(1)
         } else if (li == 1) {
-            SUB_SWITCH(cl.sub, LAUNCH(C, s, KC_FEAS, (k_feas_count<2, SUBV><<<grid, NT, sm, s>>>(K, cr, C->d_X, W, C->d_viol))));
+            FEAS_WV(2)
         } else {
-            SUB_SWITCH(cl.sub, LAUNCH(C, s, KC_FEAS, (k_feas_count<8, SUBV><<<grid, NT, sm, s>>>(K, cr, C->d_X, W, C->d_viol))));
+            FEAS_WV(8)
         }
+#undef FEAS_WV
     }
     if (C->n_int) {
         IntRows ir{C->d_int_row, C->d_int_rhs, C->d_int_eq, C->d_int_seg_start, C->d_int_seg_slot, C->n_int, C->n_int_seg};
@@ -873,18 +915,32 @@ void enqueue_eval(gfors_ctx* C, cudaStream_t s, int W) {
     const long long nchunk = (C->n + C->obj_chunk - 1) / C->obj_chunk;
     const int grid = grid_for(nchunk * 2LL * W * 32);
     const Csr Q = csr_Q(C);
-    if (C->integral) {
+    if (C->obj_bits) {
+        // linear term by coefficient bit planes, quadratic term (if any) appended as extra partial rows
+        const long long nchunk32 = (C->n + 31) / 32;
+        const int vpj = obj_vpj(C, W);
+        const long long jpw = (nchunk32 + vpj - 1) / vpj;
+        LAUNCH(C, s, KC_OBJ, (k_obj_bits<<<grid_for(jpw * W * 32), NT, 0, s>>>(C->n, vpj, C->d_planes, C->obj_nb, C->obj_cmin,
+                                                                             C->d_X, W, (long long*)C->d_zpart)));
+        long long rows = jpw;
+        if (C->hasq) {
+            long long* zq = (long long*)C->d_zpart + jpw * 64LL * W;
+            LAUNCH(C, s, KC_OBJ, (k_obj_quad<true><<<grid, NT, 0, s>>>(C->n, C->obj_chunk, Q, C->d_qval, C->d_X, W, zq)));
+            rows += nchunk;
+        }
+        LAUNCH(C, s, KC_OBJ, (k_obj_final<true><<<2 * W, 1024, 0, s>>>(rows, W, C->d_zpart, C->c0, C->d_z)));
+    } else if (C->integral) {
         if (C->hasq)
             LAUNCH(C, s, KC_OBJ, (k_obj_partial<true, true><<<grid, NT, 0, s>>>(C->n, C->obj_chunk, C->d_c, Q, C->d_qval, C->d_X, W, C->d_zpart)));
         else
             LAUNCH(C, s, KC_OBJ, (k_obj_partial<true, false><<<grid, NT, 0, s>>>(C->n, C->obj_chunk, C->d_c, Q, C->d_qval, C->d_X, W, C->d_zpart)));
-        LAUNCH(C, s, KC_OBJ, (k_obj_final<true><<<grid_for(64LL * W), NT, 0, s>>>(nchunk, W, C->d_zpart, C->c0, C->d_z)));
+        LAUNCH(C, s, KC_OBJ, (k_obj_final<true><<<2 * W, 1024, 0, s>>>(nchunk, W, C->d_zpart, C->c0, C->d_z)));
     } else {
         if (C->hasq)
             LAUNCH(C, s, KC_OBJ, (k_obj_partial<false, true><<<grid, NT, 0, s>>>(C->n, C->obj_chunk, C->d_c, Q, C->d_qval, C->d_X, W, C->d_zpart)));
         else
             LAUNCH(C, s, KC_OBJ, (k_obj_partial<false, false><<<grid, NT, 0, s>>>(C->n, C->obj_chunk, C->d_c, Q, C->d_qval, C->d_X, W, C->d_zpart)));
-        LAUNCH(C, s, KC_OBJ, (k_obj_final<false><<<grid_for(64LL * W), NT, 0, s>>>(nchunk, W, C->d_zpart, C->c0, C->d_z)));
+        LAUNCH(C, s, KC_OBJ, (k_obj_final<false><<<2 * W, 1024, 0, s>>>(nchunk, W, C->d_zpart, C->c0, C->d_z)));
     }
 }
 
@@ -910,7 +966,13 @@ void ensure_batch(gfors_ctx* C, int W) {
     }
     if (!C->d_iacc) { C->d_iacc = dalloc<unsigned long long>(1); C->iacc_len = 1; }
     const long long nchunk = (C->n + C->obj_chunk - 1) / C->obj_chunk;
-    const long long zp = nchunk * 64LL * W;
+    long long zrows = nchunk;
+    if (C->obj_bits) {
+        const long long nchunk32 = (C->n + 31) / 32;
+        const int vpj = obj_vpj(C, W);
+        zrows = (nchunk32 + vpj - 1) / vpj + (C->hasq ? nchunk : 0);
+    }
+    const long long zp = zrows * 64LL * W;
     if (zp > C->zpart_len) { dfree(C->d_zpart); C->d_zpart = dalloc<double>(zp); C->zpart_len = zp; C->gvalid = false; }
     if (64LL * W > C->z_len) { dfree(C->d_z); C->d_z = dalloc<double>(64LL * W); C->z_len = 64LL * W; C->gvalid = false; }
 }
@@ -1532,7 +1594,7 @@ int64_t gfors_launches_per_block(gfors_ctx* C, const gfors_params* p) {
     for (auto& cl : C->cnt) eval += cl.nrows ? 1 : 0;
     eval += C->n_int ? 2 : 0;
     eval += C->n_real ? 1 : 0;
-    eval += 2;  // objective partial + final
+    eval += 2 + ((C->obj_bits && C->hasq) ? 1 : 0);  // objective partial(s) + final
     const long long per_round = 1 /*reset*/ + 1 /*sample*/ + eval + 2 /*argmin, copy*/;
     C->launches = before;
     return per_iter * p->k_int + trig + per_round * p->k_r + 1 /*halt*/;

@@ -8,6 +8,7 @@
 #pragma once
 #include "common.cuh"
 #include "pdhg.cuh"
+#include <type_traits>
 
 namespace gfors {
 
@@ -136,7 +137,23 @@ __device__ __forceinline__ uint64_t count_ok(const uint64_t (&C)[BMAX], uint64_t
     return ~sat & eq;
 }
 
-template <int BMAX, int SUB>
+template <int WV>
+__device__ __forceinline__ void load_words(const uint64_t* __restrict__ p, uint64_t (&v)[WV]) {
+    if constexpr (WV == 1) {
+        v[0] = __ldg(p);
+    } else if constexpr (WV == 2) {
+        const ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(p));
+        v[0] = a.x; v[1] = a.y;
+    } else {
+        const ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(p));
+        const ulonglong2 b = __ldg(reinterpret_cast<const ulonglong2*>(p) + 1);
+        v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+    }
+}
+
+// One SUB-lane group per count row; each nonzero gathers WV words (64*WV candidates) with one
+// vector load, so a covering row over 128 candidates costs one 16-byte gather per nonzero.
+template <int BMAX, int SUB, int WV>
 __global__ void __launch_bounds__(256) k_feas_count(Csr K, CountRows cr, const uint64_t* __restrict__ X, int W,
                                                     unsigned long long* __restrict__ viol) {
     __shared__ unsigned long long s_viol[64];  // block-aggregated violations when W <= 64
@@ -159,27 +176,36 @@ __global__ void __launch_bounds__(256) k_feas_count(Csr K, CountRows cr, const u
             p0 = __ldg(K.ptr + row); p1 = __ldg(K.ptr + row + 1);
             B = cr.B[e]; t = cr.t[e]; rel = cr.rel[e];
         }
-        for (int w = 0; w < W; ++w) {
-            uint64_t C[BMAX];
+        for (int w0 = 0; w0 < W; w0 += WV) {
+            uint64_t C[WV][BMAX];
+            uint64_t sat[WV];
 #pragma unroll
-            for (int q = 0; q < BMAX; ++q) C[q] = 0ull;
-            uint64_t sat = 0ull;
+            for (int u = 0; u < WV; ++u) {
+                sat[u] = 0ull;
+#pragma unroll
+                for (int q = 0; q < BMAX; ++q) C[u][q] = 0ull;
+            }
             if (rel != 3)
                 for (long long p = p0 + lane; p < p1; p += SUB) {
-                    const uint64_t v = __ldg(X + (long long)__ldg(K.idx + p) * W + w);
-                    csa_add_bit<BMAX>(C, sat, v, B);
+                    uint64_t v[WV];
+                    load_words<WV>(X + (long long)__ldg(K.idx + p) * W + w0, v);
+#pragma unroll
+                    for (int u = 0; u < WV; ++u) csa_add_bit<BMAX>(C[u], sat[u], v[u], B);
                 }
 #pragma unroll
-            for (int o = SUB / 2; o > 0; o >>= 1) {
-                uint64_t D[BMAX];
+            for (int u = 0; u < WV; ++u) {
 #pragma unroll
-                for (int q = 0; q < BMAX; ++q) D[q] = __shfl_xor_sync(0xffffffffu, C[q], o, SUB);
-                const uint64_t dsat = __shfl_xor_sync(0xffffffffu, sat, o, SUB);
-                csa_add_counter<BMAX>(C, sat, D, dsat, B);
-            }
-            if (lane == 0 && valid) {
-                const uint64_t bad = ~count_ok<BMAX>(C, sat, B, t, rel);
-                if (bad) atomicOr(use_smem ? &s_viol[w] : viol + w, (unsigned long long)bad);
+                for (int o = SUB / 2; o > 0; o >>= 1) {
+                    uint64_t D[BMAX];
+#pragma unroll
+                    for (int q = 0; q < BMAX; ++q) D[q] = __shfl_xor_sync(0xffffffffu, C[u][q], o, SUB);
+                    const uint64_t dsat = __shfl_xor_sync(0xffffffffu, sat[u], o, SUB);
+                    csa_add_counter<BMAX>(C[u], sat[u], D, dsat, B);
+                }
+                if (lane == 0 && valid) {
+                    const uint64_t bad = ~count_ok<BMAX>(C[u], sat[u], B, t, rel);
+                    if (bad) atomicOr(use_smem ? &s_viol[w0 + u] : viol + w0 + u, (unsigned long long)bad);
+                }
             }
         }
     }
@@ -327,19 +353,113 @@ __global__ void __launch_bounds__(256) k_obj_partial(long long n, int chunk, con
     }
 }
 
-template <bool INTEGRAL>
-__global__ void k_obj_final(long long nchunk, int W, const void* __restrict__ zpart, double c0, double* __restrict__ z) {
-    const long long lanes = 64LL * W;
-    for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < lanes; l += gridDim.x * (long long)blockDim.x) {
-        if constexpr (INTEGRAL) {
-            long long s = 0;
-            for (long long ch = 0; ch < nchunk; ++ch) s += reinterpret_cast<const long long*>(zpart)[ch * lanes + l];
-            z[l] = (double)(s + (long long)c0);
-        } else {
-            double s = 0.0;
-            for (long long ch = 0; ch < nchunk; ++ch) s += reinterpret_cast<const double*>(zpart)[ch * lanes + l];
-            z[l] = s + c0;
+// Integral linear objective by bit planes: with c'_i = c_i - cmin in [0, 2^NB),
+// sum_i c_i x_li = cmin * sum_i x_li + sum_b 2^b popc(column_l & plane_b).  A warp takes 32
+// consecutive variables of one word, transposes the 32x32 bit blocks (lanes 0-31 and 32-63) with
+// shuffles so thread t holds sample lane t's 32 variable bits, then ANDs with the precomputed
+// coefficient bit planes (planes[chunk*NB + b], bit v = bit b of c'_{32 chunk + v}) and popcounts.
+__device__ __forceinline__ unsigned transpose32(unsigned x, int lane) {
+    const unsigned masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const int j = 16 >> k;
+        const unsigned m = masks[k];
+        const unsigned o = __shfl_xor_sync(0xffffffffu, x, j);
+        x = (lane & j) ? ((x & ~m) | ((o & ~m) >> j)) : ((x & m) | ((o & m) << j));
+    }
+    return x;
+}
+
+__global__ void __launch_bounds__(256) k_obj_bits(long long n, int vchunks_per_job, const unsigned* __restrict__ planes,
+                                                  int NB, long long cmin, const uint64_t* __restrict__ X, int W,
+                                                  long long* __restrict__ zpart /*[njob_per_word][64W]*/) {
+    const int lane = threadIdx.x & 31;
+    const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = (gridDim.x * (long long)blockDim.x) >> 5;
+    const long long nchunk32 = (n + 31) / 32;
+    const long long jobs_per_word = (nchunk32 + vchunks_per_job - 1) / vchunks_per_job;
+    for (long long job = warp; job < jobs_per_word * W; job += nwarps) {
+        const int w = (int)(job % W);
+        const long long jr = job / W;
+        const long long c0 = jr * vchunks_per_job, c1 = min(nchunk32, c0 + vchunks_per_job);
+        long long alo = 0, ahi = 0;
+        for (long long ch = c0; ch < c1; ++ch) {
+            const long long i = ch * 32 + lane;
+            const uint64_t xw = i < n ? __ldg(X + i * W + w) : 0ull;
+            const unsigned tlo = transpose32((unsigned)xw, lane);
+            const unsigned thi = transpose32((unsigned)(xw >> 32), lane);
+            long long slo = 0, shi = 0;
+            for (int b = 0; b < NB; ++b) {
+                const unsigned pl = __ldg(planes + ch * NB + b);
+                slo += (long long)__popc(tlo & pl) << b;
+                shi += (long long)__popc(thi & pl) << b;
+            }
+            alo += slo + cmin * __popc(tlo);
+            ahi += shi + cmin * __popc(thi);
         }
+        long long* zp = zpart + jr * 64LL * W + 64LL * w;
+        zp[lane] = alo;
+        zp[32 + lane] = ahi;
+    }
+}
+
+// Quadratic term only (x'Qx per lane), exact int64, added into zpart row `slot`
+template <bool INTEGRAL>
+__global__ void __launch_bounds__(256) k_obj_quad(long long n, int chunk, Csr Q, const double* __restrict__ qv,
+                                                  const uint64_t* __restrict__ X, int W, void* __restrict__ zpart) {
+    const int t = threadIdx.x & 31;
+    const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = (gridDim.x * (long long)blockDim.x) >> 5;
+    const long long groups = 2LL * W;
+    const long long nchunk = (n + chunk - 1) / chunk;
+    for (long long job = warp; job < nchunk * groups; job += nwarps) {
+        const long long ch = job / groups;
+        const int gidx = (int)(job - ch * groups);
+        const int w = gidx >> 1, bit = ((gidx & 1) << 5) + t;
+        const long long i0 = ch * chunk, i1 = min(n, i0 + chunk);
+        long long ai = 0;
+        double ad = 0.0;
+        for (long long ii = i0; ii < i1; ++ii) {
+            const uint64_t xi = __ldg(X + ii * W + w);
+            if (!((xi >> bit) & 1ull)) continue;
+            for (long long q = __ldg(Q.ptr + ii); q < __ldg(Q.ptr + ii + 1); ++q) {
+                const uint64_t xq = __ldg(X + (long long)__ldg(Q.idx + q) * W + w);
+                if ((xq >> bit) & 1ull) {
+                    if constexpr (INTEGRAL) ai += (long long)__ldg(qv + q); else ad += __ldg(qv + q);
+                }
+            }
+        }
+        const long long o = ch * 64LL * W + 64LL * w + bit;
+        if constexpr (INTEGRAL) reinterpret_cast<long long*>(zpart)[o] = ai;
+        else reinterpret_cast<double*>(zpart)[o] = ad;
+    }
+}
+
+// z_l = sum over partial rows (fixed order) + c0.  One CTA of 1024 threads per 32 lanes: 32 row
+// groups x 32 lanes, four independent accumulators per thread, then a fixed-order combine.
+template <bool INTEGRAL>
+__global__ void __launch_bounds__(1024) k_obj_final(long long nrows, int W, const void* __restrict__ zpart, double c0,
+                                                    double* __restrict__ z) {
+    using A = typename std::conditional<INTEGRAL, long long, double>::type;
+    __shared__ A sh[32][33];
+    const long long lanes = 64LL * W;
+    const int t = threadIdx.x & 31, grp = threadIdx.x >> 5;
+    const long long l = blockIdx.x * 32LL + t;
+    const A* zp = reinterpret_cast<const A*>(zpart);
+    A a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+    long long r = grp;
+    for (; r + 96 < nrows; r += 128) {
+        a0 += zp[r * lanes + l]; a1 += zp[(r + 32) * lanes + l];
+        a2 += zp[(r + 64) * lanes + l]; a3 += zp[(r + 96) * lanes + l];
+    }
+    for (; r < nrows; r += 32) a0 += zp[r * lanes + l];
+    sh[grp][t] = (a0 + a1) + (a2 + a3);
+    __syncthreads();
+    if (grp == 0) {
+        A s = 0;
+        for (int g = 0; g < 32; ++g) s += sh[g][t];
+        if constexpr (INTEGRAL) z[l] = (double)(s + (long long)c0);
+        else z[l] = s + c0;
     }
 }
 
