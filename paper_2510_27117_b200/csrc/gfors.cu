@@ -24,6 +24,7 @@
 #include "prep.cuh"
 #include "sample_eval.cuh"
 #include "rowblock.cuh"
+#include "trig.cuh"
 #include <cstdlib>
 
 using namespace gfors;
@@ -119,7 +120,8 @@ struct DevSeg {
 struct DirPlan {  // how one product direction (K rows or K' columns) is computed
     int sub = 32;
     bool seg = false;        // long rows: fixed-length segments + ordered combine
-    bool rb = false;         // row blocks of <= RB_NNZ nonzeros (default for short rows)
+    bool rb = false;         // row blocks of <= RB_NNZ nonzeros per CTA
+    bool wrb = false;        // warp row blocks of <= WRB_NNZ nonzeros (default for short rows)
     long long seg_len = 1024;
     DevSeg ds;
     long long* blk_row = nullptr;
@@ -154,7 +156,12 @@ DirPlan plan_direction(const std::vector<int64_t>& ptr, long long rows, cudaStre
     d.seg = (maxlen > 4096) || (groups * 32 < (long long)NUM_SMS_B200 * 2048 && nnz > (long long)NUM_SMS_B200 * 1024);
     const char* force = getenv("GFORS_SPMV");
     const std::string fm = force ? force : "";
-    if (maxlen <= RB_NNZ && fm != "short" && fm != "seg") {
+    // warp-level row blocks measured slower than CTA row blocks on config 5 (276 vs 259 us per
+    // dual launch); kept behind GFORS_SPMV=wrb for experiments
+    if (maxlen <= WRB_NNZ && fm == "wrb") {
+        d.seg = false;
+        d.wrb = true;
+    } else if (maxlen <= RB_NNZ && fm != "short" && fm != "seg") {
         d.seg = false;
         d.rb = true;
     } else if (fm == "short" && maxlen <= 4096) {
@@ -162,8 +169,8 @@ DirPlan plan_direction(const std::vector<int64_t>& ptr, long long rows, cudaStre
     } else if (fm == "seg") {
         d.seg = true;
     }
-    if (d.rb) {
-        std::vector<long long> b = make_rowblocks(ptr, rows, RB_NNZ);
+    if (d.rb || d.wrb) {
+        std::vector<long long> b = make_rowblocks(ptr, rows, d.wrb ? WRB_NNZ : RB_NNZ);
         d.nblk = (long long)b.size() - 1;
         d.blk_row = dupload(b, s);
         owned.push_back(d.blk_row);
@@ -772,7 +779,12 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
     const double* g = (const double*)C->d_g;
     const double* rh = (const double*)C->d_rh;
     if (C->m > 0) {
-        if (C->pd.rb) {
+        if (C->pd.wrb) {
+            const int grid = (int)std::min<long long>((C->pd.nblk + WRB_WARPS - 1) / WRB_WARPS, RB_GRID);
+            KIND_SWITCH(C->kkind, LAUNCH(C, s, KC_DUAL,
+                (k_dual_wrb<T, KINDV><<<grid, 32 * WRB_WARPS, 0, s>>>(csr_K(C), C->pd.blk_row, C->pd.nblk, st, g, rh,
+                                                                      C->d_rsign, C->m1, ctrl, kint, j))));
+        } else if (C->pd.rb) {
             const int grid = (int)std::min<long long>(C->pd.nblk, RB_GRID);
             KIND_SWITCH(C->kkind, LAUNCH(C, s, KC_DUAL,
                 (k_dual_rb<T, KINDV><<<grid, RB_NT, 0, s>>>(csr_K(C), C->pd.blk_row, C->pd.nblk, st, g, rh, C->d_rsign,
@@ -796,7 +808,18 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
     const T* cs = (const T*)C->d_cs;
     // K' values: SIGN rows fold the sign into w, so the transpose carries no values
     const int tkind = C->kkind;
-    if (C->pp.rb) {
+    if (C->pp.wrb) {
+        const int grid = (int)std::min<long long>((C->pp.nblk + WRB_WARPS - 1) / WRB_WARPS, RB_GRID);
+        if (C->hasq) {
+            KIND_SWITCH(tkind, LAUNCH(C, s, KC_PRIMAL,
+                (k_primal_wrb<T, KINDV, true><<<grid, 32 * WRB_WARPS, 0, s>>>(csr_Kt(C), C->pp.blk_row, C->pp.nblk, Q, qs,
+                                                                              st, cs, ctrl, kint, j))));
+        } else {
+            KIND_SWITCH(tkind, LAUNCH(C, s, KC_PRIMAL,
+                (k_primal_wrb<T, KINDV, false><<<grid, 32 * WRB_WARPS, 0, s>>>(csr_Kt(C), C->pp.blk_row, C->pp.nblk, Q, qs,
+                                                                               st, cs, ctrl, kint, j))));
+        }
+    } else if (C->pp.rb) {
         const int grid = (int)std::min<long long>(C->pp.nblk, RB_GRID);
         if (C->hasq) {
             KIND_SWITCH(tkind, LAUNCH(C, s, KC_PRIMAL,
@@ -839,7 +862,22 @@ void enqueue_trigger(gfors_ctx* C, cudaStream_t s, long long kint, long long j) 
     const double* g = (const double*)C->d_g;
     const double* rh = (const double*)C->d_rh;
     if (C->m > 0) {
-        if (C->pd.rb) {
+        if (C->pd.rb && getenv("GFORS_TRIG_CP")) {  // cp.async variant: measured slower (1.01 vs 0.65 ms)
+            const int grid = (int)std::min<long long>(C->pd.nblk, (long long)C->nb1);
+            KIND_SWITCH(C->kkind, {
+                const size_t sm = trig_cp_smem<T, KINDV>();
+                static bool attr_set = false;  // per template instantiation
+                if (!attr_set) {
+                    CK(cudaFuncSetAttribute(k_trig_rows_cp<T, KINDV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+                    attr_set = true;
+                }
+                LAUNCH(C, s, KC_TRIGR,
+                    (k_trig_rows_cp<T, KINDV><<<grid, RB_NT, sm, s>>>(csr_K(C), C->pd.blk_row, C->pd.nblk, st, g, rh,
+                                                                      C->d_rsign, C->m1, ctrl, kint, j, C->d_part1)));
+            });
+            if (grid < C->nb1)
+                LAUNCH(C, s, KC_TRIGR, (k_fill<<<1, NT, 0, s>>>(C->d_part1 + 3LL * grid, 3LL * (C->nb1 - grid), 0.0)));
+        } else if (C->pd.rb || C->pd.wrb) {
             const int grid = (int)std::min<long long>(C->pd.nblk, (long long)C->nb1);
             KIND_SWITCH(C->kkind, LAUNCH(C, s, KC_TRIGR,
                 (k_trig_rows_rb<T, KINDV><<<grid, RB_NT, 0, s>>>(csr_K(C), C->pd.blk_row, C->pd.nblk, st, g, rh,
@@ -1589,7 +1627,7 @@ int64_t gfors_launches_per_block(gfors_ctx* C, const gfors_params* p) {
     long long per_iter = 0;
     per_iter += C->m > 0 ? (C->pd.seg ? 2 : 1) : 0;
     per_iter += C->pp.seg ? 2 : 1;
-    long long trig = (C->m > 0 ? (C->pd.seg ? 3 : (C->pd.rb ? 1 + (C->pd.nblk < C->nb1 ? 1 : 0) : 1)) : 1) + 1;
+    long long trig = (C->m > 0 ? (C->pd.seg ? 3 : ((C->pd.rb || C->pd.wrb) ? 1 + (C->pd.nblk < C->nb1 ? 1 : 0) : 1)) : 1) + 1;
     long long eval = 0;
     for (auto& cl : C->cnt) eval += cl.nrows ? 1 : 0;
     eval += C->n_int ? 2 : 0;
