@@ -13,6 +13,10 @@
 #include <string.h>
 
 #include <algorithm>
+#include <climits>
+#include <mutex>
+#include <thread>
+#include <cub/cub.cuh>
 #include <cstdarg>
 #include <memory>
 #include <string>
@@ -413,303 +417,7 @@ gfors_ctx::~gfors_ctx() {
     if (own_stream && stream) cudaStreamDestroy(stream);
 }
 
-// =============================================================================================
-// Load: validate, canonicalise, layouts (a1)
-// =============================================================================================
-static void validate_csr(long long rows, long long cols, const int64_t* ptr, const int32_t* idx, const double* val,
-                         const char* name) {
-    if (ptr[0] != 0) input_error("%s: row_ptr[0] must be 0", name);
-    for (long long r = 0; r < rows; ++r) {
-        if (ptr[r + 1] < ptr[r]) input_error("%s: row_ptr decreases at row %lld", name, r);
-        for (long long p = ptr[r]; p < ptr[r + 1]; ++p) {
-            if (idx[p] < 0 || idx[p] >= cols) input_error("%s: column index out of range at nonzero %lld", name, p);
-            if (p > ptr[r] && idx[p] <= idx[p - 1])
-                input_error("%s: column indices not strictly increasing in row %lld", name, r);
-            if (!std::isfinite(val[p])) input_error("%s: non-finite value at nonzero %lld", name, p);
-            if (val[p] == 0.0) input_error("%s: explicit zero at nonzero %lld", name, p);
-        }
-    }
-}
-
-static bool is_int53(double v) { return std::isfinite(v) && v == std::floor(v) && std::fabs(v) < 9007199254740992.0; }
-
-template <typename X>
-static std::vector<X> fetch(const X* p, size_t count, int mem_space) {
-    std::vector<X> v(count);
-    if (count == 0) return v;
-    if (mem_space == 1) CK(cudaMemcpy(v.data(), p, count * sizeof(X), cudaMemcpyDeviceToHost));
-    else memcpy(v.data(), p, count * sizeof(X));
-    return v;
-}
-
-// CSR transpose by counting sort (column order stable -> ascending row within each column)
-static void transpose(long long rows, long long cols, const std::vector<int64_t>& ptr, const std::vector<int32_t>& idx,
-                      const std::vector<double>& val, std::vector<int64_t>& tptr, std::vector<int32_t>& tidx,
-                      std::vector<double>& tval) {
-    const long long nnz = ptr[rows];
-    tptr.assign(cols + 1, 0);
-    for (long long p = 0; p < nnz; ++p) tptr[idx[p] + 1]++;
-    for (long long i = 0; i < cols; ++i) tptr[i + 1] += tptr[i];
-    std::vector<int64_t> pos(tptr.begin(), tptr.end() - 1);
-    tidx.resize(nnz);
-    tval.resize(nnz);
-    for (long long r = 0; r < rows; ++r)
-        for (long long p = ptr[r]; p < ptr[r + 1]; ++p) {
-            const long long q = pos[idx[p]]++;
-            tidx[q] = (int32_t)r;
-            tval[q] = val[p];
-        }
-}
-
-static void do_load(gfors_ctx* C, const gfors_problem* P) {
-    if (!P) input_error("problem: NULL");
-    const long long n = P->n, m = P->m;
-    if (n <= 0 || n >= 2147483647LL) input_error("problem.n: must be in [1, 2^31-1)");
-    if (m < 0 || m >= 2147483647LL) input_error("problem.m: must be in [0, 2^31-1)");
-    if (P->mem_space != 0 && P->mem_space != 1) input_error("problem.mem_space: must be 0 (host) or 1 (device)");
-    if (!P->c) input_error("problem.c: NULL");
-    if (m > 0 && (!P->k_rowptr || !P->k_col || !P->k_val || !P->r || !P->sense))
-        input_error("problem: k_rowptr, k_col, k_val, r and sense are required when m > 0");
-    if (!std::isfinite(P->c0)) input_error("problem.c0: non-finite");
-    const int ms = P->mem_space;
-    CK(cudaSetDevice(C->device));
-    std::vector<int64_t> kptr = m ? fetch(P->k_rowptr, m + 1, ms) : std::vector<int64_t>(1, 0);
-    const long long nnz = kptr[m];
-    if (nnz < 0 || nnz >= 2147483647LL) input_error("problem: nnz(K) must be < 2^31");
-    std::vector<int32_t> kcol = fetch(P->k_col, nnz, ms);
-    std::vector<double> kval = fetch(P->k_val, nnz, ms);
-    std::vector<double> r = fetch(P->r, m, ms);
-    std::vector<int8_t> sense = fetch(P->sense, m, ms);
-    std::vector<double> c = fetch(P->c, n, ms);
-    if (m) validate_csr(m, n, kptr.data(), kcol.data(), kval.data(), "K");
-    for (long long j = 0; j < m; ++j) {
-        if (!std::isfinite(r[j])) input_error("r: non-finite value at row %lld", j);
-        if (sense[j] != 1 && sense[j] != 0 && sense[j] != -1) input_error("sense: row %lld must be +1, 0 or -1", j);
-    }
-    for (long long i = 0; i < n; ++i)
-        if (!std::isfinite(c[i])) input_error("c: non-finite value at %lld", i);
-    std::vector<int64_t> qptr;
-    std::vector<int32_t> qcol;
-    std::vector<double> qval;
-    if (P->q_rowptr) {
-        qptr = fetch(P->q_rowptr, n + 1, ms);
-        const long long qn = qptr[n];
-        if (qn < 0 || qn >= 2147483647LL) input_error("problem: nnz(Q) must be < 2^31");
-        if (qn > 0 && (!P->q_col || !P->q_val)) input_error("problem: q_col and q_val required with q_rowptr");
-        qcol = fetch(P->q_col, qn, ms);
-        qval = fetch(P->q_val, qn, ms);
-        validate_csr(n, n, qptr.data(), qcol.data(), qval.data(), "Q");
-        for (long long i = 0; i < n; ++i)
-            for (long long p = qptr[i]; p < qptr[i + 1]; ++p) {
-                const int j = qcol[p];
-                auto b = qcol.begin() + qptr[j], e = qcol.begin() + qptr[j + 1];
-                auto it = std::lower_bound(b, e, (int32_t)i);
-                if (it == e || *it != i || qval[qptr[j] + (it - b)] != qval[p])
-                    input_error("Q: not symmetric at (%lld, %d)", i, j);
-            }
-    } else {
-        qptr.assign(n + 1, 0);
-    }
-
-    C->free_prep();
-    C->free_problem();
-    C->stage = 0;
-    C->n = n; C->m = m; C->nnz = nnz;
-    C->maximize = P->maximize != 0;
-    const double sgn = C->maximize ? -1.0 : 1.0;
-    // objective: maximise -> minimise by negation
-    C->c.resize(n);
-    for (long long i = 0; i < n; ++i) C->c[i] = sgn * c[i];
-    C->c0 = sgn * P->c0;
-    C->qptr = qptr; C->qcol = qcol; C->qval = qval;
-    for (auto& v : C->qval) v *= sgn;
-    C->qnnz = (long long)C->qval.size();
-    C->hasq = C->qnnz > 0;
-    // rows: LE -> GE by negation; GE rows first, then EQ (stable)
-    C->kptr.assign(m + 1, 0); C->kcol.resize(nnz); C->kval.resize(nnz); C->ru.resize(m); C->perm.resize(m);
-    long long cj = 0, q = 0;
-    for (int pass = 0; pass < 2; ++pass) {
-        for (long long j = 0; j < m; ++j) {
-            if ((sense[j] == 0) != (pass == 1)) continue;
-            const double s = sense[j] == -1 ? -1.0 : 1.0;
-            C->perm[cj] = j;
-            C->ru[cj] = s * r[j];
-            for (long long p = kptr[j]; p < kptr[j + 1]; ++p, ++q) { C->kcol[q] = kcol[p]; C->kval[q] = s * kval[p]; }
-            C->kptr[cj + 1] = q;
-            ++cj;
-        }
-        if (pass == 0) C->m1 = cj;
-    }
-    C->m2 = m - C->m1;
-    // integrality (reading R12; bound of A23)
-    bool integ = is_int53(C->c0);
-    double bound = std::fabs(C->c0);
-    for (double v : C->c) { integ = integ && is_int53(v); bound += std::fabs(v); }
-    for (double v : C->qval) { integ = integ && is_int53(v); bound += std::fabs(v); }
-    for (double v : C->kval) integ = integ && is_int53(v);
-    for (double v : C->ru) integ = integ && is_int53(v);
-    if (bound >= 9007199254740992.0) integ = false;
-    C->integral = integ;
-    // value storage class of K
-    C->rsign.assign(m, 1);
-    bool sign_rows = true, i8 = true;
-    for (long long j = 0; j < m && sign_rows; ++j) {
-        if (C->kptr[j + 1] > C->kptr[j]) {
-            const double v0 = C->kval[C->kptr[j]];
-            if (v0 != 1.0 && v0 != -1.0) { sign_rows = false; break; }
-            C->rsign[j] = (signed char)(v0 > 0 ? 1 : -1);
-            for (long long p = C->kptr[j]; p < C->kptr[j + 1]; ++p)
-                if (C->kval[p] != v0) { sign_rows = false; break; }
-        }
-    }
-    for (double v : C->kval) i8 = i8 && (v == std::floor(v)) && std::fabs(v) <= 127.0;
-    C->kkind = sign_rows ? KV_SIGN : (i8 ? KV_I8 : KV_F64);
-    transpose(m, n, C->kptr, C->kcol, C->kval, C->ktptr, C->ktrow, C->ktval);
-
-    // ---- device upload ----
-    cudaStream_t s = C->stream;
-    auto own = [&](void* p) { C->owned.push_back(p); return p; };
-    C->d_kptr = (long long*)own(dupload(std::vector<long long>(C->kptr.begin(), C->kptr.end()), s));
-    C->d_kcol = (int*)own(dupload(std::vector<int>(C->kcol.begin(), C->kcol.end()), s));
-    C->d_ktptr = (long long*)own(dupload(std::vector<long long>(C->ktptr.begin(), C->ktptr.end()), s));
-    C->d_ktrow = (int*)own(dupload(std::vector<int>(C->ktrow.begin(), C->ktrow.end()), s));
-    if (C->kkind == KV_I8) {
-        std::vector<signed char> a(nnz), b(nnz);
-        for (long long p = 0; p < nnz; ++p) { a[p] = (signed char)C->kval[p]; b[p] = (signed char)C->ktval[p]; }
-        C->d_kval = own(dupload(a, s));
-        C->d_ktval = own(dupload(b, s));
-    } else if (C->kkind == KV_F64) {
-        C->d_kval = own(dupload(C->kval, s));
-        C->d_ktval = own(dupload(C->ktval, s));
-    }
-    C->d_rsign = (signed char*)own(dupload(C->rsign, s));
-    C->d_qptr = (long long*)own(dupload(std::vector<long long>(C->qptr.begin(), C->qptr.end()), s));
-    C->d_qcol = (int*)own(dupload(std::vector<int>(C->qcol.begin(), C->qcol.end()), s));
-    C->d_qval = (double*)own(dupload(C->qval, s));
-    C->d_c = (double*)own(dupload(C->c, s));
-    C->d_ru = (double*)own(dupload(C->ru, s));
-    C->pd = plan_direction(C->kptr, m, s, C->owned);
-    C->pp = plan_direction(C->ktptr, n, s, C->owned);
-
-    // ---- evaluator row classes ----
-    std::vector<int> crow[3], ct[3];
-    std::vector<signed char> crel[3], cB[3];
-    std::vector<int> irow, rrow;
-    std::vector<long long> irhs, iseg_start;
-    std::vector<int> iseg_slot;
-    std::vector<signed char> ieq;
-    long long cnt_nnz[3] = {0, 0, 0};
-    C->never_feasible = false;
-    for (long long j = 0; j < m; ++j) {
-        const long long L = C->kptr[j + 1] - C->kptr[j];
-        const bool is_eq = j >= C->m1;
-        if (!C->integral) { rrow.push_back((int)j); continue; }
-        const long long R = (long long)C->ru[j];
-        bool as_count = sign_rows;
-        if (!as_count && L > 0) {  // per-row single-sign pattern even if the matrix is mixed
-            const double v0 = C->kval[C->kptr[j]];
-            as_count = (v0 == 1.0 || v0 == -1.0);
-            for (long long p = C->kptr[j]; p < C->kptr[j + 1] && as_count; ++p) as_count = C->kval[p] == v0;
-        }
-        if (L == 0) {
-            const bool ok = is_eq ? (R == 0) : (R <= 0);
-            if (!ok) C->never_feasible = true;
-            continue;
-        }
-        if (as_count) {
-            const long long s0 = C->kval[C->kptr[j]] > 0 ? 1 : -1;
-            long long t;
-            int rel;
-            // s*c >= R  or  s*c == R  with c = #ones in [0, L]
-            if (!is_eq) {
-                if (s0 > 0) {
-                    if (R <= 0) continue;
-                    if (R > L) { C->never_feasible = true; continue; }
-                    t = R; rel = 0;
-                } else {
-                    const long long U = -R;
-                    if (U < 0) { C->never_feasible = true; continue; }
-                    if (U >= L) continue;
-                    t = U; rel = 1;
-                }
-            } else {
-                const long long V = s0 > 0 ? R : -R;
-                if (V < 0 || V > L) { C->never_feasible = true; continue; }
-                t = V; rel = 2;
-            }
-            const long long cap = rel == 0 ? t : t + 1;
-            int B = 0;
-            while ((1LL << B) - 1 < cap) ++B;
-            if (B <= 8) {
-                const int li = B <= 1 ? 0 : (B <= 2 ? 1 : 2);
-                crow[li].push_back((int)j); ct[li].push_back((int)t); crel[li].push_back((signed char)rel);
-                cB[li].push_back((signed char)B);
-                cnt_nnz[li] += L;
-                continue;
-            }
-        }
-        // general integer row
-        const long long slot = (long long)irow.size();
-        irow.push_back((int)j); irhs.push_back(R); ieq.push_back(is_eq ? 1 : 0);
-        for (long long p = C->kptr[j]; p < C->kptr[j + 1]; p += 256) { iseg_start.push_back(p); iseg_slot.push_back((int)slot); }
-    }
-    for (int li = 0; li < 3; ++li) {
-        auto& cl = C->cnt[li];
-        cl.nrows = (long long)crow[li].size();
-        if (cl.nrows) {
-            cl.row = (int*)own(dupload(crow[li], s));
-            cl.t = (int*)own(dupload(ct[li], s));
-            cl.rel = (signed char*)own(dupload(crel[li], s));
-            cl.B = (signed char*)own(dupload(cB[li], s));
-            cl.sub = pick_sub((double)cnt_nnz[li] / (double)cl.nrows / 6.0);  // ~6 gathers per lane
-        }
-    }
-    C->n_int = (long long)irow.size();
-    C->n_int_seg = (long long)iseg_slot.size();
-    if (C->n_int) {
-        // segment ends: segments are contiguous inside a row but rows need not be adjacent
-        std::vector<long long> starts;  // pairs packed as start array with explicit end per segment
-        C->d_int_row = (int*)own(dupload(irow, s));
-        C->d_int_rhs = (long long*)own(dupload(irhs, s));
-        C->d_int_eq = (signed char*)own(dupload(ieq, s));
-        // store [start, end) per segment as start/end arrays laid out as seg_start[2*k], [2*k+1]
-        std::vector<long long> se(2 * C->n_int_seg);
-        for (long long k = 0; k < C->n_int_seg; ++k) {
-            const int row = irow[iseg_slot[k]];
-            se[2 * k] = iseg_start[k];
-            se[2 * k + 1] = std::min<long long>(iseg_start[k] + 256, C->kptr[row + 1]);
-        }
-        C->d_int_seg_start = (long long*)own(dupload(se, s));
-        C->d_int_seg_slot = (int*)own(dupload(iseg_slot, s));
-    }
-    // coefficient bit planes for the objective kernel (integral c with max - min < 2^20)
-    C->obj_bits = false;
-    if (C->integral) {
-        double cmin = C->c[0], cmax = C->c[0];
-        for (double v : C->c) { cmin = std::min(cmin, v); cmax = std::max(cmax, v); }
-        const long long range = (long long)(cmax - cmin);
-        if (range < (1LL << 20)) {
-            int nb = 0;
-            while ((1LL << nb) <= range) ++nb;
-            if (nb == 0) nb = 1;
-            const long long nch = (n + 31) / 32;
-            std::vector<unsigned> planes(nch * nb, 0u);
-            for (long long i = 0; i < n; ++i) {
-                const long long cp = (long long)(C->c[i] - cmin);
-                for (int b = 0; b < nb; ++b)
-                    if ((cp >> b) & 1) planes[(i / 32) * nb + b] |= 1u << (i % 32);
-            }
-            C->d_planes = (unsigned*)own(dupload(planes, s));
-            C->obj_nb = nb;
-            C->obj_cmin = (long long)cmin;
-            C->obj_bits = getenv("GFORS_OBJ_SIMPLE") == nullptr;
-        }
-    }
-    C->n_real = (long long)rrow.size();
-    if (C->n_real) C->d_real_row = (int*)own(dupload(rrow, s));
-    CK(cudaStreamSynchronize(s));
-    C->stage = 1;
-}
+#include "load_impl.inc"
 
 // =============================================================================================
 // Typed dispatch helpers
