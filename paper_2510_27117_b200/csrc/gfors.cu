@@ -29,6 +29,7 @@
 #include "sample_eval.cuh"
 #include "rowblock.cuh"
 #include "trig.cuh"
+#include "sparse_primal.cuh"
 #include <cstdlib>
 
 using namespace gfors;
@@ -293,8 +294,13 @@ struct gfors_ctx {
     double *d_qval = nullptr, *d_c = nullptr, *d_ru = nullptr;
     signed char* d_rsign = nullptr;
     DirPlan pd, pp;  // dual (rows of K), primal (rows of K')
+    bool sparse_primal = false;     // primal skips gathers of zero duals (sparse_primal.cuh)
+    long long* sp_blk_row = nullptr;
+    long long sp_nblk = 0;
+    unsigned* d_nzbits = nullptr;
     double* d_segpart = nullptr;
     double* d_segpart2 = nullptr;
+    double* d_u = nullptr;  // K_u xbar of the block's last iteration (trigger pass, rb path)
     long long segpart_len = 0;
     // evaluator plan
     struct CountList {
@@ -389,6 +395,9 @@ void gfors_ctx::free_problem() {
     d_int_row = nullptr; d_int_rhs = nullptr; d_int_eq = nullptr; d_int_seg_start = nullptr; d_int_seg_slot = nullptr;
     d_real_row = nullptr;
     d_planes = nullptr;
+    sp_blk_row = nullptr;
+    d_nzbits = nullptr;
+    sparse_primal = false;
     obj_bits = false;
     pd = DirPlan{}; pp = DirPlan{};
 }
@@ -396,7 +405,7 @@ void gfors_ctx::free_problem() {
 void gfors_ctx::free_prep() {
     void** ps[] = {(void**)&d_s, &d_g, &d_rh, &d_cs, &d_qs, &d_x[0], &d_x[1], &d_xb[0], &d_xb[1], &d_y[0], &d_y[1],
                    &d_w, (void**)&d_tmp[0], (void**)&d_tmp[1], (void**)&d_tmp[2], (void**)&d_tmp[3],
-                   (void**)&d_red, (void**)&d_scalar, (void**)&d_segpart, (void**)&d_segpart2, (void**)&d_part1,
+                   (void**)&d_red, (void**)&d_scalar, (void**)&d_segpart, (void**)&d_segpart2, (void**)&d_u, (void**)&d_part1,
                    (void**)&d_part2, (void**)&d_hist, (void**)&d_rho, (void**)&d_trace, (void**)&d_xbest,
                    (void**)&d_X, (void**)&d_viol, (void**)&d_iacc, &d_zpart, (void**)&d_z, (void**)&d_ctrl};
     for (void** p : ps) { dfree(*p); *p = nullptr; }
@@ -496,7 +505,8 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
             const int grid = (int)std::min<long long>(C->pd.nblk, RB_GRID);
             KIND_SWITCH(C->kkind, LAUNCH(C, s, KC_DUAL,
                 (k_dual_rb<T, KINDV><<<grid, RB_NT, 0, s>>>(csr_K(C), C->pd.blk_row, C->pd.nblk, st, g, rh, C->d_rsign,
-                                                            C->m1, ctrl, kint, j))));
+                                                            C->m1, ctrl, kint, j,
+                                                            (kint == 0 || j == kint - 1) ? C->d_u : nullptr))));
         } else if (!C->pd.seg) {
             const int grid = grid_for(C->m * (long long)C->pd.sub);
             KIND_SWITCH(C->kkind, SUB_SWITCH(C->pd.sub, LAUNCH(C, s, KC_DUAL,
@@ -516,7 +526,27 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
     const T* cs = (const T*)C->d_cs;
     // K' values: SIGN rows fold the sign into w, so the transpose carries no values
     const int tkind = C->kkind;
-    if (C->pp.wrb) {
+    if (C->sparse_primal && sparse_primal_smem<T>(C->m) <= 227 * 1024) {
+        const long long nwords = (C->m + 31) / 32;
+        LAUNCH(C, s, KC_PRIMAL, (k_nzmask<T><<<grid_for(nwords * 32), NT, 0, s>>>(st.w, C->m, C->d_nzbits)));
+        const size_t sm = sparse_primal_smem<T>(C->m);
+        const int grid = (int)std::min<long long>(C->sp_nblk, NUM_SMS_B200);
+        if (C->hasq) {
+            KIND_SWITCH(tkind, {
+                static bool attr = false;
+                if (!attr) { CK(cudaFuncSetAttribute(k_primal_sparse<T, KINDV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)); attr = true; }
+                LAUNCH(C, s, KC_PRIMAL, (k_primal_sparse<T, KINDV, true><<<grid, SP_NT, sm, s>>>(csr_Kt(C), C->sp_blk_row, C->sp_nblk,
+                    C->d_nzbits, nwords, Q, qs, st, cs, ctrl, kint, j)));
+            });
+        } else {
+            KIND_SWITCH(tkind, {
+                static bool attr = false;
+                if (!attr) { CK(cudaFuncSetAttribute(k_primal_sparse<T, KINDV, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)); attr = true; }
+                LAUNCH(C, s, KC_PRIMAL, (k_primal_sparse<T, KINDV, false><<<grid, SP_NT, sm, s>>>(csr_Kt(C), C->sp_blk_row, C->sp_nblk,
+                    C->d_nzbits, nwords, Q, qs, st, cs, ctrl, kint, j)));
+            });
+        }
+    } else if (C->pp.wrb) {
         const int grid = (int)std::min<long long>((C->pp.nblk + WRB_WARPS - 1) / WRB_WARPS, RB_GRID);
         if (C->hasq) {
             KIND_SWITCH(tkind, LAUNCH(C, s, KC_PRIMAL,
@@ -585,11 +615,11 @@ void enqueue_trigger(gfors_ctx* C, cudaStream_t s, long long kint, long long j) 
             });
             if (grid < C->nb1)
                 LAUNCH(C, s, KC_TRIGR, (k_fill<<<1, NT, 0, s>>>(C->d_part1 + 3LL * grid, 3LL * (C->nb1 - grid), 0.0)));
-        } else if (C->pd.rb || C->pd.wrb) {
+        } else if (C->pd.rb) {
             const int grid = (int)std::min<long long>(C->pd.nblk, (long long)C->nb1);
             KIND_SWITCH(C->kkind, LAUNCH(C, s, KC_TRIGR,
                 (k_trig_rows_rb<T, KINDV><<<grid, RB_NT, 0, s>>>(csr_K(C), C->pd.blk_row, C->pd.nblk, st, g, rh,
-                                                                 C->d_rsign, C->m1, ctrl, kint, j, C->d_part1))));
+                                                                 C->d_rsign, C->m1, C->d_u, ctrl, kint, j, C->d_part1))));
             if (grid < C->nb1)
                 LAUNCH(C, s, KC_TRIGR, (k_fill<<<1, NT, 0, s>>>(C->d_part1 + 3LL * grid, 3LL * (C->nb1 - grid), 0.0)));
         } else if (!C->pd.seg) {
@@ -887,6 +917,7 @@ static void do_preprocess(gfors_ctx* C, const gfors_prep_opts* o, gfors_scaling*
     C->segpart_len = std::max<long long>(std::max(C->pd.ds.nseg, C->pp.ds.nseg), 1);
     C->d_segpart = dalloc<double>(C->segpart_len);
     C->d_segpart2 = dalloc<double>(C->segpart_len);
+    C->d_u = dalloc<double>(std::max<long long>(m, 1));
     C->d_ctrl = dalloc<Ctrl>(1);
     C->d_hist = dalloc<double>(3 * 1024);
     C->d_xbest = dalloc<unsigned char>(n);
@@ -1334,8 +1365,9 @@ int64_t gfors_launches_per_block(gfors_ctx* C, const gfors_params* p) {
     // a dry count: mirror enqueue_block's structure
     long long per_iter = 0;
     per_iter += C->m > 0 ? (C->pd.seg ? 2 : 1) : 0;
-    per_iter += C->pp.seg ? 2 : 1;
-    long long trig = (C->m > 0 ? (C->pd.seg ? 3 : ((C->pd.rb || C->pd.wrb) ? 1 + (C->pd.nblk < C->nb1 ? 1 : 0) : 1)) : 1) + 1;
+    const bool spp = C->sparse_primal && (C->precision == 64 ? sparse_primal_smem<double>(C->m) : sparse_primal_smem<float>(C->m)) <= 227 * 1024;
+    per_iter += spp ? 2 : (C->pp.seg ? 2 : 1);
+    long long trig = (C->m > 0 ? (C->pd.seg ? 3 : (C->pd.rb ? 1 + (C->pd.nblk < C->nb1 ? 1 : 0) : 1)) : 1) + 1;
     long long eval = 0;
     for (auto& cl : C->cnt) eval += cl.nrows ? 1 : 0;
     eval += C->n_int ? 2 : 0;

@@ -34,23 +34,29 @@ __device__ __forceinline__ void cp_async_elem(T* smem, const T* g) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;"); }
 
-// phase 1 of row block b: sv[t] = v[idx_t] for its nonzeros (values applied in phase 2)
-template <typename T>
-__device__ __forceinline__ void rb_issue(const Csr& A, const long long* __restrict__ blk_row, long long b,
-                                         long long nblk, const T* __restrict__ v, T* sv) {
+// phase 1 of row block b, split in two so the index loads of block b+2*grid are in flight while
+// block b is reduced: rb_load_idx (registers, evict-first) then rb_issue (cp.async gathers)
+__device__ __forceinline__ void rb_load_idx(const Csr& A, const long long* __restrict__ blk_row, long long b,
+                                            long long nblk, int (&cols)[RB_U]) {
     if (b < nblk) {
         const long long p0 = __ldg(A.ptr + blk_row[b]);
         const int cnt = (int)(__ldg(A.ptr + blk_row[b + 1]) - p0);
-        int cols[RB_U];
 #pragma unroll
         for (int u = 0; u < RB_U; ++u) {
             const int t = u * RB_NT + threadIdx.x;
             cols[u] = t < cnt ? ldcs_i32(A.idx + p0 + t) : -1;
         }
+    } else {
 #pragma unroll
-        for (int u = 0; u < RB_U; ++u)
-            if (cols[u] >= 0) cp_async_elem(sv + u * RB_NT + threadIdx.x, v + cols[u]);
+        for (int u = 0; u < RB_U; ++u) cols[u] = -1;
     }
+}
+
+template <typename T>
+__device__ __forceinline__ void rb_issue(const int (&cols)[RB_U], const T* __restrict__ v, T* sv) {
+#pragma unroll
+    for (int u = 0; u < RB_U; ++u)
+        if (cols[u] >= 0) cp_async_elem(sv + u * RB_NT + threadIdx.x, v + cols[u]);
     cp_async_commit();
 }
 
@@ -65,17 +71,39 @@ __device__ __forceinline__ double rb_group_sum(double v, int G) {
     return v;
 }
 
-// sum of val_q * sv[q - p0] over the row's nonzeros [q0, q1) by the G lanes of a group
-template <typename T, int KIND>
+// sum of val_q * sv[q - p0] over the row's nonzeros [q0, q1) by the G lanes of a group.
+// ILP4: four independent accumulators combined as ((a0 + a1) + (a2 + a3)) (fixed order) so the
+// shared-memory loads of a long per-thread row overlap; costs registers, used where G is small.
+template <typename T, int KIND, bool ILP4 = false>
 __device__ __forceinline__ double rb_row_sum(const Csr& A, const T* sv, long long p0, long long q0, long long q1,
                                              int lane, int G) {
-    double acc = 0.0;
-    for (long long q = q0 + lane; q < q1; q += G) {
-        const double a = (double)sv[q - p0];
-        if constexpr (KIND == KV_SIGN) acc += a;
-        else acc += kval<KIND>(A.val, q) * a;
+    const int i1 = (int)(q1 - p0);
+    int i = (int)(q0 - p0) + lane;
+    if constexpr (!ILP4) {
+        double acc = 0.0;
+        for (; i < i1; i += G) {
+            if constexpr (KIND == KV_SIGN) acc += (double)sv[i];
+            else acc += kval<KIND>(A.val, p0 + i) * (double)sv[i];
+        }
+        return acc;
+    } else {
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        if constexpr (KIND == KV_SIGN) {
+            for (; i + 3 * G < i1; i += 4 * G) {
+                a0 += (double)sv[i]; a1 += (double)sv[i + G]; a2 += (double)sv[i + 2 * G]; a3 += (double)sv[i + 3 * G];
+            }
+            for (; i < i1; i += G) a0 += (double)sv[i];
+        } else {
+            for (; i + 3 * G < i1; i += 4 * G) {
+                a0 += kval<KIND>(A.val, p0 + i) * (double)sv[i];
+                a1 += kval<KIND>(A.val, p0 + i + G) * (double)sv[i + G];
+                a2 += kval<KIND>(A.val, p0 + i + 2 * G) * (double)sv[i + 2 * G];
+                a3 += kval<KIND>(A.val, p0 + i + 3 * G) * (double)sv[i + 3 * G];
+            }
+            for (; i < i1; i += G) a0 += kval<KIND>(A.val, p0 + i) * (double)sv[i];
+        }
+        return (a0 + a1) + (a2 + a3);
     }
-    return acc;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -87,7 +115,7 @@ __global__ void __launch_bounds__(RB_NT) k_dual_rb(Csr K, const long long* __res
                                                    State<T> s, const double* __restrict__ g,
                                                    const double* __restrict__ rh, const signed char* __restrict__ rsign,
                                                    long long m1, const Ctrl* __restrict__ ctrl, long long kint,
-                                                   long long j) {
+                                                   long long j, double* __restrict__ u_out) {
     __shared__ __align__(16) T sv[2][RB_NNZ];
     const long long kk = iter_index(ctrl, kint, j);
     const int par = (int)(kk & 1);
@@ -96,9 +124,13 @@ __global__ void __launch_bounds__(RB_NT) k_dual_rb(Csr K, const long long* __res
     T* __restrict__ yout = par ? s.y[0] : s.y[1];
     const double tau2 = ctrl->tau2;
     int st = 0;
-    rb_issue<T>(K, blk_row, blockIdx.x, nblk, xb, sv[0]);
+    int nxt[RB_U];
+    rb_load_idx(K, blk_row, blockIdx.x, nblk, nxt);
+    rb_issue<T>(nxt, xb, sv[0]);
+    rb_load_idx(K, blk_row, blockIdx.x + gridDim.x, nblk, nxt);
     for (long long b = blockIdx.x; b < nblk; b += gridDim.x) {
-        rb_issue<T>(K, blk_row, b + gridDim.x, nblk, xb, sv[st ^ 1]);
+        rb_issue<T>(nxt, xb, sv[st ^ 1]);
+        rb_load_idx(K, blk_row, b + 2LL * gridDim.x, nblk, nxt);
         cp_async_wait1();
         __syncthreads();
         const long long r0 = blk_row[b], r1 = blk_row[b + 1];
@@ -119,6 +151,7 @@ __global__ void __launch_bounds__(RB_NT) k_dual_rb(Csr K, const long long* __res
                 if (row < m1 && yn < 0.0) yn = 0.0;
                 yout[row] = (T)yn;
                 s.w[row] = (T)(gj * sg * yn);
+                if (u_out) u_out[row] = sg * acc;  // (K_u xbar_{k-1})_j, kept for the trigger pass
             }
         }
         __syncthreads();
@@ -133,7 +166,7 @@ __global__ void __launch_bounds__(RB_NT) k_dual_rb(Csr K, const long long* __res
 //   xbar_k = 2 x_k - x_{k-1}
 // ---------------------------------------------------------------------------------------------
 template <typename T, int KIND, bool HASQ>
-__global__ void __launch_bounds__(RB_NT) k_primal_rb(Csr Kt, const long long* __restrict__ blk_row, long long nblk,
+__global__ void __launch_bounds__(RB_NT, 6) k_primal_rb(Csr Kt, const long long* __restrict__ blk_row, long long nblk,
                                                      Csr Q, const T* __restrict__ qs, State<T> s,
                                                      const T* __restrict__ cs, const Ctrl* __restrict__ ctrl,
                                                      long long kint, long long j) {
@@ -145,9 +178,13 @@ __global__ void __launch_bounds__(RB_NT) k_primal_rb(Csr Kt, const long long* __
     T* __restrict__ xbout = par ? s.xb[0] : s.xb[1];
     const double rho = ctrl->rho, tau1 = ctrl->tau1;
     int st = 0;
-    rb_issue<T>(Kt, blk_row, blockIdx.x, nblk, s.w, sv[0]);
+    int nxt[RB_U];
+    rb_load_idx(Kt, blk_row, blockIdx.x, nblk, nxt);
+    rb_issue<T>(nxt, s.w, sv[0]);
+    rb_load_idx(Kt, blk_row, blockIdx.x + gridDim.x, nblk, nxt);
     for (long long b = blockIdx.x; b < nblk; b += gridDim.x) {
-        rb_issue<T>(Kt, blk_row, b + gridDim.x, nblk, s.w, sv[st ^ 1]);
+        rb_issue<T>(nxt, s.w, sv[st ^ 1]);
+        rb_load_idx(Kt, blk_row, b + 2LL * gridDim.x, nblk, nxt);
         cp_async_wait1();
         __syncthreads();
         const long long r0 = blk_row[b], r1 = blk_row[b + 1];
@@ -158,9 +195,10 @@ __global__ void __launch_bounds__(RB_NT) k_primal_rb(Csr Kt, const long long* __
         for (int rb = 0; rb < nr; rb += ngr) {
             const int rr = rb + grp;
             const long long i = r0 + rr;
-            double a = 0.0, bq = 0.0;
+            double a = 0.0, bq = 0.0, xi = 0.0, ci = 0.0;
             if (rr < nr) {
-                a = rb_row_sum<T, KIND>(Kt, sv[st], p0, __ldg(Kt.ptr + i), __ldg(Kt.ptr + i + 1), lane, G);
+                if (lane == 0) { xi = (double)xin[i]; ci = (double)cs[i]; }  // issued before the reduction
+                a = rb_row_sum<T, KIND, true>(Kt, sv[st], p0, __ldg(Kt.ptr + i), __ldg(Kt.ptr + i + 1), lane, G);
                 if constexpr (HASQ)
                     for (long long q = __ldg(Q.ptr + i) + lane; q < __ldg(Q.ptr + i + 1); q += G)
                         bq += (double)__ldg(qs + q) * (double)__ldg(xin + __ldg(Q.idx + q));
@@ -168,8 +206,7 @@ __global__ void __launch_bounds__(RB_NT) k_primal_rb(Csr Kt, const long long* __
             a = rb_group_sum(a, G);
             if constexpr (HASQ) bq = rb_group_sum(bq, G);
             if (lane == 0 && rr < nr) {
-                const double xi = (double)xin[i];
-                const double delta = (((double)cs[i] + rho) - a) + 2.0 * bq - 2.0 * rho * xi;
+                const double delta = ((ci + rho) - a) + 2.0 * bq - 2.0 * rho * xi;
                 double xn = xi - tau1 * delta;
                 xn = xn < 0.0 ? 0.0 : (xn > 1.0 ? 1.0 : xn);
                 xout[i] = (T)xn;
@@ -183,71 +220,60 @@ __global__ void __launch_bounds__(RB_NT) k_primal_rb(Csr Kt, const long long* __
 }
 
 // ---------------------------------------------------------------------------------------------
-// Trigger row pass on row blocks: v = K_u x_k, d = K_u (x_k - xbar_{k-1}).
-// Once per k_int iterations; register gathers (two vectors per nonzero).
+// Trigger row pass on row blocks: v = K_u x_k (one gather per nonzero), and
+// d = K_u (x_k - xbar_{k-1}) = v - u with u = K_u xbar_{k-1} stored by the last dual of the block.
 // ---------------------------------------------------------------------------------------------
 template <typename T, int KIND>
 __global__ void __launch_bounds__(RB_NT) k_trig_rows_rb(Csr K, const long long* __restrict__ blk_row, long long nblk,
                                                         State<T> s, const double* __restrict__ g,
                                                         const double* __restrict__ rh,
                                                         const signed char* __restrict__ rsign, long long m1,
-                                                        const Ctrl* __restrict__ ctrl, long long kint, long long j,
-                                                        double* __restrict__ part1) {
-    __shared__ double sv[RB_NNZ];
-    __shared__ double sd[RB_NNZ];
+                                                        const double* __restrict__ u_prev, const Ctrl* __restrict__ ctrl,
+                                                        long long kint, long long j, double* __restrict__ part1) {
+    __shared__ __align__(16) T sv[2][RB_NNZ];
     __shared__ double sh[32];
     const long long kk = iter_index(ctrl, kint, j);
     const int par = (int)(kk & 1);
     const T* __restrict__ xk = par ? s.x[0] : s.x[1];
-    const T* __restrict__ xbp = par ? s.xb[1] : s.xb[0];
     const T* __restrict__ yprev = par ? s.y[1] : s.y[0];
     const T* __restrict__ ynew = par ? s.y[0] : s.y[1];
     const double tau2 = ctrl->tau2;
     double ge = 0.0, eq = 0.0, sy2 = 0.0;
+    int st = 0;
+    int nxt[RB_U];
+    rb_load_idx(K, blk_row, blockIdx.x, nblk, nxt);
+    rb_issue<T>(nxt, xk, sv[0]);
+    rb_load_idx(K, blk_row, blockIdx.x + gridDim.x, nblk, nxt);
     for (long long b = blockIdx.x; b < nblk; b += gridDim.x) {
+        rb_issue<T>(nxt, xk, sv[st ^ 1]);
+        rb_load_idx(K, blk_row, b + 2LL * gridDim.x, nblk, nxt);
+        cp_async_wait1();
+        __syncthreads();
         const long long r0 = blk_row[b], r1 = blk_row[b + 1];
         const long long p0 = __ldg(K.ptr + r0);
-        const int cnt = (int)(__ldg(K.ptr + r1) - p0);
-        int cols[RB_U];
-#pragma unroll
-        for (int u = 0; u < RB_U; ++u) {
-            const int t = u * RB_NT + threadIdx.x;
-            cols[u] = t < cnt ? ldcs_i32(K.idx + p0 + t) : 0;
-        }
-#pragma unroll
-        for (int u = 0; u < RB_U; ++u) {
-            const int t = u * RB_NT + threadIdx.x;
-            if (t < cnt) {
-                const double a = (double)__ldg(xk + cols[u]);
-                sv[t] = a;
-                sd[t] = a - (double)__ldg(xbp + cols[u]);
-            }
-        }
-        __syncthreads();
         const int nr = (int)(r1 - r0);
         const int G = rb_group_size(nr);
         const int lane = threadIdx.x & (G - 1), grp = threadIdx.x / G, ngr = RB_NT / G;
         for (int rb = 0; rb < nr; rb += ngr) {
             const int rr = rb + grp;
             const long long row = r0 + rr;
-            double v = 0.0, d = 0.0;
-            if (rr < nr) {
-                v = rb_row_sum<double, KIND>(K, sv, p0, __ldg(K.ptr + row), __ldg(K.ptr + row + 1), lane, G);
-                d = rb_row_sum<double, KIND>(K, sd, p0, __ldg(K.ptr + row), __ldg(K.ptr + row + 1), lane, G);
-            }
+            double v = 0.0;
+            if (rr < nr) v = rb_row_sum<T, KIND>(K, sv[st], p0, __ldg(K.ptr + row), __ldg(K.ptr + row + 1), lane, G);
             v = rb_group_sum(v, G);
-            d = rb_group_sum(d, G);
             if (lane == 0 && rr < nr) {
                 const double sg = (KIND == KV_SIGN) ? (double)rsign[row] : 1.0;
                 const double gj = g[row];
-                const double gap = rh[row] - gj * (sg * v);
+                const double ku = sg * v;  // (K_u x_k)_j
+                const double gap = rh[row] - gj * ku;
                 if (row < m1) ge = fmax(ge, fmax(gap, 0.0)); else eq = fmax(eq, fabs(gap));
-                const double sy = ((double)yprev[row] - (double)ynew[row]) / tau2 + gj * (sg * d);
+                const double sy = ((double)yprev[row] - (double)ynew[row]) / tau2 + gj * (ku - u_prev[row]);
                 sy2 += sy * sy;
             }
         }
         __syncthreads();
+        st ^= 1;
     }
+    asm volatile("cp.async.wait_all;");
     const double a = block_max<RB_NT>(ge, sh);
     const double bb = block_max<RB_NT>(eq, sh);
     const double c = block_sum<RB_NT>(sy2, sh);

@@ -317,3 +317,30 @@ def test_errors_fail_loudly(gf):
         s.run(k_b=100)
     with pytest.raises(gf.GforsError, match="sigma"):
         s.run(sigma=1.5)
+
+
+@pytest.mark.parametrize("fam", ["setcover", "general", "bqp"])
+def test_sparse_primal_variant_parity(gf, fam, monkeypatch):
+    """The zero-dual-skipping primal (forced on small instances) against the oracle: 1000 fp64
+    iterations within 1e-5, and a full run with identical incumbent sequence."""
+    monkeypatch.setenv("GFORS_SPARSE_PRIMAL", "1")
+    inst = G.SMALL[fam](11)
+    s, _, o, _ = _pair(gf, inst, 64)
+    tau = math.sqrt(0.99)
+    rho = O.rho_schedule(1e-3, 10.0, 100.0, 2.0, 1e-6, 100)
+    o.state_init()
+    x0, xb0, y0 = o.get_state()
+    s.set_state(x0, xb0, y0)
+    for b in range(100):
+        s.step(10, rho[b], tau, tau)
+        for _ in range(10):
+            o.step(rho[b], tau, tau)
+    xg, _, yg = s.get_state()
+    xo, _, yo = o.get_state()
+    assert _rel(xg, xo) <= 1e-5 and _rel(yg, yo) <= 1e-5
+    ig = s.run(max_iters=400)
+    io = o.run(max_iters=400)
+    assert ig["iters"] == io["iters"] and ig["rounds"] == io["rounds"]
+    zg, xbest, mg = s.best_incumbent()
+    zo, xo2 = o.best()
+    assert zg == zo or (math.isinf(zg) and math.isinf(zo))
