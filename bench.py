@@ -33,6 +33,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "PDHG iters/s and sampled candidates evaluated/s; time-to-incumbent at 1/2/4/8 B200"
+GATHER_CEILING_G = 271.0  # random 4-byte gathers/s (x1e9) on B200, profiles/r01_gather_microbench.txt
 UNIT = "candidates/s"
 
 
@@ -369,7 +370,11 @@ def run_gpu(args):
                        "seed": args.seed, "obj_scale": sc["obj_scale"], "k_scale": sc["k_scale"]},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "algorithmic_bytes_per_launch": byt[dom], "avg_launch_ms": per_launch_ms},
+                         "algorithmic_bytes_per_launch": byt[dom], "avg_launch_ms": per_launch_ms,
+                         # the binding limit of a random sparse product on B200: one L1TEX wavefront per
+                         # gathered element; ceiling measured by scratch/gather_bench.cu (profiles/)
+                         "gather": {"gathers_per_launch": meta["nnz"], "achieved_G_per_s": meta["nnz"] / (per_launch_ms * 1e-3) / 1e9,
+                                    "ceiling_G_per_s": GATHER_CEILING_G, "frac": meta["nnz"] / (per_launch_ms * 1e-3) / 1e9 / GATHER_CEILING_G}},
             "kernel_ms_per_step": prof, "kernel_share": {k: v / step_ms for k, v in prof.items()} if step_ms else {},
             "clocks": clocks,
             "gpu_launches": int(launches * args.steps + 8),

@@ -134,13 +134,14 @@ struct DirPlan {  // how one product direction (K rows or K' columns) is compute
 };
 
 // greedy nonzero-balanced row blocks: consecutive rows, <= cap nonzeros each (rows <= cap long)
-static std::vector<long long> make_rowblocks(const std::vector<int64_t>& ptr, long long rows, long long cap) {
+static std::vector<long long> make_rowblocks(const std::vector<int64_t>& ptr, long long rows, long long cap,
+                                             long long cap_rows = LLONG_MAX) {
     std::vector<long long> b;
     b.push_back(0);
     long long r = 0;
     while (r < rows) {
         long long e = r;
-        while (e < rows && ptr[e + 1] - ptr[r] <= cap) ++e;
+        while (e < rows && ptr[e + 1] - ptr[r] <= cap && e - r < cap_rows) ++e;
         if (e == r) e = r + 1;  // (not reached when every row is <= cap)
         b.push_back(e);
         r = e;

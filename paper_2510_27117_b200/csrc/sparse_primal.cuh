@@ -67,6 +67,36 @@ __device__ __forceinline__ int sp_group_size(int nr) {
     return G;
 }
 
+// Row blocks hold <= SP_NT rows, so phase 2 is one pass with <= one row per G-lane group; the row
+// pointers and epilogue operands of the CTA's NEXT block are loaded into registers while the current
+// block is reduced (latency hidden behind a whole phase instead of exposed at its start).
+struct SpRow {
+    long long q0, q1;
+    double xi, ci;
+    int G;
+    bool valid;
+};
+
+template <typename T>
+__device__ __forceinline__ SpRow sp_prefetch_row(const Csr& Kt, const long long* __restrict__ blk_row, long long b,
+                                                 long long nblk, const T* __restrict__ xin, const T* __restrict__ cs) {
+    SpRow r{0, 0, 0.0, 0.0, 1, false};
+    if (b < nblk) {
+        const long long r0 = blk_row[b];
+        const int nr = (int)(blk_row[b + 1] - r0);
+        r.G = sp_group_size(nr);
+        const int grp = threadIdx.x / r.G;
+        if (grp < nr) {
+            const long long i = r0 + grp;
+            r.valid = true;
+            r.q0 = __ldg(Kt.ptr + i);
+            r.q1 = __ldg(Kt.ptr + i + 1);
+            if ((threadIdx.x & (r.G - 1)) == 0) { r.xi = (double)xin[i]; r.ci = (double)cs[i]; }
+        }
+    }
+    return r;
+}
+
 template <typename T, int KIND, bool HASQ>
 __global__ void __launch_bounds__(SP_NT, 1) k_primal_sparse(Csr Kt, const long long* __restrict__ blk_row, long long nblk,
                                                             const unsigned* __restrict__ bits, long long nwords,
@@ -89,40 +119,39 @@ __global__ void __launch_bounds__(SP_NT, 1) k_primal_sparse(Csr Kt, const long l
     sp_load_idx(Kt, blk_row, blockIdx.x, nblk, nxt);
     sp_issue<T>(nxt, s.w, sbits, svb);
     sp_load_idx(Kt, blk_row, blockIdx.x + gridDim.x, nblk, nxt);
+    SpRow cur = sp_prefetch_row<T>(Kt, blk_row, blockIdx.x, nblk, xin, cs);
     for (long long b = blockIdx.x; b < nblk; b += gridDim.x) {
         sp_issue<T>(nxt, s.w, sbits, svb + (st ^ 1) * SP_NNZ);
         sp_load_idx(Kt, blk_row, b + 2LL * gridDim.x, nblk, nxt);
+        const SpRow nrow = sp_prefetch_row<T>(Kt, blk_row, b + gridDim.x, nblk, xin, cs);
         cp_async_wait1();
         __syncthreads();
         const T* sv = svb + st * SP_NNZ;
-        const long long r0 = blk_row[b], r1 = blk_row[b + 1];
+        const long long r0 = blk_row[b];
         const long long p0 = __ldg(Kt.ptr + r0);
-        const int nr = (int)(r1 - r0);
-        const int G = sp_group_size(nr);
-        const int lane = threadIdx.x & (G - 1), grp = threadIdx.x / G, ngr = SP_NT / G;
-        for (int rb = 0; rb < nr; rb += ngr) {
-            const int rr = rb + grp;
-            const long long i = r0 + rr;
-            double a = 0.0, bq = 0.0, xi = 0.0, ci = 0.0;
-            if (rr < nr) {
-                if (lane == 0) { xi = (double)xin[i]; ci = (double)cs[i]; }  // issued before the reduction
-                a = rb_row_sum<T, KIND, true>(Kt, sv, p0, __ldg(Kt.ptr + i), __ldg(Kt.ptr + i + 1), lane, G);
-                if constexpr (HASQ)
-                    for (long long q = __ldg(Q.ptr + i) + lane; q < __ldg(Q.ptr + i + 1); q += G)
-                        bq += (double)__ldg(qs + q) * (double)__ldg(xin + __ldg(Q.idx + q));
-            }
-            a = rb_group_sum(a, G);
-            if constexpr (HASQ) bq = rb_group_sum(bq, G);
-            if (lane == 0 && rr < nr) {
-                const double delta = ((ci + rho) - a) + 2.0 * bq - 2.0 * rho * xi;
-                double xn = xi - tau1 * delta;
-                xn = xn < 0.0 ? 0.0 : (xn > 1.0 ? 1.0 : xn);
-                xout[i] = (T)xn;
-                xbout[i] = (T)(2.0 * xn - xi);
-            }
+        const int G = cur.G;
+        const int lane = threadIdx.x & (G - 1);
+        const long long i = r0 + threadIdx.x / G;
+        double a = 0.0, bq = 0.0;
+        if (cur.valid) {
+            a = rb_row_sum<T, KIND, true>(Kt, sv, p0, cur.q0, cur.q1, lane, G);
+            if constexpr (HASQ)
+                for (long long q = __ldg(Q.ptr + i) + lane; q < __ldg(Q.ptr + i + 1); q += G)
+                    bq += (double)__ldg(qs + q) * (double)__ldg(xin + __ldg(Q.idx + q));
+        }
+        a = rb_group_sum(a, G);
+        if constexpr (HASQ) bq = rb_group_sum(bq, G);
+        if (lane == 0 && cur.valid) {
+            const double xi = cur.xi;
+            const double delta = ((cur.ci + rho) - a) + 2.0 * bq - 2.0 * rho * xi;
+            double xn = xi - tau1 * delta;
+            xn = xn < 0.0 ? 0.0 : (xn > 1.0 ? 1.0 : xn);
+            xout[i] = (T)xn;
+            xbout[i] = (T)(2.0 * xn - xi);
         }
         __syncthreads();
         st ^= 1;
+        cur = nrow;
     }
     asm volatile("cp.async.wait_all;");
 }
