@@ -44,7 +44,8 @@ typedef struct gfors_ctx gfors_ctx;
 /* Device/rank options.  stream: a cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream)
  * or NULL for a library-owned stream.  rank/world: sample-sharded data parallelism
  * (DESIGN.md §7): rank r draws global sample words [r*W, (r+1)*W).  nccl_id: 128-byte
- * ncclUniqueId (identical on all ranks) when world > 1, else NULL. */
+ * ncclUniqueId (identical on all ranks, see gfors_nccl_unique_id) for the in-loop incumbent exchange,
+ * or NULL: independent shards whose incumbents the caller merges (gfors_merge_records). */
 typedef struct {
     int32_t device;
     void *stream;

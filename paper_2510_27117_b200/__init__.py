@@ -97,6 +97,8 @@ EXPORTS = {
     "gfors_kernel_class_name": (C.c_char_p, [I32]),
     "gfors_launches_per_block": (I64, [P, C.POINTER(Params)]),
     "gfors_merge_records": (I32, [P, P, P, I32]),
+    "gfors_nccl_unique_id": (I32, [P]),
+    "gfors_graph_note": (C.c_char_p, [P]),
 }
 for _name, (_res, _args) in EXPORTS.items():
     _f = getattr(_lib, _name)
@@ -134,11 +136,23 @@ def _ptr(a):
     return a.ctypes.data_as(P)
 
 
-class Solver:
-    """One gfors context on one GPU."""
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id for Solver(..., nccl_id=...) (create on one rank, broadcast)."""
+    buf = (C.c_char * 128)()
+    rc = _lib.gfors_nccl_unique_id(C.cast(buf, P))
+    if rc != 0:
+        raise GforsError(rc, "ncclGetUniqueId failed / libnccl.so.2 not loadable")
+    return bytes(buf)
 
-    def __init__(self, device: int = 0, stream=None, rank: int = 0, world: int = 1):
-        opts = DeviceOpts(device, P(stream) if stream else None, rank, world, None)
+
+class Solver:
+    """One gfors context on one GPU.  rank/world shard the samples; nccl_id (bytes from
+    nccl_unique_id(), identical on all ranks) enables the in-loop incumbent exchange."""
+
+    def __init__(self, device: int = 0, stream=None, rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
+        self._nccl_buf = (C.c_char * 128).from_buffer_copy(nccl_id) if nccl_id else None
+        opts = DeviceOpts(device, P(stream) if stream else None, rank, world,
+                          C.cast(self._nccl_buf, P) if nccl_id else None)
         h = P()
         rc = _lib.gfors_create(C.byref(h), C.byref(opts))
         if rc != 0:
@@ -274,6 +288,9 @@ class Solver:
         nc = C.c_int32()
         self._chk(_lib.gfors_profile_blocks(self.h, C.byref(p), blocks, _ptr(ms), 16, C.byref(nc)))
         return {_lib.gfors_kernel_class_name(k).decode(): float(ms[k]) for k in range(nc.value)}
+
+    def graph_note(self):
+        return _lib.gfors_graph_note(self.h).decode()
 
     def launches_per_block(self, params: Params | None = None, **kw):
         p = params or default_params(**kw)

@@ -30,6 +30,7 @@
 #include "rowblock.cuh"
 #include "trig.cuh"
 #include "sparse_primal.cuh"
+#include "shard.cuh"
 #include <cstdlib>
 
 using namespace gfors;
@@ -370,6 +371,14 @@ struct gfors_ctx {
     int gkey_W = -1;
     bool gvalid = false;
 
+    // sample sharding over NCCL (shard.cuh)
+    ncclComm_t comm = nullptr;
+    bool sharded = false;
+    double* d_rec = nullptr;       // [4] local record + [4*world] gathered records
+    long long* d_regen = nullptr;  // [2] winner global index, round
+    std::string graph_note;        // why the graph fell back to the eager loop, if it did
+    bool gno = false;              // graph capture failed for gkey: use the eager loop
+
     // profiling
     bool profiling = false;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_ev;
@@ -406,7 +415,7 @@ void gfors_ctx::free_problem() {
 void gfors_ctx::free_prep() {
     void** ps[] = {(void**)&d_s, &d_g, &d_rh, &d_cs, &d_qs, &d_x[0], &d_x[1], &d_xb[0], &d_xb[1], &d_y[0], &d_y[1],
                    &d_w, (void**)&d_tmp[0], (void**)&d_tmp[1], (void**)&d_tmp[2], (void**)&d_tmp[3],
-                   (void**)&d_red, (void**)&d_scalar, (void**)&d_segpart, (void**)&d_segpart2, (void**)&d_u, (void**)&d_part1,
+                   (void**)&d_red, (void**)&d_scalar, (void**)&d_segpart, (void**)&d_segpart2, (void**)&d_u, (void**)&d_rec, (void**)&d_regen, (void**)&d_part1,
                    (void**)&d_part2, (void**)&d_hist, (void**)&d_rho, (void**)&d_trace, (void**)&d_xbest,
                    (void**)&d_X, (void**)&d_viol, (void**)&d_iacc, &d_zpart, (void**)&d_z, (void**)&d_ctrl};
     for (void** p : ps) { dfree(*p); *p = nullptr; }
@@ -423,6 +432,7 @@ gfors_ctx::~gfors_ctx() {
     if (stream) cudaStreamSynchronize(stream);
     free_prep();
     free_problem();
+    if (comm) nccl().CommDestroy(comm);
     if (cap_stream) cudaStreamDestroy(cap_stream);
     if (own_stream && stream) cudaStreamDestroy(stream);
 }
@@ -775,8 +785,19 @@ void enqueue_block(gfors_ctx* C, cudaStream_t s, const gfors_params* p, int W, H
         enqueue_reset(C, s, W, ~0ull);
         enqueue_sample<T>(C, s, nullptr, W, word_off, p->seed, kint, r, p->k_r, 0u, 0);
         enqueue_eval(C, s, W);
-        LAUNCH(C, s, KC_ARGMIN, (k_argmin<<<1, NT, 0, s>>>(C->d_z, C->d_viol, 64LL * W, word_off, C->d_ctrl, kint, r, p->k_r, 0)));
-        LAUNCH(C, s, KC_ARGMIN, (k_copy_best<<<grid_for(C->n), NT, 0, s>>>(C->d_X, W, C->n, C->d_ctrl, C->d_xbest)));
+        if (C->sharded) {
+            // record -> ncclAllGather -> identical merge on every rank -> regenerate the winner's bits
+            LAUNCH(C, s, KC_ARGMIN, (k_local_record<<<1, NT, 0, s>>>(C->d_z, C->d_viol, 64LL * W, word_off, C->d_ctrl, C->d_rec)));
+            const int rc = nccl().AllGather(C->d_rec, C->d_rec + 4, 4, ncclFloat64_, C->comm, s);
+            if (rc != 0) throw Err{GFORS_E_NCCL, std::string("ncclAllGather: ") + nccl().GetErrorString(rc)};
+            LAUNCH(C, s, KC_ARGMIN, (k_merge_records<<<1, 32, 0, s>>>(C->d_rec + 4, C->world, C->d_ctrl, kint, r, p->k_r, C->d_regen)));
+            const uint2 key = make_uint2((unsigned)(p->seed & 0xffffffffu), (unsigned)(p->seed >> 32));
+            LAUNCH(C, s, KC_ARGMIN, (k_regen_best<T><<<grid_for(C->n), NT, 0, s>>>((const T*)C->d_x[0], (const T*)C->d_x[1], C->n,
+                                                                                  C->d_ctrl, kint, key, C->d_regen, C->d_xbest)));
+        } else {
+            LAUNCH(C, s, KC_ARGMIN, (k_argmin<<<1, NT, 0, s>>>(C->d_z, C->d_viol, 64LL * W, word_off, C->d_ctrl, kint, r, p->k_r, 0)));
+            LAUNCH(C, s, KC_ARGMIN, (k_copy_best<<<grid_for(C->n), NT, 0, s>>>(C->d_X, W, C->n, C->d_ctrl, C->d_xbest)));
+        }
     }
     LAUNCH(C, s, KC_HALT, (k_halt<<<1, NT, 0, s>>>(C->d_ctrl, hp, C->d_part1, C->nb1, C->d_part2, C->nb2, C->n, C->d_hist,
                                                   C->d_rho, C->nrho, C->d_trace, h, use_handle)));
@@ -919,6 +940,8 @@ static void do_preprocess(gfors_ctx* C, const gfors_prep_opts* o, gfors_scaling*
     C->d_segpart = dalloc<double>(C->segpart_len);
     C->d_segpart2 = dalloc<double>(C->segpart_len);
     C->d_u = dalloc<double>(std::max<long long>(m, 1));
+    C->d_rec = dalloc<double>(4 + 4LL * C->world);
+    C->d_regen = dalloc<long long>(2);
     C->d_ctrl = dalloc<Ctrl>(1);
     C->d_hist = dalloc<double>(3 * 1024);
     C->d_xbest = dalloc<unsigned char>(n);
@@ -1026,7 +1049,8 @@ static void do_run_t(gfors_ctx* C, const gfors_params* p, gfors_run_info* out) {
     CK(cudaEventRecord(e0, s));
     if (max_blocks > 0) {
         if (p->use_graph) {
-            if (!(C->gvalid && same_graph_key(C->gkey, *p) && C->gkey_W == W)) {
+            const bool same = same_graph_key(C->gkey, *p) && C->gkey_W == W;
+            if (!(C->gvalid && same) && !(C->gno && same)) {
                 if (C->gexec) { cudaGraphExecDestroy(C->gexec); C->gexec = nullptr; }
                 if (C->graph) { cudaGraphDestroy(C->graph); C->graph = nullptr; }
                 CK(cudaGraphCreate(&C->graph, 0));
@@ -1042,20 +1066,34 @@ static void do_run_t(gfors_ctx* C, const gfors_params* p, gfors_run_info* out) {
                 cudaGraph_t body = cp.conditional.phGraph_out[0];
                 if (!C->cap_stream) CK(cudaStreamCreateWithFlags(&C->cap_stream, cudaStreamNonBlocking));
                 CK(cudaStreamBeginCaptureToGraph(C->cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+                bool cap_ok = true;
                 try {
                     enqueue_block<T>(C, C->cap_stream, p, W, hp, handle, 1);
-                } catch (...) {
-                    cudaGraph_t g2;
-                    cudaStreamEndCapture(C->cap_stream, &g2);
-                    throw;
+                } catch (const Err& e) {
+                    cap_ok = false;
+                    C->graph_note = "capture failed: " + e.msg;
                 }
                 cudaGraph_t g2;
-                CK(cudaStreamEndCapture(C->cap_stream, &g2));
-                CK(cudaGraphInstantiate(&C->gexec, C->graph, 0));
+                const cudaError_t ec = cudaStreamEndCapture(C->cap_stream, &g2);
+                if (ec != cudaSuccess) { cap_ok = false; C->graph_note = std::string("end capture: ") + cudaGetErrorString(ec); }
+                if (cap_ok) {
+                    const cudaError_t ei = cudaGraphInstantiate(&C->gexec, C->graph, 0);
+                    if (ei != cudaSuccess) { cap_ok = false; C->graph_note = std::string("instantiate: ") + cudaGetErrorString(ei); }
+                }
+                cudaGetLastError();
+                if (!cap_ok) {
+                    // e.g. a collective that cannot live in a conditional body: fall back to the eager loop
+                    if (C->gexec) { cudaGraphExecDestroy(C->gexec); C->gexec = nullptr; }
+                    if (C->graph) { cudaGraphDestroy(C->graph); C->graph = nullptr; }
+                    if (!C->sharded) throw Err{GFORS_E_CUDA, C->graph_note};
+                }
                 C->gkey = *p;
                 C->gkey_W = W;
-                C->gvalid = true;
+                C->gvalid = cap_ok;
+                C->gno = !cap_ok;
             }
+        }
+        if (p->use_graph && C->gvalid) {
             CK(cudaGraphLaunch(C->gexec, s));
         } else {
             // eager: one block at a time, host reads the halt flag (debug / fallback path)
@@ -1160,14 +1198,22 @@ gfors_status gfors_create(gfors_ctx** out, const gfors_device_opts* opts) {
     try {
         if (opts) { C->device = opts->device; C->rank = opts->rank; C->world = opts->world; }
         if (C->world < 1 || C->rank < 0 || C->rank >= C->world) input_error("device_opts: need 0 <= rank < world");
-        // world > 1 without an NCCL id: independent sample shard (rank r draws global words
-        // [r*W, (r+1)*W)); the caller merges incumbents with gfors_merge_records.
-        if (C->world > 1 && opts->nccl_id)
-            throw Err{GFORS_E_NCCL, "in-loop NCCL incumbent exchange is not in this build; pass nccl_id = NULL"};
+        // nccl_id == NULL with world > 1: independent sample shard (rank r draws global words
+        // [r*W, (r+1)*W)); the caller merges incumbents with gfors_merge_records.  nccl_id != NULL:
+        // in-loop record exchange over NCCL every sampling round (shard.cuh).
         int ndev = 0;
         CK(cudaGetDeviceCount(&ndev));
         if (C->device < 0 || C->device >= ndev) input_error("device_opts.device: %d not in [0,%d)", C->device, ndev);
         CK(cudaSetDevice(C->device));
+        if (opts && opts->nccl_id) {
+            NcclApi& api = nccl();
+            if (!api.ok) throw Err{GFORS_E_NCCL, api.why};
+            ncclUniqueId id;
+            memcpy(&id, opts->nccl_id, sizeof id);
+            const int rc = api.CommInitRank(&C->comm, C->world, id, C->rank);
+            if (rc != 0) throw Err{GFORS_E_NCCL, std::string("ncclCommInitRank: ") + api.GetErrorString(rc)};
+            C->sharded = true;
+        }
         if (opts && opts->stream) {
             C->stream = (cudaStream_t)opts->stream;
         } else {
@@ -1374,7 +1420,7 @@ int64_t gfors_launches_per_block(gfors_ctx* C, const gfors_params* p) {
     eval += C->n_int ? 2 : 0;
     eval += C->n_real ? 1 : 0;
     eval += 2 + ((C->obj_bits && C->hasq) ? 1 : 0);  // objective partial(s) + final
-    const long long per_round = 1 /*reset*/ + 1 /*sample*/ + eval + 2 /*argmin, copy*/;
+    const long long per_round = 1 /*reset*/ + 1 /*sample*/ + eval + (C->sharded ? 3 /*record, merge, regen*/ : 2 /*argmin, copy*/);
     C->launches = before;
     return per_iter * p->k_int + trig + per_round * p->k_r + 1 /*halt*/;
 }
@@ -1418,6 +1464,18 @@ gfors_status gfors_profile_blocks(gfors_ctx* C, const gfors_params* p, int32_t b
     if (n_classes) *n_classes = nc;
     API_END(C)
 }
+
+gfors_status gfors_nccl_unique_id(void* out128) {
+    if (!out128) return GFORS_E_INPUT;
+    NcclApi& api = nccl();
+    if (!api.ok) return GFORS_E_NCCL;
+    ncclUniqueId id;
+    if (api.GetUniqueId(&id) != 0) return GFORS_E_NCCL;
+    memcpy(out128, &id, sizeof id);
+    return GFORS_OK;
+}
+
+const char* gfors_graph_note(const gfors_ctx* C) { return C ? C->graph_note.c_str() : ""; }
 
 int32_t gfors_merge_records(const double* z, const int64_t* index, const int32_t* valid, int32_t world) {
     // lowest z among valid records, ties -> lowest global sample index (reading R11)
