@@ -24,7 +24,6 @@ import os
 import statistics
 import subprocess
 import sys
-import threading
 import time
 
 import numpy as np
@@ -168,7 +167,6 @@ def oracle_block_seconds(inst, k_int, k_b, budget_s=20.0, seed=20251030):
     O.sample_subset(x[idx], idx, seed, 0, 0, max(1, k_b // 64))
     t_samp_var = (time.perf_counter() - ts) / nsub  # per variable, all k_b lanes
     lanes = 64
-    bits = O.sample_subset(x[idx][:0], idx[:0], seed, 0, 0, 1)  # noqa: F841 (shape helper)
     full_bits = np.zeros((n, 1), dtype=np.uint64)
     rng = np.random.default_rng(seed)
     full_bits[:, 0] = rng.integers(0, 2**63, size=n, dtype=np.int64).astype(np.uint64)
@@ -264,7 +262,17 @@ def run_gpu(args):
     inst = make_instance(args.config, args.seed)
     meta = inst_meta(inst)
     stream = torch.cuda.current_stream()
-    s = gf.Solver(local, stream=stream.cuda_stream, rank=rank, world=world)
+    nccl_id = None
+    if world > 1:
+        # in-loop incumbent exchange (one 32-byte record per rank per sampling round, ncclAllGather
+        # captured in the loop graph): id made on rank 0, broadcast through torch.distributed
+        import torch.distributed as dist
+        buf = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            buf.copy_(torch.frombuffer(bytearray(gf.nccl_unique_id()), dtype=torch.uint8).cuda())
+        dist.broadcast(buf, 0)
+        nccl_id = bytes(buf.cpu().numpy().tobytes())
+    s = gf.Solver(local, stream=stream.cuda_stream, rank=rank, world=world, nccl_id=nccl_id)
     # device-resident inputs (value leg): torch tensors on cuda
     dev = {k: (torch.from_numpy(np.ascontiguousarray(v)).cuda() if isinstance(v, np.ndarray) else v)
            for k, v in inst.items()}
@@ -332,7 +340,7 @@ def run_gpu(args):
                 h2d += v.nbytes
             else:
                 host[k] = v
-        s2 = gf.Solver(local, stream=stream.cuda_stream, rank=rank, world=world)
+        s2 = gf.Solver(local, stream=stream.cuda_stream, rank=rank, world=world, nccl_id=nccl_id)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         s2.load(host)
@@ -366,7 +374,7 @@ def run_gpu(args):
                        if args.config == 5 else f"BASELINE config {args.config}",
                        "n": meta["n"], "m": meta["m"], "nnz": meta["nnz"], "k_int": args.k_int, "k_r": 1,
                        "k_b_per_rank": args.k_b, "precision": f"fp{args.precision} iterates, fp64 accumulation, exact int64 evaluation",
-                       "parallelism": f"sample-sharded x{world}, PDHG replicated", "l2": "inputs larger than L2 (K stream ~0.5 GB/iter)",
+                       "parallelism": f"sample-sharded x{world} (NCCL record all-gather per round), PDHG replicated", "l2": "inputs larger than L2 (K stream ~0.5 GB/iter)",
                        "seed": args.seed, "obj_scale": sc["obj_scale"], "k_scale": sc["k_scale"]},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
