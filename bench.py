@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--impl", default="gfors", choices=("gfors", "reference"))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--profile-blocks", type=int, default=20)
+    ap.add_argument("--profile-blocks", type=int, default=0, help="eager blocks replayed with per-kernel events (0 = --steps)")
     return ap.parse_args()
 
 
@@ -314,7 +314,7 @@ def run_gpu(args):
     z, _, inc = s.best_incumbent(want_x=False)
 
     # per-kernel device times (CUDA events around every launch of an eager replay of the same blocks)
-    prof = s.profile_blocks(args.profile_blocks, **common)
+    prof = s.profile_blocks(args.profile_blocks or args.steps, **common)
     launches = s.launches_per_block(**common)
     step_ms = sum(prof.values())
     byt = algorithmic_bytes(meta, fb)

@@ -31,6 +31,7 @@
 #include "trig.cuh"
 #include "sparse_primal.cuh"
 #include "shard.cuh"
+#include "push_dual.cuh"
 #include <cstdlib>
 
 using namespace gfors;
@@ -204,6 +205,15 @@ enum KClass { KC_DUAL = 0, KC_PRIMAL, KC_TRIGR, KC_TRIGC, KC_SAMPLE, KC_FEAS, KC
 
 }  // namespace
 
+// opt a kernel into the largest dynamic shared memory it can have next to its static shared memory
+constexpr size_t SMEM_PER_BLOCK_MAX = 227 * 1024;
+constexpr size_t SP_DYN_MAX = SMEM_PER_BLOCK_MAX - 8 * 1024;  // k_primal_sparse: static part < 8 KB
+static void set_max_dyn_smem(const void* fn) {
+    cudaFuncAttributes a;
+    CK(cudaFuncGetAttributes(&a, fn));
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(SMEM_PER_BLOCK_MAX - a.sharedSizeBytes)));
+}
+
 // =============================================================================================
 // CheckHalt + UpdatePenalty + loop control, one block of 256 threads
 // =============================================================================================
@@ -300,6 +310,11 @@ struct gfors_ctx {
     long long* sp_blk_row = nullptr;
     long long sp_nblk = 0;
     unsigned* d_nzbits = nullptr;
+    bool push_dual = false;          // sparse-xbar dual (push_dual.cuh)
+    unsigned push_thr = 0;
+    int* d_plist[2] = {nullptr, nullptr};
+    unsigned* d_pcount = nullptr;    // [2]
+    long long* d_acc = nullptr;      // [m]
     double* d_segpart = nullptr;
     double* d_segpart2 = nullptr;
     double* d_u = nullptr;  // K_u xbar of the block's last iteration (trigger pass, rb path)
@@ -415,7 +430,7 @@ void gfors_ctx::free_problem() {
 void gfors_ctx::free_prep() {
     void** ps[] = {(void**)&d_s, &d_g, &d_rh, &d_cs, &d_qs, &d_x[0], &d_x[1], &d_xb[0], &d_xb[1], &d_y[0], &d_y[1],
                    &d_w, (void**)&d_tmp[0], (void**)&d_tmp[1], (void**)&d_tmp[2], (void**)&d_tmp[3],
-                   (void**)&d_red, (void**)&d_scalar, (void**)&d_segpart, (void**)&d_segpart2, (void**)&d_u, (void**)&d_rec, (void**)&d_regen, (void**)&d_part1,
+                   (void**)&d_red, (void**)&d_scalar, (void**)&d_segpart, (void**)&d_segpart2, (void**)&d_u, (void**)&d_rec, (void**)&d_regen, (void**)&d_plist[0], (void**)&d_plist[1], (void**)&d_pcount, (void**)&d_acc, (void**)&d_part1,
                    (void**)&d_part2, (void**)&d_hist, (void**)&d_rho, (void**)&d_trace, (void**)&d_xbest,
                    (void**)&d_X, (void**)&d_viol, (void**)&d_iacc, &d_zpart, (void**)&d_z, (void**)&d_ctrl};
     for (void** p : ps) { dfree(*p); *p = nullptr; }
@@ -503,6 +518,8 @@ inline Csr csr_Q(gfors_ctx* C) { return Csr{C->d_qptr, C->d_qcol, C->d_qval, C->
 template <typename T>
 void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
     State<T> st = state_of<T>(C);
+    PushList pl{{nullptr, nullptr}, {nullptr, nullptr}, 0u, 0, nullptr};
+    if (C->push_dual) pl = PushList{{C->d_plist[0], C->d_plist[1]}, {C->d_pcount, C->d_pcount + 1}, C->push_thr, C->n, C->d_acc};
     const Ctrl* ctrl = C->d_ctrl;
     const double* g = (const double*)C->d_g;
     const double* rh = (const double*)C->d_rh;
@@ -517,7 +534,13 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
             KIND_SWITCH(C->kkind, LAUNCH(C, s, KC_DUAL,
                 (k_dual_rb<T, KINDV><<<grid, RB_NT, 0, s>>>(csr_K(C), C->pd.blk_row, C->pd.nblk, st, g, rh, C->d_rsign,
                                                             C->m1, ctrl, kint, j,
-                                                            (kint == 0 || j == kint - 1) ? C->d_u : nullptr))));
+                                                            (kint == 0 || j == kint - 1) ? C->d_u : nullptr, pl))));
+            if (C->push_dual) {
+                // the two push-mode kernels exit at once unless the xbar list is short (device decision)
+                LAUNCH(C, s, KC_DUAL, (k_push_scatter<T><<<grid_for(C->n), NT, 0, s>>>(csr_Kt(C), pl, st, ctrl, kint, j)));
+                LAUNCH(C, s, KC_DUAL, (k_push_rows<T><<<grid_for(C->m), NT, 0, s>>>(C->m, pl, st, g, rh, C->d_rsign, C->m1, ctrl,
+                                                                                  kint, j, (kint == 0 || j == kint - 1) ? C->d_u : nullptr)));
+            }
         } else if (!C->pd.seg) {
             const int grid = grid_for(C->m * (long long)C->pd.sub);
             KIND_SWITCH(C->kkind, SUB_SWITCH(C->pd.sub, LAUNCH(C, s, KC_DUAL,
@@ -537,7 +560,7 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
     const T* cs = (const T*)C->d_cs;
     // K' values: SIGN rows fold the sign into w, so the transpose carries no values
     const int tkind = C->kkind;
-    if (C->sparse_primal && sparse_primal_smem<T>(C->m) <= 227 * 1024) {
+    if (C->sparse_primal && sparse_primal_smem<T>(C->m) <= SP_DYN_MAX) {
         const long long nwords = (C->m + 31) / 32;
         LAUNCH(C, s, KC_PRIMAL, (k_nzmask<T><<<grid_for(nwords * 32), NT, 0, s>>>(st.w, C->m, C->d_nzbits)));
         const size_t sm = sparse_primal_smem<T>(C->m);
@@ -545,16 +568,16 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
         if (C->hasq) {
             KIND_SWITCH(tkind, {
                 static bool attr = false;
-                if (!attr) { CK(cudaFuncSetAttribute(k_primal_sparse<T, KINDV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)); attr = true; }
+                if (!attr) { set_max_dyn_smem((const void*)k_primal_sparse<T, KINDV, true>); attr = true; }
                 LAUNCH(C, s, KC_PRIMAL, (k_primal_sparse<T, KINDV, true><<<grid, SP_NT, sm, s>>>(csr_Kt(C), C->sp_blk_row, C->sp_nblk,
-                    C->d_nzbits, nwords, Q, qs, st, cs, ctrl, kint, j)));
+                    C->d_nzbits, nwords, Q, qs, st, cs, ctrl, kint, j, pl)));
             });
         } else {
             KIND_SWITCH(tkind, {
                 static bool attr = false;
-                if (!attr) { CK(cudaFuncSetAttribute(k_primal_sparse<T, KINDV, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)); attr = true; }
+                if (!attr) { set_max_dyn_smem((const void*)k_primal_sparse<T, KINDV, false>); attr = true; }
                 LAUNCH(C, s, KC_PRIMAL, (k_primal_sparse<T, KINDV, false><<<grid, SP_NT, sm, s>>>(csr_Kt(C), C->sp_blk_row, C->sp_nblk,
-                    C->d_nzbits, nwords, Q, qs, st, cs, ctrl, kint, j)));
+                    C->d_nzbits, nwords, Q, qs, st, cs, ctrl, kint, j, pl)));
             });
         }
     } else if (C->pp.wrb) {
@@ -573,11 +596,11 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
         if (C->hasq) {
             KIND_SWITCH(tkind, LAUNCH(C, s, KC_PRIMAL,
                 (k_primal_rb<T, KINDV, true><<<grid, RB_NT, 0, s>>>(csr_Kt(C), C->pp.blk_row, C->pp.nblk, Q, qs, st, cs,
-                                                                    ctrl, kint, j))));
+                                                                    ctrl, kint, j, pl))));
         } else {
             KIND_SWITCH(tkind, LAUNCH(C, s, KC_PRIMAL,
                 (k_primal_rb<T, KINDV, false><<<grid, RB_NT, 0, s>>>(csr_Kt(C), C->pp.blk_row, C->pp.nblk, Q, qs, st, cs,
-                                                                     ctrl, kint, j))));
+                                                                     ctrl, kint, j, pl))));
         }
     } else if (!C->pp.seg) {
         const int grid = grid_for(C->n * (long long)C->pp.sub);
@@ -941,6 +964,14 @@ static void do_preprocess(gfors_ctx* C, const gfors_prep_opts* o, gfors_scaling*
     C->d_segpart2 = dalloc<double>(C->segpart_len);
     C->d_u = dalloc<double>(std::max<long long>(m, 1));
     C->d_rec = dalloc<double>(4 + 4LL * C->world);
+    if (C->push_dual) {
+        C->d_plist[0] = dalloc<int>(n);
+        C->d_plist[1] = dalloc<int>(n);
+        C->d_pcount = dalloc<unsigned>(2);
+        C->d_acc = dalloc<long long>(std::max<long long>(m, 1));
+        CK(cudaMemsetAsync(C->d_pcount, 0xff, 2 * sizeof(unsigned), s));
+        CK(cudaMemsetAsync(C->d_acc, 0, std::max<long long>(m, 1) * sizeof(long long), s));
+    }
     C->d_regen = dalloc<long long>(2);
     C->d_ctrl = dalloc<Ctrl>(1);
     C->d_hist = dalloc<double>(3 * 1024);
@@ -1032,6 +1063,7 @@ static void do_run_t(gfors_ctx* C, const gfors_params* p, gfors_run_info* out) {
     // reset state and control
     k_init_state<T><<<grid_for(std::max(C->n, C->m)), NT, 0, s>>>(state_of<T>(C), C->n, C->m);
     CK(cudaGetLastError());
+    if (C->push_dual) CK(cudaMemsetAsync(C->d_pcount, 0xff, 2 * sizeof(unsigned), s));  // unknown -> gather mode
     Ctrl h{};
     h.blk = 0; h.k = 0; h.rho = rho[0]; h.tau1 = std::sqrt(p->sigma); h.tau2 = std::sqrt(p->sigma);
     h.max_blocks = max_blocks; h.z_best = INFINITY; h.found_iter = h.found_round = h.found_index = -1; h.win_lane = -1;
@@ -1162,6 +1194,7 @@ static void set_state_t(gfors_ctx* C, const double* x, const double* xbar, const
     if (xbar) { CK(cudaMemcpyAsync(t, xbar, C->n * 8, cudaMemcpyHostToDevice, s)); k_to_T<T><<<grid_for(C->n), NT, 0, s>>>(t, C->n, (T*)C->d_xb[0]); CK(cudaStreamSynchronize(s)); }
     if (y && C->m) { CK(cudaMemcpyAsync(t, y, C->m * 8, cudaMemcpyHostToDevice, s)); k_to_T<T><<<grid_for(C->m), NT, 0, s>>>(t, C->m, (T*)C->d_y[0]); CK(cudaStreamSynchronize(s)); }
     CK(cudaGetLastError());
+    if (C->push_dual) CK(cudaMemset(C->d_pcount, 0xff, 2 * sizeof(unsigned)));
     C->hk = 0;
 }
 
@@ -1412,7 +1445,8 @@ int64_t gfors_launches_per_block(gfors_ctx* C, const gfors_params* p) {
     // a dry count: mirror enqueue_block's structure
     long long per_iter = 0;
     per_iter += C->m > 0 ? (C->pd.seg ? 2 : 1) : 0;
-    const bool spp = C->sparse_primal && (C->precision == 64 ? sparse_primal_smem<double>(C->m) : sparse_primal_smem<float>(C->m)) <= 227 * 1024;
+    per_iter += C->push_dual ? 2 : 0;
+    const bool spp = C->sparse_primal && (C->precision == 64 ? sparse_primal_smem<double>(C->m) : sparse_primal_smem<float>(C->m)) <= SP_DYN_MAX;
     per_iter += spp ? 2 : (C->pp.seg ? 2 : 1);
     long long trig = (C->m > 0 ? (C->pd.seg ? 3 : (C->pd.rb ? 1 + (C->pd.nblk < C->nb1 ? 1 : 0) : 1)) : 1) + 1;
     long long eval = 0;

@@ -16,6 +16,7 @@
 #pragma once
 #include "common.cuh"
 #include "pdhg.cuh"
+#include "push_list.cuh"
 
 namespace gfors {
 
@@ -115,10 +116,12 @@ __global__ void __launch_bounds__(RB_NT) k_dual_rb(Csr K, const long long* __res
                                                    State<T> s, const double* __restrict__ g,
                                                    const double* __restrict__ rh, const signed char* __restrict__ rsign,
                                                    long long m1, const Ctrl* __restrict__ ctrl, long long kint,
-                                                   long long j, double* __restrict__ u_out) {
+                                                   long long j, double* __restrict__ u_out, PushList pl) {
     __shared__ __align__(16) T sv[2][RB_NNZ];
     const long long kk = iter_index(ctrl, kint, j);
     const int par = (int)(kk & 1);
+    if (push_mode(pl, par)) return;  // sparse xbar: k_push_scatter/k_push_rows do this iteration
+    if (pl.acc && blockIdx.x == 0 && threadIdx.x == 0) *pl.count[par ^ 1] = 0u;
     const T* __restrict__ xb = par ? s.xb[1] : s.xb[0];
     const T* __restrict__ yin = par ? s.y[1] : s.y[0];
     T* __restrict__ yout = par ? s.y[0] : s.y[1];
@@ -169,8 +172,11 @@ template <typename T, int KIND, bool HASQ>
 __global__ void __launch_bounds__(RB_NT, 6) k_primal_rb(Csr Kt, const long long* __restrict__ blk_row, long long nblk,
                                                      Csr Q, const T* __restrict__ qs, State<T> s,
                                                      const T* __restrict__ cs, const Ctrl* __restrict__ ctrl,
-                                                     long long kint, long long j) {
+                                                     long long kint, long long j, PushList pl) {
     __shared__ __align__(16) T sv[2][RB_NNZ];
+    __shared__ unsigned s_cnt, s_base;
+    __shared__ int s_list[RB_NT];
+    __shared__ bool s_en;
     const long long kk = iter_index(ctrl, kint, j);
     const int par = (int)(kk & 1);
     const T* __restrict__ xin = par ? s.x[1] : s.x[0];
@@ -185,6 +191,7 @@ __global__ void __launch_bounds__(RB_NT, 6) k_primal_rb(Csr Kt, const long long*
     for (long long b = blockIdx.x; b < nblk; b += gridDim.x) {
         rb_issue<T>(nxt, s.w, sv[st ^ 1]);
         rb_load_idx(Kt, blk_row, b + 2LL * gridDim.x, nblk, nxt);
+        if (threadIdx.x == 0) s_en = pl.acc && *(volatile unsigned*)pl.count[par ^ 1] <= pl.thr;
         cp_async_wait1();
         __syncthreads();
         const long long r0 = blk_row[b], r1 = blk_row[b + 1];
@@ -192,6 +199,7 @@ __global__ void __launch_bounds__(RB_NT, 6) k_primal_rb(Csr Kt, const long long*
         const int nr = (int)(r1 - r0);
         const int G = rb_group_size(nr);
         const int lane = threadIdx.x & (G - 1), grp = threadIdx.x / G, ngr = RB_NT / G;
+        const bool en = s_en;
         for (int rb = 0; rb < nr; rb += ngr) {
             const int rr = rb + grp;
             const long long i = r0 + rr;
@@ -205,13 +213,17 @@ __global__ void __launch_bounds__(RB_NT, 6) k_primal_rb(Csr Kt, const long long*
             }
             a = rb_group_sum(a, G);
             if constexpr (HASQ) bq = rb_group_sum(bq, G);
+            bool nz = false;
             if (lane == 0 && rr < nr) {
                 const double delta = ((ci + rho) - a) + 2.0 * bq - 2.0 * rho * xi;
                 double xn = xi - tau1 * delta;
                 xn = xn < 0.0 ? 0.0 : (xn > 1.0 ? 1.0 : xn);
                 xout[i] = (T)xn;
-                xbout[i] = (T)(2.0 * xn - xi);
+                const T xbn = (T)(2.0 * xn - xi);
+                xbout[i] = xbn;
+                nz = xbn != (T)0;
             }
+            push_append<RB_NT>(pl, par ^ 1, nz, (int)i, en, &s_cnt, &s_base, s_list);
         }
         __syncthreads();
         st ^= 1;

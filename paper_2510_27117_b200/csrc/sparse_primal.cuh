@@ -102,8 +102,11 @@ __global__ void __launch_bounds__(SP_NT, 1) k_primal_sparse(Csr Kt, const long l
                                                             const unsigned* __restrict__ bits, long long nwords,
                                                             Csr Q, const T* __restrict__ qs, State<T> s,
                                                             const T* __restrict__ cs, const Ctrl* __restrict__ ctrl,
-                                                            long long kint, long long j) {
+                                                            long long kint, long long j, PushList pl) {
     extern __shared__ __align__(16) unsigned char sp_smem[];
+    __shared__ unsigned s_cnt, s_base;
+    __shared__ int s_list[SP_NT];
+    __shared__ bool s_en;
     T* svb = reinterpret_cast<T*>(sp_smem);                          // [2][SP_NNZ]
     unsigned* sbits = reinterpret_cast<unsigned*>(svb + 2 * SP_NNZ);  // [nwords]
     for (long long k = threadIdx.x; k < nwords; k += SP_NT) sbits[k] = __ldg(bits + k);
@@ -124,6 +127,7 @@ __global__ void __launch_bounds__(SP_NT, 1) k_primal_sparse(Csr Kt, const long l
         sp_issue<T>(nxt, s.w, sbits, svb + (st ^ 1) * SP_NNZ);
         sp_load_idx(Kt, blk_row, b + 2LL * gridDim.x, nblk, nxt);
         const SpRow nrow = sp_prefetch_row<T>(Kt, blk_row, b + gridDim.x, nblk, xin, cs);
+        if (threadIdx.x == 0) s_en = pl.acc && *(volatile unsigned*)pl.count[par ^ 1] <= pl.thr;
         cp_async_wait1();
         __syncthreads();
         const T* sv = svb + st * SP_NNZ;
@@ -141,14 +145,18 @@ __global__ void __launch_bounds__(SP_NT, 1) k_primal_sparse(Csr Kt, const long l
         }
         a = rb_group_sum(a, G);
         if constexpr (HASQ) bq = rb_group_sum(bq, G);
+        bool nz = false;
         if (lane == 0 && cur.valid) {
             const double xi = cur.xi;
             const double delta = ((cur.ci + rho) - a) + 2.0 * bq - 2.0 * rho * xi;
             double xn = xi - tau1 * delta;
             xn = xn < 0.0 ? 0.0 : (xn > 1.0 ? 1.0 : xn);
             xout[i] = (T)xn;
-            xbout[i] = (T)(2.0 * xn - xi);
+            const T xbn = (T)(2.0 * xn - xi);
+            xbout[i] = xbn;
+            nz = xbn != (T)0;
         }
+        push_append<SP_NT>(pl, par ^ 1, nz, (int)i, s_en, &s_cnt, &s_base, s_list);
         __syncthreads();
         st ^= 1;
         cur = nrow;

@@ -344,3 +344,30 @@ def test_sparse_primal_variant_parity(gf, fam, monkeypatch):
     zg, xbest, mg = s.best_incumbent()
     zo, xo2 = o.best()
     assert zg == zo or (math.isinf(zg) and math.isinf(zo))
+
+
+@pytest.mark.parametrize("fam", ["setcover", "mis", "bqp"])
+def test_push_dual_variant_parity(gf, fam, monkeypatch):
+    """Sparse-xbar dual (fixed-point scatter, forced on) against the oracle: 1000 fp64 iterations
+    within 1e-5; a run keeps the same incumbent and iteration accounting."""
+    monkeypatch.setenv("GFORS_PUSH_DUAL", "1")
+    inst = G.SMALL[fam](12)
+    s, _, o, _ = _pair(gf, inst, 64)
+    tau = math.sqrt(0.99)
+    rho = O.rho_schedule(1e-3, 10.0, 100.0, 2.0, 1e-6, 100)
+    o.state_init()
+    x0, xb0, y0 = o.get_state()
+    s.set_state(x0, xb0, y0)
+    for b in range(100):
+        s.step(10, rho[b], tau, tau)
+        for _ in range(10):
+            o.step(rho[b], tau, tau)
+    xg, _, yg = s.get_state()
+    xo, _, yo = o.get_state()
+    assert _rel(xg, xo) <= 1e-5 and _rel(yg, yo) <= 1e-5
+    ig = s.run(max_iters=400)
+    io = o.run(max_iters=400)
+    assert ig["iters"] == io["iters"] and ig["rounds"] == io["rounds"]
+    zg, _, _ = s.best_incumbent()
+    zo, _ = o.best()
+    assert zg == zo or (math.isinf(zg) and math.isinf(zo))
