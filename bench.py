@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--impl", default="gfors", choices=("gfors", "reference"))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-tti", action="store_true", help="skip the time-to-incumbent solves of configs 1-4")
     ap.add_argument("--profile-blocks", type=int, default=0, help="eager blocks replayed with per-kernel events (0 = --steps)")
     return ap.parse_args()
 
@@ -355,6 +356,24 @@ def run_gpu(args):
                "note": "one gfors_load+preprocess+run(K blocks)+best_incumbent call chain from pinned host memory; "
                        "instance bytes amortised over the K steps", "seconds": te}
 
+    # time-to-incumbent (BASELINE metric, third part): full solves of the small configs with the
+    # default halting rule, %globaltimer stamp of the last improvement (Preprocess excluded)
+    tti = None
+    if rank == 0 and world == 1 and not args.no_tti:
+        tti = {}
+        for cfg in (1, 2, 3, 4):
+            inst_c = make_instance(cfg, args.seed)
+            sc_ = gf.Solver(local, stream=stream.cuda_stream)
+            sc_.load(inst_c)
+            sc_.preprocess(precision=args.precision)
+            info_c = sc_.run(max_iters=20000, k_b=args.k_b)
+            zc, _, mc = sc_.best_incumbent(want_x=False)
+            tti[f"config{cfg}"] = {"z_best": zc if mc["has_incumbent"] else None,
+                                   "time_to_incumbent_s": mc["found_time_s"] if mc["has_incumbent"] else None,
+                                   "found_iter": mc["found_iter"], "iters": info_c["iters"],
+                                   "halt_reason": info_c["halt_reason"], "loop_s": info_c["elapsed_s"]}
+            sc_.close()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         est = oracle_block_seconds(inst, args.k_int, args.k_b)
@@ -388,6 +407,7 @@ def run_gpu(args):
             "gpu_launches": int(launches * args.steps + 8),
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "time_to_incumbent_small_configs": tti,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
