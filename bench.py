@@ -319,8 +319,14 @@ def run_gpu(args):
     launches = s.launches_per_block(**common)
     step_ms = sum(prof.values())
     byt = algorithmic_bytes(meta, fb)
-    dom = max(("pdhg_primal", "pdhg_dual"), key=lambda k: prof.get(k, 0.0))
-    per_launch_ms = prof[dom] / args.k_int
+    act = s.profile_active()  # class -> (active ms over all profiled blocks, launches that did work)
+    # roofline kernel: the gather-mode PDHG kernel with the most active time; its average over the
+    # launches that ran the dense product (mode-switched launches that exited early are excluded)
+    dom = max(("pdhg_primal", "pdhg_dual"), key=lambda k: act.get(k, (0.0, 0))[0])
+    if act.get(dom, (0.0, 0))[1] > 0:
+        per_launch_ms = act[dom][0] / act[dom][1]
+    else:
+        per_launch_ms = prof[dom] / args.k_int
     peak, peak_src, peaks = measured_peaks()
     achieved = byt[dom] / (per_launch_ms * 1e-3) / 1e9
     traffic = None
@@ -403,6 +409,8 @@ def run_gpu(args):
                          "gather": {"gathers_per_launch": meta["nnz"], "achieved_G_per_s": meta["nnz"] / (per_launch_ms * 1e-3) / 1e9,
                                     "ceiling_G_per_s": GATHER_CEILING_G, "frac": meta["nnz"] / (per_launch_ms * 1e-3) / 1e9 / GATHER_CEILING_G}},
             "kernel_ms_per_step": prof, "kernel_share": {k: v / step_ms for k, v in prof.items()} if step_ms else {},
+            "kernel_active": {k: {"active_launches": v[1], "avg_active_ms": (v[0] / v[1]) if v[1] else None}
+                              for k, v in act.items()},
             "clocks": clocks,
             "gpu_launches": int(launches * args.steps + 8),
             "e2e": e2e,

@@ -164,6 +164,9 @@ gfors_status gfors_get_trace(gfors_ctx *ctx, double *rows, int64_t max_rows, int
 gfors_status gfors_profile_blocks(gfors_ctx *ctx, const gfors_params *p, int32_t blocks,
                                   double *ms_out, int32_t max_classes, int32_t *n_classes);
 const char *gfors_kernel_class_name(int32_t k);
+/* After gfors_profile_blocks: per kernel class, total ms and number of launches that did work
+ * (duration > 10 us; the mode-switched PDHG kernels exit in ~3 us when their mode is not chosen). */
+gfors_status gfors_profile_active(gfors_ctx *ctx, double *active_ms, double *active_launches, int32_t max_classes);
 /* Number of kernel launches per loop block for p (bench "gpu_launches" accounting). */
 int64_t gfors_launches_per_block(gfors_ctx *ctx, const gfors_params *p);
 /* Cross-rank incumbent merge rule (host-only, no GPU needed): given world records

@@ -95,6 +95,7 @@ EXPORTS = {
     "gfors_get_trace": (I32, [P, P, I64, P]),
     "gfors_profile_blocks": (I32, [P, C.POINTER(Params), I32, P, I32, P]),
     "gfors_kernel_class_name": (C.c_char_p, [I32]),
+    "gfors_profile_active": (I32, [P, P, P, I32]),
     "gfors_launches_per_block": (I64, [P, C.POINTER(Params)]),
     "gfors_merge_records": (I32, [P, P, P, I32]),
     "gfors_nccl_unique_id": (I32, [P]),
@@ -288,6 +289,13 @@ class Solver:
         nc = C.c_int32()
         self._chk(_lib.gfors_profile_blocks(self.h, C.byref(p), blocks, _ptr(ms), 16, C.byref(nc)))
         return {_lib.gfors_kernel_class_name(k).decode(): float(ms[k]) for k in range(nc.value)}
+
+    def profile_active(self):
+        """(total active ms, active launches) per kernel class of the last profile_blocks call."""
+        ams = np.zeros(16); an = np.zeros(16)
+        self._chk(_lib.gfors_profile_active(self.h, _ptr(ams), _ptr(an), 16))
+        return {_lib.gfors_kernel_class_name(k).decode(): (float(ams[k]), int(an[k])) for k in range(16)
+                if _lib.gfors_kernel_class_name(k).decode()}
 
     def graph_note(self):
         return _lib.gfors_graph_note(self.h).decode()

@@ -32,6 +32,7 @@
 #include "sparse_primal.cuh"
 #include "shard.cuh"
 #include "push_dual.cuh"
+#include "push_primal.cuh"
 #include <cstdlib>
 
 using namespace gfors;
@@ -199,9 +200,10 @@ DirPlan plan_direction(const std::vector<int64_t>& ptr, long long rows, cudaStre
     return d;
 }
 
-const char* kClassNames[] = {"pdhg_dual", "pdhg_primal", "trig_rows", "trig_cols", "sample",
-                             "feas", "obj", "argmin", "halt"};
-enum KClass { KC_DUAL = 0, KC_PRIMAL, KC_TRIGR, KC_TRIGC, KC_SAMPLE, KC_FEAS, KC_OBJ, KC_ARGMIN, KC_HALT, KC_N };
+const char* kClassNames[] = {"pdhg_dual", "pdhg_primal", "trig_rows", "trig_cols", "sample", "feas", "obj",
+                             "argmin", "halt", "pdhg_dual_push", "pdhg_primal_push"};
+enum KClass { KC_DUAL = 0, KC_PRIMAL, KC_TRIGR, KC_TRIGC, KC_SAMPLE, KC_FEAS, KC_OBJ, KC_ARGMIN, KC_HALT, KC_DUAL_PUSH,
+              KC_PRIMAL_PUSH, KC_N };
 
 }  // namespace
 
@@ -311,6 +313,13 @@ struct gfors_ctx {
     long long sp_nblk = 0;
     unsigned* d_nzbits = nullptr;
     bool push_dual = false;          // sparse-xbar dual (push_dual.cuh)
+    bool push_primal = false;        // sparse-dual primal (push_primal.cuh)
+    unsigned rthr = 0;
+    int* d_rlist = nullptr;
+    unsigned* d_rcount = nullptr;
+    unsigned long long* d_wmax = nullptr;
+    long long* d_accx = nullptr;
+    int maxcoldeg = 0;
     unsigned push_thr = 0;
     int* d_plist[2] = {nullptr, nullptr};
     unsigned* d_pcount = nullptr;    // [2]
@@ -397,6 +406,7 @@ struct gfors_ctx {
     // profiling
     bool profiling = false;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_ev;
+    std::vector<double> prof_active_ms, prof_active_n;  // per class, last gfors_profile_blocks
     long long launches = 0;
 
     ~gfors_ctx();
@@ -430,7 +440,7 @@ void gfors_ctx::free_problem() {
 void gfors_ctx::free_prep() {
     void** ps[] = {(void**)&d_s, &d_g, &d_rh, &d_cs, &d_qs, &d_x[0], &d_x[1], &d_xb[0], &d_xb[1], &d_y[0], &d_y[1],
                    &d_w, (void**)&d_tmp[0], (void**)&d_tmp[1], (void**)&d_tmp[2], (void**)&d_tmp[3],
-                   (void**)&d_red, (void**)&d_scalar, (void**)&d_segpart, (void**)&d_segpart2, (void**)&d_u, (void**)&d_rec, (void**)&d_regen, (void**)&d_plist[0], (void**)&d_plist[1], (void**)&d_pcount, (void**)&d_acc, (void**)&d_part1,
+                   (void**)&d_red, (void**)&d_scalar, (void**)&d_segpart, (void**)&d_segpart2, (void**)&d_u, (void**)&d_rec, (void**)&d_regen, (void**)&d_plist[0], (void**)&d_plist[1], (void**)&d_pcount, (void**)&d_acc, (void**)&d_rlist, (void**)&d_rcount, (void**)&d_wmax, (void**)&d_accx, (void**)&d_part1,
                    (void**)&d_part2, (void**)&d_hist, (void**)&d_rho, (void**)&d_trace, (void**)&d_xbest,
                    (void**)&d_X, (void**)&d_viol, (void**)&d_iacc, &d_zpart, (void**)&d_z, (void**)&d_ctrl};
     for (void** p : ps) { dfree(*p); *p = nullptr; }
@@ -518,8 +528,11 @@ inline Csr csr_Q(gfors_ctx* C) { return Csr{C->d_qptr, C->d_qcol, C->d_qval, C->
 template <typename T>
 void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
     State<T> st = state_of<T>(C);
-    PushList pl{{nullptr, nullptr}, {nullptr, nullptr}, 0u, 0, nullptr};
-    if (C->push_dual) pl = PushList{{C->d_plist[0], C->d_plist[1]}, {C->d_pcount, C->d_pcount + 1}, C->push_thr, C->n, C->d_acc};
+    PushList pl{{nullptr, nullptr}, {nullptr, nullptr}, 0u, 0, nullptr, nullptr, nullptr};
+    if (C->push_dual)
+        pl = PushList{{C->d_plist[0], C->d_plist[1]}, {C->d_pcount, C->d_pcount + 1}, C->push_thr, C->n, C->d_acc,
+                      C->push_primal ? C->d_rcount : nullptr, C->push_primal ? C->d_wmax : nullptr};
+    const PushPrimal ppr{C->d_rlist, C->d_rcount, C->rthr, C->d_wmax, C->d_accx, C->maxcoldeg, C->m};
     const Ctrl* ctrl = C->d_ctrl;
     const double* g = (const double*)C->d_g;
     const double* rh = (const double*)C->d_rh;
@@ -537,8 +550,8 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
                                                             (kint == 0 || j == kint - 1) ? C->d_u : nullptr, pl))));
             if (C->push_dual) {
                 // the two push-mode kernels exit at once unless the xbar list is short (device decision)
-                LAUNCH(C, s, KC_DUAL, (k_push_scatter<T><<<grid_for(C->n), NT, 0, s>>>(csr_Kt(C), pl, st, ctrl, kint, j)));
-                LAUNCH(C, s, KC_DUAL, (k_push_rows<T><<<grid_for(C->m), NT, 0, s>>>(C->m, pl, st, g, rh, C->d_rsign, C->m1, ctrl,
+                LAUNCH(C, s, KC_DUAL_PUSH, (k_push_scatter<T><<<grid_for(C->n), NT, 0, s>>>(csr_Kt(C), pl, st, ctrl, kint, j)));
+                LAUNCH(C, s, KC_DUAL_PUSH, (k_push_rows<T><<<grid_for(C->m), NT, 0, s>>>(C->m, pl, st, g, rh, C->d_rsign, C->m1, ctrl,
                                                                                   kint, j, (kint == 0 || j == kint - 1) ? C->d_u : nullptr)));
             }
         } else if (!C->pd.seg) {
@@ -560,7 +573,16 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
     const T* cs = (const T*)C->d_cs;
     // K' values: SIGN rows fold the sign into w, so the transpose carries no values
     const int tkind = C->kkind;
-    if (C->sparse_primal && sparse_primal_smem<T>(C->m) <= SP_DYN_MAX) {
+    if (C->push_primal) {
+        // list the active duals; the push kernels run iff the list is short, else k_primal_rb below
+        LAUNCH(C, s, KC_PRIMAL_PUSH, (k_wlist<T><<<grid_for(C->m), NT, 0, s>>>(st.w, ppr)));
+        LAUNCH(C, s, KC_PRIMAL_PUSH, (k_push_scatter_cols<T><<<grid_for(C->m * 32LL), NT, 0, s>>>(csr_K(C), ppr, st.w)));
+        if (C->hasq)
+            LAUNCH(C, s, KC_PRIMAL_PUSH, (k_primal_push<T, true><<<grid_for(C->n), NT, 0, s>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl)));
+        else
+            LAUNCH(C, s, KC_PRIMAL_PUSH, (k_primal_push<T, false><<<grid_for(C->n), NT, 0, s>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl)));
+    }
+    if (C->sparse_primal && !C->push_primal && sparse_primal_smem<T>(C->m) <= SP_DYN_MAX) {
         const long long nwords = (C->m + 31) / 32;
         LAUNCH(C, s, KC_PRIMAL, (k_nzmask<T><<<grid_for(nwords * 32), NT, 0, s>>>(st.w, C->m, C->d_nzbits)));
         const size_t sm = sparse_primal_smem<T>(C->m);
@@ -596,11 +618,13 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
         if (C->hasq) {
             KIND_SWITCH(tkind, LAUNCH(C, s, KC_PRIMAL,
                 (k_primal_rb<T, KINDV, true><<<grid, RB_NT, 0, s>>>(csr_Kt(C), C->pp.blk_row, C->pp.nblk, Q, qs, st, cs,
-                                                                    ctrl, kint, j, pl))));
+                                                                    ctrl, kint, j, pl, C->push_primal ? C->d_rcount : nullptr,
+                                                                    C->rthr))));
         } else {
             KIND_SWITCH(tkind, LAUNCH(C, s, KC_PRIMAL,
                 (k_primal_rb<T, KINDV, false><<<grid, RB_NT, 0, s>>>(csr_Kt(C), C->pp.blk_row, C->pp.nblk, Q, qs, st, cs,
-                                                                     ctrl, kint, j, pl))));
+                                                                     ctrl, kint, j, pl, C->push_primal ? C->d_rcount : nullptr,
+                                                                     C->rthr))));
         }
     } else if (!C->pp.seg) {
         const int grid = grid_for(C->n * (long long)C->pp.sub);
@@ -972,6 +996,15 @@ static void do_preprocess(gfors_ctx* C, const gfors_prep_opts* o, gfors_scaling*
         CK(cudaMemsetAsync(C->d_pcount, 0xff, 2 * sizeof(unsigned), s));
         CK(cudaMemsetAsync(C->d_acc, 0, std::max<long long>(m, 1) * sizeof(long long), s));
     }
+    if (C->push_primal) {
+        C->d_rlist = dalloc<int>(std::max<long long>(m, 1));
+        C->d_rcount = dalloc<unsigned>(1);
+        C->d_wmax = dalloc<unsigned long long>(1);
+        C->d_accx = dalloc<long long>(n);
+        CK(cudaMemsetAsync(C->d_rcount, 0xff, sizeof(unsigned), s));
+        CK(cudaMemsetAsync(C->d_wmax, 0, sizeof(unsigned long long), s));
+        CK(cudaMemsetAsync(C->d_accx, 0, n * sizeof(long long), s));
+    }
     C->d_regen = dalloc<long long>(2);
     C->d_ctrl = dalloc<Ctrl>(1);
     C->d_hist = dalloc<double>(3 * 1024);
@@ -1064,6 +1097,7 @@ static void do_run_t(gfors_ctx* C, const gfors_params* p, gfors_run_info* out) {
     k_init_state<T><<<grid_for(std::max(C->n, C->m)), NT, 0, s>>>(state_of<T>(C), C->n, C->m);
     CK(cudaGetLastError());
     if (C->push_dual) CK(cudaMemsetAsync(C->d_pcount, 0xff, 2 * sizeof(unsigned), s));  // unknown -> gather mode
+    if (C->push_primal) CK(cudaMemsetAsync(C->d_rcount, 0, sizeof(unsigned), s));
     Ctrl h{};
     h.blk = 0; h.k = 0; h.rho = rho[0]; h.tau1 = std::sqrt(p->sigma); h.tau2 = std::sqrt(p->sigma);
     h.max_blocks = max_blocks; h.z_best = INFINITY; h.found_iter = h.found_round = h.found_index = -1; h.win_lane = -1;
@@ -1195,6 +1229,7 @@ static void set_state_t(gfors_ctx* C, const double* x, const double* xbar, const
     if (y && C->m) { CK(cudaMemcpyAsync(t, y, C->m * 8, cudaMemcpyHostToDevice, s)); k_to_T<T><<<grid_for(C->m), NT, 0, s>>>(t, C->m, (T*)C->d_y[0]); CK(cudaStreamSynchronize(s)); }
     CK(cudaGetLastError());
     if (C->push_dual) CK(cudaMemset(C->d_pcount, 0xff, 2 * sizeof(unsigned)));
+    if (C->push_primal) CK(cudaMemset(C->d_rcount, 0, sizeof(unsigned)));
     C->hk = 0;
 }
 
@@ -1437,6 +1472,16 @@ gfors_status gfors_get_trace(gfors_ctx* C, double* rows, int64_t max_rows, int64
 
 const char* gfors_kernel_class_name(int32_t k) { return (k >= 0 && k < KC_N) ? kClassNames[k] : ""; }
 
+gfors_status gfors_profile_active(gfors_ctx* C, double* active_ms, double* active_launches, int32_t max_classes) {
+    if (!C) return GFORS_E_STATE;
+    if (C->prof_active_ms.empty()) return GFORS_E_STATE;
+    for (int k = 0; k < std::min<int>(KC_N, max_classes); ++k) {
+        active_ms[k] = C->prof_active_ms[k];
+        active_launches[k] = C->prof_active_n[k];
+    }
+    return GFORS_OK;
+}
+
 int64_t gfors_launches_per_block(gfors_ctx* C, const gfors_params* p) {
     if (!C || C->stage < 2) return -1;
     // count by enqueueing into a throwaway capture-free dry run: reuse the counter
@@ -1446,7 +1491,8 @@ int64_t gfors_launches_per_block(gfors_ctx* C, const gfors_params* p) {
     long long per_iter = 0;
     per_iter += C->m > 0 ? (C->pd.seg ? 2 : 1) : 0;
     per_iter += C->push_dual ? 2 : 0;
-    const bool spp = C->sparse_primal && (C->precision == 64 ? sparse_primal_smem<double>(C->m) : sparse_primal_smem<float>(C->m)) <= SP_DYN_MAX;
+    per_iter += C->push_primal ? 3 : 0;
+    const bool spp = C->sparse_primal && !C->push_primal && (C->precision == 64 ? sparse_primal_smem<double>(C->m) : sparse_primal_smem<float>(C->m)) <= SP_DYN_MAX;
     per_iter += spp ? 2 : (C->pp.seg ? 2 : 1);
     long long trig = (C->m > 0 ? (C->pd.seg ? 3 : (C->pd.rb ? 1 + (C->pd.nblk < C->nb1 ? 1 : 0) : 1)) : 1) + 1;
     long long eval = 0;
@@ -1485,10 +1531,13 @@ gfors_status gfors_profile_blocks(gfors_ctx* C, const gfors_params* p, int32_t b
     C->profiling = false;
     CK(cudaStreamSynchronize(C->stream));
     std::vector<double> sum(KC_N, 0.0);
+    C->prof_active_ms.assign(KC_N, 0.0);
+    C->prof_active_n.assign(KC_N, 0.0);
     for (auto& e : C->prof_ev) {
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, e.second.first, e.second.second));
         sum[e.first] += ms;
+        if (ms > 0.010f) { C->prof_active_ms[e.first] += ms; C->prof_active_n[e.first] += 1.0; }  // > 10 us: did work
         cudaEventDestroy(e.second.first);
         cudaEventDestroy(e.second.second);
     }

@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(256) k_push_rows(long long m, PushList pl, Sta
     const long long kk = iter_index(ctrl, kint, j);
     const int par = (int)(kk & 1);
     if (!push_mode(pl, par)) return;
-    if (blockIdx.x == 0 && threadIdx.x == 0) *pl.count[par ^ 1] = 0u;
+    if (blockIdx.x == 0 && threadIdx.x == 0) push_reset_next(pl, par);
     const T* __restrict__ yin = par ? s.y[1] : s.y[0];
     T* __restrict__ yout = par ? s.y[0] : s.y[1];
     const double tau2 = ctrl->tau2;

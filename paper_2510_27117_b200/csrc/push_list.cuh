@@ -13,7 +13,15 @@ struct PushList {
     unsigned thr;        // push mode iff count <= thr
     long long cap;       // list capacity (n)
     long long* acc;      // [m] int64 row accumulators, kept at 0 between uses
+    unsigned* pp_rcount;            // push-primal row list length, reset by the dual (or null)
+    unsigned long long* pp_wmax;    // push-primal max |w|, reset by the dual (or null)
 };
+
+// called by thread 0 of block 0 of whichever dual kernel is active this iteration
+__device__ __forceinline__ void push_reset_next(const PushList& pl, int par) {
+    *pl.count[par ^ 1] = 0u;
+    if (pl.pp_rcount) { *pl.pp_rcount = 0u; *pl.pp_wmax = 0ull; }
+}
 
 __device__ __forceinline__ bool push_mode(const PushList& pl, int par) {
     return pl.acc != nullptr && *(volatile unsigned*)pl.count[par] <= pl.thr;

@@ -1,0 +1,130 @@
+// push_primal.cuh — primal half-step from the nonzero duals ("push" mode).
+//
+// K'y = -K_u' w with w_j = g_j rsign_j y_j, and on covering-type instances most inequality duals sit
+// at the clamp y_j = 0 (config 5: 1 % / 7 % / 37 % nonzero after 100 / 500 / 2000 iterations).  When
+// few rows are active the product is computed from them: k_wlist lists the rows with w_j != 0 (and
+// the max |w|), k_push_scatter_cols adds w_j in fixed point (scale S = 2^e chosen from max|w| and the
+// largest column degree so no sum can overflow int64) into int64 column accumulators through the row
+// CSR with integer atomics — order-independent, hence deterministic — and k_primal_push applies the
+// box-projected update column by column (coalesced) and clears the accumulators.  With many active
+// rows the gather kernel (k_primal_rb) runs instead; the choice is made on the device from the list
+// length, every kernel of the unused mode exits at once.
+#pragma once
+#include "push_list.cuh"
+#include "rowblock.cuh"
+
+namespace gfors {
+
+struct PushPrimal {
+    int* rlist;                // rows with w_j != 0
+    unsigned* rcount;          // list length (reset by the dual of the same iteration)
+    unsigned rthr;             // push mode iff rcount <= rthr
+    unsigned long long* wmax;  // bit pattern of max |w_j| (non-negative doubles order like uint64)
+    long long* accx;           // [n] int64 column accumulators, kept at 0 between uses
+    int maxdeg;                // largest column degree of K_u (number of terms of any a_i)
+    long long m;
+};
+
+__device__ __forceinline__ bool pprimal_mode(const PushPrimal& pp) {
+    return pp.accx != nullptr && *(volatile unsigned*)pp.rcount <= pp.rthr;
+}
+
+// fixed-point scale 2^e with (max|w| * maxdeg) * 2^e < 2^62
+__device__ __forceinline__ double pprimal_scale(const PushPrimal& pp) {
+    const double wm = __longlong_as_double((long long)*(volatile unsigned long long*)pp.wmax);
+    if (!(wm > 0.0)) return 1.0;
+    int e;
+    frexp(wm * (double)pp.maxdeg, &e);  // wm*maxdeg < 2^e
+    return ldexp(1.0, 62 - e);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_wlist(const T* __restrict__ w, PushPrimal pp) {
+    __shared__ unsigned s_cnt, s_base;
+    __shared__ int s_list[256];
+    __shared__ double sh[32];
+    double mx = 0.0;
+    const long long m = pp.m;
+    const long long nbase = (m + 255) / 256;
+    for (long long bb = blockIdx.x; bb < nbase; bb += gridDim.x) {  // block-uniform trip count
+        const long long j = bb * 256 + threadIdx.x;
+        const double v = j < m ? (double)w[j] : 0.0;
+        mx = fmax(mx, fabs(v));
+        if (threadIdx.x == 0) s_cnt = 0u;
+        __syncthreads();
+        if (v != 0.0) s_list[atomicAdd(&s_cnt, 1u)] = (int)j;
+        __syncthreads();
+        if (threadIdx.x == 0) s_base = s_cnt ? atomicAdd(pp.rcount, s_cnt) : 0u;
+        __syncthreads();
+        for (unsigned t = threadIdx.x; t < s_cnt; t += 256)
+            if ((long long)s_base + t < m) pp.rlist[s_base + t] = s_list[t];
+        __syncthreads();
+    }
+    mx = block_max<256>(mx, sh);
+    if (threadIdx.x == 0 && mx > 0.0) atomicMax(pp.wmax, (unsigned long long)__double_as_longlong(mx));
+}
+
+// push mode: accx[i] += round(w_j * S) for every nonzero (j, i) of the listed rows
+template <typename T>
+__global__ void __launch_bounds__(256) k_push_scatter_cols(Csr K, PushPrimal pp, const T* __restrict__ w) {
+    if (!pprimal_mode(pp)) return;
+    const double S = pprimal_scale(pp);
+    const long long cnt = *pp.rcount;
+    // a warp per listed row: rows have 2..98 nonzeros on the set-cover workloads
+    const int lane = threadIdx.x & 31;
+    const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = (gridDim.x * (long long)blockDim.x) >> 5;
+    for (long long k = warp; k < cnt; k += nwarps) {
+        const int jr = pp.rlist[k];
+        const long long v = __double2ll_rn((double)w[jr] * S);
+        const long long q1 = __ldg(K.ptr + jr + 1);
+        for (long long q = __ldg(K.ptr + jr) + lane; q < q1; q += 32)
+            atomicAdd(reinterpret_cast<unsigned long long*>(pp.accx + __ldg(K.idx + q)), (unsigned long long)v);
+    }
+}
+
+// push mode: x_k = Pi(x_{k-1} - tau1 (c + rho - a + 2 Q x_{k-1} - 2 rho x_{k-1})), xbar_k = 2x_k - x_{k-1},
+// with a = accx / S; also hands the nonzero xbar columns to the next dual (PushList)
+template <typename T, bool HASQ>
+__global__ void __launch_bounds__(256) k_primal_push(long long n, PushPrimal pp, Csr Q, const T* __restrict__ qs,
+                                                     State<T> s, const T* __restrict__ cs, const Ctrl* __restrict__ ctrl,
+                                                     long long kint, long long j, PushList pl) {
+    __shared__ unsigned s_cnt, s_base;
+    __shared__ int s_list[256];
+    __shared__ bool s_en;
+    if (!pprimal_mode(pp)) return;
+    const double invS = 1.0 / pprimal_scale(pp);
+    const long long kk = iter_index(ctrl, kint, j);
+    const int par = (int)(kk & 1);
+    const T* __restrict__ xin = par ? s.x[1] : s.x[0];
+    T* __restrict__ xout = par ? s.x[0] : s.x[1];
+    T* __restrict__ xbout = par ? s.xb[0] : s.xb[1];
+    const double rho = ctrl->rho, tau1 = ctrl->tau1;
+    const long long nbase = (n + 255) / 256;
+    for (long long bb = blockIdx.x; bb < nbase; bb += gridDim.x) {  // block-uniform trip count
+        if (threadIdx.x == 0) s_en = pl.acc && *(volatile unsigned*)pl.count[par ^ 1] <= pl.thr;
+        const long long i = bb * 256 + threadIdx.x;
+        bool nz = false;
+        if (i < n) {
+            const long long ai = pp.accx[i];
+            if (ai) pp.accx[i] = 0;
+            const double a = (double)ai * invS;
+            double b = 0.0;
+            if constexpr (HASQ)
+                for (long long q = __ldg(Q.ptr + i); q < __ldg(Q.ptr + i + 1); ++q)
+                    b += (double)__ldg(qs + q) * (double)__ldg(xin + __ldg(Q.idx + q));
+            const double xi = (double)xin[i];
+            const double delta = (((double)cs[i] + rho) - a) + 2.0 * b - 2.0 * rho * xi;
+            double xn = xi - tau1 * delta;
+            xn = xn < 0.0 ? 0.0 : (xn > 1.0 ? 1.0 : xn);
+            xout[i] = (T)xn;
+            const T xbn = (T)(2.0 * xn - xi);
+            xbout[i] = xbn;
+            nz = xbn != (T)0;
+        }
+        __syncthreads();
+        push_append<256>(pl, par ^ 1, nz, (int)i, s_en, &s_cnt, &s_base, s_list);
+    }
+}
+
+}  // namespace gfors

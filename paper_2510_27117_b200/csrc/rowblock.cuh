@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(RB_NT) k_dual_rb(Csr K, const long long* __res
     const long long kk = iter_index(ctrl, kint, j);
     const int par = (int)(kk & 1);
     if (push_mode(pl, par)) return;  // sparse xbar: k_push_scatter/k_push_rows do this iteration
-    if (pl.acc && blockIdx.x == 0 && threadIdx.x == 0) *pl.count[par ^ 1] = 0u;
+    if (pl.acc && blockIdx.x == 0 && threadIdx.x == 0) push_reset_next(pl, par);
     const T* __restrict__ xb = par ? s.xb[1] : s.xb[0];
     const T* __restrict__ yin = par ? s.y[1] : s.y[0];
     T* __restrict__ yout = par ? s.y[0] : s.y[1];
@@ -172,11 +172,13 @@ template <typename T, int KIND, bool HASQ>
 __global__ void __launch_bounds__(RB_NT, 6) k_primal_rb(Csr Kt, const long long* __restrict__ blk_row, long long nblk,
                                                      Csr Q, const T* __restrict__ qs, State<T> s,
                                                      const T* __restrict__ cs, const Ctrl* __restrict__ ctrl,
-                                                     long long kint, long long j, PushList pl) {
+                                                     long long kint, long long j, PushList pl, const unsigned* pp_rcount,
+                                                     unsigned pp_rthr) {
     __shared__ __align__(16) T sv[2][RB_NNZ];
     __shared__ unsigned s_cnt, s_base;
     __shared__ int s_list[RB_NT];
     __shared__ bool s_en;
+    if (pp_rcount && *(volatile const unsigned*)pp_rcount <= pp_rthr) return;  // push-mode primal runs instead
     const long long kk = iter_index(ctrl, kint, j);
     const int par = (int)(kk & 1);
     const T* __restrict__ xin = par ? s.x[1] : s.x[0];

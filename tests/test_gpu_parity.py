@@ -371,3 +371,33 @@ def test_push_dual_variant_parity(gf, fam, monkeypatch):
     zg, _, _ = s.best_incumbent()
     zo, _ = o.best()
     assert zg == zo or (math.isinf(zg) and math.isinf(zo))
+
+
+@pytest.mark.parametrize("fam", ["setcover", "mis", "bqp"])
+@pytest.mark.parametrize("prec,tol", [(64, 1e-5), (32, 1e-3)])
+def test_push_primal_variant_parity(gf, fam, prec, tol, monkeypatch):
+    """Sparse-dual primal (fixed-point column scatter, forced on together with the push dual) against
+    the oracle: 1000 iterations within the north_star tolerance, same run accounting."""
+    monkeypatch.setenv("GFORS_PUSH_DUAL", "1")
+    monkeypatch.setenv("GFORS_PUSH_PRIMAL", "1")
+    inst = G.SMALL[fam](13)
+    s, _, o, _ = _pair(gf, inst, prec)
+    tau = math.sqrt(0.99)
+    rho = O.rho_schedule(1e-3, 10.0, 100.0, 2.0, 1e-6, 100)
+    o.state_init()
+    x0, xb0, y0 = o.get_state()
+    s.set_state(x0, xb0, y0)
+    for b in range(100):
+        s.step(10, rho[b], tau, tau)
+        for _ in range(10):
+            o.step(rho[b], tau, tau)
+    xg, _, yg = s.get_state()
+    xo, _, yo = o.get_state()
+    assert _rel(xg, xo) <= tol and _rel(yg, yo) <= tol
+    ig = s.run(max_iters=400)
+    io = o.run(max_iters=400)
+    assert ig["iters"] == io["iters"] and ig["rounds"] == io["rounds"]
+    if prec == 64:
+        zg, _, _ = s.best_incumbent()
+        zo, _ = o.best()
+        assert zg == zo or (math.isinf(zg) and math.isinf(zo))
