@@ -327,6 +327,7 @@ struct gfors_ctx {
     double* d_segpart = nullptr;
     double* d_segpart2 = nullptr;
     double* d_u = nullptr;  // K_u xbar of the block's last iteration (trigger pass, rb path)
+    unsigned char* d_ones = nullptr;  // per row: #entries with x_k == 1 at the last trigger (rb path)
     long long segpart_len = 0;
     // evaluator plan
     struct CountList {
@@ -440,7 +441,7 @@ void gfors_ctx::free_problem() {
 void gfors_ctx::free_prep() {
     void** ps[] = {(void**)&d_s, &d_g, &d_rh, &d_cs, &d_qs, &d_x[0], &d_x[1], &d_xb[0], &d_xb[1], &d_y[0], &d_y[1],
                    &d_w, (void**)&d_tmp[0], (void**)&d_tmp[1], (void**)&d_tmp[2], (void**)&d_tmp[3],
-                   (void**)&d_red, (void**)&d_scalar, (void**)&d_segpart, (void**)&d_segpart2, (void**)&d_u, (void**)&d_rec, (void**)&d_regen, (void**)&d_plist[0], (void**)&d_plist[1], (void**)&d_pcount, (void**)&d_acc, (void**)&d_rlist, (void**)&d_rcount, (void**)&d_wmax, (void**)&d_accx, (void**)&d_part1,
+                   (void**)&d_red, (void**)&d_scalar, (void**)&d_segpart, (void**)&d_segpart2, (void**)&d_u, (void**)&d_ones, (void**)&d_rec, (void**)&d_regen, (void**)&d_plist[0], (void**)&d_plist[1], (void**)&d_pcount, (void**)&d_acc, (void**)&d_rlist, (void**)&d_rcount, (void**)&d_wmax, (void**)&d_accx, (void**)&d_part1,
                    (void**)&d_part2, (void**)&d_hist, (void**)&d_rho, (void**)&d_trace, (void**)&d_xbest,
                    (void**)&d_X, (void**)&d_viol, (void**)&d_iacc, &d_zpart, (void**)&d_z, (void**)&d_ctrl};
     for (void** p : ps) { dfree(*p); *p = nullptr; }
@@ -677,7 +678,8 @@ void enqueue_trigger(gfors_ctx* C, cudaStream_t s, long long kint, long long j) 
             const int grid = (int)std::min<long long>(C->pd.nblk, (long long)C->nb1);
             KIND_SWITCH(C->kkind, LAUNCH(C, s, KC_TRIGR,
                 (k_trig_rows_rb<T, KINDV><<<grid, RB_NT, 0, s>>>(csr_K(C), C->pd.blk_row, C->pd.nblk, st, g, rh,
-                                                                 C->d_rsign, C->m1, C->d_u, ctrl, kint, j, C->d_part1))));
+                                                                 C->d_rsign, C->m1, C->d_u, ctrl, kint, j, C->d_part1,
+                                                                 C->d_ones))));
             if (grid < C->nb1)
                 LAUNCH(C, s, KC_TRIGR, (k_fill<<<1, NT, 0, s>>>(C->d_part1 + 3LL * grid, 3LL * (C->nb1 - grid), 0.0)));
         } else if (!C->pd.seg) {
@@ -713,7 +715,7 @@ int obj_vpj(const gfors_ctx* C, int W) {
 }
 
 // evaluation of the batch in d_X (W words per variable); viol/iacc must have been reset
-void enqueue_eval(gfors_ctx* C, cudaStream_t s, int W) {
+void enqueue_eval(gfors_ctx* C, cudaStream_t s, int W, const unsigned char* ones = nullptr) {
     const Csr K = csr_K(C);
     for (int li = 0; li < 3; ++li) {
         auto& cl = C->cnt[li];
@@ -723,9 +725,9 @@ void enqueue_eval(gfors_ctx* C, cudaStream_t s, int W) {
         const size_t sm = 0;
         const int wv = (W % 4 == 0) ? 4 : ((W % 2 == 0) ? 2 : 1);
 #define FEAS_WV(BM)                                                                                                \
-    if (wv == 4) { SUB_SWITCH(cl.sub, LAUNCH(C, s, KC_FEAS, (k_feas_count<BM, SUBV, 4><<<grid, NT, sm, s>>>(K, cr, C->d_X, W, C->d_viol)))); } \
-    else if (wv == 2) { SUB_SWITCH(cl.sub, LAUNCH(C, s, KC_FEAS, (k_feas_count<BM, SUBV, 2><<<grid, NT, sm, s>>>(K, cr, C->d_X, W, C->d_viol)))); } \
-    else { SUB_SWITCH(cl.sub, LAUNCH(C, s, KC_FEAS, (k_feas_count<BM, SUBV, 1><<<grid, NT, sm, s>>>(K, cr, C->d_X, W, C->d_viol)))); }
+    if (wv == 4) { SUB_SWITCH(cl.sub, LAUNCH(C, s, KC_FEAS, (k_feas_count<BM, SUBV, 4><<<grid, NT, sm, s>>>(K, cr, C->d_X, W, C->d_viol, ones)))); } \
+    else if (wv == 2) { SUB_SWITCH(cl.sub, LAUNCH(C, s, KC_FEAS, (k_feas_count<BM, SUBV, 2><<<grid, NT, sm, s>>>(K, cr, C->d_X, W, C->d_viol, ones)))); } \
+    else { SUB_SWITCH(cl.sub, LAUNCH(C, s, KC_FEAS, (k_feas_count<BM, SUBV, 1><<<grid, NT, sm, s>>>(K, cr, C->d_X, W, C->d_viol, ones)))); }
         if (li == 0) {
             FEAS_WV(1)
         } else if (li == 1) {
@@ -831,7 +833,8 @@ void enqueue_block(gfors_ctx* C, cudaStream_t s, const gfors_params* p, int W, H
     for (int r = 0; r < p->k_r; ++r) {
         enqueue_reset(C, s, W, ~0ull);
         enqueue_sample<T>(C, s, nullptr, W, word_off, p->seed, kint, r, p->k_r, 0u, 0);
-        enqueue_eval(C, s, W);
+        // the trigger pass of this block counted the p = 1 entries of every row (rb path)
+        enqueue_eval(C, s, W, (C->m > 0 && C->pd.rb && !getenv("GFORS_TRIG_CP")) ? C->d_ones : nullptr);
         if (C->sharded) {
             // record -> ncclAllGather -> identical merge on every rank -> regenerate the winner's bits
             LAUNCH(C, s, KC_ARGMIN, (k_local_record<<<1, NT, 0, s>>>(C->d_z, C->d_viol, 64LL * W, word_off, C->d_ctrl, C->d_rec)));
@@ -987,6 +990,7 @@ static void do_preprocess(gfors_ctx* C, const gfors_prep_opts* o, gfors_scaling*
     C->d_segpart = dalloc<double>(C->segpart_len);
     C->d_segpart2 = dalloc<double>(C->segpart_len);
     C->d_u = dalloc<double>(std::max<long long>(m, 1));
+    C->d_ones = dalloc<unsigned char>(std::max<long long>(m, 1));
     C->d_rec = dalloc<double>(4 + 4LL * C->world);
     if (C->push_dual) {
         C->d_plist[0] = dalloc<int>(n);

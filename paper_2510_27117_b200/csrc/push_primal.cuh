@@ -84,13 +84,17 @@ __global__ void __launch_bounds__(256) k_push_scatter_cols(Csr K, PushPrimal pp,
 }
 
 // push mode: x_k = Pi(x_{k-1} - tau1 (c + rho - a + 2 Q x_{k-1} - 2 rho x_{k-1})), xbar_k = 2x_k - x_{k-1},
-// with a = accx / S; also hands the nonzero xbar columns to the next dual (PushList)
+// with a = accx / S; also hands the nonzero xbar columns to the next dual (PushList).  Each thread
+// handles PP_U consecutive columns per pass so the block-staged append is amortised over
+// 256*PP_U columns.
+constexpr int PP_U = 4;
+
 template <typename T, bool HASQ>
 __global__ void __launch_bounds__(256) k_primal_push(long long n, PushPrimal pp, Csr Q, const T* __restrict__ qs,
                                                      State<T> s, const T* __restrict__ cs, const Ctrl* __restrict__ ctrl,
                                                      long long kint, long long j, PushList pl) {
     __shared__ unsigned s_cnt, s_base;
-    __shared__ int s_list[256];
+    __shared__ int s_list[256 * PP_U];
     __shared__ bool s_en;
     if (!pprimal_mode(pp)) return;
     const double invS = 1.0 / pprimal_scale(pp);
@@ -100,12 +104,16 @@ __global__ void __launch_bounds__(256) k_primal_push(long long n, PushPrimal pp,
     T* __restrict__ xout = par ? s.x[0] : s.x[1];
     T* __restrict__ xbout = par ? s.xb[0] : s.xb[1];
     const double rho = ctrl->rho, tau1 = ctrl->tau1;
-    const long long nbase = (n + 255) / 256;
+    const long long per = 256LL * PP_U;
+    const long long nbase = (n + per - 1) / per;
     for (long long bb = blockIdx.x; bb < nbase; bb += gridDim.x) {  // block-uniform trip count
-        if (threadIdx.x == 0) s_en = pl.acc && *(volatile unsigned*)pl.count[par ^ 1] <= pl.thr;
-        const long long i = bb * 256 + threadIdx.x;
-        bool nz = false;
-        if (i < n) {
+        if (threadIdx.x == 0) { s_en = pl.acc && *(volatile unsigned*)pl.count[par ^ 1] <= pl.thr; s_cnt = 0u; }
+        __syncthreads();
+        const bool en = s_en;
+#pragma unroll
+        for (int u = 0; u < PP_U; ++u) {
+            const long long i = bb * per + u * 256 + threadIdx.x;
+            if (i >= n) continue;
             const long long ai = pp.accx[i];
             if (ai) pp.accx[i] = 0;
             const double a = (double)ai * invS;
@@ -114,16 +122,23 @@ __global__ void __launch_bounds__(256) k_primal_push(long long n, PushPrimal pp,
                 for (long long q = __ldg(Q.ptr + i); q < __ldg(Q.ptr + i + 1); ++q)
                     b += (double)__ldg(qs + q) * (double)__ldg(xin + __ldg(Q.idx + q));
             const double xi = (double)xin[i];
-            const double delta = (((double)cs[i] + rho) - a) + 2.0 * b - 2.0 * rho * xi;
+            const double delta = (((double)__ldg(cs + i) + rho) - a) + 2.0 * b - 2.0 * rho * xi;
             double xn = xi - tau1 * delta;
             xn = xn < 0.0 ? 0.0 : (xn > 1.0 ? 1.0 : xn);
             xout[i] = (T)xn;
             const T xbn = (T)(2.0 * xn - xi);
             xbout[i] = xbn;
-            nz = xbn != (T)0;
+            if (en && xbn != (T)0) s_list[atomicAdd(&s_cnt, 1u)] = (int)i;
         }
         __syncthreads();
-        push_append<256>(pl, par ^ 1, nz, (int)i, s_en, &s_cnt, &s_base, s_list);
+        if (en) {
+            if (threadIdx.x == 0) s_base = s_cnt ? atomicAdd(pl.count[par ^ 1], s_cnt) : 0u;
+            __syncthreads();
+            const unsigned c = s_cnt, base = s_base;
+            for (unsigned t = threadIdx.x; t < c; t += 256)
+                if ((long long)base + t < pl.cap) pl.list[par ^ 1][base + t] = s_list[t];
+            __syncthreads();
+        }
     }
 }
 

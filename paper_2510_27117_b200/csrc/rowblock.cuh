@@ -243,7 +243,8 @@ __global__ void __launch_bounds__(RB_NT) k_trig_rows_rb(Csr K, const long long* 
                                                         const double* __restrict__ rh,
                                                         const signed char* __restrict__ rsign, long long m1,
                                                         const double* __restrict__ u_prev, const Ctrl* __restrict__ ctrl,
-                                                        long long kint, long long j, double* __restrict__ part1) {
+                                                        long long kint, long long j, double* __restrict__ part1,
+                                                        unsigned char* __restrict__ ones_out) {
     __shared__ __align__(16) T sv[2][RB_NNZ];
     __shared__ double sh[32];
     const long long kk = iter_index(ctrl, kint, j);
@@ -272,9 +273,18 @@ __global__ void __launch_bounds__(RB_NT) k_trig_rows_rb(Csr K, const long long* 
             const int rr = rb + grp;
             const long long row = r0 + rr;
             double v = 0.0;
-            if (rr < nr) v = rb_row_sum<T, KIND>(K, sv[st], p0, __ldg(K.ptr + row), __ldg(K.ptr + row + 1), lane, G);
+            int c1 = 0;  // entries of the row with x_k == 1 exactly (sampled as 1 in every lane)
+            if (rr < nr) {
+                const long long q0 = __ldg(K.ptr + row), q1 = __ldg(K.ptr + row + 1);
+                v = rb_row_sum<T, KIND>(K, sv[st], p0, q0, q1, lane, G);
+                if (ones_out)
+                    for (long long q = q0 + lane; q < q1; q += G) c1 += sv[st][q - p0] == (T)1;
+            }
             v = rb_group_sum(v, G);
+            if (ones_out)
+                for (int o = G >> 1; o > 0; o >>= 1) c1 += __shfl_xor_sync(0xffffffffu, c1, o, G);
             if (lane == 0 && rr < nr) {
+                if (ones_out) ones_out[row] = (unsigned char)min(c1, 255);
                 const double sg = (KIND == KV_SIGN) ? (double)rsign[row] : 1.0;
                 const double gj = g[row];
                 const double ku = sg * v;  // (K_u x_k)_j

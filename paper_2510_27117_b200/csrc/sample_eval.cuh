@@ -125,6 +125,7 @@ __device__ __forceinline__ void csa_add_counter(uint64_t (&C)[BMAX], uint64_t& s
 template <int BMAX>
 __device__ __forceinline__ uint64_t count_ok(const uint64_t (&C)[BMAX], uint64_t sat, int B, int t, int rel) {
     if (rel == 3) return 0ull;
+    if (rel == 4) return ~0ull;  // satisfied in every lane by variables sampled with p = 1
     uint64_t gt = 0ull, eq = ~0ull;
 #pragma unroll
     for (int q = BMAX - 1; q >= 0; --q)
@@ -155,7 +156,8 @@ __device__ __forceinline__ void load_words(const uint64_t* __restrict__ p, uint6
 // vector load, so a covering row over 128 candidates costs one 16-byte gather per nonzero.
 template <int BMAX, int SUB, int WV>
 __global__ void __launch_bounds__(256) k_feas_count(Csr K, CountRows cr, const uint64_t* __restrict__ X, int W,
-                                                    unsigned long long* __restrict__ viol) {
+                                                    unsigned long long* __restrict__ viol,
+                                                    const unsigned char* __restrict__ ones) {
     __shared__ unsigned long long s_viol[64];  // block-aggregated violations when W <= 64
     const bool use_smem = W <= 64;
     if (use_smem)
@@ -175,6 +177,9 @@ __global__ void __launch_bounds__(256) k_feas_count(Csr K, CountRows cr, const u
             const int row = cr.row[e];
             p0 = __ldg(K.ptr + row); p1 = __ldg(K.ptr + row + 1);
             B = cr.B[e]; t = cr.t[e]; rel = cr.rel[e];
+            // ones[row] = #variables of the row with p = 1 (all-ones sample words): a ">= t" row already
+            // holding t of them is satisfied in every lane — no gathers
+            if (ones && rel == 0 && (int)ones[row] >= t) { rel = 4; p1 = p0; }
         }
         for (int w0 = 0; w0 < W; w0 += WV) {
             uint64_t C[WV][BMAX];
@@ -185,7 +190,7 @@ __global__ void __launch_bounds__(256) k_feas_count(Csr K, CountRows cr, const u
 #pragma unroll
                 for (int q = 0; q < BMAX; ++q) C[u][q] = 0ull;
             }
-            if (rel != 3)
+            if (rel < 3)
                 for (long long p = p0 + lane; p < p1; p += SUB) {
                     uint64_t v[WV];
                     load_words<WV>(X + (long long)__ldg(K.idx + p) * W + w0, v);
