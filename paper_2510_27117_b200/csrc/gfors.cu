@@ -319,6 +319,9 @@ struct gfors_ctx {
     unsigned* d_rcount = nullptr;
     unsigned long long* d_wmax = nullptr;
     long long* d_accx = nullptr;
+    long long* d_accv = nullptr;       // [m] pushed K_u x_k (trigger)
+    unsigned* d_ones_cnt = nullptr;    // [m] pushed #(x_k == 1) per row (trigger)
+    unsigned* d_trig_flag = nullptr;
     int maxcoldeg = 0;
     unsigned push_thr = 0;
     int* d_plist[2] = {nullptr, nullptr};
@@ -441,7 +444,7 @@ void gfors_ctx::free_problem() {
 void gfors_ctx::free_prep() {
     void** ps[] = {(void**)&d_s, &d_g, &d_rh, &d_cs, &d_qs, &d_x[0], &d_x[1], &d_xb[0], &d_xb[1], &d_y[0], &d_y[1],
                    &d_w, (void**)&d_tmp[0], (void**)&d_tmp[1], (void**)&d_tmp[2], (void**)&d_tmp[3],
-                   (void**)&d_red, (void**)&d_scalar, (void**)&d_segpart, (void**)&d_segpart2, (void**)&d_u, (void**)&d_ones, (void**)&d_rec, (void**)&d_regen, (void**)&d_plist[0], (void**)&d_plist[1], (void**)&d_pcount, (void**)&d_acc, (void**)&d_rlist, (void**)&d_rcount, (void**)&d_wmax, (void**)&d_accx, (void**)&d_part1,
+                   (void**)&d_red, (void**)&d_scalar, (void**)&d_segpart, (void**)&d_segpart2, (void**)&d_u, (void**)&d_ones, (void**)&d_rec, (void**)&d_regen, (void**)&d_plist[0], (void**)&d_plist[1], (void**)&d_pcount, (void**)&d_acc, (void**)&d_rlist, (void**)&d_rcount, (void**)&d_wmax, (void**)&d_accx, (void**)&d_accv, (void**)&d_ones_cnt, (void**)&d_trig_flag, (void**)&d_part1,
                    (void**)&d_part2, (void**)&d_hist, (void**)&d_rho, (void**)&d_trace, (void**)&d_xbest,
                    (void**)&d_X, (void**)&d_viol, (void**)&d_iacc, &d_zpart, (void**)&d_z, (void**)&d_ctrl};
     for (void** p : ps) { dfree(*p); *p = nullptr; }
@@ -574,14 +577,18 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
     const T* cs = (const T*)C->d_cs;
     // K' values: SIGN rows fold the sign into w, so the transpose carries no values
     const int tkind = C->kkind;
+    // trigger iteration of a loop block: the push-mode primal also pushes x_k for the indicator pass
+    const bool trig_push = C->push_primal && kint > 0 && j == kint - 1;
     if (C->push_primal) {
         // list the active duals; the push kernels run iff the list is short, else k_primal_rb below
         LAUNCH(C, s, KC_PRIMAL_PUSH, (k_wlist<T><<<grid_for(C->m), NT, 0, s>>>(st.w, ppr)));
         LAUNCH(C, s, KC_PRIMAL_PUSH, (k_push_scatter_cols<T><<<grid_for(C->m * 32LL), NT, 0, s>>>(csr_K(C), ppr, st.w)));
         if (C->hasq)
-            LAUNCH(C, s, KC_PRIMAL_PUSH, (k_primal_push<T, true><<<grid_for(C->n), NT, 0, s>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl)));
+            LAUNCH(C, s, KC_PRIMAL_PUSH, (k_primal_push<T, true><<<grid_for(C->n), NT, 0, s>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
+                csr_Kt(C), trig_push ? C->d_accv : nullptr, C->d_ones_cnt, C->d_trig_flag)));
         else
-            LAUNCH(C, s, KC_PRIMAL_PUSH, (k_primal_push<T, false><<<grid_for(C->n), NT, 0, s>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl)));
+            LAUNCH(C, s, KC_PRIMAL_PUSH, (k_primal_push<T, false><<<grid_for(C->n), NT, 0, s>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
+                csr_Kt(C), trig_push ? C->d_accv : nullptr, C->d_ones_cnt, C->d_trig_flag)));
     }
     if (C->sparse_primal && !C->push_primal && sparse_primal_smem<T>(C->m) <= SP_DYN_MAX) {
         const long long nwords = (C->m + 31) / 32;
@@ -679,9 +686,15 @@ void enqueue_trigger(gfors_ctx* C, cudaStream_t s, long long kint, long long j) 
             KIND_SWITCH(C->kkind, LAUNCH(C, s, KC_TRIGR,
                 (k_trig_rows_rb<T, KINDV><<<grid, RB_NT, 0, s>>>(csr_K(C), C->pd.blk_row, C->pd.nblk, st, g, rh,
                                                                  C->d_rsign, C->m1, C->d_u, ctrl, kint, j, C->d_part1,
-                                                                 C->d_ones))));
+                                                                 C->d_ones, C->push_primal ? C->d_trig_flag : nullptr))));
             if (grid < C->nb1)
                 LAUNCH(C, s, KC_TRIGR, (k_fill<<<1, NT, 0, s>>>(C->d_part1 + 3LL * grid, 3LL * (C->nb1 - grid), 0.0)));
+            if (C->push_primal) {
+                // x_k pushed by the trigger iteration's primal: gather-free pass over the rows (writes all nb1 partials)
+                LAUNCH(C, s, KC_TRIGR, (k_trig_rows_push<T><<<C->nb1, NT, 0, s>>>(C->m, st, g, rh, C->d_rsign, C->m1, C->d_u,
+                    ctrl, kint, j, C->d_part1, C->d_ones, C->d_accv, C->d_ones_cnt, C->d_trig_flag)));
+                LAUNCH(C, s, KC_TRIGR, (k_trig_clear<<<1, 1, 0, s>>>(C->d_trig_flag)));
+            }
         } else if (!C->pd.seg) {
             KIND_SWITCH(C->kkind, SUB_SWITCH(C->pd.sub, LAUNCH(C, s, KC_TRIGR,
                 (k_trig_rows<T, KINDV, SUBV, false><<<C->nb1, NT, 0, s>>>(csr_K(C), C->pd.ds.plan(), nullptr, nullptr,
@@ -1008,6 +1021,12 @@ static void do_preprocess(gfors_ctx* C, const gfors_prep_opts* o, gfors_scaling*
         CK(cudaMemsetAsync(C->d_rcount, 0xff, sizeof(unsigned), s));
         CK(cudaMemsetAsync(C->d_wmax, 0, sizeof(unsigned long long), s));
         CK(cudaMemsetAsync(C->d_accx, 0, n * sizeof(long long), s));
+        C->d_accv = dalloc<long long>(std::max<long long>(m, 1));
+        C->d_ones_cnt = dalloc<unsigned>(std::max<long long>(m, 1));
+        C->d_trig_flag = dalloc<unsigned>(1);
+        CK(cudaMemsetAsync(C->d_accv, 0, std::max<long long>(m, 1) * sizeof(long long), s));
+        CK(cudaMemsetAsync(C->d_ones_cnt, 0, std::max<long long>(m, 1) * sizeof(unsigned), s));
+        CK(cudaMemsetAsync(C->d_trig_flag, 0, sizeof(unsigned), s));
     }
     C->d_regen = dalloc<long long>(2);
     C->d_ctrl = dalloc<Ctrl>(1);
@@ -1498,7 +1517,7 @@ int64_t gfors_launches_per_block(gfors_ctx* C, const gfors_params* p) {
     per_iter += C->push_primal ? 3 : 0;
     const bool spp = C->sparse_primal && !C->push_primal && (C->precision == 64 ? sparse_primal_smem<double>(C->m) : sparse_primal_smem<float>(C->m)) <= SP_DYN_MAX;
     per_iter += spp ? 2 : (C->pp.seg ? 2 : 1);
-    long long trig = (C->m > 0 ? (C->pd.seg ? 3 : (C->pd.rb ? 1 + (C->pd.nblk < C->nb1 ? 1 : 0) : 1)) : 1) + 1;
+    long long trig = (C->m > 0 ? (C->pd.seg ? 3 : (C->pd.rb ? 1 + (C->pd.nblk < C->nb1 ? 1 : 0) + (C->push_primal ? 2 : 0) : 1)) : 1) + 1;
     long long eval = 0;
     for (auto& cl : C->cnt) eval += cl.nrows ? 1 : 0;
     eval += C->n_int ? 2 : 0;

@@ -92,11 +92,15 @@ constexpr int PP_U = 4;
 template <typename T, bool HASQ>
 __global__ void __launch_bounds__(256) k_primal_push(long long n, PushPrimal pp, Csr Q, const T* __restrict__ qs,
                                                      State<T> s, const T* __restrict__ cs, const Ctrl* __restrict__ ctrl,
-                                                     long long kint, long long j, PushList pl) {
+                                                     long long kint, long long j, PushList pl, Csr Kt,
+                                                     long long* __restrict__ accv, unsigned* __restrict__ ones_cnt,
+                                                     unsigned* __restrict__ trig_flag) {
     __shared__ unsigned s_cnt, s_base;
     __shared__ int s_list[256 * PP_U];
     __shared__ bool s_en;
     if (!pprimal_mode(pp)) return;
+    // trigger iteration: also push x_k into the row accumulators of the indicator pass (k_trig_rows_push)
+    if (accv && blockIdx.x == 0 && threadIdx.x == 0) *trig_flag = 1u;
     const double invS = 1.0 / pprimal_scale(pp);
     const long long kk = iter_index(ctrl, kint, j);
     const int par = (int)(kk & 1);
@@ -125,10 +129,21 @@ __global__ void __launch_bounds__(256) k_primal_push(long long n, PushPrimal pp,
             const double delta = (((double)__ldg(cs + i) + rho) - a) + 2.0 * b - 2.0 * rho * xi;
             double xn = xi - tau1 * delta;
             xn = xn < 0.0 ? 0.0 : (xn > 1.0 ? 1.0 : xn);
-            xout[i] = (T)xn;
+            const T xk = (T)xn;
+            xout[i] = xk;
             const T xbn = (T)(2.0 * xn - xi);
             xbout[i] = xbn;
             if (en && xbn != (T)0) s_list[atomicAdd(&s_cnt, 1u)] = (int)i;
+            if (accv && xk != (T)0) {
+                const long long v = __double2ll_rn((double)xk * 1099511627776.0);  // 2^40 fixed point
+                const bool one = xk == (T)1;
+                const long long q1 = __ldg(Kt.ptr + i + 1);
+                for (long long q = __ldg(Kt.ptr + i); q < q1; ++q) {
+                    const int r = __ldg(Kt.idx + q);
+                    atomicAdd(reinterpret_cast<unsigned long long*>(accv + r), (unsigned long long)v);
+                    if (one) atomicAdd(ones_cnt + r, 1u);
+                }
+            }
         }
         __syncthreads();
         if (en) {
@@ -141,5 +156,47 @@ __global__ void __launch_bounds__(256) k_primal_push(long long n, PushPrimal pp,
         }
     }
 }
+
+// Trigger row pass from the pushed x_k (no gathers): v_j = (K_u x_k)_j from the fixed-point row
+// accumulators, d_j = v_j - (K_u xbar_{k-1})_j; same partial layout as k_trig_rows_rb.  Runs iff the
+// primal of the trigger iteration pushed (trig_flag), clears accumulators and flag.  +-1 rows.
+template <typename T>
+__global__ void __launch_bounds__(256) k_trig_rows_push(long long m, State<T> s, const double* __restrict__ g,
+                                                        const double* __restrict__ rh,
+                                                        const signed char* __restrict__ rsign, long long m1,
+                                                        const double* __restrict__ u_prev, const Ctrl* __restrict__ ctrl,
+                                                        long long kint, long long j, double* __restrict__ part1,
+                                                        unsigned char* __restrict__ ones_out, long long* __restrict__ accv,
+                                                        unsigned* __restrict__ ones_cnt, unsigned* __restrict__ trig_flag) {
+    __shared__ double sh[32];
+    if (*(volatile unsigned*)trig_flag == 0u) return;
+    const long long kk = iter_index(ctrl, kint, j);
+    const int par = (int)(kk & 1);
+    const T* __restrict__ yprev = par ? s.y[1] : s.y[0];
+    const T* __restrict__ ynew = par ? s.y[0] : s.y[1];
+    const double tau2 = ctrl->tau2;
+    double ge = 0.0, eq = 0.0, sy2 = 0.0;
+    for (long long row = blockIdx.x * (long long)blockDim.x + threadIdx.x; row < m; row += gridDim.x * (long long)blockDim.x) {
+        const long long a = accv[row];
+        if (a) accv[row] = 0;
+        const unsigned c1 = ones_cnt[row];
+        if (c1) ones_cnt[row] = 0u;
+        if (ones_out) ones_out[row] = (unsigned char)min(c1, 255u);
+        const double sg = (double)rsign[row];
+        const double gj = g[row];
+        const double ku = sg * ((double)a * (1.0 / 1099511627776.0));  // (K_u x_k)_j
+        const double gap = rh[row] - gj * ku;
+        if (row < m1) ge = fmax(ge, fmax(gap, 0.0)); else eq = fmax(eq, fabs(gap));
+        const double sy = ((double)yprev[row] - (double)ynew[row]) / tau2 + gj * (ku - u_prev[row]);
+        sy2 += sy * sy;
+    }
+    const double aa = block_max<256>(ge, sh);
+    const double bb = block_max<256>(eq, sh);
+    const double cc = block_sum<256>(sy2, sh);
+    if (threadIdx.x == 0) { part1[3 * blockIdx.x] = aa; part1[3 * blockIdx.x + 1] = bb; part1[3 * blockIdx.x + 2] = cc; }
+    // every block has read the flag at entry (it is cleared only by a later kernel: k_trig_clear)
+}
+
+__global__ void k_trig_clear(unsigned* trig_flag) { *trig_flag = 0u; }
 
 }  // namespace gfors

@@ -244,9 +244,11 @@ __global__ void __launch_bounds__(RB_NT) k_trig_rows_rb(Csr K, const long long* 
                                                         const signed char* __restrict__ rsign, long long m1,
                                                         const double* __restrict__ u_prev, const Ctrl* __restrict__ ctrl,
                                                         long long kint, long long j, double* __restrict__ part1,
-                                                        unsigned char* __restrict__ ones_out) {
+                                                        unsigned char* __restrict__ ones_out,
+                                                        const unsigned* __restrict__ trig_flag) {
     __shared__ __align__(16) T sv[2][RB_NNZ];
     __shared__ double sh[32];
+    if (trig_flag && *(volatile const unsigned*)trig_flag) return;  // x_k was pushed: k_trig_rows_push
     const long long kk = iter_index(ctrl, kint, j);
     const int par = (int)(kk & 1);
     const T* __restrict__ xk = par ? s.x[0] : s.x[1];
