@@ -28,7 +28,6 @@
 #include "prep.cuh"
 #include "sample_eval.cuh"
 #include "rowblock.cuh"
-#include "trig.cuh"
 #include "sparse_primal.cuh"
 #include "shard.cuh"
 #include "push_dual.cuh"
@@ -128,8 +127,7 @@ struct DevSeg {
 struct DirPlan {  // how one product direction (K rows or K' columns) is computed
     int sub = 32;
     bool seg = false;        // long rows: fixed-length segments + ordered combine
-    bool rb = false;         // row blocks of <= RB_NNZ nonzeros per CTA
-    bool wrb = false;        // warp row blocks of <= WRB_NNZ nonzeros (default for short rows)
+    bool rb = false;         // row blocks of <= RB_NNZ_OF<T> nonzeros per CTA
     long long seg_len = 1024;
     DevSeg ds;
     long long* blk_row = nullptr;
@@ -165,12 +163,7 @@ DirPlan plan_direction(const std::vector<int64_t>& ptr, long long rows, cudaStre
     d.seg = (maxlen > 4096) || (groups * 32 < (long long)NUM_SMS_B200 * 2048 && nnz > (long long)NUM_SMS_B200 * 1024);
     const char* force = getenv("GFORS_SPMV");
     const std::string fm = force ? force : "";
-    // warp-level row blocks measured slower than CTA row blocks on config 5 (276 vs 259 us per
-    // dual launch); kept behind GFORS_SPMV=wrb for experiments
-    if (maxlen <= WRB_NNZ && fm == "wrb") {
-        d.seg = false;
-        d.wrb = true;
-    } else if (maxlen <= RB_NNZ && fm != "short" && fm != "seg") {
+    if (maxlen <= RB_NNZ32 && fm != "short" && fm != "seg") {
         d.seg = false;
         d.rb = true;
     } else if (fm == "short" && maxlen <= 4096) {
@@ -178,8 +171,8 @@ DirPlan plan_direction(const std::vector<int64_t>& ptr, long long rows, cudaStre
     } else if (fm == "seg") {
         d.seg = true;
     }
-    if (d.rb || d.wrb) {
-        std::vector<long long> b = make_rowblocks(ptr, rows, d.wrb ? WRB_NNZ : RB_NNZ);
+    if (d.rb) {
+        std::vector<long long> b = make_rowblocks(ptr, rows, RB_NNZ32);
         d.nblk = (long long)b.size() - 1;
         d.blk_row = dupload(b, s);
         owned.push_back(d.blk_row);
@@ -197,6 +190,26 @@ DirPlan plan_direction(const std::vector<int64_t>& ptr, long long rows, cudaStre
         owned.push_back(d.ds.seg_row);
         owned.push_back(d.ds.row_seg);
     }
+    return d;
+}
+
+// the fp64 plan: row blocks of <= RB_NNZ64 nonzeros; rows longer than that take the short-row kernels
+DirPlan plan_direction64(const DirPlan& d32, const std::vector<int64_t>& ptr, long long rows, cudaStream_t s,
+                         std::vector<void*>& owned) {
+    DirPlan d = d32;
+    if (!d32.rb) return d;
+    long long maxlen = 0;
+    for (long long r = 0; r < rows; ++r) maxlen = std::max<long long>(maxlen, ptr[r + 1] - ptr[r]);
+    if (maxlen > RB_NNZ64) {
+        d.rb = false;
+        d.blk_row = nullptr;
+        d.nblk = 0;
+        return d;
+    }
+    std::vector<long long> b = make_rowblocks(ptr, rows, RB_NNZ64);
+    d.nblk = (long long)b.size() - 1;
+    d.blk_row = dupload(b, s);
+    owned.push_back(d.blk_row);
     return d;
 }
 
@@ -307,7 +320,9 @@ struct gfors_ctx {
     void *d_kval = nullptr, *d_ktval = nullptr;
     double *d_qval = nullptr, *d_c = nullptr, *d_ru = nullptr;
     signed char* d_rsign = nullptr;
-    DirPlan pd, pp;  // dual (rows of K), primal (rows of K')
+    DirPlan pd, pp;  // dual (rows of K), primal (rows of K') for the preprocessed precision
+    DirPlan pdv[2], ppv[2];  // [0] fp32, [1] fp64 plans (row-block size differs)
+    bool push_dual_ok = false, push_primal_ok = false;  // push modes allowed by the matrix
     bool sparse_primal = false;     // primal skips gathers of zero duals (sparse_primal.cuh)
     long long* sp_blk_row = nullptr;
     long long sp_nblk = 0;
@@ -541,12 +556,7 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
     const double* g = (const double*)C->d_g;
     const double* rh = (const double*)C->d_rh;
     if (C->m > 0) {
-        if (C->pd.wrb) {
-            const int grid = (int)std::min<long long>((C->pd.nblk + WRB_WARPS - 1) / WRB_WARPS, RB_GRID);
-            KIND_SWITCH(C->kkind, LAUNCH(C, s, KC_DUAL,
-                (k_dual_wrb<T, KINDV><<<grid, 32 * WRB_WARPS, 0, s>>>(csr_K(C), C->pd.blk_row, C->pd.nblk, st, g, rh,
-                                                                      C->d_rsign, C->m1, ctrl, kint, j))));
-        } else if (C->pd.rb) {
+        if (C->pd.rb) {
             const int grid = (int)std::min<long long>(C->pd.nblk, RB_GRID);
             KIND_SWITCH(C->kkind, LAUNCH(C, s, KC_DUAL,
                 (k_dual_rb<T, KINDV><<<grid, RB_NT, 0, s>>>(csr_K(C), C->pd.blk_row, C->pd.nblk, st, g, rh, C->d_rsign,
@@ -610,17 +620,6 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
                     C->d_nzbits, nwords, Q, qs, st, cs, ctrl, kint, j, pl)));
             });
         }
-    } else if (C->pp.wrb) {
-        const int grid = (int)std::min<long long>((C->pp.nblk + WRB_WARPS - 1) / WRB_WARPS, RB_GRID);
-        if (C->hasq) {
-            KIND_SWITCH(tkind, LAUNCH(C, s, KC_PRIMAL,
-                (k_primal_wrb<T, KINDV, true><<<grid, 32 * WRB_WARPS, 0, s>>>(csr_Kt(C), C->pp.blk_row, C->pp.nblk, Q, qs,
-                                                                              st, cs, ctrl, kint, j))));
-        } else {
-            KIND_SWITCH(tkind, LAUNCH(C, s, KC_PRIMAL,
-                (k_primal_wrb<T, KINDV, false><<<grid, 32 * WRB_WARPS, 0, s>>>(csr_Kt(C), C->pp.blk_row, C->pp.nblk, Q, qs,
-                                                                               st, cs, ctrl, kint, j))));
-        }
     } else if (C->pp.rb) {
         const int grid = (int)std::min<long long>(C->pp.nblk, RB_GRID);
         if (C->hasq) {
@@ -666,22 +665,7 @@ void enqueue_trigger(gfors_ctx* C, cudaStream_t s, long long kint, long long j) 
     const double* g = (const double*)C->d_g;
     const double* rh = (const double*)C->d_rh;
     if (C->m > 0) {
-        if (C->pd.rb && getenv("GFORS_TRIG_CP")) {  // cp.async variant: measured slower (1.01 vs 0.65 ms)
-            const int grid = (int)std::min<long long>(C->pd.nblk, (long long)C->nb1);
-            KIND_SWITCH(C->kkind, {
-                const size_t sm = trig_cp_smem<T, KINDV>();
-                static bool attr_set = false;  // per template instantiation
-                if (!attr_set) {
-                    CK(cudaFuncSetAttribute(k_trig_rows_cp<T, KINDV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-                    attr_set = true;
-                }
-                LAUNCH(C, s, KC_TRIGR,
-                    (k_trig_rows_cp<T, KINDV><<<grid, RB_NT, sm, s>>>(csr_K(C), C->pd.blk_row, C->pd.nblk, st, g, rh,
-                                                                      C->d_rsign, C->m1, ctrl, kint, j, C->d_part1)));
-            });
-            if (grid < C->nb1)
-                LAUNCH(C, s, KC_TRIGR, (k_fill<<<1, NT, 0, s>>>(C->d_part1 + 3LL * grid, 3LL * (C->nb1 - grid), 0.0)));
-        } else if (C->pd.rb) {
+        if (C->pd.rb) {
             const int grid = (int)std::min<long long>(C->pd.nblk, (long long)C->nb1);
             KIND_SWITCH(C->kkind, LAUNCH(C, s, KC_TRIGR,
                 (k_trig_rows_rb<T, KINDV><<<grid, RB_NT, 0, s>>>(csr_K(C), C->pd.blk_row, C->pd.nblk, st, g, rh,
@@ -847,7 +831,7 @@ void enqueue_block(gfors_ctx* C, cudaStream_t s, const gfors_params* p, int W, H
         enqueue_reset(C, s, W, ~0ull);
         enqueue_sample<T>(C, s, nullptr, W, word_off, p->seed, kint, r, p->k_r, 0u, 0);
         // the trigger pass of this block counted the p = 1 entries of every row (rb path)
-        enqueue_eval(C, s, W, (C->m > 0 && C->pd.rb && !getenv("GFORS_TRIG_CP")) ? C->d_ones : nullptr);
+        enqueue_eval(C, s, W, (C->m > 0 && C->pd.rb) ? C->d_ones : nullptr);
         if (C->sharded) {
             // record -> ncclAllGather -> identical merge on every rank -> regenerate the winner's bits
             LAUNCH(C, s, KC_ARGMIN, (k_local_record<<<1, NT, 0, s>>>(C->d_z, C->d_viol, 64LL * W, word_off, C->d_ctrl, C->d_rec)));
@@ -936,6 +920,15 @@ static double power_iteration(gfors_ctx* C, bool isq, double tol, int max_iter) 
     return sigma;
 }
 
+// the product plans and push modes of the preprocessed precision (row-block size is per precision)
+static void select_plans(gfors_ctx* C) {
+    const int v = C->precision == 64 ? 1 : 0;
+    C->pd = C->pdv[v];
+    C->pp = C->ppv[v];
+    C->push_dual = C->push_dual_ok && C->pd.rb && C->pp.rb;
+    C->push_primal = C->push_primal_ok && C->push_dual;
+}
+
 template <typename T>
 static void alloc_loop_data(gfors_ctx* C) {
     const long long n = C->n, m = C->m;
@@ -993,6 +986,7 @@ static void do_preprocess(gfors_ctx* C, const gfors_prep_opts* o, gfors_scaling*
     const double kap = m ? power_iteration(C, false, o->tol, o->max_iter) : 0.0;
     C->kappa = kap > 0.0 ? kap : 1.0;
     C->precision = o->precision;
+    select_plans(C);
     if (C->precision == 64) alloc_loop_data<double>(C); else alloc_loop_data<float>(C);
     // loop workspaces
     C->nb1 = 1024;

@@ -20,9 +20,16 @@
 
 namespace gfors {
 
-constexpr int RB_NNZ = 2048;  // nonzeros per row block (8 per thread)
+// Nonzeros per row block: 2048 (8 per thread) for fp32, 1024 for fp64.  The double-buffered
+// gather tile takes 2*RB_NNZ*sizeof(T) of shared memory per CTA and the rest of the SM's 256 KB
+// L1/shared array is the L1 that tracks the in-flight gathers: at 32 KB per CTA (fp64, 2048) the
+// carve-out leaves too few L1 lines and the gather rate halves (measured: 0.42 vs 0.87 gathers per
+// cycle per SM, scratch microbenchmark), at 16 KB it does not (config 5 fp64 dual 0.47 -> 0.27 ms).
+constexpr int RB_NNZ32 = 2048;
+constexpr int RB_NNZ64 = 1024;
 constexpr int RB_NT = 256;
-constexpr int RB_U = RB_NNZ / RB_NT;
+template <typename T>
+constexpr int RB_NNZ_OF = sizeof(T) == 8 ? RB_NNZ64 : RB_NNZ32;
 
 __device__ __forceinline__ int ldcs_i32(const int* p) { return __ldcs(p); }
 
@@ -37,26 +44,27 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 
 // phase 1 of row block b, split in two so the index loads of block b+2*grid are in flight while
 // block b is reduced: rb_load_idx (registers, evict-first) then rb_issue (cp.async gathers)
+template <int U>
 __device__ __forceinline__ void rb_load_idx(const Csr& A, const long long* __restrict__ blk_row, long long b,
-                                            long long nblk, int (&cols)[RB_U]) {
+                                            long long nblk, int (&cols)[U]) {
     if (b < nblk) {
         const long long p0 = __ldg(A.ptr + blk_row[b]);
         const int cnt = (int)(__ldg(A.ptr + blk_row[b + 1]) - p0);
 #pragma unroll
-        for (int u = 0; u < RB_U; ++u) {
+        for (int u = 0; u < U; ++u) {
             const int t = u * RB_NT + threadIdx.x;
             cols[u] = t < cnt ? ldcs_i32(A.idx + p0 + t) : -1;
         }
     } else {
 #pragma unroll
-        for (int u = 0; u < RB_U; ++u) cols[u] = -1;
+        for (int u = 0; u < U; ++u) cols[u] = -1;
     }
 }
 
-template <typename T>
-__device__ __forceinline__ void rb_issue(const int (&cols)[RB_U], const T* __restrict__ v, T* sv) {
+template <typename T, int U>
+__device__ __forceinline__ void rb_issue(const int (&cols)[U], const T* __restrict__ v, T* sv) {
 #pragma unroll
-    for (int u = 0; u < RB_U; ++u)
+    for (int u = 0; u < U; ++u)
         if (cols[u] >= 0) cp_async_elem(sv + u * RB_NT + threadIdx.x, v + cols[u]);
     cp_async_commit();
 }
@@ -117,7 +125,8 @@ __global__ void __launch_bounds__(RB_NT) k_dual_rb(Csr K, const long long* __res
                                                    const double* __restrict__ rh, const signed char* __restrict__ rsign,
                                                    long long m1, const Ctrl* __restrict__ ctrl, long long kint,
                                                    long long j, double* __restrict__ u_out, PushList pl) {
-    __shared__ __align__(16) T sv[2][RB_NNZ];
+    constexpr int NZ = RB_NNZ_OF<T>;
+    __shared__ __align__(16) T sv[2][NZ];
     const long long kk = iter_index(ctrl, kint, j);
     const int par = (int)(kk & 1);
     if (push_mode(pl, par)) return;  // sparse xbar: k_push_scatter/k_push_rows do this iteration
@@ -127,12 +136,12 @@ __global__ void __launch_bounds__(RB_NT) k_dual_rb(Csr K, const long long* __res
     T* __restrict__ yout = par ? s.y[0] : s.y[1];
     const double tau2 = ctrl->tau2;
     int st = 0;
-    int nxt[RB_U];
+    int nxt[NZ / RB_NT];
     rb_load_idx(K, blk_row, blockIdx.x, nblk, nxt);
-    rb_issue<T>(nxt, xb, sv[0]);
+    rb_issue(nxt, xb, sv[0]);
     rb_load_idx(K, blk_row, blockIdx.x + gridDim.x, nblk, nxt);
     for (long long b = blockIdx.x; b < nblk; b += gridDim.x) {
-        rb_issue<T>(nxt, xb, sv[st ^ 1]);
+        rb_issue(nxt, xb, sv[st ^ 1]);
         rb_load_idx(K, blk_row, b + 2LL * gridDim.x, nblk, nxt);
         cp_async_wait1();
         __syncthreads();
@@ -174,7 +183,8 @@ __global__ void __launch_bounds__(RB_NT, 6) k_primal_rb(Csr Kt, const long long*
                                                      const T* __restrict__ cs, const Ctrl* __restrict__ ctrl,
                                                      long long kint, long long j, PushList pl, const unsigned* pp_rcount,
                                                      unsigned pp_rthr) {
-    __shared__ __align__(16) T sv[2][RB_NNZ];
+    constexpr int NZ = RB_NNZ_OF<T>;
+    __shared__ __align__(16) T sv[2][NZ];
     __shared__ unsigned s_cnt, s_base;
     __shared__ int s_list[RB_NT];
     __shared__ bool s_en;
@@ -186,12 +196,12 @@ __global__ void __launch_bounds__(RB_NT, 6) k_primal_rb(Csr Kt, const long long*
     T* __restrict__ xbout = par ? s.xb[0] : s.xb[1];
     const double rho = ctrl->rho, tau1 = ctrl->tau1;
     int st = 0;
-    int nxt[RB_U];
+    int nxt[NZ / RB_NT];
     rb_load_idx(Kt, blk_row, blockIdx.x, nblk, nxt);
-    rb_issue<T>(nxt, s.w, sv[0]);
+    rb_issue(nxt, s.w, sv[0]);
     rb_load_idx(Kt, blk_row, blockIdx.x + gridDim.x, nblk, nxt);
     for (long long b = blockIdx.x; b < nblk; b += gridDim.x) {
-        rb_issue<T>(nxt, s.w, sv[st ^ 1]);
+        rb_issue(nxt, s.w, sv[st ^ 1]);
         rb_load_idx(Kt, blk_row, b + 2LL * gridDim.x, nblk, nxt);
         if (threadIdx.x == 0) s_en = pl.acc && *(volatile unsigned*)pl.count[par ^ 1] <= pl.thr;
         cp_async_wait1();
@@ -246,7 +256,8 @@ __global__ void __launch_bounds__(RB_NT) k_trig_rows_rb(Csr K, const long long* 
                                                         long long kint, long long j, double* __restrict__ part1,
                                                         unsigned char* __restrict__ ones_out,
                                                         const unsigned* __restrict__ trig_flag) {
-    __shared__ __align__(16) T sv[2][RB_NNZ];
+    constexpr int NZ = RB_NNZ_OF<T>;
+    __shared__ __align__(16) T sv[2][NZ];
     __shared__ double sh[32];
     if (trig_flag && *(volatile const unsigned*)trig_flag) return;  // x_k was pushed: k_trig_rows_push
     const long long kk = iter_index(ctrl, kint, j);
@@ -257,12 +268,12 @@ __global__ void __launch_bounds__(RB_NT) k_trig_rows_rb(Csr K, const long long* 
     const double tau2 = ctrl->tau2;
     double ge = 0.0, eq = 0.0, sy2 = 0.0;
     int st = 0;
-    int nxt[RB_U];
+    int nxt[NZ / RB_NT];
     rb_load_idx(K, blk_row, blockIdx.x, nblk, nxt);
-    rb_issue<T>(nxt, xk, sv[0]);
+    rb_issue(nxt, xk, sv[0]);
     rb_load_idx(K, blk_row, blockIdx.x + gridDim.x, nblk, nxt);
     for (long long b = blockIdx.x; b < nblk; b += gridDim.x) {
-        rb_issue<T>(nxt, xk, sv[st ^ 1]);
+        rb_issue(nxt, xk, sv[st ^ 1]);
         rb_load_idx(K, blk_row, b + 2LL * gridDim.x, nblk, nxt);
         cp_async_wait1();
         __syncthreads();
@@ -304,159 +315,6 @@ __global__ void __launch_bounds__(RB_NT) k_trig_rows_rb(Csr K, const long long* 
     const double bb = block_max<RB_NT>(eq, sh);
     const double c = block_sum<RB_NT>(sy2, sh);
     if (threadIdx.x == 0) { part1[3 * blockIdx.x] = a; part1[3 * blockIdx.x + 1] = bb; part1[3 * blockIdx.x + 2] = c; }
-}
-
-// =============================================================================================
-// Warp-level row blocks (rows <= WRB_NNZ nonzeros): each warp owns consecutive rows holding
-// <= WRB_NNZ nonzeros and pipelines them on its own (cp.async double buffer in a private smem
-// slice, __syncwarp only) — no CTA-wide barriers, so the warps of a CTA never wait for each other
-// and the LSU sees a continuous stream of gathers.
-// =============================================================================================
-constexpr int WRB_NNZ = 256;             // nonzeros per warp row block (8 per lane)
-constexpr int WRB_U = WRB_NNZ / 32;
-constexpr int WRB_WARPS = 8;             // warps per CTA
-
-template <typename T>
-__device__ __forceinline__ void wrb_issue(const Csr& A, const long long* __restrict__ blk_row, long long b,
-                                          long long nblk, const T* __restrict__ v, T* sv, int lane) {
-    if (b < nblk) {
-        const long long p0 = __ldg(A.ptr + __ldg(blk_row + b));
-        const int cnt = (int)(__ldg(A.ptr + __ldg(blk_row + b + 1)) - p0);
-        int cols[WRB_U];
-#pragma unroll
-        for (int u = 0; u < WRB_U; ++u) {
-            const int t = u * 32 + lane;
-            cols[u] = t < cnt ? ldcs_i32(A.idx + p0 + t) : -1;
-        }
-#pragma unroll
-        for (int u = 0; u < WRB_U; ++u)
-            if (cols[u] >= 0) cp_async_elem(sv + u * 32 + lane, v + cols[u]);
-    }
-    cp_async_commit();
-}
-
-__device__ __forceinline__ int wrb_group_size(int nr) {
-    int G = 32;
-    while (G > 1 && G * nr > 32) G >>= 1;
-    return G;
-}
-
-// row sum from shared memory with 2 independent accumulators
-template <typename T, int KIND>
-__device__ __forceinline__ double wrb_row_sum(const Csr& A, const T* sv, long long p0, long long q0, long long q1,
-                                              int lane, int G) {
-    double a0 = 0.0, a1 = 0.0;
-    long long q = q0 + lane;
-    for (; q + G < q1; q += 2 * G) {
-        if constexpr (KIND == KV_SIGN) { a0 += (double)sv[q - p0]; a1 += (double)sv[q + G - p0]; }
-        else { a0 += kval<KIND>(A.val, q) * (double)sv[q - p0]; a1 += kval<KIND>(A.val, q + G) * (double)sv[q + G - p0]; }
-    }
-    if (q < q1) {
-        if constexpr (KIND == KV_SIGN) a0 += (double)sv[q - p0];
-        else a0 += kval<KIND>(A.val, q) * (double)sv[q - p0];
-    }
-    return a0 + a1;
-}
-
-template <typename T, int KIND>
-__global__ void __launch_bounds__(32 * WRB_WARPS) k_dual_wrb(Csr K, const long long* __restrict__ blk_row, long long nblk,
-                                                            State<T> s, const double* __restrict__ g,
-                                                            const double* __restrict__ rh,
-                                                            const signed char* __restrict__ rsign, long long m1,
-                                                            const Ctrl* __restrict__ ctrl, long long kint, long long j) {
-    __shared__ __align__(16) T sv_all[WRB_WARPS][2][WRB_NNZ];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    T(*sv)[WRB_NNZ] = sv_all[wib];
-    const long long kk = iter_index(ctrl, kint, j);
-    const int par = (int)(kk & 1);
-    const T* __restrict__ xb = par ? s.xb[1] : s.xb[0];
-    const T* __restrict__ yin = par ? s.y[1] : s.y[0];
-    T* __restrict__ yout = par ? s.y[0] : s.y[1];
-    const double tau2 = ctrl->tau2;
-    const long long w0 = (long long)blockIdx.x * WRB_WARPS + wib, nw = (long long)gridDim.x * WRB_WARPS;
-    int st = 0;
-    wrb_issue<T>(K, blk_row, w0, nblk, xb, sv[0], lane);
-    for (long long b = w0; b < nblk; b += nw) {
-        wrb_issue<T>(K, blk_row, b + nw, nblk, xb, sv[st ^ 1], lane);
-        cp_async_wait1();
-        __syncwarp();
-        const long long r0 = __ldg(blk_row + b), r1 = __ldg(blk_row + b + 1);
-        const long long p0 = __ldg(K.ptr + r0);
-        const int nr = (int)(r1 - r0);
-        const int G = wrb_group_size(nr);
-        const int gl = lane & (G - 1), grp = lane / G, ngr = 32 / G;
-        for (int rb = 0; rb < nr; rb += ngr) {
-            const int rr = rb + grp;
-            const long long row = r0 + rr;
-            double acc = 0.0;
-            if (rr < nr) acc = wrb_row_sum<T, KIND>(K, sv[st], p0, __ldg(K.ptr + row), __ldg(K.ptr + row + 1), gl, G);
-            acc = rb_group_sum(acc, G);
-            if (gl == 0 && rr < nr) {
-                const double sg = (KIND == KV_SIGN) ? (double)rsign[row] : 1.0;
-                const double gj = g[row];
-                double yn = (double)yin[row] + tau2 * (rh[row] - gj * (sg * acc));
-                if (row < m1 && yn < 0.0) yn = 0.0;
-                yout[row] = (T)yn;
-                s.w[row] = (T)(gj * sg * yn);
-            }
-        }
-        __syncwarp();
-        st ^= 1;
-    }
-    asm volatile("cp.async.wait_all;");
-}
-
-template <typename T, int KIND, bool HASQ>
-__global__ void __launch_bounds__(32 * WRB_WARPS) k_primal_wrb(Csr Kt, const long long* __restrict__ blk_row,
-                                                              long long nblk, Csr Q, const T* __restrict__ qs, State<T> s,
-                                                              const T* __restrict__ cs, const Ctrl* __restrict__ ctrl,
-                                                              long long kint, long long j) {
-    __shared__ __align__(16) T sv_all[WRB_WARPS][2][WRB_NNZ];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    T(*sv)[WRB_NNZ] = sv_all[wib];
-    const long long kk = iter_index(ctrl, kint, j);
-    const int par = (int)(kk & 1);
-    const T* __restrict__ xin = par ? s.x[1] : s.x[0];
-    T* __restrict__ xout = par ? s.x[0] : s.x[1];
-    T* __restrict__ xbout = par ? s.xb[0] : s.xb[1];
-    const double rho = ctrl->rho, tau1 = ctrl->tau1;
-    const long long w0 = (long long)blockIdx.x * WRB_WARPS + wib, nw = (long long)gridDim.x * WRB_WARPS;
-    int st = 0;
-    wrb_issue<T>(Kt, blk_row, w0, nblk, s.w, sv[0], lane);
-    for (long long b = w0; b < nblk; b += nw) {
-        wrb_issue<T>(Kt, blk_row, b + nw, nblk, s.w, sv[st ^ 1], lane);
-        cp_async_wait1();
-        __syncwarp();
-        const long long r0 = __ldg(blk_row + b), r1 = __ldg(blk_row + b + 1);
-        const long long p0 = __ldg(Kt.ptr + r0);
-        const int nr = (int)(r1 - r0);
-        const int G = wrb_group_size(nr);
-        const int gl = lane & (G - 1), grp = lane / G, ngr = 32 / G;
-        for (int rb = 0; rb < nr; rb += ngr) {
-            const int rr = rb + grp;
-            const long long i = r0 + rr;
-            double a = 0.0, bq = 0.0;
-            if (rr < nr) {
-                a = wrb_row_sum<T, KIND>(Kt, sv[st], p0, __ldg(Kt.ptr + i), __ldg(Kt.ptr + i + 1), gl, G);
-                if constexpr (HASQ)
-                    for (long long q = __ldg(Q.ptr + i) + gl; q < __ldg(Q.ptr + i + 1); q += G)
-                        bq += (double)__ldg(qs + q) * (double)__ldg(xin + __ldg(Q.idx + q));
-            }
-            a = rb_group_sum(a, G);
-            if constexpr (HASQ) bq = rb_group_sum(bq, G);
-            if (gl == 0 && rr < nr) {
-                const double xi = (double)xin[i];
-                const double delta = (((double)cs[i] + rho) - a) + 2.0 * bq - 2.0 * rho * xi;
-                double xn = xi - tau1 * delta;
-                xn = xn < 0.0 ? 0.0 : (xn > 1.0 ? 1.0 : xn);
-                xout[i] = (T)xn;
-                xbout[i] = (T)(2.0 * xn - xi);
-            }
-        }
-        __syncwarp();
-        st ^= 1;
-    }
-    asm volatile("cp.async.wait_all;");
 }
 
 }  // namespace gfors
