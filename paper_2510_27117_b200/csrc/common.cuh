@@ -118,4 +118,16 @@ __device__ __forceinline__ double block_max(double v, double* sh) {
     return r;
 }
 
+// warp-aggregated append of idx to a shared list (one shared atomic per warp); every lane of the
+// warp must call it.  The list order is not deterministic — its consumers only add integers.
+__device__ __forceinline__ void warp_append(bool pred, int idx, unsigned* s_cnt, int* s_list) {
+    const unsigned mask = __ballot_sync(0xffffffffu, pred);
+    if (!mask) return;
+    const int lane = threadIdx.x & 31, leader = __ffs(mask) - 1;
+    unsigned base = 0u;
+    if (lane == leader) base = atomicAdd(s_cnt, (unsigned)__popc(mask));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (pred) s_list[base + __popc(mask & ((1u << lane) - 1u))] = idx;
+}
+
 }  // namespace gfors

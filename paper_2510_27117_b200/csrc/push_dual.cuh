@@ -24,8 +24,8 @@ __global__ void __launch_bounds__(256) k_push_scatter(Csr Kt, PushList pl, State
     const int par = (int)(kk & 1);
     if (!push_mode(pl, par)) return;
     const T* __restrict__ xb = par ? s.xb[1] : s.xb[0];
-    const long long cnt = *pl.count[par];
-    const int* __restrict__ list = pl.list[par];
+    const long long cnt = *pl_count(pl, par);
+    const int* __restrict__ list = pl_list(pl, par);
     for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * (long long)blockDim.x) {
         const int i = list[k];
         const long long v = __double2ll_rn((double)xb[i] * PUSH_SCALE);

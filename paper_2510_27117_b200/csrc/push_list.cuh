@@ -17,14 +17,19 @@ struct PushList {
     unsigned long long* pp_wmax;    // push-primal max |w|, reset by the dual (or null)
 };
 
+// parity-selected members without dynamic indexing of the kernel-parameter arrays (which would
+// copy the struct to local memory)
+__device__ __forceinline__ unsigned* pl_count(const PushList& pl, int p) { return p ? pl.count[1] : pl.count[0]; }
+__device__ __forceinline__ int* pl_list(const PushList& pl, int p) { return p ? pl.list[1] : pl.list[0]; }
+
 // called by thread 0 of block 0 of whichever dual kernel is active this iteration
 __device__ __forceinline__ void push_reset_next(const PushList& pl, int par) {
-    *pl.count[par ^ 1] = 0u;
+    *pl_count(pl, par ^ 1) = 0u;
     if (pl.pp_rcount) { *pl.pp_rcount = 0u; *pl.pp_wmax = 0ull; }
 }
 
 __device__ __forceinline__ bool push_mode(const PushList& pl, int par) {
-    return pl.acc != nullptr && *(volatile unsigned*)pl.count[par] <= pl.thr;
+    return pl.acc != nullptr && *(volatile unsigned*)pl_count(pl, par) <= pl.thr;
 }
 
 // block-staged append of the pass's nonzero columns (one global atomic per CTA pass); enabled is
@@ -35,13 +40,13 @@ __device__ __forceinline__ void push_append(const PushList& pl, int outpar, bool
     if (!enabled) return;
     if (threadIdx.x == 0) *s_cnt = 0u;
     __syncthreads();
-    if (nz) s_list[atomicAdd(s_cnt, 1u)] = idx;
+    warp_append(nz, idx, s_cnt, s_list);
     __syncthreads();
-    if (threadIdx.x == 0) *s_base = *s_cnt ? atomicAdd(pl.count[outpar], *s_cnt) : 0u;
+    if (threadIdx.x == 0) *s_base = *s_cnt ? atomicAdd(pl_count(pl, outpar), *s_cnt) : 0u;
     __syncthreads();
     const unsigned c = *s_cnt, base = *s_base;
     for (unsigned t = threadIdx.x; t < c; t += NT)
-        if ((long long)base + t < pl.cap) pl.list[outpar][base + t] = s_list[t];
+        if ((long long)base + t < pl.cap) pl_list(pl, outpar)[base + t] = s_list[t];
     __syncthreads();
 }
 

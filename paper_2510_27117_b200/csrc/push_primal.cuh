@@ -29,14 +29,16 @@ __device__ __forceinline__ bool pprimal_mode(const PushPrimal& pp) {
     return pp.accx != nullptr && *(volatile unsigned*)pp.rcount <= pp.rthr;
 }
 
-// fixed-point scale 2^e with (max|w| * maxdeg) * 2^e < 2^62
-__device__ __forceinline__ double pprimal_scale(const PushPrimal& pp) {
+// fixed-point scale S = 2^e with (max|w| * maxdeg) * 2^e < 2^62 (exponent read from the bits;
+// capped at 2^1000 for vanishing w); returns e, S and 1/S are then exact powers of two
+__device__ __forceinline__ int pprimal_exp(const PushPrimal& pp) {
     const double wm = __longlong_as_double((long long)*(volatile unsigned long long*)pp.wmax);
-    if (!(wm > 0.0)) return 1.0;
-    int e;
-    frexp(wm * (double)pp.maxdeg, &e);  // wm*maxdeg < 2^e
-    return ldexp(1.0, 62 - e);
+    if (!(wm > 0.0)) return 0;
+    const double b = wm * (double)pp.maxdeg;
+    const int bexp = (int)((__double_as_longlong(b) >> 52) & 0x7ff);  // b = f 2^(bexp-1023), f in [1,2)
+    return min(62 - (bexp - 1022), 1000);                               // b < 2^(bexp-1022)
 }
+__device__ __forceinline__ double pow2(int e) { return __longlong_as_double((long long)(e + 1023) << 52); }
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_wlist(const T* __restrict__ w, PushPrimal pp) {
@@ -52,7 +54,7 @@ __global__ void __launch_bounds__(256) k_wlist(const T* __restrict__ w, PushPrim
         mx = fmax(mx, fabs(v));
         if (threadIdx.x == 0) s_cnt = 0u;
         __syncthreads();
-        if (v != 0.0) s_list[atomicAdd(&s_cnt, 1u)] = (int)j;
+        warp_append(v != 0.0, (int)j, &s_cnt, s_list);
         __syncthreads();
         if (threadIdx.x == 0) s_base = s_cnt ? atomicAdd(pp.rcount, s_cnt) : 0u;
         __syncthreads();
@@ -68,7 +70,7 @@ __global__ void __launch_bounds__(256) k_wlist(const T* __restrict__ w, PushPrim
 template <typename T>
 __global__ void __launch_bounds__(256) k_push_scatter_cols(Csr K, PushPrimal pp, const T* __restrict__ w) {
     if (!pprimal_mode(pp)) return;
-    const double S = pprimal_scale(pp);
+    const double S = pow2(pprimal_exp(pp));
     const long long cnt = *pp.rcount;
     // a warp per listed row: rows have 2..98 nonzeros on the set-cover workloads
     const int lane = threadIdx.x & 31;
@@ -90,7 +92,7 @@ __global__ void __launch_bounds__(256) k_push_scatter_cols(Csr K, PushPrimal pp,
 constexpr int PP_U = 4;
 
 template <typename T, bool HASQ>
-__global__ void __launch_bounds__(256) k_primal_push(long long n, PushPrimal pp, Csr Q, const T* __restrict__ qs,
+__global__ void __launch_bounds__(256, 6) k_primal_push(long long n, PushPrimal pp, Csr Q, const T* __restrict__ qs,
                                                      State<T> s, const T* __restrict__ cs, const Ctrl* __restrict__ ctrl,
                                                      long long kint, long long j, PushList pl, Csr Kt,
                                                      long long* __restrict__ accv, unsigned* __restrict__ ones_cnt,
@@ -101,7 +103,7 @@ __global__ void __launch_bounds__(256) k_primal_push(long long n, PushPrimal pp,
     if (!pprimal_mode(pp)) return;
     // trigger iteration: also push x_k into the row accumulators of the indicator pass (k_trig_rows_push)
     if (accv && blockIdx.x == 0 && threadIdx.x == 0) *trig_flag = 1u;
-    const double invS = 1.0 / pprimal_scale(pp);
+    const double invS = pow2(-pprimal_exp(pp));
     const long long kk = iter_index(ctrl, kint, j);
     const int par = (int)(kk & 1);
     const T* __restrict__ xin = par ? s.x[1] : s.x[0];
@@ -110,30 +112,42 @@ __global__ void __launch_bounds__(256) k_primal_push(long long n, PushPrimal pp,
     const double rho = ctrl->rho, tau1 = ctrl->tau1;
     const long long per = 256LL * PP_U;
     const long long nbase = (n + per - 1) / per;
+    long long* __restrict__ accx = pp.accx;
     for (long long bb = blockIdx.x; bb < nbase; bb += gridDim.x) {  // block-uniform trip count
-        if (threadIdx.x == 0) { s_en = pl.acc && *(volatile unsigned*)pl.count[par ^ 1] <= pl.thr; s_cnt = 0u; }
+        if (threadIdx.x == 0) { s_en = pl.acc && *(volatile unsigned*)pl_count(pl, par ^ 1) <= pl.thr; s_cnt = 0u; }
         __syncthreads();
         const bool en = s_en;
+        // all loads of the PP_U columns first (independent, in flight together), then the updates
+        long long ai[PP_U];
+        double xi[PP_U], ci[PP_U];
 #pragma unroll
         for (int u = 0; u < PP_U; ++u) {
             const long long i = bb * per + u * 256 + threadIdx.x;
-            if (i >= n) continue;
-            const long long ai = pp.accx[i];
-            if (ai) pp.accx[i] = 0;
-            const double a = (double)ai * invS;
-            double b = 0.0;
-            if constexpr (HASQ)
-                for (long long q = __ldg(Q.ptr + i); q < __ldg(Q.ptr + i + 1); ++q)
-                    b += (double)__ldg(qs + q) * (double)__ldg(xin + __ldg(Q.idx + q));
-            const double xi = (double)xin[i];
-            const double delta = (((double)__ldg(cs + i) + rho) - a) + 2.0 * b - 2.0 * rho * xi;
-            double xn = xi - tau1 * delta;
-            xn = xn < 0.0 ? 0.0 : (xn > 1.0 ? 1.0 : xn);
-            const T xk = (T)xn;
-            xout[i] = xk;
-            const T xbn = (T)(2.0 * xn - xi);
-            xbout[i] = xbn;
-            if (en && xbn != (T)0) s_list[atomicAdd(&s_cnt, 1u)] = (int)i;
+            ai[u] = 0; xi[u] = 0.0; ci[u] = 0.0;
+            if (i < n) { ai[u] = __ldcs(accx + i); xi[u] = (double)xin[i]; ci[u] = (double)__ldg(cs + i); }
+        }
+#pragma unroll
+        for (int u = 0; u < PP_U; ++u) {
+            const long long i = bb * per + u * 256 + threadIdx.x;
+            bool nzb = false;
+            T xk = (T)0;
+            if (i < n) {
+                if (ai[u]) accx[i] = 0;
+                const double a = (double)ai[u] * invS;
+                double b = 0.0;
+                if constexpr (HASQ)
+                    for (long long q = __ldg(Q.ptr + i); q < __ldg(Q.ptr + i + 1); ++q)
+                        b += (double)__ldg(qs + q) * (double)__ldg(xin + __ldg(Q.idx + q));
+                const double delta = ((ci[u] + rho) - a) + 2.0 * b - 2.0 * rho * xi[u];
+                double xn = xi[u] - tau1 * delta;
+                xn = xn < 0.0 ? 0.0 : (xn > 1.0 ? 1.0 : xn);
+                xk = (T)xn;
+                xout[i] = xk;
+                const T xbn = (T)(2.0 * xn - xi[u]);
+                xbout[i] = xbn;
+                nzb = xbn != (T)0;
+            }
+            if (en) warp_append(nzb, (int)i, &s_cnt, s_list);
             if (accv && xk != (T)0) {
                 const long long v = __double2ll_rn((double)xk * 1099511627776.0);  // 2^40 fixed point
                 const bool one = xk == (T)1;
@@ -147,11 +161,11 @@ __global__ void __launch_bounds__(256) k_primal_push(long long n, PushPrimal pp,
         }
         __syncthreads();
         if (en) {
-            if (threadIdx.x == 0) s_base = s_cnt ? atomicAdd(pl.count[par ^ 1], s_cnt) : 0u;
+            if (threadIdx.x == 0) s_base = s_cnt ? atomicAdd(pl_count(pl, par ^ 1), s_cnt) : 0u;
             __syncthreads();
             const unsigned c = s_cnt, base = s_base;
             for (unsigned t = threadIdx.x; t < c; t += 256)
-                if ((long long)base + t < pl.cap) pl.list[par ^ 1][base + t] = s_list[t];
+                if ((long long)base + t < pl.cap) pl_list(pl, par ^ 1)[base + t] = s_list[t];
             __syncthreads();
         }
     }

@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(RB_NT, 6) k_primal_rb(Csr Kt, const long long*
     for (long long b = blockIdx.x; b < nblk; b += gridDim.x) {
         rb_issue(nxt, s.w, sv[st ^ 1]);
         rb_load_idx(Kt, blk_row, b + 2LL * gridDim.x, nblk, nxt);
-        if (threadIdx.x == 0) s_en = pl.acc && *(volatile unsigned*)pl.count[par ^ 1] <= pl.thr;
+        if (threadIdx.x == 0) s_en = pl.acc && *(volatile unsigned*)pl_count(pl, par ^ 1) <= pl.thr;
         cp_async_wait1();
         __syncthreads();
         const long long r0 = blk_row[b], r1 = blk_row[b + 1];

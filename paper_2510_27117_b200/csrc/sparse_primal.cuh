@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(SP_NT, 1) k_primal_sparse(Csr Kt, const long l
         sp_issue<T>(nxt, s.w, sbits, svb + (st ^ 1) * SP_NNZ);
         sp_load_idx(Kt, blk_row, b + 2LL * gridDim.x, nblk, nxt);
         const SpRow nrow = sp_prefetch_row<T>(Kt, blk_row, b + gridDim.x, nblk, xin, cs);
-        if (threadIdx.x == 0) s_en = pl.acc && *(volatile unsigned*)pl.count[par ^ 1] <= pl.thr;
+        if (threadIdx.x == 0) s_en = pl.acc && *(volatile unsigned*)pl_count(pl, par ^ 1) <= pl.thr;
         cp_async_wait1();
         __syncthreads();
         const T* sv = svb + st * SP_NNZ;
