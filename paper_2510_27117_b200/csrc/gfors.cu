@@ -341,6 +341,7 @@ struct gfors_ctx {
     unsigned push_thr = 0;
     int* d_plist[2] = {nullptr, nullptr};
     unsigned* d_pcount = nullptr;    // [2]
+    unsigned* d_pflags = nullptr;    // delta push: [0,1] dual acc valid, [2,3] primal accx valid, [4,5] primal exponent
     long long* d_acc = nullptr;      // [m]
     double* d_segpart = nullptr;
     double* d_segpart2 = nullptr;
@@ -459,7 +460,7 @@ void gfors_ctx::free_problem() {
 void gfors_ctx::free_prep() {
     void** ps[] = {(void**)&d_s, &d_g, &d_rh, &d_cs, &d_qs, &d_x[0], &d_x[1], &d_xb[0], &d_xb[1], &d_y[0], &d_y[1],
                    &d_w, (void**)&d_tmp[0], (void**)&d_tmp[1], (void**)&d_tmp[2], (void**)&d_tmp[3],
-                   (void**)&d_red, (void**)&d_scalar, (void**)&d_segpart, (void**)&d_segpart2, (void**)&d_u, (void**)&d_ones, (void**)&d_rec, (void**)&d_regen, (void**)&d_plist[0], (void**)&d_plist[1], (void**)&d_pcount, (void**)&d_acc, (void**)&d_rlist, (void**)&d_rcount, (void**)&d_wmax, (void**)&d_accx, (void**)&d_accv, (void**)&d_ones_cnt, (void**)&d_trig_flag, (void**)&d_part1,
+                   (void**)&d_red, (void**)&d_scalar, (void**)&d_segpart, (void**)&d_segpart2, (void**)&d_u, (void**)&d_ones, (void**)&d_rec, (void**)&d_regen, (void**)&d_plist[0], (void**)&d_plist[1], (void**)&d_pcount, (void**)&d_pflags, (void**)&d_acc, (void**)&d_rlist, (void**)&d_rcount, (void**)&d_wmax, (void**)&d_accx, (void**)&d_accv, (void**)&d_ones_cnt, (void**)&d_trig_flag, (void**)&d_part1,
                    (void**)&d_part2, (void**)&d_hist, (void**)&d_rho, (void**)&d_trace, (void**)&d_xbest,
                    (void**)&d_X, (void**)&d_viol, (void**)&d_iacc, &d_zpart, (void**)&d_z, (void**)&d_ctrl};
     for (void** p : ps) { dfree(*p); *p = nullptr; }
@@ -550,8 +551,11 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
     PushList pl{{nullptr, nullptr}, {nullptr, nullptr}, 0u, 0, nullptr, nullptr, nullptr};
     if (C->push_dual)
         pl = PushList{{C->d_plist[0], C->d_plist[1]}, {C->d_pcount, C->d_pcount + 1}, C->push_thr, C->n, C->d_acc,
-                      C->push_primal ? C->d_rcount : nullptr, C->push_primal ? C->d_wmax : nullptr};
-    const PushPrimal ppr{C->d_rlist, C->d_rcount, C->rthr, C->d_wmax, C->d_accx, C->maxcoldeg, C->m};
+                      C->push_primal ? C->d_rcount : nullptr, C->push_primal ? C->d_wmax : nullptr, C->d_pflags};
+    PushPrimal ppr{};
+    if (C->push_primal)
+        ppr = PushPrimal{C->d_rlist, C->d_rcount, C->rthr, C->d_wmax, C->d_accx, C->maxcoldeg, C->m,
+                         C->d_pflags + 2, reinterpret_cast<int*>(C->d_pflags + 4), (const double*)C->d_g, C->d_rsign};
     const Ctrl* ctrl = C->d_ctrl;
     const double* g = (const double*)C->d_g;
     const double* rh = (const double*)C->d_rh;
@@ -591,13 +595,13 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
     const bool trig_push = C->push_primal && kint > 0 && j == kint - 1;
     if (C->push_primal) {
         // list the active duals; the push kernels run iff the list is short, else k_primal_rb below
-        LAUNCH(C, s, KC_PRIMAL_PUSH, (k_wlist<T><<<grid_for(C->m), NT, 0, s>>>(st.w, ppr)));
-        LAUNCH(C, s, KC_PRIMAL_PUSH, (k_push_scatter_cols<T><<<grid_for(C->m * 32LL), NT, 0, s>>>(csr_K(C), ppr, st.w)));
+        LAUNCH(C, s, KC_PRIMAL_PUSH, (k_wlist<T><<<grid_for(C->m), NT, 0, s>>>(st, ppr, ctrl, kint, j)));
+        LAUNCH(C, s, KC_PRIMAL_PUSH, (k_push_scatter_cols<T><<<grid_for(C->m * 32LL), NT, 0, s>>>(csr_K(C), ppr, st, ctrl, kint, j)));
         if (C->hasq)
-            LAUNCH(C, s, KC_PRIMAL_PUSH, (k_primal_push<T, true><<<grid_for(C->n), NT, 0, s>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
+            LAUNCH(C, s, KC_PRIMAL_PUSH, (k_primal_push<T, true><<<pp_grid(C->n), NT, 0, s>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
                 csr_Kt(C), trig_push ? C->d_accv : nullptr, C->d_ones_cnt, C->d_trig_flag)));
         else
-            LAUNCH(C, s, KC_PRIMAL_PUSH, (k_primal_push<T, false><<<grid_for(C->n), NT, 0, s>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
+            LAUNCH(C, s, KC_PRIMAL_PUSH, (k_primal_push<T, false><<<pp_grid(C->n), NT, 0, s>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
                 csr_Kt(C), trig_push ? C->d_accv : nullptr, C->d_ones_cnt, C->d_trig_flag)));
     }
     if (C->sparse_primal && !C->push_primal && sparse_primal_smem<T>(C->m) <= SP_DYN_MAX) {
@@ -625,13 +629,11 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
         if (C->hasq) {
             KIND_SWITCH(tkind, LAUNCH(C, s, KC_PRIMAL,
                 (k_primal_rb<T, KINDV, true><<<grid, RB_NT, 0, s>>>(csr_Kt(C), C->pp.blk_row, C->pp.nblk, Q, qs, st, cs,
-                                                                    ctrl, kint, j, pl, C->push_primal ? C->d_rcount : nullptr,
-                                                                    C->rthr))));
+                                                                    ctrl, kint, j, pl, ppr))));
         } else {
             KIND_SWITCH(tkind, LAUNCH(C, s, KC_PRIMAL,
                 (k_primal_rb<T, KINDV, false><<<grid, RB_NT, 0, s>>>(csr_Kt(C), C->pp.blk_row, C->pp.nblk, Q, qs, st, cs,
-                                                                     ctrl, kint, j, pl, C->push_primal ? C->d_rcount : nullptr,
-                                                                     C->rthr))));
+                                                                     ctrl, kint, j, pl, ppr))));
         }
     } else if (!C->pp.seg) {
         const int grid = grid_for(C->n * (long long)C->pp.sub);
@@ -920,6 +922,20 @@ static double power_iteration(gfors_ctx* C, bool isq, double tol, int max_iter) 
     return sigma;
 }
 
+// push-mode state at the start of a run / after set_state: lists unknown (gather first), delta-push
+// accumulators cleared and invalid
+static void reset_push(gfors_ctx* C, cudaStream_t s) {
+    if (C->push_dual) {
+        CK(cudaMemsetAsync(C->d_pcount, 0xff, 2 * sizeof(unsigned), s));
+        CK(cudaMemsetAsync(C->d_acc, 0, std::max<long long>(C->m, 1) * sizeof(long long), s));
+        CK(cudaMemsetAsync(C->d_pflags, 0, 8 * sizeof(unsigned), s));
+    }
+    if (C->push_primal) {
+        CK(cudaMemsetAsync(C->d_rcount, 0, sizeof(unsigned), s));
+        CK(cudaMemsetAsync(C->d_accx, 0, C->n * sizeof(long long), s));
+    }
+}
+
 // the product plans and push modes of the preprocessed precision (row-block size is per precision)
 static void select_plans(gfors_ctx* C) {
     const int v = C->precision == 64 ? 1 : 0;
@@ -1004,8 +1020,10 @@ static void do_preprocess(gfors_ctx* C, const gfors_prep_opts* o, gfors_scaling*
         C->d_plist[1] = dalloc<int>(n);
         C->d_pcount = dalloc<unsigned>(2);
         C->d_acc = dalloc<long long>(std::max<long long>(m, 1));
+        C->d_pflags = dalloc<unsigned>(8);
         CK(cudaMemsetAsync(C->d_pcount, 0xff, 2 * sizeof(unsigned), s));
         CK(cudaMemsetAsync(C->d_acc, 0, std::max<long long>(m, 1) * sizeof(long long), s));
+        CK(cudaMemsetAsync(C->d_pflags, 0, 8 * sizeof(unsigned), s));
     }
     if (C->push_primal) {
         C->d_rlist = dalloc<int>(std::max<long long>(m, 1));
@@ -1113,8 +1131,7 @@ static void do_run_t(gfors_ctx* C, const gfors_params* p, gfors_run_info* out) {
     // reset state and control
     k_init_state<T><<<grid_for(std::max(C->n, C->m)), NT, 0, s>>>(state_of<T>(C), C->n, C->m);
     CK(cudaGetLastError());
-    if (C->push_dual) CK(cudaMemsetAsync(C->d_pcount, 0xff, 2 * sizeof(unsigned), s));  // unknown -> gather mode
-    if (C->push_primal) CK(cudaMemsetAsync(C->d_rcount, 0, sizeof(unsigned), s));
+    reset_push(C, s);
     Ctrl h{};
     h.blk = 0; h.k = 0; h.rho = rho[0]; h.tau1 = std::sqrt(p->sigma); h.tau2 = std::sqrt(p->sigma);
     h.max_blocks = max_blocks; h.z_best = INFINITY; h.found_iter = h.found_round = h.found_index = -1; h.win_lane = -1;
@@ -1245,8 +1262,8 @@ static void set_state_t(gfors_ctx* C, const double* x, const double* xbar, const
     if (xbar) { CK(cudaMemcpyAsync(t, xbar, C->n * 8, cudaMemcpyHostToDevice, s)); k_to_T<T><<<grid_for(C->n), NT, 0, s>>>(t, C->n, (T*)C->d_xb[0]); CK(cudaStreamSynchronize(s)); }
     if (y && C->m) { CK(cudaMemcpyAsync(t, y, C->m * 8, cudaMemcpyHostToDevice, s)); k_to_T<T><<<grid_for(C->m), NT, 0, s>>>(t, C->m, (T*)C->d_y[0]); CK(cudaStreamSynchronize(s)); }
     CK(cudaGetLastError());
-    if (C->push_dual) CK(cudaMemset(C->d_pcount, 0xff, 2 * sizeof(unsigned)));
-    if (C->push_primal) CK(cudaMemset(C->d_rcount, 0, sizeof(unsigned)));
+    reset_push(C, s);
+    CK(cudaStreamSynchronize(s));
     C->hk = 0;
 }
 

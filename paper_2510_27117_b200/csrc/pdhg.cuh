@@ -20,6 +20,11 @@ struct State {
     T* w;  // w_j = g_j * (rsign_j) * y_j  (so K'y = -K_u' w)
 };
 
+// w_j from the STORED dual y_j (already rounded to T), so w is a function of the stored y alone and
+// the delta push (push_primal.cuh) can recompute w_{k-1} bit-exactly from y_{k-1}
+template <typename T>
+__device__ __forceinline__ T w_of(double gj, double sg, T yt) { return (T)(gj * sg * (double)yt); }
+
 struct Csr {
     const long long* ptr;  // int64 [rows+1]
     const int* idx;        // int32 [nnz]
@@ -85,8 +90,9 @@ __global__ void __launch_bounds__(256) k_dual(Csr K, State<T> s, const double* _
             const double u = sg * acc;  // (K_u xbar)_j
             double yn = (double)yin[row] + tau2 * ((double)rh[row] - gj * u);
             if (row < m1 && yn < 0.0) yn = 0.0;
-            yout[row] = (T)yn;
-            s.w[row] = (T)(gj * sg * yn);
+            const T yt = (T)yn;
+            yout[row] = yt;
+            s.w[row] = w_of(gj, sg, yt);
         }
     }
 }
@@ -212,8 +218,9 @@ __global__ void __launch_bounds__(256) k_dual_seg_final(long long rows, SegPlan 
         const double gj = (double)g[row];
         double yn = (double)(par ? s.y[1] : s.y[0])[row] + tau2 * ((double)rh[row] - gj * (sg * acc));
         if (row < m1 && yn < 0.0) yn = 0.0;
-        (par ? s.y[0] : s.y[1])[row] = (T)yn;
-        s.w[row] = (T)(gj * sg * yn);
+        const T yt = (T)yn;
+        (par ? s.y[0] : s.y[1])[row] = yt;
+        s.w[row] = w_of(gj, sg, yt);
     }
 }
 

@@ -6,55 +6,40 @@
 // the max |w|), k_push_scatter_cols adds w_j in fixed point (scale S = 2^e chosen from max|w| and the
 // largest column degree so no sum can overflow int64) into int64 column accumulators through the row
 // CSR with integer atomics — order-independent, hence deterministic — and k_primal_push applies the
-// box-projected update column by column (coalesced) and clears the accumulators.  With many active
-// rows the gather kernel (k_primal_rb) runs instead; the choice is made on the device from the list
-// length, every kernel of the unused mode exits at once.
+// box-projected update column by column (coalesced).  The accumulators are then kept (delta push,
+// push_list.cuh): later iterations list and scatter only the rows whose y changed.  With many listed
+// rows the gather kernel (k_primal_rb) runs instead and clears them; the choice is made on the device
+// from the list length (pp_mode), every kernel of the unused mode exits at once.
 #pragma once
 #include "push_list.cuh"
 #include "rowblock.cuh"
 
 namespace gfors {
 
-struct PushPrimal {
-    int* rlist;                // rows with w_j != 0
-    unsigned* rcount;          // list length (reset by the dual of the same iteration)
-    unsigned rthr;             // push mode iff rcount <= rthr
-    unsigned long long* wmax;  // bit pattern of max |w_j| (non-negative doubles order like uint64)
-    long long* accx;           // [n] int64 column accumulators, kept at 0 between uses
-    int maxdeg;                // largest column degree of K_u (number of terms of any a_i)
-    long long m;
-};
-
-__device__ __forceinline__ bool pprimal_mode(const PushPrimal& pp) {
-    return pp.accx != nullptr && *(volatile unsigned*)pp.rcount <= pp.rthr;
-}
-
-// fixed-point scale S = 2^e with (max|w| * maxdeg) * 2^e < 2^62 (exponent read from the bits;
-// capped at 2^1000 for vanishing w); returns e, S and 1/S are then exact powers of two
-__device__ __forceinline__ int pprimal_exp(const PushPrimal& pp) {
-    const double wm = __longlong_as_double((long long)*(volatile unsigned long long*)pp.wmax);
-    if (!(wm > 0.0)) return 0;
-    const double b = wm * (double)pp.maxdeg;
-    const int bexp = (int)((__double_as_longlong(b) >> 52) & 0x7ff);  // b = f 2^(bexp-1023), f in [1,2)
-    return min(62 - (bexp - 1022), 1000);                               // b < 2^(bexp-1022)
-}
-__device__ __forceinline__ double pow2(int e) { return __longlong_as_double((long long)(e + 1023) << 52); }
-
+// lists the rows for the push-mode primal of parity par: valid accumulators -> rows whose y changed
+// this iteration, else rows with w != 0; and max |w|
 template <typename T>
-__global__ void __launch_bounds__(256) k_wlist(const T* __restrict__ w, PushPrimal pp) {
+__global__ void __launch_bounds__(256) k_wlist(State<T> s, PushPrimal pp, const Ctrl* __restrict__ ctrl, long long kint,
+                                               long long jj) {
     __shared__ unsigned s_cnt, s_base;
     __shared__ int s_list[256];
     __shared__ double sh[32];
+    const int par = (int)(iter_index(ctrl, kint, jj) & 1);
+    const bool delta = pp_valid(pp, par);
+    const T* __restrict__ ynew = par ? s.y[0] : s.y[1];
+    const T* __restrict__ yold = par ? s.y[1] : s.y[0];
     double mx = 0.0;
     const long long m = pp.m;
     const long long nbase = (m + 255) / 256;
     for (long long bb = blockIdx.x; bb < nbase; bb += gridDim.x) {  // block-uniform trip count
         const long long j = bb * 256 + threadIdx.x;
-        const double v = j < m ? (double)w[j] : 0.0;
+        const double v = j < m ? (double)s.w[j] : 0.0;
         mx = fmax(mx, fabs(v));
+        bool listed = v != 0.0;
+        if (delta) listed = j < m && ynew[j] != yold[j];
         if (threadIdx.x == 0) s_cnt = 0u;
         __syncthreads();
-        warp_append(v != 0.0, (int)j, &s_cnt, s_list);
+        warp_append(listed, (int)j, &s_cnt, s_list);
         __syncthreads();
         if (threadIdx.x == 0) s_base = s_cnt ? atomicAdd(pp.rcount, s_cnt) : 0u;
         __syncthreads();
@@ -66,11 +51,16 @@ __global__ void __launch_bounds__(256) k_wlist(const T* __restrict__ w, PushPrim
     if (threadIdx.x == 0 && mx > 0.0) atomicMax(pp.wmax, (unsigned long long)__double_as_longlong(mx));
 }
 
-// push mode: accx[i] += round(w_j * S) for every nonzero (j, i) of the listed rows
+// push mode: accx[i] += round(w_j S) for every nonzero (j, i) of the listed rows; delta push adds
+// round(w_j S) - round(w_j^prev S) with w^prev recomputed from y_{k-1} exactly as the dual made it
 template <typename T>
-__global__ void __launch_bounds__(256) k_push_scatter_cols(Csr K, PushPrimal pp, const T* __restrict__ w) {
-    if (!pprimal_mode(pp)) return;
-    const double S = pow2(pprimal_exp(pp));
+__global__ void __launch_bounds__(256) k_push_scatter_cols(Csr K, PushPrimal pp, State<T> s, const Ctrl* __restrict__ ctrl,
+                                                           long long kint, long long jj) {
+    const int par = (int)(iter_index(ctrl, kint, jj) & 1);
+    const PPMode md = pp_mode(pp, par);
+    if (!md.push) return;
+    const double S = pow2(md.e);
+    const T* __restrict__ yold = par ? s.y[1] : s.y[0];
     const long long cnt = *pp.rcount;
     // a warp per listed row: rows have 2..98 nonzeros on the set-cover workloads
     const int lane = threadIdx.x & 31;
@@ -78,7 +68,9 @@ __global__ void __launch_bounds__(256) k_push_scatter_cols(Csr K, PushPrimal pp,
     const long long nwarps = (gridDim.x * (long long)blockDim.x) >> 5;
     for (long long k = warp; k < cnt; k += nwarps) {
         const int jr = pp.rlist[k];
-        const long long v = __double2ll_rn((double)w[jr] * S);
+        long long v = __double2ll_rn((double)s.w[jr] * S);
+        if (md.delta) v -= __double2ll_rn((double)w_of(pp.g[jr], (double)pp.rsign[jr], yold[jr]) * S);
+        if (v == 0) continue;
         const long long q1 = __ldg(K.ptr + jr + 1);
         for (long long q = __ldg(K.ptr + jr) + lane; q < q1; q += 32)
             atomicAdd(reinterpret_cast<unsigned long long*>(pp.accx + __ldg(K.idx + q)), (unsigned long long)v);
@@ -86,13 +78,38 @@ __global__ void __launch_bounds__(256) k_push_scatter_cols(Csr K, PushPrimal pp,
 }
 
 // push mode: x_k = Pi(x_{k-1} - tau1 (c + rho - a + 2 Q x_{k-1} - 2 rho x_{k-1})), xbar_k = 2x_k - x_{k-1},
-// with a = accx / S; also hands the nonzero xbar columns to the next dual (PushList).  Each thread
-// handles PP_U consecutive columns per pass so the block-staged append is amortised over
-// 256*PP_U columns.
+// with a = accx / S (accumulators kept for the next delta push); also hands the nonzero (or, with
+// valid dual accumulators, the changed) xbar columns to the next dual (PushList).  A pure stream over
+// the columns (c, x_{k-1}, accx in; x_k, xbar_k out): each thread owns PP_U = 4 CONSECUTIVE columns
+// and moves them with 16-byte vector loads/stores (one instruction per array for fp32), the
+// block-staged list append is amortised over 256*PP_U columns.
 constexpr int PP_U = 4;
 
+template <typename T>
+__device__ __forceinline__ void ld4(const T* __restrict__ p, T (&o)[PP_U]) {
+    if constexpr (sizeof(T) == 4) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+        o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+    } else {
+        const double2 v0 = __ldg(reinterpret_cast<const double2*>(p)), v1 = __ldg(reinterpret_cast<const double2*>(p) + 1);
+        o[0] = v0.x; o[1] = v0.y; o[2] = v1.x; o[3] = v1.y;
+    }
+}
+template <typename T>
+__device__ __forceinline__ void st4(T* __restrict__ p, const T (&v)[PP_U]) {
+    if constexpr (sizeof(T) == 4) {
+        *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    } else {
+        reinterpret_cast<double2*>(p)[0] = make_double2(v[0], v[1]);
+        reinterpret_cast<double2*>(p)[1] = make_double2(v[2], v[3]);
+    }
+}
+
+// one CTA per 256*PP_U columns (no grid-stride tail imbalance; the scheduler balances the CTAs)
+inline int pp_grid(long long n) { return (int)std::max<long long>(1, std::min<long long>((n + 256 * PP_U - 1) / (256 * PP_U), 1LL << 30)); }
+
 template <typename T, bool HASQ>
-__global__ void __launch_bounds__(256, 6) k_primal_push(long long n, PushPrimal pp, Csr Q, const T* __restrict__ qs,
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? 6 : 4) k_primal_push(long long n, PushPrimal pp, Csr Q, const T* __restrict__ qs,
                                                      State<T> s, const T* __restrict__ cs, const Ctrl* __restrict__ ctrl,
                                                      long long kint, long long j, PushList pl, Csr Kt,
                                                      long long* __restrict__ accv, unsigned* __restrict__ ones_cnt,
@@ -100,59 +117,89 @@ __global__ void __launch_bounds__(256, 6) k_primal_push(long long n, PushPrimal 
     __shared__ unsigned s_cnt, s_base;
     __shared__ int s_list[256 * PP_U];
     __shared__ bool s_en;
-    if (!pprimal_mode(pp)) return;
-    // trigger iteration: also push x_k into the row accumulators of the indicator pass (k_trig_rows_push)
-    if (accv && blockIdx.x == 0 && threadIdx.x == 0) *trig_flag = 1u;
-    const double invS = pow2(-pprimal_exp(pp));
     const long long kk = iter_index(ctrl, kint, j);
     const int par = (int)(kk & 1);
+    const PPMode md = pp_mode(pp, par);
+    if (!md.push) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        // trigger iteration: also push x_k into the row accumulators of the indicator pass (k_trig_rows_push)
+        if (accv) *trig_flag = 1u;
+        const double wm = __longlong_as_double((long long)*(volatile unsigned long long*)pp.wmax);
+        pp_set_next(pp, par, wm > 0.0, md.e);  // accumulators kept (nothing was scattered if w == 0)
+    }
+    const double invS = pow2(-md.e);
     const T* __restrict__ xin = par ? s.x[1] : s.x[0];
     T* __restrict__ xout = par ? s.x[0] : s.x[1];
     T* __restrict__ xbout = par ? s.xb[0] : s.xb[1];
+    const T* __restrict__ xbprev = par ? s.xb[1] : s.xb[0];  // xbar_{k-1} (delta list of the next dual)
     const double rho = ctrl->rho, tau1 = ctrl->tau1;
-    const long long per = 256LL * PP_U;
-    const long long nbase = (n + per - 1) / per;
-    long long* __restrict__ accx = pp.accx;
-    for (long long bb = blockIdx.x; bb < nbase; bb += gridDim.x) {  // block-uniform trip count
-        if (threadIdx.x == 0) { s_en = pl.acc && *(volatile unsigned*)pl_count(pl, par ^ 1) <= pl.thr; s_cnt = 0u; }
+    const bool dd = pl.acc && pl_valid(pl, par ^ 1);  // constant during the kernel
+    const int per = 256 * PP_U;
+    const int nbase = (int)((n + per - 1) / per);
+    const long long* __restrict__ accx = pp.accx;
+    for (int bb = blockIdx.x; bb < nbase; bb += gridDim.x) {  // block-uniform trip count
+        if (threadIdx.x == 0) {
+            s_en = pl.acc && *(volatile unsigned*)pl_count(pl, par ^ 1) <= pl.thr;
+            s_cnt = 0u;
+        }
         __syncthreads();
         const bool en = s_en;
-        // all loads of the PP_U columns first (independent, in flight together), then the updates
+        const int i0 = bb * per + PP_U * threadIdx.x;
         long long ai[PP_U];
-        double xi[PP_U], ci[PP_U];
+        T xi[PP_U], ci[PP_U], xbp[PP_U];
+        if (i0 + PP_U <= n) {
+            const longlong2 a01 = __ldg(reinterpret_cast<const longlong2*>(accx + i0));
+            const longlong2 a23 = __ldg(reinterpret_cast<const longlong2*>(accx + i0) + 1);
+            ai[0] = a01.x; ai[1] = a01.y; ai[2] = a23.x; ai[3] = a23.y;
+            ld4(xin + i0, xi);
+            ld4(cs + i0, ci);
+            if (dd) ld4(xbprev + i0, xbp);
+        } else {
 #pragma unroll
-        for (int u = 0; u < PP_U; ++u) {
-            const long long i = bb * per + u * 256 + threadIdx.x;
-            ai[u] = 0; xi[u] = 0.0; ci[u] = 0.0;
-            if (i < n) { ai[u] = __ldcs(accx + i); xi[u] = (double)xin[i]; ci[u] = (double)__ldg(cs + i); }
-        }
-#pragma unroll
-        for (int u = 0; u < PP_U; ++u) {
-            const long long i = bb * per + u * 256 + threadIdx.x;
-            bool nzb = false;
-            T xk = (T)0;
-            if (i < n) {
-                if (ai[u]) accx[i] = 0;
-                const double a = (double)ai[u] * invS;
-                double b = 0.0;
-                if constexpr (HASQ)
-                    for (long long q = __ldg(Q.ptr + i); q < __ldg(Q.ptr + i + 1); ++q)
-                        b += (double)__ldg(qs + q) * (double)__ldg(xin + __ldg(Q.idx + q));
-                const double delta = ((ci[u] + rho) - a) + 2.0 * b - 2.0 * rho * xi[u];
-                double xn = xi[u] - tau1 * delta;
-                xn = xn < 0.0 ? 0.0 : (xn > 1.0 ? 1.0 : xn);
-                xk = (T)xn;
-                xout[i] = xk;
-                const T xbn = (T)(2.0 * xn - xi[u]);
-                xbout[i] = xbn;
-                nzb = xbn != (T)0;
+            for (int u = 0; u < PP_U; ++u) {
+                const int i = i0 + u;
+                ai[u] = i < n ? accx[i] : 0;
+                xi[u] = i < n ? xin[i] : (T)0;
+                ci[u] = i < n ? cs[i] : (T)0;
+                xbp[u] = (dd && i < n) ? xbprev[i] : (T)0;
             }
-            if (en) warp_append(nzb, (int)i, &s_cnt, s_list);
-            if (accv && xk != (T)0) {
-                const long long v = __double2ll_rn((double)xk * 1099511627776.0);  // 2^40 fixed point
-                const bool one = xk == (T)1;
-                const long long q1 = __ldg(Kt.ptr + i + 1);
-                for (long long q = __ldg(Kt.ptr + i); q < q1; ++q) {
+        }
+        T xk[PP_U], xb[PP_U];
+#pragma unroll
+        for (int u = 0; u < PP_U; ++u) {
+            double b = 0.0;
+            if constexpr (HASQ)
+                if (i0 + u < n)
+                    for (long long q = __ldg(Q.ptr + i0 + u); q < __ldg(Q.ptr + i0 + u + 1); ++q)
+                        b += (double)__ldg(qs + q) * (double)__ldg(xin + __ldg(Q.idx + q));
+            const double x0 = (double)xi[u];
+            const double delta = (((double)ci[u] + rho) - (double)ai[u] * invS) + 2.0 * b - 2.0 * rho * x0;
+            double xn = x0 - tau1 * delta;
+            xn = xn < 0.0 ? 0.0 : (xn > 1.0 ? 1.0 : xn);
+            xk[u] = (T)xn;
+            xb[u] = (T)(2.0 * xn - x0);
+        }
+        if (i0 + PP_U <= n) {
+            st4(xout + i0, xk);
+            st4(xbout + i0, xb);
+        } else {
+#pragma unroll
+            for (int u = 0; u < PP_U; ++u)
+                if (i0 + u < n) { xout[i0 + u] = xk[u]; xbout[i0 + u] = xb[u]; }
+        }
+        if (en) {
+#pragma unroll
+            for (int u = 0; u < PP_U; ++u)
+                warp_append(i0 + u < n && pl_listed(dd, xb[u], xbp[u]), i0 + u, &s_cnt, s_list);
+        }
+        if (accv) {
+#pragma unroll
+            for (int u = 0; u < PP_U; ++u) {
+                if (i0 + u >= n || xk[u] == (T)0) continue;
+                const long long v = __double2ll_rn((double)xk[u] * 1099511627776.0);  // 2^40 fixed point
+                const bool one = xk[u] == (T)1;
+                const long long q1 = __ldg(Kt.ptr + i0 + u + 1);
+                for (long long q = __ldg(Kt.ptr + i0 + u); q < q1; ++q) {
                     const int r = __ldg(Kt.idx + q);
                     atomicAdd(reinterpret_cast<unsigned long long*>(accv + r), (unsigned long long)v);
                     if (one) atomicAdd(ones_cnt + r, 1u);

@@ -130,7 +130,8 @@ __global__ void __launch_bounds__(RB_NT) k_dual_rb(Csr K, const long long* __res
     const long long kk = iter_index(ctrl, kint, j);
     const int par = (int)(kk & 1);
     if (push_mode(pl, par)) return;  // sparse xbar: k_push_scatter/k_push_rows do this iteration
-    if (pl.acc && blockIdx.x == 0 && threadIdx.x == 0) push_reset_next(pl, par);
+    const bool clear_acc = pl.acc && pl_valid(pl, par);
+    if (pl.acc && blockIdx.x == 0 && threadIdx.x == 0) { push_reset_next(pl, par); pl_set_valid(pl, par ^ 1, false); }
     const T* __restrict__ xb = par ? s.xb[1] : s.xb[0];
     const T* __restrict__ yin = par ? s.y[1] : s.y[0];
     T* __restrict__ yout = par ? s.y[0] : s.y[1];
@@ -161,9 +162,11 @@ __global__ void __launch_bounds__(RB_NT) k_dual_rb(Csr K, const long long* __res
                 const double gj = g[row];
                 double yn = (double)yin[row] + tau2 * (rh[row] - gj * (sg * acc));
                 if (row < m1 && yn < 0.0) yn = 0.0;
-                yout[row] = (T)yn;
-                s.w[row] = (T)(gj * sg * yn);
+                const T yt = (T)yn;
+                yout[row] = yt;
+                s.w[row] = w_of(gj, sg, yt);
                 if (u_out) u_out[row] = sg * acc;  // (K_u xbar_{k-1})_j, kept for the trigger pass
+                if (clear_acc) pl.acc[row] = 0;    // delta-push accumulators are stale after a gather
             }
         }
         __syncthreads();
@@ -181,19 +184,21 @@ template <typename T, int KIND, bool HASQ>
 __global__ void __launch_bounds__(RB_NT, 6) k_primal_rb(Csr Kt, const long long* __restrict__ blk_row, long long nblk,
                                                      Csr Q, const T* __restrict__ qs, State<T> s,
                                                      const T* __restrict__ cs, const Ctrl* __restrict__ ctrl,
-                                                     long long kint, long long j, PushList pl, const unsigned* pp_rcount,
-                                                     unsigned pp_rthr) {
+                                                     long long kint, long long j, PushList pl, PushPrimal pp) {
     constexpr int NZ = RB_NNZ_OF<T>;
     __shared__ __align__(16) T sv[2][NZ];
     __shared__ unsigned s_cnt, s_base;
     __shared__ int s_list[RB_NT];
-    __shared__ bool s_en;
-    if (pp_rcount && *(volatile const unsigned*)pp_rcount <= pp_rthr) return;  // push-mode primal runs instead
+    __shared__ bool s_en, s_dd;
     const long long kk = iter_index(ctrl, kint, j);
     const int par = (int)(kk & 1);
+    if (pp_mode(pp, par).push) return;  // push-mode primal runs instead
+    const bool clear_accx = pp_valid(pp, par);  // delta-push accumulators are stale after a gather
+    if (pp.accx && blockIdx.x == 0 && threadIdx.x == 0) pp_set_next(pp, par, false, 0);
     const T* __restrict__ xin = par ? s.x[1] : s.x[0];
     T* __restrict__ xout = par ? s.x[0] : s.x[1];
     T* __restrict__ xbout = par ? s.xb[0] : s.xb[1];
+    const T* __restrict__ xbprev = par ? s.xb[1] : s.xb[0];
     const double rho = ctrl->rho, tau1 = ctrl->tau1;
     int st = 0;
     int nxt[NZ / RB_NT];
@@ -203,7 +208,10 @@ __global__ void __launch_bounds__(RB_NT, 6) k_primal_rb(Csr Kt, const long long*
     for (long long b = blockIdx.x; b < nblk; b += gridDim.x) {
         rb_issue(nxt, s.w, sv[st ^ 1]);
         rb_load_idx(Kt, blk_row, b + 2LL * gridDim.x, nblk, nxt);
-        if (threadIdx.x == 0) s_en = pl.acc && *(volatile unsigned*)pl_count(pl, par ^ 1) <= pl.thr;
+        if (threadIdx.x == 0) {
+            s_en = pl.acc && *(volatile unsigned*)pl_count(pl, par ^ 1) <= pl.thr;
+            s_dd = pl.acc && pl_valid(pl, par ^ 1);
+        }
         cp_async_wait1();
         __syncthreads();
         const long long r0 = blk_row[b], r1 = blk_row[b + 1];
@@ -211,7 +219,7 @@ __global__ void __launch_bounds__(RB_NT, 6) k_primal_rb(Csr Kt, const long long*
         const int nr = (int)(r1 - r0);
         const int G = rb_group_size(nr);
         const int lane = threadIdx.x & (G - 1), grp = threadIdx.x / G, ngr = RB_NT / G;
-        const bool en = s_en;
+        const bool en = s_en, dd = s_dd;
         for (int rb = 0; rb < nr; rb += ngr) {
             const int rr = rb + grp;
             const long long i = r0 + rr;
@@ -233,7 +241,8 @@ __global__ void __launch_bounds__(RB_NT, 6) k_primal_rb(Csr Kt, const long long*
                 xout[i] = (T)xn;
                 const T xbn = (T)(2.0 * xn - xi);
                 xbout[i] = xbn;
-                nz = xbn != (T)0;
+                nz = pl_listed(dd, xbn, dd ? xbprev[i] : (T)0);
+                if (clear_accx) pp.accx[i] = 0;
             }
             push_append<RB_NT>(pl, par ^ 1, nz, (int)i, en, &s_cnt, &s_base, s_list);
         }

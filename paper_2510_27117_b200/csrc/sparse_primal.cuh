@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(SP_NT, 1) k_primal_sparse(Csr Kt, const long l
     extern __shared__ __align__(16) unsigned char sp_smem[];
     __shared__ unsigned s_cnt, s_base;
     __shared__ int s_list[SP_NT];
-    __shared__ bool s_en;
+    __shared__ bool s_en, s_dd;
     T* svb = reinterpret_cast<T*>(sp_smem);                          // [2][SP_NNZ]
     unsigned* sbits = reinterpret_cast<unsigned*>(svb + 2 * SP_NNZ);  // [nwords]
     for (long long k = threadIdx.x; k < nwords; k += SP_NT) sbits[k] = __ldg(bits + k);
@@ -116,6 +116,7 @@ __global__ void __launch_bounds__(SP_NT, 1) k_primal_sparse(Csr Kt, const long l
     const T* __restrict__ xin = par ? s.x[1] : s.x[0];
     T* __restrict__ xout = par ? s.x[0] : s.x[1];
     T* __restrict__ xbout = par ? s.xb[0] : s.xb[1];
+    const T* __restrict__ xbprev = par ? s.xb[1] : s.xb[0];
     const double rho = ctrl->rho, tau1 = ctrl->tau1;
     int st = 0;
     int nxt[SP_U];
@@ -127,7 +128,10 @@ __global__ void __launch_bounds__(SP_NT, 1) k_primal_sparse(Csr Kt, const long l
         sp_issue<T>(nxt, s.w, sbits, svb + (st ^ 1) * SP_NNZ);
         sp_load_idx(Kt, blk_row, b + 2LL * gridDim.x, nblk, nxt);
         const SpRow nrow = sp_prefetch_row<T>(Kt, blk_row, b + gridDim.x, nblk, xin, cs);
-        if (threadIdx.x == 0) s_en = pl.acc && *(volatile unsigned*)pl_count(pl, par ^ 1) <= pl.thr;
+        if (threadIdx.x == 0) {
+            s_en = pl.acc && *(volatile unsigned*)pl_count(pl, par ^ 1) <= pl.thr;
+            s_dd = pl.acc && pl_valid(pl, par ^ 1);
+        }
         cp_async_wait1();
         __syncthreads();
         const T* sv = svb + st * SP_NNZ;
@@ -154,7 +158,7 @@ __global__ void __launch_bounds__(SP_NT, 1) k_primal_sparse(Csr Kt, const long l
             xout[i] = (T)xn;
             const T xbn = (T)(2.0 * xn - xi);
             xbout[i] = xbn;
-            nz = xbn != (T)0;
+            nz = pl_listed((bool)s_dd, xbn, s_dd ? xbprev[i] : (T)0);
         }
         push_append<SP_NT>(pl, par ^ 1, nz, (int)i, s_en, &s_cnt, &s_base, s_list);
         __syncthreads();
