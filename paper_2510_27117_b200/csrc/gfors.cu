@@ -323,6 +323,7 @@ struct gfors_ctx {
     DirPlan pd, pp;  // dual (rows of K), primal (rows of K') for the preprocessed precision
     DirPlan pdv[2], ppv[2];  // [0] fp32, [1] fp64 plans (row-block size differs)
     bool push_dual_ok = false, push_primal_ok = false;  // push modes allowed by the matrix
+    bool delta_dual = true;                             // delta push of the dual (GFORS_DELTA_DUAL=0: off)
     bool sparse_primal = false;     // primal skips gathers of zero duals (sparse_primal.cuh)
     long long* sp_blk_row = nullptr;
     long long sp_nblk = 0;
@@ -551,7 +552,7 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
     PushList pl{{nullptr, nullptr}, {nullptr, nullptr}, 0u, 0, nullptr, nullptr, nullptr};
     if (C->push_dual)
         pl = PushList{{C->d_plist[0], C->d_plist[1]}, {C->d_pcount, C->d_pcount + 1}, C->push_thr, C->n, C->d_acc,
-                      C->push_primal ? C->d_rcount : nullptr, C->push_primal ? C->d_wmax : nullptr, C->d_pflags};
+                      C->push_primal ? C->d_rcount : nullptr, C->push_primal ? C->d_wmax : nullptr, C->delta_dual ? C->d_pflags : nullptr};
     PushPrimal ppr{};
     if (C->push_primal)
         ppr = PushPrimal{C->d_rlist, C->d_rcount, C->rthr, C->d_wmax, C->d_accx, C->maxcoldeg, C->m,

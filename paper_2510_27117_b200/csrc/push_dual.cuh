@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(256) k_push_rows(long long m, PushList pl, Sta
     const double tau2 = ctrl->tau2;
     for (long long row = blockIdx.x * (long long)blockDim.x + threadIdx.x; row < m; row += gridDim.x * (long long)blockDim.x) {
         const long long a = pl.acc[row];
+        if (!pl.dvalid && a) pl.acc[row] = 0;
         const double sg = (double)rsign[row];
         const double u = sg * ((double)a * PUSH_INV);  // (K_u xbar_{k-1})_j
         const double gj = g[row];

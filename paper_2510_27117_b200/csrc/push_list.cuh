@@ -33,10 +33,13 @@ __device__ __forceinline__ unsigned* pl_count(const PushList& pl, int p) { retur
 __device__ __forceinline__ int* pl_list(const PushList& pl, int p) { return p ? pl.list[1] : pl.list[0]; }
 
 // delta state the dual of parity p starts from (block-uniform)
+// (dvalid == nullptr: delta push disabled, GFORS_DELTA_DUAL=0 — accumulators cleared after each use)
 __device__ __forceinline__ bool pl_valid(const PushList& pl, int p) {
-    return *(volatile unsigned*)(p ? pl.dvalid + 1 : pl.dvalid) != 0u;
+    return pl.dvalid && *(volatile unsigned*)(p ? pl.dvalid + 1 : pl.dvalid) != 0u;
 }
-__device__ __forceinline__ void pl_set_valid(const PushList& pl, int p, bool v) { (p ? pl.dvalid[1] : pl.dvalid[0]) = v ? 1u : 0u; }
+__device__ __forceinline__ void pl_set_valid(const PushList& pl, int p, bool v) {
+    if (pl.dvalid) (p ? pl.dvalid[1] : pl.dvalid[0]) = v ? 1u : 0u;
+}
 
 // list criterion of the primal (parity p writes the list of the dual of parity p^1): with valid
 // accumulators the changed columns, else the nonzero ones
