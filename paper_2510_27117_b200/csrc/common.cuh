@@ -6,6 +6,9 @@
 
 namespace gfors {
 
+constexpr int NUM_SMS_B200 = 148;  // B200 SM count: grids are sized in multiples of it
+
+
 // Storage class of a sparse matrix's values (chosen at load).
 //  SIGN: every value of row j equals rsign[j] in {+1,-1}  -> no value array at all
 //  I8  : integral values with |v| <= 127                   -> int8 per nonzero

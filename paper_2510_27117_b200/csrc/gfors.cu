@@ -39,7 +39,6 @@ using namespace gfors;
 namespace {
 
 constexpr int NT = 256;
-constexpr int NUM_SMS_B200 = 148;
 constexpr int RB_GRID = NUM_SMS_B200 * 8;
 
 struct Err {
@@ -324,6 +323,9 @@ struct gfors_ctx {
     DirPlan pdv[2], ppv[2];  // [0] fp32, [1] fp64 plans (row-block size differs)
     bool push_dual_ok = false, push_primal_ok = false;  // push modes allowed by the matrix
     bool delta_dual = true;                             // delta push of the dual (GFORS_DELTA_DUAL=0: off)
+    bool xskip = true;                                  // stationary-column skip (GFORS_XSKIP=0: off)
+    unsigned mark_rows = 0;
+    unsigned char* d_xst = nullptr;                     // [n] stationarity counters (push_primal.cuh)
     bool sparse_primal = false;     // primal skips gathers of zero duals (sparse_primal.cuh)
     long long* sp_blk_row = nullptr;
     long long sp_nblk = 0;
@@ -461,7 +463,7 @@ void gfors_ctx::free_problem() {
 void gfors_ctx::free_prep() {
     void** ps[] = {(void**)&d_s, &d_g, &d_rh, &d_cs, &d_qs, &d_x[0], &d_x[1], &d_xb[0], &d_xb[1], &d_y[0], &d_y[1],
                    &d_w, (void**)&d_tmp[0], (void**)&d_tmp[1], (void**)&d_tmp[2], (void**)&d_tmp[3],
-                   (void**)&d_red, (void**)&d_scalar, (void**)&d_segpart, (void**)&d_segpart2, (void**)&d_u, (void**)&d_ones, (void**)&d_rec, (void**)&d_regen, (void**)&d_plist[0], (void**)&d_plist[1], (void**)&d_pcount, (void**)&d_pflags, (void**)&d_acc, (void**)&d_rlist, (void**)&d_rcount, (void**)&d_wmax, (void**)&d_accx, (void**)&d_accv, (void**)&d_ones_cnt, (void**)&d_trig_flag, (void**)&d_part1,
+                   (void**)&d_red, (void**)&d_scalar, (void**)&d_segpart, (void**)&d_segpart2, (void**)&d_u, (void**)&d_ones, (void**)&d_rec, (void**)&d_regen, (void**)&d_plist[0], (void**)&d_plist[1], (void**)&d_pcount, (void**)&d_pflags, (void**)&d_acc, (void**)&d_rlist, (void**)&d_rcount, (void**)&d_wmax, (void**)&d_accx, (void**)&d_xst, (void**)&d_accv, (void**)&d_ones_cnt, (void**)&d_trig_flag, (void**)&d_part1,
                    (void**)&d_part2, (void**)&d_hist, (void**)&d_rho, (void**)&d_trace, (void**)&d_xbest,
                    (void**)&d_X, (void**)&d_viol, (void**)&d_iacc, &d_zpart, (void**)&d_z, (void**)&d_ctrl};
     for (void** p : ps) { dfree(*p); *p = nullptr; }
@@ -556,7 +558,8 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
     PushPrimal ppr{};
     if (C->push_primal)
         ppr = PushPrimal{C->d_rlist, C->d_rcount, C->rthr, C->d_wmax, C->d_accx, C->maxcoldeg, C->m,
-                         C->d_pflags + 2, reinterpret_cast<int*>(C->d_pflags + 4), (const double*)C->d_g, C->d_rsign};
+                         C->d_pflags + 2, reinterpret_cast<int*>(C->d_pflags + 4), (const double*)C->d_g, C->d_rsign,
+                         C->d_xst, C->mark_rows};
     const Ctrl* ctrl = C->d_ctrl;
     const double* g = (const double*)C->d_g;
     const double* rh = (const double*)C->d_rh;
@@ -599,10 +602,10 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
         LAUNCH(C, s, KC_PRIMAL_PUSH, (k_wlist<T><<<grid_for(C->m), NT, 0, s>>>(st, ppr, ctrl, kint, j)));
         LAUNCH(C, s, KC_PRIMAL_PUSH, (k_push_scatter_cols<T><<<grid_for(C->m * 32LL), NT, 0, s>>>(csr_K(C), ppr, st, ctrl, kint, j)));
         if (C->hasq)
-            LAUNCH(C, s, KC_PRIMAL_PUSH, (k_primal_push<T, true><<<pp_grid(C->n), NT, 0, s>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
+            LAUNCH(C, s, KC_PRIMAL_PUSH, (k_primal_push<T, true><<<pp_grid<T>(C->n), NT, 0, s>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
                 csr_Kt(C), trig_push ? C->d_accv : nullptr, C->d_ones_cnt, C->d_trig_flag)));
         else
-            LAUNCH(C, s, KC_PRIMAL_PUSH, (k_primal_push<T, false><<<pp_grid(C->n), NT, 0, s>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
+            LAUNCH(C, s, KC_PRIMAL_PUSH, (k_primal_push<T, false><<<pp_grid<T>(C->n), NT, 0, s>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
                 csr_Kt(C), trig_push ? C->d_accv : nullptr, C->d_ones_cnt, C->d_trig_flag)));
     }
     if (C->sparse_primal && !C->push_primal && sparse_primal_smem<T>(C->m) <= SP_DYN_MAX) {
@@ -934,6 +937,7 @@ static void reset_push(gfors_ctx* C, cudaStream_t s) {
     if (C->push_primal) {
         CK(cudaMemsetAsync(C->d_rcount, 0, sizeof(unsigned), s));
         CK(cudaMemsetAsync(C->d_accx, 0, C->n * sizeof(long long), s));
+        if (C->d_xst) CK(cudaMemsetAsync(C->d_xst, 0, C->n, s));
     }
 }
 
@@ -1031,6 +1035,10 @@ static void do_preprocess(gfors_ctx* C, const gfors_prep_opts* o, gfors_scaling*
         C->d_rcount = dalloc<unsigned>(1);
         C->d_wmax = dalloc<unsigned long long>(1);
         C->d_accx = dalloc<long long>(n);
+        if (C->xskip) {
+            C->d_xst = dalloc<unsigned char>(n + 4);
+            CK(cudaMemsetAsync(C->d_xst, 0, n + 4, s));
+        }
         CK(cudaMemsetAsync(C->d_rcount, 0xff, sizeof(unsigned), s));
         CK(cudaMemsetAsync(C->d_wmax, 0, sizeof(unsigned long long), s));
         CK(cudaMemsetAsync(C->d_accx, 0, n * sizeof(long long), s));

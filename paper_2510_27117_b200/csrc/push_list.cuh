@@ -94,6 +94,8 @@ struct PushPrimal {
     int* pe;                   // [2] scale exponent of the valid accx
     const double* g;           // row scale (w_{k-1} recomputed from y_{k-1}, pdhg.cuh w_of)
     const signed char* rsign;
+    unsigned char* xst;        // [n] stationary-column counters (k_primal_push skip), null = off
+    unsigned mark_rows;        // delta scatters of <= mark_rows rows mark the columns they touch
 };
 
 constexpr int PP_HEAD = 8;     // headroom bits at a re-base
@@ -126,6 +128,12 @@ __device__ __forceinline__ PPMode pp_mode(const PushPrimal& pp, int par) {
         r.push = cnt <= pp.rthr;
     }
     return r;
+}
+
+// the delta scatter of this iteration marks touched columns (xst = 0), so the push primal may skip
+// the columns it leaves untouched; both kernels take the decision from the same device state
+__device__ __forceinline__ bool pp_marking(const PushPrimal& pp, const PPMode& md) {
+    return pp.xst && md.push && md.delta && *(volatile unsigned*)pp.rcount <= pp.mark_rows;
 }
 
 // state the next primal starts from (written by thread 0 of block 0 of the active primal kernel)

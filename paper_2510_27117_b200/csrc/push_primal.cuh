@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(256) k_push_scatter_cols(Csr K, PushPrimal pp,
     const int par = (int)(iter_index(ctrl, kint, jj) & 1);
     const PPMode md = pp_mode(pp, par);
     if (!md.push) return;
+    const bool mark = pp_marking(pp, md);
     const double S = pow2(md.e);
     const T* __restrict__ yold = par ? s.y[1] : s.y[0];
     const long long cnt = *pp.rcount;
@@ -72,11 +73,25 @@ __global__ void __launch_bounds__(256) k_push_scatter_cols(Csr K, PushPrimal pp,
         if (md.delta) v -= __double2ll_rn((double)w_of(pp.g[jr], (double)pp.rsign[jr], yold[jr]) * S);
         if (v == 0) continue;
         const long long q1 = __ldg(K.ptr + jr + 1);
-        for (long long q = __ldg(K.ptr + jr) + lane; q < q1; q += 32)
-            atomicAdd(reinterpret_cast<unsigned long long*>(pp.accx + __ldg(K.idx + q)), (unsigned long long)v);
+        for (long long q = __ldg(K.ptr + jr) + lane; q < q1; q += 32) {
+            const int i = __ldg(K.idx + q);
+            atomicAdd(reinterpret_cast<unsigned long long*>(pp.accx + i), (unsigned long long)v);
+            if (mark) pp.xst[i] = 0;
+        }
     }
 }
 
+// Stationary columns.  The update of column i is a function xn_k = F(x_{k-1}, a_k, rho) (double,
+// before rounding to T), x_k = (T)xn_k, xbar_k = (T)(2 xn_k - x_{k-1}).  Iteration k has "the same
+// inputs" as k-1 when rho is unchanged (not the first iteration of a loop block, not hook mode),
+// a_k = a_{k-1} (delta push with the same exponent, and the marking scatter left accx_i alone — a
+// touched column has xst_i cleared) and there is no Q (b depends on other columns).  xst_i = 2
+// certifies x_k = x_{k-1} = x_{k-2} and xn_k = xn_{k-1} (same inputs at k); then, if iteration k+1
+// has the same inputs again, xn_{k+1} = xn_k, so x_{k+1} = x_{k-1} and xbar_{k+1} = xbar_{k-1} —
+// exactly what the output buffers of iteration k+1 already hold — and the column is skipped:
+// bit-identical, 1 byte read instead of 24-28.  xst_i = 1: x_k = x_{k-1} only; 0: changed/touched.
+// Skipping also needs: not the trigger iteration (it pushes every x_k), and no value of a skipped
+// column for the next dual's list (delta list, where an unchanged column is not listed, or none).
 // push mode: x_k = Pi(x_{k-1} - tau1 (c + rho - a + 2 Q x_{k-1} - 2 rho x_{k-1})), xbar_k = 2x_k - x_{k-1},
 // with a = accx / S (accumulators kept for the next delta push); also hands the nonzero (or, with
 // valid dual accumulators, the changed) xbar columns to the next dual (PushList).  A pure stream over
@@ -84,6 +99,8 @@ __global__ void __launch_bounds__(256) k_push_scatter_cols(Csr K, PushPrimal pp,
 // and moves them with 16-byte vector loads/stores (one instruction per array for fp32), the
 // block-staged list append is amortised over 256*PP_U columns.
 constexpr int PP_U = 4;
+constexpr int PP_LPASSES = 4;  // passes staged in shared memory between list flushes
+constexpr int PP_OCC32 = 5, PP_OCC64 = 4;  // resident CTAs per SM (launch bounds, persistent grid)
 
 template <typename T>
 __device__ __forceinline__ void ld4(const T* __restrict__ p, T (&o)[PP_U]) {
@@ -105,17 +122,23 @@ __device__ __forceinline__ void st4(T* __restrict__ p, const T (&v)[PP_U]) {
     }
 }
 
-// one CTA per 256*PP_U columns (no grid-stride tail imbalance; the scheduler balances the CTAs)
-inline int pp_grid(long long n) { return (int)std::max<long long>(1, std::min<long long>((n + 256 * PP_U - 1) / (256 * PP_U), 1LL << 30)); }
+// persistent grid (one wave at the occupancy the launch bounds give): the per-CTA prologue (mode,
+// flags — a chain of dependent loads) is paid once, not per 1024 columns; matters when most columns
+// are skipped
+template <typename T>
+inline int pp_grid(long long n) {
+    const long long passes = (n + 256 * PP_U - 1) / (256 * PP_U);
+    return (int)std::max<long long>(1, std::min<long long>(passes, (long long)NUM_SMS_B200 * (sizeof(T) == 4 ? PP_OCC32 : PP_OCC64)));
+}
 
 template <typename T, bool HASQ>
-__global__ void __launch_bounds__(256, sizeof(T) == 4 ? 6 : 4) k_primal_push(long long n, PushPrimal pp, Csr Q, const T* __restrict__ qs,
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? PP_OCC32 : PP_OCC64) k_primal_push(long long n, PushPrimal pp, Csr Q, const T* __restrict__ qs,
                                                      State<T> s, const T* __restrict__ cs, const Ctrl* __restrict__ ctrl,
                                                      long long kint, long long j, PushList pl, Csr Kt,
                                                      long long* __restrict__ accv, unsigned* __restrict__ ones_cnt,
                                                      unsigned* __restrict__ trig_flag) {
     __shared__ unsigned s_cnt, s_base;
-    __shared__ int s_list[256 * PP_U];
+    __shared__ int s_list[PP_LPASSES * 256 * PP_U];
     __shared__ bool s_en;
     const long long kk = iter_index(ctrl, kint, j);
     const int par = (int)(kk & 1);
@@ -134,85 +157,124 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 6 : 4) k_primal_push(lon
     const T* __restrict__ xbprev = par ? s.xb[1] : s.xb[0];  // xbar_{k-1} (delta list of the next dual)
     const double rho = ctrl->rho, tau1 = ctrl->tau1;
     const bool dd = pl.acc && pl_valid(pl, par ^ 1);  // constant during the kernel
+    const bool track = !HASQ && kint > 0 && j > 0 && pp_marking(pp, md);  // same inputs as iteration k-1
+    const bool skip = track && accv == nullptr && (pl.acc == nullptr || dd);
+    unsigned char* __restrict__ xst = pp.xst;
     const int per = 256 * PP_U;
     const int nbase = (int)((n + per - 1) / per);
     const long long* __restrict__ accx = pp.accx;
+    // list the columns of the next dual while it can still be short (read once; the list has room
+    // for every column, so appending past the threshold only wastes a little work)
+    if (threadIdx.x == 0) {
+        s_en = pl.acc && *(volatile unsigned*)pl_count(pl, par ^ 1) <= pl.thr;
+        s_cnt = 0u;
+    }
+    __syncthreads();
+    const bool en = s_en;
+    uchar4 st_next = make_uchar4(0, 0, 0, 0);
+    if (xst && (long long)blockIdx.x * per + PP_U * (threadIdx.x + 1) <= n)
+        st_next = *reinterpret_cast<const uchar4*>(xst + (long long)blockIdx.x * per + PP_U * threadIdx.x);
+    int npass = 0;
     for (int bb = blockIdx.x; bb < nbase; bb += gridDim.x) {  // block-uniform trip count
-        if (threadIdx.x == 0) {
-            s_en = pl.acc && *(volatile unsigned*)pl_count(pl, par ^ 1) <= pl.thr;
-            s_cnt = 0u;
-        }
-        __syncthreads();
-        const bool en = s_en;
         const int i0 = bb * per + PP_U * threadIdx.x;
-        long long ai[PP_U];
-        T xi[PP_U], ci[PP_U], xbp[PP_U];
-        if (i0 + PP_U <= n) {
-            const longlong2 a01 = __ldg(reinterpret_cast<const longlong2*>(accx + i0));
-            const longlong2 a23 = __ldg(reinterpret_cast<const longlong2*>(accx + i0) + 1);
-            ai[0] = a01.x; ai[1] = a01.y; ai[2] = a23.x; ai[3] = a23.y;
-            ld4(xin + i0, xi);
-            ld4(cs + i0, ci);
-            if (dd) ld4(xbprev + i0, xbp);
-        } else {
+        const uchar4 st4v = st_next;  // loaded one pass ahead
+        {
+            const long long i1 = (long long)(bb + gridDim.x) * per + PP_U * threadIdx.x;
+            if (xst && i1 + PP_U <= n) st_next = *reinterpret_cast<const uchar4*>(xst + i1);
+        }
+        // the 4 columns are stationary and untouched: nothing to compute or write (see above)
+        const bool skip4 = skip && i0 + PP_U <= n && st4v.x == 2 && st4v.y == 2 && st4v.z == 2 && st4v.w == 2;
+        T xb[PP_U] = {}, xbp[PP_U] = {};
+        if (!skip4) {
+            long long ai[PP_U];
+            T xi[PP_U], ci[PP_U], xk[PP_U];
+            if (i0 + PP_U <= n) {
+                const longlong2 a01 = __ldg(reinterpret_cast<const longlong2*>(accx + i0));
+                const longlong2 a23 = __ldg(reinterpret_cast<const longlong2*>(accx + i0) + 1);
+                ai[0] = a01.x; ai[1] = a01.y; ai[2] = a23.x; ai[3] = a23.y;
+                ld4(xin + i0, xi);
+                ld4(cs + i0, ci);
+                if (dd) ld4(xbprev + i0, xbp);
+            } else {
 #pragma unroll
-            for (int u = 0; u < PP_U; ++u) {
-                const int i = i0 + u;
-                ai[u] = i < n ? accx[i] : 0;
-                xi[u] = i < n ? xin[i] : (T)0;
-                ci[u] = i < n ? cs[i] : (T)0;
-                xbp[u] = (dd && i < n) ? xbprev[i] : (T)0;
+                for (int u = 0; u < PP_U; ++u) {
+                    const int i = i0 + u;
+                    ai[u] = i < n ? accx[i] : 0;
+                    xi[u] = i < n ? xin[i] : (T)0;
+                    ci[u] = i < n ? cs[i] : (T)0;
+                    xbp[u] = (dd && i < n) ? xbprev[i] : (T)0;
+                }
             }
-        }
-        T xk[PP_U], xb[PP_U];
-#pragma unroll
-        for (int u = 0; u < PP_U; ++u) {
-            double b = 0.0;
-            if constexpr (HASQ)
-                if (i0 + u < n)
-                    for (long long q = __ldg(Q.ptr + i0 + u); q < __ldg(Q.ptr + i0 + u + 1); ++q)
-                        b += (double)__ldg(qs + q) * (double)__ldg(xin + __ldg(Q.idx + q));
-            const double x0 = (double)xi[u];
-            const double delta = (((double)ci[u] + rho) - (double)ai[u] * invS) + 2.0 * b - 2.0 * rho * x0;
-            double xn = x0 - tau1 * delta;
-            xn = xn < 0.0 ? 0.0 : (xn > 1.0 ? 1.0 : xn);
-            xk[u] = (T)xn;
-            xb[u] = (T)(2.0 * xn - x0);
-        }
-        if (i0 + PP_U <= n) {
-            st4(xout + i0, xk);
-            st4(xbout + i0, xb);
-        } else {
-#pragma unroll
-            for (int u = 0; u < PP_U; ++u)
-                if (i0 + u < n) { xout[i0 + u] = xk[u]; xbout[i0 + u] = xb[u]; }
-        }
-        if (en) {
-#pragma unroll
-            for (int u = 0; u < PP_U; ++u)
-                warp_append(i0 + u < n && pl_listed(dd, xb[u], xbp[u]), i0 + u, &s_cnt, s_list);
-        }
-        if (accv) {
 #pragma unroll
             for (int u = 0; u < PP_U; ++u) {
-                if (i0 + u >= n || xk[u] == (T)0) continue;
-                const long long v = __double2ll_rn((double)xk[u] * 1099511627776.0);  // 2^40 fixed point
-                const bool one = xk[u] == (T)1;
-                const long long q1 = __ldg(Kt.ptr + i0 + u + 1);
-                for (long long q = __ldg(Kt.ptr + i0 + u); q < q1; ++q) {
-                    const int r = __ldg(Kt.idx + q);
-                    atomicAdd(reinterpret_cast<unsigned long long*>(accv + r), (unsigned long long)v);
-                    if (one) atomicAdd(ones_cnt + r, 1u);
+                double b = 0.0;
+                if constexpr (HASQ)
+                    if (i0 + u < n)
+                        for (long long q = __ldg(Q.ptr + i0 + u); q < __ldg(Q.ptr + i0 + u + 1); ++q)
+                            b += (double)__ldg(qs + q) * (double)__ldg(xin + __ldg(Q.idx + q));
+                const double x0 = (double)xi[u];
+                const double delta = (((double)ci[u] + rho) - (double)ai[u] * invS) + 2.0 * b - 2.0 * rho * x0;
+                double xn = x0 - tau1 * delta;
+                xn = xn < 0.0 ? 0.0 : (xn > 1.0 ? 1.0 : xn);
+                xk[u] = (T)xn;
+                xb[u] = (T)(2.0 * xn - x0);
+            }
+            if (xst) {
+                // stationarity state of the computed columns (a gather-mode primal does not keep it:
+                // the iteration after one is never "same inputs", so xst restarts at <= 1)
+                unsigned char sv[PP_U] = {st4v.x, st4v.y, st4v.z, st4v.w};
+                if (i0 + PP_U > n)
+                    for (int u = 0; u < PP_U; ++u) sv[u] = i0 + u < n ? xst[i0 + u] : 0;
+                bool ch = false;
+                for (int u = 0; u < PP_U; ++u) {
+                    const unsigned char nv = xk[u] != xi[u] ? 0 : ((track && sv[u] >= 1) ? 2 : 1);
+                    ch |= nv != sv[u];
+                    sv[u] = nv;
+                }
+                if (ch) {
+                    if (i0 + PP_U <= n) *reinterpret_cast<uchar4*>(xst + i0) = make_uchar4(sv[0], sv[1], sv[2], sv[3]);
+                    else for (int u = 0; u < PP_U; ++u) if (i0 + u < n) xst[i0 + u] = sv[u];
+                }
+            }
+            if (i0 + PP_U <= n) {
+                st4(xout + i0, xk);
+                st4(xbout + i0, xb);
+            } else {
+#pragma unroll
+                for (int u = 0; u < PP_U; ++u)
+                    if (i0 + u < n) { xout[i0 + u] = xk[u]; xbout[i0 + u] = xb[u]; }
+            }
+            if (accv) {
+#pragma unroll
+                for (int u = 0; u < PP_U; ++u) {
+                    if (i0 + u >= n || xk[u] == (T)0) continue;
+                    const long long v = __double2ll_rn((double)xk[u] * 1099511627776.0);  // 2^40 fixed point
+                    const bool one = xk[u] == (T)1;
+                    const long long q1 = __ldg(Kt.ptr + i0 + u + 1);
+                    for (long long q = __ldg(Kt.ptr + i0 + u); q < q1; ++q) {
+                        const int r = __ldg(Kt.idx + q);
+                        atomicAdd(reinterpret_cast<unsigned long long*>(accv + r), (unsigned long long)v);
+                        if (one) atomicAdd(ones_cnt + r, 1u);
+                    }
                 }
             }
         }
-        __syncthreads();
         if (en) {
+#pragma unroll
+            for (int u = 0; u < PP_U; ++u)
+                warp_append(!skip4 && i0 + u < n && pl_listed(dd, xb[u], xbp[u]), i0 + u, &s_cnt, s_list);
+        }
+        // flush the staged list every PP_LPASSES passes and at the end (block-uniform decision)
+        if (en && (++npass == PP_LPASSES || bb + (int)gridDim.x >= nbase)) {
+            npass = 0;
+            __syncthreads();
             if (threadIdx.x == 0) s_base = s_cnt ? atomicAdd(pl_count(pl, par ^ 1), s_cnt) : 0u;
             __syncthreads();
             const unsigned c = s_cnt, base = s_base;
             for (unsigned t = threadIdx.x; t < c; t += 256)
                 if ((long long)base + t < pl.cap) pl_list(pl, par ^ 1)[base + t] = s_list[t];
+            __syncthreads();
+            if (threadIdx.x == 0) s_cnt = 0u;
             __syncthreads();
         }
     }

@@ -403,20 +403,22 @@ def test_push_primal_variant_parity(gf, fam, prec, tol, monkeypatch):
         assert zg == zo or (math.isinf(zg) and math.isinf(zo))
 
 
+@pytest.mark.parametrize("switch", ["GFORS_DELTA_DUAL", "GFORS_XSKIP"])
 @pytest.mark.parametrize("fam", ["setcover", "mis"])
 @pytest.mark.parametrize("prec", [64, 32])
-def test_delta_push_dual_bit_identical(gf, fam, prec, monkeypatch):
-    """Delta push of the dual (only changed xbar columns scattered, accumulators kept) adds exact
-    integer differences, so it must reproduce the plain push dual BIT FOR BIT: same iterates after
-    hook steps and the same run trace/incumbent (push modes forced on, primal delta in both)."""
+def test_exact_shortcuts_bit_identical(gf, switch, fam, prec, monkeypatch):
+    """Two shortcuts must reproduce the plain computation BIT FOR BIT (push modes forced on):
+    GFORS_DELTA_DUAL — the delta push of the dual adds exact integer differences instead of a fresh
+    fixed-point sum; GFORS_XSKIP — the push primal skips columns whose update provably returns the
+    value already stored.  Same iterates after hook steps, same run trace and incumbent."""
     monkeypatch.setenv("GFORS_PUSH_DUAL", "1")
     monkeypatch.setenv("GFORS_PUSH_PRIMAL", "1")
     inst = G.SMALL[fam](14)
     tau = math.sqrt(0.99)
     rho = O.rho_schedule(1e-3, 10.0, 100.0, 2.0, 1e-6, 60)
     out = []
-    for delta in ("0", "1"):
-        monkeypatch.setenv("GFORS_DELTA_DUAL", delta)
+    for on in ("0", "1"):
+        monkeypatch.setenv(switch, on)
         s = gf.Solver(0)
         s.load(inst)
         s.preprocess(precision=prec, tol=1e-10, max_iter=5000)
@@ -424,7 +426,7 @@ def test_delta_push_dual_bit_identical(gf, fam, prec, monkeypatch):
         for b in range(60):
             s.step(10, rho[b], tau, tau)
         st = s.get_state()
-        info = s.run(max_iters=600, tol_primal=-1.0, tol_dual=-1.0, tol_binary=-1.0, stall_rel=-1.0)
+        info = s.run(max_iters=2000, tol_primal=-1.0, tol_dual=-1.0, tol_binary=-1.0, stall_rel=-1.0)
         out.append((st, s.trace(), s.best_incumbent(), info["iters"]))
     (sa, ta, za, ia), (sb, tb, zb, ib) = out
     for u, v in zip(sa, sb):
