@@ -316,7 +316,6 @@ def run_gpu(args):
 
     # per-kernel device times (CUDA events around every launch of an eager replay of the same blocks)
     prof = s.profile_blocks(args.profile_blocks or args.steps, **common)
-    launches = s.launches_per_block(**common)
     step_ms = sum(prof.values())
     byt = algorithmic_bytes(meta, fb)
     act = s.profile_active()  # class -> (active ms over all profiled blocks, launches that did work)
@@ -412,7 +411,7 @@ def run_gpu(args):
             "kernel_active": {k: {"active_launches": v[1], "avg_active_ms": (v[0] / v[1]) if v[1] else None}
                               for k, v in act.items()},
             "clocks": clocks,
-            "gpu_launches": int(launches * args.steps + 8),
+            "gpu_launches": int(info["launches"]),
             "e2e": e2e,
             "cpu_baseline": cpu,
             "time_to_incumbent_small_configs": tti,

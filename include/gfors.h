@@ -110,6 +110,8 @@ typedef struct {
     int32_t halt_reason;
     double elapsed_s;   /* device time of the loop (CUDA events), Preprocess excluded */
     int64_t n_trace;    /* trace rows written (ring keeps the last trace_cap) */
+    int64_t launches;   /* kernels this call launched (graph mode: unconditional nodes per block x blocks
+                           + the kernels of the conditional branches taken, counted on the device) */
 } gfors_run_info;
 
 typedef struct {

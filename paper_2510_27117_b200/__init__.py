@@ -67,7 +67,7 @@ class Params(C.Structure):
 
 class RunInfo(C.Structure):
     _fields_ = [("iters", I64), ("rounds", I64), ("candidates", I64), ("halt_reason", I32),
-                ("elapsed_s", D), ("n_trace", I64)]
+                ("elapsed_s", D), ("n_trace", I64), ("launches", I64)]
 
 
 class IncumbentInfo(C.Structure):

@@ -36,6 +36,7 @@ struct Ctrl {
     int win_lane;           // winning lane of the last argmin (-1 none)
     int pad0;
     double ind[4];          // primal_gap, ||s^x||, ||s^y||, binary_gap of the last trigger
+    long long dyn_launches; // kernels of the conditional branches taken (graph mode launch count)
 };
 
 struct HaltPar {

@@ -326,6 +326,11 @@ struct gfors_ctx {
     bool xskip = true;                                  // stationary-column skip (GFORS_XSKIP=0: off)
     unsigned mark_rows = 0;
     unsigned char* d_xst = nullptr;                     // [n] stationarity counters (push_primal.cuh)
+    bool capturing = false;                             // enqueueing into the graph capture (branch())
+    bool cond_branch = false;                           // conditional-node mode branches (GFORS_COND_BRANCH=1)
+    bool dry = false;                                   // LAUNCH counts only
+    cudaStream_t cap_stream2 = nullptr;                 // captures the conditional branch bodies
+    long long gstatic = 0;                              // unconditional launches per block of the graph
     bool sparse_primal = false;     // primal skips gathers of zero duals (sparse_primal.cuh)
     long long* sp_blk_row = nullptr;
     long long sp_nblk = 0;
@@ -482,6 +487,7 @@ gfors_ctx::~gfors_ctx() {
     free_problem();
     if (comm) nccl().CommDestroy(comm);
     if (cap_stream) cudaStreamDestroy(cap_stream);
+    if (cap_stream2) cudaStreamDestroy(cap_stream2);
     if (own_stream && stream) cudaStreamDestroy(stream);
 }
 
@@ -514,12 +520,81 @@ inline void prof_end(gfors_ctx* C, cudaStream_t s, int cls, cudaEvent_t a) {
 }
 #define LAUNCH(C, s, cls, ...)                                   \
     do {                                                         \
+        if ((C)->dry) { (C)->launches++; break; } /* count only */ \
         cudaEvent_t ev_a__ = nullptr;                            \
         prof_begin((C), (s), (cls), &ev_a__);                    \
         __VA_ARGS__;                                             \
         CK(cudaGetLastError());                                  \
         prof_end((C), (s), (cls), ev_a__);                       \
     } while (0)
+
+// Mode branch (dual: gather vs push; primal: gather vs push; trigger pass: gather vs pushed).  By
+// default both branches are launched and every kernel checks the device decision itself and exits
+// at once when it is not the chosen one.  GFORS_COND_BRANCH=1: in the graph capture a one-thread
+// decide kernel sets the handle of an IF/ELSE conditional node instead, so only the chosen kernels
+// run (counted on the device, ctrl->dyn_launches) — measured SLOWER on config 5 (2.66 vs 2.55 ms
+// per block: 31 conditional nodes per block cost more than the early exits they replace).
+template <class Dec, class A, class B>
+void branch(gfors_ctx* C, cudaStream_t s, Dec decide, A then_, B else_) {
+    if (!C->capturing || C->dry || !C->cond_branch) {
+        else_(s);  // (trigger pass: the gather branch's partial fill must precede the pushed pass)
+        then_(s);
+        return;
+    }
+    const long long l0 = C->launches;
+    C->dry = true;
+    then_(s);
+    const int nthen = (int)(C->launches - l0);
+    else_(s);
+    const int nelse = (int)(C->launches - l0) - nthen;
+    C->dry = false;
+    C->launches = l0;
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t cg;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    CK(cudaStreamGetCaptureInfo(s, &cs, nullptr, &cg, &deps, &nd));
+    cudaGraphConditionalHandle h;
+    CK(cudaGraphConditionalHandleCreate(&h, cg, 0, cudaGraphCondAssignDefault));
+    decide(s, h, nthen, nelse);
+    C->launches++;
+    CK(cudaStreamGetCaptureInfo(s, &cs, nullptr, &cg, &deps, &nd));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeIf;
+    cp.conditional.size = 2;  // [0] then, [1] else
+    cudaGraphNode_t node;
+    CK(cudaGraphAddNode(&node, cg, deps, nd, &cp));
+    cudaGraph_t bodies[2] = {cp.conditional.phGraph_out[0], cp.conditional.phGraph_out[1]};
+    if (!C->cap_stream2) CK(cudaStreamCreateWithFlags(&C->cap_stream2, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+        CK(cudaStreamBeginCaptureToGraph(C->cap_stream2, bodies[b], nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+        if (b == 0) then_(C->cap_stream2); else else_(C->cap_stream2);
+        cudaGraph_t g2;
+        CK(cudaStreamEndCapture(C->cap_stream2, &g2));
+    }
+    C->launches = l0 + 1;  // the branch kernels are counted on the device
+    CK(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
+}
+
+__global__ void k_decide_dual(PushList pl, Ctrl* ctrl, long long kint, long long j, cudaGraphConditionalHandle h,
+                              int nthen, int nelse) {
+    const bool push = push_mode(pl, (int)(iter_index(ctrl, kint, j) & 1));
+    ctrl->dyn_launches += push ? nthen : nelse;
+    cudaGraphSetConditional(h, push ? 1u : 0u);
+}
+__global__ void k_decide_primal(PushPrimal pp, Ctrl* ctrl, long long kint, long long j, cudaGraphConditionalHandle h,
+                                int nthen, int nelse) {
+    const bool push = pp_mode(pp, (int)(iter_index(ctrl, kint, j) & 1)).push;
+    ctrl->dyn_launches += push ? nthen : nelse;
+    cudaGraphSetConditional(h, push ? 1u : 0u);
+}
+__global__ void k_decide_flag(const unsigned* flag, Ctrl* ctrl, cudaGraphConditionalHandle h, int nthen, int nelse) {
+    const bool on = *flag != 0u;
+    ctrl->dyn_launches += on ? nthen : nelse;
+    cudaGraphSetConditional(h, on ? 1u : 0u);
+}
 
 template <typename T>
 State<T> state_of(gfors_ctx* C) {
@@ -566,15 +641,25 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
     if (C->m > 0) {
         if (C->pd.rb) {
             const int grid = (int)std::min<long long>(C->pd.nblk, RB_GRID);
-            KIND_SWITCH(C->kkind, LAUNCH(C, s, KC_DUAL,
-                (k_dual_rb<T, KINDV><<<grid, RB_NT, 0, s>>>(csr_K(C), C->pd.blk_row, C->pd.nblk, st, g, rh, C->d_rsign,
-                                                            C->m1, ctrl, kint, j,
-                                                            (kint == 0 || j == kint - 1) ? C->d_u : nullptr, pl))));
+            double* u_out = (kint == 0 || j == kint - 1) ? C->d_u : nullptr;
+            auto gather = [&](cudaStream_t q) {
+                KIND_SWITCH(C->kkind, LAUNCH(C, q, KC_DUAL,
+                    (k_dual_rb<T, KINDV><<<grid, RB_NT, 0, q>>>(csr_K(C), C->pd.blk_row, C->pd.nblk, st, g, rh, C->d_rsign,
+                                                                C->m1, ctrl, kint, j, u_out, pl))));
+            };
             if (C->push_dual) {
-                // the two push-mode kernels exit at once unless the xbar list is short (device decision)
-                LAUNCH(C, s, KC_DUAL_PUSH, (k_push_scatter<T><<<grid_for(C->n), NT, 0, s>>>(csr_Kt(C), pl, st, ctrl, kint, j)));
-                LAUNCH(C, s, KC_DUAL_PUSH, (k_push_rows<T><<<grid_for(C->m), NT, 0, s>>>(C->m, pl, st, g, rh, C->d_rsign, C->m1, ctrl,
-                                                                                  kint, j, (kint == 0 || j == kint - 1) ? C->d_u : nullptr)));
+                // sparse xbar: scatter the listed columns into the row accumulators, then the rows
+                auto push = [&](cudaStream_t q) {
+                    LAUNCH(C, q, KC_DUAL_PUSH, (k_push_scatter<T><<<grid_for(C->n), NT, 0, q>>>(csr_Kt(C), pl, st, ctrl, kint, j)));
+                    LAUNCH(C, q, KC_DUAL_PUSH, (k_push_rows<T><<<grid_for(C->m), NT, 0, q>>>(C->m, pl, st, g, rh, C->d_rsign, C->m1,
+                                                                                      ctrl, kint, j, u_out)));
+                };
+                branch(C, s, [&](cudaStream_t q, cudaGraphConditionalHandle h, int a, int b) {
+                    k_decide_dual<<<1, 1, 0, q>>>(pl, C->d_ctrl, kint, j, h, a, b);
+                    CK(cudaGetLastError());
+                }, push, gather);
+            } else {
+                gather(s);
             }
         } else if (!C->pd.seg) {
             const int grid = grid_for(C->m * (long long)C->pd.sub);
@@ -597,69 +682,79 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
     const int tkind = C->kkind;
     // trigger iteration of a loop block: the push-mode primal also pushes x_k for the indicator pass
     const bool trig_push = C->push_primal && kint > 0 && j == kint - 1;
+    auto gather = [&](cudaStream_t q) {
+        if (C->sparse_primal && !C->push_primal && sparse_primal_smem<T>(C->m) <= SP_DYN_MAX) {
+            const long long nwords = (C->m + 31) / 32;
+            LAUNCH(C, q, KC_PRIMAL, (k_nzmask<T><<<grid_for(nwords * 32), NT, 0, q>>>(st.w, C->m, C->d_nzbits)));
+            const size_t sm = sparse_primal_smem<T>(C->m);
+            const int grid = (int)std::min<long long>(C->sp_nblk, NUM_SMS_B200);
+            if (C->hasq) {
+                KIND_SWITCH(tkind, {
+                    static bool attr = false;
+                    if (!attr) { set_max_dyn_smem((const void*)k_primal_sparse<T, KINDV, true>); attr = true; }
+                    LAUNCH(C, q, KC_PRIMAL, (k_primal_sparse<T, KINDV, true><<<grid, SP_NT, sm, q>>>(csr_Kt(C), C->sp_blk_row, C->sp_nblk,
+                        C->d_nzbits, nwords, Q, qs, st, cs, ctrl, kint, j, pl)));
+                });
+            } else {
+                KIND_SWITCH(tkind, {
+                    static bool attr = false;
+                    if (!attr) { set_max_dyn_smem((const void*)k_primal_sparse<T, KINDV, false>); attr = true; }
+                    LAUNCH(C, q, KC_PRIMAL, (k_primal_sparse<T, KINDV, false><<<grid, SP_NT, sm, q>>>(csr_Kt(C), C->sp_blk_row, C->sp_nblk,
+                        C->d_nzbits, nwords, Q, qs, st, cs, ctrl, kint, j, pl)));
+                });
+            }
+        } else if (C->pp.rb) {
+            const int grid = (int)std::min<long long>(C->pp.nblk, RB_GRID);
+            if (C->hasq) {
+                KIND_SWITCH(tkind, LAUNCH(C, q, KC_PRIMAL,
+                    (k_primal_rb<T, KINDV, true><<<grid, RB_NT, 0, q>>>(csr_Kt(C), C->pp.blk_row, C->pp.nblk, Q, qs, st, cs,
+                                                                        ctrl, kint, j, pl, ppr))));
+            } else {
+                KIND_SWITCH(tkind, LAUNCH(C, q, KC_PRIMAL,
+                    (k_primal_rb<T, KINDV, false><<<grid, RB_NT, 0, q>>>(csr_Kt(C), C->pp.blk_row, C->pp.nblk, Q, qs, st, cs,
+                                                                         ctrl, kint, j, pl, ppr))));
+            }
+        } else if (!C->pp.seg) {
+            const int grid = grid_for(C->n * (long long)C->pp.sub);
+            if (C->hasq) {
+                KIND_SWITCH(tkind, SUB_SWITCH(C->pp.sub, LAUNCH(C, q, KC_PRIMAL,
+                    (k_primal<T, KINDV, SUBV, true><<<grid, NT, 0, q>>>(csr_Kt(C), Q, qs, st, cs, ctrl, kint, j)))));
+            } else {
+                KIND_SWITCH(tkind, SUB_SWITCH(C->pp.sub, LAUNCH(C, q, KC_PRIMAL,
+                    (k_primal<T, KINDV, SUBV, false><<<grid, NT, 0, q>>>(csr_Kt(C), Q, qs, st, cs, ctrl, kint, j)))));
+            }
+        } else {
+            const int grid = grid_for(C->pp.ds.nseg * 32);
+            const int grid2 = grid_for(C->n);
+            KIND_SWITCH(tkind, LAUNCH(C, q, KC_PRIMAL,
+                (k_seg_partial<T, KINDV><<<grid, NT, 0, q>>>(csr_Kt(C), C->pp.ds.plan(), st.w, st.w, nullptr, nullptr, 0,
+                                                             ctrl, kint, j, C->d_segpart2))));
+            if (C->hasq)
+                LAUNCH(C, q, KC_PRIMAL, (k_primal_seg_final<T, true><<<grid2, NT, 0, q>>>(
+                                            C->n, C->pp.ds.plan(), C->d_segpart2, Q, qs, st, cs, ctrl, kint, j)));
+            else
+                LAUNCH(C, q, KC_PRIMAL, (k_primal_seg_final<T, false><<<grid2, NT, 0, q>>>(
+                                            C->n, C->pp.ds.plan(), C->d_segpart2, Q, qs, st, cs, ctrl, kint, j)));
+        }
+    };
     if (C->push_primal) {
-        // list the active duals; the push kernels run iff the list is short, else k_primal_rb below
+        // list the active duals (or the changed ones); the push kernels run iff the list is short
         LAUNCH(C, s, KC_PRIMAL_PUSH, (k_wlist<T><<<grid_for(C->m), NT, 0, s>>>(st, ppr, ctrl, kint, j)));
-        LAUNCH(C, s, KC_PRIMAL_PUSH, (k_push_scatter_cols<T><<<grid_for(C->m * 32LL), NT, 0, s>>>(csr_K(C), ppr, st, ctrl, kint, j)));
-        if (C->hasq)
-            LAUNCH(C, s, KC_PRIMAL_PUSH, (k_primal_push<T, true><<<pp_grid<T>(C->n), NT, 0, s>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
-                csr_Kt(C), trig_push ? C->d_accv : nullptr, C->d_ones_cnt, C->d_trig_flag)));
-        else
-            LAUNCH(C, s, KC_PRIMAL_PUSH, (k_primal_push<T, false><<<pp_grid<T>(C->n), NT, 0, s>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
-                csr_Kt(C), trig_push ? C->d_accv : nullptr, C->d_ones_cnt, C->d_trig_flag)));
-    }
-    if (C->sparse_primal && !C->push_primal && sparse_primal_smem<T>(C->m) <= SP_DYN_MAX) {
-        const long long nwords = (C->m + 31) / 32;
-        LAUNCH(C, s, KC_PRIMAL, (k_nzmask<T><<<grid_for(nwords * 32), NT, 0, s>>>(st.w, C->m, C->d_nzbits)));
-        const size_t sm = sparse_primal_smem<T>(C->m);
-        const int grid = (int)std::min<long long>(C->sp_nblk, NUM_SMS_B200);
-        if (C->hasq) {
-            KIND_SWITCH(tkind, {
-                static bool attr = false;
-                if (!attr) { set_max_dyn_smem((const void*)k_primal_sparse<T, KINDV, true>); attr = true; }
-                LAUNCH(C, s, KC_PRIMAL, (k_primal_sparse<T, KINDV, true><<<grid, SP_NT, sm, s>>>(csr_Kt(C), C->sp_blk_row, C->sp_nblk,
-                    C->d_nzbits, nwords, Q, qs, st, cs, ctrl, kint, j, pl)));
-            });
-        } else {
-            KIND_SWITCH(tkind, {
-                static bool attr = false;
-                if (!attr) { set_max_dyn_smem((const void*)k_primal_sparse<T, KINDV, false>); attr = true; }
-                LAUNCH(C, s, KC_PRIMAL, (k_primal_sparse<T, KINDV, false><<<grid, SP_NT, sm, s>>>(csr_Kt(C), C->sp_blk_row, C->sp_nblk,
-                    C->d_nzbits, nwords, Q, qs, st, cs, ctrl, kint, j, pl)));
-            });
-        }
-    } else if (C->pp.rb) {
-        const int grid = (int)std::min<long long>(C->pp.nblk, RB_GRID);
-        if (C->hasq) {
-            KIND_SWITCH(tkind, LAUNCH(C, s, KC_PRIMAL,
-                (k_primal_rb<T, KINDV, true><<<grid, RB_NT, 0, s>>>(csr_Kt(C), C->pp.blk_row, C->pp.nblk, Q, qs, st, cs,
-                                                                    ctrl, kint, j, pl, ppr))));
-        } else {
-            KIND_SWITCH(tkind, LAUNCH(C, s, KC_PRIMAL,
-                (k_primal_rb<T, KINDV, false><<<grid, RB_NT, 0, s>>>(csr_Kt(C), C->pp.blk_row, C->pp.nblk, Q, qs, st, cs,
-                                                                     ctrl, kint, j, pl, ppr))));
-        }
-    } else if (!C->pp.seg) {
-        const int grid = grid_for(C->n * (long long)C->pp.sub);
-        if (C->hasq) {
-            KIND_SWITCH(tkind, SUB_SWITCH(C->pp.sub, LAUNCH(C, s, KC_PRIMAL,
-                (k_primal<T, KINDV, SUBV, true><<<grid, NT, 0, s>>>(csr_Kt(C), Q, qs, st, cs, ctrl, kint, j)))));
-        } else {
-            KIND_SWITCH(tkind, SUB_SWITCH(C->pp.sub, LAUNCH(C, s, KC_PRIMAL,
-                (k_primal<T, KINDV, SUBV, false><<<grid, NT, 0, s>>>(csr_Kt(C), Q, qs, st, cs, ctrl, kint, j)))));
-        }
+        auto push = [&](cudaStream_t q) {
+            LAUNCH(C, q, KC_PRIMAL_PUSH, (k_push_scatter_cols<T><<<grid_for(C->m * 32LL), NT, 0, q>>>(csr_K(C), ppr, st, ctrl, kint, j)));
+            if (C->hasq)
+                LAUNCH(C, q, KC_PRIMAL_PUSH, (k_primal_push<T, true><<<pp_grid<T>(C->n), NT, 0, q>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
+                    csr_Kt(C), trig_push ? C->d_accv : nullptr, C->d_ones_cnt, C->d_trig_flag)));
+            else
+                LAUNCH(C, q, KC_PRIMAL_PUSH, (k_primal_push<T, false><<<pp_grid<T>(C->n), NT, 0, q>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
+                    csr_Kt(C), trig_push ? C->d_accv : nullptr, C->d_ones_cnt, C->d_trig_flag)));
+        };
+        branch(C, s, [&](cudaStream_t q, cudaGraphConditionalHandle h, int a, int b) {
+            k_decide_primal<<<1, 1, 0, q>>>(ppr, C->d_ctrl, kint, j, h, a, b);
+            CK(cudaGetLastError());
+        }, push, gather);
     } else {
-        const int grid = grid_for(C->pp.ds.nseg * 32);
-        const int grid2 = grid_for(C->n);
-        KIND_SWITCH(tkind, LAUNCH(C, s, KC_PRIMAL,
-            (k_seg_partial<T, KINDV><<<grid, NT, 0, s>>>(csr_Kt(C), C->pp.ds.plan(), st.w, st.w, nullptr, nullptr, 0,
-                                                         ctrl, kint, j, C->d_segpart2))));
-        if (C->hasq)
-            LAUNCH(C, s, KC_PRIMAL, (k_primal_seg_final<T, true><<<grid2, NT, 0, s>>>(
-                                        C->n, C->pp.ds.plan(), C->d_segpart2, Q, qs, st, cs, ctrl, kint, j)));
-        else
-            LAUNCH(C, s, KC_PRIMAL, (k_primal_seg_final<T, false><<<grid2, NT, 0, s>>>(
-                                        C->n, C->pp.ds.plan(), C->d_segpart2, Q, qs, st, cs, ctrl, kint, j)));
+        gather(s);
     }
 }
 
@@ -673,17 +768,27 @@ void enqueue_trigger(gfors_ctx* C, cudaStream_t s, long long kint, long long j) 
     if (C->m > 0) {
         if (C->pd.rb) {
             const int grid = (int)std::min<long long>(C->pd.nblk, (long long)C->nb1);
-            KIND_SWITCH(C->kkind, LAUNCH(C, s, KC_TRIGR,
-                (k_trig_rows_rb<T, KINDV><<<grid, RB_NT, 0, s>>>(csr_K(C), C->pd.blk_row, C->pd.nblk, st, g, rh,
-                                                                 C->d_rsign, C->m1, C->d_u, ctrl, kint, j, C->d_part1,
-                                                                 C->d_ones, C->push_primal ? C->d_trig_flag : nullptr))));
-            if (grid < C->nb1)
-                LAUNCH(C, s, KC_TRIGR, (k_fill<<<1, NT, 0, s>>>(C->d_part1 + 3LL * grid, 3LL * (C->nb1 - grid), 0.0)));
+            auto gather = [&](cudaStream_t q) {
+                KIND_SWITCH(C->kkind, LAUNCH(C, q, KC_TRIGR,
+                    (k_trig_rows_rb<T, KINDV><<<grid, RB_NT, 0, q>>>(csr_K(C), C->pd.blk_row, C->pd.nblk, st, g, rh,
+                                                                     C->d_rsign, C->m1, C->d_u, ctrl, kint, j, C->d_part1,
+                                                                     C->d_ones, C->push_primal ? C->d_trig_flag : nullptr))));
+                if (grid < C->nb1)
+                    LAUNCH(C, q, KC_TRIGR, (k_fill<<<1, NT, 0, q>>>(C->d_part1 + 3LL * grid, 3LL * (C->nb1 - grid), 0.0)));
+            };
             if (C->push_primal) {
                 // x_k pushed by the trigger iteration's primal: gather-free pass over the rows (writes all nb1 partials)
-                LAUNCH(C, s, KC_TRIGR, (k_trig_rows_push<T><<<C->nb1, NT, 0, s>>>(C->m, st, g, rh, C->d_rsign, C->m1, C->d_u,
-                    ctrl, kint, j, C->d_part1, C->d_ones, C->d_accv, C->d_ones_cnt, C->d_trig_flag)));
+                auto pushed = [&](cudaStream_t q) {
+                    LAUNCH(C, q, KC_TRIGR, (k_trig_rows_push<T><<<C->nb1, NT, 0, q>>>(C->m, st, g, rh, C->d_rsign, C->m1, C->d_u,
+                        ctrl, kint, j, C->d_part1, C->d_ones, C->d_accv, C->d_ones_cnt, C->d_trig_flag)));
+                };
+                branch(C, s, [&](cudaStream_t q, cudaGraphConditionalHandle h, int a, int b) {
+                    k_decide_flag<<<1, 1, 0, q>>>(C->d_trig_flag, C->d_ctrl, h, a, b);
+                    CK(cudaGetLastError());
+                }, pushed, gather);
                 LAUNCH(C, s, KC_TRIGR, (k_trig_clear<<<1, 1, 0, s>>>(C->d_trig_flag)));
+            } else {
+                gather(s);
             }
         } else if (!C->pd.seg) {
             KIND_SWITCH(C->kkind, SUB_SWITCH(C->pd.sub, LAUNCH(C, s, KC_TRIGR,
@@ -841,7 +946,7 @@ void enqueue_block(gfors_ctx* C, cudaStream_t s, const gfors_params* p, int W, H
         if (C->sharded) {
             // record -> ncclAllGather -> identical merge on every rank -> regenerate the winner's bits
             LAUNCH(C, s, KC_ARGMIN, (k_local_record<<<1, NT, 0, s>>>(C->d_z, C->d_viol, 64LL * W, word_off, C->d_ctrl, C->d_rec)));
-            const int rc = nccl().AllGather(C->d_rec, C->d_rec + 4, 4, ncclFloat64_, C->comm, s);
+            const int rc = C->dry ? 0 : nccl().AllGather(C->d_rec, C->d_rec + 4, 4, ncclFloat64_, C->comm, s);
             if (rc != 0) throw Err{GFORS_E_NCCL, std::string("ncclAllGather: ") + nccl().GetErrorString(rc)};
             LAUNCH(C, s, KC_ARGMIN, (k_merge_records<<<1, 32, 0, s>>>(C->d_rec + 4, C->world, C->d_ctrl, kint, r, p->k_r, C->d_regen)));
             const uint2 key = make_uint2((unsigned)(p->seed & 0xffffffffu), (unsigned)(p->seed >> 32));
@@ -1138,8 +1243,10 @@ static void do_run_t(gfors_ctx* C, const gfors_params* p, gfors_run_info* out) {
     const int tcap = std::max(1, p->trace_cap);
     if (tcap > C->trace_cap) { dfree(C->d_trace); C->d_trace = dalloc<double>(8LL * tcap); C->trace_cap = tcap; C->gvalid = false; }
     // reset state and control
+    const long long l0 = C->launches;
     k_init_state<T><<<grid_for(std::max(C->n, C->m)), NT, 0, s>>>(state_of<T>(C), C->n, C->m);
     CK(cudaGetLastError());
+    C->launches++;
     reset_push(C, s);
     Ctrl h{};
     h.blk = 0; h.k = 0; h.rho = rho[0]; h.tau1 = std::sqrt(p->sigma); h.tau2 = std::sqrt(p->sigma);
@@ -1151,11 +1258,13 @@ static void do_run_t(gfors_ctx* C, const gfors_params* p, gfors_run_info* out) {
                p->k_int, p->k_r, p->k_b * (long long)C->world};
     k_loop_start<<<1, 1, 0, s>>>(C->d_ctrl, p->time_limit_s);
     CK(cudaGetLastError());
+    C->launches++;
 
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
     CK(cudaEventRecord(e0, s));
+    bool used_graph = false;
     if (max_blocks > 0) {
         if (p->use_graph) {
             const bool same = same_graph_key(C->gkey, *p) && C->gkey_W == W;
@@ -1176,12 +1285,18 @@ static void do_run_t(gfors_ctx* C, const gfors_params* p, gfors_run_info* out) {
                 if (!C->cap_stream) CK(cudaStreamCreateWithFlags(&C->cap_stream, cudaStreamNonBlocking));
                 CK(cudaStreamBeginCaptureToGraph(C->cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
                 bool cap_ok = true;
+                const long long c0 = C->launches;
+                C->capturing = true;
                 try {
                     enqueue_block<T>(C, C->cap_stream, p, W, hp, handle, 1);
                 } catch (const Err& e) {
                     cap_ok = false;
                     C->graph_note = "capture failed: " + e.msg;
                 }
+                C->capturing = false;
+                C->dry = false;
+                C->gstatic = C->launches - c0;  // unconditional kernels per block (branch kernels: on the device)
+                C->launches = c0;
                 cudaGraph_t g2;
                 const cudaError_t ec = cudaStreamEndCapture(C->cap_stream, &g2);
                 if (ec != cudaSuccess) { cap_ok = false; C->graph_note = std::string("end capture: ") + cudaGetErrorString(ec); }
@@ -1202,7 +1317,8 @@ static void do_run_t(gfors_ctx* C, const gfors_params* p, gfors_run_info* out) {
                 C->gno = !cap_ok;
             }
         }
-        if (p->use_graph && C->gvalid) {
+        used_graph = p->use_graph && C->gvalid;
+        if (used_graph) {
             CK(cudaGraphLaunch(C->gexec, s));
         } else {
             // eager: one block at a time, host reads the halt flag (debug / fallback path)
@@ -1217,6 +1333,7 @@ static void do_run_t(gfors_ctx* C, const gfors_params* p, gfors_run_info* out) {
     }
     CK(cudaMemcpyAsync(&h, C->d_ctrl, sizeof h, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    if (used_graph) C->launches += h.blk * C->gstatic + h.dyn_launches;
     long long k_done = max_blocks > 0 ? h.k : 0;
     int reason = max_blocks > 0 ? h.halt : 2;
     long long tail_run = 0;
@@ -1236,6 +1353,7 @@ static void do_run_t(gfors_ctx* C, const gfors_params* p, gfors_run_info* out) {
     info.halt_reason = reason;
     info.elapsed_s = ms * 1e-3;
     info.n_trace = h.n_trace;
+    info.launches = C->launches - l0;
     C->last_info = info;
     C->have_run = true;
     C->hk = info.iters;
@@ -1527,25 +1645,26 @@ gfors_status gfors_profile_active(gfors_ctx* C, double* active_ms, double* activ
 
 int64_t gfors_launches_per_block(gfors_ctx* C, const gfors_params* p) {
     if (!C || C->stage < 2) return -1;
-    // count by enqueueing into a throwaway capture-free dry run: reuse the counter
+    // eager structure of one block, counted by a dry enqueue (LAUNCH counts, launches nothing)
+    gfors_params d;
+    gfors_params_default(&d);
+    if (!p) p = &d;
+    const int W = (int)(p->k_b / 64);
+    HaltPar hp{{p->tol_primal, p->tol_dual, p->tol_binary}, p->stall_rel, p->stall_window, p->trace_cap,
+               p->k_int, p->k_r, p->k_b * (long long)C->world};
     const long long before = C->launches;
     C->launches = 0;
-    // a dry count: mirror enqueue_block's structure
-    long long per_iter = 0;
-    per_iter += C->m > 0 ? (C->pd.seg ? 2 : 1) : 0;
-    per_iter += C->push_dual ? 2 : 0;
-    per_iter += C->push_primal ? 3 : 0;
-    const bool spp = C->sparse_primal && !C->push_primal && (C->precision == 64 ? sparse_primal_smem<double>(C->m) : sparse_primal_smem<float>(C->m)) <= SP_DYN_MAX;
-    per_iter += spp ? 2 : (C->pp.seg ? 2 : 1);
-    long long trig = (C->m > 0 ? (C->pd.seg ? 3 : (C->pd.rb ? 1 + (C->pd.nblk < C->nb1 ? 1 : 0) + (C->push_primal ? 2 : 0) : 1)) : 1) + 1;
-    long long eval = 0;
-    for (auto& cl : C->cnt) eval += cl.nrows ? 1 : 0;
-    eval += C->n_int ? 2 : 0;
-    eval += C->n_real ? 1 : 0;
-    eval += 2 + ((C->obj_bits && C->hasq) ? 1 : 0);  // objective partial(s) + final
-    const long long per_round = 1 /*reset*/ + 1 /*sample*/ + eval + (C->sharded ? 3 /*record, merge, regen*/ : 2 /*argmin, copy*/);
+    C->dry = true;
+    long long n = -1;
+    try {
+        if (C->precision == 64) enqueue_block<double>(C, C->stream, p, W, hp, cudaGraphConditionalHandle{}, 0);
+        else enqueue_block<float>(C, C->stream, p, W, hp, cudaGraphConditionalHandle{}, 0);
+        n = C->launches;
+    } catch (...) {
+    }
+    C->dry = false;
     C->launches = before;
-    return per_iter * p->k_int + trig + per_round * p->k_r + 1 /*halt*/;
+    return n;
 }
 
 gfors_status gfors_profile_blocks(gfors_ctx* C, const gfors_params* p, int32_t blocks, double* ms_out,

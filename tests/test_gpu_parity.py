@@ -403,14 +403,16 @@ def test_push_primal_variant_parity(gf, fam, prec, tol, monkeypatch):
         assert zg == zo or (math.isinf(zg) and math.isinf(zo))
 
 
-@pytest.mark.parametrize("switch", ["GFORS_DELTA_DUAL", "GFORS_XSKIP"])
+@pytest.mark.parametrize("switch", ["GFORS_DELTA_DUAL", "GFORS_XSKIP", "GFORS_COND_BRANCH"])
 @pytest.mark.parametrize("fam", ["setcover", "mis"])
 @pytest.mark.parametrize("prec", [64, 32])
 def test_exact_shortcuts_bit_identical(gf, switch, fam, prec, monkeypatch):
     """Two shortcuts must reproduce the plain computation BIT FOR BIT (push modes forced on):
     GFORS_DELTA_DUAL — the delta push of the dual adds exact integer differences instead of a fresh
     fixed-point sum; GFORS_XSKIP — the push primal skips columns whose update provably returns the
-    value already stored.  Same iterates after hook steps, same run trace and incumbent."""
+    value already stored; GFORS_COND_BRANCH — graph conditional nodes run only the chosen mode's
+    kernels instead of launching both with early exits.  Same iterates after hook steps, same run
+    trace and incumbent."""
     monkeypatch.setenv("GFORS_PUSH_DUAL", "1")
     monkeypatch.setenv("GFORS_PUSH_PRIMAL", "1")
     inst = G.SMALL[fam](14)
@@ -428,6 +430,7 @@ def test_exact_shortcuts_bit_identical(gf, switch, fam, prec, monkeypatch):
         st = s.get_state()
         info = s.run(max_iters=2000, tol_primal=-1.0, tol_dual=-1.0, tol_binary=-1.0, stall_rel=-1.0)
         out.append((st, s.trace(), s.best_incumbent(), info["iters"]))
+        assert info["launches"] > 0
     (sa, ta, za, ia), (sb, tb, zb, ib) = out
     for u, v in zip(sa, sb):
         assert np.array_equal(u, v)
