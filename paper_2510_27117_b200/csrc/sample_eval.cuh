@@ -154,6 +154,7 @@ __device__ __forceinline__ void load_words(const uint64_t* __restrict__ p, uint6
 
 // One SUB-lane group per count row; each nonzero gathers WV words (64*WV candidates) with one
 // vector load, so a covering row over 128 candidates costs one 16-byte gather per nonzero.
+constexpr int FEAS_U = 1;
 template <int BMAX, int SUB, int WV>
 __global__ void __launch_bounds__(256) k_feas_count(Csr K, CountRows cr, const uint64_t* __restrict__ X, int W,
                                                     unsigned long long* __restrict__ viol,
@@ -191,11 +192,24 @@ __global__ void __launch_bounds__(256) k_feas_count(Csr K, CountRows cr, const u
                 for (int q = 0; q < BMAX; ++q) C[u][q] = 0ull;
             }
             if (rel < 3)
-                for (long long p = p0 + lane; p < p1; p += SUB) {
-                    uint64_t v[WV];
-                    load_words<WV>(X + (long long)__ldg(K.idx + p) * W + w0, v);
+                // FEAS_U nonzeros per lane in flight: all index loads, then all gathers, then the adds
+                // (a zero word adds nothing, so the tail is padded with zeros)
+                for (long long p = p0 + lane; p < p1; p += FEAS_U * SUB) {
+                    int c[FEAS_U];
 #pragma unroll
-                    for (int u = 0; u < WV; ++u) csa_add_bit<BMAX>(C[u], sat[u], v[u], B);
+                    for (int f = 0; f < FEAS_U; ++f) c[f] = p + f * SUB < p1 ? __ldg(K.idx + p + f * SUB) : -1;
+                    uint64_t v[FEAS_U][WV];
+#pragma unroll
+                    for (int f = 0; f < FEAS_U; ++f) {
+                        if (c[f] >= 0) load_words<WV>(X + (long long)c[f] * W + w0, v[f]);
+                        else
+#pragma unroll
+                            for (int u = 0; u < WV; ++u) v[f][u] = 0ull;
+                    }
+#pragma unroll
+                    for (int f = 0; f < FEAS_U; ++f)
+#pragma unroll
+                        for (int u = 0; u < WV; ++u) csa_add_bit<BMAX>(C[u], sat[u], v[f][u], B);
                 }
 #pragma unroll
             for (int u = 0; u < WV; ++u) {
