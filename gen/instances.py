@@ -188,6 +188,64 @@ def random_general(n, m_ge, m_eq, deg, seed, vmax=5, real=False, with_q=False, n
     return inst
 
 
+def max_cut(n, density, seed, wmin=-8, wmax=10, name="maxcut"):
+    """Max cut QP: max sum_{(i,j) in E} w_ij (x_i + x_j - 2 x_i x_j) over x in {0,1}^V,
+    G(n, density) with integer weights w ~ U{wmin..wmax} (PAPER L254: density 0.5, w in [-8, 10];
+    integral reading, zero-weight edges dropped).  User form: maximize x'Qx + c'x with
+    Q_ij = Q_ji = -w_ij (i != j; x'Qx = -2 sum w_ij x_i x_j) and c_i = sum_j w_ij; no constraints.
+    Generated one row block at a time (upper triangle mirrored), so n = 20480 stays within a few GB."""
+    rng = _rng(seed)
+    Wup = np.zeros((n, n), dtype=np.int8)
+    B = 1024
+    for r0 in range(0, n, B):
+        r1 = min(n, r0 + B)
+        blk = rng.integers(wmin, wmax + 1, size=(r1 - r0, n), dtype=np.int16).astype(np.int8)
+        keep = rng.random((r1 - r0, n), dtype=np.float32) < density
+        blk[~keep] = 0
+        ii = np.arange(r0, r1)[:, None]
+        blk[np.arange(n)[None, :] <= ii] = 0  # strict upper triangle
+        Wup[r0:r1] = blk
+    inst = dict(name=name, n=n, m=0, k_rowptr=np.zeros(1, np.int64), k_col=np.zeros(0, np.int32),
+                k_val=np.zeros(0), r=np.zeros(0), sense=np.zeros(0, np.int8), c0=0.0, maximize=True)
+    deg = np.zeros(n, dtype=np.int64)
+    qptr = np.zeros(n + 1, dtype=np.int64)
+    cols, vals = [], []
+    for r0 in range(0, n, B):
+        r1 = min(n, r0 + B)
+        rows = Wup[r0:r1].astype(np.int16) + Wup[:, r0:r1].T.astype(np.int16)  # symmetric W rows
+        deg[r0:r1] = rows.sum(axis=1, dtype=np.int64)
+        for k in range(r1 - r0):
+            nz = np.flatnonzero(rows[k])
+            cols.append(nz.astype(np.int32))
+            vals.append(-rows[k, nz].astype(np.float64))
+            qptr[r0 + k + 1] = qptr[r0 + k] + nz.size
+    del Wup
+    inst.update(q_rowptr=qptr, q_col=np.concatenate(cols), q_val=np.concatenate(vals), c=deg.astype(np.float64))
+    return inst
+
+
+def dense_laplacian(n, density, m, seed, name="dense_psd"):
+    """Dense PSD test family for the dense-Q path: min x'Lx + c'x, L = Laplacian of G(n, density)
+    (0/1 weights, so |L_ij| <= 127 for n <= 200), c ~ U{1..100}, m covering rows of 2..8 columns.
+    Not a paper workload: the PSD (non-expansive) dense counterpart of the bqp family, on which the
+    1000-iteration parity bar applies."""
+    rng = _rng(seed)
+    A = np.triu((rng.random((n, n)) < density).astype(np.int64), 1)
+    A = A + A.T
+    L = np.diag(A.sum(1)) - A
+    inst = set_cover(m, n, 2, 8, seed + 1000, name)
+    inst.update(dense_to_csr_sym(L.astype(np.float64)))
+    inst["c"] = rng.integers(1, 101, size=n).astype(np.float64)
+    return inst
+
+
+def cut_value(inst_edges_w, x):
+    """Cut weight sum_{i<j} w_ij [x_i != x_j] from a dense symmetric weight matrix (test helper)."""
+    x = np.asarray(x).astype(bool)
+    W = inst_edges_w
+    return float(W[np.ix_(x, ~x)].sum())
+
+
 def dense_to_csr_sym(Qd):
     n = Qd.shape[0]
     qptr = np.zeros(n + 1, dtype=np.int64)
@@ -232,6 +290,9 @@ CONFIGS = {
             make=lambda s: assignment_bqp(400, 500, 4, s, "cfg4_bqp_400x500")),
     5: dict(desc="set cover n=5e6, m=1e6, row degree U{2..98}",
             make=lambda s: set_cover(1_000_000, 5_000_000, 2, 98, s, "cfg5_setcover_5M_1M")),
+    # next row f1: dense-Q workload, the paper's largest max-cut size
+    6: dict(desc="max cut QP n=20480, density 0.5, w ~ U{-8..10} (dense Q, next row f1)",
+            make=lambda s: max_cut(20_480, 0.5, s, name="cfg6_maxcut_20480")),
 }
 
 SMALL = {
@@ -241,6 +302,8 @@ SMALL = {
     "bqp": lambda s: assignment_bqp(12, 15, 4, s, "small_bqp"),
     "general": lambda s: random_general(300, 80, 20, 12, s, with_q=True, name="small_general"),
     "real": lambda s: random_general(200, 60, 10, 10, s, real=True, with_q=True, name="small_real"),
+    "maxcut": lambda s: max_cut(300, 0.5, s, name="small_maxcut"),
+    "dense_psd": lambda s: dense_laplacian(200, 0.5, 40, s, name="small_dense_psd"),
 }
 
 

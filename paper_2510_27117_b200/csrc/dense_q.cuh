@@ -1,0 +1,461 @@
+// dense_q.cuh — dense-Q path of the GFORS hot path.
+//
+// When Q is integral with |Q_ij| <= 127 and dense (max cut: density 0.5,
+// w in [-8, 10]), Q is stored ONCE as a row-major int8 matrix Qd[ld][ld] (ld = n rounded up to
+// 128, zero padded) instead of a CSR, and the two places Q enters the hot path become:
+//
+//  * the PDHG primal gradient term 2 Q~ x (Q~ = Q/omega) and the
+//    s^x residual term 2 Q~ (x_k - x_{k-1}): a dense GEMV `k_qx_dense` streaming Qd
+//    from HBM (int8: 1 byte per entry) with fp64 accumulation, units of 8 rows x 1024 columns
+//    per warp (x reused across the 8 rows), fixed-order partials per column chunk combined by
+//    `k_qx_final` -> Q.pre[i] = (sum_j Q_ij x_j) / omega.  HBM-bound: 1 B per entry per pass.
+//
+//  * the EvalBest quadratic term x_l' Q x_l for the k_b sampled candidates:
+//    a tcgen05 int8 tensor-core GEMM Y = Q X (exact int32 accumulation in TMEM) fused with its
+//    epilogue z_l += w * sum_i X_il Y_il (`k_obj_dense_tc`).  Only the upper block triangle of Q
+//    is read: z = sum_I X_I' Q_II X_I + 2 sum_{I<J} X_I' Q_IJ X_J (Q symmetric).  TMA
+//    (128B swizzle) streams Q tiles (A, K-major) and the unpacked 0/1 samples (B, K-major, from
+//    `k_unpack_samples`) through a 4-stage mbarrier pipeline; one elected thread issues
+//    tcgen05.mma.kind::i8 (M=128, N<=256, K=32); two TMEM accumulator stages let the epilogue of
+//    one work item overlap the MMAs of the next.  Integer results: bit-exact, order-free.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "pdhg.cuh"
+
+namespace gfors {
+
+// ---------------------------------------------------------------------------------------------
+// Dense GEMV (fp64 accumulation) — PDHG gradient term and Preprocess power iteration on Q
+// ---------------------------------------------------------------------------------------------
+constexpr int QX_RW = 8;       // rows per warp unit (x reuse factor)
+constexpr int QX_CW = 1024;    // columns per warp unit (two 512-column strips)
+constexpr int QX_NT = 256;
+
+// source vector of the GEMV.  ctrl == nullptr: a[0] (minus b[0] if DIFF).  Otherwise the buffer
+// is picked by the parity of the current iteration (pdhg.cuh iter_index) exactly as the kernel
+// that consumes the product picks its own input: a[par] (minus b[par] if DIFF).
+template <typename TX>
+struct QxSrc {
+    const TX* a[2];
+    const TX* b[2];
+    const Ctrl* ctrl;
+    long long kint, j;
+};
+
+__device__ __forceinline__ double i8_to_f64(uint32_t word_biased, int k) {
+    // exact int8 -> fp64 without I2F: (2^52 + (q + 128)) - (2^52 + 128); word_biased = word ^ 0x80808080
+    const uint32_t b = (word_biased >> (8 * k)) & 0xFFu;
+    return __hiloint2double(0x43300000, (int)b) - 4503599627370624.0;
+}
+
+template <typename TX>
+__device__ __forceinline__ void qx_load_x16(const TX* __restrict__ a, const TX* __restrict__ b, long long col0,
+                                            long long n, double (&xv)[16]) {
+    if (col0 + 16 <= n) {
+        if constexpr (sizeof(TX) == 4) {
+            const float4* pa = reinterpret_cast<const float4*>(a + col0);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const float4 f = __ldg(pa + v);
+                xv[4 * v] = f.x; xv[4 * v + 1] = f.y; xv[4 * v + 2] = f.z; xv[4 * v + 3] = f.w;
+            }
+            if (b) {
+                const float4* pb = reinterpret_cast<const float4*>(b + col0);
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const float4 f = __ldg(pb + v);
+                    xv[4 * v] -= (double)f.x; xv[4 * v + 1] -= (double)f.y;
+                    xv[4 * v + 2] -= (double)f.z; xv[4 * v + 3] -= (double)f.w;
+                }
+            }
+        } else {
+            const double2* pa = reinterpret_cast<const double2*>(a + col0);
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+                const double2 f = __ldg(pa + v);
+                xv[2 * v] = f.x; xv[2 * v + 1] = f.y;
+            }
+            if (b) {
+                const double2* pb = reinterpret_cast<const double2*>(b + col0);
+#pragma unroll
+                for (int v = 0; v < 8; ++v) {
+                    const double2 f = __ldg(pb + v);
+                    xv[2 * v] -= f.x; xv[2 * v + 1] -= f.y;
+                }
+            }
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const long long c = col0 + k;
+            double v = 0.0;
+            if (c < n) {
+                v = (double)a[c];
+                if (b) v -= (double)b[c];
+            }
+            xv[k] = v;
+        }
+    }
+}
+
+// part[c * ld + i] = sum_{j in column chunk c} Qd[i][j] * x_j   (fixed order within the chunk:
+// per lane ascending j, then a fixed butterfly over the 32 lanes)
+template <typename TX, bool DIFF>
+__global__ void __launch_bounds__(QX_NT, 2) k_qx_dense(const int8_t* __restrict__ Qd, long long ld, long long n,
+                                                       QxSrc<TX> src, double* __restrict__ part) {
+    int par = 0;
+    if (src.ctrl) par = (int)(iter_index(src.ctrl, src.kint, src.j) & 1);
+    const TX* __restrict__ a = par ? src.a[1] : src.a[0];  // (selects, not an indexed param copy)
+    const TX* __restrict__ b = DIFF ? (par ? src.b[1] : src.b[0]) : nullptr;
+    const int lane = threadIdx.x & 31;
+    const long long rgroups = (n + QX_RW - 1) / QX_RW;
+    const long long nchunk = (n + QX_CW - 1) / QX_CW;
+    const long long units = rgroups * nchunk;
+    const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
+    for (long long u = gw; u < units; u += nw) {
+        const long long rg = u / nchunk, c = u - rg * nchunk;
+        const long long r0 = rg * QX_RW;
+        double acc[QX_RW];
+#pragma unroll
+        for (int r = 0; r < QX_RW; ++r) acc[r] = 0.0;
+#pragma unroll 1
+        for (int s = 0; s < QX_CW / 512; ++s) {
+            const long long col0 = c * QX_CW + s * 512 + lane * 16;
+            if (col0 >= n) break;
+            uint4 q[QX_RW];
+#pragma unroll
+            for (int r = 0; r < QX_RW; ++r) {
+                const long long row = r0 + r;
+                q[r] = row < n ? __ldcs(reinterpret_cast<const uint4*>(Qd + row * ld + col0)) : make_uint4(0, 0, 0, 0);
+            }
+            double xv[16];
+            qx_load_x16<TX>(a, b, col0, n, xv);
+#pragma unroll
+            for (int r = 0; r < QX_RW; ++r) {
+                const uint32_t w[4] = {q[r].x ^ 0x80808080u, q[r].y ^ 0x80808080u, q[r].z ^ 0x80808080u,
+                                       q[r].w ^ 0x80808080u};
+                double t = acc[r];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) t = fma(i8_to_f64(w[k >> 2], k & 3), xv[k], t);
+                acc[r] = t;
+            }
+        }
+        // transpose-reduce the 8 row sums over the 32 lanes: 4+2+1 exchanges halve the value set,
+        // then two plain butterfly steps; lane L ends with row ((L>>4)&1)*4 + ((L>>3)&1)*2 + ((L>>2)&1)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const bool up = lane & 16;
+            const double send = up ? acc[k] : acc[k + 4];
+            const double keep = up ? acc[k + 4] : acc[k];
+            acc[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const bool up = lane & 8;
+            const double send = up ? acc[k] : acc[k + 2];
+            const double keep = up ? acc[k + 2] : acc[k];
+            acc[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        }
+        {
+            const bool up = lane & 4;
+            const double send = up ? acc[0] : acc[1];
+            const double keep = up ? acc[1] : acc[0];
+            acc[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        }
+        acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 2);
+        acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
+        if ((lane & 3) == 0) {
+            const int r = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+            if (r0 + r < n) part[c * ld + r0 + r] = acc[0];
+        }
+    }
+}
+
+// out[i] = (sum_c part[c][i]) / omega   (chunks in ascending order)
+__global__ void __launch_bounds__(256) k_qx_final(long long n, long long ld, long long nchunk,
+                                                  const double* __restrict__ part, double omega,
+                                                  double* __restrict__ out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += gridDim.x * (long long)blockDim.x) {
+        double s = 0.0;
+        for (long long c = 0; c < nchunk; ++c) s += part[c * ld + i];
+        out[i] = s / omega;
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Sample unpack: bit-sliced X[i][W] -> Xs[l][ld] int8 in {0,1} (sample-major, K-major B operand),
+// zero for i >= n.  Thread: one lane l, 16 consecutive variables (one 16-byte store).
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_unpack_samples(const uint64_t* __restrict__ X, int W, long long n, long long ld,
+                                                        int8_t* __restrict__ Xs) {
+    const long long groups = ld / 16;
+    const long long total = groups * 64LL * W;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += gridDim.x * (long long)blockDim.x) {
+        const long long l = t / groups, g = t - l * groups;
+        const int w = (int)(l >> 6), bit = (int)(l & 63);
+        uint32_t v[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const long long i = g * 16 + k;
+            const uint32_t b = i < n ? (uint32_t)((__ldg(X + i * W + w) >> bit) & 1ull) : 0u;
+            v[k >> 2] |= b << (8 * (k & 3));
+        }
+        *reinterpret_cast<uint4*>(Xs + l * ld + g * 16) = make_uint4(v[0], v[1], v[2], v[3]);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// tcgen05 int8 objective kernel
+// ---------------------------------------------------------------------------------------------
+constexpr int TC_BM = 128;        // rows of Q per tile (UMMA M)
+constexpr int TC_BK = 128;        // K bytes per pipeline stage (= one 128B swizzle atom row)
+constexpr int TC_NMAX = 256;      // lanes per pass (UMMA N <= 256)
+constexpr int TC_STAGES = 4;
+constexpr int TC_NT = 192;        // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2-5 epilogue
+constexpr int TC_SMEM_A = TC_BM * TC_BK;  // 16 KB
+
+// work item: row tile I, K-block range [j0, j1), weight (1 diagonal block, 2 off-diagonal)
+struct TcItem {
+    int I, j0, j1, wgt;
+};
+
+__host__ __device__ constexpr size_t tc_smem_bytes(int nbox, int lanes) {
+    return 1024 /*align slack*/ + (size_t)TC_STAGES * (TC_SMEM_A + (size_t)nbox * TC_BK) + 256 /*barriers*/ +
+           8 * (size_t)lanes /*zacc*/;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// bounded wait: a protocol bug traps (kernel error) instead of hanging the GPU
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    uint32_t ok = 0;
+    long long spins = 0;
+    while (true) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(a), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if (++spins > (1LL << 26)) __trap();
+    }
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+// UMMA shared-memory descriptor: K-major operand, 128-byte swizzle (rows of 128 B, 8-row atoms
+// of 1024 B): start >> 4 | LBO (unused for swizzled K-major, 1) | SBO = 1024 B | version 1 |
+// layout SWIZZLE_128B (2).
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)1u << 16;
+    d |= (uint64_t)(1024u >> 4) << 32;
+    d |= (uint64_t)1u << 46;
+    d |= (uint64_t)2u << 61;
+    return d;
+}
+
+// instruction descriptor of tcgen05.mma.kind::i8: D s32, A s8, B s8 (0/1), both K-major, M, N
+__device__ __forceinline__ uint32_t umma_idesc_i8(int M, int N) {
+    return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// warp transpose-reduce of 32 int values per lane: lane c ends with sum over lanes of v[c]
+__device__ __forceinline__ int warp_transpose_sum32(uint32_t (&v)[32], int lane) {
+    int x[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) x[k] = (int)v[k];
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+        const bool up = lane & s;
+#pragma unroll
+        for (int k = 0; k < s; ++k) {
+            const int send = up ? x[k] : x[k + s];
+            const int keep = up ? x[k + s] : x[k];
+            x[k] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+        }
+    }
+    return x[0];
+}
+
+// z partial rows: zrows[blockIdx.x][l] = sum over this CTA's items of wgt * sum_i X_il (Q_I,J X_J)_il
+__global__ void __launch_bounds__(TC_NT, 1)
+    k_obj_dense_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmX,
+                   const TcItem* __restrict__ items, const int* __restrict__ cta_off, int lanes, int nbox,
+                   const uint64_t* __restrict__ X, int W, long long n, long long* __restrict__ zrows) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + TC_STAGES * TC_SMEM_A;
+    const int bbytes = nbox * TC_BK;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + (size_t)TC_STAGES * bbytes);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + TC_STAGES;
+    uint64_t* tfull = bars + 2 * TC_STAGES;
+    uint64_t* tempty = bars + 2 * TC_STAGES + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * TC_STAGES + 4);
+    long long* zacc = reinterpret_cast<long long*>(bars + 32);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int it0 = cta_off[blockIdx.x], it1 = cta_off[blockIdx.x + 1];
+    const int npass = (lanes + TC_NMAX - 1) / TC_NMAX;
+
+    for (int l = threadIdx.x; l < lanes; l += blockDim.x) zacc[l] = 0;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < TC_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmQ)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- TMA producer ----------------
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int it = it0; it < it1; ++it) {
+                const TcItem t = items[it];
+                for (int p = 0; p < npass; ++p) {
+                    for (int kb = t.j0; kb < t.j1; ++kb) {
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        mbar_expect_tx(&full[stage], TC_SMEM_A + bbytes);
+                        tma_load_2d(sA + stage * TC_SMEM_A, &tmQ, &full[stage], kb * TC_BK, t.I * TC_BM);
+                        tma_load_2d(sB + stage * bbytes, &tmX, &full[stage], kb * TC_BK, p * TC_NMAX);
+                        if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer (one thread) ----------------
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t aphase = 0;
+            for (int it = it0; it < it1; ++it) {
+                const TcItem t = items[it];
+                for (int p = 0; p < npass; ++p) {
+                    const int N = min(TC_NMAX, lanes - p * TC_NMAX);
+                    const uint32_t idesc = umma_idesc_i8(TC_BM, N);
+                    mbar_wait(&tempty[acc], aphase ^ 1);
+                    tc_fence_after();
+                    const uint32_t d = tmem + (uint32_t)(acc * TC_NMAX);
+                    for (int kb = t.j0; kb < t.j1; ++kb) {
+                        mbar_wait(&full[stage], phase);
+                        tc_fence_after();
+                        const uint32_t a0 = smem_u32(sA + stage * TC_SMEM_A);
+                        const uint32_t b0 = smem_u32(sB + stage * bbytes);
+#pragma unroll
+                        for (int k = 0; k < TC_BK / 32; ++k)
+                            umma_i8(d, umma_desc_sw128(a0 + 32 * k), umma_desc_sw128(b0 + 32 * k), idesc,
+                                    (kb > t.j0 || k > 0) ? 1u : 0u);
+                        umma_commit(&empty[stage]);
+                        if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
+                    }
+                    umma_commit(&tfull[acc]);
+                    if (++acc == 2) { acc = 0; aphase ^= 1; }
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        // ---------------- epilogue (warps 2-5: TMEM lane quarter q = warp % 4) ----------------
+        const int q = warp & 3;
+        int acc = 0;
+        uint32_t aphase = 0;
+        for (int it = it0; it < it1; ++it) {
+            const TcItem t = items[it];
+            const long long row = (long long)t.I * TC_BM + q * 32 + lane;
+            for (int p = 0; p < npass; ++p) {
+                const int N = min(TC_NMAX, lanes - p * TC_NMAX);
+                mbar_wait(&tfull[acc], aphase);
+                tc_fence_after();
+                for (int cc = 0; cc < N; cc += 32) {
+                    uint32_t v[32];
+                    tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * TC_NMAX + cc), v);
+                    const int l0 = p * TC_NMAX + cc;  // global lane of column cc (multiple of 32)
+                    uint32_t h = 0u;
+                    if (row < n) h = (uint32_t)(__ldg(X + row * W + (l0 >> 6)) >> (l0 & 63));
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) v[k] = ((h >> k) & 1u) ? v[k] : 0u;
+                    const int sum = warp_transpose_sum32(v, lane);
+                    atomicAdd(reinterpret_cast<unsigned long long*>(&zacc[l0 + lane]),
+                              (unsigned long long)((long long)t.wgt * (long long)sum));
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[acc]);
+                if (++acc == 2) { acc = 0; aphase ^= 1; }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    for (int l = threadIdx.x; l < lanes; l += blockDim.x) zrows[(long long)blockIdx.x * lanes + l] = zacc[l];
+}
+
+}  // namespace gfors

@@ -32,6 +32,8 @@
 #include "shard.cuh"
 #include "push_dual.cuh"
 #include "push_primal.cuh"
+#include "dense_q.cuh"
+#include <cudaTypedefs.h>
 #include <cstdlib>
 
 using namespace gfors;
@@ -213,9 +215,9 @@ DirPlan plan_direction64(const DirPlan& d32, const std::vector<int64_t>& ptr, lo
 }
 
 const char* kClassNames[] = {"pdhg_dual", "pdhg_primal", "trig_rows", "trig_cols", "sample", "feas", "obj",
-                             "argmin", "halt", "pdhg_dual_push", "pdhg_primal_push"};
+                             "argmin", "halt", "pdhg_dual_push", "pdhg_primal_push", "pdhg_qx", "obj_tc"};
 enum KClass { KC_DUAL = 0, KC_PRIMAL, KC_TRIGR, KC_TRIGC, KC_SAMPLE, KC_FEAS, KC_OBJ, KC_ARGMIN, KC_HALT, KC_DUAL_PUSH,
-              KC_PRIMAL_PUSH, KC_N };
+              KC_PRIMAL_PUSH, KC_QX, KC_OBJ_TC, KC_N };
 
 }  // namespace
 
@@ -226,6 +228,30 @@ static void set_max_dyn_smem(const void* fn) {
     cudaFuncAttributes a;
     CK(cudaFuncGetAttributes(&a, fn));
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(SMEM_PER_BLOCK_MAX - a.sharedSizeBytes)));
+}
+
+// 2-D TMA map of a row-major int8 matrix [rows][ld] with (128-byte x box_rows) boxes and the 128-byte
+// swizzle the UMMA descriptors of dense_q.cuh expect; cuTensorMapEncodeTiled is taken from the driver
+// through the runtime's entry-point query (no libcuda link dependency)
+static CUtensorMap make_tmap_i8(const void* base, long long ld, long long rows, int box_rows) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    if (!enc) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess) throw Err{GFORS_E_CUDA, "cuTensorMapEncodeTiled not available"};
+        enc = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    }
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld};
+    const cuuint32_t box[2] = {128u, (cuuint32_t)box_rows};
+    const cuuint32_t estr[2] = {1u, 1u};
+    const CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Err{GFORS_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r)};
+    return m;
 }
 
 // =============================================================================================
@@ -312,6 +338,21 @@ struct gfors_ctx {
     std::vector<int64_t> perm;
     std::vector<signed char> rsign;
     int kkind = KV_F64;
+
+    // ---- dense-Q path (dense_q.cuh) ----
+    bool qdense = false;           // Q stored as dense int8 Qd[qld][qld]
+    long long qld = 0;             // padded dimension (multiple of 128)
+    int8_t* d_qd = nullptr;        // problem-owned
+    CUtensorMap tmQ{};             // TMA map of Qd (128 x 128 byte boxes, 128B swizzle)
+    TcItem* d_tcitems = nullptr;   // objective work items, grouped per CTA
+    int* d_tcoff = nullptr;        // [tc_grid + 1]
+    int tc_grid = 0;
+    double* d_qx = nullptr;        // [n] Q~ x of the primal input (prep-owned)
+    double* d_qdx = nullptr;       // [n] Q~ (x_k - x_{k-1}) for the trigger residual
+    double* d_qxpart = nullptr;    // [nchunk][qld] GEMV column-chunk partials
+    int8_t* d_Xs = nullptr;        // [64W][qld] unpacked samples (prep-owned)
+    long long Xs_lanes = 0;
+    CUtensorMap tmX{};
 
     // ---- device problem ----
     long long *d_kptr = nullptr, *d_ktptr = nullptr, *d_qptr = nullptr;
@@ -454,6 +495,7 @@ void gfors_ctx::free_problem() {
     d_kval = d_ktval = nullptr;
     d_qval = d_c = d_ru = nullptr;
     d_rsign = nullptr;
+    d_qd = nullptr; d_tcitems = nullptr; d_tcoff = nullptr; qdense = false; tc_grid = 0;
     for (auto& c : cnt) c = CountList{};
     d_int_row = nullptr; d_int_rhs = nullptr; d_int_eq = nullptr; d_int_seg_start = nullptr; d_int_seg_slot = nullptr;
     d_real_row = nullptr;
@@ -470,9 +512,10 @@ void gfors_ctx::free_prep() {
                    &d_w, (void**)&d_tmp[0], (void**)&d_tmp[1], (void**)&d_tmp[2], (void**)&d_tmp[3],
                    (void**)&d_red, (void**)&d_scalar, (void**)&d_segpart, (void**)&d_segpart2, (void**)&d_u, (void**)&d_ones, (void**)&d_rec, (void**)&d_regen, (void**)&d_plist[0], (void**)&d_plist[1], (void**)&d_pcount, (void**)&d_pflags, (void**)&d_acc, (void**)&d_rlist, (void**)&d_rcount, (void**)&d_wmax, (void**)&d_accx, (void**)&d_xst, (void**)&d_accv, (void**)&d_ones_cnt, (void**)&d_trig_flag, (void**)&d_part1,
                    (void**)&d_part2, (void**)&d_hist, (void**)&d_rho, (void**)&d_trace, (void**)&d_xbest,
-                   (void**)&d_X, (void**)&d_viol, (void**)&d_iacc, &d_zpart, (void**)&d_z, (void**)&d_ctrl};
+                   (void**)&d_X, (void**)&d_viol, (void**)&d_iacc, &d_zpart, (void**)&d_z, (void**)&d_ctrl,
+                   (void**)&d_qx, (void**)&d_qdx, (void**)&d_qxpart, (void**)&d_Xs};
     for (void** p : ps) { dfree(*p); *p = nullptr; }
-    X_words = iacc_len = zpart_len = z_len = 0;
+    X_words = iacc_len = zpart_len = z_len = Xs_lanes = 0;
     rho_cap = 0;
     trace_cap = 0;
     if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }
@@ -605,7 +648,21 @@ State<T> state_of(gfors_ctx* C) {
 }
 inline Csr csr_K(gfors_ctx* C) { return Csr{C->d_kptr, C->d_kcol, C->d_kval, C->m}; }
 inline Csr csr_Kt(gfors_ctx* C) { return Csr{C->d_ktptr, C->d_ktrow, C->d_ktval, C->n}; }
-inline Csr csr_Q(gfors_ctx* C) { return Csr{C->d_qptr, C->d_qcol, C->d_qval, C->n}; }
+inline Csr csr_Q(gfors_ctx* C, const double* pre = nullptr) { return Csr{C->d_qptr, C->d_qcol, C->d_qval, C->n, pre}; }
+
+// dense-Q GEMV (dense_q.cuh): out = Q~ (a - b), a/b picked on the device by iteration parity
+// (ctrl != nullptr) or taken directly (ctrl == nullptr, omega = 1: Preprocess power iteration)
+template <typename TX>
+void enqueue_qx(gfors_ctx* C, cudaStream_t s, QxSrc<TX> src, bool diff, double omega, double* out) {
+    const long long n = C->n;
+    const long long nchunk = (n + QX_CW - 1) / QX_CW;
+    const int grid = NUM_SMS_B200 * 4;
+    if (diff)
+        LAUNCH(C, s, KC_QX, (k_qx_dense<TX, true><<<grid, QX_NT, 0, s>>>(C->d_qd, C->qld, n, src, C->d_qxpart)));
+    else
+        LAUNCH(C, s, KC_QX, (k_qx_dense<TX, false><<<grid, QX_NT, 0, s>>>(C->d_qd, C->qld, n, src, C->d_qxpart)));
+    LAUNCH(C, s, KC_QX, (k_qx_final<<<grid_for(n), 256, 0, s>>>(n, C->qld, nchunk, C->d_qxpart, omega, out)));
+}
 
 #define SUB_SWITCH(sub, ...)                                  \
     switch (sub) {                                            \
@@ -675,7 +732,9 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
                                                                  C->d_rsign, C->m1, ctrl, kint, j))));
         }
     }
-    const Csr Q = csr_Q(C);
+    if (C->qdense)  // 2 Q~ x term of the primal gradient by the dense GEMV
+        enqueue_qx<T>(C, s, QxSrc<T>{{st.x[0], st.x[1]}, {nullptr, nullptr}, ctrl, kint, j}, false, C->omega, C->d_qx);
+    const Csr Q = csr_Q(C, C->qdense ? C->d_qx : nullptr);
     const T* qs = (const T*)C->d_qs;
     const T* cs = (const T*)C->d_cs;
     // K' values: SIGN rows fold the sign into w, so the transpose carries no values
@@ -807,8 +866,10 @@ void enqueue_trigger(gfors_ctx* C, cudaStream_t s, long long kint, long long j) 
     } else {
         LAUNCH(C, s, KC_TRIGR, (k_fill<<<1, NT, 0, s>>>(C->d_part1, 3LL * C->nb1, 0.0)));
     }
+    if (C->qdense)  // Q~(x_k - x_{k-1}) of s^x: x_k = par ? x[0] : x[1], x_{k-1} = par ? x[1] : x[0]
+        enqueue_qx<T>(C, s, QxSrc<T>{{st.x[1], st.x[0]}, {st.x[0], st.x[1]}, ctrl, kint, j}, true, C->omega, C->d_qdx);
     if (C->hasq)
-        LAUNCH(C, s, KC_TRIGC, (k_trig_cols<T, true><<<C->nb2, NT, 0, s>>>(C->n, csr_Q(C), (const T*)C->d_qs, st, ctrl,
+        LAUNCH(C, s, KC_TRIGC, (k_trig_cols<T, true><<<C->nb2, NT, 0, s>>>(C->n, csr_Q(C, C->qdense ? C->d_qdx : nullptr), (const T*)C->d_qs, st, ctrl,
                                                                             kint, j, C->d_part2)));
     else
         LAUNCH(C, s, KC_TRIGC, (k_trig_cols<T, false><<<C->nb2, NT, 0, s>>>(C->n, csr_Q(C), (const T*)C->d_qs, st, ctrl,
@@ -820,6 +881,19 @@ int obj_vpj(const gfors_ctx* C, int W) {
     const long long nchunk32 = (C->n + 31) / 32;
     long long v = nchunk32 * W / ((long long)NUM_SMS_B200 * 64);
     return (int)std::max<long long>(1, std::min<long long>(64, v));
+}
+
+// x_l' Q x_l of every lane of the batch by the tcgen05 int8 kernel (dense_q.cuh): unpack the bit-sliced
+// samples to int8 rows, then tc_grid partial rows of int64 lane sums at zrows
+void enqueue_obj_dense(gfors_ctx* C, cudaStream_t s, int W, long long* zrows) {
+    const long long lanes = 64LL * W;
+    LAUNCH(C, s, KC_OBJ_TC, (k_unpack_samples<<<grid_for(C->qld / 16 * lanes), NT, 0, s>>>(C->d_X, W, C->n, C->qld, C->d_Xs)));
+    const int nbox = (int)std::min<long long>(TC_NMAX, lanes);
+    const size_t sm = tc_smem_bytes(nbox, (int)lanes);
+    // the map of this batch width (host encode, ~1 us; captured by value into a graph node)
+    if (!C->dry) C->tmX = make_tmap_i8(C->d_Xs, C->qld, lanes, nbox);
+    LAUNCH(C, s, KC_OBJ_TC, (k_obj_dense_tc<<<C->tc_grid, TC_NT, sm, s>>>(C->tmQ, C->tmX, C->d_tcitems, C->d_tcoff, (int)lanes,
+                                                                         nbox, C->d_X, W, C->n, zrows)));
 }
 
 // evaluation of the batch in d_X (W words per variable); viol/iacc must have been reset
@@ -867,13 +941,22 @@ void enqueue_eval(gfors_ctx* C, cudaStream_t s, int W, const unsigned char* ones
         LAUNCH(C, s, KC_OBJ, (k_obj_bits<<<grid_for(jpw * W * 32), NT, 0, s>>>(C->n, vpj, C->d_planes, C->obj_nb, C->obj_cmin,
                                                                              C->d_X, W, (long long*)C->d_zpart)));
         long long rows = jpw;
-        if (C->hasq) {
+        if (C->qdense) {
+            enqueue_obj_dense(C, s, W, (long long*)C->d_zpart + jpw * 64LL * W);
+            rows += C->tc_grid;
+        } else if (C->hasq) {
             long long* zq = (long long*)C->d_zpart + jpw * 64LL * W;
             LAUNCH(C, s, KC_OBJ, (k_obj_quad<true><<<grid, NT, 0, s>>>(C->n, C->obj_chunk, Q, C->d_qval, C->d_X, W, zq)));
             rows += nchunk;
         }
         LAUNCH(C, s, KC_OBJ, (k_obj_final<true><<<2 * W, 1024, 0, s>>>(rows, W, C->d_zpart, C->c0, C->d_z)));
     } else if (C->integral) {
+        if (C->qdense) {
+            LAUNCH(C, s, KC_OBJ, (k_obj_partial<true, false><<<grid, NT, 0, s>>>(C->n, C->obj_chunk, C->d_c, Q, C->d_qval, C->d_X, W, C->d_zpart)));
+            enqueue_obj_dense(C, s, W, (long long*)C->d_zpart + nchunk * 64LL * W);
+            LAUNCH(C, s, KC_OBJ, (k_obj_final<true><<<2 * W, 1024, 0, s>>>(nchunk + C->tc_grid, W, C->d_zpart, C->c0, C->d_z)));
+            return;
+        }
         if (C->hasq)
             LAUNCH(C, s, KC_OBJ, (k_obj_partial<true, true><<<grid, NT, 0, s>>>(C->n, C->obj_chunk, C->d_c, Q, C->d_qval, C->d_X, W, C->d_zpart)));
         else
@@ -914,7 +997,16 @@ void ensure_batch(gfors_ctx* C, int W) {
     if (C->obj_bits) {
         const long long nchunk32 = (C->n + 31) / 32;
         const int vpj = obj_vpj(C, W);
-        zrows = (nchunk32 + vpj - 1) / vpj + (C->hasq ? nchunk : 0);
+        zrows = (nchunk32 + vpj - 1) / vpj + (C->qdense ? C->tc_grid : (C->hasq ? nchunk : 0));
+    } else if (C->qdense) {
+        zrows = nchunk + C->tc_grid;
+    }
+    if (C->qdense && 64LL * W > C->Xs_lanes) {  // grow-only: smaller batches (final round) reuse it
+        if (64LL * W > 4096) input_error("params.k_b: the dense-Q objective supports k_b <= 4096 per rank");
+        dfree(C->d_Xs);
+        C->d_Xs = dalloc<int8_t>(64LL * W * C->qld);
+        C->Xs_lanes = 64LL * W;
+        C->gvalid = false;
     }
     const long long zp = zrows * 64LL * W;
     if (zp > C->zpart_len) { dfree(C->d_zpart); C->d_zpart = dalloc<double>(zp); C->zpart_len = zp; C->gvalid = false; }
@@ -994,14 +1086,18 @@ static double power_iteration(gfors_ctx* C, bool isq, double tol, int max_iter) 
     bool restarted = false;
     const int gr = grid_for(rows * 32LL), gc = grid_for(cols * 32LL);
     for (int t = 1; t <= max_iter; ++t) {
-        if (isq) {
+        if (isq && C->qdense) {
+            enqueue_qx<double>(C, s, QxSrc<double>{{v, v}, {nullptr, nullptr}, nullptr, 0, 0}, false, 1.0, w);
+        } else if (isq) {
             k_spmv_rows<KV_F64><<<gr, NT, 0, s>>>(csr_Q(C), nullptr, nullptr, v, w);
         } else {
             KIND_SWITCH(C->kkind, (k_spmv_rows<KINDV><<<gr, NT, 0, s>>>(csr_K(C), C->d_rsign, C->d_s, v, w)));
         }
         CK(cudaGetLastError());
         sigma = dev_norm(C, w, rows);
-        if (isq) {
+        if (isq && C->qdense) {
+            enqueue_qx<double>(C, s, QxSrc<double>{{w, w}, {nullptr, nullptr}, nullptr, 0, 0}, false, 1.0, u);
+        } else if (isq) {
             k_spmv_rows<KV_F64><<<gc, NT, 0, s>>>(csr_Q(C), nullptr, nullptr, w, u);
         } else {
             KIND_SWITCH(C->kkind, (k_spmv_cols<KINDV><<<gc, NT, 0, s>>>(csr_Kt(C), C->d_rsign, C->d_s, w, u)));
@@ -1058,7 +1154,7 @@ static void select_plans(gfors_ctx* C) {
 template <typename T>
 static void alloc_loop_data(gfors_ctx* C) {
     const long long n = C->n, m = C->m;
-    C->d_g = dalloc<double>(m); C->d_rh = dalloc<double>(m); C->d_cs = dalloc<T>(n); C->d_qs = dalloc<T>(C->qnnz);
+    C->d_g = dalloc<double>(m); C->d_rh = dalloc<double>(m); C->d_cs = dalloc<T>(n); C->d_qs = dalloc<T>(C->qdense ? 1 : C->qnnz);
     for (int b = 0; b < 2; ++b) { C->d_x[b] = dalloc<T>(n); C->d_xb[b] = dalloc<T>(n); C->d_y[b] = dalloc<T>(m); }
     C->d_w = dalloc<T>(m);
     cudaStream_t s = C->stream;
@@ -1066,7 +1162,7 @@ static void alloc_loop_data(gfors_ctx* C) {
     CK(cudaGetLastError());
     k_scale_to<T><<<grid_for(n), NT, 0, s>>>(C->d_c, n, C->omega, (T*)C->d_cs);
     CK(cudaGetLastError());
-    if (C->qnnz) {
+    if (C->qnnz && !C->qdense) {
         k_scale_to<T><<<grid_for(C->qnnz), NT, 0, s>>>(C->d_qval, C->qnnz, C->omega, (T*)C->d_qs);
         CK(cudaGetLastError());
     }
@@ -1091,6 +1187,11 @@ static void do_preprocess(gfors_ctx* C, const gfors_prep_opts* o, gfors_scaling*
     C->d_red = dalloc<double>(2048);
     C->d_scalar = dalloc<double>(1);
     C->d_s = dalloc<double>(m);
+    if (C->qdense) {
+        C->d_qx = dalloc<double>(n);
+        C->d_qdx = dalloc<double>(n);
+        C->d_qxpart = dalloc<double>((n + QX_CW - 1) / QX_CW * C->qld);
+    }
     unsigned long long* d_zr = dalloc<unsigned long long>(1);
     CK(cudaMemsetAsync(d_zr, 0, sizeof(unsigned long long), s));
     // step 1: row 2-norms of K

@@ -30,6 +30,7 @@ struct Csr {
     const int* idx;        // int32 [nnz]
     const void* val;       // by KKind (nullptr for SIGN)
     long long rows;
+    const double* pre = nullptr;  // Q only: precomputed row products (dense-Q path, dense_q.cuh)
 };
 
 // Row-segment plan for long rows: segment s covers nonzeros [seg_start[s], seg_start[s+1]),
@@ -135,9 +136,13 @@ __global__ void __launch_bounds__(256) k_primal(Csr Kt, Csr Q, const T* __restri
             }
             for (; p < p1; p += SUB) a += kval<KIND>(Kt.val, p) * (double)__ldg(w + __ldg(Kt.idx + p));
             if constexpr (HASQ) {
-                const long long q0 = __ldg(Q.ptr + i), q1 = __ldg(Q.ptr + i + 1);
-                for (long long q = q0 + lane; q < q1; q += SUB)
-                    b += (double)__ldg(qs + q) * (double)__ldg(xin + __ldg(Q.idx + q));
+                if (Q.pre) {
+                    if (lane == 0) b = Q.pre[i];
+                } else {
+                    const long long q0 = __ldg(Q.ptr + i), q1 = __ldg(Q.ptr + i + 1);
+                    for (long long q = q0 + lane; q < q1; q += SUB)
+                        b += (double)__ldg(qs + q) * (double)__ldg(xin + __ldg(Q.idx + q));
+                }
             }
         }
         a = group_sum<SUB>(a);
@@ -236,8 +241,11 @@ __global__ void __launch_bounds__(256) k_primal_seg_final(long long n, SegPlan s
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += gridDim.x * (long long)blockDim.x) {
         double a = 0.0, b = 0.0;
         for (long long q = sp.row_seg[i]; q < sp.row_seg[i + 1]; ++q) a += part[q];
-        if constexpr (HASQ)
-            for (long long q = Q.ptr[i]; q < Q.ptr[i + 1]; ++q) b += (double)qs[q] * (double)xin[Q.idx[q]];
+        if constexpr (HASQ) {
+            if (Q.pre) b = Q.pre[i];
+            else
+                for (long long q = Q.ptr[i]; q < Q.ptr[i + 1]; ++q) b += (double)qs[q] * (double)xin[Q.idx[q]];
+        }
         const double xi = (double)xin[i];
         const double delta = (((double)cs[i] + rho) - a) + 2.0 * b - 2.0 * rho * xi;
         double xn = xi - tau1 * delta;
@@ -322,11 +330,14 @@ __global__ void __launch_bounds__(256) k_trig_cols(long long n, Csr Q, const T* 
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += gridDim.x * (long long)blockDim.x) {
         const double xi = (double)xk[i], xo = (double)xp[i];
         double e = 0.0;
-        if constexpr (HASQ)
-            for (long long q = Q.ptr[i]; q < Q.ptr[i + 1]; ++q) {
-                const int c = Q.idx[q];
-                e += (double)qs[q] * ((double)xk[c] - (double)xp[c]);
-            }
+        if constexpr (HASQ) {
+            if (Q.pre) e = Q.pre[i];  // dense-Q path: Q~(x_k - x_{k-1}) precomputed
+            else
+                for (long long q = Q.ptr[i]; q < Q.ptr[i + 1]; ++q) {
+                    const int c = Q.idx[q];
+                    e += (double)qs[q] * ((double)xk[c] - (double)xp[c]);
+                }
+        }
         const double sx = (xo - xi) / tau1 + 2.0 * e - 2.0 * rho * (xi - xo);
         sx2 += sx * sx;
         bg += xi * (1.0 - xi);

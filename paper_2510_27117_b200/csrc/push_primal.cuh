@@ -209,9 +209,12 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? PP_OCC32 : PP_OCC64) k_p
             for (int u = 0; u < PP_U; ++u) {
                 double b = 0.0;
                 if constexpr (HASQ)
-                    if (i0 + u < n)
-                        for (long long q = __ldg(Q.ptr + i0 + u); q < __ldg(Q.ptr + i0 + u + 1); ++q)
-                            b += (double)__ldg(qs + q) * (double)__ldg(xin + __ldg(Q.idx + q));
+                    if (i0 + u < n) {
+                        if (Q.pre) b = Q.pre[i0 + u];
+                        else
+                            for (long long q = __ldg(Q.ptr + i0 + u); q < __ldg(Q.ptr + i0 + u + 1); ++q)
+                                b += (double)__ldg(qs + q) * (double)__ldg(xin + __ldg(Q.idx + q));
+                    }
                 const double x0 = (double)xi[u];
                 const double delta = (((double)ci[u] + rho) - (double)ai[u] * invS) + 2.0 * b - 2.0 * rho * x0;
                 double xn = x0 - tau1 * delta;

@@ -143,9 +143,14 @@ __global__ void __launch_bounds__(SP_NT, 1) k_primal_sparse(Csr Kt, const long l
         double a = 0.0, bq = 0.0;
         if (cur.valid) {
             a = rb_row_sum<T, KIND, true>(Kt, sv, p0, cur.q0, cur.q1, lane, G);
-            if constexpr (HASQ)
-                for (long long q = __ldg(Q.ptr + i) + lane; q < __ldg(Q.ptr + i + 1); q += G)
-                    bq += (double)__ldg(qs + q) * (double)__ldg(xin + __ldg(Q.idx + q));
+            if constexpr (HASQ) {
+                if (Q.pre) {
+                    if (lane == 0) bq = Q.pre[i];
+                } else {
+                    for (long long q = __ldg(Q.ptr + i) + lane; q < __ldg(Q.ptr + i + 1); q += G)
+                        bq += (double)__ldg(qs + q) * (double)__ldg(xin + __ldg(Q.idx + q));
+                }
+            }
         }
         a = rb_group_sum(a, G);
         if constexpr (HASQ) bq = rb_group_sum(bq, G);

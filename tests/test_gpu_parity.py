@@ -14,7 +14,11 @@ from tests.util import brute_force, exhaustive_bits, inst_from_dense
 
 pytestmark = pytest.mark.gpu
 
-FAMILIES = ["setcover", "mis", "mkp", "bqp", "general", "real"]
+FAMILIES = ["setcover", "mis", "mkp", "bqp", "general", "real", "maxcut", "dense_psd"]
+# families whose PDHG map is (up to the small -2 rho x term) non-expansive, where the 1000-iteration bar
+# applies.  maxcut's Q is indefinite: the map expands free coordinates by up to 1 + 2 tau (||Q~|| + rho),
+# so rounding-order differences grow geometrically (reading R21; test_gpu_dense_q.py pins that bound).
+CONTRACTIVE = [f for f in FAMILIES if f != "maxcut"]
 
 
 @pytest.fixture(scope="module")
@@ -172,7 +176,7 @@ def test_one_step_parity(gf, fam, prec, tol):
     assert _rel(xg, xo) <= tol and _rel(xbg, xbo) <= tol and _rel(yg, yo) <= tol
 
 
-@pytest.mark.parametrize("fam", FAMILIES)
+@pytest.mark.parametrize("fam", CONTRACTIVE)
 @pytest.mark.parametrize("prec,tol", [(64, 1e-5), (32, 1e-3)])
 def test_1000_iteration_parity(gf, fam, prec, tol):
     """1000 iterations under the default rho schedule, sampling off."""
@@ -222,7 +226,7 @@ def _compare_runs(gf, inst, prec=64, graph=1, **kw):
     return s, o, ig, io, (zg, xg, mg), (zo, xo)
 
 
-@pytest.mark.parametrize("fam", ["setcover", "bqp", "mkp", "general"])
+@pytest.mark.parametrize("fam", ["setcover", "bqp", "mkp", "general", "dense_psd"])
 @pytest.mark.parametrize("graph", [1, 0])
 def test_run_parity_fp64(gf, fam, graph):
     """fp64 trajectories agree, so the incumbent sequence is identical."""

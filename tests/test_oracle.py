@@ -11,7 +11,7 @@ import pytest
 
 from gen import instances as G
 from oracle import oracle as O
-from tests.util import brute_force, exhaustive_bits, inst_from_dense
+from tests.util import all_points, brute_force, exhaustive_bits, inst_from_dense
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 SPEC = json.load(open(os.path.join(GOLD, "spec_examples.json")))
@@ -404,6 +404,25 @@ def test_eval_exhaustive_equals_brute_force(fam, seed):
         assert np.allclose(z, sign * zu, rtol=1e-12, atol=1e-9)
     if zb is not None:
         assert abs(z[feas.astype(bool)].min() - sign * zb) <= 1e-9
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_maxcut_qp_equals_cut_definition(seed):
+    """Max cut (next row f1): the oracle's EvalBest of the QP form on all 2^n points
+    equals the cut weight sum_{i<j} w_ij [x_i != x_j] computed from the edge weights by definition,
+    and its best lane is the maximum cut found by enumerating bipartitions directly."""
+    n = 13
+    inst = G.max_cut(n, 0.5, seed)
+    Wd = -G.dense_Q(inst)  # user Q_ij = -w_ij
+    assert np.all(np.diag(Wd) == 0) and np.array_equal(Wd, Wd.T)
+    assert np.abs(Wd).max() <= 10 and Wd.min() >= -8
+    o = O.Oracle(inst)
+    feas, z = o.eval(exhaustive_bits(n))
+    assert feas.all()
+    pts = all_points(n).astype(bool)
+    cuts = np.array([Wd[np.ix_(x, ~x)].sum() for x in pts])
+    assert np.array_equal(-z, cuts)  # canonical minimisation value = -cut
+    assert -z.min() == cuts.max()
 
 
 def test_brute_force_vs_milp():
