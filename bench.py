@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tti", action="store_true", help="skip the time-to-incumbent solves of configs 1-4")
     ap.add_argument("--profile-blocks", type=int, default=0, help="eager blocks replayed with per-kernel events (0 = --steps)")
+    ap.add_argument("--no-f1", action="store_true", help="skip the dense-Q max-cut leg (next row f1, config 6)")
+    ap.add_argument("--f1-steps", type=int, default=50)
     return ap.parse_args()
 
 
@@ -249,6 +251,75 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------------------------------------
+def run_f1_maxcut(args, gf, stream, local):
+    """Next row f1: the dense-Q path on the paper's largest max-cut size (config 6,
+    n = 20480, density 0.5).  Same step definition and clock as the headline line
+    (one Alg. 1 block per step, one graph launch for all timed blocks, CUDA events); rooflines of
+    its two kernels: the dense int8 GEMV (HBM: n^2 bytes of Q per launch) and the tcgen05 int8
+    objective (tensor: 2 * 128^2 * k_b ops per upper-triangle tile; HBM: its Q tile bytes)."""
+    import torch
+    t_gen = time.perf_counter()
+    inst = make_instance(6, args.seed)
+    t_gen = time.perf_counter() - t_gen
+    n = int(inst["n"])
+    s = gf.Solver(local, stream=stream.cuda_stream)
+    t0 = time.perf_counter()
+    s.load(inst)
+    sc = s.preprocess(precision=args.precision)
+    torch.cuda.synchronize()
+    t_load = time.perf_counter() - t0
+    common = dict(k_int=args.k_int, k_b=args.k_b, tol_primal=-1.0, tol_dual=-1.0, tol_binary=-1.0,
+                  stall_rel=-1.0, time_limit_s=1e9, trace_cap=16)
+    s.run(max_iters=max(3, args.warmup) * args.k_int, **common)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    K = args.f1_steps
+    e0.record(stream)
+    info = s.run(max_iters=K * args.k_int, **common)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    z, _, inc = s.best_incumbent(want_x=False)
+    prof = s.profile_blocks(min(K, 20), **common)
+    act = s.profile_active()
+    nb = min(K, 20)
+    peak_hbm, peak_src, peaks = measured_peaks()
+    fb = 8 if args.precision == 64 else 4
+    # GEMV: k_int primal products + 1 trigger difference product per block (each = dense + final launch)
+    qx_ms, qx_launches = act.get("pdhg_qx", (0.0, 0))
+    gemv_per_block = args.k_int + 1
+    gemv_ms = qx_ms / (nb * gemv_per_block)
+    gemv_bytes = n * n + 2 * n * fb + 8 * n
+    # objective tensor kernel: the upper block triangle of Q (T(T+1)/2 tiles of 128 x 128)
+    T = (n + 127) // 128
+    tiles = T * (T + 1) // 2
+    tc_ms, _ = act.get("obj_tc", (0.0, 0))
+    tc_ms /= nb
+    tc_ops = 2.0 * tiles * 128 * 128 * args.k_b
+    tc_bytes = tiles * 128 * 128 + (n * args.k_b)  # Q tiles + unpacked samples (first touch)
+    i8_peak = peaks.get("bf16_tflops", 1628.4) * 2.0  # int8 dense = 2x bf16 (guide's nominal ratio)
+    value = K * args.k_b / (ms * 1e-3)
+    s.close()
+    return {
+        "workload": "config6", "desc": "max cut QP n=20480, density 0.5, w ~ U{-8..10} (dense int8 Q)",
+        "n": n, "qnnz": int(inst["q_rowptr"][-1]), "value": value, "unit": UNIT, "steps": K,
+        "ms_per_step": ms / K, "pdhg_iters_per_s": K * args.k_int / (ms * 1e-3),
+        "z_best": z if inc["has_incumbent"] else None, "obj_scale": sc["obj_scale"],
+        "gen_s": t_gen, "load_preprocess_s": t_load, "kernel_ms_per_step": prof,
+        "roofline_gemv": {"bound": "hbm", "kernel": "k_qx_dense+k_qx_final", "achieved": gemv_bytes / (gemv_ms * 1e-3) / 1e9,
+                          "peak": peak_hbm, "unit": "GB/s", "frac": gemv_bytes / (gemv_ms * 1e-3) / 1e9 / peak_hbm,
+                          "algorithmic_bytes_per_launch": gemv_bytes, "avg_launch_ms": gemv_ms, "peak_source": peak_src},
+        "roofline_obj_tc": {"bound": "hbm" if tc_bytes / (peak_hbm * 1e9) > tc_ops / (i8_peak * 1e12) else "tensor",
+                            "kernel": "k_unpack_samples+k_obj_dense_tc", "avg_launch_ms": tc_ms,
+                            "achieved_tops": tc_ops / (tc_ms * 1e-3) / 1e12, "peak_tops_int8": i8_peak,
+                            "tensor_frac": tc_ops / (tc_ms * 1e-3) / 1e12 / i8_peak,
+                            "achieved_gbs": tc_bytes / (tc_ms * 1e-3) / 1e9, "hbm_frac": tc_bytes / (tc_ms * 1e-3) / 1e9 / peak_hbm,
+                            "ops_per_launch": tc_ops, "bytes_per_launch": tc_bytes,
+                            "peak_note": "int8 peak = MEASURED_PEAKS bf16 burst x 2 (nominal int8/bf16 ratio)"},
+    }
+
+
 def run_gpu(args):
     import torch
     rank, world, local = dist_env()
@@ -379,6 +450,10 @@ def run_gpu(args):
                                    "halt_reason": info_c["halt_reason"], "loop_s": info_c["elapsed_s"]}
             sc_.close()
 
+    f1 = None
+    if rank == 0 and world == 1 and not args.no_f1 and args.config != 6:
+        f1 = run_f1_maxcut(args, gf, stream, local)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         est = oracle_block_seconds(inst, args.k_int, args.k_b)
@@ -415,6 +490,7 @@ def run_gpu(args):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "time_to_incumbent_small_configs": tti,
+            "next_rows": {"f1_dense_q_maxcut": f1},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -32,7 +32,7 @@ namespace gfors {
 // Dense GEMV (fp64 accumulation) — PDHG gradient term and Preprocess power iteration on Q
 // ---------------------------------------------------------------------------------------------
 constexpr int QX_RW = 8;       // rows per warp unit (x reuse factor)
-constexpr int QX_CW = 1024;    // columns per warp unit (two 512-column strips)
+constexpr int QX_CW = 2048;    // columns per unit (partials are per 2048-column chunk)
 constexpr int QX_NT = 256;
 
 // source vector of the GEMV.  ctrl == nullptr: a[0] (minus b[0] if DIFF).  Otherwise the buffer
@@ -456,6 +456,162 @@ __global__ void __launch_bounds__(TC_NT, 1)
     tc_fence_after();
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
     for (int l = threadIdx.x; l < lanes; l += blockDim.x) zrows[(long long)blockIdx.x * lanes + l] = zacc[l];
+}
+
+// ---------------------------------------------------------------------------------------------
+// TMA-pipelined dense GEMV (the default): 64-row x 256-column int8 tiles of Qd stream through a
+// 6-stage mbarrier ring per CTA (one elected producer thread, 8 consumer warps), so ~96 KB per CTA
+// are in flight independently of the registers of the arithmetic.  Consumer warp w owns 8 rows of
+// the tile (x reused by 8 rows), lane l owns 8 columns (LDS.64 per row: conflict-free).  Unit =
+// (64-row block, 2048-column chunk); fixed-order reductions exactly as k_qx_dense.
+// ---------------------------------------------------------------------------------------------
+constexpr int QT_ROWS = 64, QT_COLS = 256, QT_STAGES = 6, QT_NT = 288;
+constexpr int QT_TILE = QT_ROWS * QT_COLS;  // 16 KB
+constexpr size_t qt_smem_bytes() { return 1024 + (size_t)QT_STAGES * QT_TILE + 256; }
+
+template <typename TX>
+__device__ __forceinline__ void qt_load_x8(const TX* __restrict__ a, const TX* __restrict__ b, long long col0,
+                                           long long n, double (&xv)[8]) {
+    if (col0 + 8 <= n) {
+        if constexpr (sizeof(TX) == 4) {
+            const float4 f0 = __ldg(reinterpret_cast<const float4*>(a + col0));
+            const float4 f1 = __ldg(reinterpret_cast<const float4*>(a + col0) + 1);
+            xv[0] = f0.x; xv[1] = f0.y; xv[2] = f0.z; xv[3] = f0.w; xv[4] = f1.x; xv[5] = f1.y; xv[6] = f1.z; xv[7] = f1.w;
+            if (b) {
+                const float4 g0 = __ldg(reinterpret_cast<const float4*>(b + col0));
+                const float4 g1 = __ldg(reinterpret_cast<const float4*>(b + col0) + 1);
+                xv[0] -= (double)g0.x; xv[1] -= (double)g0.y; xv[2] -= (double)g0.z; xv[3] -= (double)g0.w;
+                xv[4] -= (double)g1.x; xv[5] -= (double)g1.y; xv[6] -= (double)g1.z; xv[7] -= (double)g1.w;
+            }
+        } else {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const double2 f = __ldg(reinterpret_cast<const double2*>(a + col0) + v);
+                xv[2 * v] = f.x; xv[2 * v + 1] = f.y;
+            }
+            if (b) {
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const double2 f = __ldg(reinterpret_cast<const double2*>(b + col0) + v);
+                    xv[2 * v] -= f.x; xv[2 * v + 1] -= f.y;
+                }
+            }
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const long long c = col0 + k;
+            double v = 0.0;
+            if (c < n) {
+                v = (double)a[c];
+                if (b) v -= (double)b[c];
+            }
+            xv[k] = v;
+        }
+    }
+}
+
+template <typename TX, bool DIFF>
+__global__ void __launch_bounds__(QT_NT, 2) k_qx_tma(const __grid_constant__ CUtensorMap tmQ, long long n, long long ld,
+                                                    QxSrc<TX> src, double* __restrict__ part) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* tiles = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    uint64_t* full = reinterpret_cast<uint64_t*>(tiles + (size_t)QT_STAGES * QT_TILE);
+    uint64_t* empty = full + QT_STAGES;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long rblocks = (n + QT_ROWS - 1) / QT_ROWS;
+    const long long nchunk = (n + QX_CW - 1) / QX_CW;
+    const long long ntiles = (n + QT_COLS - 1) / QT_COLS;
+    const long long units = rblocks * nchunk;
+    constexpr int TPC = QX_CW / QT_COLS;  // tiles per chunk
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < QT_STAGES; ++st) { mbar_init(&full[st], 1); mbar_init(&empty[st], 8); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == 8) {
+        // ---------------- producer ----------------
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmQ)) : "memory");
+            int stage = 0;
+            uint32_t phase = 0;
+            for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+                const long long rb = u / nchunk, c = u - rb * nchunk;
+                const long long t1 = min(ntiles, (c + 1) * TPC);
+                for (long long t = c * TPC; t < t1; ++t) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_expect_tx(&full[stage], QT_TILE);
+                    tma_load_2d(tiles + (size_t)stage * QT_TILE, &tmQ, &full[stage], (int)(t * QT_COLS), (int)(rb * QT_ROWS));
+                    if (++stage == QT_STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+        return;
+    }
+    // ---------------- consumers ----------------
+    int par = 0;
+    if (src.ctrl) par = (int)(iter_index(src.ctrl, src.kint, src.j) & 1);
+    const TX* __restrict__ a = par ? src.a[1] : src.a[0];
+    const TX* __restrict__ b = DIFF ? (par ? src.b[1] : src.b[0]) : nullptr;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+        const long long rb = u / nchunk, c = u - rb * nchunk;
+        const long long t1 = min(ntiles, (c + 1) * TPC);
+        double acc[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) acc[r] = 0.0;
+        for (long long t = c * TPC; t < t1; ++t) {
+            double xv[8];
+            qt_load_x8<TX>(a, b, t * QT_COLS + 8 * lane, n, xv);  // issued before the wait
+            mbar_wait(&full[stage], phase);
+            const uint8_t* tile = tiles + (size_t)stage * QT_TILE + (size_t)(8 * warp) * QT_COLS + 8 * lane;
+            uint2 q[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) q[r] = *reinterpret_cast<const uint2*>(tile + r * QT_COLS);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            if (++stage == QT_STAGES) { stage = 0; phase ^= 1; }
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const uint32_t w0 = q[r].x ^ 0x80808080u, w1 = q[r].y ^ 0x80808080u;
+                double s_ = acc[r];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) s_ = fma(i8_to_f64(w0, k), xv[k], s_);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) s_ = fma(i8_to_f64(w1, k), xv[4 + k], s_);
+                acc[r] = s_;
+            }
+        }
+        // fixed-order transpose-reduce over the 32 lanes (as k_qx_dense)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const bool up = lane & 16;
+            const double send = up ? acc[k] : acc[k + 4];
+            const double keep = up ? acc[k + 4] : acc[k];
+            acc[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const bool up = lane & 8;
+            const double send = up ? acc[k] : acc[k + 2];
+            const double keep = up ? acc[k + 2] : acc[k];
+            acc[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        }
+        {
+            const bool up = lane & 4;
+            const double send = up ? acc[0] : acc[1];
+            const double keep = up ? acc[1] : acc[0];
+            acc[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        }
+        acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 2);
+        acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
+        if ((lane & 3) == 0) {
+            const int r = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+            const long long row = rb * QT_ROWS + 8 * warp + r;
+            if (row < n) part[c * ld + row] = acc[0];
+        }
+    }
 }
 
 }  // namespace gfors

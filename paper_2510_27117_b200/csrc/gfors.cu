@@ -233,7 +233,8 @@ static void set_max_dyn_smem(const void* fn) {
 // 2-D TMA map of a row-major int8 matrix [rows][ld] with (128-byte x box_rows) boxes and the 128-byte
 // swizzle the UMMA descriptors of dense_q.cuh expect; cuTensorMapEncodeTiled is taken from the driver
 // through the runtime's entry-point query (no libcuda link dependency)
-static CUtensorMap make_tmap_i8(const void* base, long long ld, long long rows, int box_rows) {
+static CUtensorMap make_tmap_i8(const void* base, long long ld, long long rows, int box_rows, int box_cols = 128,
+                                bool swz128 = true) {
     static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
     if (!enc) {
         void* fn = nullptr;
@@ -245,10 +246,11 @@ static CUtensorMap make_tmap_i8(const void* base, long long ld, long long rows, 
     CUtensorMap m;
     const cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
     const cuuint64_t strides[1] = {(cuuint64_t)ld};
-    const cuuint32_t box[2] = {128u, (cuuint32_t)box_rows};
+    const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
     const cuuint32_t estr[2] = {1u, 1u};
     const CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, swz128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Err{GFORS_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r)};
     return m;
@@ -344,6 +346,8 @@ struct gfors_ctx {
     long long qld = 0;             // padded dimension (multiple of 128)
     int8_t* d_qd = nullptr;        // problem-owned
     CUtensorMap tmQ{};             // TMA map of Qd (128 x 128 byte boxes, 128B swizzle)
+    CUtensorMap tmQ64{};           // TMA map of Qd for the GEMV (256-byte x 64-row boxes, no swizzle)
+    bool qx_tma = true;            // TMA-pipelined GEMV (GFORS_QX_TMA=0: the register-streaming k_qx_dense)
     TcItem* d_tcitems = nullptr;   // objective work items, grouped per CTA
     int* d_tcoff = nullptr;        // [tc_grid + 1]
     int tc_grid = 0;
@@ -656,11 +660,27 @@ template <typename TX>
 void enqueue_qx(gfors_ctx* C, cudaStream_t s, QxSrc<TX> src, bool diff, double omega, double* out) {
     const long long n = C->n;
     const long long nchunk = (n + QX_CW - 1) / QX_CW;
-    const int grid = NUM_SMS_B200 * 4;
-    if (diff)
-        LAUNCH(C, s, KC_QX, (k_qx_dense<TX, true><<<grid, QX_NT, 0, s>>>(C->d_qd, C->qld, n, src, C->d_qxpart)));
-    else
-        LAUNCH(C, s, KC_QX, (k_qx_dense<TX, false><<<grid, QX_NT, 0, s>>>(C->d_qd, C->qld, n, src, C->d_qxpart)));
+    if (C->qx_tma) {
+        const long long units = (n + QT_ROWS - 1) / QT_ROWS * nchunk;
+        const int grid = (int)std::min<long long>(units, NUM_SMS_B200 * 2LL);
+        static bool attr[4] = {false, false, false, false};
+        const int ai = (sizeof(TX) == 8 ? 2 : 0) + (diff ? 1 : 0);
+        if (!attr[ai]) {
+            if (diff) CK(cudaFuncSetAttribute(k_qx_tma<TX, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qt_smem_bytes()));
+            else CK(cudaFuncSetAttribute(k_qx_tma<TX, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qt_smem_bytes()));
+            attr[ai] = true;
+        }
+        if (diff)
+            LAUNCH(C, s, KC_QX, (k_qx_tma<TX, true><<<grid, QT_NT, qt_smem_bytes(), s>>>(C->tmQ64, n, C->qld, src, C->d_qxpart)));
+        else
+            LAUNCH(C, s, KC_QX, (k_qx_tma<TX, false><<<grid, QT_NT, qt_smem_bytes(), s>>>(C->tmQ64, n, C->qld, src, C->d_qxpart)));
+    } else {
+        const int grid = NUM_SMS_B200 * 4;
+        if (diff)
+            LAUNCH(C, s, KC_QX, (k_qx_dense<TX, true><<<grid, QX_NT, 0, s>>>(C->d_qd, C->qld, n, src, C->d_qxpart)));
+        else
+            LAUNCH(C, s, KC_QX, (k_qx_dense<TX, false><<<grid, QX_NT, 0, s>>>(C->d_qd, C->qld, n, src, C->d_qxpart)));
+    }
     LAUNCH(C, s, KC_QX, (k_qx_final<<<grid_for(n), 256, 0, s>>>(n, C->qld, nchunk, C->d_qxpart, omega, out)));
 }
 
