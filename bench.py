@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--profile-blocks", type=int, default=0, help="eager blocks replayed with per-kernel events (0 = --steps)")
     ap.add_argument("--no-f1", action="store_true", help="skip the dense-Q max-cut leg (next row f1, config 6)")
     ap.add_argument("--f1-steps", type=int, default=50)
+    ap.add_argument("--no-f2", action="store_true", help="skip the TU-reformulation facility-location leg (next row f2, config 7)")
+    ap.add_argument("--f2-iters", type=int, default=3000)
     return ap.parse_args()
 
 
@@ -320,6 +322,51 @@ def run_f1_maxcut(args, gf, stream, local):
     }
 
 
+def run_f2_facility(args, gf, stream, local):
+    """Next row f2: TUReformulate (PAPER §2.4.1) on the paper's facility-location
+    workload at (nf, nc) = (512, 2048) (config 7).  The same Alg. 1 run (SPEC
+    default halting, bounded by --f2-iters) with and without the reformulation: objective reached,
+    time to incumbent (device %globaltimer, Preprocess excluded as in PAPER L193), candidates/s,
+    and the host time of the reformulation itself (the paper's 'Avg. TU Time' column)."""
+    import torch
+    inst = make_instance(7, args.seed)
+    out = {"workload": "config7", "desc": "facility location nf=512, nc=2048 (n = 1,049,088; m = 1,050,624)",
+           "n": int(inst["n"]), "m": int(inst["m"])}
+    for tu in (True, False):
+        s = gf.Solver(local, stream=stream.cuda_stream)
+        s.load(inst)
+        t_tu = None
+        if tu:
+            t0 = time.perf_counter()
+            s.tu_reformulate(inst["tu_rows"], inst["tu_cols"])
+            t_tu = time.perf_counter() - t0
+        s.preprocess(precision=args.precision)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        info = s.run(max_iters=args.f2_iters, k_int=args.k_int, k_b=args.k_b)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        z, x, meta = s.best_incumbent()
+        feasible = None
+        if meta["has_incumbent"]:
+            # the lifted incumbent against the ORIGINAL rows (host check, exact integers)
+            K_rows = np.repeat(np.arange(inst["m"]), np.diff(inst["k_rowptr"]))
+            ax = np.bincount(K_rows, weights=inst["k_val"] * x[inst["k_col"]], minlength=inst["m"])
+            ok = np.where(inst["sense"] == 0, ax == inst["r"], np.where(inst["sense"] == 1, ax >= inst["r"], ax <= inst["r"]))
+            feasible = bool(ok.all()) and float(inst["c"] @ x) == z
+        out["tu" if tu else "no_tu"] = {
+            "reduced_n": s.n, "reduced_m": s.m, "tu_seconds": t_tu, "iters": info["iters"],
+            "halt_reason": info["halt_reason"], "z_best": z if meta["has_incumbent"] else None,
+            "time_to_incumbent_s": meta["found_time_s"] if meta["has_incumbent"] else None,
+            "loop_ms": ms, "candidates_per_s": info["candidates"] / (ms * 1e-3),
+            "pdhg_iters_per_s": info["iters"] / (ms * 1e-3), "incumbent_feasible_for_original": feasible}
+        s.close()
+    return out
+
+
 def run_gpu(args):
     import torch
     rank, world, local = dist_env()
@@ -453,6 +500,9 @@ def run_gpu(args):
     f1 = None
     if rank == 0 and world == 1 and not args.no_f1 and args.config != 6:
         f1 = run_f1_maxcut(args, gf, stream, local)
+    f2 = None
+    if rank == 0 and world == 1 and not args.no_f2:
+        f2 = run_f2_facility(args, gf, stream, local)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -490,7 +540,7 @@ def run_gpu(args):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "time_to_incumbent_small_configs": tti,
-            "next_rows": {"f1_dense_q_maxcut": f1},
+            "next_rows": {"f1_dense_q_maxcut": f1, "f2_tu_facility": f2},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

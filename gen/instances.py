@@ -239,6 +239,38 @@ def dense_laplacian(n, density, m, seed, name="dense_psd"):
     return inst
 
 
+def facility_location(nf, nc, seed, name="facility"):
+    """Uncapacitated facility location: min f'x + sum_ij c_ij y_ij s.t.
+    sum_i y_ij = 1 for every customer j (EQ), y_ij <= x_i (LE as y_ij - x_i <= 0).  Reading R24:
+    c_ij ~ U{1..100}, f_i ~ U{1..100} * ceil(nc/nf).  Variables: x_i at i, y_ij at nf + j*nf + i.
+    Rows: the nc customer rows first, then y_ij - x_i <= 0 in (j, i) order.  Also returns the TU
+    index sets of the paper's reformulation: J = the customer rows, I = for each
+    customer its cheapest y_ij (lowest i on ties) -> B_JI = identity."""
+    rng = _rng(seed)
+    f = (rng.integers(1, 101, size=nf) * -(-nc // nf)).astype(np.float64)
+    cost = rng.integers(1, 101, size=(nc, nf)).astype(np.float64)
+    n = nf + nf * nc
+    y = lambda j, i: nf + j * nf + i  # noqa: E731
+    rows_c, rows_v = [], []
+    for j in range(nc):
+        rows_c.append(np.array([y(j, i) for i in range(nf)]))
+        rows_v.append(np.ones(nf))
+    for j in range(nc):
+        for i in range(nf):
+            rows_c.append(np.array([i, y(j, i)]))
+            rows_v.append(np.array([-1.0, 1.0]))
+    m = nc + nf * nc
+    ptr, col, val = _csr_from_rows(rows_c, rows_v, m)
+    sense = np.concatenate([np.zeros(nc, np.int8), -np.ones(nf * nc, np.int8)])
+    r = np.concatenate([np.ones(nc), np.zeros(nf * nc)])
+    c = np.concatenate([f, cost.reshape(-1)])
+    inst = dict(name=name, n=n, m=m, k_rowptr=ptr, k_col=col, k_val=val, r=r, sense=sense,
+                q_rowptr=None, q_col=None, q_val=None, c=c, c0=0.0, maximize=False)
+    inst["tu_rows"] = np.arange(nc, dtype=np.int64)
+    inst["tu_cols"] = np.array([y(j, int(np.argmin(cost[j]))) for j in range(nc)], dtype=np.int32)
+    return inst
+
+
 def cut_value(inst_edges_w, x):
     """Cut weight sum_{i<j} w_ij [x_i != x_j] from a dense symmetric weight matrix (test helper)."""
     x = np.asarray(x).astype(bool)
@@ -293,6 +325,9 @@ CONFIGS = {
     # next row f1: dense-Q workload, the paper's largest max-cut size
     6: dict(desc="max cut QP n=20480, density 0.5, w ~ U{-8..10} (dense Q, next row f1)",
             make=lambda s: max_cut(20_480, 0.5, s, name="cfg6_maxcut_20480")),
+    # next row f2: the paper's facility-location TU workload at (nf, nc) = (512, 2048)
+    7: dict(desc="facility location nf=512, nc=2048 (TU reformulation, next row f2)",
+            make=lambda s: facility_location(512, 2048, s, name="cfg7_facility_512x2048")),
 }
 
 SMALL = {
@@ -304,6 +339,7 @@ SMALL = {
     "real": lambda s: random_general(200, 60, 10, 10, s, real=True, with_q=True, name="small_real"),
     "maxcut": lambda s: max_cut(300, 0.5, s, name="small_maxcut"),
     "dense_psd": lambda s: dense_laplacian(200, 0.5, 40, s, name="small_dense_psd"),
+    "facility": lambda s: facility_location(6, 24, s, name="small_facility"),
 }
 
 

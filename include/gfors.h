@@ -128,12 +128,28 @@ gfors_status gfors_create(gfors_ctx **out, const gfors_device_opts *opts);
  * negate; LE -> GE by negation; rows stably permuted GE first), builds the device
  * layouts (CSR K, CSR K', CSR Q) and classifies rows for the evaluator.  Copies inputs. */
 gfors_status gfors_load(gfors_ctx *ctx, const gfors_problem *prob);
+/* TUReformulate (PAPER §2.4.1, Theorem L823-846; Alg. 1), optional,
+ * between gfors_load and gfors_preprocess.  rows_J[count]: INPUT row indices (as passed to
+ * gfors_load) of equality rows; cols_I[count]: columns; B_JI (rows J, columns I) must be a signed
+ * permutation matrix (row J[t] meets I exactly at column I[t] with value +-1; general invertible
+ * B_JI needs the paper's LU-applied S and returns GFORS_E_INPUT), B_J and d_J integral.  Eliminates
+ * x_I = s + S x_Ibar (s = B_JI^-1 d_J, S = -B_JI^-1 B_J,Ibar) exactly by substitution into Q, c, c0
+ * and the other rows, adds the box rows S x >= -s, -S x >= s - 1 (those every binary x satisfies
+ * are dropped) and loads the reduced problem in place (reduced variables = Ibar ascending; rows =
+ * the non-J input rows in input order, then the box rows; reading R24).  Afterwards
+ * gfors_sample/gfors_eval/state hooks work on the reduced variables (gfors_dims), while
+ * gfors_best_incumbent returns z in the original sense and x lifted to the ORIGINAL n variables.
+ * Host only; copies; errors name the offending row/column. */
+gfors_status gfors_tu_reformulate(gfors_ctx *ctx, const int64_t *rows_J, const int32_t *cols_I, int64_t count);
+/* Current problem dimensions (reduced after gfors_tu_reformulate) and the original n. */
+gfors_status gfors_dims(gfors_ctx *ctx, int64_t *n, int64_t *m, int64_t *n_orig);
 /* Preprocess on the device (row norms, power iterations).  out may be NULL. */
 gfors_status gfors_preprocess(gfors_ctx *ctx, const gfors_prep_opts *opts, gfors_scaling *out);
 /* Alg. 1 from x0 = 0.5*1, y0 = 0 (reading R14).  Blocks until the loop has finished.
  * Collective when world > 1 (all ranks must call with identical params except k_b). */
 gfors_status gfors_run(gfors_ctx *ctx, const gfors_params *p, gfors_run_info *out);
-/* z: objective in ORIGINAL units and sense (+inf if none); x: n bytes (0/1) or NULL (host).
+/* z: objective in ORIGINAL units and sense (+inf if none); x: n bytes (0/1) or NULL (host); after
+ * gfors_tu_reformulate, x has the ORIGINAL n (n_orig of gfors_dims) entries, lifted.
  * Returns GFORS_NO_INCUMBENT if no feasible point was found. */
 gfors_status gfors_best_incumbent(gfors_ctx *ctx, double *z, uint8_t *x, gfors_incumbent_info *info);
 const char *gfors_last_error(const gfors_ctx *ctx);

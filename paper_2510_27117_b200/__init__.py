@@ -98,6 +98,8 @@ EXPORTS = {
     "gfors_profile_active": (I32, [P, P, P, I32]),
     "gfors_launches_per_block": (I64, [P, C.POINTER(Params)]),
     "gfors_merge_records": (I32, [P, P, P, I32]),
+    "gfors_tu_reformulate": (I32, [P, P, P, I64]),
+    "gfors_dims": (I32, [P, P, P, P]),
     "gfors_nccl_unique_id": (I32, [P]),
     "gfors_graph_note": (C.c_char_p, [P]),
 }
@@ -211,6 +213,17 @@ class Solver:
         pr.maximize = int(bool(inst.get("maximize", False)))
         self._chk(_lib.gfors_load(self.h, C.byref(pr)))
         self.n, self.m = pr.n, pr.m
+        self.n_orig = pr.n
+        return self
+
+    def tu_reformulate(self, rows_J, cols_I):
+        """gfors_tu_reformulate (PAPER §2.4.1): eliminate x_I through the equality rows J."""
+        J = np.ascontiguousarray(rows_J, dtype=np.int64)
+        I = np.ascontiguousarray(cols_I, dtype=np.int32)
+        self._chk(_lib.gfors_tu_reformulate(self.h, _ptr(J), _ptr(I), len(J)))
+        n, m, no = I64(), I64(), I64()
+        self._chk(_lib.gfors_dims(self.h, C.byref(n), C.byref(m), C.byref(no)))
+        self.n, self.m, self.n_orig = n.value, m.value, no.value
         return self
 
     def preprocess(self, tol=1e-7, max_iter=500, precision=64):
@@ -233,7 +246,7 @@ class Solver:
 
     def best_incumbent(self, want_x=True):
         z = C.c_double()
-        x = np.zeros(self.n, dtype=np.uint8) if want_x else None
+        x = np.zeros(getattr(self, "n_orig", self.n), dtype=np.uint8) if want_x else None
         info = IncumbentInfo()
         self._chk(_lib.gfors_best_incumbent(self.h, C.byref(z), _ptr(x), C.byref(info)), ok=(0, 2))
         meta = {f: getattr(info, f) for f, _ in IncumbentInfo._fields_}

@@ -341,6 +341,19 @@ struct gfors_ctx {
     std::vector<signed char> rsign;
     int kkind = KV_F64;
 
+    // ---- TUReformulate lift data (tu_impl.inc) ----
+    struct TuLift {
+        bool active = false;
+        long long n_orig = 0;
+        bool maximize = false;          // sense of the ORIGINAL problem (the reduced one is canonical)
+        std::vector<int> keep;          // reduced variable -> original column (Ibar, ascending)
+        std::vector<int> icol;          // eliminated columns I
+        std::vector<double> s;          // x_I = s + S x_Ibar
+        std::vector<int64_t> sptr;
+        std::vector<int32_t> scol;
+        std::vector<double> sval;
+    } tu;
+
     // ---- dense-Q path (dense_q.cuh) ----
     bool qdense = false;           // Q stored as dense int8 Qd[qld][qld]
     long long qld = 0;             // padded dimension (multiple of 128)
@@ -539,6 +552,7 @@ gfors_ctx::~gfors_ctx() {
 }
 
 #include "load_impl.inc"
+#include "tu_impl.inc"
 
 // =============================================================================================
 // Typed dispatch helpers
@@ -1581,7 +1595,23 @@ gfors_status gfors_create(gfors_ctx** out, const gfors_device_opts* opts) {
 
 gfors_status gfors_load(gfors_ctx* C, const gfors_problem* prob) {
     API_BEGIN(C)
+    C->tu = gfors_ctx::TuLift{};
     do_load(C, prob);
+    API_END(C)
+}
+
+gfors_status gfors_tu_reformulate(gfors_ctx* C, const int64_t* rows_J, const int32_t* cols_I, int64_t count) {
+    API_BEGIN(C)
+    do_tu_reformulate(C, rows_J, cols_I, count);
+    API_END(C)
+}
+
+gfors_status gfors_dims(gfors_ctx* C, int64_t* n, int64_t* m, int64_t* n_orig) {
+    API_BEGIN(C)
+    if (C->stage < 1) throw Err{GFORS_E_STATE, "gfors_dims: call gfors_load first"};
+    if (n) *n = C->n;
+    if (m) *m = C->m;
+    if (n_orig) *n_orig = C->tu.active ? C->tu.n_orig : C->n;
     API_END(C)
 }
 
@@ -1609,9 +1639,13 @@ gfors_status gfors_best_incumbent(gfors_ctx* C, double* z, uint8_t* x, gfors_inc
         if (!C->have_run) throw Err{GFORS_E_STATE, "gfors_best_incumbent: call gfors_run first"};
         Ctrl h;
         CK(cudaMemcpyAsync(&h, C->d_ctrl, sizeof h, cudaMemcpyDeviceToHost, C->stream));
-        if (x) CK(cudaMemcpyAsync(x, C->d_xbest, C->n, cudaMemcpyDeviceToHost, C->stream));
+        std::vector<uint8_t> xr;
+        if (x && C->tu.active) xr.resize(C->n);
+        if (x) CK(cudaMemcpyAsync(C->tu.active ? xr.data() : x, C->d_xbest, C->n, cudaMemcpyDeviceToHost, C->stream));
         CK(cudaStreamSynchronize(C->stream));
-        const double zz = h.has_inc ? (C->maximize ? -h.z_best : h.z_best) : INFINITY;
+        if (x && C->tu.active) tu_lift(C, xr.data(), x);  // x_I = s + S x_Ibar
+        const bool maxi = C->tu.active ? C->tu.maximize : C->maximize;
+        const double zz = h.has_inc ? (maxi ? -h.z_best : h.z_best) : INFINITY;
         if (z) *z = zz;
         if (info) {
             info->found_iter = h.found_iter; info->found_round = h.found_round; info->found_index = h.found_index;
