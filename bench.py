@@ -329,9 +329,18 @@ def run_f2_facility(args, gf, stream, local):
     time to incumbent (device %globaltimer, Preprocess excluded as in PAPER L193), candidates/s,
     and the host time of the reformulation itself (the paper's 'Avg. TU Time' column)."""
     import torch
-    inst = make_instance(7, args.seed)
+    from gen import instances as G
     out = {"workload": "config7", "desc": "facility location nf=512, nc=2048 (n = 1,049,088; m = 1,050,624)",
-           "n": int(inst["n"]), "m": int(inst["m"])}
+           "note": "fixed iteration budget, halting disabled; 'small' = (nf, nc) = (16, 64), fp64, 30000 iterations"}
+    for key, inst, iters, prec in (("", make_instance(7, args.seed), args.f2_iters, args.precision),
+                                   ("small_", G.facility_location(16, 64, args.seed), 30000, 64)):
+        _f2_pair(out, key, inst, iters, prec, args, gf, stream, local)
+    return out
+
+
+def _f2_pair(out, key, inst, iters, prec, args, gf, stream, local):
+    import torch
+    out[key + "n"], out[key + "m"] = int(inst["n"]), int(inst["m"])
     for tu in (True, False):
         s = gf.Solver(local, stream=stream.cuda_stream)
         s.load(inst)
@@ -340,12 +349,13 @@ def run_f2_facility(args, gf, stream, local):
             t0 = time.perf_counter()
             s.tu_reformulate(inst["tu_rows"], inst["tu_cols"])
             t_tu = time.perf_counter() - t0
-        s.preprocess(precision=args.precision)
+        s.preprocess(precision=prec)
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        info = s.run(max_iters=args.f2_iters, k_int=args.k_int, k_b=args.k_b)
+        info = s.run(max_iters=iters, k_int=args.k_int, k_b=args.k_b, tol_primal=-1.0, tol_dual=-1.0,
+                     tol_binary=-1.0, stall_rel=-1.0)
         e1.record(stream)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
@@ -357,14 +367,13 @@ def run_f2_facility(args, gf, stream, local):
             ax = np.bincount(K_rows, weights=inst["k_val"] * x[inst["k_col"]], minlength=inst["m"])
             ok = np.where(inst["sense"] == 0, ax == inst["r"], np.where(inst["sense"] == 1, ax >= inst["r"], ax <= inst["r"]))
             feasible = bool(ok.all()) and float(inst["c"] @ x) == z
-        out["tu" if tu else "no_tu"] = {
+        out[key + ("tu" if tu else "no_tu")] = {
             "reduced_n": s.n, "reduced_m": s.m, "tu_seconds": t_tu, "iters": info["iters"],
             "halt_reason": info["halt_reason"], "z_best": z if meta["has_incumbent"] else None,
             "time_to_incumbent_s": meta["found_time_s"] if meta["has_incumbent"] else None,
             "loop_ms": ms, "candidates_per_s": info["candidates"] / (ms * 1e-3),
             "pdhg_iters_per_s": info["iters"] / (ms * 1e-3), "incumbent_feasible_for_original": feasible}
         s.close()
-    return out
 
 
 def run_gpu(args):

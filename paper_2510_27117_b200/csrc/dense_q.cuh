@@ -614,4 +614,147 @@ __global__ void __launch_bounds__(QT_NT, 2) k_qx_tma(const __grid_constant__ CUt
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// fp32 iterates: the same TMA ring, but the products are EXACT integer dot products.  x (fp32, in
+// [0,1]) is taken on the 2^-31 fixed-point grid (X = rint(x 2^31) < 2^32; the difference of the
+// trigger in [-1,1] on 2^-30: a signed int32), split into 4 byte digits, and
+// sum_j Q_ij X_j = sum_d 2^(8d) sum_j Q_ij X_jd with dp4a (4 int8 x 4 byte MACs into int32 per
+// instruction; |partial| <= 127*255*64 per lane and unit, no overflow).  Exact and order-free;
+// the only approximation is the fixed-point image of x (|error| <= 2^-32 per element, far below the
+// fp32 rounding of the stored iterate).  One dp4a per element instead of two fp64 operations.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ int dp4a_su(uint32_t a_s8, uint32_t b_u8, int c) {
+    int d;
+    asm("dp4a.s32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a_s8), "r"(b_u8), "r"(c));
+    return d;
+}
+__device__ __forceinline__ int dp4a_ss(uint32_t a_s8, uint32_t b_s8, int c) {
+    int d;
+    asm("dp4a.s32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a_s8), "r"(b_s8), "r"(c));
+    return d;
+}
+
+// byte digits of 4 fixed-point values, transposed: w[d] = byte d of X0 | byte d of X1 << 8 | ...
+__device__ __forceinline__ void digits4(uint32_t X0, uint32_t X1, uint32_t X2, uint32_t X3, uint32_t (&w)[4]) {
+    const uint32_t lo01 = __byte_perm(X0, X1, 0x5140), hi01 = __byte_perm(X0, X1, 0x7362);  // b0a0b1a1.. per pair
+    const uint32_t lo23 = __byte_perm(X2, X3, 0x5140), hi23 = __byte_perm(X2, X3, 0x7362);
+    w[0] = __byte_perm(lo01, lo23, 0x5410);
+    w[1] = __byte_perm(lo01, lo23, 0x7632);
+    w[2] = __byte_perm(hi01, hi23, 0x5410);
+    w[3] = __byte_perm(hi01, hi23, 0x7632);
+}
+
+template <bool DIFF>
+__global__ void __launch_bounds__(QT_NT, 2) k_qx_tma_fix(const __grid_constant__ CUtensorMap tmQ, long long n, long long ld,
+                                                        QxSrc<float> src, double* __restrict__ part) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* tiles = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    uint64_t* full = reinterpret_cast<uint64_t*>(tiles + (size_t)QT_STAGES * QT_TILE);
+    uint64_t* empty = full + QT_STAGES;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long rblocks = (n + QT_ROWS - 1) / QT_ROWS;
+    const long long nchunk = (n + QX_CW - 1) / QX_CW;
+    const long long ntiles = (n + QT_COLS - 1) / QT_COLS;
+    const long long units = rblocks * nchunk;
+    constexpr int TPC = QX_CW / QT_COLS;
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < QT_STAGES; ++st) { mbar_init(&full[st], 1); mbar_init(&empty[st], 8); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == 8) {
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmQ)) : "memory");
+            int stage = 0;
+            uint32_t phase = 0;
+            for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+                const long long rb = u / nchunk, c = u - rb * nchunk;
+                const long long t1 = min(ntiles, (c + 1) * TPC);
+                for (long long t = c * TPC; t < t1; ++t) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_expect_tx(&full[stage], QT_TILE);
+                    tma_load_2d(tiles + (size_t)stage * QT_TILE, &tmQ, &full[stage], (int)(t * QT_COLS), (int)(rb * QT_ROWS));
+                    if (++stage == QT_STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+        return;
+    }
+    int par = 0;
+    if (src.ctrl) par = (int)(iter_index(src.ctrl, src.kint, src.j) & 1);
+    const float* __restrict__ a = par ? src.a[1] : src.a[0];
+    const float* __restrict__ b = DIFF ? (par ? src.b[1] : src.b[0]) : nullptr;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+        const long long rb = u / nchunk, c = u - rb * nchunk;
+        const long long t1 = min(ntiles, (c + 1) * TPC);
+        int acc[8][4];
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+            for (int d = 0; d < 4; ++d) acc[r][d] = 0;
+        for (long long t = c * TPC; t < t1; ++t) {
+            // fixed-point digits of this lane's 8 columns (issued before the wait)
+            double xv[8];
+            qt_load_x8<float>(a, b, t * QT_COLS + 8 * lane, n, xv);
+            uint32_t X[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                X[k] = DIFF ? (uint32_t)__double2int_rn(xv[k] * 1073741824.0) : (uint32_t)__double2ull_rn(xv[k] * 2147483648.0);
+            uint32_t w0[4], w1[4];
+            digits4(X[0], X[1], X[2], X[3], w0);
+            digits4(X[4], X[5], X[6], X[7], w1);
+            mbar_wait(&full[stage], phase);
+            const uint8_t* tile = tiles + (size_t)stage * QT_TILE + (size_t)(8 * warp) * QT_COLS + 8 * lane;
+            uint2 q[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) q[r] = *reinterpret_cast<const uint2*>(tile + r * QT_COLS);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            if (++stage == QT_STAGES) { stage = 0; phase ^= 1; }
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+#pragma unroll
+                for (int d = 0; d < 3; ++d) acc[r][d] = dp4a_su(q[r].y, w1[d], dp4a_su(q[r].x, w0[d], acc[r][d]));
+                if (DIFF) acc[r][3] = dp4a_ss(q[r].y, w1[3], dp4a_ss(q[r].x, w0[3], acc[r][3]));
+                else acc[r][3] = dp4a_su(q[r].y, w1[3], dp4a_su(q[r].x, w0[3], acc[r][3]));
+            }
+        }
+        long long v[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+            v[r] = (long long)acc[r][0] + ((long long)acc[r][1] << 8) + ((long long)acc[r][2] << 16) +
+                   ((long long)acc[r][3] << 24);
+        // exact integer transpose-reduce over the 32 lanes
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const bool up = lane & 16;
+            const long long send = up ? v[k] : v[k + 4];
+            const long long keep = up ? v[k + 4] : v[k];
+            v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const bool up = lane & 8;
+            const long long send = up ? v[k] : v[k + 2];
+            const long long keep = up ? v[k + 2] : v[k];
+            v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        }
+        {
+            const bool up = lane & 4;
+            const long long send = up ? v[0] : v[1];
+            const long long keep = up ? v[1] : v[0];
+            v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        }
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+        if ((lane & 3) == 0) {
+            const int r = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+            const long long row = rb * QT_ROWS + 8 * warp + r;
+            if (row < n) part[c * ld + row] = (double)v[0] * (DIFF ? 9.313225746154785e-10 : 4.656612873077393e-10);
+        }
+    }
+}
+
 }  // namespace gfors

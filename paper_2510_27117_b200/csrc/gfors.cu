@@ -136,6 +136,10 @@ struct DirPlan {  // how one product direction (K rows or K' columns) is compute
 };
 
 // greedy nonzero-balanced row blocks: consecutive rows, <= cap nonzeros each (rows <= cap long)
+// rows per row block at most (empty rows, e.g. every column when m = 0, would otherwise pile into
+// one CTA: max cut's primal took 84 us per launch for n = 20480 in a single block)
+constexpr long long RB_ROWS_MAX = 512;
+
 static std::vector<long long> make_rowblocks(const std::vector<int64_t>& ptr, long long rows, long long cap,
                                              long long cap_rows = LLONG_MAX) {
     std::vector<long long> b;
@@ -173,7 +177,7 @@ DirPlan plan_direction(const std::vector<int64_t>& ptr, long long rows, cudaStre
         d.seg = true;
     }
     if (d.rb) {
-        std::vector<long long> b = make_rowblocks(ptr, rows, RB_NNZ32);
+        std::vector<long long> b = make_rowblocks(ptr, rows, RB_NNZ32, RB_ROWS_MAX);
         d.nblk = (long long)b.size() - 1;
         d.blk_row = dupload(b, s);
         owned.push_back(d.blk_row);
@@ -207,7 +211,7 @@ DirPlan plan_direction64(const DirPlan& d32, const std::vector<int64_t>& ptr, lo
         d.nblk = 0;
         return d;
     }
-    std::vector<long long> b = make_rowblocks(ptr, rows, RB_NNZ64);
+    std::vector<long long> b = make_rowblocks(ptr, rows, RB_NNZ64, RB_ROWS_MAX);
     d.nblk = (long long)b.size() - 1;
     d.blk_row = dupload(b, s);
     owned.push_back(d.blk_row);
@@ -361,6 +365,7 @@ struct gfors_ctx {
     CUtensorMap tmQ{};             // TMA map of Qd (128 x 128 byte boxes, 128B swizzle)
     CUtensorMap tmQ64{};           // TMA map of Qd for the GEMV (256-byte x 64-row boxes, no swizzle)
     bool qx_tma = true;            // TMA-pipelined GEMV (GFORS_QX_TMA=0: the register-streaming k_qx_dense)
+    bool qx_fix = true;            // fp32 iterates: exact fixed-point dp4a GEMV (GFORS_QX_FIX=0: fp64 FMA)
     TcItem* d_tcitems = nullptr;   // objective work items, grouped per CTA
     int* d_tcoff = nullptr;        // [tc_grid + 1]
     int tc_grid = 0;
@@ -674,6 +679,24 @@ template <typename TX>
 void enqueue_qx(gfors_ctx* C, cudaStream_t s, QxSrc<TX> src, bool diff, double omega, double* out) {
     const long long n = C->n;
     const long long nchunk = (n + QX_CW - 1) / QX_CW;
+    if constexpr (sizeof(TX) == 4) {
+        if (C->qx_fix) {  // fp32 iterates: exact dp4a products on the fixed-point image of x
+            const long long units = (n + QT_ROWS - 1) / QT_ROWS * nchunk;
+            const int grid = (int)std::min<long long>(units, NUM_SMS_B200 * 2LL);
+            static bool attr[2] = {false, false};
+            if (!attr[diff ? 1 : 0]) {
+                if (diff) CK(cudaFuncSetAttribute(k_qx_tma_fix<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qt_smem_bytes()));
+                else CK(cudaFuncSetAttribute(k_qx_tma_fix<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qt_smem_bytes()));
+                attr[diff ? 1 : 0] = true;
+            }
+            if (diff)
+                LAUNCH(C, s, KC_QX, (k_qx_tma_fix<true><<<grid, QT_NT, qt_smem_bytes(), s>>>(C->tmQ64, n, C->qld, src, C->d_qxpart)));
+            else
+                LAUNCH(C, s, KC_QX, (k_qx_tma_fix<false><<<grid, QT_NT, qt_smem_bytes(), s>>>(C->tmQ64, n, C->qld, src, C->d_qxpart)));
+            LAUNCH(C, s, KC_QX, (k_qx_final<<<grid_for(n), 256, 0, s>>>(n, C->qld, nchunk, C->d_qxpart, omega, out)));
+            return;
+        }
+    }
     if (C->qx_tma) {
         const long long units = (n + QT_ROWS - 1) / QT_ROWS * nchunk;
         const int grid = (int)std::min<long long>(units, NUM_SMS_B200 * 2LL);
