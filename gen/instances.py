@@ -271,6 +271,23 @@ def facility_location(nf, nc, seed, name="facility"):
     return inst
 
 
+def assignment3d(n, seed, name="assign3d"):
+    """3D assignment (PAPER eq. assign3d): min c'x over x in {0,1}^(n^3), sum_{jk} x_ijk = 1,
+    sum_{ik} x_ijk = 1, sum_{ij} x_ijk = 1; c_ijk ~ U{1..100} (reading R25).  Variable (i,j,k) at flat
+    index i*n^2 + j*n + k; rows: the n i-rows, then the n j-rows, then the n k-rows (all EQ)."""
+    rng = _rng(seed)
+    N = n ** 3
+    v = np.arange(N)
+    I, J, K = v // (n * n), (v // n) % n, v % n
+    rows_c = [np.flatnonzero(I == a) for a in range(n)] + [np.flatnonzero(J == a) for a in range(n)] + \
+             [np.flatnonzero(K == a) for a in range(n)]
+    ptr, col, val = _csr_from_rows(rows_c, [np.ones(len(r)) for r in rows_c], 3 * n)
+    c = rng.integers(1, 101, size=N).astype(np.float64)
+    return dict(name=name, n=N, m=3 * n, k_rowptr=ptr, k_col=col, k_val=val, r=np.ones(3 * n),
+                sense=np.zeros(3 * n, np.int8), q_rowptr=None, q_col=None, q_val=None, c=c, c0=0.0,
+                maximize=False, a3_n=n)
+
+
 def cut_value(inst_edges_w, x):
     """Cut weight sum_{i<j} w_ij [x_i != x_j] from a dense symmetric weight matrix (test helper)."""
     x = np.asarray(x).astype(bool)
@@ -328,6 +345,9 @@ CONFIGS = {
     # next row f2: the paper's facility-location TU workload at (nf, nc) = (512, 2048)
     7: dict(desc="facility location nf=512, nc=2048 (TU reformulation, next row f2)",
             make=lambda s: facility_location(512, 2048, s, name="cfg7_facility_512x2048")),
+    # next row f3: 3D assignment n = 64 (262,144 binaries, 192 equality rows) for Alg. 4 sampling
+    8: dict(desc="3D assignment n=64 (customised sampling, next row f3)",
+            make=lambda s: assignment3d(64, s, name="cfg8_assign3d_64")),
 }
 
 SMALL = {
@@ -340,6 +360,7 @@ SMALL = {
     "maxcut": lambda s: max_cut(300, 0.5, s, name="small_maxcut"),
     "dense_psd": lambda s: dense_laplacian(200, 0.5, 40, s, name="small_dense_psd"),
     "facility": lambda s: facility_location(6, 24, s, name="small_facility"),
+    "assign3d": lambda s: assignment3d(8, s, name="small_assign3d"),
 }
 
 

@@ -102,6 +102,15 @@ typedef struct {
     uint64_t seed;                /* Philox key */
     int32_t use_graph;            /* 1: CUDA graph with a device WHILE node (default); 0: eager */
     int32_t trace_cap;            /* trace ring-buffer rows (default 4096) */
+    /* RandSampleStep: 0 = Bernoulli(x_k) (Alg. 3, default); 1 = customised 3D-assignment sampler
+     * (Alg. 4; R25): variables must be the a3_n^3
+     * triples (i,j,k) at flat index i*a3_n^2 + j*a3_n + k (a3_n <= 32767); every candidate is a
+     * feasible 3D assignment built from the ceil(a3_gamma*a3_n) largest x_k, a random completion
+     * and a3_ls pairwise interchanges (-1: 2*a3_n; SPEC L381 defaults gamma 4, L 2n). */
+    int32_t sampler;
+    int32_t a3_ls;
+    int64_t a3_n;
+    double a3_gamma;
 } gfors_params;
 
 /* halt_reason: 1 criteria met, 2 max_iters, 3 time limit, 4 diverged. */
@@ -141,6 +150,11 @@ gfors_status gfors_load(gfors_ctx *ctx, const gfors_problem *prob);
  * gfors_best_incumbent returns z in the original sense and x lifted to the ORIGINAL n variables.
  * Host only; copies; errors name the offending row/column. */
 gfors_status gfors_tu_reformulate(gfors_ctx *ctx, const int64_t *rows_J, const int32_t *cols_I, int64_t count);
+/* Test hook: one Alg. 4 batch (sampler 1) of n_words*64 candidates from the fixed p (n entries,
+ * host), Philox key seed, round id, lanes 64*word_begin ...; bits as gfors_sample. */
+gfors_status gfors_sample_assign3d(gfors_ctx *ctx, const double *p, uint64_t seed, uint32_t round_id,
+                                   int64_t word_begin, int64_t n_words, int64_t a3_n, double a3_gamma,
+                                   int64_t a3_ls, uint64_t *bits);
 /* Current problem dimensions (reduced after gfors_tu_reformulate) and the original n. */
 gfors_status gfors_dims(gfors_ctx *ctx, int64_t *n, int64_t *m, int64_t *n_orig);
 /* Preprocess on the device (row norms, power iterations).  out may be NULL. */

@@ -575,6 +575,99 @@ void orc_sample_subset(const double *p_sub, const int64_t *idx, int64_t count, u
 }
 
 /* ------------------------------------------------------------------------- */
+/* Customised RandSampleStep for 3D assignment (PAPER Alg. 4)  */
+/* ------------------------------------------------------------------------- */
+typedef struct { double p; int64_t idx; } a3_entry;
+static int a3_cmp(const void *x, const void *y) {
+    const a3_entry *a = (const a3_entry *)x, *b = (const a3_entry *)y;
+    if (a->p > b->p) return -1;          /* descending p */
+    if (a->p < b->p) return 1;
+    return (a->idx < b->idx) ? -1 : (a->idx > b->idx);  /* ties: lower flat index first */
+}
+
+static uint32_t a3_draw(uint32_t lane, uint32_t round_id, uint32_t step, uint32_t tag,
+                        const uint32_t key[2], uint32_t out[4]) {
+    const uint32_t ctr[4] = {lane, round_id, step, tag};
+    orc_philox4x32_10(ctr, key, out);
+    return out[0];
+}
+
+void orc_sample_assign3d(const double *p, int64_t n, const double *cost, uint64_t seed, uint32_t round_id,
+                         int64_t word_begin, int64_t n_words, double gamma, int64_t L, uint64_t *bits) {
+    const int64_t N = n * n * n;
+    const uint32_t key[2] = {(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32)};
+    memset(bits, 0, (size_t)(N * n_words) * sizeof(uint64_t));
+    /* (1) the ceil(gamma*n) largest entries of p */
+    int64_t K = (int64_t)ceil(gamma * (double)n);
+    if (K > N) K = N;
+    a3_entry *e = (a3_entry *)malloc((size_t)N * sizeof(a3_entry));
+    for (int64_t v = 0; v < N; ++v) { e[v].p = p[v]; e[v].idx = v; }
+    qsort(e, (size_t)N, sizeof(a3_entry), a3_cmp);
+    /* (2) greedy partial non-conflict assignment in that order */
+    int64_t *sj0 = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+    int64_t *sk0 = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+    char *uj = (char *)calloc((size_t)n, 1), *uk = (char *)calloc((size_t)n, 1);
+    for (int64_t i = 0; i < n; ++i) sj0[i] = sk0[i] = -1;
+    for (int64_t t = 0; t < K; ++t) {
+        const int64_t v = e[t].idx, i = v / (n * n), j = (v / n) % n, k = v % n;
+        if (sj0[i] < 0 && !uj[j] && !uk[k]) { sj0[i] = j; sk0[i] = k; uj[j] = 1; uk[k] = 1; }
+    }
+    int64_t r = 0;
+    int64_t *Ri = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+    int64_t *Rj = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+    int64_t *Rk = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+    int64_t rj = 0, rk = 0;
+    for (int64_t i = 0; i < n; ++i) if (sj0[i] < 0) Ri[r++] = i;
+    for (int64_t j = 0; j < n; ++j) if (!uj[j]) Rj[rj++] = j;
+    for (int64_t k = 0; k < n; ++k) if (!uk[k]) Rk[rk++] = k;
+    int64_t *pj = (int64_t *)malloc((size_t)n * sizeof(int64_t)), *pk = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+    int64_t *sj = (int64_t *)malloc((size_t)n * sizeof(int64_t)), *sk = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+    for (int64_t w = 0; w < n_words; ++w) {
+        for (int b = 0; b < 64; ++b) {
+            const uint32_t lane = (uint32_t)(64 * (word_begin + w) + b);
+            uint32_t o4[4];
+            /* (3) random completion: Fisher-Yates on the unused j's and k's */
+            for (int64_t t = 0; t < r; ++t) { pj[t] = Rj[t]; pk[t] = Rk[t]; }
+            for (int64_t t = r - 1; t >= 1; --t) {
+                uint64_t u = a3_draw(lane, round_id, (uint32_t)t, 0xA3D00001u, key, o4);
+                int64_t q = (int64_t)((u * (uint64_t)(t + 1)) >> 32);
+                int64_t tmp = pj[t]; pj[t] = pj[q]; pj[q] = tmp;
+                u = a3_draw(lane, round_id, (uint32_t)t, 0xA3D00002u, key, o4);
+                q = (int64_t)((u * (uint64_t)(t + 1)) >> 32);
+                tmp = pk[t]; pk[t] = pk[q]; pk[q] = tmp;
+            }
+            for (int64_t i = 0; i < n; ++i) { sj[i] = sj0[i]; sk[i] = sk0[i]; }
+            for (int64_t t = 0; t < r; ++t) { sj[Ri[t]] = pj[t]; sk[Ri[t]] = pk[t]; }
+            /* (4) L pairwise interchanges (swap a coordinate iff the cost strictly decreases) */
+            for (int64_t st = 0; st < L && n >= 2; ++st) {
+                a3_draw(lane, round_id, (uint32_t)st, 0xA3D00003u, key, o4);
+                const int64_t a = (int64_t)(((uint64_t)o4[0] * (uint64_t)n) >> 32);
+                int64_t bb = (int64_t)(((uint64_t)o4[1] * (uint64_t)(n - 1)) >> 32);
+                if (bb >= a) bb += 1;
+                const double old_c = cost[a * n * n + sj[a] * n + sk[a]] + cost[bb * n * n + sj[bb] * n + sk[bb]];
+                if ((o4[2] & 1u) == 0) {
+                    const double new_c = cost[a * n * n + sj[bb] * n + sk[a]] + cost[bb * n * n + sj[a] * n + sk[bb]];
+                    if (new_c < old_c) { int64_t tmp = sj[a]; sj[a] = sj[bb]; sj[bb] = tmp; }
+                } else {
+                    const double new_c = cost[a * n * n + sj[a] * n + sk[bb]] + cost[bb * n * n + sj[bb] * n + sk[a]];
+                    if (new_c < old_c) { int64_t tmp = sk[a]; sk[a] = sk[bb]; sk[bb] = tmp; }
+                }
+            }
+            for (int64_t i = 0; i < n; ++i) {
+                const int64_t v = i * n * n + sj[i] * n + sk[i];
+                bits[v * n_words + w] |= (uint64_t)1 << b;
+            }
+        }
+    }
+    free(e); free(sj0); free(sk0); free(uj); free(uk); free(Ri); free(Rj); free(Rk);
+    free(pj); free(pk); free(sj); free(sk);
+}
+
+void orc_canonical_c(const orc_ctx *o, double *c) {
+    for (int64_t i = 0; i < o->n; ++i) c[i] = o->c[i];
+}
+
+/* ------------------------------------------------------------------------- */
 /* EvalBest pieces (readings R11, R12) */
 /* ------------------------------------------------------------------------- */
 static void eval_one(const orc_ctx *o, const uint8_t *xh, int *feasible, double *z) {
@@ -684,6 +777,7 @@ void orc_params_default(orc_params *p) {
     p->tol_primal = 1e-6; p->tol_dual = 1e-6; p->tol_binary = 1e-6;
     p->stall_rel = 1e-8; p->stall_window = 50;
     p->max_iters = 100000; p->time_limit_s = 1800.0; p->seed = 20251030ull;
+    p->sampler = 0; p->a3_ls = -1; p->a3_n = 0; p->a3_gamma = 4.0;  /* SPEC L381 */
 }
 
 static double now_s(void) {
@@ -718,6 +812,8 @@ int orc_run(orc_ctx *o, const orc_params *p, orc_run_info *info,
     if (!(p->sigma > 0.0 && p->sigma < 1.0)) return fail(-3, "sigma must be in (0,1)");
     if (p->k_b <= 0 || p->k_b % 64) return fail(-3, "k_b must be a positive multiple of 64");
     if (p->k_int < 1 || p->k_r < 1) return fail(-3, "k_int and k_r must be >= 1");
+    if (p->sampler == 1 && (p->a3_n < 1 || p->a3_n * p->a3_n * p->a3_n != o->n || !(p->a3_gamma > 0.0)))
+        return fail(-3, "sampler 1 (3D assignment): n must equal a3_n^3 and a3_gamma > 0");
     const int64_t n = o->n;
     const double tau1 = sqrt(p->sigma), tau2 = sqrt(p->sigma);  /* reading R3 */
     const int64_t n_words = p->k_b / 64;
@@ -747,7 +843,11 @@ int orc_run(orc_ctx *o, const orc_params *p, orc_run_info *info,
             int improved = 0;
             for (int32_t rr = 0; rr < p->k_r; ++rr) {
                 int64_t round_id = (k / p->k_int - 1) * p->k_r + rr;
-                orc_sample(o->x, n, p->seed, (uint32_t)round_id, 0, n_words, bits);
+                if (p->sampler == 1)
+                    orc_sample_assign3d(o->x, p->a3_n, o->c, p->seed, (uint32_t)round_id, 0, n_words, p->a3_gamma,
+                                        p->a3_ls < 0 ? 2 * p->a3_n : p->a3_ls, bits);
+                else
+                    orc_sample(o->x, n, p->seed, (uint32_t)round_id, 0, n_words, bits);
                 improved |= eval_best(o, bits, n_words, 0, k, round_id, feas, z);
                 rounds++;
             }

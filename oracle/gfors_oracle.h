@@ -87,6 +87,21 @@ void orc_sample(const double *p, int64_t n, uint64_t seed, uint32_t round_id,
 void orc_sample_subset(const double *p_sub, const int64_t *idx, int64_t count, uint64_t seed,
                        uint32_t round_id, int64_t word_begin, int64_t n_words, uint64_t *bits);
 
+/* Customised RandSampleStep for 3D assignment (PAPER Alg. 4; next row
+ * f3; reading R25).  Variables are the n^3 triples (i,j,k) at flat index i*n^2 + j*n + k; p and
+ * cost (canonical, minimisation) have n^3 entries.  (1) the K = ceil(gamma*n) largest p (ties:
+ * lower flat index); (2) greedy partial assignment in that order (accept a triple iff its i, j and
+ * k are all unused); (3) per lane: the unused j's and k's (ascending) are shuffled by Fisher-Yates
+ * (t = r-1..1: s = (u*(t+1)) >> 32, u = Philox out0 of ctr (lane, round, t, 0xA3D00001 / 2)) and
+ * assigned to the unused i's in ascending order; (4) L pairwise interchanges: step s draws
+ * Philox ctr (lane, round, s, 0xA3D00003): a = (o0*n)>>32, b = (o1*(n-1))>>32 (+1 if >= a),
+ * coordinate j if o2 is even else k; the two triples swap that coordinate iff the cost sum
+ * strictly decreases.  Lane = 64*(word_begin + w) + bit.  Every lane is a feasible assignment. */
+void orc_sample_assign3d(const double *p, int64_t n, const double *cost, uint64_t seed, uint32_t round_id,
+                         int64_t word_begin, int64_t n_words, double gamma, int64_t L, uint64_t *bits);
+/* canonical (minimisation) cost vector c (n entries) of a loaded problem */
+void orc_canonical_c(const orc_ctx *o, double *c);
+
 /* Evaluate a bit-sliced batch on the ORIGINAL canonical data (SPEC L147-155,
  * L138-146): feasible[l] in {0,1}, z[l] canonical (minimisation) objective. */
 int orc_eval(const orc_ctx *o, const uint64_t *bits, int64_t n_words,
@@ -115,6 +130,10 @@ typedef struct {
     double rho_min, rho_max, growth_T, growth_p, rho_delta;
     double tol_primal, tol_dual, tol_binary, stall_rel; int32_t stall_window;
     int64_t max_iters; double time_limit_s; uint64_t seed;
+    int32_t sampler;        /* 0: Bernoulli (Alg. 3), 1: 3D assignment (Alg. 4) */
+    int32_t a3_ls;          /* Alg. 4 L (-1: 2*a3_n) */
+    int64_t a3_n;           /* Alg. 4 n (variables = a3_n^3) */
+    double a3_gamma;        /* Alg. 4 gamma (default 4) */
 } orc_params;
 void orc_params_default(orc_params *p);
 typedef struct {

@@ -50,7 +50,8 @@ class OrcParams(C.Structure):
     _fields_ = [("sigma", D), ("k_int", C.c_int32), ("k_r", C.c_int32), ("k_b", I64),
                 ("rho_min", D), ("rho_max", D), ("growth_T", D), ("growth_p", D), ("rho_delta", D),
                 ("tol_primal", D), ("tol_dual", D), ("tol_binary", D), ("stall_rel", D),
-                ("stall_window", C.c_int32), ("max_iters", I64), ("time_limit_s", D), ("seed", C.c_uint64)]
+                ("stall_window", C.c_int32), ("max_iters", I64), ("time_limit_s", D), ("seed", C.c_uint64),
+                ("sampler", C.c_int32), ("a3_ls", C.c_int32), ("a3_n", I64), ("a3_gamma", D)]
 
 
 class OrcRunInfo(C.Structure):
@@ -85,6 +86,8 @@ def _declare(L):
     L.orc_indicators.argtypes = [P, D, D, D, P]
     L.orc_sample.argtypes = [P, I64, C.c_uint64, C.c_uint32, I64, I64, P]
     L.orc_sample_subset.argtypes = [P, P, I64, C.c_uint64, C.c_uint32, I64, I64, P]
+    L.orc_sample_assign3d.argtypes = [P, I64, P, C.c_uint64, C.c_uint32, I64, I64, D, I64, P]
+    L.orc_canonical_c.argtypes = [P, P]
     L.orc_eval.argtypes = [P, P, I64, P, P]
     L.orc_eval_point.argtypes = [P, P, P, P]
     L.orc_halt_init.argtypes = [C.POINTER(OrcHaltState), D, D, D, D, C.c_int]
@@ -124,6 +127,17 @@ def sample(p, seed, round_id, word_begin, n_words):
     p = np.ascontiguousarray(p, dtype=np.float64)
     bits = np.zeros((p.shape[0], n_words), dtype=np.uint64)
     lib().orc_sample(_ptr(p), p.shape[0], seed, round_id, word_begin, n_words, _ptr(bits))
+    return bits
+
+
+def sample_assign3d(p, a3n, cost, seed, round_id, word_begin, n_words, gamma=4.0, L=None):
+    """Alg. 4 customised sampler (3D assignment).  cost: canonical (minimisation) c."""
+    p = np.ascontiguousarray(p, dtype=np.float64)
+    cost = np.ascontiguousarray(cost, dtype=np.float64)
+    assert p.shape[0] == a3n ** 3 == cost.shape[0]
+    bits = np.zeros((p.shape[0], n_words), dtype=np.uint64)
+    lib().orc_sample_assign3d(_ptr(p), a3n, _ptr(cost), seed, round_id, word_begin, n_words, float(gamma),
+                              2 * a3n if L is None else int(L), _ptr(bits))
     return bits
 
 
@@ -238,6 +252,11 @@ class Oracle:
         feas = np.zeros(64 * nw, dtype=np.uint8); z = np.zeros(64 * nw)
         self._chk(lib().orc_eval(self.h, _ptr(bits), nw, _ptr(feas), _ptr(z)))
         return feas, z
+
+    def canonical_c(self):
+        c = np.zeros(self.n)
+        lib().orc_canonical_c(self.h, _ptr(c))
+        return c
 
     def eval_point(self, x):
         x = np.ascontiguousarray(x, dtype=np.uint8)

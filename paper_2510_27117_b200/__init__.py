@@ -62,7 +62,8 @@ class Params(C.Structure):
                 ("rho_min", D), ("rho_max", D), ("growth_T", D), ("growth_p", D), ("rho_delta", D),
                 ("tol_primal", D), ("tol_dual", D), ("tol_binary", D), ("stall_rel", D),
                 ("stall_window", I32), ("max_iters", I64), ("time_limit_s", D), ("seed", U64),
-                ("use_graph", I32), ("trace_cap", I32)]
+                ("use_graph", I32), ("trace_cap", I32),
+                ("sampler", I32), ("a3_ls", I32), ("a3_n", I64), ("a3_gamma", D)]
 
 
 class RunInfo(C.Structure):
@@ -100,6 +101,7 @@ EXPORTS = {
     "gfors_merge_records": (I32, [P, P, P, I32]),
     "gfors_tu_reformulate": (I32, [P, P, P, I64]),
     "gfors_dims": (I32, [P, P, P, P]),
+    "gfors_sample_assign3d": (I32, [P, P, U64, C.c_uint32, I64, I64, I64, D, I64, P]),
     "gfors_nccl_unique_id": (I32, [P]),
     "gfors_graph_note": (C.c_char_p, [P]),
 }
@@ -262,6 +264,13 @@ class Solver:
         p = np.ascontiguousarray(p, dtype=np.float64)
         bits = np.zeros((self.n, n_words), dtype=np.uint64)
         self._chk(_lib.gfors_sample(self.h, _ptr(p), seed, round_id, word_begin, n_words, _ptr(bits)))
+        return bits
+
+    def sample_assign3d(self, p, seed, round_id, word_begin, n_words, a3_n, gamma=4.0, L=None):
+        p = np.ascontiguousarray(p, dtype=np.float64)
+        bits = np.zeros((self.n, n_words), dtype=np.uint64)
+        self._chk(_lib.gfors_sample_assign3d(self.h, _ptr(p), seed, round_id, word_begin, n_words, a3_n,
+                                             float(gamma), -1 if L is None else int(L), _ptr(bits)))
         return bits
 
     def eval(self, bits):

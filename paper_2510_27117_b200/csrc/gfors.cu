@@ -33,6 +33,7 @@
 #include "push_dual.cuh"
 #include "push_primal.cuh"
 #include "dense_q.cuh"
+#include "assign3d.cuh"
 #include <cudaTypedefs.h>
 #include <cstdlib>
 
@@ -358,6 +359,20 @@ struct gfors_ctx {
         std::vector<double> sval;
     } tu;
 
+    // ---- customised 3D-assignment sampler (assign3d.cuh) ----
+    struct A3 {
+        int sampler = 0;        // of the current run / hook call
+        long long n = 0, K = 0, L = 0;
+        unsigned long long* keys[2] = {nullptr, nullptr};
+        int* vals[2] = {nullptr, nullptr};
+        void* tmp = nullptr;
+        size_t tmp_bytes = 0;
+        short *sj0 = nullptr, *sk0 = nullptr, *Ri = nullptr, *Rj = nullptr, *Rk = nullptr;
+        int* meta = nullptr;
+        unsigned char* used = nullptr;
+        long long alloc_n = 0;
+    } a3;
+
     // ---- dense-Q path (dense_q.cuh) ----
     bool qdense = false;           // Q stored as dense int8 Qd[qld][qld]
     long long qld = 0;             // padded dimension (multiple of 128)
@@ -538,6 +553,11 @@ void gfors_ctx::free_prep() {
                    (void**)&d_qx, (void**)&d_qdx, (void**)&d_qxpart, (void**)&d_Xs};
     for (void** p : ps) { dfree(*p); *p = nullptr; }
     X_words = iacc_len = zpart_len = z_len = Xs_lanes = 0;
+    for (int b = 0; b < 2; ++b) { dfree(a3.keys[b]); dfree(a3.vals[b]); }
+    for (void* q : {(void*)a3.tmp, (void*)a3.sj0, (void*)a3.sk0, (void*)a3.Ri, (void*)a3.Rj, (void*)a3.Rk,
+                    (void*)a3.meta, (void*)a3.used})
+        dfree(q);
+    a3 = A3{};
     rho_cap = 0;
     trace_cap = 0;
     if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }
@@ -1070,9 +1090,76 @@ void ensure_batch(gfors_ctx* C, int W) {
     if (64LL * W > C->z_len) { dfree(C->d_z); C->d_z = dalloc<double>(64LL * W); C->z_len = 64LL * W; C->gvalid = false; }
 }
 
+void ensure_a3(gfors_ctx* C, long long a3n);
+
+// select the RandSampleStep of a run / hook (validates Alg. 4's parameters against the problem)
+void set_sampler(gfors_ctx* C, int sampler, long long a3n, double gamma, long long ls) {
+    C->a3.sampler = sampler;
+    if (sampler != 1) return;
+    if (a3n < 1 || a3n > 32767 || a3n * a3n * a3n != C->n)
+        input_error("params.a3_n: sampler 1 needs n = a3_n^3 variables (a3_n = %lld, n = %lld)", a3n, C->n);
+    if (!(gamma > 0.0)) input_error("params.a3_gamma: must be > 0");
+    ensure_a3(C, a3n);
+    C->a3.n = a3n;
+    C->a3.K = std::min<long long>(C->n, (long long)std::ceil(gamma * (double)a3n));
+    C->a3.L = ls < 0 ? 2 * a3n : ls;
+}
+
+// buffers of the Alg. 4 sampler for a3_n (grow-only; the radix-sort temp storage is sized for n^3)
+void ensure_a3(gfors_ctx* C, long long a3n) {
+    auto& A = C->a3;
+    if (a3n <= A.alloc_n) return;
+    const long long N = C->n;
+    for (int b = 0; b < 2; ++b) { dfree(A.keys[b]); dfree(A.vals[b]); A.keys[b] = dalloc<unsigned long long>(N); A.vals[b] = dalloc<int>(N); }
+    dfree(A.tmp); A.tmp = nullptr;
+    size_t bytes = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, A.keys[0], A.keys[1], A.vals[0], A.vals[1], (int)N));
+    A.tmp = dalloc<unsigned char>(bytes);
+    A.tmp_bytes = bytes;
+    for (short** q : {&A.sj0, &A.sk0, &A.Ri, &A.Rj, &A.Rk}) { dfree(*q); *q = dalloc<short>(a3n); }
+    dfree(A.meta); A.meta = dalloc<int>(1);
+    dfree(A.used); A.used = dalloc<unsigned char>(2 * a3n);
+    A.alloc_n = a3n;
+    C->gvalid = false;
+}
+
+// Alg. 4 (assign3d.cuh): sort -> greedy partial assignment -> per-lane completion + interchanges
+template <typename T>
+void enqueue_sample_a3(gfors_ctx* C, cudaStream_t s, const double* pfix, int W, long long word_off, uint64_t seed,
+                       long long kint, int r, int kr, unsigned round_fixed, int use_fixed) {
+    auto& A = C->a3;
+    const long long N = C->n;
+    const uint2 key = make_uint2((unsigned)(seed & 0xffffffffu), (unsigned)(seed >> 32));
+    if (!C->dry) CK(cudaMemsetAsync(C->d_X, 0, N * (long long)W * sizeof(uint64_t), s));
+    LAUNCH(C, s, KC_SAMPLE, (k_a3_keys<T><<<grid_for(N), NT, 0, s>>>((const T*)C->d_x[0], (const T*)C->d_x[1], pfix, N,
+                                                                   C->d_ctrl, kint, use_fixed, A.keys[0], A.vals[0])));
+    if (!C->dry) {
+        size_t bytes = A.tmp_bytes;
+        CK(cub::DeviceRadixSort::SortPairs(A.tmp, bytes, A.keys[0], A.keys[1], A.vals[0], A.vals[1], (int)N, 0, 64, s));
+    }
+    // (the CUB radix-sort kernels are library launches: not counted in gfors_run_info.launches)
+    LAUNCH(C, s, KC_SAMPLE, (k_a3_greedy<<<1, 32, 0, s>>>(A.vals[1], A.K, (int)A.n, A.sj0, A.sk0, A.Ri, A.Rj, A.Rk,
+                                                          A.meta, A.used)));
+    const int lanes = 64 * W;
+    const size_t per = 8 * (size_t)A.n;
+    int tpb = (int)std::min<size_t>(64, std::max<size_t>(1, (200 * 1024) / per));
+    const size_t sm = per * tpb;
+    static size_t attr_sm = 0;
+    if (sm > 48 * 1024 && sm > attr_sm) {
+        CK(cudaFuncSetAttribute(k_a3_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        attr_sm = sm;
+    }
+    LAUNCH(C, s, KC_SAMPLE, (k_a3_sample<<<(lanes + tpb - 1) / tpb, tpb, sm, s>>>((int)A.n, A.sj0, A.sk0, A.Ri, A.Rj, A.Rk,
+        A.meta, C->d_c, key, C->d_ctrl, r, kr, round_fixed, use_fixed, word_off, W, A.L, C->d_X)));
+}
+
 template <typename T>
 void enqueue_sample(gfors_ctx* C, cudaStream_t s, const double* pfix, int W, long long word_off, uint64_t seed,
                     long long kint, int r, int kr, unsigned round_fixed, int use_fixed) {
+    if (C->a3.sampler == 1) {
+        enqueue_sample_a3<T>(C, s, pfix, W, word_off, seed, kint, r, kr, round_fixed, use_fixed);
+        return;
+    }
     const uint2 key = make_uint2((unsigned)(seed & 0xffffffffu), (unsigned)(seed >> 32));
     LAUNCH(C, s, KC_SAMPLE, (k_sample<T><<<grid_for(C->n * (long long)W), NT, 0, s>>>(
                                 (const T*)C->d_x[0], (const T*)C->d_x[1], pfix, C->n, W, word_off, key, C->d_ctrl, kint, r,
@@ -1354,12 +1441,14 @@ static void validate_params(const gfors_params* p) {
     if (!(p->time_limit_s > 0.0)) input_error("params.time_limit_s: must be > 0");
     if (!(p->rho_min >= 0.0) || !(p->rho_max >= p->rho_min)) input_error("params.rho_min/rho_max: need 0 <= rho_min <= rho_max");
     if (p->trace_cap < 0) input_error("params.trace_cap: must be >= 0");
+    if (p->sampler != 0 && p->sampler != 1) input_error("params.sampler: must be 0 (Bernoulli) or 1 (3D assignment)");
 }
 
 static bool same_graph_key(const gfors_params& a, const gfors_params& b) {
     return a.sigma == b.sigma && a.k_int == b.k_int && a.k_r == b.k_r && a.k_b == b.k_b && a.tol_primal == b.tol_primal &&
            a.tol_dual == b.tol_dual && a.tol_binary == b.tol_binary && a.stall_rel == b.stall_rel &&
-           a.stall_window == b.stall_window && a.seed == b.seed && a.trace_cap == b.trace_cap;
+           a.stall_window == b.stall_window && a.seed == b.seed && a.trace_cap == b.trace_cap &&
+           a.sampler == b.sampler && a.a3_n == b.a3_n && a.a3_gamma == b.a3_gamma && a.a3_ls == b.a3_ls;
 }
 
 template <typename T>
@@ -1384,6 +1473,7 @@ static void do_run_t(gfors_ctx* C, const gfors_params* p, gfors_run_info* out) {
     cudaStream_t s = C->stream;
     const int W = (int)(p->k_b / 64);
     ensure_batch(C, W);
+    set_sampler(C, p->sampler, p->a3_n, p->a3_gamma, p->a3_ls);
     const long long max_blocks = p->max_iters / p->k_int;
     const long long tail = p->max_iters % p->k_int;
     // rho table (host pow, like the oracle; reading R7)
@@ -1572,6 +1662,7 @@ void gfors_params_default(gfors_params* p) {
     p->rho_min = 1e-3; p->rho_max = 10.0; p->growth_T = 100.0; p->growth_p = 2.0; p->rho_delta = 1e-6;
     p->tol_primal = 1e-6; p->tol_dual = 1e-6; p->tol_binary = 1e-6; p->stall_rel = 1e-8; p->stall_window = 50;
     p->max_iters = 100000; p->time_limit_s = 1800.0; p->seed = 20251030ull; p->use_graph = 1; p->trace_cap = 4096;
+    p->sampler = 0; p->a3_ls = -1; p->a3_n = 0; p->a3_gamma = 4.0;
 }
 
 void gfors_prep_opts_default(gfors_prep_opts* p) {
@@ -1709,6 +1800,7 @@ gfors_status gfors_sample(gfors_ctx* C, const double* p, uint64_t seed, uint32_t
     for (long long i = 0; i < C->n; ++i)
         if (!(p[i] >= 0.0 && p[i] <= 1.0)) input_error("gfors_sample: p[%lld] not in [0,1]", i);
     ensure_batch(C, (int)n_words);
+    set_sampler(C, 0, 0, 0.0, 0);
     cudaStream_t s = C->stream;
     double* dp = C->d_tmp[3];
     CK(cudaMemcpyAsync(dp, p, C->n * sizeof(double), cudaMemcpyHostToDevice, s));
@@ -1718,6 +1810,28 @@ gfors_status gfors_sample(gfors_ctx* C, const double* p, uint64_t seed, uint32_t
         enqueue_sample<float>(C, s, dp, (int)n_words, word_begin, seed, 1, 0, 1, round_id, 1);
     CK(cudaMemcpyAsync(bits, C->d_X, C->n * n_words * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    API_END(C)
+}
+
+gfors_status gfors_sample_assign3d(gfors_ctx* C, const double* p, uint64_t seed, uint32_t round_id, int64_t word_begin,
+                                   int64_t n_words, int64_t a3_n, double a3_gamma, int64_t a3_ls, uint64_t* bits) {
+    API_BEGIN(C)
+    if (C->stage < 2) throw Err{GFORS_E_STATE, "gfors_sample_assign3d: call gfors_preprocess first"};
+    if (!p || !bits) input_error("gfors_sample_assign3d: p and bits required");
+    if (n_words < 1 || n_words > (1 << 14)) input_error("gfors_sample_assign3d: n_words out of range");
+    if (word_begin < 0 || 64 * (word_begin + n_words) > (1LL << 32)) input_error("gfors_sample_assign3d: lane range exceeds 2^32");
+    ensure_batch(C, (int)n_words);
+    set_sampler(C, 1, a3_n, a3_gamma, a3_ls);
+    cudaStream_t s = C->stream;
+    double* dp = C->d_tmp[3];
+    CK(cudaMemcpyAsync(dp, p, C->n * sizeof(double), cudaMemcpyHostToDevice, s));
+    if (C->precision == 64)
+        enqueue_sample<double>(C, s, dp, (int)n_words, word_begin, seed, 1, 0, 1, round_id, 1);
+    else
+        enqueue_sample<float>(C, s, dp, (int)n_words, word_begin, seed, 1, 0, 1, round_id, 1);
+    CK(cudaMemcpyAsync(bits, C->d_X, C->n * n_words * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    C->a3.sampler = 0;
     API_END(C)
 }
 
