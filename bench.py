@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--f1-steps", type=int, default=50)
     ap.add_argument("--no-f2", action="store_true", help="skip the TU-reformulation facility-location leg (next row f2, config 7)")
     ap.add_argument("--f2-iters", type=int, default=3000)
+    ap.add_argument("--no-f3", action="store_true", help="skip the customised-sampler 3D-assignment leg (next row f3, config 8)")
+    ap.add_argument("--f3-iters", type=int, default=2000)
     return ap.parse_args()
 
 
@@ -376,6 +378,42 @@ def _f2_pair(out, key, inst, iters, prec, args, gf, stream, local):
         s.close()
 
 
+def run_f3_assign3d(args, gf, stream, local):
+    """Next row f3: the customised RandSampleStep of Alg. 4 on 3D
+    assignment n = 64 (config 8; 262,144 binaries, 192 equality rows) against the default Bernoulli
+    sampler, same iteration budget (halting disabled): objective reached, time to incumbent,
+    candidates/s and the sampler's share of the step (CUDA events of an eager replay)."""
+    import torch
+    inst = make_instance(8, args.seed)
+    n3 = int(inst["a3_n"])
+    out = {"workload": "config8", "desc": "3D assignment n=64 (n^3 = 262,144 binaries)", "a3_n": n3,
+           "gamma": 4.0, "L": 2 * n3}
+    for sampler in (1, 0):
+        s = gf.Solver(local, stream=stream.cuda_stream)
+        s.load(inst)
+        s.preprocess(precision=args.precision)
+        kw = dict(k_int=args.k_int, k_b=args.k_b, tol_primal=-1.0, tol_dual=-1.0, tol_binary=-1.0, stall_rel=-1.0,
+                  sampler=sampler, a3_n=n3)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        info = s.run(max_iters=args.f3_iters, **kw)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        z, _, meta = s.best_incumbent(want_x=False)
+        prof = s.profile_blocks(20, **kw)
+        out["custom" if sampler else "default"] = {
+            "iters": info["iters"], "z_best": z if meta["has_incumbent"] else None,
+            "time_to_incumbent_s": meta["found_time_s"] if meta["has_incumbent"] else None,
+            "found_iter": meta["found_iter"], "loop_ms": ms, "candidates_per_s": info["candidates"] / (ms * 1e-3),
+            "pdhg_iters_per_s": info["iters"] / (ms * 1e-3), "sample_ms_per_block": prof.get("sample"),
+            "block_ms_eager": sum(prof.values())}
+        s.close()
+    return out
+
+
 def run_gpu(args):
     import torch
     rank, world, local = dist_env()
@@ -512,6 +550,9 @@ def run_gpu(args):
     f2 = None
     if rank == 0 and world == 1 and not args.no_f2:
         f2 = run_f2_facility(args, gf, stream, local)
+    f3 = None
+    if rank == 0 and world == 1 and not args.no_f3:
+        f3 = run_f3_assign3d(args, gf, stream, local)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -549,7 +590,7 @@ def run_gpu(args):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "time_to_incumbent_small_configs": tti,
-            "next_rows": {"f1_dense_q_maxcut": f1, "f2_tu_facility": f2},
+            "next_rows": {"f1_dense_q_maxcut": f1, "f2_tu_facility": f2, "f3_assign3d_custom_sampler": f3},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

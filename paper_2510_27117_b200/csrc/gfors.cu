@@ -1949,6 +1949,7 @@ int64_t gfors_launches_per_block(gfors_ctx* C, const gfors_params* p) {
     C->dry = true;
     long long n = -1;
     try {
+        set_sampler(C, p->sampler, p->a3_n, p->a3_gamma, p->a3_ls);
         if (C->precision == 64) enqueue_block<double>(C, C->stream, p, W, hp, cudaGraphConditionalHandle{}, 0);
         else enqueue_block<float>(C, C->stream, p, W, hp, cudaGraphConditionalHandle{}, 0);
         n = C->launches;
