@@ -381,6 +381,11 @@ struct gfors_ctx {
     CUtensorMap tmQ64{};           // TMA map of Qd for the GEMV (256-byte x 64-row boxes, no swizzle)
     bool qx_tma = true;            // TMA-pipelined GEMV (GFORS_QX_TMA=0: the register-streaming k_qx_dense)
     bool qx_fix = true;            // fp32 iterates: exact fixed-point dp4a GEMV (GFORS_QX_FIX=0: fp64 FMA)
+    bool qx_sym = false;           // ... reading only the upper-triangle tiles (GFORS_QX_SYM=1; slower)
+    int* d_qs_uoff = nullptr;      // symmetric GEMV: first unit of each 256-column tile (problem-owned)
+    int qs_ntc = 0;
+    long long qs_units = 0;
+    unsigned long long* d_qacc = nullptr;  // [n] int64 fixed-point accumulators (prep-owned, kept zero)
     TcItem* d_tcitems = nullptr;   // objective work items, grouped per CTA
     int* d_tcoff = nullptr;        // [tc_grid + 1]
     int tc_grid = 0;
@@ -532,7 +537,7 @@ void gfors_ctx::free_problem() {
     d_kval = d_ktval = nullptr;
     d_qval = d_c = d_ru = nullptr;
     d_rsign = nullptr;
-    d_qd = nullptr; d_tcitems = nullptr; d_tcoff = nullptr; qdense = false; tc_grid = 0;
+    d_qd = nullptr; d_tcitems = nullptr; d_tcoff = nullptr; qdense = false; tc_grid = 0; d_qs_uoff = nullptr;
     for (auto& c : cnt) c = CountList{};
     d_int_row = nullptr; d_int_rhs = nullptr; d_int_eq = nullptr; d_int_seg_start = nullptr; d_int_seg_slot = nullptr;
     d_real_row = nullptr;
@@ -550,7 +555,7 @@ void gfors_ctx::free_prep() {
                    (void**)&d_red, (void**)&d_scalar, (void**)&d_segpart, (void**)&d_segpart2, (void**)&d_u, (void**)&d_ones, (void**)&d_rec, (void**)&d_regen, (void**)&d_plist[0], (void**)&d_plist[1], (void**)&d_pcount, (void**)&d_pflags, (void**)&d_acc, (void**)&d_rlist, (void**)&d_rcount, (void**)&d_wmax, (void**)&d_accx, (void**)&d_xst, (void**)&d_accv, (void**)&d_ones_cnt, (void**)&d_trig_flag, (void**)&d_part1,
                    (void**)&d_part2, (void**)&d_hist, (void**)&d_rho, (void**)&d_trace, (void**)&d_xbest,
                    (void**)&d_X, (void**)&d_viol, (void**)&d_iacc, &d_zpart, (void**)&d_z, (void**)&d_ctrl,
-                   (void**)&d_qx, (void**)&d_qdx, (void**)&d_qxpart, (void**)&d_Xs};
+                   (void**)&d_qx, (void**)&d_qdx, (void**)&d_qxpart, (void**)&d_Xs, (void**)&d_qacc};
     for (void** p : ps) { dfree(*p); *p = nullptr; }
     X_words = iacc_len = zpart_len = z_len = Xs_lanes = 0;
     for (int b = 0; b < 2; ++b) { dfree(a3.keys[b]); dfree(a3.vals[b]); }
@@ -700,6 +705,22 @@ void enqueue_qx(gfors_ctx* C, cudaStream_t s, QxSrc<TX> src, bool diff, double o
     const long long n = C->n;
     const long long nchunk = (n + QX_CW - 1) / QX_CW;
     if constexpr (sizeof(TX) == 4) {
+        if (C->qx_fix && C->qx_sym) {  // symmetric: upper-triangle tiles used for rows and columns
+            static bool attr_s[2] = {false, false};
+            if (!attr_s[diff ? 1 : 0]) {
+                if (diff) CK(cudaFuncSetAttribute(k_qx_sym<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qt_smem_bytes()));
+                else CK(cudaFuncSetAttribute(k_qx_sym<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qt_smem_bytes()));
+                attr_s[diff ? 1 : 0] = true;
+            }
+            const int grid = (int)std::min<long long>(C->qs_units, NUM_SMS_B200 * 2LL);
+            if (diff)
+                LAUNCH(C, s, KC_QX, (k_qx_sym<true><<<grid, QT_NT, qt_smem_bytes(), s>>>(C->tmQ64, n, C->d_qs_uoff, C->qs_ntc, src, C->d_qacc)));
+            else
+                LAUNCH(C, s, KC_QX, (k_qx_sym<false><<<grid, QT_NT, qt_smem_bytes(), s>>>(C->tmQ64, n, C->d_qs_uoff, C->qs_ntc, src, C->d_qacc)));
+            LAUNCH(C, s, KC_QX, (k_qx_final_acc<<<grid_for(n), 256, 0, s>>>(n, C->d_qacc, diff ? 9.313225746154785e-10 : 4.656612873077393e-10,
+                                                                           omega, out)));
+            return;
+        }
         if (C->qx_fix) {  // fp32 iterates: exact dp4a products on the fixed-point image of x
             const long long units = (n + QT_ROWS - 1) / QT_ROWS * nchunk;
             const int grid = (int)std::min<long long>(units, NUM_SMS_B200 * 2LL);
@@ -1335,6 +1356,8 @@ static void do_preprocess(gfors_ctx* C, const gfors_prep_opts* o, gfors_scaling*
         C->d_qx = dalloc<double>(n);
         C->d_qdx = dalloc<double>(n);
         C->d_qxpart = dalloc<double>((n + QX_CW - 1) / QX_CW * C->qld);
+        C->d_qacc = dalloc<unsigned long long>(n);
+        CK(cudaMemsetAsync(C->d_qacc, 0, n * sizeof(unsigned long long), s));
     }
     unsigned long long* d_zr = dalloc<unsigned long long>(1);
     CK(cudaMemsetAsync(d_zr, 0, sizeof(unsigned long long), s));

@@ -162,3 +162,31 @@ def test_config6_fullsize_sampled(gf):
         assert f and zg[lane] == zz
     z, _, _ = s.best_incumbent(want_x=False)
     assert np.isfinite(z)
+
+
+@pytest.mark.parametrize("n", [300, 1000, 1300])
+def test_symmetric_gemv_bit_identical(gf, n):
+    """fp32 iterates: the symmetric GEMV (upper-triangle tiles used for rows and columns, int64 atomics)
+    and the full GEMV compute the same exact integer sums on the fixed-point x (and the same trigger
+    difference product), so steps and indicators are bit-identical."""
+    inst = G.max_cut(n, 0.5, 3 * n)
+    out = []
+    for sym in ("1", "0"):  # GFORS_QX_SYM=1 forces the symmetric kernel (off by default)
+        old = os.environ.get("GFORS_QX_SYM")
+        os.environ["GFORS_QX_SYM"] = sym
+        try:
+            s, _ = _solver(gf, inst, 32)
+        finally:
+            if old is None:
+                os.environ.pop("GFORS_QX_SYM", None)
+            else:
+                os.environ["GFORS_QX_SYM"] = old
+        rng = np.random.default_rng(n)
+        x = rng.random(n).astype(np.float32).astype(np.float64)
+        x[rng.random(n) < 0.3] = 0.0
+        s.set_state(x, x, np.zeros(0))
+        s.step(3, 0.01, 0.99 ** 0.5, 0.99 ** 0.5)
+        ind = s.indicators(0.01, 0.99 ** 0.5, 0.99 ** 0.5)
+        out.append((s.get_state()[0], ind))
+    assert np.array_equal(out[0][0], out[1][0])
+    assert out[0][1] == out[1][1]
