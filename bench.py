@@ -388,12 +388,14 @@ def run_f3_assign3d(args, gf, stream, local):
     n3 = int(inst["a3_n"])
     out = {"workload": "config8", "desc": "3D assignment n=64 (n^3 = 262,144 binaries)", "a3_n": n3,
            "gamma": 4.0, "L": 2 * n3}
-    for sampler in (1, 0):
+    # custom = Alg. 4 sampler; default = Bernoulli sampler; relax_repair = Bernoulli sampler on the
+    # monotone relaxation + repair (next row f4)
+    for name, sampler, relax in (("custom", 1, 0), ("default", 0, 0), ("relax_repair", 0, 1)):
         s = gf.Solver(local, stream=stream.cuda_stream)
         s.load(inst)
         s.preprocess(precision=args.precision)
         kw = dict(k_int=args.k_int, k_b=args.k_b, tol_primal=-1.0, tol_dual=-1.0, tol_binary=-1.0, stall_rel=-1.0,
-                  sampler=sampler, a3_n=n3)
+                  sampler=sampler, a3_n=n3, relax=relax, repair=relax)
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -404,7 +406,7 @@ def run_f3_assign3d(args, gf, stream, local):
         ms = e0.elapsed_time(e1)
         z, _, meta = s.best_incumbent(want_x=False)
         prof = s.profile_blocks(20, **kw)
-        out["custom" if sampler else "default"] = {
+        out[name] = {
             "iters": info["iters"], "z_best": z if meta["has_incumbent"] else None,
             "time_to_incumbent_s": meta["found_time_s"] if meta["has_incumbent"] else None,
             "found_iter": meta["found_iter"], "loop_ms": ms, "candidates_per_s": info["candidates"] / (ms * 1e-3),

@@ -104,13 +104,20 @@ typedef struct {
     int32_t trace_cap;            /* trace ring-buffer rows (default 4096) */
     /* RandSampleStep: 0 = Bernoulli(x_k) (Alg. 3, default); 1 = customised 3D-assignment sampler
      * (Alg. 4; R25): variables must be the a3_n^3
-     * triples (i,j,k) at flat index i*a3_n^2 + j*a3_n + k (a3_n <= 32767); every candidate is a
+     * triples (i,j,k) at flat index i*a3_n^2 + j*a3_n + k (a3_n <= 4096); every candidate is a
      * feasible 3D assignment built from the ceil(a3_gamma*a3_n) largest x_k, a random completion
      * and a3_ls pairwise interchanges (-1: 2*a3_n; SPEC L381 defaults gamma 4, L 2n). */
     int32_t sampler;
     int32_t a3_ls;
     int64_t a3_n;
     double a3_gamma;
+    /* Monotone relaxation (R26): relax = 1 needs Q = 0,
+     * canonical c >= 0 and K_u >= 0; the PDHG step and indicators then treat every row as >= (upper
+     * closure) while EvalBest keeps the original equalities.  repair = 1 (needs relax, integral
+     * data, m <= 16384, world == 1) drops each lane's 1-entries in decreasing-cost order while all
+     * rows stay >= before EvalBest (lanes with > 8192 entries are left as they are). */
+    int32_t relax;
+    int32_t repair;
 } gfors_params;
 
 /* halt_reason: 1 criteria met, 2 max_iters, 3 time limit, 4 diverged. */
@@ -155,6 +162,10 @@ gfors_status gfors_tu_reformulate(gfors_ctx *ctx, const int64_t *rows_J, const i
 gfors_status gfors_sample_assign3d(gfors_ctx *ctx, const double *p, uint64_t seed, uint32_t round_id,
                                    int64_t word_begin, int64_t n_words, int64_t a3_n, double a3_gamma,
                                    int64_t a3_ls, uint64_t *bits);
+/* Test hooks of f4: the relaxation for gfors_step / gfors_indicators (0/1), and the repair of a
+ * host batch in place (bits as gfors_sample, n_words words per variable; needs relax = 1). */
+gfors_status gfors_set_relax(gfors_ctx *ctx, int32_t relax);
+gfors_status gfors_repair(gfors_ctx *ctx, uint64_t *bits, int64_t n_words);
 /* Current problem dimensions (reduced after gfors_tu_reformulate) and the original n. */
 gfors_status gfors_dims(gfors_ctx *ctx, int64_t *n, int64_t *m, int64_t *n_orig);
 /* Preprocess on the device (row norms, power iterations).  out may be NULL. */

@@ -52,6 +52,8 @@ static int is_integer_value(double v) {
 
 struct orc_ctx {
     int64_t n, m, m1, m2;
+    int64_t m1p;            /* rows [0,m1p) are inequalities for the PDHG step: m1, or m under the
+                               monotone relaxation (reading R26) */
     int maximize, integral;
     /* canonical user form: rows [0,m1) are  Ku x >= ru,  rows [m1,m) are  Ku x = ru */
     csr_t Ku;
@@ -220,6 +222,7 @@ int orc_create(orc_ctx **out, int64_t n, int64_t m,
         if (pass == 0) o->m1 = cj;
     }
     o->m2 = m - o->m1;
+    o->m1p = o->m1;
 
     /* Integral data => exact integer evaluation (reading R12, A23). */
     int integral = is_integer_value(o->c0);
@@ -458,9 +461,21 @@ int orc_get_state(const orc_ctx *o, double *x, double *xbar, double *y) {
     return 0;
 }
 
+int orc_set_relax(orc_ctx *o, int relax) {
+    if (relax) {
+        for (int64_t i = 0; i < o->n; ++i)
+            if (o->c[i] < 0.0) return fail(-3, "monotone relaxation: needs c >= 0 (canonical)");
+        if (o->Q.nnz) return fail(-3, "monotone relaxation: needs Q = 0");
+        for (int64_t p = 0; p < o->Ku.nnz; ++p)
+            if (o->Ku.val[p] < 0.0) return fail(-3, "monotone relaxation: needs K_u >= 0");
+    }
+    o->m1p = relax ? o->m : o->m1;
+    return 0;
+}
+
 int orc_step(orc_ctx *o, double rho, double tau1, double tau2) {
     if (!o->have_state) return fail(-7, "state not initialised");
-    const int64_t n = o->n, m = o->m, m1 = o->m1;
+    const int64_t n = o->n, m = o->m, m1 = o->m1p;
     /* keep x_{k-1}, xbar_{k-1}, y_{k-1} for the Thm. 2 residuals */
     for (int64_t i = 0; i < n; ++i) { o->x_prev[i] = o->x[i]; o->xbar_prev[i] = o->xbar[i]; }
     for (int64_t j = 0; j < m; ++j) o->y_prev[j] = o->y[j];
@@ -502,7 +517,7 @@ int orc_step(orc_ctx *o, double rho, double tau1, double tau2) {
  *       = (y_{k-1}-y_k)/tau2 - K(x_k - xbar_{k-1})                       by eq:dy (L428) */
 int orc_indicators(const orc_ctx *o, double rho, double tau1, double tau2, double *out) {
     if (!o->have_prev) return fail(-7, "no step taken");
-    const int64_t n = o->n, m = o->m, m1 = o->m1;
+    const int64_t n = o->n, m = o->m, m1 = o->m1p;
     double pg_ineq = 0.0, pg_eq = 0.0, sy2 = 0.0;
     for (int64_t j = 0; j < m; ++j) {
         double kx = 0.0, kd = 0.0;
@@ -663,6 +678,57 @@ void orc_sample_assign3d(const double *p, int64_t n, const double *cost, uint64_
     free(pj); free(pk); free(sj); free(sk);
 }
 
+/* Repair after the monotone relaxation (reading R26): per lane, the lane's 1-entries in
+ * order of decreasing canonical cost (ties: lower index first) are dropped one by one while every row
+ * keeps sum_i K_ji x_i >= r_j (all rows read as >=).  Requires the relaxation (m1p == m). */
+typedef struct { double c; int64_t i; } rp_entry;
+static int rp_cmp(const void *x, const void *y) {
+    const rp_entry *a = (const rp_entry *)x, *b = (const rp_entry *)y;
+    if (a->c > b->c) return -1;
+    if (a->c < b->c) return 1;
+    return (a->i < b->i) ? -1 : (a->i > b->i);
+}
+
+int orc_repair(const orc_ctx *o, uint64_t *bits, int64_t n_words) {
+    if (o->m1p != o->m) return fail(-3, "repair needs the monotone relaxation");
+    const int64_t n = o->n, m = o->m;
+    /* column lists of K_u (plain transpose by scanning the rows in order) */
+    int64_t *cptr = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
+    for (int64_t p = 0; p < o->Ku.nnz; ++p) cptr[o->Ku.idx[p] + 1]++;
+    for (int64_t i = 0; i < n; ++i) cptr[i + 1] += cptr[i];
+    int64_t *crow = (int64_t *)malloc((size_t)(o->Ku.nnz ? o->Ku.nnz : 1) * sizeof(int64_t));
+    double *cval = (double *)malloc((size_t)(o->Ku.nnz ? o->Ku.nnz : 1) * sizeof(double));
+    int64_t *fill = (int64_t *)calloc((size_t)n, sizeof(int64_t));
+    for (int64_t j = 0; j < m; ++j)
+        for (int64_t p = o->Ku.ptr[j]; p < o->Ku.ptr[j + 1]; ++p) {
+            const int64_t i = o->Ku.idx[p];
+            crow[cptr[i] + fill[i]] = j; cval[cptr[i] + fill[i]] = o->Ku.val[p]; fill[i]++;
+        }
+    rp_entry *ones = (rp_entry *)malloc((size_t)n * sizeof(rp_entry));
+    double *srow = (double *)malloc((size_t)(m ? m : 1) * sizeof(double));
+    for (int64_t l = 0; l < 64 * n_words; ++l) {
+        const int64_t w = l / 64;
+        const uint64_t bit = (uint64_t)1 << (l % 64);
+        int64_t cnt = 0;
+        for (int64_t i = 0; i < n; ++i)
+            if (bits[i * n_words + w] & bit) { ones[cnt].c = o->c[i]; ones[cnt].i = i; cnt++; }
+        qsort(ones, (size_t)cnt, sizeof(rp_entry), rp_cmp);
+        for (int64_t j = 0; j < m; ++j) srow[j] = 0.0;
+        for (int64_t t = 0; t < cnt; ++t)
+            for (int64_t q = cptr[ones[t].i]; q < cptr[ones[t].i + 1]; ++q) srow[crow[q]] += cval[q];
+        for (int64_t t = 0; t < cnt; ++t) {
+            const int64_t i = ones[t].i;
+            int ok = 1;
+            for (int64_t q = cptr[i]; q < cptr[i + 1] && ok; ++q) ok = (srow[crow[q]] - cval[q] >= o->ru[crow[q]]);
+            if (!ok) continue;
+            for (int64_t q = cptr[i]; q < cptr[i + 1]; ++q) srow[crow[q]] -= cval[q];
+            bits[i * n_words + w] &= ~bit;
+        }
+    }
+    free(cptr); free(crow); free(cval); free(fill); free(ones); free(srow);
+    return 0;
+}
+
 void orc_canonical_c(const orc_ctx *o, double *c) {
     for (int64_t i = 0; i < o->n; ++i) c[i] = o->c[i];
 }
@@ -778,6 +844,7 @@ void orc_params_default(orc_params *p) {
     p->stall_rel = 1e-8; p->stall_window = 50;
     p->max_iters = 100000; p->time_limit_s = 1800.0; p->seed = 20251030ull;
     p->sampler = 0; p->a3_ls = -1; p->a3_n = 0; p->a3_gamma = 4.0;  /* SPEC L381 */
+    p->relax = 0; p->repair = 0;
 }
 
 static double now_s(void) {
@@ -814,6 +881,11 @@ int orc_run(orc_ctx *o, const orc_params *p, orc_run_info *info,
     if (p->k_int < 1 || p->k_r < 1) return fail(-3, "k_int and k_r must be >= 1");
     if (p->sampler == 1 && (p->a3_n < 1 || p->a3_n * p->a3_n * p->a3_n != o->n || !(p->a3_gamma > 0.0)))
         return fail(-3, "sampler 1 (3D assignment): n must equal a3_n^3 and a3_gamma > 0");
+    if (p->repair && !p->relax) return fail(-3, "repair needs relax = 1");
+    {
+        int rc0 = orc_set_relax(o, p->relax);
+        if (rc0) return rc0;
+    }
     const int64_t n = o->n;
     const double tau1 = sqrt(p->sigma), tau2 = sqrt(p->sigma);  /* reading R3 */
     const int64_t n_words = p->k_b / 64;
@@ -848,6 +920,7 @@ int orc_run(orc_ctx *o, const orc_params *p, orc_run_info *info,
                                         p->a3_ls < 0 ? 2 * p->a3_n : p->a3_ls, bits);
                 else
                     orc_sample(o->x, n, p->seed, (uint32_t)round_id, 0, n_words, bits);
+                if (p->repair) orc_repair(o, bits, n_words);
                 improved |= eval_best(o, bits, n_words, 0, k, round_id, feas, z);
                 rounds++;
             }

@@ -99,6 +99,13 @@ void orc_sample_subset(const double *p_sub, const int64_t *idx, int64_t count, u
  * strictly decreases.  Lane = 64*(word_begin + w) + bit.  Every lane is a feasible assignment. */
 void orc_sample_assign3d(const double *p, int64_t n, const double *cost, uint64_t seed, uint32_t round_id,
                          int64_t word_begin, int64_t n_words, double gamma, int64_t L, uint64_t *bits);
+/* Monotone relaxation (reading R26): with Q = 0, c >= 0 and K_u >= 0 (canonical),
+ * the PDHG step and indicators treat every row as >= (upper closure); EvalBest keeps the original
+ * equalities.  relax = 0 restores the original senses. */
+int orc_set_relax(orc_ctx *o, int relax);
+/* Repair (reading R26): per lane, drop 1-entries in order of decreasing cost (ties: lower index
+ * first) while every row keeps sum K_ji x_i >= r_j; needs the relaxation. */
+int orc_repair(const orc_ctx *o, uint64_t *bits, int64_t n_words);
 /* canonical (minimisation) cost vector c (n entries) of a loaded problem */
 void orc_canonical_c(const orc_ctx *o, double *c);
 
@@ -134,6 +141,8 @@ typedef struct {
     int32_t a3_ls;          /* Alg. 4 L (-1: 2*a3_n) */
     int64_t a3_n;           /* Alg. 4 n (variables = a3_n^3) */
     double a3_gamma;        /* Alg. 4 gamma (default 4) */
+    int32_t relax;          /* monotone relaxation: equality rows act as >= in PDHG */
+    int32_t repair;         /* per-lane greedy repair before EvalBest (needs relax) */
 } orc_params;
 void orc_params_default(orc_params *p);
 typedef struct {

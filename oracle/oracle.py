@@ -51,7 +51,8 @@ class OrcParams(C.Structure):
                 ("rho_min", D), ("rho_max", D), ("growth_T", D), ("growth_p", D), ("rho_delta", D),
                 ("tol_primal", D), ("tol_dual", D), ("tol_binary", D), ("stall_rel", D),
                 ("stall_window", C.c_int32), ("max_iters", I64), ("time_limit_s", D), ("seed", C.c_uint64),
-                ("sampler", C.c_int32), ("a3_ls", C.c_int32), ("a3_n", I64), ("a3_gamma", D)]
+                ("sampler", C.c_int32), ("a3_ls", C.c_int32), ("a3_n", I64), ("a3_gamma", D),
+                ("relax", C.c_int32), ("repair", C.c_int32)]
 
 
 class OrcRunInfo(C.Structure):
@@ -88,6 +89,8 @@ def _declare(L):
     L.orc_sample_subset.argtypes = [P, P, I64, C.c_uint64, C.c_uint32, I64, I64, P]
     L.orc_sample_assign3d.argtypes = [P, I64, P, C.c_uint64, C.c_uint32, I64, I64, D, I64, P]
     L.orc_canonical_c.argtypes = [P, P]
+    L.orc_set_relax.argtypes = [P, C.c_int]
+    L.orc_repair.argtypes = [P, P, I64]
     L.orc_eval.argtypes = [P, P, I64, P, P]
     L.orc_eval_point.argtypes = [P, P, P, P]
     L.orc_halt_init.argtypes = [C.POINTER(OrcHaltState), D, D, D, D, C.c_int]
@@ -252,6 +255,14 @@ class Oracle:
         feas = np.zeros(64 * nw, dtype=np.uint8); z = np.zeros(64 * nw)
         self._chk(lib().orc_eval(self.h, _ptr(bits), nw, _ptr(feas), _ptr(z)))
         return feas, z
+
+    def set_relax(self, relax):
+        self._chk(lib().orc_set_relax(self.h, int(relax)))
+
+    def repair(self, bits):
+        bits = np.array(bits, dtype=np.uint64, copy=True)
+        self._chk(lib().orc_repair(self.h, _ptr(bits), bits.shape[1]))
+        return bits
 
     def canonical_c(self):
         c = np.zeros(self.n)

@@ -63,7 +63,8 @@ class Params(C.Structure):
                 ("tol_primal", D), ("tol_dual", D), ("tol_binary", D), ("stall_rel", D),
                 ("stall_window", I32), ("max_iters", I64), ("time_limit_s", D), ("seed", U64),
                 ("use_graph", I32), ("trace_cap", I32),
-                ("sampler", I32), ("a3_ls", I32), ("a3_n", I64), ("a3_gamma", D)]
+                ("sampler", I32), ("a3_ls", I32), ("a3_n", I64), ("a3_gamma", D),
+                ("relax", I32), ("repair", I32)]
 
 
 class RunInfo(C.Structure):
@@ -102,6 +103,8 @@ EXPORTS = {
     "gfors_tu_reformulate": (I32, [P, P, P, I64]),
     "gfors_dims": (I32, [P, P, P, P]),
     "gfors_sample_assign3d": (I32, [P, P, U64, C.c_uint32, I64, I64, I64, D, I64, P]),
+    "gfors_set_relax": (I32, [P, I32]),
+    "gfors_repair": (I32, [P, P, I64]),
     "gfors_nccl_unique_id": (I32, [P]),
     "gfors_graph_note": (C.c_char_p, [P]),
 }
@@ -271,6 +274,14 @@ class Solver:
         bits = np.zeros((self.n, n_words), dtype=np.uint64)
         self._chk(_lib.gfors_sample_assign3d(self.h, _ptr(p), seed, round_id, word_begin, n_words, a3_n,
                                              float(gamma), -1 if L is None else int(L), _ptr(bits)))
+        return bits
+
+    def set_relax(self, relax):
+        self._chk(_lib.gfors_set_relax(self.h, int(relax)))
+
+    def repair(self, bits):
+        bits = np.array(bits, dtype=np.uint64, copy=True)
+        self._chk(_lib.gfors_repair(self.h, _ptr(bits), bits.shape[1]))
         return bits
 
     def eval(self, bits):

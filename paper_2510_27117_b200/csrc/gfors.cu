@@ -34,6 +34,7 @@
 #include "push_primal.cuh"
 #include "dense_q.cuh"
 #include "assign3d.cuh"
+#include "repair.cuh"
 #include <cudaTypedefs.h>
 #include <cstdlib>
 
@@ -337,6 +338,8 @@ struct gfors_ctx {
 
     // ---- canonical problem (host) ----
     long long n = 0, m = 0, m1 = 0, m2 = 0, nnz = 0, qnnz = 0;
+    long long m1p = 0;      // rows [0,m1p) are inequalities for the PDHG step (m under the relaxation, R26)
+    bool repair = false;    // repair lanes before EvalBest (repair.cuh)
     bool maximize = false, integral = false, hasq = false;
     double c0 = 0.0;
     std::vector<int64_t> kptr, ktptr, qptr;
@@ -800,13 +803,13 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
             auto gather = [&](cudaStream_t q) {
                 KIND_SWITCH(C->kkind, LAUNCH(C, q, KC_DUAL,
                     (k_dual_rb<T, KINDV><<<grid, RB_NT, 0, q>>>(csr_K(C), C->pd.blk_row, C->pd.nblk, st, g, rh, C->d_rsign,
-                                                                C->m1, ctrl, kint, j, u_out, pl))));
+                                                                C->m1p, ctrl, kint, j, u_out, pl))));
             };
             if (C->push_dual) {
                 // sparse xbar: scatter the listed columns into the row accumulators, then the rows
                 auto push = [&](cudaStream_t q) {
                     LAUNCH(C, q, KC_DUAL_PUSH, (k_push_scatter<T><<<grid_for(C->n), NT, 0, q>>>(csr_Kt(C), pl, st, ctrl, kint, j)));
-                    LAUNCH(C, q, KC_DUAL_PUSH, (k_push_rows<T><<<grid_for(C->m), NT, 0, q>>>(C->m, pl, st, g, rh, C->d_rsign, C->m1,
+                    LAUNCH(C, q, KC_DUAL_PUSH, (k_push_rows<T><<<grid_for(C->m), NT, 0, q>>>(C->m, pl, st, g, rh, C->d_rsign, C->m1p,
                                                                                       ctrl, kint, j, u_out)));
                 };
                 branch(C, s, [&](cudaStream_t q, cudaGraphConditionalHandle h, int a, int b) {
@@ -819,7 +822,7 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
         } else if (!C->pd.seg) {
             const int grid = grid_for(C->m * (long long)C->pd.sub);
             KIND_SWITCH(C->kkind, SUB_SWITCH(C->pd.sub, LAUNCH(C, s, KC_DUAL,
-                (k_dual<T, KINDV, SUBV><<<grid, NT, 0, s>>>(csr_K(C), st, g, rh, C->d_rsign, C->m1, ctrl, kint, j)))));
+                (k_dual<T, KINDV, SUBV><<<grid, NT, 0, s>>>(csr_K(C), st, g, rh, C->d_rsign, C->m1p, ctrl, kint, j)))));
         } else {
             const int grid = grid_for(C->pd.ds.nseg * 32);
             const int grid2 = grid_for(C->m);
@@ -827,7 +830,7 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
                 (k_seg_partial<T, KINDV><<<grid, NT, 0, s>>>(csr_K(C), C->pd.ds.plan(), st.xb[0], st.xb[1], nullptr,
                                                              nullptr, 1, ctrl, kint, j, C->d_segpart));
                 (k_dual_seg_final<T, KINDV><<<grid2, NT, 0, s>>>(C->m, C->pd.ds.plan(), C->d_segpart, st, g, rh,
-                                                                 C->d_rsign, C->m1, ctrl, kint, j))));
+                                                                 C->d_rsign, C->m1p, ctrl, kint, j))));
         }
     }
     if (C->qdense)  // 2 Q~ x term of the primal gradient by the dense GEMV
@@ -928,7 +931,7 @@ void enqueue_trigger(gfors_ctx* C, cudaStream_t s, long long kint, long long j) 
             auto gather = [&](cudaStream_t q) {
                 KIND_SWITCH(C->kkind, LAUNCH(C, q, KC_TRIGR,
                     (k_trig_rows_rb<T, KINDV><<<grid, RB_NT, 0, q>>>(csr_K(C), C->pd.blk_row, C->pd.nblk, st, g, rh,
-                                                                     C->d_rsign, C->m1, C->d_u, ctrl, kint, j, C->d_part1,
+                                                                     C->d_rsign, C->m1p, C->d_u, ctrl, kint, j, C->d_part1,
                                                                      C->d_ones, C->push_primal ? C->d_trig_flag : nullptr))));
                 if (grid < C->nb1)
                     LAUNCH(C, q, KC_TRIGR, (k_fill<<<1, NT, 0, q>>>(C->d_part1 + 3LL * grid, 3LL * (C->nb1 - grid), 0.0)));
@@ -936,7 +939,7 @@ void enqueue_trigger(gfors_ctx* C, cudaStream_t s, long long kint, long long j) 
             if (C->push_primal) {
                 // x_k pushed by the trigger iteration's primal: gather-free pass over the rows (writes all nb1 partials)
                 auto pushed = [&](cudaStream_t q) {
-                    LAUNCH(C, q, KC_TRIGR, (k_trig_rows_push<T><<<C->nb1, NT, 0, q>>>(C->m, st, g, rh, C->d_rsign, C->m1, C->d_u,
+                    LAUNCH(C, q, KC_TRIGR, (k_trig_rows_push<T><<<C->nb1, NT, 0, q>>>(C->m, st, g, rh, C->d_rsign, C->m1p, C->d_u,
                         ctrl, kint, j, C->d_part1, C->d_ones, C->d_accv, C->d_ones_cnt, C->d_trig_flag)));
                 };
                 branch(C, s, [&](cudaStream_t q, cudaGraphConditionalHandle h, int a, int b) {
@@ -950,7 +953,7 @@ void enqueue_trigger(gfors_ctx* C, cudaStream_t s, long long kint, long long j) 
         } else if (!C->pd.seg) {
             KIND_SWITCH(C->kkind, SUB_SWITCH(C->pd.sub, LAUNCH(C, s, KC_TRIGR,
                 (k_trig_rows<T, KINDV, SUBV, false><<<C->nb1, NT, 0, s>>>(csr_K(C), C->pd.ds.plan(), nullptr, nullptr,
-                    st, g, rh, C->d_rsign, C->m1, ctrl, kint, j, C->d_part1)))));
+                    st, g, rh, C->d_rsign, C->m1p, ctrl, kint, j, C->d_part1)))));
         } else {
             const int grid = grid_for(C->pd.ds.nseg * 32);
             KIND_SWITCH(C->kkind, LAUNCH(C, s, KC_TRIGR,
@@ -959,7 +962,7 @@ void enqueue_trigger(gfors_ctx* C, cudaStream_t s, long long kint, long long j) 
                 (k_seg_partial<T, KINDV><<<grid, NT, 0, s>>>(csr_K(C), C->pd.ds.plan(), st.x[0], st.x[1], st.xb[0],
                                                              st.xb[1], 2, ctrl, kint, j, C->d_segpart2));
                 (k_trig_rows<T, KINDV, 32, true><<<C->nb1, NT, 0, s>>>(csr_K(C), C->pd.ds.plan(), C->d_segpart,
-                    C->d_segpart2, st, g, rh, C->d_rsign, C->m1, ctrl, kint, j, C->d_part1))));
+                    C->d_segpart2, st, g, rh, C->d_rsign, C->m1p, ctrl, kint, j, C->d_part1))));
         }
     } else {
         LAUNCH(C, s, KC_TRIGR, (k_fill<<<1, NT, 0, s>>>(C->d_part1, 3LL * C->nb1, 0.0)));
@@ -1113,11 +1116,43 @@ void ensure_batch(gfors_ctx* C, int W) {
 
 void ensure_a3(gfors_ctx* C, long long a3n);
 
+// monotone relaxation (R26): every row acts as >= in the PDHG step / indicators; EvalBest unchanged
+void set_relax(gfors_ctx* C, int relax, int repair) {
+    if (repair && !relax) input_error("params.repair: needs relax = 1");
+    if (relax) {
+        if (C->hasq) input_error("params.relax: the monotone relaxation needs Q = 0");
+        for (long long i = 0; i < C->n; ++i)
+            if (C->c[i] < 0.0) input_error("params.relax: needs c >= 0 (canonical; c[%lld] < 0)", i);
+        for (double v : C->kval)
+            if (v < 0.0) input_error("params.relax: needs K_u >= 0 (canonical)");
+    }
+    if (repair) {
+        if (!C->integral) input_error("params.repair: needs integral data");
+        if (C->m > 16384) input_error("params.repair: needs m <= 16384 (per-lane row sums in shared memory)");
+        if (C->sharded) input_error("params.repair: not with the NCCL-sharded loop (winner regeneration)");
+    }
+    if (C->m1p != (relax ? C->m : C->m1)) C->gvalid = false;
+    C->m1p = relax ? C->m : C->m1;
+    C->repair = repair != 0;
+}
+
+void enqueue_repair(gfors_ctx* C, cudaStream_t s, int W) {
+    const size_t sm = rp_smem_bytes(C->m);
+    KIND_SWITCH(C->kkind, {
+        static bool attr = false;
+        if (!attr) {
+            CK(cudaFuncSetAttribute(k_repair<KINDV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rp_smem_bytes(16384)));
+            attr = true;
+        }
+        LAUNCH(C, s, KC_SAMPLE, (k_repair<KINDV><<<64 * W, RP_NT, sm, s>>>(C->n, C->m, csr_Kt(C), C->d_c, C->d_ru, C->d_X, W)));
+    });
+}
+
 // select the RandSampleStep of a run / hook (validates Alg. 4's parameters against the problem)
 void set_sampler(gfors_ctx* C, int sampler, long long a3n, double gamma, long long ls) {
     C->a3.sampler = sampler;
     if (sampler != 1) return;
-    if (a3n < 1 || a3n > 32767 || a3n * a3n * a3n != C->n)
+    if (a3n < 1 || a3n > 4096 || a3n * a3n * a3n != C->n)
         input_error("params.a3_n: sampler 1 needs n = a3_n^3 variables (a3_n = %lld, n = %lld)", a3n, C->n);
     if (!(gamma > 0.0)) input_error("params.a3_gamma: must be > 0");
     ensure_a3(C, a3n);
@@ -1139,7 +1174,7 @@ void ensure_a3(gfors_ctx* C, long long a3n) {
     A.tmp_bytes = bytes;
     for (short** q : {&A.sj0, &A.sk0, &A.Ri, &A.Rj, &A.Rk}) { dfree(*q); *q = dalloc<short>(a3n); }
     dfree(A.meta); A.meta = dalloc<int>(1);
-    dfree(A.used); A.used = dalloc<unsigned char>(2 * a3n);
+    dfree(A.used); A.used = dalloc<unsigned char>(2 * a3n);  // (unused since the shared-memory greedy)
     A.alloc_n = a3n;
     C->gvalid = false;
 }
@@ -1159,19 +1194,25 @@ void enqueue_sample_a3(gfors_ctx* C, cudaStream_t s, const double* pfix, int W, 
         CK(cub::DeviceRadixSort::SortPairs(A.tmp, bytes, A.keys[0], A.keys[1], A.vals[0], A.vals[1], (int)N, 0, 64, s));
     }
     // (the CUB radix-sort kernels are library launches: not counted in gfors_run_info.launches)
-    LAUNCH(C, s, KC_SAMPLE, (k_a3_greedy<<<1, 32, 0, s>>>(A.vals[1], A.K, (int)A.n, A.sj0, A.sk0, A.Ri, A.Rj, A.Rk,
-                                                          A.meta, A.used)));
+    const size_t gsm = a3_greedy_smem((int)A.n);
+    static size_t gattr = 0;
+    if (gsm > 48 * 1024 && gsm > gattr) {
+        CK(cudaFuncSetAttribute(k_a3_greedy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm));
+        gattr = gsm;
+    }
+    LAUNCH(C, s, KC_SAMPLE, (k_a3_greedy<<<1, A3_GNT, gsm, s>>>(A.vals[1], A.K, (int)A.n, A.sj0, A.sk0, A.Ri, A.Rj, A.Rk,
+                                                                  A.meta)));
     const int lanes = 64 * W;
-    const size_t per = 8 * (size_t)A.n;
-    int tpb = (int)std::min<size_t>(64, std::max<size_t>(1, (200 * 1024) / per));
-    const size_t sm = per * tpb;
+    const size_t per = a3_warp_smem(A.n, A.L);
+    const int wpb = (int)std::max<size_t>(1, std::min<size_t>(8, (200 * 1024) / per));
+    const size_t sm = per * wpb;
     static size_t attr_sm = 0;
     if (sm > 48 * 1024 && sm > attr_sm) {
         CK(cudaFuncSetAttribute(k_a3_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         attr_sm = sm;
     }
-    LAUNCH(C, s, KC_SAMPLE, (k_a3_sample<<<(lanes + tpb - 1) / tpb, tpb, sm, s>>>((int)A.n, A.sj0, A.sk0, A.Ri, A.Rj, A.Rk,
-        A.meta, C->d_c, key, C->d_ctrl, r, kr, round_fixed, use_fixed, word_off, W, A.L, C->d_X)));
+    LAUNCH(C, s, KC_SAMPLE, (k_a3_sample<<<(lanes + wpb - 1) / wpb, 32 * wpb, sm, s>>>((int)A.n, A.sj0, A.sk0, A.Ri, A.Rj,
+        A.Rk, A.meta, C->d_c, key, C->d_ctrl, r, kr, round_fixed, use_fixed, word_off, W, A.L, C->d_X)));
 }
 
 template <typename T>
@@ -1198,6 +1239,7 @@ void enqueue_block(gfors_ctx* C, cudaStream_t s, const gfors_params* p, int W, H
     for (int r = 0; r < p->k_r; ++r) {
         enqueue_reset(C, s, W, ~0ull);
         enqueue_sample<T>(C, s, nullptr, W, word_off, p->seed, kint, r, p->k_r, 0u, 0);
+        if (C->repair) enqueue_repair(C, s, W);
         // the trigger pass of this block counted the p = 1 entries of every row (rb path)
         enqueue_eval(C, s, W, (C->m > 0 && C->pd.rb) ? C->d_ones : nullptr);
         if (C->sharded) {
@@ -1471,7 +1513,8 @@ static bool same_graph_key(const gfors_params& a, const gfors_params& b) {
     return a.sigma == b.sigma && a.k_int == b.k_int && a.k_r == b.k_r && a.k_b == b.k_b && a.tol_primal == b.tol_primal &&
            a.tol_dual == b.tol_dual && a.tol_binary == b.tol_binary && a.stall_rel == b.stall_rel &&
            a.stall_window == b.stall_window && a.seed == b.seed && a.trace_cap == b.trace_cap &&
-           a.sampler == b.sampler && a.a3_n == b.a3_n && a.a3_gamma == b.a3_gamma && a.a3_ls == b.a3_ls;
+           a.sampler == b.sampler && a.a3_n == b.a3_n && a.a3_gamma == b.a3_gamma && a.a3_ls == b.a3_ls &&
+           a.relax == b.relax && a.repair == b.repair;
 }
 
 template <typename T>
@@ -1497,6 +1540,7 @@ static void do_run_t(gfors_ctx* C, const gfors_params* p, gfors_run_info* out) {
     const int W = (int)(p->k_b / 64);
     ensure_batch(C, W);
     set_sampler(C, p->sampler, p->a3_n, p->a3_gamma, p->a3_ls);
+    set_relax(C, p->relax, p->repair);
     const long long max_blocks = p->max_iters / p->k_int;
     const long long tail = p->max_iters % p->k_int;
     // rho table (host pow, like the oracle; reading R7)
@@ -1686,6 +1730,7 @@ void gfors_params_default(gfors_params* p) {
     p->tol_primal = 1e-6; p->tol_dual = 1e-6; p->tol_binary = 1e-6; p->stall_rel = 1e-8; p->stall_window = 50;
     p->max_iters = 100000; p->time_limit_s = 1800.0; p->seed = 20251030ull; p->use_graph = 1; p->trace_cap = 4096;
     p->sampler = 0; p->a3_ls = -1; p->a3_n = 0; p->a3_gamma = 4.0;
+    p->relax = 0; p->repair = 0;
 }
 
 void gfors_prep_opts_default(gfors_prep_opts* p) {
@@ -1858,6 +1903,30 @@ gfors_status gfors_sample_assign3d(gfors_ctx* C, const double* p, uint64_t seed,
     API_END(C)
 }
 
+gfors_status gfors_set_relax(gfors_ctx* C, int32_t relax) {
+    API_BEGIN(C)
+    if (C->stage < 1) throw Err{GFORS_E_STATE, "gfors_set_relax: call gfors_load first"};
+    set_relax(C, relax, 0);
+    API_END(C)
+}
+
+gfors_status gfors_repair(gfors_ctx* C, uint64_t* bits, int64_t n_words) {
+    API_BEGIN(C)
+    if (C->stage < 2) throw Err{GFORS_E_STATE, "gfors_repair: call gfors_preprocess first"};
+    if (!bits || n_words < 1 || n_words > (1 << 14)) input_error("gfors_repair: bits and 1 <= n_words <= 16384 required");
+    const long long keep_m1p = C->m1p;
+    set_relax(C, 1, 1);
+    C->m1p = keep_m1p;  // the hook does not change the PDHG senses
+    ensure_batch(C, (int)n_words);
+    cudaStream_t s = C->stream;
+    CK(cudaMemcpyAsync(C->d_X, bits, C->n * n_words * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+    enqueue_repair(C, s, (int)n_words);
+    CK(cudaMemcpyAsync(bits, C->d_X, C->n * n_words * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    C->repair = false;
+    API_END(C)
+}
+
 gfors_status gfors_eval(gfors_ctx* C, const uint64_t* bits, int64_t n_words, uint8_t* feasible, double* z) {
     API_BEGIN(C)
     if (C->stage < 1) throw Err{GFORS_E_STATE, "gfors_eval: call gfors_load first"};
@@ -1973,6 +2042,7 @@ int64_t gfors_launches_per_block(gfors_ctx* C, const gfors_params* p) {
     long long n = -1;
     try {
         set_sampler(C, p->sampler, p->a3_n, p->a3_gamma, p->a3_ls);
+        set_relax(C, p->relax, p->repair);
         if (C->precision == 64) enqueue_block<double>(C, C->stream, p, W, hp, cudaGraphConditionalHandle{}, 0);
         else enqueue_block<float>(C, C->stream, p, W, hp, cudaGraphConditionalHandle{}, 0);
         n = C->launches;
