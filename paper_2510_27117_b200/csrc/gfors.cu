@@ -899,7 +899,8 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
     };
     if (C->push_primal) {
         // list the active duals (or the changed ones); the push kernels run iff the list is short
-        LAUNCH(C, s, KC_PRIMAL_PUSH, (k_wlist<T><<<grid_for(C->m), NT, 0, s>>>(st, ppr, ctrl, kint, j)));
+        LAUNCH(C, s, KC_PRIMAL_PUSH, (k_wlist<T><<<(int)std::min<long long>((C->m + 255) / 256, NUM_SMS_B200 * 4LL), NT, 0, s>>>(
+                                          st, ppr, ctrl, kint, j)));
         auto push = [&](cudaStream_t q) {
             LAUNCH(C, q, KC_PRIMAL_PUSH, (k_push_scatter_cols<T><<<grid_for(C->m * 32LL), NT, 0, q>>>(csr_K(C), ppr, st, ctrl, kint, j)));
             if (C->hasq)

@@ -18,11 +18,15 @@ namespace gfors {
 
 // lists the rows for the push-mode primal of parity par: valid accumulators -> rows whose y changed
 // this iteration, else rows with w != 0; and max |w|
+constexpr int WL_CAP = 4096;  // staged list entries per CTA between global flushes
 template <typename T>
 __global__ void __launch_bounds__(256) k_wlist(State<T> s, PushPrimal pp, const Ctrl* __restrict__ ctrl, long long kint,
                                                long long jj) {
+    // each CTA scans a contiguous range of rows in 256-row passes and stages its list in shared
+    // memory; one global atomic per WL_CAP staged rows (the single list counter was the contended
+    // resource of the per-pass flush: ~4000 same-address atomics per launch on config 5)
     __shared__ unsigned s_cnt, s_base;
-    __shared__ int s_list[256];
+    __shared__ int s_list[WL_CAP];
     __shared__ double sh[32];
     const int par = (int)(iter_index(ctrl, kint, jj) & 1);
     const bool delta = pp_valid(pp, par);
@@ -30,23 +34,32 @@ __global__ void __launch_bounds__(256) k_wlist(State<T> s, PushPrimal pp, const 
     const T* __restrict__ yold = par ? s.y[1] : s.y[0];
     double mx = 0.0;
     const long long m = pp.m;
-    const long long nbase = (m + 255) / 256;
-    for (long long bb = blockIdx.x; bb < nbase; bb += gridDim.x) {  // block-uniform trip count
-        const long long j = bb * 256 + threadIdx.x;
-        const double v = j < m ? (double)s.w[j] : 0.0;
-        mx = fmax(mx, fabs(v));
-        bool listed = v != 0.0;
-        if (delta) listed = j < m && ynew[j] != yold[j];
-        if (threadIdx.x == 0) s_cnt = 0u;
-        __syncthreads();
-        warp_append(listed, (int)j, &s_cnt, s_list);
+    const long long per = ((m + gridDim.x - 1) / gridDim.x + 255) / 256 * 256;
+    const long long r0 = blockIdx.x * per, r1 = min(m, r0 + per);
+    if (threadIdx.x == 0) s_cnt = 0u;
+    __syncthreads();
+    auto flush = [&]() {
         __syncthreads();
         if (threadIdx.x == 0) s_base = s_cnt ? atomicAdd(pp.rcount, s_cnt) : 0u;
         __syncthreads();
-        for (unsigned t = threadIdx.x; t < s_cnt; t += 256)
-            if ((long long)s_base + t < m) pp.rlist[s_base + t] = s_list[t];
+        const unsigned c = s_cnt, b = s_base;
+        for (unsigned t = threadIdx.x; t < c; t += 256)
+            if ((long long)b + t < m) pp.rlist[b + t] = s_list[t];
         __syncthreads();
+        if (threadIdx.x == 0) s_cnt = 0u;
+        __syncthreads();
+    };
+    for (long long b0 = r0; b0 < r1; b0 += 256) {  // block-uniform trip count
+        const long long j = b0 + threadIdx.x;
+        const double v = j < r1 ? (double)s.w[j] : 0.0;
+        mx = fmax(mx, fabs(v));
+        bool listed = v != 0.0;
+        if (delta) listed = j < r1 && ynew[j] != yold[j];
+        warp_append(listed, (int)j, &s_cnt, s_list);
+        __syncthreads();
+        if (s_cnt > WL_CAP - 256) flush();  // (block-uniform: read after the barrier)
     }
+    flush();
     mx = block_max<256>(mx, sh);
     if (threadIdx.x == 0 && mx > 0.0) atomicMax(pp.wmax, (unsigned long long)__double_as_longlong(mx));
 }
