@@ -189,23 +189,30 @@ __global__ void __launch_bounds__(256) k_qx_final(long long n, long long ld, lon
 
 // ---------------------------------------------------------------------------------------------
 // Sample unpack: bit-sliced X[i][W] -> Xs[l][ld] int8 in {0,1} (sample-major, K-major B operand),
-// zero for i >= n.  Thread: one lane l, 16 consecutive variables (one 16-byte store).
+// zero for i >= n.  Thread: 16 consecutive variables, one word column and 8 of its 64 lanes: 16 word
+// loads (cached), 8 lanes' 16-byte pieces (consecutive threads write consecutive pieces of a row).
 // ---------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_unpack_samples(const uint64_t* __restrict__ X, int W, long long n, long long ld,
                                                         int8_t* __restrict__ Xs) {
     const long long groups = ld / 16;
-    const long long total = groups * 64LL * W;
+    const long long total = groups * W * 8;  // (variable group, word, 8-lane slice)
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += gridDim.x * (long long)blockDim.x) {
-        const long long l = t / groups, g = t - l * groups;
-        const int w = (int)(l >> 6), bit = (int)(l & 63);
-        uint32_t v[4] = {0u, 0u, 0u, 0u};
+        const long long g = t % groups, ws = t / groups;
+        const long long w = ws >> 3;
+        const int b0 = (int)(ws & 7) * 8;
+        uint64_t x[16];
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
             const long long i = g * 16 + k;
-            const uint32_t b = i < n ? (uint32_t)((__ldg(X + i * W + w) >> bit) & 1ull) : 0u;
-            v[k >> 2] |= b << (8 * (k & 3));
+            x[k] = i < n ? __ldg(X + i * W + w) : 0ull;
         }
-        *reinterpret_cast<uint4*>(Xs + l * ld + g * 16) = make_uint4(v[0], v[1], v[2], v[3]);
+#pragma unroll 2
+        for (int bit = b0; bit < b0 + 8; ++bit) {
+            uint32_t v[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+            for (int k = 0; k < 16; ++k) v[k >> 2] |= (uint32_t)((x[k] >> bit) & 1ull) << (8 * (k & 3));
+            *reinterpret_cast<uint4*>(Xs + (64 * w + bit) * ld + g * 16) = make_uint4(v[0], v[1], v[2], v[3]);
+        }
     }
 }
 

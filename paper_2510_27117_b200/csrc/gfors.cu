@@ -989,7 +989,7 @@ int obj_vpj(const gfors_ctx* C, int W) {
 // samples to int8 rows, then tc_grid partial rows of int64 lane sums at zrows
 void enqueue_obj_dense(gfors_ctx* C, cudaStream_t s, int W, long long* zrows) {
     const long long lanes = 64LL * W;
-    LAUNCH(C, s, KC_OBJ_TC, (k_unpack_samples<<<grid_for(C->qld / 16 * lanes), NT, 0, s>>>(C->d_X, W, C->n, C->qld, C->d_Xs)));
+    LAUNCH(C, s, KC_OBJ_TC, (k_unpack_samples<<<grid_for(C->qld / 16 * W * 8), NT, 0, s>>>(C->d_X, W, C->n, C->qld, C->d_Xs)));
     const int nbox = (int)std::min<long long>(TC_NMAX, lanes);
     const size_t sm = tc_smem_bytes(nbox, (int)lanes);
     // the map of this batch width (host encode, ~1 us; captured by value into a graph node)
