@@ -703,7 +703,6 @@ inline Csr csr_Q(gfors_ctx* C, const double* pre = nullptr) { return Csr{C->d_qp
 
 // dense-Q GEMV (dense_q.cuh): out = Q~ (a - b), a/b picked on the device by iteration parity
 // (ctrl != nullptr) or taken directly (ctrl == nullptr, omega = 1: Preprocess power iteration)
-// out == nullptr: the consumer sums the chunk partials itself (csr_Qpart, pdhg.cuh q_pre)
 template <typename TX>
 void enqueue_qx(gfors_ctx* C, cudaStream_t s, QxSrc<TX> src, bool diff, double omega, double* out) {
     const long long n = C->n;
@@ -738,7 +737,7 @@ void enqueue_qx(gfors_ctx* C, cudaStream_t s, QxSrc<TX> src, bool diff, double o
                 LAUNCH(C, s, KC_QX, (k_qx_tma_fix<true><<<grid, QT_NT, qt_smem_bytes(), s>>>(C->tmQ64, n, C->qld, src, C->d_qxpart)));
             else
                 LAUNCH(C, s, KC_QX, (k_qx_tma_fix<false><<<grid, QT_NT, qt_smem_bytes(), s>>>(C->tmQ64, n, C->qld, src, C->d_qxpart)));
-            if (out) LAUNCH(C, s, KC_QX, (k_qx_final<<<grid_for(n), 256, 0, s>>>(n, C->qld, nchunk, C->d_qxpart, omega, out)));
+            LAUNCH(C, s, KC_QX, (k_qx_final<<<grid_for(n), 256, 0, s>>>(n, C->qld, nchunk, C->d_qxpart, omega, out)));
             return;
         }
     }
@@ -763,20 +762,7 @@ void enqueue_qx(gfors_ctx* C, cudaStream_t s, QxSrc<TX> src, bool diff, double o
         else
             LAUNCH(C, s, KC_QX, (k_qx_dense<TX, false><<<grid, QX_NT, 0, s>>>(C->d_qd, C->qld, n, src, C->d_qxpart)));
     }
-    if (out) LAUNCH(C, s, KC_QX, (k_qx_final<<<grid_for(n), 256, 0, s>>>(n, C->qld, nchunk, C->d_qxpart, omega, out)));
-}
-
-// the dense-Q row products for a consumer kernel: the chunk partials of the last enqueue_qx with
-// out == nullptr (fused final), or the finished vector of the symmetric GEMV
-inline Csr csr_Qpart(gfors_ctx* C, double* finished) {
-    Csr q = csr_Q(C, finished);
-    if (!(C->precision == 32 && C->qx_fix && C->qx_sym)) {
-        q.pre = C->d_qxpart;
-        q.pre_ld = C->qld;
-        q.pre_nchunk = (int)((C->n + QX_CW - 1) / QX_CW);
-        q.pre_div = C->omega;
-    }
-    return q;
+    LAUNCH(C, s, KC_QX, (k_qx_final<<<grid_for(n), 256, 0, s>>>(n, C->qld, nchunk, C->d_qxpart, omega, out)));
 }
 
 #define SUB_SWITCH(sub, ...)                                  \
@@ -847,11 +833,9 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
                                                                  C->d_rsign, C->m1p, ctrl, kint, j))));
         }
     }
-    const bool qsym = sizeof(T) == 4 && C->qx_fix && C->qx_sym;  // the symmetric GEMV always finishes
     if (C->qdense)  // 2 Q~ x term of the primal gradient by the dense GEMV
-        enqueue_qx<T>(C, s, QxSrc<T>{{st.x[0], st.x[1]}, {nullptr, nullptr}, ctrl, kint, j}, false, C->omega,
-                      qsym ? C->d_qx : nullptr);
-    const Csr Q = C->qdense ? csr_Qpart(C, C->d_qx) : csr_Q(C);
+        enqueue_qx<T>(C, s, QxSrc<T>{{st.x[0], st.x[1]}, {nullptr, nullptr}, ctrl, kint, j}, false, C->omega, C->d_qx);
+    const Csr Q = csr_Q(C, C->qdense ? C->d_qx : nullptr);
     const T* qs = (const T*)C->d_qs;
     const T* cs = (const T*)C->d_cs;
     // K' values: SIGN rows fold the sign into w, so the transpose carries no values
@@ -984,12 +968,10 @@ void enqueue_trigger(gfors_ctx* C, cudaStream_t s, long long kint, long long j) 
     } else {
         LAUNCH(C, s, KC_TRIGR, (k_fill<<<1, NT, 0, s>>>(C->d_part1, 3LL * C->nb1, 0.0)));
     }
-    const bool qsym = sizeof(T) == 4 && C->qx_fix && C->qx_sym;
     if (C->qdense)  // Q~(x_k - x_{k-1}) of s^x: x_k = par ? x[0] : x[1], x_{k-1} = par ? x[1] : x[0]
-        enqueue_qx<T>(C, s, QxSrc<T>{{st.x[1], st.x[0]}, {st.x[0], st.x[1]}, ctrl, kint, j}, true, C->omega,
-                      qsym ? C->d_qdx : nullptr);
+        enqueue_qx<T>(C, s, QxSrc<T>{{st.x[1], st.x[0]}, {st.x[0], st.x[1]}, ctrl, kint, j}, true, C->omega, C->d_qdx);
     if (C->hasq)
-        LAUNCH(C, s, KC_TRIGC, (k_trig_cols<T, true><<<C->nb2, NT, 0, s>>>(C->n, C->qdense ? csr_Qpart(C, C->d_qdx) : csr_Q(C), (const T*)C->d_qs, st, ctrl,
+        LAUNCH(C, s, KC_TRIGC, (k_trig_cols<T, true><<<C->nb2, NT, 0, s>>>(C->n, csr_Q(C, C->qdense ? C->d_qdx : nullptr), (const T*)C->d_qs, st, ctrl,
                                                                             kint, j, C->d_part2)));
     else
         LAUNCH(C, s, KC_TRIGC, (k_trig_cols<T, false><<<C->nb2, NT, 0, s>>>(C->n, csr_Q(C), (const T*)C->d_qs, st, ctrl,

@@ -31,20 +31,7 @@ struct Csr {
     const void* val;       // by KKind (nullptr for SIGN)
     long long rows;
     const double* pre = nullptr;  // Q only: precomputed row products (dense-Q path, dense_q.cuh)
-    long long pre_ld = 0;         // pre_nchunk > 0: pre holds column-chunk partials pre[c*pre_ld + i]
-    int pre_nchunk = 0;           //   whose ascending sum / pre_div is the row product (k_qx_final fused)
-    double pre_div = 1.0;
 };
-
-// the precomputed dense-Q row product of row i (dense_q.cuh): either final values, or the partials
-// of the GEMV's column chunks, summed here in ascending chunk order and divided by omega exactly as
-// k_qx_final would (one launch per product saved)
-__device__ __forceinline__ double q_pre(const Csr& Q, long long i) {
-    if (Q.pre_nchunk == 0) return Q.pre[i];
-    double s = 0.0;
-    for (int c = 0; c < Q.pre_nchunk; ++c) s += Q.pre[(long long)c * Q.pre_ld + i];
-    return s / Q.pre_div;
-}
 
 // Row-segment plan for long rows: segment s covers nonzeros [seg_start[s], seg_start[s+1]),
 // row r owns segments [row_seg[r], row_seg[r+1]).
@@ -150,7 +137,7 @@ __global__ void __launch_bounds__(256) k_primal(Csr Kt, Csr Q, const T* __restri
             for (; p < p1; p += SUB) a += kval<KIND>(Kt.val, p) * (double)__ldg(w + __ldg(Kt.idx + p));
             if constexpr (HASQ) {
                 if (Q.pre) {
-                    if (lane == 0) b = q_pre(Q, i);
+                    if (lane == 0) b = Q.pre[i];
                 } else {
                     const long long q0 = __ldg(Q.ptr + i), q1 = __ldg(Q.ptr + i + 1);
                     for (long long q = q0 + lane; q < q1; q += SUB)
@@ -255,7 +242,7 @@ __global__ void __launch_bounds__(256) k_primal_seg_final(long long n, SegPlan s
         double a = 0.0, b = 0.0;
         for (long long q = sp.row_seg[i]; q < sp.row_seg[i + 1]; ++q) a += part[q];
         if constexpr (HASQ) {
-            if (Q.pre) b = q_pre(Q, i);
+            if (Q.pre) b = Q.pre[i];
             else
                 for (long long q = Q.ptr[i]; q < Q.ptr[i + 1]; ++q) b += (double)qs[q] * (double)xin[Q.idx[q]];
         }
@@ -344,7 +331,7 @@ __global__ void __launch_bounds__(256) k_trig_cols(long long n, Csr Q, const T* 
         const double xi = (double)xk[i], xo = (double)xp[i];
         double e = 0.0;
         if constexpr (HASQ) {
-            if (Q.pre) e = q_pre(Q, i);  // dense-Q path: Q~(x_k - x_{k-1}) precomputed
+            if (Q.pre) e = Q.pre[i];  // dense-Q path: Q~(x_k - x_{k-1}) precomputed
             else
                 for (long long q = Q.ptr[i]; q < Q.ptr[i + 1]; ++q) {
                     const int c = Q.idx[q];

@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? PP_OCC32 : PP_OCC64) k_p
                 double b = 0.0;
                 if constexpr (HASQ)
                     if (i0 + u < n) {
-                        if (Q.pre) b = q_pre(Q, i0 + u);
+                        if (Q.pre) b = Q.pre[i0 + u];
                         else
                             for (long long q = __ldg(Q.ptr + i0 + u); q < __ldg(Q.ptr + i0 + u + 1); ++q)
                                 b += (double)__ldg(qs + q) * (double)__ldg(xin + __ldg(Q.idx + q));

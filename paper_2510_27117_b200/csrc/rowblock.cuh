@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(RB_NT, 6) k_primal_rb(Csr Kt, const long long*
                 a = rb_row_sum<T, KIND, true>(Kt, sv[st], p0, __ldg(Kt.ptr + i), __ldg(Kt.ptr + i + 1), lane, G);
                 if constexpr (HASQ) {
                     if (Q.pre) {
-                        if (lane == 0) bq = q_pre(Q, i);
+                        if (lane == 0) bq = Q.pre[i];
                     } else {
                         for (long long q = __ldg(Q.ptr + i) + lane; q < __ldg(Q.ptr + i + 1); q += G)
                             bq += (double)__ldg(qs + q) * (double)__ldg(xin + __ldg(Q.idx + q));

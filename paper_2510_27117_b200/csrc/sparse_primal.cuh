@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(SP_NT, 1) k_primal_sparse(Csr Kt, const long l
             a = rb_row_sum<T, KIND, true>(Kt, sv, p0, cur.q0, cur.q1, lane, G);
             if constexpr (HASQ) {
                 if (Q.pre) {
-                    if (lane == 0) bq = q_pre(Q, i);
+                    if (lane == 0) bq = Q.pre[i];
                 } else {
                     for (long long q = __ldg(Q.ptr + i) + lane; q < __ldg(Q.ptr + i + 1); q += G)
                         bq += (double)__ldg(qs + q) * (double)__ldg(xin + __ldg(Q.idx + q));
