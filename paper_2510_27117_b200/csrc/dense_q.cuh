@@ -702,13 +702,29 @@ __global__ void __launch_bounds__(QT_NT, 2) k_qx_tma_fix(const __grid_constant__
 #pragma unroll
             for (int d = 0; d < 4; ++d) acc[r][d] = 0;
         for (long long t = c * TPC; t < t1; ++t) {
-            // fixed-point digits of this lane's 8 columns (issued before the wait)
-            double xv[8];
-            qt_load_x8<float>(a, b, t * QT_COLS + 8 * lane, n, xv);
+            // fixed-point digits of this lane's 8 columns (issued before the wait).  x itself: x*2^31 is
+            // exact in fp32, so the fp32 conversion rounds exactly like the fp64 one; the difference
+            // x_k - x_{k-1} is formed in fp64 (exact) and converted there
             uint32_t X[8];
+            if constexpr (DIFF) {
+                double xv[8];
+                qt_load_x8<float>(a, b, t * QT_COLS + 8 * lane, n, xv);
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
-                X[k] = DIFF ? (uint32_t)__double2int_rn(xv[k] * 1073741824.0) : (uint32_t)__double2ull_rn(xv[k] * 2147483648.0);
+                for (int k = 0; k < 8; ++k) X[k] = (uint32_t)__double2int_rn(xv[k] * 1073741824.0);
+            } else {
+                const long long col0 = t * QT_COLS + 8 * lane;
+                float xf[8];
+                if (col0 + 8 <= n) {
+                    const float4 f0 = __ldg(reinterpret_cast<const float4*>(a + col0));
+                    const float4 f1 = __ldg(reinterpret_cast<const float4*>(a + col0) + 1);
+                    xf[0] = f0.x; xf[1] = f0.y; xf[2] = f0.z; xf[3] = f0.w; xf[4] = f1.x; xf[5] = f1.y; xf[6] = f1.z; xf[7] = f1.w;
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) xf[k] = col0 + k < n ? a[col0 + k] : 0.0f;
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k) X[k] = __float2uint_rn(xf[k] * 2147483648.0f);
+            }
             uint32_t w0[4], w1[4];
             digits4(X[0], X[1], X[2], X[3], w0);
             digits4(X[4], X[5], X[6], X[7], w1);
