@@ -474,7 +474,7 @@ __global__ void __launch_bounds__(TC_NT, 1)
 // ---------------------------------------------------------------------------------------------
 constexpr int QT_ROWS = 64, QT_COLS = 256, QT_STAGES = 6, QT_NT = 288;
 constexpr int QT_TILE = QT_ROWS * QT_COLS;  // 16 KB
-constexpr size_t qt_smem_bytes() { return 1024 + (size_t)QT_STAGES * QT_TILE + 256 + 256 * 8; }
+constexpr size_t qt_smem_bytes(int stages = QT_STAGES) { return 1024 + (size_t)stages * QT_TILE + 256 + 256 * 8; }
 
 template <typename TX>
 __device__ __forceinline__ void qt_load_x8(const TX* __restrict__ a, const TX* __restrict__ b, long long col0,
@@ -651,13 +651,13 @@ __device__ __forceinline__ void digits4(uint32_t X0, uint32_t X1, uint32_t X2, u
     w[3] = __byte_perm(hi01, hi23, 0x7632);
 }
 
-template <bool DIFF>
-__global__ void __launch_bounds__(QT_NT, 2) k_qx_tma_fix(const __grid_constant__ CUtensorMap tmQ, long long n, long long ld,
+template <bool DIFF, int ST = QT_STAGES, int MINB = 2>
+__global__ void __launch_bounds__(QT_NT, MINB) k_qx_tma_fix(const __grid_constant__ CUtensorMap tmQ, long long n, long long ld,
                                                         QxSrc<float> src, double* __restrict__ part) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* tiles = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-    uint64_t* full = reinterpret_cast<uint64_t*>(tiles + (size_t)QT_STAGES * QT_TILE);
-    uint64_t* empty = full + QT_STAGES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(tiles + (size_t)ST * QT_TILE);
+    uint64_t* empty = full + ST;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long rblocks = (n + QT_ROWS - 1) / QT_ROWS;
     const long long nchunk = (n + QX_CW - 1) / QX_CW;
@@ -665,7 +665,7 @@ __global__ void __launch_bounds__(QT_NT, 2) k_qx_tma_fix(const __grid_constant__
     const long long units = rblocks * nchunk;
     constexpr int TPC = QX_CW / QT_COLS;
     if (threadIdx.x == 0) {
-        for (int st = 0; st < QT_STAGES; ++st) { mbar_init(&full[st], 1); mbar_init(&empty[st], 8); }
+        for (int st = 0; st < ST; ++st) { mbar_init(&full[st], 1); mbar_init(&empty[st], 8); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -681,7 +681,7 @@ __global__ void __launch_bounds__(QT_NT, 2) k_qx_tma_fix(const __grid_constant__
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_expect_tx(&full[stage], QT_TILE);
                     tma_load_2d(tiles + (size_t)stage * QT_TILE, &tmQ, &full[stage], (int)(t * QT_COLS), (int)(rb * QT_ROWS));
-                    if (++stage == QT_STAGES) { stage = 0; phase ^= 1; }
+                    if (++stage == ST) { stage = 0; phase ^= 1; }
                 }
             }
         }
@@ -735,7 +735,7 @@ __global__ void __launch_bounds__(QT_NT, 2) k_qx_tma_fix(const __grid_constant__
             for (int r = 0; r < 8; ++r) q[r] = *reinterpret_cast<const uint2*>(tile + r * QT_COLS);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stage]);
-            if (++stage == QT_STAGES) { stage = 0; phase ^= 1; }
+            if (++stage == ST) { stage = 0; phase ^= 1; }
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
 #pragma unroll

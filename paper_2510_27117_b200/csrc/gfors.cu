@@ -384,6 +384,7 @@ struct gfors_ctx {
     CUtensorMap tmQ64{};           // TMA map of Qd for the GEMV (256-byte x 64-row boxes, no swizzle)
     bool qx_tma = true;            // TMA-pipelined GEMV (GFORS_QX_TMA=0: the register-streaming k_qx_dense)
     bool qx_fix = true;            // fp32 iterates: exact fixed-point dp4a GEMV (GFORS_QX_FIX=0: fp64 FMA)
+    int qx_cfg = 0;                // ring depth x CTAs/SM of the fixed-point GEMV (GFORS_QX_CFG: 0 6x2, 1 4x3, 2 3x4, 3 8x1)
     bool qx_sym = false;           // ... reading only the upper-triangle tiles (GFORS_QX_SYM=1; slower)
     int* d_qs_uoff = nullptr;      // symmetric GEMV: first unit of each 256-column tile (problem-owned)
     int qs_ntc = 0;
@@ -726,17 +727,29 @@ void enqueue_qx(gfors_ctx* C, cudaStream_t s, QxSrc<TX> src, bool diff, double o
         }
         if (C->qx_fix) {  // fp32 iterates: exact dp4a products on the fixed-point image of x
             const long long units = (n + QT_ROWS - 1) / QT_ROWS * nchunk;
-            const int grid = (int)std::min<long long>(units, NUM_SMS_B200 * 2LL);
-            static bool attr[2] = {false, false};
-            if (!attr[diff ? 1 : 0]) {
-                if (diff) CK(cudaFuncSetAttribute(k_qx_tma_fix<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qt_smem_bytes()));
-                else CK(cudaFuncSetAttribute(k_qx_tma_fix<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qt_smem_bytes()));
-                attr[diff ? 1 : 0] = true;
-            }
-            if (diff)
-                LAUNCH(C, s, KC_QX, (k_qx_tma_fix<true><<<grid, QT_NT, qt_smem_bytes(), s>>>(C->tmQ64, n, C->qld, src, C->d_qxpart)));
-            else
-                LAUNCH(C, s, KC_QX, (k_qx_tma_fix<false><<<grid, QT_NT, qt_smem_bytes(), s>>>(C->tmQ64, n, C->qld, src, C->d_qxpart)));
+            // ring depth x CTAs per SM (GFORS_QX_CFG experiments: 6x2 default, 4x3, 3x4, 8x1)
+            const int cfg = C->qx_cfg;
+            const int minb = cfg == 1 ? 3 : (cfg == 2 ? 4 : (cfg == 3 ? 1 : 2));
+            const int grid = (int)std::min<long long>(units, (long long)NUM_SMS_B200 * minb);
+#define QXF_LAUNCH(STV, MBV)                                                                                          \
+    {                                                                                                                 \
+        static bool attr_f[2] = {false, false};                                                                      \
+        const size_t smb = qt_smem_bytes(STV);                                                                        \
+        if (!attr_f[diff ? 1 : 0]) {                                                                                  \
+            if (diff) CK(cudaFuncSetAttribute(k_qx_tma_fix<true, STV, MBV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb)); \
+            else CK(cudaFuncSetAttribute(k_qx_tma_fix<false, STV, MBV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb)); \
+            attr_f[diff ? 1 : 0] = true;                                                                              \
+        }                                                                                                             \
+        if (diff)                                                                                                     \
+            LAUNCH(C, s, KC_QX, (k_qx_tma_fix<true, STV, MBV><<<grid, QT_NT, smb, s>>>(C->tmQ64, n, C->qld, src, C->d_qxpart))); \
+        else                                                                                                          \
+            LAUNCH(C, s, KC_QX, (k_qx_tma_fix<false, STV, MBV><<<grid, QT_NT, smb, s>>>(C->tmQ64, n, C->qld, src, C->d_qxpart))); \
+    }
+            if (cfg == 1) QXF_LAUNCH(4, 3)
+            else if (cfg == 2) QXF_LAUNCH(3, 4)
+            else if (cfg == 3) QXF_LAUNCH(8, 1)
+            else QXF_LAUNCH(6, 2)
+#undef QXF_LAUNCH
             LAUNCH(C, s, KC_QX, (k_qx_final<<<grid_for(n), 256, 0, s>>>(n, C->qld, nchunk, C->d_qxpart, omega, out)));
             return;
         }
