@@ -1169,6 +1169,8 @@ void set_sampler(gfors_ctx* C, int sampler, long long a3n, double gamma, long lo
     if (a3n < 1 || a3n > 4096 || a3n * a3n * a3n != C->n)
         input_error("params.a3_n: sampler 1 needs n = a3_n^3 variables (a3_n = %lld, n = %lld)", a3n, C->n);
     if (!(gamma > 0.0)) input_error("params.a3_gamma: must be > 0");
+    if (C->sharded) input_error("params.sampler: the Alg. 4 sampler is not combined with the NCCL-sharded loop "
+                                "(its winner regeneration replays the Bernoulli contract)");
     ensure_a3(C, a3n);
     C->a3.n = a3n;
     C->a3.K = std::min<long long>(C->n, (long long)std::ceil(gamma * (double)a3n));
