@@ -13,6 +13,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <climits>
 #include <mutex>
 #include <thread>
@@ -384,7 +385,7 @@ struct gfors_ctx {
     CUtensorMap tmQ64{};           // TMA map of Qd for the GEMV (256-byte x 64-row boxes, no swizzle)
     bool qx_tma = true;            // TMA-pipelined GEMV (GFORS_QX_TMA=0: the register-streaming k_qx_dense)
     bool qx_fix = true;            // fp32 iterates: exact fixed-point dp4a GEMV (GFORS_QX_FIX=0: fp64 FMA)
-    int qx_cfg = 0;                // ring depth x CTAs/SM of the fixed-point GEMV (GFORS_QX_CFG: 0 6x2, 1 4x3, 2 3x4, 3 8x1)
+    int qx_cfg = 1;                // ring depth x CTAs/SM of the fixed-point GEMV (GFORS_QX_CFG: 0 6x2, 1 4x3 default, 2 3x4, 3 8x1)
     bool qx_sym = false;           // ... reading only the upper-triangle tiles (GFORS_QX_SYM=1; slower)
     int* d_qs_uoff = nullptr;      // symmetric GEMV: first unit of each 256-column tile (problem-owned)
     int qs_ntc = 0;
