@@ -75,8 +75,20 @@ X* dalloc(size_t count) {
     CK(cudaMalloc(&p, count * sizeof(X)));
     return reinterpret_cast<X*>(p);
 }
-template <typename X>
-X* dupload(const std::vector<X>& v, cudaStream_t s) {
+// allocator whose resize() leaves new elements uninitialised: the large host copies of K are then
+// first touched by the parallel copy loops instead of a serial value-initialisation pass
+template <typename T>
+struct DefaultInitAlloc : std::allocator<T> {
+    template <typename U> struct rebind { using other = DefaultInitAlloc<U>; };
+    DefaultInitAlloc() = default;
+    template <typename U> DefaultInitAlloc(const DefaultInitAlloc<U>&) {}
+    template <typename U> void construct(U* p) noexcept { ::new ((void*)p) U; }
+    template <typename U, typename... A> void construct(U* p, A&&... a) { ::new ((void*)p) U(std::forward<A>(a)...); }
+};
+template <typename T> using hvec = std::vector<T, DefaultInitAlloc<T>>;
+
+template <typename X, typename Al>
+X* dupload(const std::vector<X, Al>& v, cudaStream_t s) {
     X* p = dalloc<X>(v.size());
     if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(X), cudaMemcpyHostToDevice, s));
     return p;
@@ -344,8 +356,10 @@ struct gfors_ctx {
     bool maximize = false, integral = false, hasq = false;
     double c0 = 0.0;
     std::vector<int64_t> kptr, ktptr, qptr;
-    std::vector<int32_t> kcol, ktrow, qcol;
-    std::vector<double> kval, ktval, qval, ru, c;
+    hvec<int32_t> kcol;
+    hvec<double> kval;
+    std::vector<int32_t> ktrow, qcol;
+    std::vector<double> ktval, qval, ru, c;
     std::vector<int64_t> perm;
     std::vector<signed char> rsign;
     int kkind = KV_F64;

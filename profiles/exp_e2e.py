@@ -14,7 +14,7 @@ from gen import instances as G  # noqa: E402
 inst = G.make_config(5, 1)
 host = {k: (torch.from_numpy(np.ascontiguousarray(v)).pin_memory().numpy() if isinstance(v, np.ndarray) else v)
         for k, v in inst.items()}
-for rep in range(2):
+for rep in range(4):
     s = gf.Solver(0)
     torch.cuda.synchronize()
     t0 = time.perf_counter(); s.load(host); torch.cuda.synchronize(); t1 = time.perf_counter()
