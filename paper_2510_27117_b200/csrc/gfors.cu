@@ -399,6 +399,9 @@ struct gfors_ctx {
     CUtensorMap tmQ64{};           // TMA map of Qd for the GEMV (256-byte x 64-row boxes, no swizzle)
     bool qx_tma = true;            // TMA-pipelined GEMV (GFORS_QX_TMA=0: the register-streaming k_qx_dense)
     bool qx_fix = true;            // fp32 iterates: exact fixed-point dp4a GEMV (GFORS_QX_FIX=0: fp64 FMA)
+    bool qx_reuse = true;          // fp32 loop: the trigger's product of x_k serves the next block's first primal (GFORS_QX_REUSE=0: off)
+    double* d_qxpart2 = nullptr;   // [nchunk][qld] partials of the trigger's product (prep-owned)
+    long long* d_qreuse = nullptr; // block index whose first primal may reuse d_qxpart2 (prep-owned)
     int qx_cfg = 1;                // ring depth x CTAs/SM of the fixed-point GEMV (GFORS_QX_CFG: 0 6x2, 1 4x3 default, 2 3x4, 3 8x1)
     bool qx_sym = false;           // ... reading only the upper-triangle tiles (GFORS_QX_SYM=1; slower)
     int* d_qs_uoff = nullptr;      // symmetric GEMV: first unit of each 256-column tile (problem-owned)
@@ -574,7 +577,8 @@ void gfors_ctx::free_prep() {
                    (void**)&d_red, (void**)&d_scalar, (void**)&d_segpart, (void**)&d_segpart2, (void**)&d_u, (void**)&d_ones, (void**)&d_rec, (void**)&d_regen, (void**)&d_plist[0], (void**)&d_plist[1], (void**)&d_pcount, (void**)&d_pflags, (void**)&d_acc, (void**)&d_rlist, (void**)&d_rcount, (void**)&d_wmax, (void**)&d_accx, (void**)&d_xst, (void**)&d_accv, (void**)&d_ones_cnt, (void**)&d_trig_flag, (void**)&d_part1,
                    (void**)&d_part2, (void**)&d_hist, (void**)&d_rho, (void**)&d_trace, (void**)&d_xbest,
                    (void**)&d_X, (void**)&d_viol, (void**)&d_iacc, &d_zpart, (void**)&d_z, (void**)&d_ctrl,
-                   (void**)&d_qx, (void**)&d_qdx, (void**)&d_qxpart, (void**)&d_Xs, (void**)&d_qacc};
+                   (void**)&d_qx, (void**)&d_qdx, (void**)&d_qxpart, (void**)&d_Xs, (void**)&d_qacc,
+                   (void**)&d_qxpart2, (void**)&d_qreuse};
     for (void** p : ps) { dfree(*p); *p = nullptr; }
     X_words = iacc_len = zpart_len = z_len = Xs_lanes = 0;
     for (int b = 0; b < 2; ++b) { dfree(a3.keys[b]); dfree(a3.vals[b]); }
@@ -746,6 +750,17 @@ void enqueue_qx(gfors_ctx* C, cudaStream_t s, QxSrc<TX> src, bool diff, double o
             const int cfg = C->qx_cfg;
             const int minb = cfg == 1 ? 3 : (cfg == 2 ? 4 : (cfg == 3 ? 1 : 2));
             const int grid = (int)std::min<long long>(units, (long long)NUM_SMS_B200 * minb);
+            // product reuse across loop blocks (qx_reuse): the trigger computes S(x_k) (not the
+            // difference) into d_qxpart2; the next block's first primal skips its GEMV and reads it
+            // (k_int > 1: with one iteration per block the skipped GEMV would be the trigger's x_{k-1} product)
+            const bool trig_reuse = diff && C->qx_reuse && src.ctrl && src.kint > 1;
+            const bool prim_reuse = !diff && C->qx_reuse && src.ctrl && src.kint > 1 && src.j == 0;
+            double* dst = trig_reuse ? C->d_qxpart2 : C->d_qxpart;
+            const long long* reuse = prim_reuse ? C->d_qreuse : nullptr;
+            if (trig_reuse) {
+                diff = false;
+                src = QxSrc<TX>{{src.a[0], src.a[1]}, {nullptr, nullptr}, src.ctrl, src.kint, src.j};
+            }
 #define QXF_LAUNCH(STV, MBV)                                                                                          \
     {                                                                                                                 \
         static bool attr_f[2] = {false, false};                                                                      \
@@ -756,16 +771,23 @@ void enqueue_qx(gfors_ctx* C, cudaStream_t s, QxSrc<TX> src, bool diff, double o
             attr_f[diff ? 1 : 0] = true;                                                                              \
         }                                                                                                             \
         if (diff)                                                                                                     \
-            LAUNCH(C, s, KC_QX, (k_qx_tma_fix<true, STV, MBV><<<grid, QT_NT, smb, s>>>(C->tmQ64, n, C->qld, src, C->d_qxpart))); \
+            LAUNCH(C, s, KC_QX, (k_qx_tma_fix<true, STV, MBV><<<grid, QT_NT, smb, s>>>(C->tmQ64, n, C->qld, src, dst, reuse))); \
         else                                                                                                          \
-            LAUNCH(C, s, KC_QX, (k_qx_tma_fix<false, STV, MBV><<<grid, QT_NT, smb, s>>>(C->tmQ64, n, C->qld, src, C->d_qxpart))); \
+            LAUNCH(C, s, KC_QX, (k_qx_tma_fix<false, STV, MBV><<<grid, QT_NT, smb, s>>>(C->tmQ64, n, C->qld, src, dst, reuse))); \
     }
             if (cfg == 1) QXF_LAUNCH(4, 3)
             else if (cfg == 2) QXF_LAUNCH(3, 4)
             else if (cfg == 3) QXF_LAUNCH(8, 1)
             else QXF_LAUNCH(6, 2)
 #undef QXF_LAUNCH
-            LAUNCH(C, s, KC_QX, (k_qx_final<<<grid_for(n), 256, 0, s>>>(n, C->qld, nchunk, C->d_qxpart, omega, out)));
+            if (trig_reuse)
+                LAUNCH(C, s, KC_QX, (k_qx_diff_final<<<grid_for(n), 256, 0, s>>>(n, C->qld, nchunk, C->d_qxpart2, C->d_qxpart,
+                                                                                omega, out, C->d_qreuse, src.ctrl)));
+            else if (prim_reuse)
+                LAUNCH(C, s, KC_QX, (k_qx_final_sel<<<grid_for(n), 256, 0, s>>>(n, C->qld, nchunk, C->d_qxpart, C->d_qxpart2,
+                                                                               C->d_qreuse, src.ctrl, src.kint, src.j, omega, out)));
+            else
+                LAUNCH(C, s, KC_QX, (k_qx_final<<<grid_for(n), 256, 0, s>>>(n, C->qld, nchunk, C->d_qxpart, omega, out)));
             return;
         }
     }
@@ -1430,6 +1452,9 @@ static void do_preprocess(gfors_ctx* C, const gfors_prep_opts* o, gfors_scaling*
         C->d_qdx = dalloc<double>(n);
         C->d_qxpart = dalloc<double>((n + QX_CW - 1) / QX_CW * C->qld);
         C->d_qacc = dalloc<unsigned long long>(n);
+        C->d_qxpart2 = dalloc<double>((n + QX_CW - 1) / QX_CW * C->qld);
+        C->d_qreuse = dalloc<long long>(1);
+        CK(cudaMemsetAsync(C->d_qreuse, 0xff, sizeof(long long), s));  // -1: nothing to reuse
         CK(cudaMemsetAsync(C->d_qacc, 0, n * sizeof(unsigned long long), s));
     }
     unsigned long long* d_zr = dalloc<unsigned long long>(1);

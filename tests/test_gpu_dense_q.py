@@ -190,3 +190,34 @@ def test_symmetric_gemv_bit_identical(gf, n):
         out.append((s.get_state()[0], ind))
     assert np.array_equal(out[0][0], out[1][0])
     assert out[0][1] == out[1][1]
+
+
+@pytest.mark.parametrize("kint", [10, 3, 1])
+def test_gemv_reuse_across_blocks(gf, kint):
+    """fp32 loop: the trigger's product of x_k serving the next block's first primal (GFORS_QX_REUSE)
+    gives the same trajectory as recomputing it (the first primal's product is bit-identical; the
+    s^x term of the indicators differs only in how the fixed-point difference is formed), and the
+    same incumbent."""
+    inst = G.max_cut(400, 0.5, 21)
+    res = []
+    for reuse in ("1", "0"):
+        old = os.environ.get("GFORS_QX_REUSE")
+        os.environ["GFORS_QX_REUSE"] = reuse
+        try:
+            s, _ = _solver(gf, inst, 32)
+        finally:
+            if old is None:
+                os.environ.pop("GFORS_QX_REUSE", None)
+            else:
+                os.environ["GFORS_QX_REUSE"] = old
+        kw = dict(k_int=kint, k_b=128, tol_primal=-1.0, tol_dual=-1.0, tol_binary=-1.0, stall_rel=-1.0)
+        s.run(max_iters=30 * kint, **kw)
+        x = s.get_state()[0]
+        z, xb, _ = s.best_incumbent()
+        tr = s.trace()
+        res.append((x, z, xb, tr))
+    assert np.array_equal(res[0][0], res[1][0])
+    assert res[0][1] == res[1][1] and np.array_equal(res[0][2], res[1][2])
+    t0, t1 = res[0][3], res[1][3]
+    assert np.array_equal(t0[:, [0, 1, 2, 4, 5, 6, 7]], t1[:, [0, 1, 2, 4, 5, 6, 7]])
+    assert np.allclose(t0[:, 3], t1[:, 3], rtol=1e-6, atol=1e-9)  # ||s^x||
