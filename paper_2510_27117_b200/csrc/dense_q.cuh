@@ -250,7 +250,8 @@ __global__ void __launch_bounds__(256) k_unpack_samples(const uint64_t* __restri
 constexpr int TC_BM = 128;        // rows of Q per tile (UMMA M)
 constexpr int TC_BK = 128;        // K bytes per pipeline stage (= one 128B swizzle atom row)
 constexpr int TC_NMAX = 256;      // lanes per pass (UMMA N <= 256)
-constexpr int TC_STAGES = 4;
+constexpr int TC_STAGES = 4;       // minimum ring depth; the launch uses as many as fit (<= TC_STAGES_MAX)
+constexpr int TC_STAGES_MAX = 8;
 constexpr int TC_NT = 192;        // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2-5 epilogue
 constexpr int TC_SMEM_A = TC_BM * TC_BK;  // 16 KB
 
@@ -259,8 +260,14 @@ struct TcItem {
     int I, j0, j1, wgt;
 };
 
+// ring depth: as many (A + B) stages as fit next to the barriers and the lane sums (227 KB per CTA)
+__host__ __device__ constexpr int tc_stages(int nbox, int lanes) {
+    return (int)(((227 * 1024 - 1024 - 256 - 8 * (size_t)lanes) / (TC_SMEM_A + (size_t)nbox * TC_BK)) > TC_STAGES_MAX
+                     ? TC_STAGES_MAX
+                     : ((227 * 1024 - 1024 - 256 - 8 * (size_t)lanes) / (TC_SMEM_A + (size_t)nbox * TC_BK)));
+}
 __host__ __device__ constexpr size_t tc_smem_bytes(int nbox, int lanes) {
-    return 1024 /*align slack*/ + (size_t)TC_STAGES * (TC_SMEM_A + (size_t)nbox * TC_BK) + 256 /*barriers*/ +
+    return 1024 /*align slack*/ + (size_t)tc_stages(nbox, lanes) * (TC_SMEM_A + (size_t)nbox * TC_BK) + 256 /*barriers*/ +
            8 * (size_t)lanes /*zacc*/;
 }
 
@@ -370,15 +377,16 @@ __global__ void __launch_bounds__(TC_NT, 1)
                    const uint64_t* __restrict__ X, int W, long long n, long long* __restrict__ zrows) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    const int ST = tc_stages(nbox, lanes);
     uint8_t* sA = smem;
-    uint8_t* sB = smem + TC_STAGES * TC_SMEM_A;
+    uint8_t* sB = smem + ST * TC_SMEM_A;
     const int bbytes = nbox * TC_BK;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + (size_t)TC_STAGES * bbytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + (size_t)ST * bbytes);
     uint64_t* full = bars;
-    uint64_t* empty = bars + TC_STAGES;
-    uint64_t* tfull = bars + 2 * TC_STAGES;
-    uint64_t* tempty = bars + 2 * TC_STAGES + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * TC_STAGES + 4);
+    uint64_t* empty = bars + ST;
+    uint64_t* tfull = bars + 2 * ST;
+    uint64_t* tempty = bars + 2 * ST + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * ST + 4);
     long long* zacc = reinterpret_cast<long long*>(bars + 32);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -387,7 +395,7 @@ __global__ void __launch_bounds__(TC_NT, 1)
 
     for (int l = threadIdx.x; l < lanes; l += blockDim.x) zacc[l] = 0;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < TC_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int s = 0; s < ST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
         for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -417,7 +425,7 @@ __global__ void __launch_bounds__(TC_NT, 1)
                         mbar_expect_tx(&full[stage], TC_SMEM_A + bbytes);
                         tma_load_2d(sA + stage * TC_SMEM_A, &tmQ, &full[stage], kb * TC_BK, t.I * TC_BM);
                         tma_load_2d(sB + stage * bbytes, &tmX, &full[stage], kb * TC_BK, p * TC_NMAX);
-                        if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
+                        if (++stage == ST) { stage = 0; phase ^= 1; }
                     }
                 }
             }
@@ -447,7 +455,7 @@ __global__ void __launch_bounds__(TC_NT, 1)
                             umma_i8(d, umma_desc_sw128(a0 + 32 * k), umma_desc_sw128(b0 + 32 * k), idesc,
                                     (kb > t.j0 || k > 0) ? 1u : 0u);
                         umma_commit(&empty[stage]);
-                        if (++stage == TC_STAGES) { stage = 0; phase ^= 1; }
+                        if (++stage == ST) { stage = 0; phase ^= 1; }
                     }
                     umma_commit(&tfull[acc]);
                     if (++acc == 2) { acc = 0; aphase ^= 1; }

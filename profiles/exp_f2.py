@@ -23,9 +23,11 @@ for nf, nc in sizes:
         s.preprocess(precision=int(os.environ.get("PREC", "32")))
         kw = {} if os.environ.get("HALT", "1") == "1" else dict(tol_primal=-1.0, tol_dual=-1.0, tol_binary=-1.0,
                                                                 stall_rel=-1.0)
+        if "SIGMA" in os.environ:
+            kw["sigma"] = float(os.environ["SIGMA"])
         info = s.run(max_iters=MAXIT, k_b=int(os.environ.get("KB", "128")), **kw)
         z, x, meta = s.best_incumbent(want_x=False)
-        print(json.dumps({"nf": nf, "nc": nc, "tu": tu, "tu_s": round(t_tu, 3), "iters": info["iters"],
+        print(json.dumps({"nf": nf, "nc": nc, "tu": tu, "sigma": kw.get("sigma", 0.99), "tu_s": round(t_tu, 3), "iters": info["iters"],
                           "halt": info["halt_reason"], "z": z if meta["has_incumbent"] else None,
                           "found_iter": meta["found_iter"], "tti_s": meta["found_time_s"] if meta["has_incumbent"] else None,
                           "loop_s": info["elapsed_s"]}), flush=True)
