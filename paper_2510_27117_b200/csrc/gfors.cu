@@ -402,7 +402,8 @@ struct gfors_ctx {
     bool qx_reuse = true;          // fp32 loop: the trigger's product of x_k serves the next block's first primal (GFORS_QX_REUSE=0: off)
     double* d_qxpart2 = nullptr;   // [nchunk][qld] partials of the trigger's product (prep-owned)
     long long* d_qreuse = nullptr; // block index whose first primal may reuse d_qxpart2 (prep-owned)
-    int qx_cfg = 1;                // ring depth x CTAs/SM of the fixed-point GEMV (GFORS_QX_CFG: 0 6x2, 1 4x3 default, 2 3x4, 3 8x1)
+    int qx_cfg = 1;
+    int pp_occ = 0;                // fp32 push-mode primal: CTAs per SM (GFORS_PP_OCC experiments: 3, 5 default, 6, 8)                // ring depth x CTAs/SM of the fixed-point GEMV (GFORS_QX_CFG: 0 6x2, 1 4x3 default, 2 3x4, 3 8x1)
     bool qx_sym = false;           // ... reading only the upper-triangle tiles (GFORS_QX_SYM=1; slower)
     int* d_qs_uoff = nullptr;      // symmetric GEMV: first unit of each 256-column tile (problem-owned)
     int qs_ntc = 0;
@@ -955,6 +956,15 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
             LAUNCH(C, q, KC_PRIMAL_PUSH, (k_push_scatter_cols<T><<<grid_for(C->m * 32LL), NT, 0, q>>>(csr_K(C), ppr, st, ctrl, kint, j)));
             if (C->hasq)
                 LAUNCH(C, q, KC_PRIMAL_PUSH, (k_primal_push<T, true><<<pp_grid<T>(C->n), NT, 0, q>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
+                    csr_Kt(C), trig_push ? C->d_accv : nullptr, C->d_ones_cnt, C->d_trig_flag)));
+            else if (sizeof(T) == 4 && C->pp_occ == 3)
+                LAUNCH(C, q, KC_PRIMAL_PUSH, (k_primal_push<T, false, 3><<<pp_grid<T>(C->n, 3), NT, 0, q>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
+                    csr_Kt(C), trig_push ? C->d_accv : nullptr, C->d_ones_cnt, C->d_trig_flag)));
+            else if (sizeof(T) == 4 && C->pp_occ == 6)
+                LAUNCH(C, q, KC_PRIMAL_PUSH, (k_primal_push<T, false, 6><<<pp_grid<T>(C->n, 6), NT, 0, q>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
+                    csr_Kt(C), trig_push ? C->d_accv : nullptr, C->d_ones_cnt, C->d_trig_flag)));
+            else if (sizeof(T) == 4 && C->pp_occ == 8)
+                LAUNCH(C, q, KC_PRIMAL_PUSH, (k_primal_push<T, false, 8><<<pp_grid<T>(C->n, 8), NT, 0, q>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
                     csr_Kt(C), trig_push ? C->d_accv : nullptr, C->d_ones_cnt, C->d_trig_flag)));
             else
                 LAUNCH(C, q, KC_PRIMAL_PUSH, (k_primal_push<T, false><<<pp_grid<T>(C->n), NT, 0, q>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,

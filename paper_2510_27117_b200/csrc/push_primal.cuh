@@ -139,13 +139,14 @@ __device__ __forceinline__ void st4(T* __restrict__ p, const T (&v)[PP_U]) {
 // flags — a chain of dependent loads) is paid once, not per 1024 columns; matters when most columns
 // are skipped
 template <typename T>
-inline int pp_grid(long long n) {
+inline int pp_grid(long long n, int occ = 0) {
     const long long passes = (n + 256 * PP_U - 1) / (256 * PP_U);
-    return (int)std::max<long long>(1, std::min<long long>(passes, (long long)NUM_SMS_B200 * (sizeof(T) == 4 ? PP_OCC32 : PP_OCC64)));
+    if (occ <= 0) occ = sizeof(T) == 4 ? PP_OCC32 : PP_OCC64;
+    return (int)std::max<long long>(1, std::min<long long>(passes, (long long)NUM_SMS_B200 * occ));
 }
 
-template <typename T, bool HASQ>
-__global__ void __launch_bounds__(256, sizeof(T) == 4 ? PP_OCC32 : PP_OCC64) k_primal_push(long long n, PushPrimal pp, Csr Q, const T* __restrict__ qs,
+template <typename T, bool HASQ, int OCC = (sizeof(T) == 4 ? PP_OCC32 : PP_OCC64)>
+__global__ void __launch_bounds__(256, OCC) k_primal_push(long long n, PushPrimal pp, Csr Q, const T* __restrict__ qs,
                                                      State<T> s, const T* __restrict__ cs, const Ctrl* __restrict__ ctrl,
                                                      long long kint, long long j, PushList pl, Csr Kt,
                                                      long long* __restrict__ accv, unsigned* __restrict__ ones_cnt,
