@@ -104,7 +104,8 @@ void orc_sample_assign3d(const double *p, int64_t n, const double *cost, uint64_
  * equalities.  relax = 0 restores the original senses. */
 int orc_set_relax(orc_ctx *o, int relax);
 /* Repair (reading R26): per lane, drop 1-entries in order of decreasing cost (ties: lower index
- * first) while every row keeps sum K_ji x_i >= r_j; needs the relaxation. */
+ * first) while every row keeps sum K_ji x_i >= r_j; needs the relaxation.  Lanes with more than
+ * 8192 1-entries are left unchanged (bounded repair, R26). */
 int orc_repair(const orc_ctx *o, uint64_t *bits, int64_t n_words);
 /* canonical (minimisation) cost vector c (n entries) of a loaded problem */
 void orc_canonical_c(const orc_ctx *o, double *c);

@@ -83,3 +83,21 @@ def test_relax_errors(gf):
     s2, _ = _solver(gf, G.assignment3d(3, 1))
     with pytest.raises(gf.GforsError, match="repair"):
         s2.run(max_iters=20, repair=1)
+
+
+def test_repair_leaves_oversized_lanes(gf):
+    """Reading R26: a lane with more than 8192 1-entries is not repaired (GPU and oracle alike); the
+    other lanes of the batch are."""
+    n = 21  # 9261 variables
+    inst = G.assignment3d(n, 4)
+    s, o = _solver(gf, inst)
+    o.set_relax(1)
+    rng = np.random.default_rng(5)
+    bits = O.sample(np.full(n ** 3, 0.02), 9, 1, 0, 1)
+    bits[:, 0] |= np.uint64(1)  # lane 0: all 9261 entries
+    a = s.repair(bits)
+    b = o.repair(bits)
+    assert np.array_equal(a, b)
+    assert np.all((a[:, 0] & np.uint64(1)) == np.uint64(1))  # lane 0 untouched
+    assert not np.array_equal(a, bits)
+    del rng
