@@ -112,3 +112,51 @@ def test_configs_2_3_4_full_size(gf, cfg):
     if not math.isinf(z):
         f, zz = o.eval_point(xbest)
         assert f and zz == (-z if inst["maximize"] else z)
+
+
+def test_config7_tu_fullsize_lift_consistency(gf):
+    """Facility location 512 x 2048 (next row f2) with TUReformulate at full size: for sampled lanes of
+    the reduced problem, the GPU's feasibility and objective equal the oracle's evaluation of the
+    lifted point x_I = 1 - sum_{i != i_j} y_ij on the ORIGINAL rows (exactness of the theorem)."""
+    inst = G.make_config(7, 1)
+    s = gf.Solver(0)
+    s.load(inst)
+    s.tu_reformulate(inst["tu_rows"], inst["tu_cols"])
+    s.preprocess(precision=32)
+    n = inst["n"]
+    keep = np.setdiff1d(np.arange(n), inst["tu_cols"])
+    assert s.n == keep.size
+    rng = np.random.default_rng(3)
+    p = np.where(rng.random(keep.size) < 0.999, 0.0, 1.0)  # sparse assignments: some lanes feasible
+    p[: 512] = 1.0  # open every facility
+    bits = O.sample(p, 5, 0, 0, 2)
+    feas, z = s.eval(bits)
+    o = O.Oracle(inst)
+    nf, nc = 512, 2048
+    for lane in (0, 1, 77, 127):
+        xr = ((bits[:, lane // 64] >> np.uint64(lane % 64)) & np.uint64(1)).astype(np.uint8)
+        x = np.zeros(n, dtype=np.int64)
+        x[keep] = xr
+        y = x[nf:].reshape(nc, nf)
+        for j, col in enumerate(inst["tu_cols"]):
+            x[col] = 1 - (y[j].sum() - y[j, col - nf - j * nf])
+        f, zz = o.eval_point(np.clip(x, 0, 1).astype(np.uint8))
+        ok_bin = np.all((x >= 0) & (x <= 1))
+        assert bool(feas[lane]) == (f and ok_bin)
+        if feas[lane]:
+            assert z[lane] == zz
+
+
+def test_config8_assign3d_fullsize_bit_exact(gf):
+    """3D assignment n = 64 (next row f3): one Alg. 4 batch at full size is bit-identical to the
+    oracle's, and every lane is feasible."""
+    inst = G.make_config(8, 1)
+    s = gf.Solver(0)
+    s.load(inst)
+    s.preprocess(precision=32)
+    o = O.Oracle(inst)
+    p = G.p_vectors(inst["n"], 2)["mix"]
+    a = s.sample_assign3d(p, 20251030, 17, 0, 2, 64)
+    b = O.sample_assign3d(p, 64, o.canonical_c(), 20251030, 17, 0, 2)
+    assert np.array_equal(a, b)
+    assert s.eval(a)[0].all()
