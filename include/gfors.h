@@ -118,6 +118,10 @@ typedef struct {
      * rows stay >= before EvalBest (lanes with > 8192 entries are left as they are). */
     int32_t relax;
     int32_t repair;
+    /* complete = 1: cover completion before EvalBest (R27): every covering
+     * row (>=, coefficients 1, rhs 1) a lane violates gets its largest-x_k variable (ties: lowest
+     * index) switched on in that lane; decisions on the batch as sampled (order-free).  One rank. */
+    int32_t complete;
 } gfors_params;
 
 /* halt_reason: 1 criteria met, 2 max_iters, 3 time limit, 4 diverged. */
@@ -165,6 +169,8 @@ gfors_status gfors_sample_assign3d(gfors_ctx *ctx, const double *p, uint64_t see
 /* Test hooks of f4: the relaxation for gfors_step / gfors_indicators (0/1), and the repair of a
  * host batch in place (bits as gfors_sample, n_words words per variable; needs relax = 1). */
 gfors_status gfors_set_relax(gfors_ctx *ctx, int32_t relax);
+/* Test hook: cover completion (complete = 1) of a host batch in place, p host (n entries). */
+gfors_status gfors_cover_complete(gfors_ctx *ctx, const double *p, uint64_t *bits, int64_t n_words);
 gfors_status gfors_repair(gfors_ctx *ctx, uint64_t *bits, int64_t n_words);
 /* Current problem dimensions (reduced after gfors_tu_reformulate) and the original n. */
 gfors_status gfors_dims(gfors_ctx *ctx, int64_t *n, int64_t *m, int64_t *n_orig);

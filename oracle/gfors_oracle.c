@@ -730,6 +730,38 @@ int orc_repair(const orc_ctx *o, uint64_t *bits, int64_t n_words) {
     return 0;
 }
 
+/* Cover completion (reading R27): in each lane, every covering row (>= row, all
+ * coefficients 1, right-hand side 1) that the lane violates gets its variable with the largest p
+ * (ties: lowest index) switched on; all decisions are taken on the batch as passed in. */
+int orc_cover_complete(const orc_ctx *o, const double *p, uint64_t *bits, int64_t n_words) {
+    const int64_t m1 = o->m1;
+    int64_t *best = (int64_t *)malloc((size_t)(m1 ? m1 : 1) * sizeof(int64_t));
+    char *elig = (char *)calloc((size_t)(m1 ? m1 : 1), 1);
+    for (int64_t j = 0; j < m1; ++j) {
+        int ok = o->ru[j] == 1.0 && o->Ku.ptr[j + 1] > o->Ku.ptr[j];
+        for (int64_t q = o->Ku.ptr[j]; q < o->Ku.ptr[j + 1] && ok; ++q) ok = o->Ku.val[q] == 1.0;
+        elig[j] = (char)ok;
+        best[j] = -1;
+        if (!ok) continue;
+        for (int64_t q = o->Ku.ptr[j]; q < o->Ku.ptr[j + 1]; ++q) {
+            const int64_t i = o->Ku.idx[q];
+            if (best[j] < 0 || p[i] > p[best[j]] || (p[i] == p[best[j]] && i < best[j])) best[j] = i;
+        }
+    }
+    uint64_t *add = (uint64_t *)calloc((size_t)(o->n * n_words), sizeof(uint64_t));
+    for (int64_t j = 0; j < m1; ++j) {
+        if (!elig[j]) continue;
+        for (int64_t w = 0; w < n_words; ++w) {
+            uint64_t covered = 0;
+            for (int64_t q = o->Ku.ptr[j]; q < o->Ku.ptr[j + 1]; ++q) covered |= bits[o->Ku.idx[q] * n_words + w];
+            add[best[j] * n_words + w] |= ~covered;
+        }
+    }
+    for (int64_t t = 0; t < o->n * n_words; ++t) bits[t] |= add[t];
+    free(best); free(elig); free(add);
+    return 0;
+}
+
 void orc_canonical_c(const orc_ctx *o, double *c) {
     for (int64_t i = 0; i < o->n; ++i) c[i] = o->c[i];
 }
@@ -845,7 +877,7 @@ void orc_params_default(orc_params *p) {
     p->stall_rel = 1e-8; p->stall_window = 50;
     p->max_iters = 100000; p->time_limit_s = 1800.0; p->seed = 20251030ull;
     p->sampler = 0; p->a3_ls = -1; p->a3_n = 0; p->a3_gamma = 4.0;  /* SPEC L381 */
-    p->relax = 0; p->repair = 0;
+    p->relax = 0; p->repair = 0; p->complete = 0;
 }
 
 static double now_s(void) {
@@ -922,6 +954,7 @@ int orc_run(orc_ctx *o, const orc_params *p, orc_run_info *info,
                 else
                     orc_sample(o->x, n, p->seed, (uint32_t)round_id, 0, n_words, bits);
                 if (p->repair) orc_repair(o, bits, n_words);
+                if (p->complete) orc_cover_complete(o, o->x, bits, n_words);
                 improved |= eval_best(o, bits, n_words, 0, k, round_id, feas, z);
                 rounds++;
             }

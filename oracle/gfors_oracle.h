@@ -107,6 +107,10 @@ int orc_set_relax(orc_ctx *o, int relax);
  * first) while every row keeps sum K_ji x_i >= r_j; needs the relaxation.  Lanes with more than
  * 8192 1-entries are left unchanged (bounded repair, R26). */
 int orc_repair(const orc_ctx *o, uint64_t *bits, int64_t n_words);
+/* Cover completion (R27): each covering row (>=, coefficients 1, rhs 1) violated by a
+ * lane gets its variable with the largest p (ties: lowest index) switched on in that lane; the
+ * decisions are all taken on the batch as passed in (order-free). */
+int orc_cover_complete(const orc_ctx *o, const double *p, uint64_t *bits, int64_t n_words);
 /* canonical (minimisation) cost vector c (n entries) of a loaded problem */
 void orc_canonical_c(const orc_ctx *o, double *c);
 
@@ -144,6 +148,7 @@ typedef struct {
     double a3_gamma;        /* Alg. 4 gamma (default 4) */
     int32_t relax;          /* monotone relaxation: equality rows act as >= in PDHG */
     int32_t repair;         /* per-lane greedy repair before EvalBest (needs relax) */
+    int32_t complete;       /* cover completion of the sampled lanes before EvalBest (R27) */
 } orc_params;
 void orc_params_default(orc_params *p);
 typedef struct {

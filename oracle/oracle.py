@@ -52,7 +52,7 @@ class OrcParams(C.Structure):
                 ("tol_primal", D), ("tol_dual", D), ("tol_binary", D), ("stall_rel", D),
                 ("stall_window", C.c_int32), ("max_iters", I64), ("time_limit_s", D), ("seed", C.c_uint64),
                 ("sampler", C.c_int32), ("a3_ls", C.c_int32), ("a3_n", I64), ("a3_gamma", D),
-                ("relax", C.c_int32), ("repair", C.c_int32)]
+                ("relax", C.c_int32), ("repair", C.c_int32), ("complete", C.c_int32)]
 
 
 class OrcRunInfo(C.Structure):
@@ -91,6 +91,7 @@ def _declare(L):
     L.orc_canonical_c.argtypes = [P, P]
     L.orc_set_relax.argtypes = [P, C.c_int]
     L.orc_repair.argtypes = [P, P, I64]
+    L.orc_cover_complete.argtypes = [P, P, P, I64]
     L.orc_eval.argtypes = [P, P, I64, P, P]
     L.orc_eval_point.argtypes = [P, P, P, P]
     L.orc_halt_init.argtypes = [C.POINTER(OrcHaltState), D, D, D, D, C.c_int]
@@ -262,6 +263,12 @@ class Oracle:
     def repair(self, bits):
         bits = np.array(bits, dtype=np.uint64, copy=True)
         self._chk(lib().orc_repair(self.h, _ptr(bits), bits.shape[1]))
+        return bits
+
+    def cover_complete(self, p, bits):
+        p = np.ascontiguousarray(p, dtype=np.float64)
+        bits = np.array(bits, dtype=np.uint64, copy=True)
+        self._chk(lib().orc_cover_complete(self.h, _ptr(p), _ptr(bits), bits.shape[1]))
         return bits
 
     def canonical_c(self):

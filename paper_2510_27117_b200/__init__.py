@@ -64,7 +64,7 @@ class Params(C.Structure):
                 ("stall_window", I32), ("max_iters", I64), ("time_limit_s", D), ("seed", U64),
                 ("use_graph", I32), ("trace_cap", I32),
                 ("sampler", I32), ("a3_ls", I32), ("a3_n", I64), ("a3_gamma", D),
-                ("relax", I32), ("repair", I32)]
+                ("relax", I32), ("repair", I32), ("complete", I32)]
 
 
 class RunInfo(C.Structure):
@@ -105,6 +105,7 @@ EXPORTS = {
     "gfors_sample_assign3d": (I32, [P, P, U64, C.c_uint32, I64, I64, I64, D, I64, P]),
     "gfors_set_relax": (I32, [P, I32]),
     "gfors_repair": (I32, [P, P, I64]),
+    "gfors_cover_complete": (I32, [P, P, P, I64]),
     "gfors_nccl_unique_id": (I32, [P]),
     "gfors_graph_note": (C.c_char_p, [P]),
 }
@@ -282,6 +283,12 @@ class Solver:
     def repair(self, bits):
         bits = np.array(bits, dtype=np.uint64, copy=True)
         self._chk(_lib.gfors_repair(self.h, _ptr(bits), bits.shape[1]))
+        return bits
+
+    def cover_complete(self, p, bits):
+        p = np.ascontiguousarray(p, dtype=np.float64)
+        bits = np.array(bits, dtype=np.uint64, copy=True)
+        self._chk(_lib.gfors_cover_complete(self.h, _ptr(p), _ptr(bits), bits.shape[1]))
         return bits
 
     def eval(self, bits):

@@ -36,6 +36,7 @@
 #include "dense_q.cuh"
 #include "assign3d.cuh"
 #include "repair.cuh"
+#include "cover.cuh"
 #include <cudaTypedefs.h>
 #include <cstdlib>
 
@@ -353,6 +354,12 @@ struct gfors_ctx {
     long long n = 0, m = 0, m1 = 0, m2 = 0, nnz = 0, qnnz = 0;
     long long m1p = 0;      // rows [0,m1p) are inequalities for the PDHG step (m under the relaxation, R26)
     bool repair = false;    // repair lanes before EvalBest (repair.cuh)
+    bool complete = false;  // cover completion before EvalBest (cover.cuh)
+    int* d_cover_rows = nullptr;      // eligible covering rows (prep-owned, built on first use)
+    long long n_cover = -1;
+    int* d_cover_best = nullptr;
+    uint64_t* d_cover_viol = nullptr;
+    long long cover_viol_len = 0;
     bool maximize = false, integral = false, hasq = false;
     double c0 = 0.0;
     std::vector<int64_t> kptr, ktptr, qptr;
@@ -579,9 +586,12 @@ void gfors_ctx::free_prep() {
                    (void**)&d_part2, (void**)&d_hist, (void**)&d_rho, (void**)&d_trace, (void**)&d_xbest,
                    (void**)&d_X, (void**)&d_viol, (void**)&d_iacc, &d_zpart, (void**)&d_z, (void**)&d_ctrl,
                    (void**)&d_qx, (void**)&d_qdx, (void**)&d_qxpart, (void**)&d_Xs, (void**)&d_qacc,
-                   (void**)&d_qxpart2, (void**)&d_qreuse};
+                   (void**)&d_qxpart2, (void**)&d_qreuse, (void**)&d_cover_rows, (void**)&d_cover_best,
+                   (void**)&d_cover_viol};
     for (void** p : ps) { dfree(*p); *p = nullptr; }
     X_words = iacc_len = zpart_len = z_len = Xs_lanes = 0;
+    n_cover = -1;
+    cover_viol_len = 0;
     for (int b = 0; b < 2; ++b) { dfree(a3.keys[b]); dfree(a3.vals[b]); }
     for (void* q : {(void*)a3.tmp, (void*)a3.sj0, (void*)a3.sk0, (void*)a3.Ri, (void*)a3.Rj, (void*)a3.Rk,
                     (void*)a3.meta, (void*)a3.used})
@@ -1197,6 +1207,42 @@ void set_relax(gfors_ctx* C, int relax, int repair) {
     C->repair = repair != 0;
 }
 
+// cover completion (cover.cuh, R27): eligible rows built once, phase buffers sized for W
+void set_complete(gfors_ctx* C, int complete, int W) {
+    C->complete = complete != 0;
+    if (!complete) return;
+    if (C->sharded) input_error("params.complete: not with the NCCL-sharded loop (winner regeneration)");
+    if (C->n_cover < 0) {
+        std::vector<int> rows;
+        for (long long j = 0; j < C->m1; ++j) {
+            bool ok = C->ru[j] == 1.0 && C->kptr[j + 1] > C->kptr[j];
+            for (long long q = C->kptr[j]; q < C->kptr[j + 1] && ok; ++q) ok = C->kval[q] == 1.0;
+            if (ok) rows.push_back((int)j);
+        }
+        C->n_cover = (long long)rows.size();
+        dfree(C->d_cover_rows);
+        C->d_cover_rows = dupload(rows, C->stream);
+        dfree(C->d_cover_best);
+        C->d_cover_best = dalloc<int>(std::max<long long>(C->n_cover, 1));
+        C->gvalid = false;
+    }
+    if (C->n_cover * (long long)W > C->cover_viol_len) {
+        dfree(C->d_cover_viol);
+        C->d_cover_viol = dalloc<uint64_t>(std::max<long long>(C->n_cover * (long long)W, 1));
+        C->cover_viol_len = C->n_cover * (long long)W;
+        C->gvalid = false;
+    }
+}
+
+template <typename T>
+void enqueue_cover(gfors_ctx* C, cudaStream_t s, const double* pfix, int W, long long kint) {
+    if (C->n_cover <= 0) return;
+    LAUNCH(C, s, KC_SAMPLE, (k_cover_scan<T><<<grid_for(C->n_cover * 32LL), NT, 0, s>>>(csr_K(C), C->d_cover_rows, C->n_cover,
+        (const T*)C->d_x[0], (const T*)C->d_x[1], pfix, C->d_ctrl, kint, C->d_X, W, C->d_cover_best, C->d_cover_viol)));
+    LAUNCH(C, s, KC_SAMPLE, (k_cover_apply<<<grid_for(C->n_cover * (long long)W), NT, 0, s>>>(C->n_cover, C->d_cover_best,
+        C->d_cover_viol, W, ~0ull, C->d_X)));
+}
+
 void enqueue_repair(gfors_ctx* C, cudaStream_t s, int W) {
     const size_t sm = rp_smem_bytes(C->m);
     KIND_SWITCH(C->kkind, {
@@ -1303,6 +1349,7 @@ void enqueue_block(gfors_ctx* C, cudaStream_t s, const gfors_params* p, int W, H
         enqueue_reset(C, s, W, ~0ull);
         enqueue_sample<T>(C, s, nullptr, W, word_off, p->seed, kint, r, p->k_r, 0u, 0);
         if (C->repair) enqueue_repair(C, s, W);
+        if (C->complete) enqueue_cover<T>(C, s, nullptr, W, kint);
         // the trigger pass of this block counted the p = 1 entries of every row (rb path)
         enqueue_eval(C, s, W, (C->m > 0 && C->pd.rb) ? C->d_ones : nullptr);
         if (C->sharded) {
@@ -1580,7 +1627,7 @@ static bool same_graph_key(const gfors_params& a, const gfors_params& b) {
            a.tol_dual == b.tol_dual && a.tol_binary == b.tol_binary && a.stall_rel == b.stall_rel &&
            a.stall_window == b.stall_window && a.seed == b.seed && a.trace_cap == b.trace_cap &&
            a.sampler == b.sampler && a.a3_n == b.a3_n && a.a3_gamma == b.a3_gamma && a.a3_ls == b.a3_ls &&
-           a.relax == b.relax && a.repair == b.repair;
+           a.relax == b.relax && a.repair == b.repair && a.complete == b.complete;
 }
 
 template <typename T>
@@ -1607,6 +1654,7 @@ static void do_run_t(gfors_ctx* C, const gfors_params* p, gfors_run_info* out) {
     ensure_batch(C, W);
     set_sampler(C, p->sampler, p->a3_n, p->a3_gamma, p->a3_ls);
     set_relax(C, p->relax, p->repair);
+    set_complete(C, p->complete, W);
     const long long max_blocks = p->max_iters / p->k_int;
     const long long tail = p->max_iters % p->k_int;
     // rho table (host pow, like the oracle; reading R7)
@@ -1796,7 +1844,7 @@ void gfors_params_default(gfors_params* p) {
     p->tol_primal = 1e-6; p->tol_dual = 1e-6; p->tol_binary = 1e-6; p->stall_rel = 1e-8; p->stall_window = 50;
     p->max_iters = 100000; p->time_limit_s = 1800.0; p->seed = 20251030ull; p->use_graph = 1; p->trace_cap = 4096;
     p->sampler = 0; p->a3_ls = -1; p->a3_n = 0; p->a3_gamma = 4.0;
-    p->relax = 0; p->repair = 0;
+    p->relax = 0; p->repair = 0; p->complete = 0;
 }
 
 void gfors_prep_opts_default(gfors_prep_opts* p) {
@@ -1993,6 +2041,23 @@ gfors_status gfors_repair(gfors_ctx* C, uint64_t* bits, int64_t n_words) {
     API_END(C)
 }
 
+gfors_status gfors_cover_complete(gfors_ctx* C, const double* p, uint64_t* bits, int64_t n_words) {
+    API_BEGIN(C)
+    if (C->stage < 2) throw Err{GFORS_E_STATE, "gfors_cover_complete: call gfors_preprocess first"};
+    if (!p || !bits || n_words < 1 || n_words > (1 << 14)) input_error("gfors_cover_complete: p, bits and 1 <= n_words <= 16384 required");
+    ensure_batch(C, (int)n_words);
+    set_complete(C, 1, (int)n_words);
+    cudaStream_t s = C->stream;
+    double* dp = C->d_tmp[3];
+    CK(cudaMemcpyAsync(dp, p, C->n * sizeof(double), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(C->d_X, bits, C->n * n_words * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+    if (C->precision == 64) enqueue_cover<double>(C, s, dp, (int)n_words, 1); else enqueue_cover<float>(C, s, dp, (int)n_words, 1);
+    CK(cudaMemcpyAsync(bits, C->d_X, C->n * n_words * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    C->complete = false;
+    API_END(C)
+}
+
 gfors_status gfors_eval(gfors_ctx* C, const uint64_t* bits, int64_t n_words, uint8_t* feasible, double* z) {
     API_BEGIN(C)
     if (C->stage < 1) throw Err{GFORS_E_STATE, "gfors_eval: call gfors_load first"};
@@ -2109,6 +2174,7 @@ int64_t gfors_launches_per_block(gfors_ctx* C, const gfors_params* p) {
     try {
         set_sampler(C, p->sampler, p->a3_n, p->a3_gamma, p->a3_ls);
         set_relax(C, p->relax, p->repair);
+    set_complete(C, p->complete, W);
         if (C->precision == 64) enqueue_block<double>(C, C->stream, p, W, hp, cudaGraphConditionalHandle{}, 0);
         else enqueue_block<float>(C, C->stream, p, W, hp, cudaGraphConditionalHandle{}, 0);
         n = C->launches;
