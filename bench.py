@@ -491,7 +491,7 @@ def run_gpu(args):
         e2 = torch.cuda.Event(enable_timing=True)
         e3 = torch.cuda.Event(enable_timing=True)
         e2.record(stream)
-        ic = s.run(max_iters=1000, **dict(common, complete=1))
+        ic = s.run(max_iters=1000, **dict(common, complete=1, trace_cap=1000))
         e3.record(stream)
         torch.cuda.synchronize()
         zc, _, mc = s.best_incumbent(want_x=False)

@@ -16,8 +16,8 @@
 
 namespace gfors {
 
-// phase 1: one warp per eligible row
-template <typename T>
+// phase 1: SUB lanes per eligible row (rows of set cover have 2..98 entries)
+template <typename T, int SUB>
 __global__ void __launch_bounds__(256) k_cover_scan(Csr K, const int* __restrict__ rows, long long nrows,
                                                     const T* __restrict__ xa, const T* __restrict__ xb2,
                                                     const double* __restrict__ pfix, const Ctrl* __restrict__ ctrl,
@@ -28,17 +28,24 @@ __global__ void __launch_bounds__(256) k_cover_scan(Csr K, const int* __restrict
         const long long b = ctrl->blk;
         p = (((b + 1) * kint) & 1) ? xb2 : xa;  // x_k of the block (as k_sample)
     }
-    const int lane = threadIdx.x & 31;
+    constexpr int RPW = 32 / SUB;
+    const int lane = threadIdx.x & (SUB - 1);
+    const int gsub = (threadIdx.x & 31) / SUB;
     const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = (gridDim.x * (long long)blockDim.x) >> 5;
-    for (long long e = warp; e < nrows; e += nwarps) {
-        const int row = rows[e];
-        const long long q0 = __ldg(K.ptr + row), q1 = __ldg(K.ptr + row + 1);
+    for (long long base = warp * RPW; base < nrows; base += nwarps * RPW) {  // warp-uniform trip count
+        const long long e = base + gsub;
+        const bool valid = e < nrows;
+        long long q0 = 0, q1 = 0;
+        if (valid) {
+            const int row = rows[e];
+            q0 = __ldg(K.ptr + row); q1 = __ldg(K.ptr + row + 1);
+        }
         double bp = -1.0;
         int bi = 0x7fffffff;
         for (int w0 = 0; w0 < W; w0 += 4) {
             uint64_t o[4] = {0ull, 0ull, 0ull, 0ull};
-            for (long long q = q0 + lane; q < q1; q += 32) {
+            for (long long q = q0 + lane; q < q1; q += SUB) {
                 const int i = __ldg(K.idx + q);
                 if (w0 == 0) {
                     const double pv = pfix ? pfix[i] : (double)p[i];
@@ -51,17 +58,17 @@ __global__ void __launch_bounds__(256) k_cover_scan(Csr K, const int* __restrict
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
 #pragma unroll
-                for (int off = 16; off > 0; off >>= 1) o[u] |= __shfl_xor_sync(0xffffffffu, o[u], off);
-                if (lane == 0 && w0 + u < W) viol[e * W + w0 + u] = ~o[u];
+                for (int off = SUB / 2; off > 0; off >>= 1) o[u] |= __shfl_xor_sync(0xffffffffu, o[u], off, SUB);
+                if (lane == 0 && valid && w0 + u < W) viol[e * W + w0 + u] = ~o[u];
             }
         }
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            const double op = __shfl_xor_sync(0xffffffffu, bp, off);
-            const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+        for (int off = SUB / 2; off > 0; off >>= 1) {
+            const double op = __shfl_xor_sync(0xffffffffu, bp, off, SUB);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, off, SUB);
             if (op > bp || (op == bp && oi < bi)) { bp = op; bi = oi; }
         }
-        if (lane == 0) best[e] = q1 > q0 ? bi : -1;
+        if (lane == 0 && valid) best[e] = q1 > q0 ? bi : -1;
     }
 }
 

@@ -1237,7 +1237,7 @@ void set_complete(gfors_ctx* C, int complete, int W) {
 template <typename T>
 void enqueue_cover(gfors_ctx* C, cudaStream_t s, const double* pfix, int W, long long kint) {
     if (C->n_cover <= 0) return;
-    LAUNCH(C, s, KC_SAMPLE, (k_cover_scan<T><<<grid_for(C->n_cover * 32LL), NT, 0, s>>>(csr_K(C), C->d_cover_rows, C->n_cover,
+    LAUNCH(C, s, KC_SAMPLE, (k_cover_scan<T, 8><<<grid_for(C->n_cover * 8LL), NT, 0, s>>>(csr_K(C), C->d_cover_rows, C->n_cover,
         (const T*)C->d_x[0], (const T*)C->d_x[1], pfix, C->d_ctrl, kint, C->d_X, W, C->d_cover_best, C->d_cover_viol)));
     LAUNCH(C, s, KC_SAMPLE, (k_cover_apply<<<grid_for(C->n_cover * (long long)W), NT, 0, s>>>(C->n_cover, C->d_cover_best,
         C->d_cover_viol, W, ~0ull, C->d_X)));
