@@ -524,6 +524,10 @@ def run_gpu(args):
         tj = json.load(open(tpath))
         traffic = tj.get(f"config{args.config}_fp{args.precision}", {}).get(dom)
 
+    # the device-resident solver is done: release its memory before the e2e leg allocates its own
+    s.close()
+    torch.cuda.synchronize()
+
     # e2e through the public API from pinned host buffers
     e2e = None
     if not args.no_e2e and rank == 0 or (world > 1 and not args.no_e2e):

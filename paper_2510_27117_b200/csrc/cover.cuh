@@ -22,7 +22,8 @@ __global__ void __launch_bounds__(256) k_cover_scan(Csr K, const int* __restrict
                                                     const T* __restrict__ xa, const T* __restrict__ xb2,
                                                     const double* __restrict__ pfix, const Ctrl* __restrict__ ctrl,
                                                     long long kint, const uint64_t* __restrict__ X, int W,
-                                                    int* __restrict__ best, uint64_t* __restrict__ viol) {
+                                                    int* __restrict__ best, uint64_t* __restrict__ viol,
+                                                    const unsigned char* __restrict__ ones) {
     const T* __restrict__ p = nullptr;
     if (!pfix) {
         const long long b = ctrl->blk;
@@ -40,7 +41,11 @@ __global__ void __launch_bounds__(256) k_cover_scan(Csr K, const int* __restrict
         if (valid) {
             const int row = rows[e];
             q0 = __ldg(K.ptr + row); q1 = __ldg(K.ptr + row + 1);
+            // a variable with p = 1 (counted by the block's trigger pass) covers the row in every
+            // lane: nothing violated, no gathers (same result)
+            if (ones && ones[row] >= 1) { q1 = q0; }
         }
+        const bool covered_all = valid && ones && q1 == q0 && ones[rows[e]] >= 1;
         double bp = -1.0;
         int bi = 0x7fffffff;
         for (int w0 = 0; w0 < W; w0 += 4) {
@@ -59,7 +64,7 @@ __global__ void __launch_bounds__(256) k_cover_scan(Csr K, const int* __restrict
             for (int u = 0; u < 4; ++u) {
 #pragma unroll
                 for (int off = SUB / 2; off > 0; off >>= 1) o[u] |= __shfl_xor_sync(0xffffffffu, o[u], off, SUB);
-                if (lane == 0 && valid && w0 + u < W) viol[e * W + w0 + u] = ~o[u];
+                if (lane == 0 && valid && w0 + u < W) viol[e * W + w0 + u] = covered_all ? 0ull : ~o[u];
             }
         }
 #pragma unroll

@@ -1235,10 +1235,11 @@ void set_complete(gfors_ctx* C, int complete, int W) {
 }
 
 template <typename T>
-void enqueue_cover(gfors_ctx* C, cudaStream_t s, const double* pfix, int W, long long kint) {
+void enqueue_cover(gfors_ctx* C, cudaStream_t s, const double* pfix, int W, long long kint,
+                   const unsigned char* ones = nullptr) {
     if (C->n_cover <= 0) return;
     LAUNCH(C, s, KC_SAMPLE, (k_cover_scan<T, 8><<<grid_for(C->n_cover * 8LL), NT, 0, s>>>(csr_K(C), C->d_cover_rows, C->n_cover,
-        (const T*)C->d_x[0], (const T*)C->d_x[1], pfix, C->d_ctrl, kint, C->d_X, W, C->d_cover_best, C->d_cover_viol)));
+        (const T*)C->d_x[0], (const T*)C->d_x[1], pfix, C->d_ctrl, kint, C->d_X, W, C->d_cover_best, C->d_cover_viol, ones)));
     LAUNCH(C, s, KC_SAMPLE, (k_cover_apply<<<grid_for(C->n_cover * (long long)W), NT, 0, s>>>(C->n_cover, C->d_cover_best,
         C->d_cover_viol, W, ~0ull, C->d_X)));
 }
@@ -1349,7 +1350,7 @@ void enqueue_block(gfors_ctx* C, cudaStream_t s, const gfors_params* p, int W, H
         enqueue_reset(C, s, W, ~0ull);
         enqueue_sample<T>(C, s, nullptr, W, word_off, p->seed, kint, r, p->k_r, 0u, 0);
         if (C->repair) enqueue_repair(C, s, W);
-        if (C->complete) enqueue_cover<T>(C, s, nullptr, W, kint);
+        if (C->complete) enqueue_cover<T>(C, s, nullptr, W, kint, (C->m > 0 && C->pd.rb) ? C->d_ones : nullptr);
         // the trigger pass of this block counted the p = 1 entries of every row (rb path)
         enqueue_eval(C, s, W, (C->m > 0 && C->pd.rb) ? C->d_ones : nullptr);
         if (C->sharded) {
