@@ -120,7 +120,9 @@ typedef struct {
     int32_t repair;
     /* complete = 1: cover completion before EvalBest (R27): every covering
      * row (>=, coefficients 1, rhs 1) a lane violates gets its largest-x_k variable (ties: lowest
-     * index) switched on in that lane; decisions on the batch as sampled (order-free).  One rank. */
+     * index) switched on in that lane; decisions on the batch as sampled (order-free).  One rank
+ * (repair, complete and sampler 1 are rejected with the NCCL-sharded loop: its winner regeneration
+ * replays the Bernoulli contract). */
     int32_t complete;
 } gfors_params;
 

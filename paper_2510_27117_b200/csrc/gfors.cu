@@ -235,9 +235,9 @@ DirPlan plan_direction64(const DirPlan& d32, const std::vector<int64_t>& ptr, lo
 }
 
 const char* kClassNames[] = {"pdhg_dual", "pdhg_primal", "trig_rows", "trig_cols", "sample", "feas", "obj",
-                             "argmin", "halt", "pdhg_dual_push", "pdhg_primal_push", "pdhg_qx", "obj_tc"};
+                             "argmin", "halt", "pdhg_dual_push", "pdhg_primal_push", "pdhg_qx", "obj_tc", "cover"};
 enum KClass { KC_DUAL = 0, KC_PRIMAL, KC_TRIGR, KC_TRIGC, KC_SAMPLE, KC_FEAS, KC_OBJ, KC_ARGMIN, KC_HALT, KC_DUAL_PUSH,
-              KC_PRIMAL_PUSH, KC_QX, KC_OBJ_TC, KC_N };
+              KC_PRIMAL_PUSH, KC_QX, KC_OBJ_TC, KC_COVER, KC_N };
 
 }  // namespace
 
@@ -1238,9 +1238,9 @@ template <typename T>
 void enqueue_cover(gfors_ctx* C, cudaStream_t s, const double* pfix, int W, long long kint,
                    const unsigned char* ones = nullptr) {
     if (C->n_cover <= 0) return;
-    LAUNCH(C, s, KC_SAMPLE, (k_cover_scan<T, 8><<<grid_for(C->n_cover * 8LL), NT, 0, s>>>(csr_K(C), C->d_cover_rows, C->n_cover,
+    LAUNCH(C, s, KC_COVER, (k_cover_scan<T, 8><<<grid_for(C->n_cover * 8LL), NT, 0, s>>>(csr_K(C), C->d_cover_rows, C->n_cover,
         (const T*)C->d_x[0], (const T*)C->d_x[1], pfix, C->d_ctrl, kint, C->d_X, W, C->d_cover_best, C->d_cover_viol, ones)));
-    LAUNCH(C, s, KC_SAMPLE, (k_cover_apply<<<grid_for(C->n_cover * (long long)W), NT, 0, s>>>(C->n_cover, C->d_cover_best,
+    LAUNCH(C, s, KC_COVER, (k_cover_apply<<<grid_for(C->n_cover * (long long)W), NT, 0, s>>>(C->n_cover, C->d_cover_best,
         C->d_cover_viol, W, ~0ull, C->d_X)));
 }
 
