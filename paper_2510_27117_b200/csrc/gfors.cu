@@ -394,7 +394,6 @@ struct gfors_ctx {
         size_t tmp_bytes = 0;
         short *sj0 = nullptr, *sk0 = nullptr, *Ri = nullptr, *Rj = nullptr, *Rk = nullptr;
         int* meta = nullptr;
-        unsigned char* used = nullptr;
         long long alloc_n = 0;
     } a3;
 
@@ -594,7 +593,7 @@ void gfors_ctx::free_prep() {
     cover_viol_len = 0;
     for (int b = 0; b < 2; ++b) { dfree(a3.keys[b]); dfree(a3.vals[b]); }
     for (void* q : {(void*)a3.tmp, (void*)a3.sj0, (void*)a3.sk0, (void*)a3.Ri, (void*)a3.Rj, (void*)a3.Rk,
-                    (void*)a3.meta, (void*)a3.used})
+                    (void*)a3.meta})
         dfree(q);
     a3 = A3{};
     rho_cap = 0;
@@ -1284,7 +1283,6 @@ void ensure_a3(gfors_ctx* C, long long a3n) {
     A.tmp_bytes = bytes;
     for (short** q : {&A.sj0, &A.sk0, &A.Ri, &A.Rj, &A.Rk}) { dfree(*q); *q = dalloc<short>(a3n); }
     dfree(A.meta); A.meta = dalloc<int>(1);
-    dfree(A.used); A.used = dalloc<unsigned char>(2 * a3n);  // (unused since the shared-memory greedy)
     A.alloc_n = a3n;
     C->gvalid = false;
 }
