@@ -221,3 +221,17 @@ def test_gemv_reuse_across_blocks(gf, kint):
     t0, t1 = res[0][3], res[1][3]
     assert np.array_equal(t0[:, [0, 1, 2, 4, 5, 6, 7]], t1[:, [0, 1, 2, 4, 5, 6, 7]])
     assert np.allclose(t0[:, 3], t1[:, 3], rtol=1e-6, atol=1e-9)  # ||s^x||
+
+
+def test_dense_objective_max_batch(gf):
+    """k_b = 4096 per rank (the dense objective's limit): 16 tcgen05 passes of N = 256, a 4-stage ring
+    next to the 32 KB of lane sums; bit-exact against the oracle."""
+    inst = G.max_cut(300, 0.5, 99)
+    s, _ = _solver(gf, inst)
+    o = O.Oracle(inst)
+    bits = O.sample(G.p_vectors(300, 7)["unif"], 2, 5, 0, 64)
+    fg, zg = s.eval(bits)
+    fo, zo = o.eval(bits)
+    assert np.array_equal(zg, zo)
+    with pytest.raises(gf.GforsError, match="4096"):
+        s.eval(np.zeros((300, 65), dtype=np.uint64))
