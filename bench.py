@@ -524,6 +524,22 @@ def run_gpu(args):
         tj = json.load(open(tpath))
         traffic = tj.get(f"config{args.config}_fp{args.precision}", {}).get(dom)
 
+    # the streaming column pass of the push-mode primal (k_primal_push), the largest non-gather kernel
+    # of the steady state: bytes if every column is streamed (stationary columns are skipped, so
+    # this bounds its algorithmic bytes from above) and the DRAM bytes of its ncu capture
+    col = None
+    if act.get("pdhg_primal_col", (0.0, 0))[1] > 0:
+        col_ms = act["pdhg_primal_col"][0] / act["pdhg_primal_col"][1]
+        sbytes = meta["n"] * (5 * fb + 8 + 1)
+        dram = None
+        if os.path.exists(tpath):
+            dram = json.load(open(tpath)).get(f"config{args.config}_fp{args.precision}", {}).get("pdhg_primal_col")
+        col = {"kernel": "k_primal_push", "avg_active_launch_ms": col_ms, "stream_bytes_per_launch": sbytes,
+               "stream_GBs": sbytes / (col_ms * 1e-3) / 1e9, "stream_frac": sbytes / (col_ms * 1e-3) / 1e9 / peak,
+               "dram_bytes_per_launch_ncu": dram,
+               "dram_GBs": (dram / (col_ms * 1e-3) / 1e9) if dram else None,
+               "dram_frac": (dram / (col_ms * 1e-3) / 1e9 / peak) if dram else None}
+
     # the device-resident solver is done: release its memory before the e2e leg allocates its own
     s.close()
     torch.cuda.synchronize()
@@ -611,6 +627,7 @@ def run_gpu(args):
                          # gathered element; ceiling measured by scratch/gather_bench.cu (profiles/)
                          "gather": {"gathers_per_launch": meta["nnz"], "achieved_G_per_s": meta["nnz"] / (per_launch_ms * 1e-3) / 1e9,
                                     "ceiling_G_per_s": GATHER_CEILING_G, "frac": meta["nnz"] / (per_launch_ms * 1e-3) / 1e9 / GATHER_CEILING_G}},
+            "roofline_push_primal_column_pass": col,
             "kernel_ms_per_step": prof, "kernel_share": {k: v / step_ms for k, v in prof.items()} if step_ms else {},
             "kernel_active": {k: {"active_launches": v[1], "avg_active_ms": (v[0] / v[1]) if v[1] else None}
                               for k, v in act.items()},

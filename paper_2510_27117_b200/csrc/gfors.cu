@@ -235,9 +235,10 @@ DirPlan plan_direction64(const DirPlan& d32, const std::vector<int64_t>& ptr, lo
 }
 
 const char* kClassNames[] = {"pdhg_dual", "pdhg_primal", "trig_rows", "trig_cols", "sample", "feas", "obj",
-                             "argmin", "halt", "pdhg_dual_push", "pdhg_primal_push", "pdhg_qx", "obj_tc", "cover"};
+                             "argmin", "halt", "pdhg_dual_push", "pdhg_primal_push", "pdhg_qx", "obj_tc", "cover",
+                             "pdhg_primal_col"};
 enum KClass { KC_DUAL = 0, KC_PRIMAL, KC_TRIGR, KC_TRIGC, KC_SAMPLE, KC_FEAS, KC_OBJ, KC_ARGMIN, KC_HALT, KC_DUAL_PUSH,
-              KC_PRIMAL_PUSH, KC_QX, KC_OBJ_TC, KC_COVER, KC_N };
+              KC_PRIMAL_PUSH, KC_QX, KC_OBJ_TC, KC_COVER, KC_PRIMAL_COL, KC_N };  // PRIMAL_COL: k_primal_push alone
 
 }  // namespace
 
@@ -964,19 +965,19 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
         auto push = [&](cudaStream_t q) {
             LAUNCH(C, q, KC_PRIMAL_PUSH, (k_push_scatter_cols<T><<<grid_for(C->m * 32LL), NT, 0, q>>>(csr_K(C), ppr, st, ctrl, kint, j)));
             if (C->hasq)
-                LAUNCH(C, q, KC_PRIMAL_PUSH, (k_primal_push<T, true><<<pp_grid<T>(C->n), NT, 0, q>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
+                LAUNCH(C, q, KC_PRIMAL_COL, (k_primal_push<T, true><<<pp_grid<T>(C->n), NT, 0, q>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
                     csr_Kt(C), trig_push ? C->d_accv : nullptr, C->d_ones_cnt, C->d_trig_flag)));
             else if (sizeof(T) == 4 && C->pp_occ == 3)
-                LAUNCH(C, q, KC_PRIMAL_PUSH, (k_primal_push<T, false, 3><<<pp_grid<T>(C->n, 3), NT, 0, q>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
+                LAUNCH(C, q, KC_PRIMAL_COL, (k_primal_push<T, false, 3><<<pp_grid<T>(C->n, 3), NT, 0, q>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
                     csr_Kt(C), trig_push ? C->d_accv : nullptr, C->d_ones_cnt, C->d_trig_flag)));
             else if (sizeof(T) == 4 && C->pp_occ == 6)
-                LAUNCH(C, q, KC_PRIMAL_PUSH, (k_primal_push<T, false, 6><<<pp_grid<T>(C->n, 6), NT, 0, q>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
+                LAUNCH(C, q, KC_PRIMAL_COL, (k_primal_push<T, false, 6><<<pp_grid<T>(C->n, 6), NT, 0, q>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
                     csr_Kt(C), trig_push ? C->d_accv : nullptr, C->d_ones_cnt, C->d_trig_flag)));
             else if (sizeof(T) == 4 && C->pp_occ == 8)
-                LAUNCH(C, q, KC_PRIMAL_PUSH, (k_primal_push<T, false, 8><<<pp_grid<T>(C->n, 8), NT, 0, q>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
+                LAUNCH(C, q, KC_PRIMAL_COL, (k_primal_push<T, false, 8><<<pp_grid<T>(C->n, 8), NT, 0, q>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
                     csr_Kt(C), trig_push ? C->d_accv : nullptr, C->d_ones_cnt, C->d_trig_flag)));
             else
-                LAUNCH(C, q, KC_PRIMAL_PUSH, (k_primal_push<T, false><<<pp_grid<T>(C->n), NT, 0, q>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
+                LAUNCH(C, q, KC_PRIMAL_COL, (k_primal_push<T, false><<<pp_grid<T>(C->n), NT, 0, q>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
                     csr_Kt(C), trig_push ? C->d_accv : nullptr, C->d_ones_cnt, C->d_trig_flag)));
         };
         branch(C, s, [&](cudaStream_t q, cudaGraphConditionalHandle h, int a, int b) {
