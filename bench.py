@@ -433,6 +433,15 @@ def run_gpu(args):
     inst = make_instance(args.config, args.seed)
     meta = inst_meta(inst)
     stream = torch.cuda.current_stream()
+    def fresh_nccl_id():
+        """a new ncclUniqueId made on rank 0 and broadcast (one per communicator: ids are not reused)"""
+        import torch.distributed as dist
+        buf = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            buf.copy_(torch.frombuffer(bytearray(gf.nccl_unique_id()), dtype=torch.uint8).cuda())
+        dist.broadcast(buf, 0)
+        return bytes(buf.cpu().numpy().tobytes())
+
     nccl_id = None
     if world > 1:
         # in-loop incumbent exchange (one 32-byte record per rank per sampling round, ncclAllGather
@@ -556,7 +565,8 @@ def run_gpu(args):
                 h2d += v.nbytes
             else:
                 host[k] = v
-        s2 = gf.Solver(local, stream=stream.cuda_stream, rank=rank, world=world, nccl_id=nccl_id)
+        s2 = gf.Solver(local, stream=stream.cuda_stream, rank=rank, world=world,
+                       nccl_id=fresh_nccl_id() if world > 1 else None)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         s2.load(host)
