@@ -77,17 +77,55 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md recipe)."""
+    """SM clocks + throttle reasons sampled DURING the timed region (B200_PROFILING.md recipe).
+
+    NVML in a background thread every 10 ms (the device is found by UUID, so CUDA_VISIBLE_DEVICES
+    remapping cannot point it at another GPU); only samples inside [region_begin, region_end] count.
+    Falls back to `nvidia-smi -lms 100` when NVML is unavailable."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, gpu_index):
         self.idx = gpu_index
         self.proc = None
+        self.thread = None
+        self.samples = []  # (perf_counter, sm_mhz, max_mhz, reasons)
+        self.t0 = self.t1 = None
+
+    def _nvml_handle(self):
+        import pynvml
+        import torch
+        pynvml.nvmlInit()
+        try:
+            uuid = str(torch.cuda.get_device_properties(self.idx).uuid)
+            return pynvml, pynvml.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.idx)
 
     def start(self):
+        import threading
+        try:
+            nv, h = self._nvml_handle()
+            bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+            mx = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self.stop_flag = threading.Event()
+
+            def loop():
+                while not self.stop_flag.is_set():
+                    sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append((time.perf_counter(), sm, mx,
+                                         [nm for nm, b in zip(self.NAMES, bits) if r & b]))
+                    time.sleep(0.01)
+            self.thread = threading.Thread(target=loop, daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            self.thread = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
@@ -95,13 +133,28 @@ class ClockSampler:
         except Exception:
             self.proc = None
 
+    def region_begin(self):
+        self.t0 = time.perf_counter()
+
+    def region_end(self):
+        self.t1 = time.perf_counter()
+
     def stop(self):
+        if self.thread is not None:
+            self.stop_flag.set()
+            self.thread.join(timeout=5)
+            inside = [s for s in self.samples
+                      if (self.t0 is None or s[0] >= self.t0) and (self.t1 is None or s[0] <= self.t1)]
+            sm = [s[1] for s in inside]
+            reasons = sorted({nm for s in inside for nm in s[3]})
+            return {"sm_mhz": statistics.median(sm) if sm else None,
+                    "sm_max_mhz": self.samples[0][2] if self.samples else None,
+                    "reasons": reasons, "samples": len(sm), "source": "nvml, 10 ms, timed region only"}
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
         out, _ = self.proc.communicate(timeout=10)
         sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in out.strip().splitlines():
             f = [x.strip() for x in line.split(",")]
             if len(f) < 7:
@@ -110,11 +163,11 @@ class ClockSampler:
                 sm.append(float(f[0])); mx = float(f[1])
             except ValueError:
                 continue
-            for nm, v in zip(names, f[3:7]):
+            for nm, v in zip(self.NAMES, f[3:7]):
                 if v.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi -lms 100"}
 
 
 def algorithmic_bytes(inst_meta, fb):
@@ -475,10 +528,12 @@ def run_gpu(args):
     torch.cuda.synchronize()
     clk.start()
     time.sleep(0.3)
+    clk.region_begin()
     e0.record(stream)
     info = s.run(max_iters=args.steps * args.k_int, **common)
     e1.record(stream)
     torch.cuda.synchronize()
+    clk.region_end()
     clocks = clk.stop()
     ms = e0.elapsed_time(e1)
     if world > 1:
