@@ -634,7 +634,8 @@ def run_gpu(args):
         e2e = {"value": args.steps * args.k_b * world / te, "unit": UNIT, "h2d_bytes_per_step": h2d / args.steps,
                "d2h_bytes_per_step": (meta["n"] + 64) / args.steps,
                "note": "one gfors_load+preprocess+run(K blocks)+best_incumbent call chain from pinned host memory; "
-                       "instance bytes amortised over the K steps", "seconds": te}
+                       "instance bytes amortised over the K steps; the device leg before it is its warm-up (the library's "
+                       "device memory pool keeps the memory the closed solver released)", "seconds": te}
 
     # time-to-incumbent (BASELINE metric, third part): full solves of the small configs with the
     # default halting rule, %globaltimer stamp of the last improvement (Preprocess excluded)
