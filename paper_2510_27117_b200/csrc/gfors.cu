@@ -396,7 +396,8 @@ struct gfors_ctx {
     hvec<int32_t> kcol;
     hvec<double> kval;
     std::vector<int32_t> ktrow, qcol;
-    std::vector<double> ktval, qval, ru, c;
+    std::vector<double> ktval, qval, ru;
+    hvec<double> c;  // first touched by the parallel copy in the load
     std::vector<int64_t> perm;
     std::vector<signed char> rsign;
     int kkind = KV_F64;
