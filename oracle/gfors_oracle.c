@@ -712,7 +712,6 @@ int orc_repair(const orc_ctx *o, uint64_t *bits, int64_t n_words) {
         int64_t cnt = 0;
         for (int64_t i = 0; i < n; ++i)
             if (bits[i * n_words + w] & bit) { ones[cnt].c = o->c[i]; ones[cnt].i = i; cnt++; }
-        if (cnt > 8192) continue;  /* reading R26: lanes with more than 8192 entries are not repaired */
         qsort(ones, (size_t)cnt, sizeof(rp_entry), rp_cmp);
         for (int64_t j = 0; j < m; ++j) srow[j] = 0.0;
         for (int64_t t = 0; t < cnt; ++t)

@@ -104,8 +104,8 @@ void orc_sample_assign3d(const double *p, int64_t n, const double *cost, uint64_
  * equalities.  relax = 0 restores the original senses. */
 int orc_set_relax(orc_ctx *o, int relax);
 /* Repair (reading R26): per lane, drop 1-entries in order of decreasing cost (ties: lower index
- * first) while every row keeps sum K_ji x_i >= r_j; needs the relaxation.  Lanes with more than
- * 8192 1-entries are left unchanged (bounded repair, R26). */
+ * first) while every row keeps sum K_ji x_i >= r_j; needs the relaxation.  Every lane is repaired,
+ * whatever its number of 1-entries. */
 int orc_repair(const orc_ctx *o, uint64_t *bits, int64_t n_words);
 /* Cover completion (R27): each covering row (>=, coefficients 1, rhs 1) violated by a
  * lane gets its variable with the largest p (ties: lowest index) switched on in that lane; the

@@ -49,21 +49,39 @@ def test_sample_dyadic_thresholds_closed_form():
             assert int(bits[i, w]) == expect
 
 
-def test_sample_threshold_exactness():
-    """T = ceil(p 2^32): the result only depends on T (p and p' with equal T give equal bits),
-    and p = 1 - 2^-33 still differs from p = 1 only where u = 2^32-1 (never in this draw)."""
-    seed = 99
-    base = np.array([0.3, 0.3 + 1e-12, (1 << 31) / 2**32, ((1 << 31) - 1) / 2**32 + 1e-15])
-    b = O.sample(base, seed, 0, 0, 4)
-    # entries 0 and 1 share T (1e-12 * 2^32 < 1 but both ceil to the same integer)
-    T0 = math.ceil(base[0] * 2**32); T1 = math.ceil(base[1] * 2**32)
-    if T0 == T1:
-        # same threshold but different variable index -> different streams; compare via a copy
-        b2 = O.sample(np.array([base[1], base[1]]), seed, 0, 0, 4)
-        b3 = O.sample(np.array([base[0], base[0]]), seed, 0, 0, 4)
-        assert np.array_equal(b2, b3)
-    # entry 2 (p = 1/2 exactly) and entry 3 (p just above (2^31-1)/2^32) have equal T = 2^31
-    assert math.ceil(base[3] * 2**32) == 1 << 31
+def _uniform(i, w, rnd, seed, b):
+    """u of (variable i, lane 64w+b) assembled from all 32 planes, plane 0 the MSB (App. B)."""
+    u = 0
+    for q in range(16):
+        p0, p1 = _planes(i, w, rnd, seed, q)
+        u = (u << 1) | ((p0 >> b) & 1)
+        u = (u << 1) | ((p1 >> b) & 1)
+    return u
+
+
+def test_sample_non_dyadic_threshold_by_hand():
+    """Bernoulli(p) = [u < ceil(p 2^32)] (reading R10) for NON-dyadic p, where the lazy
+    MSB-first compare has to look past the first planes: every lane is recomputed from the 32 Philox
+    planes (generator pinned by the KAT above) and compared with the integer threshold worked by hand.
+    0.3 * 2^32 = 1288490188.8 -> T = 1288490189; 0.7 -> 3006477107.2 -> 3006477108; 1/3 ->
+    1431655765.33 -> 1431655766; and p = 1288490189 / 2^32 (T exactly, no rounding) gives the same
+    bits as 0.3."""
+    seed, rnd, w0 = 0xDEADBEEF12345, 5, 2
+    T = {0.3: 1288490189, 0.7: 3006477108, 1.0 / 3.0: 1431655766, 1288490189 / 2**32: 1288490189}
+    ps = np.array(list(T))
+    bits = O.sample(ps, seed, rnd, w0, 2)
+    for i, p in enumerate(ps):
+        assert math.ceil(p * 2**32) == T[p]
+        for w in range(2):
+            expect = 0
+            for b in range(64):
+                if _uniform(i, w0 + w, rnd, seed, b) < T[p]:
+                    expect |= 1 << b
+            assert int(bits[i, w]) == expect
+    # equal thresholds -> equal decisions on the same stream (variable 0 at p = 0.3 and at T/2^32)
+    same = O.sample(np.array([0.3]), seed, rnd, w0, 2)
+    exact = O.sample(np.array([1288490189 / 2**32]), seed, rnd, w0, 2)
+    assert np.array_equal(same, exact)
 
 
 def test_sample_constant_and_statistics():
@@ -497,3 +515,127 @@ def test_run_deterministic():
         outs.append(o.run(max_iters=300, trace_max=100))
     assert np.array_equal(outs[0]["trace"], outs[1]["trace"])
     assert outs[0]["z_best"] == outs[1]["z_best"]
+
+
+def _alg1_by_hand(inst, prm, alt=None):
+    """Alg. 1 written out from the paper for a few blocks, using only primitives
+    pinned elsewhere in this file (Alg. 2 step, sampler, EvalBest): ρ from the closed form of
+    PAPER L28-31 with n advancing once per block (R7) and ρ_{-1} = ρ_min (R8); x_k sampled after the
+    k-th step; round_id = (k/k_int - 1)·k_r + r (R19); best lane = min z, ties lowest index, replace
+    iff strictly better (R11).  `alt` switches in one plausible orchestration mistake."""
+    o = O.Oracle(inst)
+    o.preprocess()
+    o.state_init()
+    tau = math.sqrt(prm["sigma"])
+    kint, kr, W = prm["k_int"], prm["k_r"], prm["k_b"] // 64
+    rho, prev = [], prm["rho_min"]
+    for t in range(prm["max_iters"] + 2):
+        v = min(max(prm["rho_min"] * (1 + t / prm["growth_T"]) ** prm["growth_p"], prev + prm["rho_delta"]), 10.0)
+        rho.append(v)
+        prev = v
+    if alt == "rho_minus1_is_rho0":
+        rho = [prm["rho_min"]] + rho[:-1]
+    zb, found, trace = math.inf, (-1, -1, -1), []
+    for k in range(1, prm["max_iters"] + 1):
+        r = rho[k - 1] if alt == "rho_per_iteration" else rho[(k - 1) // kint]
+        x_before = o.get_state()[0].copy()
+        o.step(r, tau, tau)
+        if k % kint:
+            continue
+        x = x_before if alt == "sample_x_k_minus_1" else o.get_state()[0]
+        imp = 0
+        for rr in range(kr):
+            rid = (k // kint - 1) * kr + rr
+            if alt == "round_id_plus_1":
+                rid += kr
+            if alt == "round_id_ignores_r":
+                rid = k // kint - 1
+            f, z = o.eval(O.sample(x, prm["seed"], rid, 0, W))
+            zz = np.where(f == 1, z, np.inf)
+            l = int(np.argmin(zz)) if alt != "ties_highest_index" else len(zz) - 1 - int(np.argmin(zz[::-1]))
+            if f[l] and (zz[l] < zb or (alt == "non_strict" and zz[l] <= zb)):
+                zb, found, imp = zz[l], (k, rid, l), 1
+        trace.append((k, r, zb, imp))
+    return found, zb, trace
+
+
+_ALTS = ["rho_minus1_is_rho0", "rho_per_iteration", "sample_x_k_minus_1", "round_id_plus_1",
+         "round_id_ignores_r", "ties_highest_index", "non_strict"]
+
+
+@pytest.mark.parametrize("cfg_seed,seed", [(1, 1), (4, 1), (2, 2)])
+def test_run_orchestration_matches_alg1_by_hand(cfg_seed, seed):
+    """orc_run's orchestration = Alg. 1 written out (4 blocks, k_int = 3, k_r = 2): same incumbent
+    (iteration, round, lane, z), same per-block ρ (trace column 1) and improvement flags.  The cases
+    are chosen so that each plausible mistake in `_ALTS` changes the outcome in at least one of them
+    (checked below), i.e. the pin is discriminating."""
+    inst = G.make_config(1, cfg_seed)
+    prm = dict(sigma=0.9, k_int=3, k_r=2, k_b=64, max_iters=12, seed=seed, rho_min=0.05, growth_T=1.0,
+               growth_p=1.0, rho_delta=0.01)
+    o = O.Oracle(inst)
+    o.preprocess()
+    res = o.run(trace_max=10, **prm)
+    found, zb, trace = _alg1_by_hand(inst, prm)
+    assert (res["found_iter"], res["found_round"], res["found_index"]) == found
+    assert res["z_best"] == zb and res["rounds"] == 4 * 2 and res["iters"] == 12
+    tr = res["trace"]
+    assert [int(t[0]) for t in tr] == [t[0] for t in trace] == [3, 6, 9, 12]
+    assert [t[1] for t in tr] == [t[1] for t in trace]          # ρ per block, bit-exact
+    assert [t[1] for t in trace] == pytest.approx([0.06, 0.1, 0.15, 0.2], rel=1e-15)  # max(0.05(1+t), ρ_prev+δ), ρ_0 = ρ_min+δ
+    assert [int(t[7]) for t in tr] == [t[3] for t in trace]
+    assert [t[6] for t in tr] == [t[2] for t in trace]
+
+
+def test_run_orchestration_pin_is_discriminating():
+    """Every alternative orchestration in _ALTS gives a different incumbent or trace on at least one
+    of the cases of test_run_orchestration_matches_alg1_by_hand."""
+    prm0 = dict(sigma=0.9, k_int=3, k_r=2, k_b=64, max_iters=12, rho_min=0.05, growth_T=1.0, growth_p=1.0,
+                rho_delta=0.01)
+    caught = set()
+    for cfg_seed, seed in [(1, 1), (4, 1), (2, 2)]:
+        inst = G.make_config(1, cfg_seed)
+        prm = dict(prm0, seed=seed)
+        ref = _alg1_by_hand(inst, prm)
+        for a in _ALTS:
+            alt = _alg1_by_hand(inst, prm, a)
+            if alt[0] != ref[0] or [t[1:] for t in alt[2]] != [t[1:] for t in ref[2]]:
+                caught.add(a)
+    assert caught == set(_ALTS)
+
+
+def test_run_final_round_half_goes_to_one():
+    """PAPER L391 EvalBest(round(x_k)) with the tie x = 0.5 -> 1 (R13): one free variable with zero
+    gradient (c = 0, no rows: g = ρ - 2ρ·0.5 = 0 exactly) stays at x0 = 0.5; with max_iters < k_int no
+    sampling round happens, so the only candidate is the rounded point, x = (1), found at the last
+    iteration with round = index = -1."""
+    inst = inst_from_dense([], [], [], c=[0.0])
+    o = O.Oracle(inst)
+    o.preprocess()
+    res = o.run(max_iters=3, k_int=10)
+    z, x = o.best()
+    assert res["rounds"] == 0 and res["has_incumbent"]
+    assert (res["found_iter"], res["found_round"], res["found_index"]) == (3, -1, -1)
+    assert z == 0.0 and list(x) == [1]
+    assert o.get_state()[0][0] == 0.5
+
+
+def test_sample_subset_is_rows_of_full_sample():
+    """The bounded-sample helper draws variable idx[k] from the same Philox stream as the full
+    sampler (counter word c0 = the variable index, App. B), so it equals those rows of the full batch."""
+    p = np.random.default_rng(4).random(300)
+    idx = np.array([0, 7, 150, 299], dtype=np.int64)
+    full = O.sample(p, 77, 3, 1, 2)
+    sub = O.sample_subset(p[idx], idx, 77, 3, 1, 2)
+    assert np.array_equal(sub, full[idx])
+
+
+def test_row_scales_are_row_norms():
+    """PAPER L15 (Preprocess K1): s_j = ||K_j||_2 of the user rows (numpy.linalg.norm of the dense
+    rows, in the oracle's canonical GE-first row order); zero rows keep s_j = 1."""
+    inst = G.SMALL["general"](2)
+    o = O.Oracle(inst)
+    o.preprocess()
+    K = G.dense_K(inst)[o.row_perm()]
+    want = np.linalg.norm(K, axis=1)
+    want[want == 0] = 1.0
+    assert np.allclose(o.row_scales(), want, rtol=1e-15, atol=0)

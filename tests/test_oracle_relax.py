@@ -106,3 +106,20 @@ def test_relaxed_feasible_set_contains_original():
     assert np.all(relx[orig])
     c = inst["c"]
     assert (P[relx] @ c).min() <= (P[orig] @ c).min()
+
+
+def test_repair_large_lane_is_minimal_cover():
+    """SPEC L354 has no size cap: a lane holding all 21^3 = 9261 entries (more than the 8192 that
+    round 1 skipped) is repaired to a minimal cover of the relaxed rows, a subset of the lane."""
+    n = 21
+    inst = G.assignment3d(n, 4)
+    o = O.Oracle(inst)
+    o.set_relax(1)
+    bits = np.zeros((n ** 3, 1), dtype=np.uint64)
+    bits[:, 0] = np.uint64(1)
+    y = (o.repair(bits)[:, 0] & np.uint64(1)).astype(np.int64)
+    Ku = G.dense_K(inst)
+    cov = Ku @ y
+    assert np.all(cov >= 1) and y.sum() < n ** 3
+    for i in np.flatnonzero(y):
+        assert np.any(cov - Ku[:, i] < 1)
