@@ -51,6 +51,11 @@ typedef struct {
     void *stream;
     int32_t rank, world;
     const void *nccl_id;
+    /* loopback != 0 (test mode, needs rank = 0 and nccl_id = NULL): this one context runs all `world`
+     * ranks of the exchange one after another on its stream — rank q's words [q*W, (q+1)*W), its
+     * record written straight into the gathered slots — then the same merge, winner regeneration and
+     * halt agreement as the NCCL path; the result equals one rank with k_b*world. */
+    int32_t loopback;
 } gfors_device_opts;
 
 /* Problem in USER form.  CSR K (m x n): k_rowptr[m+1] (nondecreasing, [0]=0),
@@ -114,8 +119,8 @@ typedef struct {
     /* Monotone relaxation (R26): relax = 1 needs Q = 0,
      * canonical c >= 0 and K_u >= 0; the PDHG step and indicators then treat every row as >= (upper
      * closure) while EvalBest keeps the original equalities.  repair = 1 (needs relax, integral
-     * data, m <= 16384, world == 1) drops each lane's 1-entries in decreasing-cost order while all
-     * rows stay >= before EvalBest (lanes with > 8192 entries are left as they are). */
+     * data, world == 1) drops each lane's 1-entries in decreasing-cost order (ties: lower index)
+     * while all rows stay >= before EvalBest; every lane is repaired, whatever its size. */
     int32_t relax;
     int32_t repair;
     /* complete = 1: cover completion before EvalBest (R27): every covering
@@ -186,6 +191,13 @@ gfors_status gfors_run(gfors_ctx *ctx, const gfors_params *p, gfors_run_info *ou
  * Returns GFORS_NO_INCUMBENT if no feasible point was found. */
 gfors_status gfors_best_incumbent(gfors_ctx *ctx, double *z, uint8_t *x, gfors_incumbent_info *info);
 const char *gfors_last_error(const gfors_ctx *ctx);
+/* Test/benchmark options (production defaults otherwise); invalidate the cached loop graph.
+ *   "force_deadline_rank" r, "force_deadline_block" b: rank r (a loopback rank, or this rank) reports
+ *     its time limit as passed from block b on — the OR over ranks must halt every rank together
+ *     (CheckHalt);
+ *   "force_capture_fail" 1: a sharded run's graph capture fails, so the eager loop runs instead.
+ * Unknown key: GFORS_E_INPUT. */
+gfors_status gfors_set_option(gfors_ctx *ctx, const char *key, int64_t value);
 void gfors_destroy(gfors_ctx *ctx);
 
 /* ---------------- hooks for parity tests and benchmarks (same library, host buffers) ------- */

@@ -40,7 +40,7 @@ class GforsError(RuntimeError):
 
 
 class DeviceOpts(C.Structure):
-    _fields_ = [("device", I32), ("stream", P), ("rank", I32), ("world", I32), ("nccl_id", P)]
+    _fields_ = [("device", I32), ("stream", P), ("rank", I32), ("world", I32), ("nccl_id", P), ("loopback", I32)]
 
 
 class Problem(C.Structure):
@@ -108,6 +108,7 @@ EXPORTS = {
     "gfors_cover_complete": (I32, [P, P, P, I64]),
     "gfors_nccl_unique_id": (I32, [P]),
     "gfors_graph_note": (C.c_char_p, [P]),
+    "gfors_set_option": (I32, [P, C.c_char_p, I64]),
 }
 for _name, (_res, _args) in EXPORTS.items():
     _f = getattr(_lib, _name)
@@ -158,10 +159,11 @@ class Solver:
     """One gfors context on one GPU.  rank/world shard the samples; nccl_id (bytes from
     nccl_unique_id(), identical on all ranks) enables the in-loop incumbent exchange."""
 
-    def __init__(self, device: int = 0, stream=None, rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
+    def __init__(self, device: int = 0, stream=None, rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
+                 loopback: bool = False):
         self._nccl_buf = (C.c_char * 128).from_buffer_copy(nccl_id) if nccl_id else None
         opts = DeviceOpts(device, P(stream) if stream else None, rank, world,
-                          C.cast(self._nccl_buf, P) if nccl_id else None)
+                          C.cast(self._nccl_buf, P) if nccl_id else None, int(bool(loopback)))
         h = P()
         rc = _lib.gfors_create(C.byref(h), C.byref(opts))
         if rc != 0:
@@ -190,13 +192,27 @@ class Solver:
         """gfors_load.  inst: dict of the user-form arrays (see gen/instances.py).  numpy arrays are
         passed as host memory; torch CUDA tensors as device memory (all arrays must agree)."""
         keep = []
-        is_dev = any(hasattr(v, "is_cuda") and v.is_cuda for v in inst.values())
+        tensors = {k: v for k, v in inst.items() if hasattr(v, "is_cuda")}
+        is_dev = any(v.is_cuda for v in tensors.values())
+        if is_dev:
+            host = [k for k in ("k_rowptr", "k_col", "k_val", "r", "sense", "q_rowptr", "q_col", "q_val", "c")
+                    if inst.get(k) is not None and not (k in tensors and tensors[k].is_cuda)]
+            if host:
+                raise ValueError(f"load: mixed host and device inputs ({', '.join(host)} not CUDA tensors)")
+            import torch
+            torch.cuda.current_stream().synchronize()  # inputs written on a torch stream are complete
+
+        _TORCH_DT = {np.int64: "int64", np.int32: "int32", np.float64: "float64", np.int8: "int8"}
 
         def arr(key, dt):
             v = inst.get(key)
             if v is None:
                 return None
             if is_dev:
+                import torch
+                want = getattr(torch, _TORCH_DT[dt])
+                if v.dtype != want or not v.is_contiguous():
+                    v = v.to(dtype=want).contiguous()  # the C ABI element types (include/gfors.h)
                 keep.append(v)
                 return v
             a = np.ascontiguousarray(v, dtype=dt)
@@ -336,6 +352,11 @@ class Solver:
         self._chk(_lib.gfors_profile_active(self.h, _ptr(ams), _ptr(an), 16))
         return {_lib.gfors_kernel_class_name(k).decode(): (float(ams[k]), int(an[k])) for k in range(16)
                 if _lib.gfors_kernel_class_name(k).decode()}
+
+    def set_option(self, key: str, value: int):
+        """gfors_set_option (test/benchmark options, include/gfors.h)."""
+        self._chk(_lib.gfors_set_option(self.h, key.encode(), int(value)))
+        return self
 
     def graph_note(self):
         return _lib.gfors_graph_note(self.h).decode()

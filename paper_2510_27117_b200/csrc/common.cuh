@@ -34,7 +34,7 @@ struct Ctrl {
     long long found_iter, found_round, found_index;
     unsigned long long found_ns;
     int win_lane;           // winning lane of the last argmin (-1 none)
-    int pad0;
+    int tl_any;             // sharded: some rank's time limit has passed (OR of the exchanged flags)
     double ind[4];          // primal_gap, ||s^x||, ||s^y||, binary_gap of the last trigger
     long long dyn_launches; // kernels of the conditional branches taken (graph mode launch count)
 };
@@ -46,6 +46,7 @@ struct HaltPar {
     int trace_cap;
     int k_int, k_r;
     long long k_b_total;   // samples per round over all ranks
+    int sharded;           // time limit from the exchanged flags (Ctrl::tl_any), not the local clock
 };
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -68,6 +69,43 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
 }
 
 template <typename T> __device__ __forceinline__ T ldg(const T* p) { return __ldg(p); }
+// L2 eviction-priority policies (PTX createpolicy + .L2::cache_hint): the evaluator keeps the sample
+// batch X (80 MB at config 5, k_b = 128) resident in the 126 MB L2 while the 200 MB index stream
+// passes through with evict-first priority; the last reader of X demotes it again.
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ int ld_hint_i32(const int* a, uint64_t pol) {
+    int v;
+    asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ unsigned char ld_hint_u8(const unsigned char* a, uint64_t pol) {
+    unsigned short v;
+    asm volatile("ld.global.nc.L2::cache_hint.u8 %0, [%1], %2;" : "=h"(v) : "l"(a), "l"(pol));
+    return (unsigned char)v;
+}
+__device__ __forceinline__ void st_hint_u64(uint64_t* a, uint64_t v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(a), "l"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ ulonglong2 ld_hint_u64x2(const uint64_t* a, uint64_t pol) {
+    ulonglong2 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;" : "=l"(v.x), "=l"(v.y) : "l"(a), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint64_t ld_hint_u64(const uint64_t* a, uint64_t pol) {
+    uint64_t v;
+    asm volatile("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(a), "l"(pol));
+    return v;
+}
+
 
 // value of nonzero p of a K-like matrix in the given storage class
 template <int KIND>

@@ -36,6 +36,7 @@
 #include "dense_q.cuh"
 #include "assign3d.cuh"
 #include "repair.cuh"
+#include "feas_rb.cuh"
 #include "cover.cuh"
 #include <cudaTypedefs.h>
 #include <cstdlib>
@@ -185,8 +186,8 @@ struct DirPlan {  // how one product direction (K rows or K' columns) is compute
 // one CTA: max cut's primal took 84 us per launch for n = 20480 in a single block)
 constexpr long long RB_ROWS_MAX = 512;
 
-static std::vector<long long> make_rowblocks(const std::vector<int64_t>& ptr, long long rows, long long cap,
-                                             long long cap_rows = LLONG_MAX) {
+static std::vector<long long> make_rowblocks_from(const std::vector<int64_t>& ptr, long long rows, long long cap,
+                                                  long long cap_rows = LLONG_MAX) {
     std::vector<long long> b;
     b.push_back(0);
     long long r = 0;
@@ -198,6 +199,10 @@ static std::vector<long long> make_rowblocks(const std::vector<int64_t>& ptr, lo
         r = e;
     }
     return b;
+}
+static std::vector<long long> make_rowblocks(const std::vector<int64_t>& ptr, long long rows, long long cap,
+                                             long long cap_rows = LLONG_MAX) {
+    return make_rowblocks_from(ptr, rows, cap, cap_rows);
 }
 
 DirPlan plan_direction(const std::vector<int64_t>& ptr, long long rows, cudaStream_t s,
@@ -345,7 +350,7 @@ __global__ void __launch_bounds__(256) k_halt(Ctrl* __restrict__ ctrl, HaltPar h
             all_ok = all_ok && ok;
         }
         if (all_ok && ctrl->since_improve >= W) halt = 1;
-        else if (globaltimer_ns() >= ctrl->deadline_ns) halt = 3;
+        else if (hp.sharded ? ctrl->tl_any != 0 : globaltimer_ns() >= ctrl->deadline_ns) halt = 3;
         else if (ctrl->blk + 1 >= ctrl->max_blocks) halt = 2;
     }
     const long long k = (ctrl->blk + 1) * hp.k_int;
@@ -374,6 +379,7 @@ __global__ void k_loop_start(Ctrl* ctrl, double time_limit_s) {
 // =============================================================================================
 struct gfors_ctx {
     int device = 0;
+    int num_sms = NUM_SMS_B200;  // queried at create
     cudaStream_t stream = nullptr, cap_stream = nullptr;
     bool own_stream = false;
     int rank = 0, world = 1;
@@ -387,6 +393,11 @@ struct gfors_ctx {
     bool complete = false;  // cover completion before EvalBest (cover.cuh)
     int* d_cover_rows = nullptr;      // eligible covering rows (prep-owned, built on first use)
     long long n_cover = -1;
+    int* d_rp_rank = nullptr;         // repair drop order (repair.cuh): rank of each variable, built on first use
+    int* d_rp_order = nullptr;        // its inverse
+    long long* d_rp_srow = nullptr;   // per-lane row sums when m > RP_SROWS
+    long long rp_srow_len = 0;
+    uint32_t* d_Tsamp = nullptr;      // RandSampleStep thresholds ceil(p 2^32) (0: no planes needed)
     int* d_cover_best = nullptr;
     uint64_t* d_cover_viol = nullptr;
     long long cover_viol_len = 0;
@@ -507,7 +518,12 @@ struct gfors_ctx {
         signed char* B = nullptr;
         long long nrows = 0;
         int sub = 32;
-    } cnt[3];  // BMAX 1, 2, 8
+    } cnt[3];  // BMAX 1, 2, 8: rows longer than FB_NNZ (k_feas_count)
+    struct CountRb {               // rows <= FB_NNZ nonzeros of each class (k_feas_rb, feas_rb.cuh)
+        CountList rows;
+        ClassCsr cc{};
+        unsigned char* skip = nullptr;  // [nrows] per-round "satisfied by p = 1 variables" flags
+    } cntrb[3];
     int* d_int_row = nullptr;
     long long* d_int_rhs = nullptr;
     signed char* d_int_eq = nullptr;
@@ -569,6 +585,14 @@ struct gfors_ctx {
     // sample sharding over NCCL (shard.cuh)
     ncclComm_t comm = nullptr;
     bool sharded = false;
+    bool loopback = false;         // world simulated ranks in this context (test mode, no NCCL)
+
+    // options set through gfors_set_option (tests, benchmarks); defaults are the production path
+    struct Options {
+        long long force_deadline_rank = -1;   // this (simulated) rank reports its time limit as passed ...
+        long long force_deadline_block = -1;  // ... from this block on (tests of the halt agreement)
+        long long force_capture_fail = 0;     // sharded: make the graph capture fail (eager fallback test)
+    } opt;
     double* d_rec = nullptr;       // [4] local record + [4*world] gathered records
     long long* d_regen = nullptr;  // [2] winner global index, round
     std::string graph_note;        // why the graph fell back to the eager loop, if it did
@@ -602,6 +626,7 @@ void gfors_ctx::free_problem() {
     d_rsign = nullptr;
     d_qd = nullptr; d_tcitems = nullptr; d_tcoff = nullptr; qdense = false; tc_grid = 0; d_qs_uoff = nullptr;
     for (auto& c : cnt) c = CountList{};
+    for (auto& c : cntrb) c = CountRb{};
     d_int_row = nullptr; d_int_rhs = nullptr; d_int_eq = nullptr; d_int_seg_start = nullptr; d_int_seg_slot = nullptr;
     d_real_row = nullptr;
     d_planes = nullptr;
@@ -620,11 +645,12 @@ void gfors_ctx::free_prep() {
                    (void**)&d_X, (void**)&d_viol, (void**)&d_iacc, &d_zpart, (void**)&d_z, (void**)&d_ctrl,
                    (void**)&d_qx, (void**)&d_qdx, (void**)&d_qxpart, (void**)&d_Xs, (void**)&d_qacc,
                    (void**)&d_qxpart2, (void**)&d_qreuse, (void**)&d_cover_rows, (void**)&d_cover_best,
-                   (void**)&d_cover_viol};
+                   (void**)&d_cover_viol, (void**)&d_rp_rank, (void**)&d_rp_order, (void**)&d_rp_srow, (void**)&d_Tsamp};
     for (void** p : ps) { dfree(*p); *p = nullptr; }
     X_words = iacc_len = zpart_len = z_len = Xs_lanes = 0;
     n_cover = -1;
     cover_viol_len = 0;
+    rp_srow_len = 0;
     for (int b = 0; b < 2; ++b) { dfree(a3.keys[b]); dfree(a3.vals[b]); }
     for (void* q : {(void*)a3.tmp, (void*)a3.sj0, (void*)a3.sk0, (void*)a3.Ri, (void*)a3.Rj, (void*)a3.Rk,
                     (void*)a3.meta})
@@ -1081,11 +1107,18 @@ void enqueue_trigger(gfors_ctx* C, cudaStream_t s, long long kint, long long j) 
                                                                              kint, j, C->d_part2)));
 }
 
-// 32-variable chunks per warp job of k_obj_bits: enough jobs for ~64 warps per SM
-int obj_vpj(const gfors_ctx* C, int W) {
+// k_obj_bits launch shape: gx CTAs per word group (<= 8 per SM in total, >= 16 chunks each)
+struct ObjBitsShape { int wv; int nwg; long long gx; long long cpc; };
+ObjBitsShape obj_bits_shape(const gfors_ctx* C, int W) {
+    ObjBitsShape o;
+    o.wv = (W % 2 == 0) ? 2 : 1;
+    o.nwg = W / o.wv;
     const long long nchunk32 = (C->n + 31) / 32;
-    long long v = nchunk32 * W / ((long long)NUM_SMS_B200 * 64);
-    return (int)std::max<long long>(1, std::min<long long>(64, v));
+    long long gx = std::max<long long>(1, (long long)C->num_sms * 8 / o.nwg);
+    gx = std::min<long long>(gx, (nchunk32 + 15) / 16);
+    o.cpc = (nchunk32 + gx - 1) / gx;
+    o.gx = (nchunk32 + o.cpc - 1) / o.cpc;
+    return o;
 }
 
 // x_l' Q x_l of every lane of the batch by the tcgen05 int8 kernel (dense_q.cuh): unpack the bit-sliced
@@ -1104,6 +1137,23 @@ void enqueue_obj_dense(gfors_ctx* C, cudaStream_t s, int W, long long* zrows) {
 // evaluation of the batch in d_X (W words per variable); viol/iacc must have been reset
 void enqueue_eval(gfors_ctx* C, cudaStream_t s, int W, const unsigned char* ones = nullptr) {
     const Csr K = csr_K(C);
+    for (int li = 0; li < 3; ++li) {
+        auto& rb = C->cntrb[li];
+        if (!rb.rows.nrows) continue;
+        CountRows cr{rb.rows.row, rb.rows.t, rb.rows.rel, rb.rows.B, rb.rows.nrows};
+        if (ones) LAUNCH(C, s, KC_FEAS, (k_feas_skip<<<grid_for(cr.nrows), NT, 0, s>>>(cr, ones, rb.skip)));
+        const unsigned char* sk = ones ? rb.skip : nullptr;
+        const int wv = (W % 2 == 0) ? 2 : 1;
+        const int nwg = W / wv;
+        // 6 CTAs per SM (37 KB of shared memory each) over all word groups
+        const dim3 grid((unsigned)std::max<long long>(1, std::min<long long>(rb.cc.nblk, (long long)C->num_sms * 6 / nwg)),
+                        (unsigned)nwg);
+#define FEAS_RB(BM) \
+        if (wv == 2) LAUNCH(C, s, KC_FEAS, (k_feas_rb<BM, 2><<<grid, FB_NT, 0, s>>>(rb.cc, sk, C->d_X, W, C->d_viol))); \
+        else LAUNCH(C, s, KC_FEAS, (k_feas_rb<BM, 1><<<grid, FB_NT, 0, s>>>(rb.cc, sk, C->d_X, W, C->d_viol)));
+        if (li == 0) { FEAS_RB(1) } else if (li == 1) { FEAS_RB(2) } else { FEAS_RB(8) }
+#undef FEAS_RB
+    }
     for (int li = 0; li < 3; ++li) {
         auto& cl = C->cnt[li];
         if (!cl.nrows) continue;
@@ -1140,11 +1190,15 @@ void enqueue_eval(gfors_ctx* C, cudaStream_t s, int W, const unsigned char* ones
     const Csr Q = csr_Q(C);
     if (C->obj_bits) {
         // linear term by coefficient bit planes, quadratic term (if any) appended as extra partial rows
-        const long long nchunk32 = (C->n + 31) / 32;
-        const int vpj = obj_vpj(C, W);
-        const long long jpw = (nchunk32 + vpj - 1) / vpj;
-        LAUNCH(C, s, KC_OBJ, (k_obj_bits<<<grid_for(jpw * W * 32), NT, 0, s>>>(C->n, vpj, C->d_planes, C->obj_nb, C->obj_cmin,
-                                                                             C->d_X, W, (long long*)C->d_zpart)));
+        const ObjBitsShape ob = obj_bits_shape(C, W);
+        const long long jpw = ob.gx;
+        const dim3 og((unsigned)ob.gx, (unsigned)ob.nwg);
+        if (ob.wv == 2)
+            LAUNCH(C, s, KC_OBJ, (k_obj_bits<2><<<og, 256, 0, s>>>(C->n, ob.cpc, C->d_planes, C->obj_nb, C->obj_cmin,
+                                                                  C->d_X, W, (long long*)C->d_zpart)));
+        else
+            LAUNCH(C, s, KC_OBJ, (k_obj_bits<1><<<og, 256, 0, s>>>(C->n, ob.cpc, C->d_planes, C->obj_nb, C->obj_cmin,
+                                                                  C->d_X, W, (long long*)C->d_zpart)));
         long long rows = jpw;
         if (C->qdense) {
             enqueue_obj_dense(C, s, W, (long long*)C->d_zpart + jpw * 64LL * W);
@@ -1192,6 +1246,7 @@ void ensure_batch(gfors_ctx* C, int W) {
         dfree(C->d_viol); C->d_viol = dalloc<unsigned long long>(W);
         C->gvalid = false;
     }
+    if (!C->d_Tsamp) { C->d_Tsamp = dalloc<uint32_t>(C->n); C->gvalid = false; }
     const long long niacc = C->n_int * 64LL * W;
     if (niacc > C->iacc_len) {
         dfree(C->d_iacc); C->d_iacc = dalloc<unsigned long long>(niacc); C->iacc_len = niacc; C->gvalid = false;
@@ -1200,9 +1255,7 @@ void ensure_batch(gfors_ctx* C, int W) {
     const long long nchunk = (C->n + C->obj_chunk - 1) / C->obj_chunk;
     long long zrows = nchunk;
     if (C->obj_bits) {
-        const long long nchunk32 = (C->n + 31) / 32;
-        const int vpj = obj_vpj(C, W);
-        zrows = (nchunk32 + vpj - 1) / vpj + (C->qdense ? C->tc_grid : (C->hasq ? nchunk : 0));
+        zrows = obj_bits_shape(C, W).gx + (C->qdense ? C->tc_grid : (C->hasq ? nchunk : 0));
     } else if (C->qdense) {
         zrows = nchunk + C->tc_grid;
     }
@@ -1232,12 +1285,22 @@ void set_relax(gfors_ctx* C, int relax, int repair) {
     }
     if (repair) {
         if (!C->integral) input_error("params.repair: needs integral data");
-        if (C->m > 16384) input_error("params.repair: needs m <= 16384 (per-lane row sums in shared memory)");
         if (C->sharded) input_error("params.repair: not with the NCCL-sharded loop (winner regeneration)");
     }
     if (C->m1p != (relax ? C->m : C->m1)) C->gvalid = false;
     C->m1p = relax ? C->m : C->m1;
     C->repair = repair != 0;
+    if (C->repair && !C->d_rp_rank) {
+        // the drop order of every lane: decreasing canonical cost, ties lower index first (R26)
+        std::vector<int> order((size_t)C->n), rank((size_t)C->n);
+        for (long long i = 0; i < C->n; ++i) order[i] = (int)i;
+        std::sort(order.begin(), order.end(), [&](int a, int b) {
+            return C->c[a] > C->c[b] || (C->c[a] == C->c[b] && a < b);
+        });
+        for (long long t = 0; t < C->n; ++t) rank[order[t]] = (int)t;
+        C->d_rp_order = dupload(order, C->stream);
+        C->d_rp_rank = dupload(rank, C->stream);
+    }
 }
 
 // cover completion (cover.cuh, R27): eligible rows built once, phase buffers sized for W
@@ -1279,13 +1342,16 @@ void enqueue_cover(gfors_ctx* C, cudaStream_t s, const double* pfix, int W, long
 
 void enqueue_repair(gfors_ctx* C, cudaStream_t s, int W) {
     const size_t sm = rp_smem_bytes(C->m);
+    if (C->m > RP_SROWS && 64LL * W * C->m > C->rp_srow_len) {
+        dfree(C->d_rp_srow);
+        C->d_rp_srow = dalloc<long long>(64LL * W * C->m);
+        C->rp_srow_len = 64LL * W * C->m;
+        C->gvalid = false;
+    }
     KIND_SWITCH(C->kkind, {
-        static bool attr = false;
-        if (!attr) {
-            CK(cudaFuncSetAttribute(k_repair<KINDV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rp_smem_bytes(16384)));
-            attr = true;
-        }
-        LAUNCH(C, s, KC_SAMPLE, (k_repair<KINDV><<<64 * W, RP_NT, sm, s>>>(C->n, C->m, csr_Kt(C), C->d_c, C->d_ru, C->d_X, W)));
+        CK(cudaFuncSetAttribute(k_repair<KINDV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rp_smem_bytes(RP_SROWS)));
+        LAUNCH(C, s, KC_SAMPLE, (k_repair<KINDV><<<64 * W, RP_NT, sm, s>>>(C->n, C->m, csr_Kt(C), C->d_rp_rank, C->d_rp_order,
+                                                                         C->d_ru, C->d_X, W, C->d_rp_srow)));
     });
 }
 
@@ -1364,10 +1430,15 @@ void enqueue_sample(gfors_ctx* C, cudaStream_t s, const double* pfix, int W, lon
         enqueue_sample_a3<T>(C, s, pfix, W, word_off, seed, kint, r, kr, round_fixed, use_fixed);
         return;
     }
-    const uint2 key = make_uint2((unsigned)(seed & 0xffffffffu), (unsigned)(seed >> 32));
-    LAUNCH(C, s, KC_SAMPLE, (k_sample<T><<<grid_for(C->n * (long long)W), NT, 0, s>>>(
-                                (const T*)C->d_x[0], (const T*)C->d_x[1], pfix, C->n, W, word_off, key, C->d_ctrl, kint, r,
-                                kr, round_fixed, use_fixed, C->d_X)));
+    PhiloxKeys rk;
+    for (int t = 0; t < 10; ++t) {  // round t uses key + t*(W0, W1) (mod 2^32)
+        rk.k0[t] = (uint32_t)(seed & 0xffffffffu) + (uint32_t)t * 0x9E3779B9u;
+        rk.k1[t] = (uint32_t)(seed >> 32) + (uint32_t)t * 0xBB67AE85u;
+    }
+    LAUNCH(C, s, KC_SAMPLE, (k_sample_thr<T><<<grid_for(C->n), NT, 0, s>>>((const T*)C->d_x[0], (const T*)C->d_x[1], pfix,
+                                C->n, W, C->d_ctrl, kint, use_fixed, C->d_Tsamp, C->d_X)));
+    LAUNCH(C, s, KC_SAMPLE, (k_sample<<<C->num_sms * 8, NT, 0, s>>>(C->d_Tsamp, C->n, W, word_off, rk, C->d_ctrl, r, kr,
+                                round_fixed, use_fixed, C->d_X)));
 }
 
 // one whole Alg. 1 sampling block (graph body)
@@ -1377,26 +1448,40 @@ void enqueue_block(gfors_ctx* C, cudaStream_t s, const gfors_params* p, int W, H
     const long long kint = p->k_int;
     for (long long j = 0; j < kint; ++j) enqueue_iter<T>(C, s, kint, j);
     enqueue_trigger<T>(C, s, kint, kint - 1);
-    const long long word_off = (long long)C->rank * W;
+    // loopback (test mode): all `world` ranks run here one after another, records written straight
+    // into the gathered slots; otherwise this rank's own word range and an ncclAllGather
+    const int nsim = C->loopback ? C->world : 1;
     for (int r = 0; r < p->k_r; ++r) {
-        enqueue_reset(C, s, W, ~0ull);
-        enqueue_sample<T>(C, s, nullptr, W, word_off, p->seed, kint, r, p->k_r, 0u, 0);
-        if (C->repair) enqueue_repair(C, s, W);
-        if (C->complete) enqueue_cover<T>(C, s, nullptr, W, kint, (C->m > 0 && C->pd.rb) ? C->d_ones : nullptr);
-        // the trigger pass of this block counted the p = 1 entries of every row (rb path)
-        enqueue_eval(C, s, W, (C->m > 0 && C->pd.rb) ? C->d_ones : nullptr);
+        for (int q = 0; q < nsim; ++q) {
+            const int rank = C->loopback ? q : C->rank;
+            const long long word_off = (long long)rank * W;
+            enqueue_reset(C, s, W, ~0ull);
+            enqueue_sample<T>(C, s, nullptr, W, word_off, p->seed, kint, r, p->k_r, 0u, 0);
+            if (C->repair) enqueue_repair(C, s, W);
+            if (C->complete) enqueue_cover<T>(C, s, nullptr, W, kint, (C->m > 0 && C->pd.rb) ? C->d_ones : nullptr);
+            // the trigger pass of this block counted the p = 1 entries of every row (rb path)
+            enqueue_eval(C, s, W, (C->m > 0 && C->pd.rb) ? C->d_ones : nullptr);
+            if (!C->sharded) {
+                LAUNCH(C, s, KC_ARGMIN, (k_argmin<<<1, NT, 0, s>>>(C->d_z, C->d_viol, 64LL * W, word_off, C->d_ctrl, kint, r, p->k_r, 0)));
+                LAUNCH(C, s, KC_ARGMIN, (k_copy_best<<<grid_for(C->n), NT, 0, s>>>(C->d_X, W, C->n, C->d_ctrl, C->d_xbest)));
+                continue;
+            }
+            // record (-> ncclAllGather) -> identical merge on every rank -> regenerate the winner's bits
+            const long long fb = (C->opt.force_deadline_rank == rank) ? C->opt.force_deadline_block : -1;
+            double* rec = C->loopback ? C->d_rec + 4 + 4 * q : C->d_rec;
+            LAUNCH(C, s, KC_ARGMIN, (k_local_record<<<1, NT, 0, s>>>(C->d_z, C->d_viol, 64LL * W, word_off, C->d_ctrl, rec,
+                                                                   q == 0, fb)));
+        }
         if (C->sharded) {
-            // record -> ncclAllGather -> identical merge on every rank -> regenerate the winner's bits
-            LAUNCH(C, s, KC_ARGMIN, (k_local_record<<<1, NT, 0, s>>>(C->d_z, C->d_viol, 64LL * W, word_off, C->d_ctrl, C->d_rec)));
-            const int rc = C->dry ? 0 : nccl().AllGather(C->d_rec, C->d_rec + 4, 4, ncclFloat64_, C->comm, s);
-            if (rc != 0) throw Err{GFORS_E_NCCL, std::string("ncclAllGather: ") + nccl().GetErrorString(rc)};
+            if (C->capturing && C->opt.force_capture_fail) throw Err{GFORS_E_CUDA, "forced capture failure (test option)"};
+            if (!C->loopback) {
+                const int rc = C->dry ? 0 : nccl().AllGather(C->d_rec, C->d_rec + 4, 4, ncclFloat64_, C->comm, s);
+                if (rc != 0) throw Err{GFORS_E_NCCL, std::string("ncclAllGather: ") + nccl().GetErrorString(rc)};
+            }
             LAUNCH(C, s, KC_ARGMIN, (k_merge_records<<<1, 32, 0, s>>>(C->d_rec + 4, C->world, C->d_ctrl, kint, r, p->k_r, C->d_regen)));
             const uint2 key = make_uint2((unsigned)(p->seed & 0xffffffffu), (unsigned)(p->seed >> 32));
             LAUNCH(C, s, KC_ARGMIN, (k_regen_best<T><<<grid_for(C->n), NT, 0, s>>>((const T*)C->d_x[0], (const T*)C->d_x[1], C->n,
                                                                                   C->d_ctrl, kint, key, C->d_regen, C->d_xbest)));
-        } else {
-            LAUNCH(C, s, KC_ARGMIN, (k_argmin<<<1, NT, 0, s>>>(C->d_z, C->d_viol, 64LL * W, word_off, C->d_ctrl, kint, r, p->k_r, 0)));
-            LAUNCH(C, s, KC_ARGMIN, (k_copy_best<<<grid_for(C->n), NT, 0, s>>>(C->d_X, W, C->n, C->d_ctrl, C->d_xbest)));
         }
     }
     LAUNCH(C, s, KC_HALT, (k_halt<<<1, NT, 0, s>>>(C->d_ctrl, hp, C->d_part1, C->nb1, C->d_part2, C->nb2, C->n, C->d_hist,
@@ -1717,7 +1802,7 @@ static void do_run_t(gfors_ctx* C, const gfors_params* p, gfors_run_info* out) {
     CK(cudaMemsetAsync(C->d_xbest, 0, C->n, s));
     CK(cudaMemsetAsync(C->d_hist, 0, 3 * 1024 * sizeof(double), s));
     HaltPar hp{{p->tol_primal, p->tol_dual, p->tol_binary}, p->stall_rel, p->stall_window, p->trace_cap,
-               p->k_int, p->k_r, p->k_b * (long long)C->world};
+               p->k_int, p->k_r, p->k_b * (long long)C->world, C->sharded ? 1 : 0};
     k_loop_start<<<1, 1, 0, s>>>(C->d_ctrl, p->time_limit_s);
     CK(cudaGetLastError());
     C->launches++;
@@ -1891,6 +1976,11 @@ gfors_status gfors_create(gfors_ctx** out, const gfors_device_opts* opts) {
     try {
         if (opts) { C->device = opts->device; C->rank = opts->rank; C->world = opts->world; }
         if (C->world < 1 || C->rank < 0 || C->rank >= C->world) input_error("device_opts: need 0 <= rank < world");
+        if (opts && opts->loopback) {
+            if (opts->nccl_id || C->rank != 0) input_error("device_opts.loopback: needs rank = 0 and nccl_id = NULL");
+            C->loopback = true;
+            C->sharded = true;  // the exchange protocol (record, merge, regeneration, halt flags) without NCCL
+        }
         // nccl_id == NULL with world > 1: independent sample shard (rank r draws global words
         // [r*W, (r+1)*W)); the caller merges incumbents with gfors_merge_records.  nccl_id != NULL:
         // in-loop record exchange over NCCL every sampling round (shard.cuh).
@@ -1898,6 +1988,7 @@ gfors_status gfors_create(gfors_ctx** out, const gfors_device_opts* opts) {
         CK(cudaGetDeviceCount(&ndev));
         if (C->device < 0 || C->device >= ndev) input_error("device_opts.device: %d not in [0,%d)", C->device, ndev);
         CK(cudaSetDevice(C->device));
+        CK(cudaDeviceGetAttribute(&C->num_sms, cudaDevAttrMultiProcessorCount, C->device));
         if (opts && opts->nccl_id) {
             NcclApi& api = nccl();
             if (!api.ok) throw Err{GFORS_E_NCCL, api.why};
@@ -1920,6 +2011,19 @@ gfors_status gfors_create(gfors_ctx** out, const gfors_device_opts* opts) {
     }
     *out = C;
     return GFORS_OK;
+}
+
+gfors_status gfors_set_option(gfors_ctx* C, const char* key, int64_t value) {
+    API_BEGIN(C)
+    if (!key) input_error("gfors_set_option: key is NULL");
+    const std::string k(key);
+    if (k == "force_deadline_rank") C->opt.force_deadline_rank = value;
+    else if (k == "force_deadline_block") C->opt.force_deadline_block = value;
+    else if (k == "force_capture_fail") C->opt.force_capture_fail = value;
+    else input_error("gfors_set_option: unknown key '%s'", key);
+    C->gvalid = false;
+    C->gno = false;
+    API_END(C)
 }
 
 gfors_status gfors_load(gfors_ctx* C, const gfors_problem* prob) {
@@ -2199,7 +2303,7 @@ int64_t gfors_launches_per_block(gfors_ctx* C, const gfors_params* p) {
     if (!p) p = &d;
     const int W = (int)(p->k_b / 64);
     HaltPar hp{{p->tol_primal, p->tol_dual, p->tol_binary}, p->stall_rel, p->stall_window, p->trace_cap,
-               p->k_int, p->k_r, p->k_b * (long long)C->world};
+               p->k_int, p->k_r, p->k_b * (long long)C->world, C->sharded ? 1 : 0};
     const long long before = C->launches;
     C->launches = 0;
     C->dry = true;

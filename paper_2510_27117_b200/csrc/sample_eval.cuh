@@ -47,27 +47,116 @@ __device__ __forceinline__ uint64_t bernoulli_word(double p, unsigned i, unsigne
     return res;  // lanes with u == T stay 0 ([u < T] false)
 }
 
-// p: either a fixed vector (pfix != nullptr) or x_k of the loop (parity from ctrl).
-template <typename T>
-__global__ void __launch_bounds__(256) k_sample(const T* __restrict__ xa, const T* __restrict__ xb2,
-                                                const double* __restrict__ pfix, long long n, int W,
-                                                long long word_off, uint2 key, const Ctrl* __restrict__ ctrl,
-                                                long long kint, int r, int kr, unsigned round_fixed, int use_fixed,
-                                                uint64_t* __restrict__ X) {
-    const T* __restrict__ p = nullptr;
-    unsigned round = round_fixed;
-    if (!use_fixed) {
-        const long long b = ctrl->blk;
-        p = (((b + 1) * kint) & 1) ? xb2 : xa;  // x_k written by iteration (b+1)*kint - 1
-        round = (unsigned)(b * kr + r);
+// Philox4x32-10 round keys precomputed on the host (round r uses key + r*(W0, W1)): kernel parameters,
+// so each key is a constant-bank operand of the 3-input XOR (philox_rkw below).
+struct PhiloxKeys {
+    uint32_t k0[10], k1[10];
+};
+
+// 32x32 -> 64-bit product in one IMAD.WIDE.U32 (the register pair holds lo, hi)
+__device__ __forceinline__ uint64_t mul_wide_u32(uint32_t a, uint32_t b) {
+    uint64_t r;
+    asm("mul.wide.u32 %0, %1, %2;" : "=l"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ uint4 philox_rkw(uint4 c, const PhiloxKeys& rk) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = mul_wide_u32(0xD2511F53u, c.x), p1 = mul_wide_u32(0xCD9E8D57u, c.z);
+        c = make_uint4((uint32_t)(p1 >> 32) ^ c.y ^ rk.k0[r], (uint32_t)p1, (uint32_t)(p0 >> 32) ^ c.w ^ rk.k1[r],
+                       (uint32_t)p0);
     }
-    const long long total = n * (long long)W;
-    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-         idx += gridDim.x * (long long)blockDim.x) {
-        const long long i = idx / W;
-        const int wl = (int)(idx - i * W);
-        const double pi = pfix ? pfix[i] : (double)p[i];
-        X[idx] = bernoulli_word(pi, (unsigned)i, (unsigned)(word_off + wl), round, key);
+    return c;
+}
+
+// RandSampleStep pass 1: T_i = ceil(p_i 2^32) for every variable (fp64, exact), stored as uint32 with
+// 0 meaning "no random planes needed": the words of variables with T = 0 (p = 0) or T = 2^32 (p = 1)
+// are written here (all zeros / all ones).  p: a fixed vector (pfix) or x_k of the loop.
+template <typename T>
+__global__ void __launch_bounds__(256) k_sample_thr(const T* __restrict__ xa, const T* __restrict__ xb2,
+                                                    const double* __restrict__ pfix, long long n, int W,
+                                                    const Ctrl* __restrict__ ctrl, long long kint, int use_fixed,
+                                                    uint32_t* __restrict__ Tarr, uint64_t* __restrict__ X) {
+    const T* __restrict__ p = nullptr;
+    if (!use_fixed) p = (((ctrl->blk + 1) * kint) & 1) ? xb2 : xa;  // x_k written by iteration (b+1)*kint - 1
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += gridDim.x * (long long)blockDim.x) {
+        double pi = pfix ? pfix[i] : (double)p[i];
+        pi = pi < 0.0 ? 0.0 : (pi > 1.0 ? 1.0 : pi);
+        const double Td = ceil(pi * 4294967296.0);
+        uint32_t t = 0;
+        if (Td <= 0.0) { for (int w = 0; w < W; ++w) X[i * W + w] = 0ull; }
+        else if (Td >= 4294967296.0) { for (int w = 0; w < W; ++w) X[i * W + w] = ~0ull; }
+        else t = (uint32_t)Td;
+        Tarr[i] = t;
+    }
+}
+
+// RandSampleStep pass 2 (Alg. 3, contract R10): the MSB-first compare decides a 64-lane word after a
+// data-dependent number of plane pairs (E ~ 3.7 Philox calls, up to 16), so a thread that owned one
+// word would idle until the slowest lane of its warp finished.  Instead every thread walks its own
+// variables (i = tid, tid + stride, ...), their W words one after another, and runs ONE plane pair
+// per loop trip: when a word is decided it is stored and the next one starts, so all lanes do useful
+// Philox work until the tail.  T of the next variable is prefetched; T = 0 variables were written by
+// pass 1.  Identical output to bernoulli_word.
+__global__ void __launch_bounds__(256) k_sample(const uint32_t* __restrict__ Tarr, long long n, int W, long long word_off,
+                                                const __grid_constant__ PhiloxKeys rk, const Ctrl* __restrict__ ctrl,
+                                                int r, int kr, unsigned round_fixed, int use_fixed, uint64_t* __restrict__ X) {
+    const unsigned round = use_fixed ? round_fixed : (unsigned)(ctrl->blk * kr + r);
+    const long long stride = gridDim.x * (long long)blockDim.x;
+    const uint64_t pol = l2_policy_evict_last();  // the batch is gathered by the evaluator next
+    long long ni = blockIdx.x * (long long)blockDim.x + threadIdx.x;  // next variable
+    uint32_t nT = ni < n ? __ldg(Tarr + ni) : 0u;
+    long long ci = -1;  // current variable
+    int cw = 0;         // its current word
+    uint32_t Tv = 0, Tsh = 0, q = 0;
+    uint32_t ul = 0, uh = 0, rl = 0, rh = 0;
+    bool active = false;
+    while (true) {
+        if (!active) {
+            if (ci >= 0 && ++cw < W) {  // next word of the same variable
+                active = true;
+            } else {
+                while (ni < n && nT == 0u) {  // pass-1 variables: nothing to draw
+                    ni += stride;
+                    nT = ni < n ? __ldg(Tarr + ni) : 0u;
+                }
+                if (ni < n) {
+                    ci = ni; cw = 0; Tv = nT; active = true;
+                    ni += stride;
+                    nT = ni < n ? __ldg(Tarr + ni) : 0u;
+                } else {
+                    ci = -1;
+                }
+            }
+            if (active) { Tsh = Tv; q = 0; ul = uh = ~0u; rl = rh = 0u; }
+        }
+        if (!__any_sync(0xffffffffu, active)) break;
+        if (active) {
+            // two plane pairs per loop trip (halves the loop/fetch overhead; a word decided by the first
+            // pair wastes the second, ~0.5 call per word).  Plane with T-bit t: t = 1 -> lanes with
+            // u-bit 0 decide 1 (res |= und & ~pl), und &= pl; t = 0 -> lanes with u-bit 1 decide 0,
+            // und &= ~pl.   m = t ? ~0 : 0.  Planes after the word is decided change nothing (und = 0).
+            const uint4 o = philox_rkw(make_uint4((uint32_t)ci, (uint32_t)(word_off + cw), q, round), rk);
+            const uint4 o2 = philox_rkw(make_uint4((uint32_t)ci, (uint32_t)(word_off + cw), q + 1, round), rk);
+            uint32_t m = 0u - (Tsh >> 31);
+            rl |= ul & ~o.x & m; rh |= uh & ~o.y & m;
+            ul &= ~(o.x ^ m);    uh &= ~(o.y ^ m);
+            m = 0u - ((Tsh >> 30) & 1u);
+            rl |= ul & ~o.z & m; rh |= uh & ~o.w & m;
+            ul &= ~(o.z ^ m);    uh &= ~(o.w ^ m);
+            m = 0u - ((Tsh >> 29) & 1u);
+            rl |= ul & ~o2.x & m; rh |= uh & ~o2.y & m;
+            ul &= ~(o2.x ^ m);    uh &= ~(o2.y ^ m);
+            m = 0u - ((Tsh >> 28) & 1u);
+            rl |= ul & ~o2.z & m; rh |= uh & ~o2.w & m;
+            ul &= ~(o2.z ^ m);    uh &= ~(o2.w ^ m);
+            Tsh <<= 4;
+            q += 2;
+            if ((ul | uh) == 0u || q == 16) {  // decided (u == T lanes stay 0)
+                st_hint_u64(X + ci * W + cw, (uint64_t)rl | ((uint64_t)rh << 32), pol);
+                active = false;
+            }
+        }
     }
 }
 
@@ -139,15 +228,15 @@ __device__ __forceinline__ uint64_t count_ok(const uint64_t (&C)[BMAX], uint64_t
 }
 
 template <int WV>
-__device__ __forceinline__ void load_words(const uint64_t* __restrict__ p, uint64_t (&v)[WV]) {
+__device__ __forceinline__ void load_words(const uint64_t* __restrict__ p, uint64_t (&v)[WV], uint64_t pol) {
     if constexpr (WV == 1) {
-        v[0] = __ldg(p);
+        v[0] = ld_hint_u64(p, pol);
     } else if constexpr (WV == 2) {
-        const ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(p));
+        const ulonglong2 a = ld_hint_u64x2(p, pol);
         v[0] = a.x; v[1] = a.y;
     } else {
-        const ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(p));
-        const ulonglong2 b = __ldg(reinterpret_cast<const ulonglong2*>(p) + 1);
+        const ulonglong2 a = ld_hint_u64x2(p, pol);
+        const ulonglong2 b = ld_hint_u64x2(p + 2, pol);
         v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
     }
 }
@@ -165,6 +254,7 @@ __global__ void __launch_bounds__(256) k_feas_count(Csr K, CountRows cr, const u
         for (int w = threadIdx.x; w < W; w += blockDim.x) s_viol[w] = 0ull;
     __syncthreads();
     constexpr int RPW = 32 / SUB;
+    const uint64_t pfirst = l2_policy_evict_first(), plast = l2_policy_evict_last();
     const int lane = threadIdx.x & (SUB - 1);
     const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = (gridDim.x * (long long)blockDim.x) >> 5;
@@ -197,11 +287,11 @@ __global__ void __launch_bounds__(256) k_feas_count(Csr K, CountRows cr, const u
                 for (long long p = p0 + lane; p < p1; p += FEAS_U * SUB) {
                     int c[FEAS_U];
 #pragma unroll
-                    for (int f = 0; f < FEAS_U; ++f) c[f] = p + f * SUB < p1 ? __ldg(K.idx + p + f * SUB) : -1;
+                    for (int f = 0; f < FEAS_U; ++f) c[f] = p + f * SUB < p1 ? ld_hint_i32(K.idx + p + f * SUB, pfirst) : -1;
                     uint64_t v[FEAS_U][WV];
 #pragma unroll
                     for (int f = 0; f < FEAS_U; ++f) {
-                        if (c[f] >= 0) load_words<WV>(X + (long long)c[f] * W + w0, v[f]);
+                        if (c[f] >= 0) load_words<WV>(X + (long long)c[f] * W + w0, v[f], plast);
                         else
 #pragma unroll
                             for (int u = 0; u < WV; ++u) v[f][u] = 0ull;
@@ -389,36 +479,77 @@ __device__ __forceinline__ unsigned transpose32(unsigned x, int lane) {
     return x;
 }
 
-__global__ void __launch_bounds__(256) k_obj_bits(long long n, int vchunks_per_job, const unsigned* __restrict__ planes,
+// One CTA of 8 warps per (chunk range, word group of WV words): every lane loads its variable's WV
+// words with one vector load, each warp walks chunks cta*cpc + warp + 8k (two at a time, loads
+// first), and the 8 warps' int64 lane sums are added in shared memory in a fixed order, giving ONE
+// partial row per CTA column block: zpart[blockIdx.x][64*w + lane] (k_obj_final adds gridDim.x rows).
+template <int WV>
+__global__ void __launch_bounds__(256) k_obj_bits(long long n, long long cpc, const unsigned* __restrict__ planes,
                                                   int NB, long long cmin, const uint64_t* __restrict__ X, int W,
-                                                  long long* __restrict__ zpart /*[njob_per_word][64W]*/) {
-    const int lane = threadIdx.x & 31;
-    const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-    const long long nwarps = (gridDim.x * (long long)blockDim.x) >> 5;
+                                                  long long* __restrict__ zpart /*[gridDim.x][64W]*/) {
+    __shared__ long long sacc[8][64 * WV];
+    const uint64_t pdem = l2_policy_evict_first();  // last reader of the batch: demote it in L2
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int w0 = blockIdx.y * WV;
     const long long nchunk32 = (n + 31) / 32;
-    const long long jobs_per_word = (nchunk32 + vchunks_per_job - 1) / vchunks_per_job;
-    for (long long job = warp; job < jobs_per_word * W; job += nwarps) {
-        const int w = (int)(job % W);
-        const long long jr = job / W;
-        const long long c0 = jr * vchunks_per_job, c1 = min(nchunk32, c0 + vchunks_per_job);
-        long long alo = 0, ahi = 0;
-        for (long long ch = c0; ch < c1; ++ch) {
-            const long long i = ch * 32 + lane;
-            const uint64_t xw = i < n ? __ldg(X + i * W + w) : 0ull;
-            const unsigned tlo = transpose32((unsigned)xw, lane);
-            const unsigned thi = transpose32((unsigned)(xw >> 32), lane);
-            long long slo = 0, shi = 0;
-            for (int b = 0; b < NB; ++b) {
-                const unsigned pl = __ldg(planes + ch * NB + b);
-                slo += (long long)__popc(tlo & pl) << b;
-                shi += (long long)__popc(thi & pl) << b;
+    const long long c0 = blockIdx.x * cpc, c1 = min(nchunk32, c0 + cpc);
+    long long alo[WV], ahi[WV];
+#pragma unroll
+    for (int v = 0; v < WV; ++v) alo[v] = ahi[v] = 0;
+    auto load = [&](long long ch, uint64_t (&xw)[WV]) {
+        const long long i = ch * 32 + lane;
+        if (ch < c1 && i < n) {
+            if constexpr (WV == 2) {
+                const ulonglong2 a = ld_hint_u64x2(X + i * W + w0, pdem);
+                xw[0] = a.x; xw[1] = a.y;
+            } else {
+                xw[0] = ld_hint_u64(X + i * W + w0, pdem);
             }
-            alo += slo + cmin * __popc(tlo);
-            ahi += shi + cmin * __popc(thi);
+        } else {
+#pragma unroll
+            for (int v = 0; v < WV; ++v) xw[v] = 0ull;
         }
-        long long* zp = zpart + jr * 64LL * W + 64LL * w;
-        zp[lane] = alo;
-        zp[32 + lane] = ahi;
+    };
+    auto consume = [&](long long ch, const uint64_t (&xw)[WV]) {
+        if (ch >= c1) return;
+        unsigned tlo[WV], thi[WV];
+#pragma unroll
+        for (int v = 0; v < WV; ++v) {
+            tlo[v] = transpose32((unsigned)xw[v], lane);
+            thi[v] = transpose32((unsigned)(xw[v] >> 32), lane);
+        }
+        int slo[WV], shi[WV];
+#pragma unroll
+        for (int v = 0; v < WV; ++v) { slo[v] = 0; shi[v] = 0; }
+        for (int b = 0; b < NB; ++b) {
+            const unsigned pl = __ldg(planes + ch * NB + b);
+#pragma unroll
+            for (int v = 0; v < WV; ++v) {
+                slo[v] += __popc(tlo[v] & pl) << b;
+                shi[v] += __popc(thi[v] & pl) << b;
+            }
+        }
+#pragma unroll
+        for (int v = 0; v < WV; ++v) {
+            alo[v] += (long long)slo[v] + cmin * __popc(tlo[v]);
+            ahi[v] += (long long)shi[v] + cmin * __popc(thi[v]);
+        }
+    };
+    for (long long ch = c0 + wib; ch < c1; ch += 16) {
+        uint64_t xa[WV], xb[WV];
+        load(ch, xa);
+        load(ch + 8, xb);
+        consume(ch, xa);
+        consume(ch + 8, xb);
+    }
+#pragma unroll
+    for (int v = 0; v < WV; ++v) { sacc[wib][64 * v + lane] = alo[v]; sacc[wib][64 * v + 32 + lane] = ahi[v]; }
+    __syncthreads();
+    if (threadIdx.x < 64 * WV) {
+        long long t = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) t += sacc[k][threadIdx.x];
+        zpart[blockIdx.x * 64LL * W + 64LL * w0 + threadIdx.x] = t;
     }
 }
 

@@ -56,9 +56,11 @@ inline NcclApi& nccl() {
 
 // rec[0] = best z of this rank's batch (+inf if none), rec[1] = its global sample index,
 // rec[2] = 1 if a feasible candidate exists.  Single block of 256 threads.
+// rec[3] = 1 if this rank's own time limit has passed (or a test forces it from block force_blk on):
+// the flags are OR-ed by the merge, so every rank halts at the same block (CheckHalt L38-40).
 __global__ void __launch_bounds__(256) k_local_record(const double* __restrict__ z, const unsigned long long* __restrict__ viol,
                                                       long long lanes, long long word_off, Ctrl* __restrict__ ctrl,
-                                                      double* __restrict__ rec) {
+                                                      double* __restrict__ rec, int count_round, long long force_blk) {
     __shared__ double sz[256];
     __shared__ long long sl[256];
     double bz = INFINITY;
@@ -80,22 +82,25 @@ __global__ void __launch_bounds__(256) k_local_record(const double* __restrict__
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        ctrl->rounds += 1;
+        if (count_round) ctrl->rounds += 1;
         const long long l = sl[0];
         rec[0] = l >= 0 ? sz[0] : INFINITY;
         rec[1] = l >= 0 ? (double)(64 * word_off + l) : -1.0;
         rec[2] = l >= 0 ? 1.0 : 0.0;
-        rec[3] = 0.0;
+        const bool late = globaltimer_ns() >= ctrl->deadline_ns || (force_blk >= 0 && ctrl->blk >= force_blk);
+        rec[3] = late ? 1.0 : 0.0;
     }
 }
 
-// identical on every rank: pick the winner record, update the incumbent iff strictly better
+// identical on every rank: pick the winner record, update the incumbent iff strictly better; OR the
+// time-limit flags
 __global__ void k_merge_records(const double* __restrict__ all, int world, Ctrl* __restrict__ ctrl, long long kint,
                                 int r, int kr, long long* __restrict__ regen /* [0]=global index or -1, [1]=round */) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     int best = -1;
     for (int q = 0; q < world; ++q) {
         const double* rq = all + 4 * q;
+        if (rq[3] != 0.0) ctrl->tl_any = 1;  // some rank's time limit passed: all ranks halt after this block
         if (rq[2] == 0.0) continue;
         if (best < 0 || rq[0] < all[4 * best] || (rq[0] == all[4 * best] && rq[1] < all[4 * best + 1])) best = q;
     }

@@ -59,13 +59,19 @@ def test_config5_run_invariants_and_sampled_parity(gf, cfg5):
     assert f1 and fg.all() and zg[0] == z1 == inst["c"].sum()
 
 
-def test_config5_one_step_parity_full_size(gf, cfg5):
-    """One Alg. 2 step at full size from an identical state (oracle preprocess to 1e-12)."""
+@pytest.fixture(scope="module")
+def cfg5_tight(cfg5):
     inst, _, _, o = cfg5
+    oc = o.preprocess(tol=1e-12, max_iter=2000)
+    return inst, o, oc
+
+
+def test_config5_one_step_parity_full_size(gf, cfg5_tight):
+    """One Alg. 2 step at full size from an identical state (oracle preprocess to 1e-12)."""
+    inst, o, oc = cfg5_tight
     s = gf.Solver(0)
     s.load(inst)
     s.preprocess(precision=64, tol=1e-12, max_iter=2000)
-    oc = o.preprocess(tol=1e-12, max_iter=2000)
     rng = np.random.default_rng(3)
     x = rng.random(inst["n"]); xb = rng.random(inst["n"]); y = rng.random(inst["m"]) * 1e-3
     s.set_state(x, xb, y)
@@ -77,6 +83,29 @@ def test_config5_one_step_parity_full_size(gf, cfg5):
     assert np.linalg.norm(xg - xo) <= 1e-10 * np.linalg.norm(xo)
     assert np.linalg.norm(yg - yo) <= 1e-10 * max(np.linalg.norm(yo), 1e-30)
     assert oc["zero_rows"] == 0
+    d = np.abs(xg - xo) / np.maximum(np.abs(xo), 1e-3)
+    assert d.max() <= 1e-10, d.max()
+
+
+def test_config5_one_step_parity_full_size_fp32(gf, cfg5_tight):
+    """The bench's precision: one fp32 step at full size (multi-block row kernels, 2.4e4 row blocks)
+    from an fp32-representable state; every element within 1e-6 of the oracle's fp64 step."""
+    inst, o, _ = cfg5_tight
+    s = gf.Solver(0)
+    s.load(inst)
+    s.preprocess(precision=32, tol=1e-12, max_iter=2000)
+    rng = np.random.default_rng(4)
+    f32 = lambda v: v.astype(np.float32).astype(np.float64)  # noqa: E731
+    x = f32(rng.random(inst["n"])); xb = f32(rng.random(inst["n"])); y = f32(rng.random(inst["m"]) * 1e-3)
+    s.set_state(x, xb, y)
+    o.set_state(x, xb, y)
+    s.step(1, 0.01, 0.99 ** 0.5, 0.99 ** 0.5)
+    o.step(0.01, 0.99 ** 0.5, 0.99 ** 0.5)
+    xg, xbg, yg = s.get_state()
+    xo, xbo, yo = o.get_state()
+    for g, v in ((xg, xo), (xbg, xbo), (yg, yo)):
+        d = np.abs(g - v) / np.maximum(np.abs(v), 1e-3)
+        assert d.max() <= 1e-6, d.max()
 
 
 @pytest.mark.parametrize("cfg", [2, 3, 4])

@@ -66,3 +66,92 @@ def test_nccl_exchange_config1_incumbent(gf):
     _, i0, (z0, x0, m0) = _solve(gf, inst, max_iters=2000)
     _, i1, (z1, x1, m1) = _solve(gf, inst, max_iters=2000, rank=0, world=1, nccl_id=nid)
     assert z0 == z1 and np.array_equal(x0, x1) and i0["iters"] == i1["iters"]
+
+
+# ----------------------------------------------------------------------------- loopback ranks
+def _loop(gf, inst, R, graph=1, opts=(), **kw):
+    s = gf.Solver(0, world=R, loopback=True)
+    for k, v in opts:
+        s.set_option(k, v)
+    s.load(inst)
+    s.preprocess()
+    info = s.run(use_graph=graph, trace_cap=4096, **kw)
+    return s, info, s.best_incumbent()
+
+
+@pytest.mark.parametrize("R", [2, 4, 8])
+@pytest.mark.parametrize("graph", [1, 0])
+def test_loopback_ranks_equal_one_rank_with_R_times_k_b(gf, R, graph):
+    """SURVEY §4(i) / App. B rank invariance: R ranks with k_b each, exchanging records through the
+    merge (record -> merge -> Philox regeneration of the winner -> CheckHalt), reproduce one rank with
+    R*k_b bit for bit: iterations, halt reason, rounds, incumbent (z, x, iteration, round, global
+    index) and the whole trace."""
+    inst = G.SMALL["setcover"](2)
+    kw = dict(max_iters=600, k_b=64)
+    s1 = gf.Solver(0)
+    s1.load(inst)
+    s1.preprocess()
+    i1 = s1.run(use_graph=graph, trace_cap=4096, max_iters=600, k_b=64 * R)
+    z1, x1, m1 = s1.best_incumbent()
+    s, iR, (zR, xR, mR) = _loop(gf, inst, R, graph, **kw)
+    assert (i1["iters"], i1["halt_reason"], i1["rounds"]) == (iR["iters"], iR["halt_reason"], iR["rounds"])
+    assert iR["candidates"] == i1["candidates"]
+    assert z1 == zR or (math.isinf(z1) and math.isinf(zR))
+    assert np.array_equal(x1, xR)
+    assert (m1["found_iter"], m1["found_round"], m1["found_index"]) == (mR["found_iter"], mR["found_round"], mR["found_index"])
+    assert np.array_equal(s1.trace(), s.trace())
+
+
+@pytest.mark.parametrize("R,rank,blk", [(2, 1, 3), (4, 2, 5), (8, 7, 0)])
+@pytest.mark.parametrize("graph", [1, 0])
+def test_loopback_time_limit_flag_halts_every_rank_together(gf, R, rank, blk, graph):
+    """CheckHalt's time limit must be agreed: one rank whose clock passes its deadline
+    during block `blk` flags it in its record, the merge ORs the flags, and the loop (of every rank)
+    stops after that block with halt reason 3 — never with one rank leaving the exchange early."""
+    inst = G.SMALL["setcover"](3)
+    _, info, _ = _loop(gf, inst, R, graph, opts=[("force_deadline_rank", rank), ("force_deadline_block", blk)],
+                       max_iters=1000, k_b=64, **FIXED)
+    assert info["halt_reason"] == 3
+    assert info["iters"] == (blk + 1) * 10
+
+
+def test_loopback_real_time_limit(gf):
+    """A time limit that has already passed when the first record is written halts after block 1."""
+    inst = G.SMALL["setcover"](1)
+    _, info, _ = _loop(gf, inst, 4, 1, max_iters=1000, k_b=64, time_limit_s=1e-9, **FIXED)
+    assert info["halt_reason"] == 3 and info["iters"] == 10
+
+
+def test_nccl_path_time_limit_flag(gf):
+    """The same agreement on the NCCL path (1-rank communicator: its own flag goes through the
+    all-gather and the merge)."""
+    try:
+        nid = gf.nccl_unique_id()
+    except gf.GforsError:
+        pytest.skip("libnccl.so.2 not loadable")
+    inst = G.SMALL["setcover"](1)
+    s = gf.Solver(0, rank=0, world=1, nccl_id=nid)
+    s.set_option("force_deadline_rank", 0).set_option("force_deadline_block", 2)
+    s.load(inst)
+    s.preprocess()
+    info = s.run(max_iters=1000, k_b=64, **FIXED)
+    assert info["halt_reason"] == 3 and info["iters"] == 30
+
+
+def test_capture_failure_falls_back_to_eager_loop(gf):
+    """If the loop graph cannot be captured (e.g. a collective that cannot live in a conditional
+    body) the sharded run falls back to the eager loop with identical results."""
+    inst = G.SMALL["setcover"](2)
+    _, i0, (z0, x0, m0) = _loop(gf, inst, 2, 1, max_iters=400, k_b=64)
+    s, i1, (z1, x1, m1) = _loop(gf, inst, 2, 1, opts=[("force_capture_fail", 1)], max_iters=400, k_b=64)
+    assert "forced capture failure" in s.graph_note()
+    assert (i0["iters"], i0["halt_reason"], i0["rounds"]) == (i1["iters"], i1["halt_reason"], i1["rounds"])
+    assert z0 == z1 or (math.isinf(z0) and math.isinf(z1))
+    assert np.array_equal(x0, x1)
+    assert (m0["found_iter"], m0["found_round"], m0["found_index"]) == (m1["found_iter"], m1["found_round"], m1["found_index"])
+
+
+def test_set_option_rejects_unknown_key(gf):
+    s = gf.Solver(0)
+    with pytest.raises(gf.GforsError, match="unknown key"):
+        s.set_option("no_such_option", 1)
