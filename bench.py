@@ -32,14 +32,19 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "PDHG iters/s and sampled candidates evaluated/s; time-to-incumbent at 1/2/4/8 B200"
-GATHER_CEILING_G = 271.0  # random 4-byte gathers/s (x1e9) on B200, profiles/r01_gather_microbench.txt
+# measured random-gather ceilings (x1e9 gathers/s) on B200, profiles/gather_bench.cu ->
+# profiles/r02_gather_microbench.txt: 4-byte elements from a 20 MB vector (x-bar of the PDHG dual,
+# cp.async 2048-chunk recipe) and 16-byte elements from an 80 MB vector (the k_b = 128 sample batch
+# read by the feasibility kernel, cp.async 1024-chunk recipe)
+GATHER_CEILING_G = 253.9
+GATHER16_CEILING_G = 211.6
 UNIT = "candidates/s"
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--seed", type=int, default=1)
@@ -203,42 +208,54 @@ def inst_meta(inst):
 
 
 # ------------------------------------------------------------------------------------------------
-def oracle_block_seconds(inst, k_int, k_b, budget_s=20.0, seed=20251030):
-    """Time the CPU oracle (as it stands) on a bounded sample of the workload and compose the time of
-    one Alg. 1 block: k_int PDHG iterations + k_b sampled candidates (sampling + evaluation).
-    PDHG: whole iterations on the full instance.  Sampling: a fixed subset of variables (the per-
-    variable cost is uniform); evaluation: a few candidate lanes (each lane evaluates every row)."""
+def _oracle_one_block(o, k_int, k_b, seed):
+    """One real Alg. 1 block of the oracle as it stands (orc_run: k_int PDHG iterations, sampling of k_b
+    candidates, EvalBest, indicators, CheckHalt); returns its wall time."""
     from oracle import oracle as O
+    prm = O.params(k_int=k_int, k_b=k_b, max_iters=k_int, tol_primal=-1.0, tol_dual=-1.0, tol_binary=-1.0,
+                   stall_rel=-1.0, seed=seed)
     t0 = time.perf_counter()
+    o.run(prm)
+    return time.perf_counter() - t0
+
+
+def oracle_baseline(inst, k_int, seed=20251030, max_procs=32):
+    """cpu_baseline: the CPU oracle as it stands on the FULL instance, one real Alg. 1 block with
+    k_b = 64 candidates (the bounded sample: 64 instead of 128 candidates per block; Preprocess
+    bounded to 5 power iterations, excluded from the time as in PAPER L193).
+    1 core: one process.  All host cores: the same block in os.cpu_count() forked processes at
+    once (copy-on-write instance, each its own candidates: weak scaling over cores), candidates/s =
+    procs * 64 / wall."""
+    from oracle import oracle as O
     o = O.Oracle(inst)
-    o.preprocess(max_iter=5)  # scaling accuracy is irrelevant for timing; bounded
-    o.state_init()
-    n = inst["n"]
-    nnz = int(inst["k_rowptr"][-1])
-    iters = 1 if nnz > 5_000_000 else 5
-    ts = time.perf_counter()
-    for _ in range(iters):
-        o.step(1e-3, 0.99 ** 0.5, 0.99 ** 0.5)
-    t_iter = (time.perf_counter() - ts) / iters
-    x = o.get_state()[0]
-    nsub = min(n, 20000)
-    idx = np.linspace(0, n - 1, nsub).astype(np.int64)
-    ts = time.perf_counter()
-    O.sample_subset(x[idx], idx, seed, 0, 0, max(1, k_b // 64))
-    t_samp_var = (time.perf_counter() - ts) / nsub  # per variable, all k_b lanes
-    lanes = 64
-    full_bits = np.zeros((n, 1), dtype=np.uint64)
-    rng = np.random.default_rng(seed)
-    full_bits[:, 0] = rng.integers(0, 2**63, size=n, dtype=np.int64).astype(np.uint64)
-    ts = time.perf_counter()
-    o.eval(full_bits)
-    t_eval_lane = (time.perf_counter() - ts) / lanes
-    t_block = k_int * t_iter + n * t_samp_var + k_b * t_eval_lane
-    return {"t_block": t_block, "t_iter": t_iter, "t_sample_per_var": t_samp_var, "t_eval_per_lane": t_eval_lane,
-            "wall_s": time.perf_counter() - t0,
-            "sample": (f"full instance; {iters} PDHG iteration(s) timed, sampling timed on {nsub} of {n} variables "
-                       f"({k_b} lanes), evaluation timed on 64 lanes; block time composed as "
-                       f"k_int*t_iter + n*t_sample_var + k_b*t_eval_lane")}
+    o.preprocess(max_iter=5)
+    t1 = _oracle_one_block(o, k_int, 64, seed)
+    procs = max(1, min(os.cpu_count() or 1, max_procs))
+    all_cores = None
+    if procs > 1 and hasattr(os, "fork"):
+        t0 = time.perf_counter()
+        pids = []
+        for p in range(procs):
+            pid = os.fork()
+            if pid == 0:
+                try:
+                    _oracle_one_block(o, k_int, 64, seed + p)
+                finally:
+                    os._exit(0)
+            pids.append(pid)
+        ok = all(os.waitpid(pid, 0)[1] == 0 for pid in pids)
+        wall = time.perf_counter() - t0
+        if ok:
+            all_cores = {"value": procs * 64 / wall, "cores": procs, "wall_s": wall}
+    try:
+        model = [l.split(":", 1)[1].strip() for l in subprocess.run(["lscpu"], capture_output=True, text=True).stdout.splitlines()
+                 if l.startswith("Model name")][0]
+    except Exception:
+        model = None
+    return {"t_block": t1, "value": 64 / t1, "all_cores": all_cores, "cpu_model": model,
+            "sample": (f"oracle (1 thread, as it stands) Alg. 1 on the full config instance: one block of {k_int} PDHG "
+                       f"iterations + sampling and EvalBest of 64 candidates (k_b = 64 instead of 128) + indicators + "
+                       f"CheckHalt; Preprocess bounded to 5 power iterations and not timed")}
 
 
 def scaled_instance(cfg, seed, f):
@@ -280,13 +297,14 @@ def run_reference(args):
     o.preprocess(max_iter=50)
     prm = O.params(k_int=args.k_int, k_b=k_b_total, max_iters=args.k_int, tol_primal=-1.0, tol_dual=-1.0,
                    tol_binary=-1.0, stall_rel=-1.0)
-    times = []
+    times, raw = [], []
     for st in range(nsteps):
         t0 = time.perf_counter()
         o.run(prm)
         dt = time.perf_counter() - t0
         if st >= args.warmup:
             times.append(dt / f)
+            raw.append(dt)
     t = statistics.median(times)
     value = k_b_total / t
     full = inst_meta(make_instance(args.config, args.seed)) if f < 1.0 else inst_meta(inst)
@@ -296,6 +314,9 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "pdhg_iters_per_s": args.k_int / t,
+            "extrapolation": {"size_fraction": f, "ms_per_step_measured": statistics.median(raw) * 1e3,
+                              "note": "each step is one real oracle block on the size-f instance of the same recipe; "
+                                      "ms_per_step = measured / f (cost linear in the instance size)"},
             "config": {"workload": f"config{args.config}", "n": full["n"], "m": full["m"], "nnz": full["nnz"],
                        "k_int": args.k_int, "k_b_per_rank": args.k_b, "seed": args.seed},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
@@ -548,6 +569,47 @@ def run_gpu(args):
     iters_s = args.steps * args.k_int / t_s
     z, _, inc = s.best_incumbent(want_x=False)
 
+    # phases of the trajectory (the per-block cost falls as the iterate sparsifies and the
+    # push modes engage, so the headline depends on K): blocks 1..K from x0 is what --steps K times
+    # (the headline); the steady window 181..200 is t(200 blocks) - t(180 blocks), same clock
+    phases = None
+    if rank == 0 and world == 1:
+        def run_ms(blocks):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            s.run(max_iters=blocks * args.k_int, **common)
+            b.record(stream)
+            torch.cuda.synchronize()
+            return a.elapsed_time(b)
+        t200, t180 = run_ms(200), run_ms(180)
+        phases = {"blocks_1_to_K": {"K": args.steps, "candidates_per_s": value, "ms_per_block": ms / args.steps},
+                  "blocks_181_to_200": {"candidates_per_s": 20 * args.k_b / ((t200 - t180) * 1e-3),
+                                        "ms_per_block": (t200 - t180) / 20,
+                                        "how": "t(200 blocks from x0) - t(180 blocks from x0), CUDA events"},
+                  "blocks_1_to_200": {"candidates_per_s": 200 * args.k_b / (t200 * 1e-3), "ms_per_block": t200 / 200}}
+
+    # PDHG alone (sampling off): Alg. 2 steps through the step hook (same kernels, eager launches),
+    # fixed rho = rho_min, from x0 (dense phase: iterations 1-100) and after 1000 steps (1001-1100)
+    pdhg_only = None
+    if rank == 0 and world == 1:
+        x0 = np.full(meta["n"], 0.5)
+        s.set_state(x0, x0, np.zeros(meta["m"]))
+        tau = 0.99 ** 0.5
+        def steps_ms(k):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            s.step(k, 1e-3, tau, tau)
+            b.record(stream)
+            torch.cuda.synchronize()
+            return a.elapsed_time(b)
+        d = steps_ms(100)
+        s.step(900, 1e-3, tau, tau)
+        l = steps_ms(100)
+        pdhg_only = {"iters_1_100_per_s": 100 / (d * 1e-3), "iters_1001_1100_per_s": 100 / (l * 1e-3),
+                     "how": "gfors_step hook (eager launches, rho = 1e-3 fixed, no sampling), CUDA events"}
+
     # time-to-incumbent on the headline workload: the default (Alg. 3) sampler finds no feasible set
     # cover within the run; with the cover completion of the samples (R27) every lane is feasible
     cover = None
@@ -587,6 +649,28 @@ def run_gpu(args):
     if os.path.exists(tpath):
         tj = json.load(open(tpath))
         traffic = tj.get(f"config{args.config}_fp{args.precision}", {}).get(dom)
+
+    # EvalBest + RandSampleStep per round (k_b candidates): algorithmic bytes with the batch X materialised
+    # (DESIGN §6): sampler reads p (n fb) and writes X (n W 8); feasibility streams the indices of the
+    # count rows (4 nnz + 4 m) and reads X once (gathers assumed cache hits); the objective reads X and
+    # the coefficient planes (n NB/8, NB = 7 for c in [1, 100]).  The binding limits are the 16-byte
+    # random gathers of the feasibility kernel (one per nonzero) and the sampler's Philox ALU work.
+    W = args.k_b // 64
+    ev_ms = {k: prof.get(k, 0.0) for k in ("sample", "feas", "obj")}
+    ev_total = sum(ev_ms.values())
+    ev_bytes = meta["n"] * fb + meta["n"] * W * 8 + (4 * meta["nnz"] + 4 * meta["m"] + meta["n"] * W * 8) \
+        + (meta["n"] * W * 8 + meta["n"] * 7 // 8)
+    evaluator = None
+    if ev_total > 0:
+        feas_g = meta["nnz"] * max(1, W // 2) / (ev_ms["feas"] * 1e-3) / 1e9 if ev_ms["feas"] else None
+        evaluator = {"kernels": "k_sample_thr+k_sample, k_feas_skip+k_feas_rb, k_obj_bits+k_obj_final",
+                     "ms_per_round": ev_total, "ms_by_class": ev_ms, "algorithmic_bytes_per_round": ev_bytes,
+                     "achieved": ev_bytes / (ev_total * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                     "frac": ev_bytes / (ev_total * 1e-3) / 1e9 / peak,
+                     "feas_gather": {"gathers_per_round": meta["nnz"] * max(1, W // 2), "bytes_per_gather": 16 if W % 2 == 0 else 8,
+                                     "achieved_G_per_s": feas_g, "ceiling_G_per_s": GATHER16_CEILING_G,
+                                     "frac": feas_g / GATHER16_CEILING_G if feas_g else None},
+                     "window": f"blocks 1..{args.profile_blocks or args.steps} from x0 (eager replay with per-launch events)"}
 
     # the streaming column pass of the push-mode primal (k_primal_push), the largest non-gather kernel
     # of the steady state: bytes if every column is streamed (stationary columns are skipped, so
@@ -667,9 +751,9 @@ def run_gpu(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        est = oracle_block_seconds(inst, args.k_int, args.k_b)
-        cpu = {"value": args.k_b / est["t_block"], "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": est["sample"], "pdhg_iters_per_s": 1.0 / est["t_iter"],
+        ob = oracle_baseline(inst, args.k_int)
+        cpu = {"value": ob["value"], "unit": UNIT, "cores": 1, "kind": "oracle", "sample": ob["sample"],
+               "ms_per_block": ob["t_block"] * 1e3, "all_host_cores": ob["all_cores"], "cpu_model": ob["cpu_model"],
                "host_cpu_count": os.cpu_count()}
 
     if rank == 0:
@@ -694,6 +778,9 @@ def run_gpu(args):
                          "gather": {"gathers_per_launch": meta["nnz"], "achieved_G_per_s": meta["nnz"] / (per_launch_ms * 1e-3) / 1e9,
                                     "ceiling_G_per_s": GATHER_CEILING_G, "frac": meta["nnz"] / (per_launch_ms * 1e-3) / 1e9 / GATHER_CEILING_G}},
             "roofline_push_primal_column_pass": col,
+            "roofline_evaluator": evaluator,
+            "phases": phases,
+            "pdhg_only": pdhg_only,
             "kernel_ms_per_step": prof, "kernel_share": {k: v / step_ms for k, v in prof.items()} if step_ms else {},
             "kernel_active": {k: {"active_launches": v[1], "avg_active_ms": (v[0] / v[1]) if v[1] else None}
                               for k, v in act.items()},

@@ -179,12 +179,14 @@ struct DirPlan {  // how one product direction (K rows or K' columns) is compute
     DevSeg ds;
     long long* blk_row = nullptr;
     long long nblk = 0;
+    int4* desc = nullptr;    // per row block {first row, rows | log2(G) << 16, first nonzero, nonzeros} (k_dual_rb)
+    int* ptr32 = nullptr;    // int32 copy of the row pointers (nnz < 2^31)
 };
 
 // greedy nonzero-balanced row blocks: consecutive rows, <= cap nonzeros each (rows <= cap long)
 // rows per row block at most (empty rows, e.g. every column when m = 0, would otherwise pile into
 // one CTA: max cut's primal took 84 us per launch for n = 20480 in a single block)
-constexpr long long RB_ROWS_MAX = 512;
+constexpr long long RB_ROWS_MAX = RB_RMAX;  // per-row data of a block is staged in smem (k_dual_rb)
 
 static std::vector<long long> make_rowblocks_from(const std::vector<int64_t>& ptr, long long rows, long long cap,
                                                   long long cap_rows = LLONG_MAX) {
@@ -203,6 +205,23 @@ static std::vector<long long> make_rowblocks_from(const std::vector<int64_t>& pt
 static std::vector<long long> make_rowblocks(const std::vector<int64_t>& ptr, long long rows, long long cap,
                                              long long cap_rows = LLONG_MAX) {
     return make_rowblocks_from(ptr, rows, cap, cap_rows);
+}
+
+// descriptors of the row blocks for k_dual_rb (G = 2^lg lanes per row, the largest power of two <= 32
+// with G * rows <= RB_NT)
+int4* upload_desc(const std::vector<long long>& b, const std::vector<int64_t>& ptr, cudaStream_t s,
+                  std::vector<void*>& owned) {
+    const long long nb = (long long)b.size() - 1;
+    std::vector<int4> desc((size_t)std::max<long long>(nb, 1));
+    for (long long k = 0; k < nb; ++k) {
+        const int nr = (int)(b[k + 1] - b[k]);
+        int lg = 5;
+        while (lg > 0 && (1 << lg) * nr > RB_NT) --lg;
+        desc[k] = make_int4((int)b[k], nr | (lg << 16), (int)ptr[b[k]], (int)(ptr[b[k + 1]] - ptr[b[k]]));
+    }
+    int4* dd = dupload(desc, s);
+    owned.push_back(dd);
+    return dd;
 }
 
 DirPlan plan_direction(const std::vector<int64_t>& ptr, long long rows, cudaStream_t s,
@@ -231,6 +250,10 @@ DirPlan plan_direction(const std::vector<int64_t>& ptr, long long rows, cudaStre
         d.nblk = (long long)b.size() - 1;
         d.blk_row = dupload(b, s);
         owned.push_back(d.blk_row);
+        d.desc = upload_desc(b, ptr, s, owned);
+        std::vector<int> p32(ptr.begin(), ptr.begin() + rows + 1);
+        d.ptr32 = dupload(p32, s);
+        owned.push_back(d.ptr32);
     }
     if (d.seg) {
         long long L = 1024;
@@ -265,6 +288,7 @@ DirPlan plan_direction64(const DirPlan& d32, const std::vector<int64_t>& ptr, lo
     d.nblk = (long long)b.size() - 1;
     d.blk_row = dupload(b, s);
     owned.push_back(d.blk_row);
+    d.desc = upload_desc(b, ptr, s, owned);
     return d;
 }
 
@@ -922,8 +946,8 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
             double* u_out = (kint == 0 || j == kint - 1) ? C->d_u : nullptr;
             auto gather = [&](cudaStream_t q) {
                 KIND_SWITCH(C->kkind, LAUNCH(C, q, KC_DUAL,
-                    (k_dual_rb<T, KINDV><<<grid, RB_NT, 0, q>>>(csr_K(C), C->pd.blk_row, C->pd.nblk, st, g, rh, C->d_rsign,
-                                                                C->m1p, ctrl, kint, j, u_out, pl))));
+                    (k_dual_rb<T, KINDV><<<grid, RB_NT, 0, q>>>(csr_K(C), C->pd.desc, C->pd.ptr32, C->pd.nblk, st, g, rh,
+                                                                C->d_rsign, C->m1p, ctrl, kint, j, u_out, pl))));
             };
             if (C->push_dual) {
                 // sparse xbar: scatter the listed columns into the row accumulators, then the rows

@@ -118,15 +118,41 @@ __device__ __forceinline__ double rb_row_sum(const Csr& A, const T* sv, long lon
 // ---------------------------------------------------------------------------------------------
 // Dual half-step on row blocks of K_u:
 //   y_k = Pi( y_{k-1} + tau2 (K xbar_{k-1} + r) ),  K = -diag(g) K_u,  w = g rsign y_k
+// Nothing on the issue path waits on a dependent load: each row block has a 16-byte descriptor
+// {first row, rows | log2(G) << 16, first nonzero, nonzeros} (host-built, int32: nnz < 2^31); a CTA loads the
+// descriptor of unit b + 3*grid and the column indices of b + 2*grid while it reduces unit b, and at
+// the top of each iteration issues unit b + grid at once: one cp.async per nonzero (x-bar gather),
+// plus cp.async copies of the block's row pointers and sign bytes, so the reduction reads only shared
+// memory; the per-row y, g, r-hat loads of the epilogue are issued before the row's reduction.  The
+// shared-memory footprint stays ~18 KB per CTA: the L1 left over tracks the in-flight 4-byte gathers
+// (at ~26 KB per CTA x 8 CTAs the dual ran 1.8x slower).
 // ---------------------------------------------------------------------------------------------
+constexpr int RB_RMAX = 192;  // rows per row block (the plans cap them; per-row data lives in smem)
+
+template <typename T>
+struct DualBuf {  // (ordered so every member is naturally aligned for its cp.async)
+    T tile[RB_NNZ_OF<T>];
+    int4 d;                    // the unit's descriptor
+    int rp[RB_RMAX + 1];
+    int sgw[RB_RMAX / 4 + 2];  // sign bytes, 4-byte aligned window starting at row (r0 & ~3)
+};
+
+__device__ __forceinline__ void cp_async4(void* smem, const void* g) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(g));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* g) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(g));
+}
+
 template <typename T, int KIND>
-__global__ void __launch_bounds__(RB_NT) k_dual_rb(Csr K, const long long* __restrict__ blk_row, long long nblk,
-                                                   State<T> s, const double* __restrict__ g,
+__global__ void __launch_bounds__(RB_NT, 8) k_dual_rb(Csr K, const int4* __restrict__ desc, const int* __restrict__ ptr32,
+                                                   long long nblk, State<T> s, const double* __restrict__ g,
                                                    const double* __restrict__ rh, const signed char* __restrict__ rsign,
                                                    long long m1, const Ctrl* __restrict__ ctrl, long long kint,
                                                    long long j, double* __restrict__ u_out, PushList pl) {
     constexpr int NZ = RB_NNZ_OF<T>;
-    __shared__ __align__(16) T sv[2][NZ];
+    constexpr int U = NZ / RB_NT;
+    __shared__ __align__(16) DualBuf<T> buf[2];
     const long long kk = iter_index(ctrl, kint, j);
     const int par = (int)(kk & 1);
     if (push_mode(pl, par)) return;  // sparse xbar: k_push_scatter/k_push_rows do this iteration
@@ -136,31 +162,66 @@ __global__ void __launch_bounds__(RB_NT) k_dual_rb(Csr K, const long long* __res
     const T* __restrict__ yin = par ? s.y[1] : s.y[0];
     T* __restrict__ yout = par ? s.y[0] : s.y[1];
     const double tau2 = ctrl->tau2;
+    const long long G0 = gridDim.x;
+    auto ldesc = [&](long long b) { return b < nblk ? __ldg(desc + b) : make_int4(0, 0, 0, 0); };
+    int cols[U];
+    auto load = [&](const int4& d) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int t = u * RB_NT + threadIdx.x;
+            cols[u] = t < d.w ? ldcs_i32(K.idx + d.z + t) : -1;
+        }
+    };
+    auto issue = [&](long long b, const int4& d, int bi) {
+        DualBuf<T>& B = buf[bi];
+        if (b < nblk) {
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (cols[u] >= 0) cp_async_elem(B.tile + u * RB_NT + threadIdx.x, xb + cols[u]);
+            const int nr = d.y & 0xffff, r0 = d.x, t = threadIdx.x;
+            if (t <= nr) cp_async4(&B.rp[t], ptr32 + r0 + t);
+            if constexpr (KIND == KV_SIGN) {
+                const int a0 = r0 & ~3;
+                if (t < ((r0 + nr - a0) + 3) / 4) cp_async4(&B.sgw[t], rsign + a0 + 4 * t);
+            }
+            if (t == 0) B.d = d;
+        }
+        asm volatile("cp.async.commit_group;");
+    };
+    const long long b0 = blockIdx.x;
+    int4 d1 = ldesc(b0), d2 = ldesc(b0 + G0), d3;
+    load(d1);
+    issue(b0, d1, 0);
+    load(d2);
+    d1 = d2;
+    d2 = ldesc(b0 + 2 * G0);
     int st = 0;
-    int nxt[NZ / RB_NT];
-    rb_load_idx(K, blk_row, blockIdx.x, nblk, nxt);
-    rb_issue(nxt, xb, sv[0]);
-    rb_load_idx(K, blk_row, blockIdx.x + gridDim.x, nblk, nxt);
-    for (long long b = blockIdx.x; b < nblk; b += gridDim.x) {
-        rb_issue(nxt, xb, sv[st ^ 1]);
-        rb_load_idx(K, blk_row, b + 2LL * gridDim.x, nblk, nxt);
+    for (long long b = b0; b < nblk; b += G0) {
+        issue(b + G0, d1, st ^ 1);
+        load(d2);
+        d3 = ldesc(b + 3 * G0);
         cp_async_wait1();
         __syncthreads();
-        const long long r0 = blk_row[b], r1 = blk_row[b + 1];
-        const long long p0 = __ldg(K.ptr + r0);
-        const int nr = (int)(r1 - r0);
-        const int G = rb_group_size(nr);
-        const int lane = threadIdx.x & (G - 1), grp = threadIdx.x / G, ngr = RB_NT / G;
+        const DualBuf<T>& B = buf[st];
+        const int4 d = B.d;
+        const int nr = d.y & 0xffff, lg = d.y >> 16, G = 1 << lg;
+        const long long r0 = d.x;
+        const int p0 = d.z;
+        const int lane = threadIdx.x & (G - 1), grp = threadIdx.x >> lg, ngr = RB_NT >> lg;
         for (int rb = 0; rb < nr; rb += ngr) {
             const int rr = rb + grp;
             const long long row = r0 + rr;
-            double acc = 0.0;
-            if (rr < nr) acc = rb_row_sum<T, KIND>(K, sv[st], p0, __ldg(K.ptr + row), __ldg(K.ptr + row + 1), lane, G);
+            double acc = 0.0, gj = 0.0, rhj = 0.0, yj = 0.0;
+            if (rr < nr) {
+                if (lane == 0) { gj = g[row]; rhj = rh[row]; yj = (double)yin[row]; }  // in flight during the sum
+                acc = rb_row_sum<T, KIND>(K, B.tile, p0, B.rp[rr], B.rp[rr + 1], lane, G);
+            }
             acc = rb_group_sum(acc, G);
             if (lane == 0 && rr < nr) {
-                const double sg = (KIND == KV_SIGN) ? (double)rsign[row] : 1.0;
-                const double gj = g[row];
-                double yn = (double)yin[row] + tau2 * (rh[row] - gj * (sg * acc));
+                double sg = 1.0;
+                if constexpr (KIND == KV_SIGN)
+                    sg = (double)reinterpret_cast<const signed char*>(B.sgw)[(r0 & 3) + rr];
+                double yn = yj + tau2 * (rhj - gj * (sg * acc));
                 if (row < m1 && yn < 0.0) yn = 0.0;
                 const T yt = (T)yn;
                 yout[row] = yt;
@@ -170,6 +231,8 @@ __global__ void __launch_bounds__(RB_NT) k_dual_rb(Csr K, const long long* __res
             }
         }
         __syncthreads();
+        d1 = d2;
+        d2 = d3;
         st ^= 1;
     }
     asm volatile("cp.async.wait_all;");
