@@ -271,6 +271,37 @@ def facility_location(nf, nc, seed, name="facility"):
     return inst
 
 
+def facility_location_slack(nf, nc, seed, name="facility_slack"):
+    """The facility-location instance of facility_location (same costs) with every constraint an
+    equality (reading R24, round 2; "when it eliminates all inequality constraints"):
+    y_ij - x_i + s_ij = 0 with a binary slack s_ij (cost 0) replaces y_ij <= x_i, so the whole
+    constraint matrix B (customer rows + linking rows) is TU and TUReformulate can remove every row.
+    Variables: x_i at i, y_ij at nf + j*nf + i, s_ij at nf + nf*nc + j*nf + i.  Rows: the nc customer
+    rows, then the linking rows in (j, i) order.  TU sets: J = all rows; I = for customer row j its
+    cheapest y_ij (lowest i on ties), for linking row (j, i) the slack s_ij — B_JI is unit triangular
+    (the linking row of the cheapest facility meets both y_{i*j} and s_{i*j}), not a permutation."""
+    base = facility_location(nf, nc, seed)
+    n0 = base["n"]
+    ns = nf * nc
+    rows_c, rows_v = [], []
+    ptr, col, val = base["k_rowptr"], base["k_col"], base["k_val"]
+    for j in range(nc):
+        rows_c.append(col[ptr[j]:ptr[j + 1]]); rows_v.append(val[ptr[j]:ptr[j + 1]])
+    for j in range(nc):
+        for i in range(nf):
+            rows_c.append(np.array([i, nf + j * nf + i, n0 + j * nf + i]))
+            rows_v.append(np.array([-1.0, 1.0, 1.0]))
+    m = nc + ns
+    kp, kc, kv = _csr_from_rows(rows_c, rows_v, m)
+    c = np.concatenate([base["c"], np.zeros(ns)])
+    inst = dict(name=name, n=n0 + ns, m=m, k_rowptr=kp, k_col=kc, k_val=kv,
+                r=np.concatenate([np.ones(nc), np.zeros(ns)]), sense=np.zeros(m, np.int8),
+                q_rowptr=None, q_col=None, q_val=None, c=c, c0=0.0, maximize=False)
+    inst["tu_rows"] = np.arange(m, dtype=np.int64)
+    inst["tu_cols"] = np.concatenate([base["tu_cols"], n0 + np.arange(ns)]).astype(np.int32)
+    return inst
+
+
 def assignment3d(n, seed, name="assign3d"):
     """3D assignment (PAPER eq. assign3d): min c'x over x in {0,1}^(n^3), sum_{jk} x_ijk = 1,
     sum_{ik} x_ijk = 1, sum_{ij} x_ijk = 1; c_ijk ~ U{1..100} (reading R25).  Variable (i,j,k) at flat

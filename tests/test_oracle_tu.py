@@ -98,3 +98,73 @@ def test_facility_location_exact_small():
     assert zb == zr
     f, z = O.Oracle(inst).eval_point(lift(xr))
     assert f and z == zb
+
+
+def _interval_tu_instance(seed):
+    """Tiny instance whose J rows are overlapping intervals (consecutive ones) over a column order:
+    an interval matrix is TU, and with I_t = the first column of interval t (distinct starts) B_JI is
+    unit triangular but NOT a permutation (later intervals cover earlier starts).  Plus random
+    general rows and an indefinite Q."""
+    rng = np.random.default_rng(100 + seed)
+    n = 10
+    order = rng.permutation(n)
+    K, r, sense, J, I = [], [], [], [], []
+    starts = [0, 2, 3]
+    for t, a in enumerate(starts):
+        b = a + int(rng.integers(3, 5))
+        row = np.zeros(n)
+        row[order[a:b]] = 1.0
+        K.append(row); r.append(1.0); sense.append(0)
+        J.append(len(K) - 1); I.append(int(order[a]))
+    for _ in range(3):
+        row = np.zeros(n)
+        idx = rng.choice(n, size=4, replace=False)
+        row[idx] = rng.integers(-3, 4, size=4)
+        K.append(row); r.append(float(rng.integers(-2, 3))); sense.append(int(rng.choice([1, -1])))
+    Qd = rng.integers(-2, 3, size=(n, n)).astype(float)
+    Qd = np.triu(Qd) + np.triu(Qd, 1).T
+    inst = inst_from_dense(K, r, sense, rng.integers(-9, 10, size=n).astype(float), Q=Qd,
+                           c0=float(rng.integers(-3, 4)), maximize=bool(seed % 2))
+    return inst, J, I
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_general_bji_exactness_by_enumeration(seed):
+    """The theorem for a NON-permutation B_JI (the case the paper applies with an LU of
+    B_JI): B_JI really is not a signed permutation here, and the reduced problem is exact — brute
+    force optima equal, and every feasible reduced point lifts to a feasible original point with the
+    same objective, one to one."""
+    inst, J, I = _interval_tu_instance(seed)
+    Kd = G.dense_K(inst)
+    BJI = Kd[np.ix_(J, I)]
+    assert np.count_nonzero(BJI) > len(J)  # not a permutation
+    red, lift = tu_reformulate(inst, J, I)
+    zb, _, okb, _ = brute_force(inst)
+    zr, xr, okr, zur = brute_force(red)
+    assert (zb is None) == (zr is None)
+    if zb is None:
+        return
+    assert zr == zb
+    o = O.Oracle(inst)
+    X = all_points(red["n"])
+    for l in np.flatnonzero(okr):
+        f, z = o.eval_point(lift(X[l]))
+        assert f and (-z if inst["maximize"] else z) == zur[l]
+    assert okb.sum() == okr.sum()
+
+
+def test_facility_location_slack_form_removes_every_row():
+    """Reading R24 (round 2): with binary slacks the facility-location constraints are all equalities
+    of a TU matrix; eliminating them (B_JI unit triangular) leaves only box rows, and the optimum is
+    the facility-location optimum (brute force of the inequality form, nf = 2, nc = 3)."""
+    fl = G.facility_location(2, 3, 5)
+    sl = G.facility_location_slack(2, 3, 5)
+    red, lift = tu_reformulate(sl, sl["tu_rows"], sl["tu_cols"])
+    assert red["n"] == fl["n"] - 3          # x_i and the non-cheapest y_ij remain
+    assert np.all(red["sense"] == 1)         # only the box rows of x_I = s + S x_Ibar are left
+    zb, xb, _, _ = brute_force(fl)
+    zr, xr, _, _ = brute_force(red)
+    assert zr == zb
+    x = lift(xr)
+    f, z = O.Oracle(fl).eval_point(x[: fl["n"]])
+    assert f and z == zb
