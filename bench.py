@@ -403,28 +403,31 @@ def run_f1_maxcut(args, gf, stream, local):
 
 def run_f2_facility(args, gf, stream, local):
     """Next row f2: TUReformulate (PAPER §2.4.1) on the paper's facility-location
-    workload at (nf, nc) = (512, 2048) (config 7).  The same Alg. 1 run (SPEC
-    default halting, bounded by --f2-iters) with and without the reformulation: objective reached,
-    time to incumbent (device %globaltimer, Preprocess excluded as in PAPER L193), candidates/s,
-    and the host time of the reformulation itself (the paper's 'Avg. TU Time' column)."""
-    import torch
+    workload at (nf, nc) = (512, 2048) (config 7), three forms, same Alg. 1 run
+    (fixed iteration budget, halting disabled): "tu" = all-equality slack form with every row
+    eliminated (general, unit-triangular B_JI: sparse exact elimination; reading R24 rev.),
+    "tu_gub" = inequality form with the customer rows eliminated (B_JI = identity; round-1 reading),
+    "no_tu" = inequality form as is.  Objective reached, time to incumbent (device %globaltimer,
+    Preprocess excluded as in PAPER L193), candidates/s, and the host time of the reformulation
+    itself (the paper's 'Avg. TU Time' column)."""
     from gen import instances as G
     out = {"workload": "config7", "desc": "facility location nf=512, nc=2048 (n = 1,049,088; m = 1,050,624)",
            "note": "fixed iteration budget, halting disabled; 'small' = (nf, nc) = (16, 64), fp64, 30000 iterations"}
-    for key, inst, iters, prec in (("", make_instance(7, args.seed), args.f2_iters, args.precision),
-                                   ("small_", G.facility_location(16, 64, args.seed), 30000, 64)):
-        _f2_pair(out, key, inst, iters, prec, args, gf, stream, local)
+    for key, nf, nc, iters, prec in (("", 512, 2048, args.f2_iters, args.precision), ("small_", 16, 64, 30000, 64)):
+        _f2_forms(out, key, nf, nc, iters, prec, args, gf, stream, local, G)
     return out
 
 
-def _f2_pair(out, key, inst, iters, prec, args, gf, stream, local):
+def _f2_forms(out, key, nf, nc, iters, prec, args, gf, stream, local, G):
     import torch
-    out[key + "n"], out[key + "m"] = int(inst["n"]), int(inst["m"])
-    for tu in (True, False):
+    fl = G.facility_location(nf, nc, args.seed)
+    out[key + "n"], out[key + "m"] = int(fl["n"]), int(fl["m"])
+    for form in ("tu", "tu_gub", "no_tu"):
+        inst = G.facility_location_slack(nf, nc, args.seed) if form == "tu" else fl
         s = gf.Solver(local, stream=stream.cuda_stream)
         s.load(inst)
         t_tu = None
-        if tu:
+        if form != "no_tu":
             t0 = time.perf_counter()
             s.tu_reformulate(inst["tu_rows"], inst["tu_cols"])
             t_tu = time.perf_counter() - t0
@@ -441,12 +444,13 @@ def _f2_pair(out, key, inst, iters, prec, args, gf, stream, local):
         z, x, meta = s.best_incumbent()
         feasible = None
         if meta["has_incumbent"]:
-            # the lifted incumbent against the ORIGINAL rows (host check, exact integers)
-            K_rows = np.repeat(np.arange(inst["m"]), np.diff(inst["k_rowptr"]))
-            ax = np.bincount(K_rows, weights=inst["k_val"] * x[inst["k_col"]], minlength=inst["m"])
-            ok = np.where(inst["sense"] == 0, ax == inst["r"], np.where(inst["sense"] == 1, ax >= inst["r"], ax <= inst["r"]))
-            feasible = bool(ok.all()) and float(inst["c"] @ x) == z
-        out[key + ("tu" if tu else "no_tu")] = {
+            # the lifted incumbent against the ORIGINAL inequality rows (host check, exact integers)
+            x = x[: fl["n"]]
+            K_rows = np.repeat(np.arange(fl["m"]), np.diff(fl["k_rowptr"]))
+            ax = np.bincount(K_rows, weights=fl["k_val"] * x[fl["k_col"]], minlength=fl["m"])
+            ok = np.where(fl["sense"] == 0, ax == fl["r"], np.where(fl["sense"] == 1, ax >= fl["r"], ax <= fl["r"]))
+            feasible = bool(ok.all()) and float(fl["c"] @ x) == z
+        out[key + form] = {
             "reduced_n": s.n, "reduced_m": s.m, "tu_seconds": t_tu, "iters": info["iters"],
             "halt_reason": info["halt_reason"], "z_best": z if meta["has_incumbent"] else None,
             "time_to_incumbent_s": meta["found_time_s"] if meta["has_incumbent"] else None,

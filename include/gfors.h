@@ -157,9 +157,11 @@ gfors_status gfors_create(gfors_ctx **out, const gfors_device_opts *opts);
 gfors_status gfors_load(gfors_ctx *ctx, const gfors_problem *prob);
 /* TUReformulate (PAPER §2.4.1, Theorem L823-846; Alg. 1), optional,
  * between gfors_load and gfors_preprocess.  rows_J[count]: INPUT row indices (as passed to
- * gfors_load) of equality rows; cols_I[count]: columns; B_JI (rows J, columns I) must be a signed
- * permutation matrix (row J[t] meets I exactly at column I[t] with value +-1; general invertible
- * B_JI needs the paper's LU-applied S and returns GFORS_E_INPUT), B_J and d_J integral.  Eliminates
+ * gfors_load) of equality rows; cols_I[count]: columns (no pairing between J[t] and I[t] needed);
+ * B_J must be TU with B_J, d_J integral and B_JI invertible (any such B_JI: signed permutation,
+ * triangular, ...).  S is formed by an exact sparse Gauss-Jordan elimination of the J rows with +-1
+ * pivots (the paper applies an LU of B_JI instead, L848-850); a singular B_JI or a non-TU B_J (an
+ * entry outside {-1,0,1} appears) returns GFORS_E_INPUT.  Eliminates
  * x_I = s + S x_Ibar (s = B_JI^-1 d_J, S = -B_JI^-1 B_J,Ibar) exactly by substitution into Q, c, c0
  * and the other rows, adds the box rows S x >= -s, -S x >= s - 1 (those every binary x satisfies
  * are dropped) and loads the reduced problem in place (reduced variables = Ibar ascending; rows =

@@ -9,7 +9,7 @@ import pytest
 from gen import instances as G
 from oracle import oracle as O
 from oracle.tu import tu_reformulate
-from tests.test_oracle_tu import _random_tu_instance
+from tests.test_oracle_tu import _interval_tu_instance, _random_tu_instance
 
 pytestmark = pytest.mark.gpu
 
@@ -31,11 +31,19 @@ def _pair(gf, inst, J, I, precision=64):
     return s, o, red, lift
 
 
-@pytest.mark.parametrize("case", ["facility"] + [f"rand{k}" for k in range(6)])
+@pytest.mark.parametrize("case", ["facility", "facility_slack"] + [f"rand{k}" for k in range(6)]
+                         + [f"interval{k}" for k in range(6)])
 def test_reduced_problem_evaluates_identically(gf, case):
+    """Signed-permutation B_JI (facility, rand*) and general B_JI eliminated with fill (facility_slack:
+    unit triangular; interval*: overlapping consecutive-ones rows)."""
     if case == "facility":
         inst = G.SMALL["facility"](2)
         J, I = inst["tu_rows"], inst["tu_cols"]
+    elif case == "facility_slack":
+        inst = G.facility_location_slack(6, 24, 2)
+        J, I = inst["tu_rows"], inst["tu_cols"]
+    elif case.startswith("interval"):
+        inst, J, I = _interval_tu_instance(int(case[8:]))
     else:
         inst, J, I = _random_tu_instance(int(case[4:]))
     s, o, red, _ = _pair(gf, inst, J, I)
@@ -64,15 +72,43 @@ def test_facility_run_parity_and_lift(gf, seed):
     assert f and z == zg
 
 
+@pytest.mark.parametrize("seed", [1, 2])
+def test_facility_slack_run_parity_and_lift(gf, seed):
+    """The all-equality facility location (reading R24 rev.): the library's elimination (B_JI unit
+    triangular, with fill) gives the oracle's reduced problem — identical fp64 runs — and the lifted
+    incumbent is feasible for the ORIGINAL (inequality) facility-location problem."""
+    inst = G.facility_location_slack(6, 24, seed)
+    s, o, red, lift = _pair(gf, inst, inst["tu_rows"], inst["tu_cols"])
+    assert s.m == red["m"] and np.all(red["sense"] == 1)
+    kw = dict(max_iters=3000, k_b=128)
+    ig = s.run(**kw)
+    io = o.run(**kw)
+    assert ig["iters"] == io["iters"] and ig["halt_reason"] == io["halt_reason"]
+    zg, xg, _ = s.best_incumbent()
+    zo, xo = o.best()
+    assert zg == zo
+    if np.isfinite(zg):
+        assert np.array_equal(xg, lift(xo))
+        fl = G.facility_location(6, 24, seed)
+        f, z = O.Oracle(fl).eval_point(xg[: fl["n"]])
+        assert f and z == zg
+
+
 def test_tu_errors(gf):
     inst = G.SMALL["facility"](1)
     s = gf.Solver(0)
     s.load(inst)
     with pytest.raises(gf.GforsError, match="not an equality row"):
         s.tu_reformulate([30], [0])
-    with pytest.raises(gf.GforsError, match="signed permutation"):
-        # two customer rows, but the column of row 0 is given for row 1 too (it meets I twice)
-        s.tu_reformulate([0, 1], [inst["tu_cols"][0], 6])
-    s.load(inst)
-    with pytest.raises(gf.GforsError, match="does not occur"):
+    with pytest.raises(gf.GforsError, match="no \\+-1 pivot"):
+        # customer row 0 does not contain the cheapest column of customer 1: B_JI = 0 is singular
         s.tu_reformulate([0], [inst["tu_cols"][1]])
+    s.load(inst)
+    with pytest.raises(gf.GforsError, match="repeated"):
+        s.tu_reformulate([0, 0], [inst["tu_cols"][0], inst["tu_cols"][1]])
+    # a non-TU B_J: rows x0 + x1 + x2 = 1, x0 - x1 + x2 = 1 with I = {0, 1}: eliminating leaves a 2
+    from tests.util import inst_from_dense
+    bad = inst_from_dense([[1, 1, 1, 0], [1, -1, 1, 1]], [1, 1], [0, 0], [1.0, 2.0, 3.0, 4.0])
+    s.load(bad)
+    with pytest.raises(gf.GforsError, match="not TU"):
+        s.tu_reformulate([0, 1], [0, 1])
