@@ -366,9 +366,9 @@ def run_f1_maxcut(args, gf, stream, local):
     fb = 8 if args.precision == 64 else 4
     # GEMV: k_int primal products + 1 trigger product per block (each = dense + final launch); with
     # fp32 iterates and k_int > 1 the next block's first primal reuses the trigger's product
-    # (GFORS_QX_REUSE), so k_int products are computed per block
+    # (option qx_reuse, on by default), so k_int products are computed per block
     qx_ms, qx_launches = act.get("pdhg_qx", (0.0, 0))
-    reuse = args.precision == 32 and args.k_int > 1 and os.environ.get("GFORS_QX_REUSE", "1") != "0"
+    reuse = args.precision == 32 and args.k_int > 1
     gemv_per_block = args.k_int if reuse else args.k_int + 1
     gemv_ms = qx_ms / (nb * gemv_per_block)
     gemv_bytes = n * n + 2 * n * fb + 8 * n

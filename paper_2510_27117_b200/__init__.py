@@ -160,7 +160,7 @@ class Solver:
     nccl_unique_id(), identical on all ranks) enables the in-loop incumbent exchange."""
 
     def __init__(self, device: int = 0, stream=None, rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
-                 loopback: bool = False):
+                 loopback: bool = False, options: dict | None = None):
         self._nccl_buf = (C.c_char * 128).from_buffer_copy(nccl_id) if nccl_id else None
         opts = DeviceOpts(device, P(stream) if stream else None, rank, world,
                           C.cast(self._nccl_buf, P) if nccl_id else None, int(bool(loopback)))
@@ -170,6 +170,8 @@ class Solver:
             raise GforsError(rc, "gfors_create failed")
         self.h = h
         self.n = self.m = 0
+        for k, v in (options or {}).items():  # gfors_set_option (load-time choices apply to the next load)
+            self.set_option(k, v)
 
     def close(self):
         if getattr(self, "h", None):

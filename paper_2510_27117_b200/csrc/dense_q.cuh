@@ -5,10 +5,11 @@
 // 128, zero padded) instead of a CSR, and the two places Q enters the hot path become:
 //
 //  * the PDHG primal gradient term 2 Q~ x (Q~ = Q/omega) and the
-//    s^x residual term 2 Q~ (x_k - x_{k-1}): a dense GEMV `k_qx_dense` streaming Qd
-//    from HBM (int8: 1 byte per entry) with fp64 accumulation, units of 8 rows x 1024 columns
-//    per warp (x reused across the 8 rows), fixed-order partials per column chunk combined by
-//    `k_qx_final` -> Q.pre[i] = (sum_j Q_ij x_j) / omega.  HBM-bound: 1 B per entry per pass.
+//    s^x residual term 2 Q~ (x_k - x_{k-1}): a dense GEMV streaming Qd from HBM
+//    through a TMA ring (int8: 1 byte per entry) — `k_qx_tma` (fp64 FMA, fp64 iterates) or
+//    `k_qx_tma_fix` (exact dp4a on the fixed-point image of x, fp32 iterates) — with fixed-order
+//    partials per column chunk combined by `k_qx_final` -> Q.pre[i] = (sum_j Q_ij x_j) / omega.
+//    HBM-bound: 1 B per entry per pass.
 //
 //  * the EvalBest quadratic term x_l' Q x_l for the k_b sampled candidates:
 //    a tcgen05 int8 tensor-core GEMM Y = Q X (exact int32 accumulation in TMEM) fused with its
@@ -98,80 +99,6 @@ __device__ __forceinline__ void qx_load_x16(const TX* __restrict__ a, const TX* 
                 if (b) v -= (double)b[c];
             }
             xv[k] = v;
-        }
-    }
-}
-
-// part[c * ld + i] = sum_{j in column chunk c} Qd[i][j] * x_j   (fixed order within the chunk:
-// per lane ascending j, then a fixed butterfly over the 32 lanes)
-template <typename TX, bool DIFF>
-__global__ void __launch_bounds__(QX_NT, 2) k_qx_dense(const int8_t* __restrict__ Qd, long long ld, long long n,
-                                                       QxSrc<TX> src, double* __restrict__ part) {
-    int par = 0;
-    if (src.ctrl) par = (int)(iter_index(src.ctrl, src.kint, src.j) & 1);
-    const TX* __restrict__ a = par ? src.a[1] : src.a[0];  // (selects, not an indexed param copy)
-    const TX* __restrict__ b = DIFF ? (par ? src.b[1] : src.b[0]) : nullptr;
-    const int lane = threadIdx.x & 31;
-    const long long rgroups = (n + QX_RW - 1) / QX_RW;
-    const long long nchunk = (n + QX_CW - 1) / QX_CW;
-    const long long units = rgroups * nchunk;
-    const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-    const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
-    for (long long u = gw; u < units; u += nw) {
-        const long long rg = u / nchunk, c = u - rg * nchunk;
-        const long long r0 = rg * QX_RW;
-        double acc[QX_RW];
-#pragma unroll
-        for (int r = 0; r < QX_RW; ++r) acc[r] = 0.0;
-#pragma unroll 1
-        for (int s = 0; s < QX_CW / 512; ++s) {
-            const long long col0 = c * QX_CW + s * 512 + lane * 16;
-            if (col0 >= n) break;
-            uint4 q[QX_RW];
-#pragma unroll
-            for (int r = 0; r < QX_RW; ++r) {
-                const long long row = r0 + r;
-                q[r] = row < n ? __ldcs(reinterpret_cast<const uint4*>(Qd + row * ld + col0)) : make_uint4(0, 0, 0, 0);
-            }
-            double xv[16];
-            qx_load_x16<TX>(a, b, col0, n, xv);
-#pragma unroll
-            for (int r = 0; r < QX_RW; ++r) {
-                const uint32_t w[4] = {q[r].x ^ 0x80808080u, q[r].y ^ 0x80808080u, q[r].z ^ 0x80808080u,
-                                       q[r].w ^ 0x80808080u};
-                double t = acc[r];
-#pragma unroll
-                for (int k = 0; k < 16; ++k) t = fma(i8_to_f64(w[k >> 2], k & 3), xv[k], t);
-                acc[r] = t;
-            }
-        }
-        // transpose-reduce the 8 row sums over the 32 lanes: 4+2+1 exchanges halve the value set,
-        // then two plain butterfly steps; lane L ends with row ((L>>4)&1)*4 + ((L>>3)&1)*2 + ((L>>2)&1)
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const bool up = lane & 16;
-            const double send = up ? acc[k] : acc[k + 4];
-            const double keep = up ? acc[k + 4] : acc[k];
-            acc[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-        }
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const bool up = lane & 8;
-            const double send = up ? acc[k] : acc[k + 2];
-            const double keep = up ? acc[k + 2] : acc[k];
-            acc[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-        }
-        {
-            const bool up = lane & 4;
-            const double send = up ? acc[0] : acc[1];
-            const double keep = up ? acc[1] : acc[0];
-            acc[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-        }
-        acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 2);
-        acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
-        if ((lane & 3) == 0) {
-            const int r = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-            if (r0 + r < n) part[c * ld + r0 + r] = acc[0];
         }
     }
 }
@@ -506,7 +433,8 @@ __global__ void __launch_bounds__(TC_NT, 1)
 // 6-stage mbarrier ring per CTA (one elected producer thread, 8 consumer warps), so ~96 KB per CTA
 // are in flight independently of the registers of the arithmetic.  Consumer warp w owns 8 rows of
 // the tile (x reused by 8 rows), lane l owns 8 columns (LDS.64 per row: conflict-free).  Unit =
-// (64-row block, 2048-column chunk); fixed-order reductions exactly as k_qx_dense.
+// (64-row block, 2048-column chunk); fixed-order reductions (per lane ascending j, then a fixed
+// butterfly over the 32 lanes).
 // ---------------------------------------------------------------------------------------------
 constexpr int QT_ROWS = 64, QT_COLS = 256, QT_STAGES = 6, QT_NT = 288;
 constexpr int QT_TILE = QT_ROWS * QT_COLS;  // 16 KB
@@ -626,7 +554,7 @@ __global__ void __launch_bounds__(QT_NT, 2) k_qx_tma(const __grid_constant__ CUt
                 acc[r] = s_;
             }
         }
-        // fixed-order transpose-reduce over the 32 lanes (as k_qx_dense)
+        // fixed-order transpose-reduce over the 32 lanes
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const bool up = lane & 16;
@@ -817,235 +745,6 @@ __global__ void __launch_bounds__(QT_NT, MINB) k_qx_tma_fix(const __grid_constan
             const long long row = rb * QT_ROWS + 8 * warp + r;
             if (row < n) part[c * ld + row] = (double)v[0] * (DIFF ? 9.313225746154785e-10 : 4.656612873077393e-10);
         }
-    }
-}
-
-// ---------------------------------------------------------------------------------------------
-// Symmetric variant of k_qx_tma_fix (GFORS_QX_SYM=1; measured SLOWER: 105 vs 85 us per product at
-// n = 20480 — half the bytes but 2.5x the instructions per tile, issue-bound): Q = Q', so only the
-// tiles on or above the diagonal are read and each is used twice — y_I += Q_IJ x_J (rows) and
-// y_J += Q_IJ' x_I (columns) — halving the HBM bytes of the GEMV.  Tile (R, T) = rows
-// [64R, 64R+64) x columns [256T, 256T+256) is read iff it holds an entry with col >= row; in the
-// four diagonal-crossing tiles per column tile, an entry feeds the row sum iff col >= row and the
-// column sum iff col > row (byte masks).  Unit = (column tile T, <= 8 consecutive row blocks): the
-// column sums of T stay in registers over the unit (dp4a on an 8x8 byte transpose of the lane's
-// block with the fixed-point digits of the warp's 8 x_I values), the row sums of each tile are
-// reduced over the lanes and added with int64 atomics; column sums are combined across the 8
-// warps with shared int64 atomics and added once per unit.  Integer sums: exact, order-free and
-// bit-identical to k_qx_tma_fix.  acc[] is zeroed by k_qx_final_acc.
-// ---------------------------------------------------------------------------------------------
-constexpr int QS_CHUNK = 8;  // row blocks per unit
-
-__device__ __forceinline__ void transpose8x8(const uint2 (&q)[8], uint2 (&t)[8]) {
-    // t[k] = bytes k of q[0..3] (x) and of q[4..7] (y): the lane's column k over its 8 rows
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const uint32_t a0 = h ? q[0].y : q[0].x, a1 = h ? q[1].y : q[1].x, a2 = h ? q[2].y : q[2].x, a3 = h ? q[3].y : q[3].x;
-        const uint32_t b0 = h ? q[4].y : q[4].x, b1 = h ? q[5].y : q[5].x, b2 = h ? q[6].y : q[6].x, b3 = h ? q[7].y : q[7].x;
-        uint32_t wa[4], wb[4];
-        digits4(a0, a1, a2, a3, wa);  // wa[k] = byte k of a0..a3 (the same transpose as the digit packing)
-        digits4(b0, b1, b2, b3, wb);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) { t[4 * h + k].x = wa[k]; t[4 * h + k].y = wb[k]; }
-    }
-}
-
-template <bool DIFF>
-__device__ __forceinline__ void x_digits8(const float* __restrict__ a, const float* __restrict__ b, long long col0,
-                                          long long n, uint32_t (&w0)[4], uint32_t (&w1)[4]) {
-    double xv[8];
-    qt_load_x8<float>(a, b, col0, n, xv);
-    uint32_t X[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-        X[k] = DIFF ? (uint32_t)__double2int_rn(xv[k] * 1073741824.0) : (uint32_t)__double2ull_rn(xv[k] * 2147483648.0);
-    digits4(X[0], X[1], X[2], X[3], w0);
-    digits4(X[4], X[5], X[6], X[7], w1);
-}
-
-template <bool DIFF>
-__device__ __forceinline__ int dp4a_d(uint32_t a, uint32_t b, int c, int d) {
-    return (DIFF && d == 3) ? dp4a_ss(a, b, c) : dp4a_su(a, b, c);
-}
-
-__device__ __forceinline__ long long combine_digits(int a0, int a1, int a2, int a3) {
-    return (long long)a0 + ((long long)a1 << 8) + ((long long)a2 << 16) + ((long long)a3 << 24);
-}
-
-// unit u -> (column tile T, first row block); unit_off[T] = first unit of column tile T
-template <bool DIFF>
-__global__ void __launch_bounds__(QT_NT, 2) k_qx_sym(const __grid_constant__ CUtensorMap tmQ, long long n,
-                                                    const int* __restrict__ unit_off, int ntc, QxSrc<float> src,
-                                                    unsigned long long* __restrict__ acc) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* tiles = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-    uint64_t* full = reinterpret_cast<uint64_t*>(tiles + (size_t)QT_STAGES * QT_TILE);
-    uint64_t* empty = full + QT_STAGES;
-    unsigned long long* colsum = reinterpret_cast<unsigned long long*>(empty + QT_STAGES);  // [256]
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const long long RB = (n + QT_ROWS - 1) / QT_ROWS;
-    const int units = unit_off[ntc];
-    if (threadIdx.x == 0) {
-        for (int st = 0; st < QT_STAGES; ++st) { mbar_init(&full[st], 1); mbar_init(&empty[st], 8); }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    for (int c = threadIdx.x; c < QT_COLS; c += blockDim.x) colsum[c] = 0ull;
-    __syncthreads();
-    auto unit_tiles = [&](int u, int& T, long long& r0, long long& r1) {
-        int lo = 0, hi = ntc - 1;  // last T with unit_off[T] <= u
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (unit_off[mid] <= u) lo = mid; else hi = mid - 1;
-        }
-        T = lo;
-        const long long nr = min(RB, 4LL * T + 4);  // row blocks with an entry col >= row
-        r0 = (long long)(u - unit_off[T]) * QS_CHUNK;
-        r1 = min(nr, r0 + QS_CHUNK);
-    };
-    if (warp == 8) {
-        if (lane == 0) {
-            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmQ)) : "memory");
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int u = blockIdx.x; u < units; u += gridDim.x) {
-                int T;
-                long long r0, r1;
-                unit_tiles(u, T, r0, r1);
-                for (long long R = r0; R < r1; ++R) {
-                    mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_expect_tx(&full[stage], QT_TILE);
-                    tma_load_2d(tiles + (size_t)stage * QT_TILE, &tmQ, &full[stage], (int)(T * QT_COLS), (int)(R * QT_ROWS));
-                    if (++stage == QT_STAGES) { stage = 0; phase ^= 1; }
-                }
-            }
-        }
-        return;
-    }
-    int par = 0;
-    if (src.ctrl) par = (int)(iter_index(src.ctrl, src.kint, src.j) & 1);
-    const float* __restrict__ a = par ? src.a[1] : src.a[0];
-    const float* __restrict__ b = DIFF ? (par ? src.b[1] : src.b[0]) : nullptr;
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        int T;
-        long long r0, r1;
-        unit_tiles(u, T, r0, r1);
-        const long long c0 = (long long)T * QT_COLS + 8 * lane;  // this lane's 8 columns
-        uint32_t xj0[4], xj1[4];
-        x_digits8<DIFF>(a, b, c0, n, xj0, xj1);
-        int cacc[8][4];
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-#pragma unroll
-            for (int d = 0; d < 4; ++d) cacc[k][d] = 0;
-        for (long long R = r0; R < r1; ++R) {
-            const long long i0 = R * QT_ROWS + 8 * warp;  // this warp's 8 rows
-            uint32_t xi0[4], xi1[4];
-            x_digits8<DIFF>(a, b, i0, n, xi0, xi1);
-            mbar_wait(&full[stage], phase);
-            const uint8_t* tile = tiles + (size_t)stage * QT_TILE + (size_t)(8 * warp) * QT_COLS + 8 * lane;
-            uint2 qr[8];
-#pragma unroll
-            for (int r = 0; r < 8; ++r) qr[r] = *reinterpret_cast<const uint2*>(tile + r * QT_COLS);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[stage]);
-            if (++stage == QT_STAGES) { stage = 0; phase ^= 1; }
-            const bool diag = R >= 4LL * T;  // diagonal-crossing tile: rows use col >= row, columns col > row
-            if (diag) {
-#pragma unroll
-                for (int r = 0; r < 8; ++r) {
-                    const long long i = i0 + r;
-                    uint32_t mr0 = 0u, mr1 = 0u;
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        if (c0 + k >= i) mr0 |= 0xFFu << (8 * k);
-                        if (c0 + 4 + k >= i) mr1 |= 0xFFu << (8 * k);
-                    }
-                    qr[r].x &= mr0; qr[r].y &= mr1;
-                }
-            }
-            // row sums of this tile: sum over the lane's 8 columns, then over the lanes
-            long long v[8];
-#pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                int t[4];
-#pragma unroll
-                for (int d = 0; d < 4; ++d) t[d] = dp4a_d<DIFF>(qr[r].y, xj1[d], dp4a_d<DIFF>(qr[r].x, xj0[d], 0, d), d);
-                v[r] = combine_digits(t[0], t[1], t[2], t[3]);
-            }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const bool up = lane & 16;
-                const long long send = up ? v[k] : v[k + 4];
-                const long long keep = up ? v[k + 4] : v[k];
-                v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-            }
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-                const bool up = lane & 8;
-                const long long send = up ? v[k] : v[k + 2];
-                const long long keep = up ? v[k + 2] : v[k];
-                v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-            }
-            {
-                const bool up = lane & 4;
-                const long long send = up ? v[0] : v[1];
-                const long long keep = up ? v[1] : v[0];
-                v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-            }
-            v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
-            v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
-            if ((lane & 3) == 0) {
-                const int r = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-                if (i0 + r < n && v[0] != 0) atomicAdd(acc + i0 + r, (unsigned long long)v[0]);
-            }
-            // column sums: the lane's 8 columns over the warp's 8 rows (col > row: drop the diagonal)
-            if (diag) {
-#pragma unroll
-                for (int r = 0; r < 8; ++r) {
-                    const long long i = i0 + r;
-                    uint32_t mc0 = 0u, mc1 = 0u;
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        if (c0 + k > i) mc0 |= 0xFFu << (8 * k);
-                        if (c0 + 4 + k > i) mc1 |= 0xFFu << (8 * k);
-                    }
-                    qr[r].x &= mc0; qr[r].y &= mc1;
-                }
-            }
-            uint2 tq[8];
-            transpose8x8(qr, tq);
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-#pragma unroll
-                for (int d = 0; d < 4; ++d)
-                    cacc[k][d] = dp4a_d<DIFF>(tq[k].y, xi1[d], dp4a_d<DIFF>(tq[k].x, xi0[d], cacc[k][d], d), d);
-        }
-        // combine the 8 warps' column sums in shared memory, one global atomic per column
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const long long cv = combine_digits(cacc[k][0], cacc[k][1], cacc[k][2], cacc[k][3]);
-            if (cv != 0) atomicAdd(colsum + 8 * lane + k, (unsigned long long)cv);
-        }
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        {
-            const int c = threadIdx.x;  // 256 consumer threads, one column each
-            const unsigned long long cv = colsum[c];
-            if (cv != 0ull && (long long)T * QT_COLS + c < n) atomicAdd(acc + (long long)T * QT_COLS + c, cv);
-            colsum[c] = 0ull;
-        }
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-    }
-}
-
-// out[i] = acc[i] * 2^-31 (2^-30 for the difference) / omega; acc[i] = 0 for the next product
-__global__ void __launch_bounds__(256) k_qx_final_acc(long long n, unsigned long long* __restrict__ acc, double scale,
-                                                      double omega, double* __restrict__ out) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += gridDim.x * (long long)blockDim.x) {
-        const long long v = (long long)acc[i];
-        acc[i] = 0ull;
-        out[i] = ((double)v * scale) / omega;
     }
 }
 

@@ -235,15 +235,9 @@ DirPlan plan_direction(const std::vector<int64_t>& ptr, long long rows, cudaStre
     // long or few rows: fixed-length segments, one warp each (>= 8 warps per SM of work)
     const long long groups = rows;
     d.seg = (maxlen > 4096) || (groups * 32 < (long long)NUM_SMS_B200 * 2048 && nnz > (long long)NUM_SMS_B200 * 1024);
-    const char* force = getenv("GFORS_SPMV");
-    const std::string fm = force ? force : "";
-    if (maxlen <= RB_NNZ32 && fm != "short" && fm != "seg") {
+    if (maxlen <= RB_NNZ32) {
         d.seg = false;
         d.rb = true;
-    } else if (fm == "short" && maxlen <= 4096) {
-        d.seg = false;
-    } else if (fm == "seg") {
-        d.seg = true;
     }
     if (d.rb) {
         std::vector<long long> b = make_rowblocks(ptr, rows, RB_NNZ32, RB_ROWS_MAX);
@@ -469,18 +463,10 @@ struct gfors_ctx {
     int8_t* d_qd = nullptr;        // problem-owned
     CUtensorMap tmQ{};             // TMA map of Qd (128 x 128 byte boxes, 128B swizzle)
     CUtensorMap tmQ64{};           // TMA map of Qd for the GEMV (256-byte x 64-row boxes, no swizzle)
-    bool qx_tma = true;            // TMA-pipelined GEMV (GFORS_QX_TMA=0: the register-streaming k_qx_dense)
-    bool qx_fix = true;            // fp32 iterates: exact fixed-point dp4a GEMV (GFORS_QX_FIX=0: fp64 FMA)
-    bool qx_reuse = true;          // fp32 loop: the trigger's product of x_k serves the next block's first primal (GFORS_QX_REUSE=0: off)
+    bool qx_fix = true;            // fp32 iterates: exact fixed-point dp4a GEMV (option qx_fix = 0: fp64 FMA)
+    bool qx_reuse = true;          // fp32 loop: the trigger's product of x_k serves the next block's first primal (option qx_reuse)
     double* d_qxpart2 = nullptr;   // [nchunk][qld] partials of the trigger's product (prep-owned)
     long long* d_qreuse = nullptr; // block index whose first primal may reuse d_qxpart2 (prep-owned)
-    int qx_cfg = 1;
-    int pp_occ = 0;                // fp32 push-mode primal: CTAs per SM (GFORS_PP_OCC experiments: 3, 5 default, 6, 8)                // ring depth x CTAs/SM of the fixed-point GEMV (GFORS_QX_CFG: 0 6x2, 1 4x3 default, 2 3x4, 3 8x1)
-    bool qx_sym = false;           // ... reading only the upper-triangle tiles (GFORS_QX_SYM=1; slower)
-    int* d_qs_uoff = nullptr;      // symmetric GEMV: first unit of each 256-column tile (problem-owned)
-    int qs_ntc = 0;
-    long long qs_units = 0;
-    unsigned long long* d_qacc = nullptr;  // [n] int64 fixed-point accumulators (prep-owned, kept zero)
     TcItem* d_tcitems = nullptr;   // objective work items, grouped per CTA
     int* d_tcoff = nullptr;        // [tc_grid + 1]
     int tc_grid = 0;
@@ -500,12 +486,12 @@ struct gfors_ctx {
     DirPlan pd, pp;  // dual (rows of K), primal (rows of K') for the preprocessed precision
     DirPlan pdv[2], ppv[2];  // [0] fp32, [1] fp64 plans (row-block size differs)
     bool push_dual_ok = false, push_primal_ok = false;  // push modes allowed by the matrix
-    bool delta_dual = true;                             // delta push of the dual (GFORS_DELTA_DUAL=0: off)
-    bool xskip = true;                                  // stationary-column skip (GFORS_XSKIP=0: off)
+    bool delta_dual = true;                             // delta push of the dual (option delta_dual)
+    bool xskip = true;                                  // stationary-column skip (option xskip)
     unsigned mark_rows = 0;
     unsigned char* d_xst = nullptr;                     // [n] stationarity counters (push_primal.cuh)
     bool capturing = false;                             // enqueueing into the graph capture (branch())
-    bool cond_branch = false;                           // conditional-node mode branches (GFORS_COND_BRANCH=1)
+    bool cond_branch = false;                           // conditional-node mode branches (option cond_branch)
     bool dry = false;                                   // LAUNCH counts only
     cudaStream_t cap_stream2 = nullptr;                 // captures the conditional branch bodies
     long long gstatic = 0;                              // unconditional launches per block of the graph
@@ -616,6 +602,18 @@ struct gfors_ctx {
         long long force_deadline_rank = -1;   // this (simulated) rank reports its time limit as passed ...
         long long force_deadline_block = -1;  // ... from this block on (tests of the halt agreement)
         long long force_capture_fail = 0;     // sharded: make the graph capture fail (eager fallback test)
+        // load-time choices (applied by the next gfors_load; -1 = automatic)
+        long long dense_q = -1;       // dense int8 Q storage (dense_q.cuh): 1 force, 0 off
+        long long qx_fix = 1;         // fp32 iterates: exact fixed-point dp4a GEMV (0: fp64 FMA GEMV)
+        long long qx_reuse = 1;       // fp32 loop: the trigger's product of x_k serves the next block's first primal
+        long long push_dual = -1;     // sparse-xbar dual (push_dual.cuh): 1 force, 0 off
+        long long push_primal = -1;   // sparse-y primal (push_primal.cuh): 1 force, 0 off
+        long long delta_dual = 1;     // delta push of the dual
+        long long xskip = 1;          // stationary-column skip of the push primal
+        long long cond_branch = 0;    // graph conditional nodes run only the chosen mode's kernels
+        long long sparse_primal = -1; // zero-dual-skipping gather primal (sparse_primal.cuh): 1 force, 0 off
+        long long obj_bits = 1;       // bit-plane objective kernel for integral c (0: exact per-lane kernel)
+        long long load_timing = 0;    // print the load phases (host timer)
     } opt;
     double* d_rec = nullptr;       // [4] local record + [4*world] gathered records
     long long* d_regen = nullptr;  // [2] winner global index, round
@@ -648,7 +646,7 @@ void gfors_ctx::free_problem() {
     d_kval = d_ktval = nullptr;
     d_qval = d_c = d_ru = nullptr;
     d_rsign = nullptr;
-    d_qd = nullptr; d_tcitems = nullptr; d_tcoff = nullptr; qdense = false; tc_grid = 0; d_qs_uoff = nullptr;
+    d_qd = nullptr; d_tcitems = nullptr; d_tcoff = nullptr; qdense = false; tc_grid = 0;
     for (auto& c : cnt) c = CountList{};
     for (auto& c : cntrb) c = CountRb{};
     d_int_row = nullptr; d_int_rhs = nullptr; d_int_eq = nullptr; d_int_seg_start = nullptr; d_int_seg_slot = nullptr;
@@ -667,7 +665,7 @@ void gfors_ctx::free_prep() {
                    (void**)&d_red, (void**)&d_scalar, (void**)&d_segpart, (void**)&d_segpart2, (void**)&d_u, (void**)&d_ones, (void**)&d_rec, (void**)&d_regen, (void**)&d_plist[0], (void**)&d_plist[1], (void**)&d_pcount, (void**)&d_pflags, (void**)&d_acc, (void**)&d_rlist, (void**)&d_rcount, (void**)&d_wmax, (void**)&d_accx, (void**)&d_xst, (void**)&d_accv, (void**)&d_ones_cnt, (void**)&d_trig_flag, (void**)&d_part1,
                    (void**)&d_part2, (void**)&d_hist, (void**)&d_rho, (void**)&d_trace, (void**)&d_xbest,
                    (void**)&d_X, (void**)&d_viol, (void**)&d_iacc, &d_zpart, (void**)&d_z, (void**)&d_ctrl,
-                   (void**)&d_qx, (void**)&d_qdx, (void**)&d_qxpart, (void**)&d_Xs, (void**)&d_qacc,
+                   (void**)&d_qx, (void**)&d_qdx, (void**)&d_qxpart, (void**)&d_Xs,
                    (void**)&d_qxpart2, (void**)&d_qreuse, (void**)&d_cover_rows, (void**)&d_cover_best,
                    (void**)&d_cover_viol, (void**)&d_rp_rank, (void**)&d_rp_order, (void**)&d_rp_srow, (void**)&d_Tsamp};
     for (void** p : ps) { dfree(*p); *p = nullptr; }
@@ -738,7 +736,7 @@ inline void prof_end(gfors_ctx* C, cudaStream_t s, int cls, cudaEvent_t a) {
 
 // Mode branch (dual: gather vs push; primal: gather vs push; trigger pass: gather vs pushed).  By
 // default both branches are launched and every kernel checks the device decision itself and exits
-// at once when it is not the chosen one.  GFORS_COND_BRANCH=1: in the graph capture a one-thread
+// at once when it is not the chosen one.  Option cond_branch = 1: in the graph capture a one-thread
 // decide kernel sets the handle of an IF/ELSE conditional node instead, so only the chosen kernels
 // run (counted on the device, ctrl->dyn_launches) — measured SLOWER on config 5 (2.66 vs 2.55 ms
 // per block: 31 conditional nodes per block cost more than the early exits they replace).
@@ -822,28 +820,10 @@ void enqueue_qx(gfors_ctx* C, cudaStream_t s, QxSrc<TX> src, bool diff, double o
     const long long n = C->n;
     const long long nchunk = (n + QX_CW - 1) / QX_CW;
     if constexpr (sizeof(TX) == 4) {
-        if (C->qx_fix && C->qx_sym) {  // symmetric: upper-triangle tiles used for rows and columns
-            static bool attr_s[2] = {false, false};
-            if (!attr_s[diff ? 1 : 0]) {
-                if (diff) CK(cudaFuncSetAttribute(k_qx_sym<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qt_smem_bytes()));
-                else CK(cudaFuncSetAttribute(k_qx_sym<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qt_smem_bytes()));
-                attr_s[diff ? 1 : 0] = true;
-            }
-            const int grid = (int)std::min<long long>(C->qs_units, NUM_SMS_B200 * 2LL);
-            if (diff)
-                LAUNCH(C, s, KC_QX, (k_qx_sym<true><<<grid, QT_NT, qt_smem_bytes(), s>>>(C->tmQ64, n, C->d_qs_uoff, C->qs_ntc, src, C->d_qacc)));
-            else
-                LAUNCH(C, s, KC_QX, (k_qx_sym<false><<<grid, QT_NT, qt_smem_bytes(), s>>>(C->tmQ64, n, C->d_qs_uoff, C->qs_ntc, src, C->d_qacc)));
-            LAUNCH(C, s, KC_QX, (k_qx_final_acc<<<grid_for(n), 256, 0, s>>>(n, C->d_qacc, diff ? 9.313225746154785e-10 : 4.656612873077393e-10,
-                                                                           omega, out)));
-            return;
-        }
         if (C->qx_fix) {  // fp32 iterates: exact dp4a products on the fixed-point image of x
             const long long units = (n + QT_ROWS - 1) / QT_ROWS * nchunk;
-            // ring depth x CTAs per SM (GFORS_QX_CFG experiments: 6x2 default, 4x3, 3x4, 8x1)
-            const int cfg = C->qx_cfg;
-            const int minb = cfg == 1 ? 3 : (cfg == 2 ? 4 : (cfg == 3 ? 1 : 2));
-            const int grid = (int)std::min<long long>(units, (long long)NUM_SMS_B200 * minb);
+            // 4-stage ring x 3 CTAs per SM (sweep in round 1: 78.6 us vs 83.1 for 6x2 at n = 20480)
+            const int grid = (int)std::min<long long>(units, (long long)C->num_sms * 3);
             // product reuse across loop blocks (qx_reuse): the trigger computes S(x_k) (not the
             // difference) into d_qxpart2; the next block's first primal skips its GEMV and reads it
             // (k_int > 1: with one iteration per block the skipped GEMV would be the trigger's x_{k-1} product)
@@ -869,10 +849,7 @@ void enqueue_qx(gfors_ctx* C, cudaStream_t s, QxSrc<TX> src, bool diff, double o
         else                                                                                                          \
             LAUNCH(C, s, KC_QX, (k_qx_tma_fix<false, STV, MBV><<<grid, QT_NT, smb, s>>>(C->tmQ64, n, C->qld, src, dst, reuse))); \
     }
-            if (cfg == 1) QXF_LAUNCH(4, 3)
-            else if (cfg == 2) QXF_LAUNCH(3, 4)
-            else if (cfg == 3) QXF_LAUNCH(8, 1)
-            else QXF_LAUNCH(6, 2)
+            QXF_LAUNCH(4, 3)
 #undef QXF_LAUNCH
             if (trig_reuse)
                 LAUNCH(C, s, KC_QX, (k_qx_diff_final<<<grid_for(n), 256, 0, s>>>(n, C->qld, nchunk, C->d_qxpart2, C->d_qxpart,
@@ -885,7 +862,7 @@ void enqueue_qx(gfors_ctx* C, cudaStream_t s, QxSrc<TX> src, bool diff, double o
             return;
         }
     }
-    if (C->qx_tma) {
+    {
         const long long units = (n + QT_ROWS - 1) / QT_ROWS * nchunk;
         const int grid = (int)std::min<long long>(units, NUM_SMS_B200 * 2LL);
         static bool attr[4] = {false, false, false, false};
@@ -899,12 +876,6 @@ void enqueue_qx(gfors_ctx* C, cudaStream_t s, QxSrc<TX> src, bool diff, double o
             LAUNCH(C, s, KC_QX, (k_qx_tma<TX, true><<<grid, QT_NT, qt_smem_bytes(), s>>>(C->tmQ64, n, C->qld, src, C->d_qxpart)));
         else
             LAUNCH(C, s, KC_QX, (k_qx_tma<TX, false><<<grid, QT_NT, qt_smem_bytes(), s>>>(C->tmQ64, n, C->qld, src, C->d_qxpart)));
-    } else {
-        const int grid = NUM_SMS_B200 * 4;
-        if (diff)
-            LAUNCH(C, s, KC_QX, (k_qx_dense<TX, true><<<grid, QX_NT, 0, s>>>(C->d_qd, C->qld, n, src, C->d_qxpart)));
-        else
-            LAUNCH(C, s, KC_QX, (k_qx_dense<TX, false><<<grid, QX_NT, 0, s>>>(C->d_qd, C->qld, n, src, C->d_qxpart)));
     }
     LAUNCH(C, s, KC_QX, (k_qx_final<<<grid_for(n), 256, 0, s>>>(n, C->qld, nchunk, C->d_qxpart, omega, out)));
 }
@@ -1049,15 +1020,6 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
             LAUNCH(C, q, KC_PRIMAL_PUSH, (k_push_scatter_cols<T><<<grid_for(C->m * 32LL), NT, 0, q>>>(csr_K(C), ppr, st, ctrl, kint, j)));
             if (C->hasq)
                 LAUNCH(C, q, KC_PRIMAL_COL, (k_primal_push<T, true><<<pp_grid<T>(C->n), NT, 0, q>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
-                    csr_Kt(C), trig_push ? C->d_accv : nullptr, C->d_ones_cnt, C->d_trig_flag)));
-            else if (sizeof(T) == 4 && C->pp_occ == 3)
-                LAUNCH(C, q, KC_PRIMAL_COL, (k_primal_push<T, false, 3><<<pp_grid<T>(C->n, 3), NT, 0, q>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
-                    csr_Kt(C), trig_push ? C->d_accv : nullptr, C->d_ones_cnt, C->d_trig_flag)));
-            else if (sizeof(T) == 4 && C->pp_occ == 6)
-                LAUNCH(C, q, KC_PRIMAL_COL, (k_primal_push<T, false, 6><<<pp_grid<T>(C->n, 6), NT, 0, q>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
-                    csr_Kt(C), trig_push ? C->d_accv : nullptr, C->d_ones_cnt, C->d_trig_flag)));
-            else if (sizeof(T) == 4 && C->pp_occ == 8)
-                LAUNCH(C, q, KC_PRIMAL_COL, (k_primal_push<T, false, 8><<<pp_grid<T>(C->n, 8), NT, 0, q>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
                     csr_Kt(C), trig_push ? C->d_accv : nullptr, C->d_ones_cnt, C->d_trig_flag)));
             else
                 LAUNCH(C, q, KC_PRIMAL_COL, (k_primal_push<T, false><<<pp_grid<T>(C->n), NT, 0, q>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
@@ -1650,11 +1612,9 @@ static void do_preprocess(gfors_ctx* C, const gfors_prep_opts* o, gfors_scaling*
         C->d_qx = dalloc<double>(n);
         C->d_qdx = dalloc<double>(n);
         C->d_qxpart = dalloc<double>((n + QX_CW - 1) / QX_CW * C->qld);
-        C->d_qacc = dalloc<unsigned long long>(n);
         C->d_qxpart2 = dalloc<double>((n + QX_CW - 1) / QX_CW * C->qld);
         C->d_qreuse = dalloc<long long>(1);
         CK(cudaMemsetAsync(C->d_qreuse, 0xff, sizeof(long long), s));  // -1: nothing to reuse
-        CK(cudaMemsetAsync(C->d_qacc, 0, n * sizeof(unsigned long long), s));
     }
     unsigned long long* d_zr = dalloc<unsigned long long>(1);
     CK(cudaMemsetAsync(d_zr, 0, sizeof(unsigned long long), s));
@@ -2044,6 +2004,17 @@ gfors_status gfors_set_option(gfors_ctx* C, const char* key, int64_t value) {
     if (k == "force_deadline_rank") C->opt.force_deadline_rank = value;
     else if (k == "force_deadline_block") C->opt.force_deadline_block = value;
     else if (k == "force_capture_fail") C->opt.force_capture_fail = value;
+    else if (k == "dense_q") C->opt.dense_q = value;
+    else if (k == "qx_fix") C->opt.qx_fix = value;
+    else if (k == "qx_reuse") C->opt.qx_reuse = value;
+    else if (k == "push_dual") C->opt.push_dual = value;
+    else if (k == "push_primal") C->opt.push_primal = value;
+    else if (k == "delta_dual") C->opt.delta_dual = value;
+    else if (k == "xskip") C->opt.xskip = value;
+    else if (k == "cond_branch") C->opt.cond_branch = value;
+    else if (k == "sparse_primal") C->opt.sparse_primal = value;
+    else if (k == "obj_bits") C->opt.obj_bits = value;
+    else if (k == "load_timing") C->opt.load_timing = value;
     else input_error("gfors_set_option: unknown key '%s'", key);
     C->gvalid = false;
     C->gno = false;

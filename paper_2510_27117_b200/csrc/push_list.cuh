@@ -33,7 +33,7 @@ __device__ __forceinline__ unsigned* pl_count(const PushList& pl, int p) { retur
 __device__ __forceinline__ int* pl_list(const PushList& pl, int p) { return p ? pl.list[1] : pl.list[0]; }
 
 // delta state the dual of parity p starts from (block-uniform)
-// (dvalid == nullptr: delta push disabled, GFORS_DELTA_DUAL=0 — accumulators cleared after each use)
+// (dvalid == nullptr: delta push disabled, option delta_dual = 0 — accumulators cleared after each use)
 __device__ __forceinline__ bool pl_valid(const PushList& pl, int p) {
     return pl.dvalid && *(volatile unsigned*)(p ? pl.dvalid + 1 : pl.dvalid) != 0u;
 }

@@ -1,8 +1,7 @@
 """Dense-Q path (csrc/dense_q.cuh): the int8 dense GEMV in the PDHG step and
 the tcgen05 int8 objective kernel, against the CPU oracle (integer objectives bit-exact) and against
-the CSR path of the same library (GFORS_DENSE_Q=0).  One-step / 1000-iteration / whole-run parity
+the CSR path of the same library (option dense_q = 0).  One-step / 1000-iteration / whole-run parity
 of the dense path runs in test_gpu_parity.py (family "maxcut", which loads as dense Q)."""
-import os
 
 import numpy as np
 import pytest
@@ -19,18 +18,12 @@ def gf():
     return gf
 
 
-def _solver(gf, inst, precision=64, dense=None, tight=False):
-    old = os.environ.get("GFORS_DENSE_Q")
+def _solver(gf, inst, precision=64, dense=None, tight=False, options=None):
+    opts = dict(options or {})
     if dense is not None:
-        os.environ["GFORS_DENSE_Q"] = "1" if dense else "0"
-    try:
-        s = gf.Solver(0)
-        s.load(inst)
-    finally:
-        if old is None:
-            os.environ.pop("GFORS_DENSE_Q", None)
-        else:
-            os.environ["GFORS_DENSE_Q"] = old
+        opts["dense_q"] = 1 if dense else 0
+    s = gf.Solver(0, options=opts)
+    s.load(inst)
     tol, it = (1e-14, 100000) if tight else (1e-7, 500)
     sc = s.preprocess(precision=precision, tol=tol, max_iter=it)
     return s, sc
@@ -164,52 +157,16 @@ def test_config6_fullsize_sampled(gf):
     assert np.isfinite(z)
 
 
-@pytest.mark.parametrize("n", [300, 1000, 1300])
-def test_symmetric_gemv_bit_identical(gf, n):
-    """fp32 iterates: the symmetric GEMV (upper-triangle tiles used for rows and columns, int64 atomics)
-    and the full GEMV compute the same exact integer sums on the fixed-point x (and the same trigger
-    difference product), so steps and indicators are bit-identical."""
-    inst = G.max_cut(n, 0.5, 3 * n)
-    out = []
-    for sym in ("1", "0"):  # GFORS_QX_SYM=1 forces the symmetric kernel (off by default)
-        old = os.environ.get("GFORS_QX_SYM")
-        os.environ["GFORS_QX_SYM"] = sym
-        try:
-            s, _ = _solver(gf, inst, 32)
-        finally:
-            if old is None:
-                os.environ.pop("GFORS_QX_SYM", None)
-            else:
-                os.environ["GFORS_QX_SYM"] = old
-        rng = np.random.default_rng(n)
-        x = rng.random(n).astype(np.float32).astype(np.float64)
-        x[rng.random(n) < 0.3] = 0.0
-        s.set_state(x, x, np.zeros(0))
-        s.step(3, 0.01, 0.99 ** 0.5, 0.99 ** 0.5)
-        ind = s.indicators(0.01, 0.99 ** 0.5, 0.99 ** 0.5)
-        out.append((s.get_state()[0], ind))
-    assert np.array_equal(out[0][0], out[1][0])
-    assert out[0][1] == out[1][1]
-
-
 @pytest.mark.parametrize("kint", [10, 3, 1])
 def test_gemv_reuse_across_blocks(gf, kint):
-    """fp32 loop: the trigger's product of x_k serving the next block's first primal (GFORS_QX_REUSE)
+    """fp32 loop: the trigger's product of x_k serving the next block's first primal (option qx_reuse)
     gives the same trajectory as recomputing it (the first primal's product is bit-identical; the
     s^x term of the indicators differs only in how the fixed-point difference is formed), and the
     same incumbent."""
     inst = G.max_cut(400, 0.5, 21)
     res = []
-    for reuse in ("1", "0"):
-        old = os.environ.get("GFORS_QX_REUSE")
-        os.environ["GFORS_QX_REUSE"] = reuse
-        try:
-            s, _ = _solver(gf, inst, 32)
-        finally:
-            if old is None:
-                os.environ.pop("GFORS_QX_REUSE", None)
-            else:
-                os.environ["GFORS_QX_REUSE"] = old
+    for reuse in (1, 0):
+        s, _ = _solver(gf, inst, 32, options={"qx_reuse": reuse})
         kw = dict(k_int=kint, k_b=128, tol_primal=-1.0, tol_dual=-1.0, tol_binary=-1.0, stall_rel=-1.0)
         s.run(max_iters=30 * kint, **kw)
         x = s.get_state()[0]

@@ -27,11 +27,12 @@ def gf():
     return gf
 
 
-def _pair(gf, inst, precision=64, tight=False):
+def _pair(gf, inst, precision=64, tight=False, options=None):
     """tight: run both power iterations to 1e-14 so the scalings agree far below the PDHG tolerance
-    (at the default 1e-7 stop they agree to ~1e-8 only)."""
+    (at the default 1e-7 stop they agree to ~1e-8 only).  options: gfors_set_option before
+    the load (forced PDHG variants)."""
     tol, it = (1e-14, 100000) if tight else (1e-7, 500)
-    s = gf.Solver(0)
+    s = gf.Solver(0, options=options)
     s.load(inst)
     sc = s.preprocess(precision=precision, tol=tol, max_iter=it)
     o = O.Oracle(inst)
@@ -324,12 +325,11 @@ def test_errors_fail_loudly(gf):
 
 
 @pytest.mark.parametrize("fam", ["setcover", "general", "bqp"])
-def test_sparse_primal_variant_parity(gf, fam, monkeypatch):
+def test_sparse_primal_variant_parity(gf, fam):
     """The zero-dual-skipping primal (forced on small instances) against the oracle: 1000 fp64
     iterations within 1e-5, and a full run with identical incumbent sequence."""
-    monkeypatch.setenv("GFORS_SPARSE_PRIMAL", "1")
     inst = G.SMALL[fam](11)
-    s, _, o, _ = _pair(gf, inst, 64)
+    s, _, o, _ = _pair(gf, inst, 64, options={"sparse_primal": 1})
     tau = math.sqrt(0.99)
     rho = O.rho_schedule(1e-3, 10.0, 100.0, 2.0, 1e-6, 100)
     o.state_init()
@@ -351,12 +351,11 @@ def test_sparse_primal_variant_parity(gf, fam, monkeypatch):
 
 
 @pytest.mark.parametrize("fam", ["setcover", "mis", "bqp"])
-def test_push_dual_variant_parity(gf, fam, monkeypatch):
+def test_push_dual_variant_parity(gf, fam):
     """Sparse-xbar dual (fixed-point scatter, forced on) against the oracle: 1000 fp64 iterations
     within 1e-5; a run keeps the same incumbent and iteration accounting."""
-    monkeypatch.setenv("GFORS_PUSH_DUAL", "1")
     inst = G.SMALL[fam](12)
-    s, _, o, _ = _pair(gf, inst, 64)
+    s, _, o, _ = _pair(gf, inst, 64, options={"push_dual": 1})
     tau = math.sqrt(0.99)
     rho = O.rho_schedule(1e-3, 10.0, 100.0, 2.0, 1e-6, 100)
     o.state_init()
@@ -379,13 +378,11 @@ def test_push_dual_variant_parity(gf, fam, monkeypatch):
 
 @pytest.mark.parametrize("fam", ["setcover", "mis", "bqp"])
 @pytest.mark.parametrize("prec,tol", [(64, 1e-5), (32, 1e-3)])
-def test_push_primal_variant_parity(gf, fam, prec, tol, monkeypatch):
+def test_push_primal_variant_parity(gf, fam, prec, tol):
     """Sparse-dual primal (fixed-point column scatter, forced on together with the push dual) against
     the oracle: 1000 iterations within the north_star tolerance, same run accounting."""
-    monkeypatch.setenv("GFORS_PUSH_DUAL", "1")
-    monkeypatch.setenv("GFORS_PUSH_PRIMAL", "1")
     inst = G.SMALL[fam](13)
-    s, _, o, _ = _pair(gf, inst, prec)
+    s, _, o, _ = _pair(gf, inst, prec, options={"push_dual": 1, "push_primal": 1})
     tau = math.sqrt(0.99)
     rho = O.rho_schedule(1e-3, 10.0, 100.0, 2.0, 1e-6, 100)
     o.state_init()
@@ -407,25 +404,22 @@ def test_push_primal_variant_parity(gf, fam, prec, tol, monkeypatch):
         assert zg == zo or (math.isinf(zg) and math.isinf(zo))
 
 
-@pytest.mark.parametrize("switch", ["GFORS_DELTA_DUAL", "GFORS_XSKIP", "GFORS_COND_BRANCH"])
+@pytest.mark.parametrize("switch", ["delta_dual", "xskip", "cond_branch"])
 @pytest.mark.parametrize("fam", ["setcover", "mis"])
 @pytest.mark.parametrize("prec", [64, 32])
-def test_exact_shortcuts_bit_identical(gf, switch, fam, prec, monkeypatch):
-    """Two shortcuts must reproduce the plain computation BIT FOR BIT (push modes forced on):
-    GFORS_DELTA_DUAL — the delta push of the dual adds exact integer differences instead of a fresh
-    fixed-point sum; GFORS_XSKIP — the push primal skips columns whose update provably returns the
-    value already stored; GFORS_COND_BRANCH — graph conditional nodes run only the chosen mode's
-    kernels instead of launching both with early exits.  Same iterates after hook steps, same run
-    trace and incumbent."""
-    monkeypatch.setenv("GFORS_PUSH_DUAL", "1")
-    monkeypatch.setenv("GFORS_PUSH_PRIMAL", "1")
+def test_exact_shortcuts_bit_identical(gf, switch, fam, prec):
+    """Shortcuts that must reproduce the plain computation BIT FOR BIT (push modes forced on):
+    delta_dual — the delta push of the dual adds exact integer differences instead of a fresh
+    fixed-point sum; xskip — the push primal skips columns whose update provably returns the value
+    already stored; cond_branch — graph conditional nodes run only the chosen mode's kernels
+    instead of launching both with early exits.  Same iterates after hook steps, same run trace and
+    incumbent."""
     inst = G.SMALL[fam](14)
     tau = math.sqrt(0.99)
     rho = O.rho_schedule(1e-3, 10.0, 100.0, 2.0, 1e-6, 60)
     out = []
-    for on in ("0", "1"):
-        monkeypatch.setenv(switch, on)
-        s = gf.Solver(0)
+    for on in (0, 1):
+        s = gf.Solver(0, options={"push_dual": 1, "push_primal": 1, switch: on})
         s.load(inst)
         s.preprocess(precision=prec, tol=1e-10, max_iter=5000)
         s.set_state(np.zeros(inst["n"]), np.zeros(inst["n"]), np.zeros(inst["m"]))
