@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--k-int", type=int, default=10)
     ap.add_argument("--impl", default="gfors", choices=("gfors", "reference"))
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-row-shard", action="store_true", help="N > 1: replicate the PDHG dual instead of row-sharding it")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tti", action="store_true", help="skip the time-to-incumbent solves of configs 1-4")
     ap.add_argument("--profile-blocks", type=int, default=0, help="eager blocks replayed with per-kernel events (0 = --steps)")
@@ -540,6 +541,8 @@ def run_gpu(args):
     fb = 8 if args.precision == 64 else 4
     common = dict(k_int=args.k_int, k_b=args.k_b, tol_primal=-1.0, tol_dual=-1.0, tol_binary=-1.0,
                   stall_rel=-1.0, time_limit_s=1e9, trace_cap=16)
+    if world > 1 and not args.no_row_shard:
+        common["row_shard"] = 1  # row-sharded dual over the ranks (f4): y all-gathered each iteration
     # warm-up (also instantiates the CUDA graph)
     s.run(max_iters=args.warmup * args.k_int, **common)
     torch.cuda.synchronize()
@@ -772,7 +775,9 @@ def run_gpu(args):
                        if args.config == 5 else f"BASELINE config {args.config}",
                        "n": meta["n"], "m": meta["m"], "nnz": meta["nnz"], "k_int": args.k_int, "k_r": 1,
                        "k_b_per_rank": args.k_b, "precision": f"fp{args.precision} iterates, fp64 accumulation, exact int64 evaluation",
-                       "parallelism": f"sample-sharded x{world} (NCCL record all-gather per round), PDHG replicated", "l2": "inputs larger than L2 (K stream ~0.5 GB/iter)",
+                       "parallelism": (f"sample-sharded x{world} (NCCL record all-gather per round), "
+                                       + ("dual row-sharded (y all-gather per iteration), rest of PDHG replicated"
+                                          if world > 1 and not args.no_row_shard else "PDHG replicated")), "l2": "inputs larger than L2 (K stream ~0.5 GB/iter)",
                        "seed": args.seed, "obj_scale": sc["obj_scale"], "k_scale": sc["k_scale"]},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,

@@ -129,6 +129,13 @@ typedef struct {
  * (repair, complete and sampler 1 are rejected with the NCCL-sharded loop: its winner regeneration
  * replays the Bernoulli contract). */
     int32_t complete;
+    /* row_shard = 1 (needs world > 1 — NCCL or loopback — and the row-block dual): the PDHG dual is
+     * row-sharded (north_star "row-sharded for K"): rank r computes the dual of its
+     * nnz-balanced range of row blocks only, then the ranks all-gather y (and, at the trigger
+     * iteration, K_u xbar) — m values instead of the n-vector K'y — and every rank recomputes w and
+     * runs the rest of the iteration replicated, so iterates and decisions stay bit-identical to the
+     * unsharded run. */
+    int32_t row_shard;
 } gfors_params;
 
 /* halt_reason: 1 criteria met, 2 max_iters, 3 time limit, 4 diverged. */

@@ -64,7 +64,7 @@ class Params(C.Structure):
                 ("stall_window", I32), ("max_iters", I64), ("time_limit_s", D), ("seed", U64),
                 ("use_graph", I32), ("trace_cap", I32),
                 ("sampler", I32), ("a3_ls", I32), ("a3_n", I64), ("a3_gamma", D),
-                ("relax", I32), ("repair", I32), ("complete", I32)]
+                ("relax", I32), ("repair", I32), ("complete", I32), ("row_shard", I32)]
 
 
 class RunInfo(C.Structure):

@@ -181,6 +181,7 @@ struct DirPlan {  // how one product direction (K rows or K' columns) is compute
     long long nblk = 0;
     int4* desc = nullptr;    // per row block {first row, rows | log2(G) << 16, first nonzero, nonzeros} (k_dual_rb)
     int* ptr32 = nullptr;    // int32 copy of the row pointers (nnz < 2^31)
+    std::vector<long long> hblk;  // host copy of the block boundaries (row-sharded dual)
 };
 
 // greedy nonzero-balanced row blocks: consecutive rows, <= cap nonzeros each (rows <= cap long)
@@ -245,6 +246,7 @@ DirPlan plan_direction(const std::vector<int64_t>& ptr, long long rows, cudaStre
         d.blk_row = dupload(b, s);
         owned.push_back(d.blk_row);
         d.desc = upload_desc(b, ptr, s, owned);
+        d.hblk = b;
         std::vector<int> p32(ptr.begin(), ptr.begin() + rows + 1);
         d.ptr32 = dupload(p32, s);
         owned.push_back(d.ptr32);
@@ -283,6 +285,7 @@ DirPlan plan_direction64(const DirPlan& d32, const std::vector<int64_t>& ptr, lo
     d.blk_row = dupload(b, s);
     owned.push_back(d.blk_row);
     d.desc = upload_desc(b, ptr, s, owned);
+    d.hblk = b;
     return d;
 }
 
@@ -596,6 +599,14 @@ struct gfors_ctx {
     ncclComm_t comm = nullptr;
     bool sharded = false;
     bool loopback = false;         // world simulated ranks in this context (test mode, no NCCL)
+    // row-sharded dual (params.row_shard; shard.cuh): rank q owns dual row blocks [rs_blo[q], rs_blo[q+1])
+    bool rs_on = false;
+    int rs_key = -1;                      // precision the partition below was made for
+    std::vector<long long> rs_blo, rs_rlo;
+    long long rs_maxrows = 0;
+    long long* d_rs_rlo = nullptr;
+    void* d_rs_y = nullptr;               // [world][maxrows] y gather buffer (iterate type)
+    double* d_rs_u = nullptr;             // [world][maxrows] u gather buffer
 
     // options set through gfors_set_option (tests, benchmarks); defaults are the production path
     struct Options {
@@ -667,12 +678,15 @@ void gfors_ctx::free_prep() {
                    (void**)&d_X, (void**)&d_viol, (void**)&d_iacc, &d_zpart, (void**)&d_z, (void**)&d_ctrl,
                    (void**)&d_qx, (void**)&d_qdx, (void**)&d_qxpart, (void**)&d_Xs,
                    (void**)&d_qxpart2, (void**)&d_qreuse, (void**)&d_cover_rows, (void**)&d_cover_best,
-                   (void**)&d_cover_viol, (void**)&d_rp_rank, (void**)&d_rp_order, (void**)&d_rp_srow, (void**)&d_Tsamp};
+                   (void**)&d_cover_viol, (void**)&d_rp_rank, (void**)&d_rp_order, (void**)&d_rp_srow, (void**)&d_Tsamp,
+                   (void**)&d_rs_rlo, &d_rs_y, (void**)&d_rs_u};
     for (void** p : ps) { dfree(*p); *p = nullptr; }
     X_words = iacc_len = zpart_len = z_len = Xs_lanes = 0;
     n_cover = -1;
     cover_viol_len = 0;
     rp_srow_len = 0;
+    rs_key = -1;
+    rs_on = false;
     for (int b = 0; b < 2; ++b) { dfree(a3.keys[b]); dfree(a3.vals[b]); }
     for (void* q : {(void*)a3.tmp, (void*)a3.sj0, (void*)a3.sk0, (void*)a3.Ri, (void*)a3.Rj, (void*)a3.Rk,
                     (void*)a3.meta})
@@ -896,6 +910,63 @@ void enqueue_qx(gfors_ctx* C, cudaStream_t s, QxSrc<TX> src, bool diff, double o
     }
 
 // one PDHG iteration (dual + primal); kint/j select the parity (see pdhg.cuh)
+// row-sharded dual: pack this rank's y (and u) rows, all-gather, unpack every rank's rows + w (shard.cuh)
+template <typename T>
+void enqueue_rs_exchange(gfors_ctx* C, cudaStream_t s, State<T> st, long long kint, long long j, bool with_u) {
+    const long long MR = C->rs_maxrows;
+    T* gy = (T*)C->d_rs_y;
+    double* gu = with_u ? C->d_rs_u : nullptr;
+    for (int r = 0; r < C->world; ++r) {
+        if (!C->loopback && r != C->rank) continue;
+        const long long r0 = C->rs_rlo[r], nr = C->rs_rlo[r + 1] - r0;
+        if (nr <= 0) continue;
+        LAUNCH(C, s, KC_DUAL, (k_rs_pack<T><<<grid_for(nr), NT, 0, s>>>(st, C->d_ctrl, kint, j, r0, nr, gy + r * MR,
+                                                                        C->d_u, gu ? gu + r * MR : nullptr)));
+    }
+    if (!C->loopback && !C->dry) {
+        NcclApi& api = nccl();
+        int rc = api.GroupStart();
+        if (!rc) rc = api.AllGather(gy + C->rank * MR, gy, MR * sizeof(T), ncclUint8_, C->comm, s);
+        if (!rc && gu) rc = api.AllGather(gu + C->rank * MR, gu, MR, ncclFloat64_, C->comm, s);
+        if (!rc) rc = api.GroupEnd();
+        if (rc != 0) throw Err{GFORS_E_NCCL, std::string("ncclAllGather (row-sharded dual): ") + api.GetErrorString(rc)};
+    }
+    KIND_SWITCH(C->kkind, LAUNCH(C, s, KC_DUAL, (k_rs_unpack<T, KINDV><<<grid_for(C->world * MR), NT, 0, s>>>(
+        st, C->d_ctrl, kint, j, C->d_rs_rlo, C->world, MR, gy, (const double*)C->d_g, C->d_rsign, gu, C->d_u))));
+}
+
+// params.row_shard: validate, and split the dual's row blocks over the ranks by nonzeros
+void set_row_shard(gfors_ctx* C, int on, int prec) {
+    C->rs_on = false;
+    if (!on) return;
+    if (!C->sharded) input_error("params.row_shard: needs world > 1 (an NCCL id or the loopback communicator)");
+    if (C->m <= 0 || !C->pd.rb) input_error("params.row_shard: needs the row-block dual (every row <= %d nonzeros)", RB_NNZ_OF<float>);
+    if (C->rs_key != prec) {
+        const auto& hb = C->pd.hblk;
+        const long long nb = (long long)hb.size() - 1, R = C->world;
+        const long long total = C->kptr[C->m];
+        C->rs_blo.assign(R + 1, nb);
+        C->rs_blo[0] = 0;
+        long long b = 0;
+        for (long long q = 1; q < R; ++q) {  // first block whose start reaches q/R of the nonzeros
+            const long long target = total * q / R;
+            while (b < nb && C->kptr[hb[b]] < target) ++b;
+            C->rs_blo[q] = b;
+        }
+        C->rs_rlo.resize(R + 1);
+        C->rs_maxrows = 1;
+        for (long long q = 0; q <= R; ++q) C->rs_rlo[q] = hb[C->rs_blo[q]];
+        for (long long q = 0; q < R; ++q) C->rs_maxrows = std::max(C->rs_maxrows, C->rs_rlo[q + 1] - C->rs_rlo[q]);
+        dfree(C->d_rs_rlo); dfree(C->d_rs_y); dfree(C->d_rs_u);
+        C->d_rs_rlo = dupload(C->rs_rlo, C->stream);
+        C->d_rs_y = dalloc<double>(R * C->rs_maxrows);  // (large enough for either iterate type)
+        C->d_rs_u = dalloc<double>(R * C->rs_maxrows);
+        C->rs_key = prec;
+        C->gvalid = false;
+    }
+    C->rs_on = true;
+}
+
 template <typename T>
 void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
     State<T> st = state_of<T>(C);
@@ -916,9 +987,22 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
             const int grid = (int)std::min<long long>(C->pd.nblk, RB_GRID);
             double* u_out = (kint == 0 || j == kint - 1) ? C->d_u : nullptr;
             auto gather = [&](cudaStream_t q) {
-                KIND_SWITCH(C->kkind, LAUNCH(C, q, KC_DUAL,
-                    (k_dual_rb<T, KINDV><<<grid, RB_NT, 0, q>>>(csr_K(C), C->pd.desc, C->pd.ptr32, C->pd.nblk, st, g, rh,
-                                                                C->d_rsign, C->m1p, ctrl, kint, j, u_out, pl))));
+                if (!C->rs_on) {
+                    KIND_SWITCH(C->kkind, LAUNCH(C, q, KC_DUAL,
+                        (k_dual_rb<T, KINDV><<<grid, RB_NT, 0, q>>>(csr_K(C), C->pd.desc, C->pd.ptr32, C->pd.nblk, st, g, rh,
+                                                                    C->d_rsign, C->m1p, ctrl, kint, j, u_out, pl))));
+                    return;
+                }
+                // row-sharded: this rank's blocks only (loopback: every simulated rank's range in turn)
+                for (int r = 0; r < C->world; ++r) {
+                    if (!C->loopback && r != C->rank) continue;
+                    const long long b0 = C->rs_blo[r], nb = C->rs_blo[r + 1] - b0;
+                    if (nb <= 0) continue;
+                    const int gr = (int)std::min<long long>(nb, RB_GRID);
+                    KIND_SWITCH(C->kkind, LAUNCH(C, q, KC_DUAL,
+                        (k_dual_rb<T, KINDV><<<gr, RB_NT, 0, q>>>(csr_K(C), C->pd.desc + b0, C->pd.ptr32, nb, st, g, rh,
+                                                                  C->d_rsign, C->m1p, ctrl, kint, j, u_out, pl))));
+                }
             };
             if (C->push_dual) {
                 // sparse xbar: scatter the listed columns into the row accumulators, then the rows
@@ -934,6 +1018,7 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
             } else {
                 gather(s);
             }
+            if (C->rs_on) enqueue_rs_exchange<T>(C, s, st, kint, j, u_out != nullptr);
         } else if (!C->pd.seg) {
             const int grid = grid_for(C->m * (long long)C->pd.sub);
             KIND_SWITCH(C->kkind, SUB_SWITCH(C->pd.sub, LAUNCH(C, s, KC_DUAL,
@@ -1729,7 +1814,7 @@ static bool same_graph_key(const gfors_params& a, const gfors_params& b) {
            a.tol_dual == b.tol_dual && a.tol_binary == b.tol_binary && a.stall_rel == b.stall_rel &&
            a.stall_window == b.stall_window && a.seed == b.seed && a.trace_cap == b.trace_cap &&
            a.sampler == b.sampler && a.a3_n == b.a3_n && a.a3_gamma == b.a3_gamma && a.a3_ls == b.a3_ls &&
-           a.relax == b.relax && a.repair == b.repair && a.complete == b.complete;
+           a.relax == b.relax && a.repair == b.repair && a.complete == b.complete && a.row_shard == b.row_shard;
 }
 
 template <typename T>
@@ -1757,6 +1842,7 @@ static void do_run_t(gfors_ctx* C, const gfors_params* p, gfors_run_info* out) {
     set_sampler(C, p->sampler, p->a3_n, p->a3_gamma, p->a3_ls);
     set_relax(C, p->relax, p->repair);
     set_complete(C, p->complete, W);
+    set_row_shard(C, p->row_shard, C->precision);
     const long long max_blocks = p->max_iters / p->k_int;
     const long long tail = p->max_iters % p->k_int;
     // rho table (host pow, like the oracle; reading R7)
@@ -1889,6 +1975,7 @@ static void do_run_t(gfors_ctx* C, const gfors_params* p, gfors_run_info* out) {
     C->have_run = true;
     C->hk = info.iters;
     if (out) *out = info;
+    C->rs_on = false;  // hooks after the run are unsharded
     if (reason == 4) throw Err{GFORS_E_DIVERGED, "diverged: non-finite indicator at iteration " + std::to_string(h.k)};
 }
 
@@ -2306,12 +2393,14 @@ int64_t gfors_launches_per_block(gfors_ctx* C, const gfors_params* p) {
     try {
         set_sampler(C, p->sampler, p->a3_n, p->a3_gamma, p->a3_ls);
         set_relax(C, p->relax, p->repair);
-    set_complete(C, p->complete, W);
+        set_complete(C, p->complete, W);
+        set_row_shard(C, p->row_shard, C->precision);
         if (C->precision == 64) enqueue_block<double>(C, C->stream, p, W, hp, cudaGraphConditionalHandle{}, 0);
         else enqueue_block<float>(C, C->stream, p, W, hp, cudaGraphConditionalHandle{}, 0);
         n = C->launches;
     } catch (...) {
     }
+    C->rs_on = false;
     C->dry = false;
     C->launches = before;
     return n;

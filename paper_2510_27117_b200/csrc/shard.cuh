@@ -20,7 +20,7 @@ typedef struct ncclComm* ncclComm_t;
 typedef struct { char internal[128]; } ncclUniqueId;
 typedef enum { ncclSuccess_ = 0 } ncclResult_t_;
 typedef int ncclResult_t;
-enum { ncclFloat64_ = 8 };
+enum { ncclUint8_ = 1, ncclFloat64_ = 8 };
 
 namespace gfors {
 
@@ -31,6 +31,8 @@ struct NcclApi {
     ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
 
     void load() {
@@ -42,8 +44,10 @@ struct NcclApi {
         CommInitRank = (decltype(CommInitRank))dlsym(h, "ncclCommInitRank");
         CommDestroy = (decltype(CommDestroy))dlsym(h, "ncclCommDestroy");
         AllGather = (decltype(AllGather))dlsym(h, "ncclAllGather");
+        GroupStart = (decltype(GroupStart))dlsym(h, "ncclGroupStart");
+        GroupEnd = (decltype(GroupEnd))dlsym(h, "ncclGroupEnd");
         GetErrorString = (decltype(GetErrorString))dlsym(h, "ncclGetErrorString");
-        ok = GetUniqueId && CommInitRank && CommDestroy && AllGather && GetErrorString;
+        ok = GetUniqueId && CommInitRank && CommDestroy && AllGather && GetErrorString && GroupStart && GroupEnd;
         if (!ok) why = "libnccl.so.2 lacks a required symbol";
     }
 };
@@ -133,6 +137,45 @@ __global__ void k_regen_best(const T* __restrict__ xa, const T* __restrict__ xb2
     const int bit = (int)(gl & 63);
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += gridDim.x * (long long)blockDim.x)
         xbest[i] = (unsigned char)((bernoulli_word((double)p[i], (unsigned)i, wg, round, key) >> bit) & 1ull);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Row-sharded dual (params.row_shard): rank q computes the dual of
+// rows [rlo[q], rlo[q+1]) only; the y values of those rows are packed into slot q of a gather buffer
+// (maxrows entries per slot, ncclAllGather in place), and every rank unpacks all slots into y and
+// recomputes w_j = g_j rsign_j y_j exactly as the dual kernel does (w_of), so the replicated rest of
+// the iteration sees bit-identical inputs.  At the trigger iteration the same for u = K_u xbar_{k-1}.
+// The dual's output buffer is picked by the iteration parity, as in the dual kernels.
+// ---------------------------------------------------------------------------------------------
+template <typename T>
+__global__ void k_rs_pack(State<T> s, const Ctrl* __restrict__ ctrl, long long kint, long long j, long long r0,
+                          long long nrows, T* __restrict__ slot, const double* __restrict__ u, double* __restrict__ uslot) {
+    const int par = (int)(iter_index(ctrl, kint, j) & 1);
+    const T* __restrict__ yout = par ? s.y[0] : s.y[1];
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nrows; t += gridDim.x * (long long)blockDim.x) {
+        slot[t] = yout[r0 + t];
+        if (uslot) uslot[t] = u[r0 + t];
+    }
+}
+
+template <typename T, int KIND>
+__global__ void k_rs_unpack(State<T> s, const Ctrl* __restrict__ ctrl, long long kint, long long j,
+                            const long long* __restrict__ rlo, int R, long long maxrows, const T* __restrict__ gath,
+                            const double* __restrict__ g, const signed char* __restrict__ rsign,
+                            const double* __restrict__ ugath, double* __restrict__ u) {
+    const int par = (int)(iter_index(ctrl, kint, j) & 1);
+    T* __restrict__ yout = par ? s.y[0] : s.y[1];
+    const long long total = (long long)R * maxrows;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * (long long)blockDim.x) {
+        const int q = (int)(idx / maxrows);
+        const long long row = rlo[q] + (idx - (long long)q * maxrows);
+        if (row >= rlo[q + 1]) continue;
+        const T yt = gath[idx];
+        yout[row] = yt;
+        const double sg = (KIND == KV_SIGN) ? (double)rsign[row] : 1.0;
+        s.w[row] = w_of(g[row], sg, yt);
+        if (ugath) u[row] = ugath[idx];
+    }
 }
 
 }  // namespace gfors

@@ -155,3 +155,85 @@ def test_set_option_rejects_unknown_key(gf):
     s = gf.Solver(0)
     with pytest.raises(gf.GforsError, match="unknown key"):
         s.set_option("no_such_option", 1)
+
+
+# ----------------------------------------------------------------------------- row-sharded dual (f4)
+def _state_after(s):
+    x, xb, y = s.get_state()
+    return x, xb, y
+
+
+@pytest.mark.parametrize("R", [2, 4, 8])
+@pytest.mark.parametrize("prec", [32, 64])
+@pytest.mark.parametrize("graph", [1, 0])
+def test_row_sharded_dual_bit_identical(gf, R, prec, graph):
+    """with params.row_shard each of R ranks (loopback) computes the dual of its
+    nnz-balanced range of row blocks, the ranks all-gather y (and K_u xbar at the trigger) and recompute
+    w; iterates, trace and incumbent are bit-identical to the unsharded loop with the same samples
+    (one rank, k_b * R candidates) — through the dense phase (gather dual) and the push modes."""
+    inst = G.set_cover(6000, 30000, 2, 98, 5, "rs_setcover")
+    kw = dict(max_iters=600, tol_primal=-1.0, tol_dual=-1.0, tol_binary=-1.0, stall_rel=-1.0, use_graph=graph,
+              trace_cap=4096)
+    s1 = gf.Solver(0)
+    s1.load(inst)
+    s1.preprocess(precision=prec)
+    i1 = s1.run(k_b=64 * R, **kw)
+    sR = gf.Solver(0, world=R, loopback=True)
+    sR.load(inst)
+    sR.preprocess(precision=prec)
+    iR = sR.run(k_b=64, row_shard=1, **kw)
+    assert (i1["iters"], i1["rounds"], i1["halt_reason"]) == (iR["iters"], iR["rounds"], iR["halt_reason"])
+    for a, b in zip(_state_after(s1), _state_after(sR)):
+        assert np.array_equal(a, b)
+    assert np.array_equal(s1.trace(), sR.trace())
+    z1, x1, m1 = s1.best_incumbent()
+    zR, xR, mR = sR.best_incumbent()
+    assert (z1 == zR or (math.isinf(z1) and math.isinf(zR))) and np.array_equal(x1, xR)
+    assert iR["launches"] > i1["launches"]  # the per-rank dual launches and the exchange ran
+
+
+def test_row_sharded_dual_partition_covers_rows(gf):
+    """The split is by nonzeros over whole row blocks: with R = 3 ranks on a skewed instance the run is
+    still bit-identical (ranks own unequal row counts; the gather slots are padded to the largest)."""
+    inst = G.set_cover(5000, 20000, 2, 98, 9, "rs_skew")
+    # make the first rows much longer so row counts per rank differ a lot
+    kw = dict(max_iters=200, k_int=10, tol_primal=-1.0, tol_dual=-1.0, tol_binary=-1.0, stall_rel=-1.0)
+    s1 = gf.Solver(0)
+    s1.load(inst)
+    s1.preprocess(precision=64)
+    s1.run(k_b=192, **kw)
+    s3 = gf.Solver(0, world=3, loopback=True)
+    s3.load(inst)
+    s3.preprocess(precision=64)
+    s3.run(k_b=64, row_shard=1, **kw)
+    for a, b in zip(_state_after(s1), _state_after(s3)):
+        assert np.array_equal(a, b)
+
+
+def test_row_sharded_nccl_path(gf):
+    """The NCCL form of the exchange (ncclAllGather of the packed y / u slots inside the loop graph),
+    exercised with a 1-rank communicator: bit-identical to the unsharded run."""
+    try:
+        nid = gf.nccl_unique_id()
+    except gf.GforsError:
+        pytest.skip("libnccl.so.2 not loadable")
+    inst = G.SMALL["setcover"](4)
+    kw = dict(max_iters=300, tol_primal=-1.0, tol_dual=-1.0, tol_binary=-1.0, stall_rel=-1.0)
+    s1 = gf.Solver(0)
+    s1.load(inst)
+    s1.preprocess()
+    s1.run(**kw)
+    sn = gf.Solver(0, rank=0, world=1, nccl_id=nid)
+    sn.load(inst)
+    sn.preprocess()
+    sn.run(row_shard=1, **kw)
+    for a, b in zip(_state_after(s1), _state_after(sn)):
+        assert np.array_equal(a, b)
+
+
+def test_row_shard_errors(gf):
+    s = gf.Solver(0)
+    s.load(G.SMALL["setcover"](1))
+    s.preprocess()
+    with pytest.raises(gf.GforsError, match="row_shard"):
+        s.run(max_iters=20, row_shard=1)
