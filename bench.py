@@ -402,6 +402,41 @@ def run_f1_maxcut(args, gf, stream, local):
     }
 
 
+def run_f1_dense_k(args, gf, stream, local):
+    """Next row f1, dense-K half ("int8 MMA for MKP's K.X"): config 3 (MKP n = 1e5, m = 50,
+    density 0.5).  Per Alg. 1 block (eager replay with per-launch CUDA events, 20 blocks from x0): the
+    feasibility class with the integer rows on tensor cores (split-K tcgen05 kind::i8, exact int32)
+    against the CUDA-core integer path (option dense_k = 0), and the tensor kernel's roofline: ops
+    2 * ceil128(m) * k_b * ceil128(n) per launch; bytes = the int8 rows + the unpacked samples."""
+    inst = make_instance(3, args.seed)
+    n, m = int(inst["n"]), int(inst["m"])
+    out = {"workload": "config3", "desc": "multi-dimensional knapsack n=1e5, m=50, density 0.5"}
+    peak_hbm, _, peaks = measured_peaks()
+    i8_peak = peaks.get("bf16_tflops", 1628.4) * 2.0
+    for dk in (1, 0):
+        s = gf.Solver(local, stream=stream.cuda_stream, options={"dense_k": dk})
+        s.load(inst)
+        s.preprocess(precision=args.precision)
+        common = dict(k_int=args.k_int, k_b=args.k_b, tol_primal=-1.0, tol_dual=-1.0, tol_binary=-1.0, stall_rel=-1.0)
+        prof = s.profile_blocks(20, **common)
+        act = s.profile_active()
+        out["tensor_core" if dk else "cuda_core"] = {"feas_ms_per_block": prof.get("feas"), "unpack_ms_per_block": prof.get("obj_tc"),
+                                                     "block_ms": sum(prof.values())}
+        s.close()
+    tc_ms = out["tensor_core"]["feas_ms_per_block"]
+    ld = (n + 127) // 128 * 128
+    ops = 2.0 * 128 * args.k_b * ld
+    byts = 128 * ld + args.k_b * ld
+    out["roofline_feas_tc"] = {"kernel": "k_obj_dense_tc<FEAS>+k_feas_dense_final (feas class per round)",
+                               "ops_per_launch": ops, "bytes_per_launch": byts, "ms": tc_ms,
+                               "tensor_frac": ops / (tc_ms * 1e-3) / 1e12 / i8_peak,
+                               "hbm_frac": byts / (tc_ms * 1e-3) / 1e9 / peak_hbm,
+                               "note": "k_b = 128 leaves the MMA N-starved and the split-K K-ranges short (5 K-blocks per CTA): "
+                                       "latency-bound; the win is against the per-(nonzero, lane) integer path"}
+    out["speedup_feas"] = out["cuda_core"]["feas_ms_per_block"] / tc_ms if tc_ms else None
+    return out
+
+
 def run_f2_facility(args, gf, stream, local):
     """Next row f2: TUReformulate (PAPER §2.4.1) on the paper's facility-location
     workload at (nf, nc) = (512, 2048) (config 7), three forms, same Alg. 1 run
@@ -749,6 +784,9 @@ def run_gpu(args):
     f1 = None
     if rank == 0 and world == 1 and not args.no_f1 and args.config != 6:
         f1 = run_f1_maxcut(args, gf, stream, local)
+    f1k = None
+    if rank == 0 and world == 1 and not args.no_f1:
+        f1k = run_f1_dense_k(args, gf, stream, local)
     f2 = None
     if rank == 0 and world == 1 and not args.no_f2:
         f2 = run_f2_facility(args, gf, stream, local)
@@ -799,7 +837,8 @@ def run_gpu(args):
             "cpu_baseline": cpu,
             "time_to_incumbent_small_configs": tti,
             "config5_with_cover_completion": cover,
-            "next_rows": {"f1_dense_q_maxcut": f1, "f2_tu_facility": f2, "f3_assign3d_custom_sampler": f3},
+            "next_rows": {"f1_dense_q_maxcut": f1, "f1_dense_k_mkp": f1k, "f2_tu_facility": f2,
+                          "f3_assign3d_custom_sampler": f3},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -297,11 +297,18 @@ __device__ __forceinline__ int warp_transpose_sum32(uint32_t (&v)[32], int lane)
     return x[0];
 }
 
-// z partial rows: zrows[blockIdx.x][l] = sum over this CTA's items of wgt * sum_i X_il (Q_I,J X_J)_il
+// OBJ (FEAS = false): z partial rows: zrows[blockIdx.x][l] = sum over this CTA's items of
+//   wgt * sum_i X_il (Q_I,J X_J)_il  (x_l'Q x_l, the upper block triangle of Q).
+// FEAS = true (dense integer rows of K, SURVEY §8(f) f1 "int8 MMA for MKP's K.X"): tmQ maps Kd
+//   (row tiles I of the dense rows, K = the variables) and every item is (I, a K-block range) of a
+//   split-K: the 128 x N int32 accumulator of the range is added to S[row][lane] (int32 atomics,
+//   exact: |sum| <= 127 n < 2^31) for the n real rows; k_feas_dense_final compares with the rhs.
+template <bool FEAS>
 __global__ void __launch_bounds__(TC_NT, 1)
     k_obj_dense_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmX,
                    const TcItem* __restrict__ items, const int* __restrict__ cta_off, int lanes, int nbox,
-                   const uint64_t* __restrict__ X, int W, long long n, long long* __restrict__ zrows) {
+                   const uint64_t* __restrict__ X, int W, long long n, long long* __restrict__ zrows,
+                   int* __restrict__ S) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     const int ST = tc_stages(nbox, lanes);
@@ -320,7 +327,8 @@ __global__ void __launch_bounds__(TC_NT, 1)
     const int it0 = cta_off[blockIdx.x], it1 = cta_off[blockIdx.x + 1];
     const int npass = (lanes + TC_NMAX - 1) / TC_NMAX;
 
-    for (int l = threadIdx.x; l < lanes; l += blockDim.x) zacc[l] = 0;
+    if constexpr (!FEAS)
+        for (int l = threadIdx.x; l < lanes; l += blockDim.x) zacc[l] = 0;
     if (threadIdx.x == 0) {
         for (int s = 0; s < ST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
         for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
@@ -406,6 +414,13 @@ __global__ void __launch_bounds__(TC_NT, 1)
                     uint32_t v[32];
                     tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * TC_NMAX + cc), v);
                     const int l0 = p * TC_NMAX + cc;  // global lane of column cc (multiple of 32)
+                    if constexpr (FEAS) {
+                        if (row < n)
+#pragma unroll
+                            for (int k = 0; k < 32; ++k)
+                                if (v[k]) atomicAdd(S + row * lanes + l0 + k, (int)v[k]);
+                        continue;
+                    }
                     uint32_t h = 0u;
                     if (row < n) h = (uint32_t)(__ldg(X + row * W + (l0 >> 6)) >> (l0 & 63));
 #pragma unroll
@@ -425,7 +440,23 @@ __global__ void __launch_bounds__(TC_NT, 1)
     __syncthreads();
     tc_fence_after();
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-    for (int l = threadIdx.x; l < lanes; l += blockDim.x) zrows[(long long)blockIdx.x * lanes + l] = zacc[l];
+    if constexpr (!FEAS)
+        for (int l = threadIdx.x; l < lanes; l += blockDim.x) zrows[(long long)blockIdx.x * lanes + l] = zacc[l];
+}
+
+// dense integer rows: lane l violates row j iff S[j][l] >= rhs_j fails (== for EQ rows); S is reset
+__global__ void __launch_bounds__(256) k_feas_dense_final(int* __restrict__ S, long long nrows, int lanes,
+                                                          const long long* __restrict__ rhs, const signed char* __restrict__ eq,
+                                                          unsigned long long* __restrict__ viol) {
+    const long long total = nrows * lanes;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += gridDim.x * (long long)blockDim.x) {
+        const long long j = t / lanes;
+        const int l = (int)(t - j * lanes);
+        const long long v = S[t];
+        S[t] = 0;
+        const bool ok = eq[j] ? v == rhs[j] : v >= rhs[j];
+        if (!ok) atomicOr(viol + (l >> 6), 1ull << (l & 63));
+    }
 }
 
 // ---------------------------------------------------------------------------------------------

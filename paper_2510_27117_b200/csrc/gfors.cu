@@ -476,7 +476,18 @@ struct gfors_ctx {
     double* d_qx = nullptr;        // [n] Q~ x of the primal input (prep-owned)
     double* d_qdx = nullptr;       // [n] Q~ (x_k - x_{k-1}) for the trigger residual
     double* d_qxpart = nullptr;    // [nchunk][qld] GEMV column-chunk partials
-    int8_t* d_Xs = nullptr;        // [64W][qld] unpacked samples (prep-owned)
+    int8_t* d_Xs = nullptr;        // [64W][xld] unpacked samples (prep-owned)
+    long long xld = 0;             // leading dimension of the unpacked samples (n rounded up to 128)
+    // dense integer rows of K (MKP's K.X on tensor cores): the general integer rows
+    // as int8 Kd[ceil128(n_int)][xld], split-K work items of the FEAS instance of k_obj_dense_tc
+    bool kdense = false;
+    int8_t* d_kd = nullptr;
+    CUtensorMap tmK{};
+    TcItem* d_kitems = nullptr;
+    int* d_koff = nullptr;
+    int k_tc_grid = 0;
+    int* d_kS = nullptr;           // [n_int][lanes] int32 row sums (kept zero between rounds)
+    long long kS_len = 0;
     long long Xs_lanes = 0;
     CUtensorMap tmX{};
 
@@ -615,6 +626,7 @@ struct gfors_ctx {
         long long force_capture_fail = 0;     // sharded: make the graph capture fail (eager fallback test)
         // load-time choices (applied by the next gfors_load; -1 = automatic)
         long long dense_q = -1;       // dense int8 Q storage (dense_q.cuh): 1 force, 0 off
+        long long dense_k = -1;       // dense int8 integer rows of K on tensor cores: 1 force, 0 off
         long long qx_fix = 1;         // fp32 iterates: exact fixed-point dp4a GEMV (0: fp64 FMA GEMV)
         long long qx_reuse = 1;       // fp32 loop: the trigger's product of x_k serves the next block's first primal
         long long push_dual = -1;     // sparse-xbar dual (push_dual.cuh): 1 force, 0 off
@@ -658,6 +670,7 @@ void gfors_ctx::free_problem() {
     d_qval = d_c = d_ru = nullptr;
     d_rsign = nullptr;
     d_qd = nullptr; d_tcitems = nullptr; d_tcoff = nullptr; qdense = false; tc_grid = 0;
+    kdense = false; d_kd = nullptr; d_kitems = nullptr; d_koff = nullptr; k_tc_grid = 0; xld = 0;
     for (auto& c : cnt) c = CountList{};
     for (auto& c : cntrb) c = CountRb{};
     d_int_row = nullptr; d_int_rhs = nullptr; d_int_eq = nullptr; d_int_seg_start = nullptr; d_int_seg_slot = nullptr;
@@ -676,12 +689,12 @@ void gfors_ctx::free_prep() {
                    (void**)&d_red, (void**)&d_scalar, (void**)&d_segpart, (void**)&d_segpart2, (void**)&d_u, (void**)&d_ones, (void**)&d_rec, (void**)&d_regen, (void**)&d_plist[0], (void**)&d_plist[1], (void**)&d_pcount, (void**)&d_pflags, (void**)&d_acc, (void**)&d_rlist, (void**)&d_rcount, (void**)&d_wmax, (void**)&d_accx, (void**)&d_xst, (void**)&d_accv, (void**)&d_ones_cnt, (void**)&d_trig_flag, (void**)&d_part1,
                    (void**)&d_part2, (void**)&d_hist, (void**)&d_rho, (void**)&d_trace, (void**)&d_xbest,
                    (void**)&d_X, (void**)&d_viol, (void**)&d_iacc, &d_zpart, (void**)&d_z, (void**)&d_ctrl,
-                   (void**)&d_qx, (void**)&d_qdx, (void**)&d_qxpart, (void**)&d_Xs,
+                   (void**)&d_qx, (void**)&d_qdx, (void**)&d_qxpart, (void**)&d_Xs, (void**)&d_kS,
                    (void**)&d_qxpart2, (void**)&d_qreuse, (void**)&d_cover_rows, (void**)&d_cover_best,
                    (void**)&d_cover_viol, (void**)&d_rp_rank, (void**)&d_rp_order, (void**)&d_rp_srow, (void**)&d_Tsamp,
                    (void**)&d_rs_rlo, &d_rs_y, (void**)&d_rs_u};
     for (void** p : ps) { dfree(*p); *p = nullptr; }
-    X_words = iacc_len = zpart_len = z_len = Xs_lanes = 0;
+    X_words = iacc_len = zpart_len = z_len = Xs_lanes = kS_len = 0;
     n_cover = -1;
     cover_viol_len = 0;
     rp_srow_len = 0;
@@ -1194,15 +1207,34 @@ ObjBitsShape obj_bits_shape(const gfors_ctx* C, int W) {
 
 // x_l' Q x_l of every lane of the batch by the tcgen05 int8 kernel (dense_q.cuh): unpack the bit-sliced
 // samples to int8 rows, then tc_grid partial rows of int64 lane sums at zrows
-void enqueue_obj_dense(gfors_ctx* C, cudaStream_t s, int W, long long* zrows) {
+// unpack the round's batch into sample-major int8 rows (the B operand of the tensor-core kernels) and
+// encode its tensor map; once per round when both dense paths run
+void enqueue_unpack(gfors_ctx* C, cudaStream_t s, int W) {
     const long long lanes = 64LL * W;
-    LAUNCH(C, s, KC_OBJ_TC, (k_unpack_samples<<<grid_for(C->qld / 16 * W * 8), NT, 0, s>>>(C->d_X, W, C->n, C->qld, C->d_Xs)));
+    LAUNCH(C, s, KC_OBJ_TC, (k_unpack_samples<<<grid_for(C->xld / 16 * W * 8), NT, 0, s>>>(C->d_X, W, C->n, C->xld, C->d_Xs)));
+    // the map of this batch width (host encode, ~1 us; captured by value into a graph node)
+    if (!C->dry) C->tmX = make_tmap_i8(C->d_Xs, C->xld, lanes, (int)std::min<long long>(TC_NMAX, lanes));
+}
+
+void enqueue_obj_dense(gfors_ctx* C, cudaStream_t s, int W, long long* zrows, bool unpacked) {
+    const long long lanes = 64LL * W;
+    if (!unpacked) enqueue_unpack(C, s, W);
     const int nbox = (int)std::min<long long>(TC_NMAX, lanes);
     const size_t sm = tc_smem_bytes(nbox, (int)lanes);
-    // the map of this batch width (host encode, ~1 us; captured by value into a graph node)
-    if (!C->dry) C->tmX = make_tmap_i8(C->d_Xs, C->qld, lanes, nbox);
-    LAUNCH(C, s, KC_OBJ_TC, (k_obj_dense_tc<<<C->tc_grid, TC_NT, sm, s>>>(C->tmQ, C->tmX, C->d_tcitems, C->d_tcoff, (int)lanes,
-                                                                         nbox, C->d_X, W, C->n, zrows)));
+    LAUNCH(C, s, KC_OBJ_TC, (k_obj_dense_tc<false><<<C->tc_grid, TC_NT, sm, s>>>(C->tmQ, C->tmX, C->d_tcitems, C->d_tcoff,
+                                                                                (int)lanes, nbox, C->d_X, W, C->n, zrows, nullptr)));
+}
+
+// K.X for the dense integer rows on tensor cores (split-K), then the row test
+void enqueue_feas_dense(gfors_ctx* C, cudaStream_t s, int W) {
+    const long long lanes = 64LL * W;
+    enqueue_unpack(C, s, W);
+    const int nbox = (int)std::min<long long>(TC_NMAX, lanes);
+    const size_t sm = tc_smem_bytes(nbox, (int)lanes);
+    LAUNCH(C, s, KC_FEAS, (k_obj_dense_tc<true><<<C->k_tc_grid, TC_NT, sm, s>>>(C->tmK, C->tmX, C->d_kitems, C->d_koff,
+                                                                               (int)lanes, nbox, C->d_X, W, C->n_int, nullptr, C->d_kS)));
+    LAUNCH(C, s, KC_FEAS, (k_feas_dense_final<<<grid_for(C->n_int * lanes), NT, 0, s>>>(C->d_kS, C->n_int, (int)lanes, C->d_int_rhs,
+                                                                                        C->d_int_eq, C->d_viol)));
 }
 
 // evaluation of the batch in d_X (W words per variable); viol/iacc must have been reset
@@ -1245,7 +1277,11 @@ void enqueue_eval(gfors_ctx* C, cudaStream_t s, int W, const unsigned char* ones
         }
 #undef FEAS_WV
     }
-    if (C->n_int) {
+    bool unpacked = false;
+    if (C->n_int && C->kdense) {
+        enqueue_feas_dense(C, s, W);
+        unpacked = true;
+    } else if (C->n_int) {
         IntRows ir{C->d_int_row, C->d_int_rhs, C->d_int_eq, C->d_int_seg_start, C->d_int_seg_slot, C->n_int, C->n_int_seg};
         const int grid = grid_for(C->n_int_seg * 2LL * W * 32);
         KIND_SWITCH(C->kkind, LAUNCH(C, s, KC_FEAS, (k_feas_int_partial<KINDV><<<grid, NT, 0, s>>>(K, ir, C->d_X, W, C->d_iacc))));
@@ -1272,7 +1308,7 @@ void enqueue_eval(gfors_ctx* C, cudaStream_t s, int W, const unsigned char* ones
                                                                   C->d_X, W, (long long*)C->d_zpart)));
         long long rows = jpw;
         if (C->qdense) {
-            enqueue_obj_dense(C, s, W, (long long*)C->d_zpart + jpw * 64LL * W);
+            enqueue_obj_dense(C, s, W, (long long*)C->d_zpart + jpw * 64LL * W, unpacked);
             rows += C->tc_grid;
         } else if (C->hasq) {
             long long* zq = (long long*)C->d_zpart + jpw * 64LL * W;
@@ -1283,7 +1319,7 @@ void enqueue_eval(gfors_ctx* C, cudaStream_t s, int W, const unsigned char* ones
     } else if (C->integral) {
         if (C->qdense) {
             LAUNCH(C, s, KC_OBJ, (k_obj_partial<true, false><<<grid, NT, 0, s>>>(C->n, C->obj_chunk, C->d_c, Q, C->d_qval, C->d_X, W, C->d_zpart)));
-            enqueue_obj_dense(C, s, W, (long long*)C->d_zpart + nchunk * 64LL * W);
+            enqueue_obj_dense(C, s, W, (long long*)C->d_zpart + nchunk * 64LL * W, unpacked);
             LAUNCH(C, s, KC_OBJ, (k_obj_final<true><<<2 * W, 1024, 0, s>>>(nchunk + C->tc_grid, W, C->d_zpart, C->c0, C->d_z)));
             return;
         }
@@ -1330,11 +1366,18 @@ void ensure_batch(gfors_ctx* C, int W) {
     } else if (C->qdense) {
         zrows = nchunk + C->tc_grid;
     }
-    if (C->qdense && 64LL * W > C->Xs_lanes) {  // grow-only: smaller batches (final round) reuse it
-        if (64LL * W > 4096) input_error("params.k_b: the dense-Q objective supports k_b <= 4096 per rank");
+    if ((C->qdense || C->kdense) && 64LL * W > C->Xs_lanes) {  // grow-only: smaller batches (final round) reuse it
+        if (64LL * W > 4096) input_error("params.k_b: the dense tensor-core evaluation supports k_b <= 4096 per rank");
         dfree(C->d_Xs);
-        C->d_Xs = dalloc<int8_t>(64LL * W * C->qld);
+        C->d_Xs = dalloc<int8_t>(64LL * W * C->xld);
         C->Xs_lanes = 64LL * W;
+        C->gvalid = false;
+    }
+    if (C->kdense && C->n_int * 64LL * W > C->kS_len) {
+        dfree(C->d_kS);
+        C->d_kS = dalloc<int>(C->n_int * 64LL * W);
+        CK(cudaMemsetAsync(C->d_kS, 0, C->n_int * 64LL * W * sizeof(int), C->stream));
+        C->kS_len = C->n_int * 64LL * W;
         C->gvalid = false;
     }
     const long long zp = zrows * 64LL * W;
@@ -2092,6 +2135,7 @@ gfors_status gfors_set_option(gfors_ctx* C, const char* key, int64_t value) {
     else if (k == "force_deadline_block") C->opt.force_deadline_block = value;
     else if (k == "force_capture_fail") C->opt.force_capture_fail = value;
     else if (k == "dense_q") C->opt.dense_q = value;
+    else if (k == "dense_k") C->opt.dense_k = value;
     else if (k == "qx_fix") C->opt.qx_fix = value;
     else if (k == "qx_reuse") C->opt.qx_reuse = value;
     else if (k == "push_dual") C->opt.push_dual = value;
