@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <chrono>
 #include <climits>
+#include <map>
 #include <mutex>
 #include <thread>
 #include <cub/cub.cuh>
@@ -76,6 +77,10 @@ struct Err {
 // config-5 load varies 42-300 ms with plain cudaMalloc/cudaFree).  Allocation and free run on a
 // private non-blocking stream and are made synchronous (allocate + sync; device sync + free), so
 // the semantics are those of cudaMalloc/cudaFree for every caller stream.
+static cudaMemPool_t& pool_of(int dev) {
+    static cudaMemPool_t pools[64] = {};
+    return pools[dev];
+}
 static cudaStream_t alloc_stream() {
     static std::mutex mu;
     static cudaStream_t st[64] = {};
@@ -84,13 +89,33 @@ static cudaStream_t alloc_stream() {
     std::lock_guard<std::mutex> g(mu);
     if (dev < 0 || dev >= 64) return nullptr;
     if (!st[dev]) {
-        cudaMemPool_t pool;
-        CK(cudaDeviceGetDefaultMemPool(&pool, dev));
+        // a PRIVATE pool (the device's default pool, which other libraries share, is left untouched)
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        CK(cudaMemPoolCreate(&pool_of(dev), &props));
         unsigned long long thr = ~0ull;
-        CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        CK(cudaMemPoolSetAttribute(pool_of(dev), cudaMemPoolAttrReleaseThreshold, &thr));
         CK(cudaStreamCreateWithFlags(&st[dev], cudaStreamNonBlocking));
     }
     return st[dev];
+}
+
+// contexts alive per device (create +1, destroy -1); returns the new count
+static int live_contexts(int dev, int delta) {
+    static std::mutex mu;
+    static int live[64] = {};
+    if (dev < 0 || dev >= 64) return 1;
+    std::lock_guard<std::mutex> g(mu);
+    live[dev] = std::max(0, live[dev] + delta);
+    return live[dev];
+}
+
+// after the last context of a device is destroyed its pool returns the memory to the system
+static void pool_trim(int dev) {
+    if (dev >= 0 && dev < 64 && pool_of(dev)) cudaMemPoolTrimTo(pool_of(dev), 0);
 }
 
 template <typename X>
@@ -99,7 +124,9 @@ X* dalloc(size_t count) {
     void* p = nullptr;
     cudaStream_t as = alloc_stream();
     if (as) {
-        CK(cudaMallocAsync(&p, count * sizeof(X), as));
+        int dev = 0;
+        CK(cudaGetDevice(&dev));
+        CK(cudaMallocFromPoolAsync(&p, count * sizeof(X), pool_of(dev), as));
         CK(cudaStreamSynchronize(as));
     } else {
         CK(cudaMalloc(&p, count * sizeof(X)));
@@ -300,10 +327,23 @@ enum KClass { KC_DUAL = 0, KC_PRIMAL, KC_TRIGR, KC_TRIGC, KC_SAMPLE, KC_FEAS, KC
 // opt a kernel into the largest dynamic shared memory it can have next to its static shared memory
 constexpr size_t SMEM_PER_BLOCK_MAX = 227 * 1024;
 constexpr size_t SP_DYN_MAX = SMEM_PER_BLOCK_MAX - 8 * 1024;  // k_primal_sparse: static part < 8 KB
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device: remember, per (kernel, device), the
+// largest size set so far (thread-safe); a second solver on another GPU sets its own
+static void smem_attr(const void* fn, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> done;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> g(mu);
+    size_t& cur = done[{fn, dev}];
+    if (bytes <= cur) return;
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    cur = bytes;
+}
 static void set_max_dyn_smem(const void* fn) {
     cudaFuncAttributes a;
     CK(cudaFuncGetAttributes(&a, fn));
-    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(SMEM_PER_BLOCK_MAX - a.sharedSizeBytes)));
+    smem_attr(fn, SMEM_PER_BLOCK_MAX - a.sharedSizeBytes);
 }
 
 // 2-D TMA map of a row-major int8 matrix [rows][ld] with (128-byte x box_rows) boxes and the 128-byte
@@ -401,6 +441,7 @@ __global__ void k_loop_start(Ctrl* ctrl, double time_limit_s) {
 struct gfors_ctx {
     int device = 0;
     int num_sms = NUM_SMS_B200;  // queried at create
+    bool counted = false;        // counted in live_contexts (the device pool is trimmed after the last)
     cudaStream_t stream = nullptr, cap_stream = nullptr;
     bool own_stream = false;
     int rank = 0, world = 1;
@@ -654,14 +695,17 @@ struct gfors_ctx {
     void free_prep();
 };
 
+// Every API call leaves the context's stream idle (the calls are synchronous), and the free-batches
+// (free_prep / free_problem) synchronise that stream first, so no kernel of this context still uses p;
+// the free is ordered on the allocation stream before any later allocation from the pool.
 static void dfree(void* p) {
     if (!p) return;
     cudaStream_t as = alloc_stream();
-    cudaDeviceSynchronize();  // what cudaFree implies: no caller stream still uses p
     if (as) cudaFreeAsync(p, as); else cudaFree(p);
 }
 
 void gfors_ctx::free_problem() {
+    if (stream) cudaStreamSynchronize(stream);
     for (void* p : owned) dfree(p);
     owned.clear();
     d_kptr = d_ktptr = d_qptr = nullptr;
@@ -684,6 +728,7 @@ void gfors_ctx::free_problem() {
 }
 
 void gfors_ctx::free_prep() {
+    if (stream) cudaStreamSynchronize(stream);
     void** ps[] = {(void**)&d_s, &d_g, &d_rh, &d_cs, &d_qs, &d_x[0], &d_x[1], &d_xb[0], &d_xb[1], &d_y[0], &d_y[1],
                    &d_w, (void**)&d_tmp[0], (void**)&d_tmp[1], (void**)&d_tmp[2], (void**)&d_tmp[3],
                    (void**)&d_red, (void**)&d_scalar, (void**)&d_segpart, (void**)&d_segpart2, (void**)&d_u, (void**)&d_ones, (void**)&d_rec, (void**)&d_regen, (void**)&d_plist[0], (void**)&d_plist[1], (void**)&d_pcount, (void**)&d_pflags, (void**)&d_acc, (void**)&d_rlist, (void**)&d_rcount, (void**)&d_wmax, (void**)&d_accx, (void**)&d_xst, (void**)&d_accv, (void**)&d_ones_cnt, (void**)&d_trig_flag, (void**)&d_part1,
@@ -717,6 +762,13 @@ gfors_ctx::~gfors_ctx() {
     if (stream) cudaStreamSynchronize(stream);
     free_prep();
     free_problem();
+    // the pool keeps freed memory while other contexts of the device live (fast reloads); the last
+    // one returns it to the system
+    if (counted && live_contexts(device, -1) == 0) {
+        cudaStream_t as = alloc_stream();
+        if (as) cudaStreamSynchronize(as);
+        pool_trim(device);
+    }
     if (comm) nccl().CommDestroy(comm);
     if (cap_stream) cudaStreamDestroy(cap_stream);
     if (cap_stream2) cudaStreamDestroy(cap_stream2);
@@ -864,13 +916,9 @@ void enqueue_qx(gfors_ctx* C, cudaStream_t s, QxSrc<TX> src, bool diff, double o
             }
 #define QXF_LAUNCH(STV, MBV)                                                                                          \
     {                                                                                                                 \
-        static bool attr_f[2] = {false, false};                                                                      \
         const size_t smb = qt_smem_bytes(STV);                                                                        \
-        if (!attr_f[diff ? 1 : 0]) {                                                                                  \
-            if (diff) CK(cudaFuncSetAttribute(k_qx_tma_fix<true, STV, MBV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb)); \
-            else CK(cudaFuncSetAttribute(k_qx_tma_fix<false, STV, MBV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb)); \
-            attr_f[diff ? 1 : 0] = true;                                                                              \
-        }                                                                                                             \
+        if (diff) smem_attr((const void*)k_qx_tma_fix<true, STV, MBV>, smb);                                         \
+        else smem_attr((const void*)k_qx_tma_fix<false, STV, MBV>, smb);                                             \
         if (diff)                                                                                                     \
             LAUNCH(C, s, KC_QX, (k_qx_tma_fix<true, STV, MBV><<<grid, QT_NT, smb, s>>>(C->tmQ64, n, C->qld, src, dst, reuse))); \
         else                                                                                                          \
@@ -892,13 +940,8 @@ void enqueue_qx(gfors_ctx* C, cudaStream_t s, QxSrc<TX> src, bool diff, double o
     {
         const long long units = (n + QT_ROWS - 1) / QT_ROWS * nchunk;
         const int grid = (int)std::min<long long>(units, NUM_SMS_B200 * 2LL);
-        static bool attr[4] = {false, false, false, false};
-        const int ai = (sizeof(TX) == 8 ? 2 : 0) + (diff ? 1 : 0);
-        if (!attr[ai]) {
-            if (diff) CK(cudaFuncSetAttribute(k_qx_tma<TX, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qt_smem_bytes()));
-            else CK(cudaFuncSetAttribute(k_qx_tma<TX, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qt_smem_bytes()));
-            attr[ai] = true;
-        }
+        if (diff) smem_attr((const void*)k_qx_tma<TX, true>, qt_smem_bytes());
+        else smem_attr((const void*)k_qx_tma<TX, false>, qt_smem_bytes());
         if (diff)
             LAUNCH(C, s, KC_QX, (k_qx_tma<TX, true><<<grid, QT_NT, qt_smem_bytes(), s>>>(C->tmQ64, n, C->qld, src, C->d_qxpart)));
         else
@@ -1063,15 +1106,13 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
             const int grid = (int)std::min<long long>(C->sp_nblk, NUM_SMS_B200);
             if (C->hasq) {
                 KIND_SWITCH(tkind, {
-                    static bool attr = false;
-                    if (!attr) { set_max_dyn_smem((const void*)k_primal_sparse<T, KINDV, true>); attr = true; }
+                    set_max_dyn_smem((const void*)k_primal_sparse<T, KINDV, true>);
                     LAUNCH(C, q, KC_PRIMAL, (k_primal_sparse<T, KINDV, true><<<grid, SP_NT, sm, q>>>(csr_Kt(C), C->sp_blk_row, C->sp_nblk,
                         C->d_nzbits, nwords, Q, qs, st, cs, ctrl, kint, j, pl)));
                 });
             } else {
                 KIND_SWITCH(tkind, {
-                    static bool attr = false;
-                    if (!attr) { set_max_dyn_smem((const void*)k_primal_sparse<T, KINDV, false>); attr = true; }
+                    set_max_dyn_smem((const void*)k_primal_sparse<T, KINDV, false>);
                     LAUNCH(C, q, KC_PRIMAL, (k_primal_sparse<T, KINDV, false><<<grid, SP_NT, sm, q>>>(csr_Kt(C), C->sp_blk_row, C->sp_nblk,
                         C->d_nzbits, nwords, Q, qs, st, cs, ctrl, kint, j, pl)));
                 });
@@ -1463,7 +1504,7 @@ void enqueue_repair(gfors_ctx* C, cudaStream_t s, int W) {
         C->gvalid = false;
     }
     KIND_SWITCH(C->kkind, {
-        CK(cudaFuncSetAttribute(k_repair<KINDV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rp_smem_bytes(RP_SROWS)));
+        smem_attr((const void*)k_repair<KINDV>, rp_smem_bytes(RP_SROWS));
         LAUNCH(C, s, KC_SAMPLE, (k_repair<KINDV><<<64 * W, RP_NT, sm, s>>>(C->n, C->m, csr_Kt(C), C->d_rp_rank, C->d_rp_order,
                                                                          C->d_ru, C->d_X, W, C->d_rp_srow)));
     });
@@ -1517,22 +1558,14 @@ void enqueue_sample_a3(gfors_ctx* C, cudaStream_t s, const double* pfix, int W, 
     }
     // (the CUB radix-sort kernels are library launches: not counted in gfors_run_info.launches)
     const size_t gsm = a3_greedy_smem((int)A.n);
-    static size_t gattr = 0;
-    if (gsm > 48 * 1024 && gsm > gattr) {
-        CK(cudaFuncSetAttribute(k_a3_greedy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm));
-        gattr = gsm;
-    }
+    if (gsm > 48 * 1024) smem_attr((const void*)k_a3_greedy, gsm);
     LAUNCH(C, s, KC_SAMPLE, (k_a3_greedy<<<1, A3_GNT, gsm, s>>>(A.vals[1], A.K, (int)A.n, A.sj0, A.sk0, A.Ri, A.Rj, A.Rk,
                                                                   A.meta)));
     const int lanes = 64 * W;
     const size_t per = a3_warp_smem(A.n, A.L);
     const int wpb = (int)std::max<size_t>(1, std::min<size_t>(8, (200 * 1024) / per));
     const size_t sm = per * wpb;
-    static size_t attr_sm = 0;
-    if (sm > 48 * 1024 && sm > attr_sm) {
-        CK(cudaFuncSetAttribute(k_a3_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        attr_sm = sm;
-    }
+    if (sm > 48 * 1024) smem_attr((const void*)k_a3_sample, sm);
     LAUNCH(C, s, KC_SAMPLE, (k_a3_sample<<<(lanes + wpb - 1) / wpb, 32 * wpb, sm, s>>>((int)A.n, A.sj0, A.sk0, A.Ri, A.Rj,
         A.Rk, A.meta, C->d_c, key, C->d_ctrl, r, kr, round_fixed, use_fixed, word_off, W, A.L, C->d_X)));
 }
@@ -2103,6 +2136,8 @@ gfors_status gfors_create(gfors_ctx** out, const gfors_device_opts* opts) {
         if (C->device < 0 || C->device >= ndev) input_error("device_opts.device: %d not in [0,%d)", C->device, ndev);
         CK(cudaSetDevice(C->device));
         CK(cudaDeviceGetAttribute(&C->num_sms, cudaDevAttrMultiProcessorCount, C->device));
+        live_contexts(C->device, +1);
+        C->counted = true;
         if (opts && opts->nccl_id) {
             NcclApi& api = nccl();
             if (!api.ok) throw Err{GFORS_E_NCCL, api.why};
