@@ -92,52 +92,41 @@ __global__ void __launch_bounds__(256) k_sample_thr(const T* __restrict__ xa, co
 }
 
 // RandSampleStep pass 2 (Alg. 3, contract R10): the MSB-first compare decides a 64-lane word after a
-// data-dependent number of plane pairs (E ~ 3.7 Philox calls, up to 16), so a thread that owned one
-// word would idle until the slowest lane of its warp finished.  Instead every thread walks its own
-// variables (i = tid, tid + stride, ...), their W words one after another, and runs ONE plane pair
-// per loop trip: when a word is decided it is stored and the next one starts, so all lanes do useful
-// Philox work until the tail.  T of the next variable is prefetched; T = 0 variables were written by
-// pass 1.  Identical output to bernoulli_word.
+// data-dependent number of plane pairs (E ~ 3.7 Philox calls, up to 16).  Every thread walks its own
+// variables (i = tid, tid + stride, ...) and their W words one after another; lanes of a warp run
+// independently (a lane whose word is decided goes on to its next word while the others finish
+// theirs: independent thread scheduling, no warp-wide vote), two plane pairs per loop trip.  T of the
+// next variable is prefetched; T = 0 variables were written by pass 1.  32-bit indices (n < 2^31)
+// keep the loop state small.  Identical output to bernoulli_word.
 __global__ void __launch_bounds__(256) k_sample(const uint32_t* __restrict__ Tarr, long long n, int W, long long word_off,
                                                 const __grid_constant__ PhiloxKeys rk, const Ctrl* __restrict__ ctrl,
                                                 int r, int kr, unsigned round_fixed, int use_fixed, uint64_t* __restrict__ X) {
     const unsigned round = use_fixed ? round_fixed : (unsigned)(ctrl->blk * kr + r);
-    const long long stride = gridDim.x * (long long)blockDim.x;
+    const unsigned nn = (unsigned)n;  // n < 2^31 (load requirement): 32-bit indices throughout
+    const unsigned stride = gridDim.x * blockDim.x;
     const uint64_t pol = l2_policy_evict_last();  // the batch is gathered by the evaluator next
-    long long ni = blockIdx.x * (long long)blockDim.x + threadIdx.x;  // next variable
-    uint32_t nT = ni < n ? __ldg(Tarr + ni) : 0u;
-    long long ci = -1;  // current variable
-    int cw = 0;         // its current word
-    uint32_t Tv = 0, Tsh = 0, q = 0;
-    uint32_t ul = 0, uh = 0, rl = 0, rh = 0;
-    bool active = false;
+    const unsigned wbase = (unsigned)word_off;
+    unsigned i = blockIdx.x * blockDim.x + threadIdx.x;  // current variable
+    uint32_t Tv = i < nn ? __ldg(Tarr + i) : 0u;
+    unsigned ni = i + stride;                            // next variable, its threshold prefetched
+    uint32_t nT = ni < nn ? __ldg(Tarr + ni) : 0u;
+    int w = 0;
     while (true) {
-        if (!active) {
-            if (ci >= 0 && ++cw < W) {  // next word of the same variable
-                active = true;
-            } else {
-                while (ni < n && nT == 0u) {  // pass-1 variables: nothing to draw
-                    ni += stride;
-                    nT = ni < n ? __ldg(Tarr + ni) : 0u;
-                }
-                if (ni < n) {
-                    ci = ni; cw = 0; Tv = nT; active = true;
-                    ni += stride;
-                    nT = ni < n ? __ldg(Tarr + ni) : 0u;
-                } else {
-                    ci = -1;
-                }
-            }
-            if (active) { Tsh = Tv; q = 0; ul = uh = ~0u; rl = rh = 0u; }
+        // next word to draw: skip variables with T = 0 (written by pass 1)
+        while (i < nn && Tv == 0u) {
+            i = ni; Tv = nT; w = 0;
+            ni = i + stride;
+            nT = ni < nn ? __ldg(Tarr + ni) : 0u;
         }
-        if (!__any_sync(0xffffffffu, active)) break;
-        if (active) {
-            // two plane pairs per loop trip (halves the loop/fetch overhead; a word decided by the first
-            // pair wastes the second, ~0.5 call per word).  Plane with T-bit t: t = 1 -> lanes with
-            // u-bit 0 decide 1 (res |= und & ~pl), und &= pl; t = 0 -> lanes with u-bit 1 decide 0,
-            // und &= ~pl.   m = t ? ~0 : 0.  Planes after the word is decided change nothing (und = 0).
-            const uint4 o = philox_rkw(make_uint4((uint32_t)ci, (uint32_t)(word_off + cw), q, round), rk);
-            const uint4 o2 = philox_rkw(make_uint4((uint32_t)ci, (uint32_t)(word_off + cw), q + 1, round), rk);
+        if (i >= nn) break;
+        // one 64-lane word: two plane pairs per trip until every lane is decided (MSB-first compare);
+        // plane with T-bit t: t = 1 -> lanes with u-bit 0 decide 1, und &= pl; t = 0 -> lanes with u-bit 1
+        // decide 0, und &= ~pl (m = t ? ~0 : 0).  Planes after the word is decided change nothing.
+        uint32_t ul = ~0u, uh = ~0u, rl = 0u, rh = 0u, Tsh = Tv;
+        const unsigned wg = wbase + (unsigned)w;
+        for (unsigned q = 0; q < 16; q += 2) {
+            const uint4 o = philox_rkw(make_uint4(i, wg, q, round), rk);
+            const uint4 o2 = philox_rkw(make_uint4(i, wg, q + 1, round), rk);
             uint32_t m = 0u - (Tsh >> 31);
             rl |= ul & ~o.x & m; rh |= uh & ~o.y & m;
             ul &= ~(o.x ^ m);    uh &= ~(o.y ^ m);
@@ -151,12 +140,10 @@ __global__ void __launch_bounds__(256) k_sample(const uint32_t* __restrict__ Tar
             rl |= ul & ~o2.z & m; rh |= uh & ~o2.w & m;
             ul &= ~(o2.z ^ m);    uh &= ~(o2.w ^ m);
             Tsh <<= 4;
-            q += 2;
-            if ((ul | uh) == 0u || q == 16) {  // decided (u == T lanes stay 0)
-                st_hint_u64(X + ci * W + cw, (uint64_t)rl | ((uint64_t)rh << 32), pol);
-                active = false;
-            }
+            if ((ul | uh) == 0u) break;  // (u == T lanes stay 0)
         }
+        st_hint_u64(X + (size_t)i * W + w, (uint64_t)rl | ((uint64_t)rh << 32), pol);
+        if (++w == W) { i = ni; Tv = nT; w = 0; ni = i + stride; nT = ni < nn ? __ldg(Tarr + ni) : 0u; }
     }
 }
 
