@@ -389,7 +389,7 @@ def run_f1_maxcut(args, gf, stream, local):
         "ms_per_step": ms / K, "pdhg_iters_per_s": K * args.k_int / (ms * 1e-3),
         "z_best": z if inc["has_incumbent"] else None, "obj_scale": sc["obj_scale"],
         "gen_s": t_gen, "load_preprocess_s": t_load, "kernel_ms_per_step": prof,
-        "roofline_gemv": {"bound": "hbm", "kernel": "k_qx_dense+k_qx_final", "achieved": gemv_bytes / (gemv_ms * 1e-3) / 1e9,
+        "roofline_gemv": {"bound": "hbm", "kernel": "k_qx_tma_fix+k_qx_final" if args.precision == 32 else "k_qx_tma+k_qx_final", "achieved": gemv_bytes / (gemv_ms * 1e-3) / 1e9,
                           "peak": peak_hbm, "unit": "GB/s", "frac": gemv_bytes / (gemv_ms * 1e-3) / 1e9 / peak_hbm,
                           "algorithmic_bytes_per_launch": gemv_bytes, "avg_launch_ms": gemv_ms, "peak_source": peak_src},
         "roofline_obj_tc": {"bound": "hbm" if tc_bytes / (peak_hbm * 1e9) > tc_ops / (i8_peak * 1e12) else "tensor",
