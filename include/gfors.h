@@ -220,6 +220,11 @@ gfors_status gfors_sample(gfors_ctx *ctx, const double *p, uint64_t seed, uint32
 /* EvalBest pieces on a host batch bits[n][n_words]: feasible[64*n_words] (0/1) and z (canonical
  * minimisation objective, original units). */
 gfors_status gfors_eval(gfors_ctx *ctx, const uint64_t *bits, int64_t n_words, uint8_t *feasible, double *z);
+/* Sampling-only throughput (bench): `rounds` rounds of RandSampleStep of p (host fp64,
+ * uploaded once) for k_b = 64*n_words candidates (round ids 0..rounds-1) + EvalBest + argmin, on the
+ * device, no PDHG and no incumbent update; *ms_out = CUDA-event time of the rounds. */
+gfors_status gfors_sample_eval_timed(gfors_ctx *ctx, const double *p, uint64_t seed, int64_t n_words, int32_t rounds,
+                                     double *ms_out);
 /* Set/get the PDHG iterate (host fp64; y in canonical row order). */
 gfors_status gfors_set_state(gfors_ctx *ctx, const double *x, const double *xbar, const double *y);
 gfors_status gfors_get_state(gfors_ctx *ctx, double *x, double *xbar, double *y);

@@ -109,6 +109,7 @@ EXPORTS = {
     "gfors_nccl_unique_id": (I32, [P]),
     "gfors_graph_note": (C.c_char_p, [P]),
     "gfors_set_option": (I32, [P, C.c_char_p, I64]),
+    "gfors_sample_eval_timed": (I32, [P, P, U64, I64, I32, P]),
 }
 for _name, (_res, _args) in EXPORTS.items():
     _f = getattr(_lib, _name)
@@ -354,6 +355,13 @@ class Solver:
         self._chk(_lib.gfors_profile_active(self.h, _ptr(ams), _ptr(an), 16))
         return {_lib.gfors_kernel_class_name(k).decode(): (float(ams[k]), int(an[k])) for k in range(16)
                 if _lib.gfors_kernel_class_name(k).decode()}
+
+    def sample_eval_timed(self, p, seed, n_words, rounds):
+        """gfors_sample_eval_timed: device ms of `rounds` sampling + evaluation rounds at fixed p."""
+        p = np.ascontiguousarray(p, dtype=np.float64)
+        ms = D()
+        self._chk(_lib.gfors_sample_eval_timed(self.h, _ptr(p), int(seed), int(n_words), int(rounds), C.byref(ms)))
+        return ms.value
 
     def set_option(self, key: str, value: int):
         """gfors_set_option (test/benchmark options, include/gfors.h)."""

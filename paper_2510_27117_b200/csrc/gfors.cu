@@ -2380,6 +2380,41 @@ gfors_status gfors_eval(gfors_ctx* C, const uint64_t* bits, int64_t n_words, uin
     API_END(C)
 }
 
+gfors_status gfors_sample_eval_timed(gfors_ctx* C, const double* p, uint64_t seed, int64_t n_words, int32_t rounds,
+                                     double* ms_out) {
+    API_BEGIN(C)
+    if (C->stage < 2) throw Err{GFORS_E_STATE, "gfors_sample_eval_timed: call gfors_preprocess first"};
+    if (!p || !ms_out || rounds < 1) input_error("gfors_sample_eval_timed: p, ms_out and rounds >= 1 required");
+    if (n_words < 1 || n_words > (1 << 14)) input_error("gfors_sample_eval_timed: n_words out of range");
+    for (long long i = 0; i < C->n; ++i)
+        if (!(p[i] >= 0.0 && p[i] <= 1.0)) input_error("gfors_sample_eval_timed: p[%lld] not in [0,1]", i);
+    const int W = (int)n_words;
+    ensure_batch(C, W);
+    set_sampler(C, 0, 0, 0.0, 0);
+    cudaStream_t s = C->stream;
+    double* dp = C->d_tmp[3];
+    CK(cudaMemcpyAsync(dp, p, C->n * sizeof(double), cudaMemcpyHostToDevice, s));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, s));
+    for (int r = 0; r < rounds; ++r) {  // RandSampleStep + EvalBest + argmin (hook mode: no incumbent update)
+        if (C->precision == 64) enqueue_sample<double>(C, s, dp, W, 0, seed, 1, 0, 1, (unsigned)r, 1);
+        else enqueue_sample<float>(C, s, dp, W, 0, seed, 1, 0, 1, (unsigned)r, 1);
+        enqueue_reset(C, s, W, ~0ull);
+        enqueue_eval(C, s, W);
+        LAUNCH(C, s, KC_ARGMIN, (k_argmin<<<1, NT, 0, s>>>(C->d_z, C->d_viol, 64LL * W, 0, C->d_ctrl, 0, 0, 1, 2)));
+    }
+    CK(cudaEventRecord(e1, s));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *ms_out = ms;
+    API_END(C)
+}
+
 gfors_status gfors_set_state(gfors_ctx* C, const double* x, const double* xbar, const double* y) {
     API_BEGIN(C)
     if (C->stage < 2) throw Err{GFORS_E_STATE, "gfors_set_state: call gfors_preprocess first"};

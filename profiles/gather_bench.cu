@@ -55,6 +55,18 @@ __global__ void __launch_bounds__(256) k_stream(const int* __restrict__ idx, lon
     out[blockIdx.x * (long long)blockDim.x + threadIdx.x] = (float)acc;
 }
 
+// L2-resident streaming read (the bound of the small configs 2-4, whose per-iteration working sets
+// fit in L2): every thread sums float4 loads over a buffer of B bytes, REPS passes
+__global__ void __launch_bounds__(256) k_l2read(const float4* __restrict__ a, long long n4, int reps, float* __restrict__ out) {
+    float acc = 0.f;
+    for (int r = 0; r < reps; ++r)
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+            const float4 v = __ldcg(a + i);
+            acc += v.x + v.y + v.z + v.w;
+        }
+    out[blockIdx.x * (long long)blockDim.x + threadIdx.x] = acc;
+}
+
 template <int EB>
 __device__ __forceinline__ void cpa(void* s, const void* g) {
     const unsigned a = (unsigned)__cvta_generic_to_shared(s);
@@ -149,6 +161,13 @@ int main(int argc, char** argv) {
             if (eb == 8) { REG(8, 1); REG(8, 4); CPA(8, 1024); }
             if (eb == 16) { REG(16, 1); REG(16, 4); CPA(16, 512); CPA(16, 1024); }
         }
+    }
+    // L2-resident streaming read bandwidth (buffers well inside the 126 MB L2)
+    for (long long mb : {8LL, 16LL, 32LL, 48LL}) {
+        const long long n4 = (mb << 20) / 16;
+        const int reps = 20;
+        const double ms = time_ms([&] { k_l2read<<<grid, 256>>>((const float4*)d_v, n4, reps, d_out); });
+        printf("  L2 read %lld MB x %d: %.1f us = %.2f TB/s\n", mb, reps, ms * 1e3, (double)reps * (mb << 20) / (ms * 1e-3) / 1e12);
     }
     // the index stream alone (no gathers)
     {
