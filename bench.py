@@ -668,13 +668,14 @@ def run_gpu(args):
             x_now = None
         if x_now is not None:
             pv["traj"] = np.clip(x_now, 0.0, 1.0)
-        sampling_only = {"how": "10 rounds of sample + evaluate + argmin at fixed p, CUDA events (gfors_sample_eval_timed)",
+        sampling_only = {"how": "10 rounds of sample + evaluate + argmin at fixed p after one warm-up round, CUDA events (gfors_sample_eval_timed)",
                          "traj": f"x_k after {args.steps} blocks from x0"}
         for name in ("traj", "unif", "mix"):
             if name not in pv:
                 continue
             row = {}
             for kb in (64, 128, 1024, 4096):
+                s.sample_eval_timed(pv[name], 20251030, kb // 64, 1)  # warm-up: first launches load the kernels
                 ms_r = s.sample_eval_timed(pv[name], 20251030, kb // 64, 10)
                 row[str(kb)] = 10 * kb / (ms_r * 1e-3)
             sampling_only[name] = row

@@ -28,7 +28,8 @@
 
 namespace gfors {
 
-constexpr int FB_NNZ = 1024;   // nonzeros per row block: 16 KB of 16-byte gathers per buffer
+constexpr int FB_NNZ = 1024;   // nonzeros per row block, k_b <= 128 per unit (2 words: 16 KB of 16-byte gathers per buffer)
+constexpr int FB_NNZ8 = 256;   // nonzeros per row block of the wide plan: 8 words (64 bytes) per nonzero, 16 KB per buffer
 constexpr int FB_NT = 256;
 constexpr int FB_ROWS = 255;   // rows per block (row-in-block index is a byte)
 
@@ -53,20 +54,24 @@ __device__ __forceinline__ void fb_cp_async(uint64_t* smem, const uint64_t* g, u
     else asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(s), "l"(g), "l"(pol));
 }
 
-template <int WV>
+template <int WV, int NNZ>
 struct FbBuf {
-    uint64_t tile[FB_NNZ * WV];
+    uint64_t tile[NNZ * WV];
     int rp[FB_ROWS + 1];
     int info[FB_ROWS];
     int nr;
 };
 
-template <int BMAX, int WV>
+// WV words per nonzero and unit: 1 or 2 (one 8/16-byte cp.async per nonzero, plan of FB_NNZ), or 8
+// (k_b >= 512: the 64-byte piece of the sample row is moved by 4 consecutive lanes with 16 bytes each —
+// one cache line per nonzero per warp instruction instead of 4 separate gathers; plan of FB_NNZ8)
+template <int BMAX, int WV, int NNZ>
 __global__ void __launch_bounds__(FB_NT, 6) k_feas_rb(ClassCsr cc, const unsigned char* __restrict__ skip,
                                                    const uint64_t* __restrict__ X, int W,
                                                    unsigned long long* __restrict__ viol) {
-    constexpr int U = FB_NNZ / FB_NT;
-    __shared__ __align__(16) FbBuf<WV> buf[2];
+    constexpr int LPN = WV >= 2 ? WV / 2 : 1;  // lanes per nonzero (16 bytes each)
+    constexpr int U = NNZ * LPN / FB_NT;
+    __shared__ __align__(16) FbBuf<WV, NNZ> buf[2];
     __shared__ unsigned long long s_viol[64];
     __shared__ unsigned char s_skip[2][FB_NT];  // skip flags of the rows of the next unit to issue (ring of 2)
     const bool use_smem = W <= 64;
@@ -83,7 +88,7 @@ __global__ void __launch_bounds__(FB_NT, 6) k_feas_rb(ClassCsr cc, const unsigne
     auto load = [&](const int4& d) {
 #pragma unroll
         for (int k = 0; k < U; ++k) {
-            const int t = k * FB_NT + threadIdx.x;
+            const int t = (k * FB_NT + threadIdx.x) / LPN;
             cols[k] = t < d.w ? ld_hint_i32(cc.idx + d.z + t, pf) : -1;
             if (skip) ribs[k] = t < d.w ? ld_hint_u8(cc.rib + d.z + t, pf) : 0;
         }
@@ -91,14 +96,16 @@ __global__ void __launch_bounds__(FB_NT, 6) k_feas_rb(ClassCsr cc, const unsigne
     };
     // phase 1b: gathers + row metadata of unit u into buffer bi
     auto issue = [&](long long u, const int4& d, int bi) {
-        FbBuf<WV>& B = buf[bi];
+        FbBuf<WV, NNZ>& B = buf[bi];
         if (u < nunits) {
             const int nr = d.y & 0xff;
             const unsigned char* sk = skip ? s_skip[bi] : nullptr;
 #pragma unroll
             for (int k = 0; k < U; ++k)
-                if (cols[k] >= 0 && !(sk && sk[ribs[k]]))
-                    fb_cp_async<WV>(B.tile + (k * FB_NT + threadIdx.x) * WV, X + (long long)cols[k] * W + w0, pl);
+                if (cols[k] >= 0 && !(sk && sk[ribs[k]])) {
+                    const int pq = k * FB_NT + threadIdx.x, t = pq / LPN, c = pq % LPN;
+                    fb_cp_async<WV == 1 ? 1 : 2>(B.tile + t * WV + 2 * c, X + (long long)cols[k] * W + w0 + 2 * c, pl);
+                }
             if ((int)threadIdx.x <= nr) fb_cp4(&B.rp[threadIdx.x], cc.ptr + d.x + threadIdx.x);
             if ((int)threadIdx.x < nr) fb_cp4(&B.info[threadIdx.x], cc.info + d.x + threadIdx.x);
             if (threadIdx.x == 0) B.nr = d.y;
@@ -124,10 +131,14 @@ __global__ void __launch_bounds__(FB_NT, 6) k_feas_rb(ClassCsr cc, const unsigne
         asm volatile("cp.async.wait_group 1;");
         __syncthreads();
         // phase 2: unit u from buffer st
-        const FbBuf<WV>& B = buf[st];
+        const FbBuf<WV, NNZ>& B = buf[st];
         const int nr = B.nr & 0xff, G = B.nr >> 8;
         const int p0 = B.rp[0];
         const int lane = threadIdx.x & (G - 1), grp = threadIdx.x / G, ngr = FB_NT / G;
+        // VB words per pass over the rows (both words for k_b = 128; one at a time for the 8-word units,
+        // whose counters would not fit in registers)
+        constexpr int VB = WV <= 2 ? WV : 1;
+        for (int v0 = 0; v0 < WV; v0 += VB)
         for (int rb = 0; rb < nr; rb += ngr) {
             const int rr = rb + grp;
             const bool valid = rr < nr;
@@ -138,47 +149,49 @@ __global__ void __launch_bounds__(FB_NT, 6) k_feas_rb(ClassCsr cc, const unsigne
                 q0 = B.rp[rr] - p0; q1 = B.rp[rr + 1] - p0;
                 if (skip && s_skip[st][rr]) { rel = 4; q1 = q0; }
             }
-            uint64_t Cn[WV][BMAX], sat[WV];
+            uint64_t Cn[VB][BMAX], sat[VB];
 #pragma unroll
-            for (int v = 0; v < WV; ++v) {
+            for (int v = 0; v < VB; ++v) {
                 sat[v] = 0ull;
 #pragma unroll
                 for (int q = 0; q < BMAX; ++q) Cn[v][q] = 0ull;
             }
             if constexpr (BMAX == 1) {
                 // one plane (B = 1, count capped at 1): the count is the OR of the words
-                uint64_t o[WV];
+                uint64_t o[VB];
 #pragma unroll
-                for (int v = 0; v < WV; ++v) o[v] = 0ull;
+                for (int v = 0; v < VB; ++v) o[v] = 0ull;
                 if (rel < 3)
                     for (int i = q0 + lane; i < q1; i += G) {
 #pragma unroll
-                        for (int v = 0; v < WV; ++v) o[v] |= B.tile[i * WV + v];
+                        for (int v = 0; v < VB; ++v) o[v] |= B.tile[i * WV + v0 + v];
                     }
 #pragma unroll
-                for (int v = 0; v < WV; ++v) {
+                for (int v = 0; v < VB; ++v) {
                     for (int sh = G >> 1; sh > 0; sh >>= 1) o[v] |= __shfl_xor_sync(0xffffffffu, o[v], sh, G);
                     Cn[v][0] = o[v];
                 }
-            } else if (rel < 3) {
-                for (int i = q0 + lane; i < q1; i += G) {
+            } else {
+                if (rel < 3)
+                    for (int i = q0 + lane; i < q1; i += G) {
 #pragma unroll
-                    for (int v = 0; v < WV; ++v) csa_add_bit<BMAX>(Cn[v], sat[v], B.tile[i * WV + v], Bp);
-                }
+                        for (int v = 0; v < VB; ++v) csa_add_bit<BMAX>(Cn[v], sat[v], B.tile[i * WV + v0 + v], Bp);
+                    }
+#pragma unroll
+                for (int v = 0; v < VB; ++v)
+                    for (int o = G >> 1; o > 0; o >>= 1) {
+                        uint64_t D[BMAX];
+#pragma unroll
+                        for (int q = 0; q < BMAX; ++q) D[q] = __shfl_xor_sync(0xffffffffu, Cn[v][q], o, G);
+                        const uint64_t dsat = __shfl_xor_sync(0xffffffffu, sat[v], o, G);
+                        csa_add_counter<BMAX>(Cn[v], sat[v], D, dsat, Bp);
+                    }
             }
+            if (lane == 0 && valid) {
 #pragma unroll
-            for (int v = 0; v < WV; ++v) {
-                if constexpr (BMAX > 1)
-                for (int o = G >> 1; o > 0; o >>= 1) {
-                    uint64_t D[BMAX];
-#pragma unroll
-                    for (int q = 0; q < BMAX; ++q) D[q] = __shfl_xor_sync(0xffffffffu, Cn[v][q], o, G);
-                    const uint64_t dsat = __shfl_xor_sync(0xffffffffu, sat[v], o, G);
-                    csa_add_counter<BMAX>(Cn[v], sat[v], D, dsat, Bp);
-                }
-                if (lane == 0 && valid) {
+                for (int v = 0; v < VB; ++v) {
                     const uint64_t bad = ~count_ok<BMAX>(Cn[v], sat[v], Bp, t, rel);
-                    if (bad) atomicOr(use_smem ? &s_viol[w0 + v] : viol + w0 + v, (unsigned long long)bad);
+                    if (bad) atomicOr(use_smem ? &s_viol[w0 + v0 + v] : viol + w0 + v0 + v, (unsigned long long)bad);
                 }
             }
         }

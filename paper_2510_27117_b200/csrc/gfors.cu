@@ -586,7 +586,8 @@ struct gfors_ctx {
     } cnt[3];  // BMAX 1, 2, 8: rows longer than FB_NNZ (k_feas_count)
     struct CountRb {               // rows <= FB_NNZ nonzeros of each class (k_feas_rb, feas_rb.cuh)
         CountList rows;
-        ClassCsr cc{};
+        ClassCsr cc{};                  // blocks of FB_NNZ nonzeros (units of 1-2 words)
+        ClassCsr cc8{};                 // blocks of FB_NNZ8 nonzeros (units of 8 words, k_b % 512 == 0)
         unsigned char* skip = nullptr;  // [nrows] per-round "satisfied by p = 1 variables" flags
     } cntrb[3];
     int* d_int_row = nullptr;
@@ -1287,14 +1288,16 @@ void enqueue_eval(gfors_ctx* C, cudaStream_t s, int W, const unsigned char* ones
         CountRows cr{rb.rows.row, rb.rows.t, rb.rows.rel, rb.rows.B, rb.rows.nrows};
         if (ones) LAUNCH(C, s, KC_FEAS, (k_feas_skip<<<grid_for(cr.nrows), NT, 0, s>>>(cr, ones, rb.skip)));
         const unsigned char* sk = ones ? rb.skip : nullptr;
-        const int wv = (W % 2 == 0) ? 2 : 1;
+        const int wv = (W % 8 == 0) ? 8 : ((W % 2 == 0) ? 2 : 1);
         const int nwg = W / wv;
+        const ClassCsr& cc = wv == 8 ? rb.cc8 : rb.cc;
         // 6 CTAs per SM (37 KB of shared memory each) over all word groups
-        const dim3 grid((unsigned)std::max<long long>(1, std::min<long long>(rb.cc.nblk, (long long)C->num_sms * 6 / nwg)),
+        const dim3 grid((unsigned)std::max<long long>(1, std::min<long long>(cc.nblk, (long long)C->num_sms * 6 / nwg)),
                         (unsigned)nwg);
 #define FEAS_RB(BM) \
-        if (wv == 2) LAUNCH(C, s, KC_FEAS, (k_feas_rb<BM, 2><<<grid, FB_NT, 0, s>>>(rb.cc, sk, C->d_X, W, C->d_viol))); \
-        else LAUNCH(C, s, KC_FEAS, (k_feas_rb<BM, 1><<<grid, FB_NT, 0, s>>>(rb.cc, sk, C->d_X, W, C->d_viol)));
+        if (wv == 8) LAUNCH(C, s, KC_FEAS, (k_feas_rb<BM, 8, FB_NNZ8><<<grid, FB_NT, 0, s>>>(cc, sk, C->d_X, W, C->d_viol))); \
+        else if (wv == 2) LAUNCH(C, s, KC_FEAS, (k_feas_rb<BM, 2, FB_NNZ><<<grid, FB_NT, 0, s>>>(cc, sk, C->d_X, W, C->d_viol))); \
+        else LAUNCH(C, s, KC_FEAS, (k_feas_rb<BM, 1, FB_NNZ><<<grid, FB_NT, 0, s>>>(cc, sk, C->d_X, W, C->d_viol)));
         if (li == 0) { FEAS_RB(1) } else if (li == 1) { FEAS_RB(2) } else { FEAS_RB(8) }
 #undef FEAS_RB
     }
