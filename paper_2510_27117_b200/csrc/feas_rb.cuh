@@ -215,4 +215,17 @@ __global__ void k_feas_skip(CountRows cr, const unsigned char* __restrict__ ones
         skip[e] = (cr.rel[e] == 0 && (int)ones[cr.row[e]] >= cr.t[e]) ? 1 : 0;
 }
 
+// load time: the row-in-block byte of every nonzero of a plan, from its descriptors (one warp per row;
+// rib is indexed like idx, i.e. from position base of the class's nonzeros)
+__global__ void __launch_bounds__(256) k_fb_rib(const int4* __restrict__ desc, const int* __restrict__ ptr, long long nblk,
+                                                long long base, unsigned char* __restrict__ rib) {
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (long long b = blockIdx.x; b < nblk; b += gridDim.x) {
+        const int4 d = desc[b];
+        const int nr = d.y & 0xff;
+        for (int r = wid; r < nr; r += blockDim.x >> 5)
+            for (long long q = ptr[d.x + r] + lane; q < ptr[d.x + r + 1]; q += 32) rib[q - base] = (unsigned char)r;
+    }
+}
+
 }  // namespace gfors

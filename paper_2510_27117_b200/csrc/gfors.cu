@@ -452,6 +452,7 @@ struct gfors_ctx {
     long long n = 0, m = 0, m1 = 0, m2 = 0, nnz = 0, qnnz = 0;
     long long m1p = 0;      // rows [0,m1p) are inequalities for the PDHG step (m under the relaxation, R26)
     bool repair = false;    // repair lanes before EvalBest (repair.cuh)
+    bool kcan_pinned = false;  // d_kcol was uploaded straight from the caller's pinned K columns (load)
     bool complete = false;  // cover completion before EvalBest (cover.cuh)
     int* d_cover_rows = nullptr;      // eligible covering rows (prep-owned, built on first use)
     long long n_cover = -1;

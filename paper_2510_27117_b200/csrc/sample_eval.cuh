@@ -466,6 +466,24 @@ __device__ __forceinline__ unsigned transpose32(unsigned x, int lane) {
     return x;
 }
 
+// load time: the bit planes of c - cmin (planes[h * nb + b] bit i % 32 = bit b of c_{32h + i%32} - cmin)
+__global__ void __launch_bounds__(256) k_obj_planes(const double* __restrict__ c, long long n, double cmin, int nb,
+                                                    unsigned* __restrict__ planes) {
+    const long long nch = (n + 31) / 32;
+    for (long long h = blockIdx.x * (long long)blockDim.x + threadIdx.x; h < nch; h += gridDim.x * (long long)blockDim.x) {
+        unsigned w[20] = {};
+        for (int k = 0; k < 32 && h * 32 + k < n; ++k) {
+            const long long cp = (long long)(c[h * 32 + k] - cmin);
+#pragma unroll
+            for (int b = 0; b < 20; ++b)
+                if (b < nb) w[b] |= (unsigned)((cp >> b) & 1) << k;
+        }
+#pragma unroll
+        for (int b = 0; b < 20; ++b)
+            if (b < nb) planes[h * nb + b] = w[b];
+    }
+}
+
 // One CTA of 8 warps per (chunk range, word group of WV words): every lane loads its variable's WV
 // words with one vector load, each warp walks chunks cta*cpc + warp + 8k (two at a time, loads
 // first), and the 8 warps' int64 lane sums are added in shared memory in a fixed order, giving ONE
