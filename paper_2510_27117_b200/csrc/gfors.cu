@@ -460,7 +460,8 @@ struct gfors_ctx {
     int* d_rp_order = nullptr;        // its inverse
     long long* d_rp_srow = nullptr;   // per-lane row sums when m > RP_SROWS
     long long rp_srow_len = 0;
-    uint32_t* d_Tsamp = nullptr;      // RandSampleStep thresholds ceil(p 2^32) (0: no planes needed)
+    uint2* d_slist = nullptr;         // RandSampleStep list of (i, ceil(p_i 2^32)) with 0 < p_i < 1
+    unsigned* d_scnt = nullptr;       // its length, the k_sample exit ticket, its u64 work counter (zero between rounds)
     int* d_cover_best = nullptr;
     uint64_t* d_cover_viol = nullptr;
     long long cover_viol_len = 0;
@@ -738,7 +739,7 @@ void gfors_ctx::free_prep() {
                    (void**)&d_X, (void**)&d_viol, (void**)&d_iacc, &d_zpart, (void**)&d_z, (void**)&d_ctrl,
                    (void**)&d_qx, (void**)&d_qdx, (void**)&d_qxpart, (void**)&d_Xs, (void**)&d_kS,
                    (void**)&d_qxpart2, (void**)&d_qreuse, (void**)&d_cover_rows, (void**)&d_cover_best,
-                   (void**)&d_cover_viol, (void**)&d_rp_rank, (void**)&d_rp_order, (void**)&d_rp_srow, (void**)&d_Tsamp,
+                   (void**)&d_cover_viol, (void**)&d_rp_rank, (void**)&d_rp_order, (void**)&d_rp_srow, (void**)&d_slist, (void**)&d_scnt,
                    (void**)&d_rs_rlo, &d_rs_y, (void**)&d_rs_u};
     for (void** p : ps) { dfree(*p); *p = nullptr; }
     X_words = iacc_len = zpart_len = z_len = Xs_lanes = kS_len = 0;
@@ -1398,7 +1399,12 @@ void ensure_batch(gfors_ctx* C, int W) {
         dfree(C->d_viol); C->d_viol = dalloc<unsigned long long>(W);
         C->gvalid = false;
     }
-    if (!C->d_Tsamp) { C->d_Tsamp = dalloc<uint32_t>(C->n); C->gvalid = false; }
+    if (!C->d_slist) {
+        C->d_slist = dalloc<uint2>(C->n);
+        C->d_scnt = dalloc<unsigned>(4);
+        CK(cudaMemset(C->d_scnt, 0, 4 * sizeof(unsigned)));
+        C->gvalid = false;
+    }
     const long long niacc = C->n_int * 64LL * W;
     if (niacc > C->iacc_len) {
         dfree(C->d_iacc); C->d_iacc = dalloc<unsigned long long>(niacc); C->iacc_len = niacc; C->gvalid = false;
@@ -1587,8 +1593,8 @@ void enqueue_sample(gfors_ctx* C, cudaStream_t s, const double* pfix, int W, lon
         rk.k1[t] = (uint32_t)(seed >> 32) + (uint32_t)t * 0xBB67AE85u;
     }
     LAUNCH(C, s, KC_SAMPLE, (k_sample_thr<T><<<grid_for(C->n), NT, 0, s>>>((const T*)C->d_x[0], (const T*)C->d_x[1], pfix,
-                                C->n, W, C->d_ctrl, kint, use_fixed, C->d_Tsamp, C->d_X)));
-    LAUNCH(C, s, KC_SAMPLE, (k_sample<<<C->num_sms * 8, NT, 0, s>>>(C->d_Tsamp, C->n, W, word_off, rk, C->d_ctrl, r, kr,
+                                C->n, W, C->d_ctrl, kint, use_fixed, C->d_slist, C->d_scnt, C->d_X)));
+    LAUNCH(C, s, KC_SAMPLE, (k_sample<<<C->num_sms * SMP_CTAS, NT, 0, s>>>(C->d_slist, C->d_scnt, W, word_off, rk, C->d_ctrl, r, kr,
                                 round_fixed, use_fixed, C->d_X)));
 }
 

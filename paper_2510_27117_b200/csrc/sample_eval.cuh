@@ -69,81 +69,129 @@ __device__ __forceinline__ uint4 philox_rkw(uint4 c, const PhiloxKeys& rk) {
     return c;
 }
 
-// RandSampleStep pass 1: T_i = ceil(p_i 2^32) for every variable (fp64, exact), stored as uint32 with
-// 0 meaning "no random planes needed": the words of variables with T = 0 (p = 0) or T = 2^32 (p = 1)
-// are written here (all zeros / all ones).  p: a fixed vector (pfix) or x_k of the loop.
+// RandSampleStep pass 1: T_i = ceil(p_i 2^32) for every variable (fp64, exact).  The words of variables
+// with T = 0 (p = 0) or T = 2^32 (p = 1) need no random planes and are written here (all zeros / all
+// ones); the others are appended to a compact list of (i, T) (warp-aggregated atomic, any order: a
+// word's value depends only on (i, word, T, round)).  p: a fixed vector (pfix) or x_k of the loop.
 template <typename T>
 __global__ void __launch_bounds__(256) k_sample_thr(const T* __restrict__ xa, const T* __restrict__ xb2,
                                                     const double* __restrict__ pfix, long long n, int W,
                                                     const Ctrl* __restrict__ ctrl, long long kint, int use_fixed,
-                                                    uint32_t* __restrict__ Tarr, uint64_t* __restrict__ X) {
+                                                    uint2* __restrict__ list, unsigned* __restrict__ cnt,
+                                                    uint64_t* __restrict__ X) {
+    constexpr int PER = 4;  // variables per thread and chunk: one list atomic per 1024 variables
+    __shared__ unsigned s_off[8], s_base;
     const T* __restrict__ p = nullptr;
     if (!use_fixed) p = (((ctrl->blk + 1) * kint) & 1) ? xb2 : xa;  // x_k written by iteration (b+1)*kint - 1
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += gridDim.x * (long long)blockDim.x) {
-        double pi = pfix ? pfix[i] : (double)p[i];
-        pi = pi < 0.0 ? 0.0 : (pi > 1.0 ? 1.0 : pi);
-        const double Td = ceil(pi * 4294967296.0);
-        uint32_t t = 0;
-        if (Td <= 0.0) { for (int w = 0; w < W; ++w) X[i * W + w] = 0ull; }
-        else if (Td >= 4294967296.0) { for (int w = 0; w < W; ++w) X[i * W + w] = ~0ull; }
-        else t = (uint32_t)Td;
-        Tarr[i] = t;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (long long c0 = (long long)blockIdx.x * 256 * PER; c0 < n; c0 += (long long)gridDim.x * 256 * PER) {
+        uint32_t t[PER];
+        unsigned bal[PER], tot = 0;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const long long i = c0 + k * 256 + threadIdx.x;
+            t[k] = 0;
+            if (i < n) {
+                double pi = pfix ? pfix[i] : (double)p[i];
+                pi = pi < 0.0 ? 0.0 : (pi > 1.0 ? 1.0 : pi);
+                const double Td = ceil(pi * 4294967296.0);
+                if (Td <= 0.0) { for (int w = 0; w < W; ++w) X[i * W + w] = 0ull; }
+                else if (Td >= 4294967296.0) { for (int w = 0; w < W; ++w) X[i * W + w] = ~0ull; }
+                else t[k] = (uint32_t)Td;
+            }
+            bal[k] = __ballot_sync(0xffffffffu, t[k] != 0u);
+            tot += __popc(bal[k]);
+        }
+        if (lane == 0) s_off[wid] = tot;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned acc = 0;
+            for (int w = 0; w < 8; ++w) { const unsigned v = s_off[w]; s_off[w] = acc; acc += v; }
+            s_base = acc ? atomicAdd(cnt, acc) : 0u;
+        }
+        __syncthreads();
+        unsigned o = s_base + s_off[wid];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            if (t[k]) list[o + __popc(bal[k] & ((1u << lane) - 1u))] = make_uint2((unsigned)(c0 + k * 256 + threadIdx.x), t[k]);
+            o += __popc(bal[k]);
+        }
+        __syncthreads();  // s_off / s_base reused by the next chunk
     }
 }
 
 // RandSampleStep pass 2 (Alg. 3, contract R10): the MSB-first compare decides a 64-lane word after a
-// data-dependent number of plane pairs (E ~ 3.7 Philox calls, up to 16).  Every thread walks its own
-// variables (i = tid, tid + stride, ...) and their W words one after another; lanes of a warp run
-// independently (a lane whose word is decided goes on to its next word while the others finish
-// theirs: independent thread scheduling, no warp-wide vote), two plane pairs per loop trip.  T of the
-// next variable is prefetched; T = 0 variables were written by pass 1.  32-bit indices (n < 2^31)
-// keep the loop state small.  Identical output to bernoulli_word.
-__global__ void __launch_bounds__(256) k_sample(const uint32_t* __restrict__ Tarr, long long n, int W, long long word_off,
-                                                const __grid_constant__ PhiloxKeys rk, const Ctrl* __restrict__ ctrl,
-                                                int r, int kr, unsigned round_fixed, int use_fixed, uint64_t* __restrict__ X) {
+// data-dependent number of plane pairs (E ~ 3.9 Philox calls for p away from 0 and 1, up to 16).  The
+// work items are the words (list entry e, word w) of the listed variables, item k = e*W + w; thread t
+// takes items t, t + S, t + 2S, ... (S = threads in the grid).  ONE flat loop: every trip makes two
+// Philox calls (four planes; independent chains) for the thread's current word, and a thread whose
+// word got decided stores it and moves on to its next item (prefetched) inside the same trip.  There
+// is no inner per-word loop, so the lanes of a warp never wait at a reconvergence point for the
+// slowest word: a warp runs for the max over its lanes of the SUM of their trips (~33 words each on
+// config 5), not the sum over words of the max.  The last CTA to finish zeroes the list counter for
+// the next round.  Identical output to bernoulli_word.
+constexpr int SMP_CTAS = 6;  // resident CTAs per SM of k_sample (grid = SMP_CTAS x SMs: one wave)
+__global__ void __launch_bounds__(256, SMP_CTAS) k_sample(const uint2* __restrict__ list, unsigned* __restrict__ cnt, int W,
+                                                         long long word_off, const __grid_constant__ PhiloxKeys rk,
+                                                         const Ctrl* __restrict__ ctrl, int r, int kr, unsigned round_fixed,
+                                                         int use_fixed, uint64_t* __restrict__ X) {
     const unsigned round = use_fixed ? round_fixed : (unsigned)(ctrl->blk * kr + r);
-    const unsigned nn = (unsigned)n;  // n < 2^31 (load requirement): 32-bit indices throughout
-    const unsigned stride = gridDim.x * blockDim.x;
     const uint64_t pol = l2_policy_evict_last();  // the batch is gathered by the evaluator next
     const unsigned wbase = (unsigned)word_off;
-    unsigned i = blockIdx.x * blockDim.x + threadIdx.x;  // current variable
-    uint32_t Tv = i < nn ? __ldg(Tarr + i) : 0u;
-    unsigned ni = i + stride;                            // next variable, its threshold prefetched
-    uint32_t nT = ni < nn ? __ldg(Tarr + ni) : 0u;
-    int w = 0;
-    while (true) {
-        // next word to draw: skip variables with T = 0 (written by pass 1)
-        while (i < nn && Tv == 0u) {
-            i = ni; Tv = nT; w = 0;
-            ni = i + stride;
-            nT = ni < nn ? __ldg(Tarr + ni) : 0u;
+    const long long nitems = (long long)*(volatile unsigned*)cnt * W;
+    const long long S = (long long)gridDim.x * blockDim.x;
+    // item k = (entry e, word w); the item S further is (e + qS, w + rS) carried over
+    const long long qS = S / W;
+    const unsigned rS = (unsigned)(S % W);
+    long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    long long e = k / W;
+    unsigned w = (unsigned)(k - e * W);
+    auto advance = [&]() { k += S; e += qS; w += rS; if (w >= (unsigned)W) { w -= W; ++e; } };
+    // current item (i, T, word) and the next one, prefetched
+    uint2 cur = k < nitems ? __ldg(list + e) : make_uint2(0u, 0u);
+    unsigned cwo = w;
+    bool active = k < nitems;
+    advance();
+    uint2 nxt = k < nitems ? __ldg(list + e) : make_uint2(0u, 0u);
+    unsigned nwo = w;
+    bool nact = k < nitems;
+    unsigned Tsh = cur.y, q = 0u, ul = ~0u, uh = ~0u, rl = 0u, rh = 0u;
+    while (__any_sync(0xffffffffu, active)) {
+        // planes 2q (T bit 31 - 2q), 2q + 1, 2q + 2, 2q + 3 from two Philox calls: t = 1 -> lanes with
+        // u-bit 0 decide 1, und &= pl; t = 0 -> lanes with u-bit 1 decide 0, und &= ~pl (m = t ? ~0 : 0).
+        // Planes after the word is decided change nothing.
+        const unsigned wg = wbase + cwo;
+        const uint4 o = philox_rkw(make_uint4(cur.x, wg, q, round), rk);
+        const uint4 o2 = philox_rkw(make_uint4(cur.x, wg, q + 1u, round), rk);
+        uint32_t m = 0u - (Tsh >> 31);
+        rl |= ul & ~o.x & m; rh |= uh & ~o.y & m;
+        ul &= ~(o.x ^ m);    uh &= ~(o.y ^ m);
+        m = 0u - ((Tsh >> 30) & 1u);
+        rl |= ul & ~o.z & m; rh |= uh & ~o.w & m;
+        ul &= ~(o.z ^ m);    uh &= ~(o.w ^ m);
+        m = 0u - ((Tsh >> 29) & 1u);
+        rl |= ul & ~o2.x & m; rh |= uh & ~o2.y & m;
+        ul &= ~(o2.x ^ m);    uh &= ~(o2.y ^ m);
+        m = 0u - ((Tsh >> 28) & 1u);
+        rl |= ul & ~o2.z & m; rh |= uh & ~o2.w & m;
+        ul &= ~(o2.z ^ m);    uh &= ~(o2.w ^ m);
+        Tsh <<= 4;
+        q += 2u;
+        if ((ul | uh) == 0u || q == 16u) {  // word decided (u == T lanes stay 0): store, take the next item
+            if (active) st_hint_u64(X + (size_t)cur.x * W + cwo, (uint64_t)rl | ((uint64_t)rh << 32), pol);
+            cur = nxt; cwo = nwo; active = nact;
+            advance();
+            nxt = k < nitems ? __ldg(list + e) : make_uint2(0u, 0u);
+            nwo = w;
+            nact = k < nitems;
+            Tsh = cur.y; q = 0u; ul = uh = ~0u; rl = rh = 0u;
         }
-        if (i >= nn) break;
-        // one 64-lane word: two plane pairs per trip until every lane is decided (MSB-first compare);
-        // plane with T-bit t: t = 1 -> lanes with u-bit 0 decide 1, und &= pl; t = 0 -> lanes with u-bit 1
-        // decide 0, und &= ~pl (m = t ? ~0 : 0).  Planes after the word is decided change nothing.
-        uint32_t ul = ~0u, uh = ~0u, rl = 0u, rh = 0u, Tsh = Tv;
-        const unsigned wg = wbase + (unsigned)w;
-        for (unsigned q = 0; q < 16; q += 2) {
-            const uint4 o = philox_rkw(make_uint4(i, wg, q, round), rk);
-            const uint4 o2 = philox_rkw(make_uint4(i, wg, q + 1, round), rk);
-            uint32_t m = 0u - (Tsh >> 31);
-            rl |= ul & ~o.x & m; rh |= uh & ~o.y & m;
-            ul &= ~(o.x ^ m);    uh &= ~(o.y ^ m);
-            m = 0u - ((Tsh >> 30) & 1u);
-            rl |= ul & ~o.z & m; rh |= uh & ~o.w & m;
-            ul &= ~(o.z ^ m);    uh &= ~(o.w ^ m);
-            m = 0u - ((Tsh >> 29) & 1u);
-            rl |= ul & ~o2.x & m; rh |= uh & ~o2.y & m;
-            ul &= ~(o2.x ^ m);    uh &= ~(o2.y ^ m);
-            m = 0u - ((Tsh >> 28) & 1u);
-            rl |= ul & ~o2.z & m; rh |= uh & ~o2.w & m;
-            ul &= ~(o2.z ^ m);    uh &= ~(o2.w ^ m);
-            Tsh <<= 4;
-            if ((ul | uh) == 0u) break;  // (u == T lanes stay 0)
-        }
-        st_hint_u64(X + (size_t)i * W + w, (uint64_t)rl | ((uint64_t)rh << 32), pol);
-        if (++w == W) { i = ni; Tv = nT; w = 0; ni = i + stride; nT = ni < nn ? __ldg(Tarr + ni) : 0u; }
+    }
+    // the last CTA out resets the list counter (every CTA read it above)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(cnt + 1, 1u) == gridDim.x - 1) { cnt[0] = 0u; cnt[1] = 0u; __threadfence(); }
     }
 }
 
