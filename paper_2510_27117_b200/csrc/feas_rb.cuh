@@ -7,8 +7,8 @@
 // k_dual_rb recipe (rowblock.cuh) — and that nothing on the issue path waits on a dependent load:
 //   * each count class has its own CSR (an alias of K's when the class is a contiguous row range,
 //     else a compacted copy) cut into blocks of <= FB_NNZ nonzeros and <= FB_ROWS rows, described by
-//     one 16-byte record per block {first entry, rows | G << 8, first nonzero, nonzeros} (int32:
-//     nnz < 2^31; G = lanes per row, ~12 nonzeros per lane, chosen on the host);
+//     one 16-byte record per block {first entry, rows | log2(G) << 8, first nonzero, nonzeros} (int32:
+//     nnz < 2^31; G = lanes per row, the largest power of two <= 32 with G * rows <= FB_NT);
 //   * a CTA (blockIdx.y = its group of WV words) walks blocks u, u + grid, ...; the record of block
 //     u + 3*grid is loaded while unit u is reduced, the column indices (and row-in-block bytes) of
 //     u + 2*grid likewise, so at the top of each iteration unit u + grid can be issued at once:
@@ -37,7 +37,7 @@ struct ClassCsr {
     const int* ptr;             // [nrows+1] class-local row pointers into idx (int32: nnz < 2^31)
     const int* idx;             // column indices
     const unsigned char* rib;   // row-in-block of each nonzero (indexed like idx)
-    const int4* desc;           // [nblk] {first entry, rows | G << 8, first nonzero, nonzeros}
+    const int4* desc;           // [nblk] {first entry, rows | log2(G) << 8, first nonzero, nonzeros}
     const int* info;            // [nrows] packed target: t | rel << 16 | B << 20
     long long nblk;
 };
@@ -65,13 +65,14 @@ struct FbBuf {
 // WV words per nonzero and unit: 1 or 2 (one 8/16-byte cp.async per nonzero, plan of FB_NNZ), or 8
 // (k_b >= 512: the 64-byte piece of the sample row is moved by 4 consecutive lanes with 16 bytes each —
 // one cache line per nonzero per warp instruction instead of 4 separate gathers; plan of FB_NNZ8)
-template <int BMAX, int WV, int NNZ>
+template <int BMAX, int WV, int NNZ, bool SKIP>
 __global__ void __launch_bounds__(FB_NT, 6) k_feas_rb(ClassCsr cc, const unsigned char* __restrict__ skip,
                                                    const uint64_t* __restrict__ X, int W,
                                                    unsigned long long* __restrict__ viol) {
     constexpr int LPN = WV >= 2 ? WV / 2 : 1;  // lanes per nonzero (16 bytes each)
     constexpr int U = NNZ * LPN / FB_NT;
-    __shared__ __align__(16) FbBuf<WV, NNZ> buf[2];
+    extern __shared__ __align__(16) unsigned char fb_smem[];  // two FbBuf (dynamic: > 48 KB for FB_NNZ)
+    FbBuf<WV, NNZ>* buf = reinterpret_cast<FbBuf<WV, NNZ>*>(fb_smem);
     __shared__ unsigned long long s_viol[64];
     __shared__ unsigned char s_skip[2][FB_NT];  // skip flags of the rows of the next unit to issue (ring of 2)
     const bool use_smem = W <= 64;
@@ -90,19 +91,18 @@ __global__ void __launch_bounds__(FB_NT, 6) k_feas_rb(ClassCsr cc, const unsigne
         for (int k = 0; k < U; ++k) {
             const int t = (k * FB_NT + threadIdx.x) / LPN;
             cols[k] = t < d.w ? ld_hint_i32(cc.idx + d.z + t, pf) : -1;
-            if (skip) ribs[k] = t < d.w ? ld_hint_u8(cc.rib + d.z + t, pf) : 0;
+            if (SKIP) ribs[k] = t < d.w ? ld_hint_u8(cc.rib + d.z + t, pf) : 0;
         }
-        skf = (skip && (int)threadIdx.x < (d.y & 0xff)) ? __ldg(skip + d.x + threadIdx.x) : 0;
+        skf = (SKIP && (int)threadIdx.x < (d.y & 0xff)) ? __ldg(skip + d.x + threadIdx.x) : 0;
     };
     // phase 1b: gathers + row metadata of unit u into buffer bi
     auto issue = [&](long long u, const int4& d, int bi) {
         FbBuf<WV, NNZ>& B = buf[bi];
         if (u < nunits) {
             const int nr = d.y & 0xff;
-            const unsigned char* sk = skip ? s_skip[bi] : nullptr;
 #pragma unroll
             for (int k = 0; k < U; ++k)
-                if (cols[k] >= 0 && !(sk && sk[ribs[k]])) {
+                if (cols[k] >= 0 && !(SKIP && s_skip[bi][ribs[k]])) {
                     const int pq = k * FB_NT + threadIdx.x, t = pq / LPN, c = pq % LPN;
                     fb_cp_async<WV == 1 ? 1 : 2>(B.tile + t * WV + 2 * c, X + (long long)cols[k] * W + w0 + 2 * c, pl);
                 }
@@ -132,9 +132,9 @@ __global__ void __launch_bounds__(FB_NT, 6) k_feas_rb(ClassCsr cc, const unsigne
         __syncthreads();
         // phase 2: unit u from buffer st
         const FbBuf<WV, NNZ>& B = buf[st];
-        const int nr = B.nr & 0xff, G = B.nr >> 8;
+        const int nr = B.nr & 0xff, lgG = B.nr >> 8, G = 1 << lgG;
         const int p0 = B.rp[0];
-        const int lane = threadIdx.x & (G - 1), grp = threadIdx.x / G, ngr = FB_NT / G;
+        const int lane = threadIdx.x & (G - 1), grp = threadIdx.x >> lgG, ngr = FB_NT >> lgG;
         // VB words per pass over the rows (both words for k_b = 128; one at a time for the 8-word units,
         // whose counters would not fit in registers)
         constexpr int VB = WV <= 2 ? WV : 1;
@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(FB_NT, 6) k_feas_rb(ClassCsr cc, const unsigne
                 const int in = B.info[rr];
                 t = in & 0xffff; rel = (in >> 16) & 0xf; Bp = (in >> 20) & 0xf;
                 q0 = B.rp[rr] - p0; q1 = B.rp[rr + 1] - p0;
-                if (skip && s_skip[st][rr]) { rel = 4; q1 = q0; }
+                if (SKIP && s_skip[st][rr]) { rel = 4; q1 = q0; }
             }
             uint64_t Cn[VB][BMAX], sat[VB];
 #pragma unroll

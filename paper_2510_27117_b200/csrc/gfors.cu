@@ -1293,15 +1293,29 @@ void enqueue_eval(gfors_ctx* C, cudaStream_t s, int W, const unsigned char* ones
         const int wv = (W % 8 == 0) ? 8 : ((W % 2 == 0) ? 2 : 1);
         const int nwg = W / wv;
         const ClassCsr& cc = wv == 8 ? rb.cc8 : rb.cc;
-        // 6 CTAs per SM (37 KB of shared memory each) over all word groups
-        const dim3 grid((unsigned)std::max<long long>(1, std::min<long long>(cc.nblk, (long long)C->num_sms * 6 / nwg)),
+        // grid: the resident CTAs per SM (shared memory bound) x SMs, over all word groups
+        auto feas_grid = [&](const void* fn, size_t smb) {
+            smem_attr(fn, smb);
+            int per_sm = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, FB_NT, smb));
+            return dim3((unsigned)std::max<long long>(1, std::min<long long>(cc.nblk, (long long)C->num_sms * std::max(per_sm, 1) / nwg)),
                         (unsigned)nwg);
-#define FEAS_RB(BM) \
-        if (wv == 8) LAUNCH(C, s, KC_FEAS, (k_feas_rb<BM, 8, FB_NNZ8><<<grid, FB_NT, 0, s>>>(cc, sk, C->d_X, W, C->d_viol))); \
-        else if (wv == 2) LAUNCH(C, s, KC_FEAS, (k_feas_rb<BM, 2, FB_NNZ><<<grid, FB_NT, 0, s>>>(cc, sk, C->d_X, W, C->d_viol))); \
-        else LAUNCH(C, s, KC_FEAS, (k_feas_rb<BM, 1, FB_NNZ><<<grid, FB_NT, 0, s>>>(cc, sk, C->d_X, W, C->d_viol)));
+        };
+#define FEAS_LAUNCH(BM, WVV, NNZV, SK)                                                                            \
+        {                                                                                                       \
+            const size_t smb = 2 * sizeof(FbBuf<WVV, NNZV>);                                                    \
+            const dim3 grid = feas_grid((const void*)k_feas_rb<BM, WVV, NNZV, SK>, smb);                        \
+            LAUNCH(C, s, KC_FEAS, (k_feas_rb<BM, WVV, NNZV, SK><<<grid, FB_NT, smb, s>>>(cc, sk, C->d_X, W, C->d_viol))); \
+        }
+#define FEAS_RB2(BM, SK) \
+        if (wv == 8) FEAS_LAUNCH(BM, 8, FB_NNZ8, SK) \
+        else if (wv == 2) FEAS_LAUNCH(BM, 2, FB_NNZ, SK) \
+        else FEAS_LAUNCH(BM, 1, FB_NNZ, SK)
+#define FEAS_RB(BM) if (sk) { FEAS_RB2(BM, true) } else { FEAS_RB2(BM, false) }
         if (li == 0) { FEAS_RB(1) } else if (li == 1) { FEAS_RB(2) } else { FEAS_RB(8) }
 #undef FEAS_RB
+#undef FEAS_RB2
+#undef FEAS_LAUNCH
     }
     for (int li = 0; li < 3; ++li) {
         auto& cl = C->cnt[li];
