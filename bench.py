@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--no-f2", action="store_true", help="skip the TU-reformulation facility-location leg (next row f2, config 7)")
     ap.add_argument("--f2-iters", type=int, default=3000)
     ap.add_argument("--no-f3", action="store_true", help="skip the customised-sampler 3D-assignment leg (next row f3, config 8)")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the PDHG-only and sampling-only legs (the ncu launch list of the step uses this)")
     ap.add_argument("--f3-iters", type=int, default=2000)
     return ap.parse_args()
 
@@ -635,7 +637,7 @@ def run_gpu(args):
     # PDHG alone (sampling off): Alg. 2 steps through the step hook (same kernels, eager launches),
     # fixed rho = rho_min, from x0 (dense phase: iterations 1-100) and after 1000 steps (1001-1100)
     pdhg_only = None
-    if rank == 0 and world == 1:
+    if rank == 0 and world == 1 and not args.no_extras:
         x0 = np.full(meta["n"], 0.5)
         s.set_state(x0, x0, np.zeros(meta["m"]))
         tau = 0.99 ** 0.5
@@ -657,7 +659,7 @@ def run_gpu(args):
     # PDHG, per p-distribution (x_k of the blocks 1-K trajectory, U(0,1), 90/10 exact/uniform mix)
     # and per k_b; device time over 10 rounds (gfors_sample_eval_timed)
     sampling_only = None
-    if rank == 0 and world == 1:
+    if rank == 0 and world == 1 and not args.no_extras:
         from gen import instances as G
         pv = G.p_vectors(meta["n"], 5)
         x_now = None
@@ -779,17 +781,22 @@ def run_gpu(args):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         s2.load(host)
+        ta = time.perf_counter()
         s2.preprocess(precision=args.precision)
+        tb = time.perf_counter()
         s2.run(max_iters=args.steps * args.k_int, **common)
+        tc = time.perf_counter()
         z2, x2, _ = s2.best_incumbent()
         torch.cuda.synchronize()
         te = time.perf_counter() - t0
         s2.close()
+        e2e_split = {"load_s": ta - t0, "preprocess_s": tb - ta, "run_s": tc - tb, "best_incumbent_s": t0 + te - tc}
         e2e = {"value": args.steps * args.k_b * world / te, "unit": UNIT, "h2d_bytes_per_step": h2d / args.steps,
                "d2h_bytes_per_step": (meta["n"] + 64) / args.steps,
                "note": "one gfors_load+preprocess+run(K blocks)+best_incumbent call chain from pinned host memory; "
                        "instance bytes amortised over the K steps; the device leg before it is its warm-up (the library's "
-                       "device memory pool keeps the memory the closed solver released)", "seconds": te}
+                       "device memory pool keeps the memory the closed solver released)", "seconds": te,
+               "split_s": e2e_split}
 
     # time-to-incumbent (BASELINE metric, third part): full solves of the small configs with the
     # default halting rule, %globaltimer stamp of the last improvement (Preprocess excluded)

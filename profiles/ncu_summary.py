@@ -65,7 +65,7 @@ def stalls(rep):
         names = [n for n in h if n.startswith("stall_") and "Not Issued" not in n]
         agg = {n[6:]: sum(float(r[h.index(n)] or 0) for r in body) for n in names}
         tot = sum(agg.values()) or 1.0
-        res.append(sorted(((round(100 * v / tot, 1), k) for k, v in agg.items()), reverse=True)[:5])
+        res.append((sec["name"], sorted(((round(100 * v / tot, 1), k) for k, v in agg.items()), reverse=True)[:5]))
     return res
 
 
@@ -86,10 +86,18 @@ def main():
     launches = []
     for rep in sys.argv[2:]:
         ls = raw(rep)
-        st = stalls(rep)
-        for d, s in zip(ls, st + [None] * (len(ls) - len(st))):
-            if s:
-                d["top_stalls_pct"] = s
+        st = stalls(rep)  # [(function name, top stalls)] per source-page section
+        # the source page groups its sections by function: pair them with the launches of the same
+        # function, in order
+        by_fn = {}
+        for name, top in st:
+            by_fn.setdefault(name, []).append(top)
+        for d in ls:
+            base = d["kernel"].split("(")[0].replace("void ", "").split("<")[0].split("::")[-1]
+            for name, tops in by_fn.items():
+                if tops and name.split("(")[0].replace("void ", "").split("<")[0].split("::")[-1] == base:
+                    d["top_stalls_pct"] = tops.pop(0)
+                    break
             launches.append(d)
     json.dump({"launches": launches}, open(sys.argv[1], "w"), indent=1)
     for d in launches:
