@@ -145,6 +145,13 @@ struct DefaultInitAlloc : std::allocator<T> {
 };
 template <typename T> using hvec = std::vector<T, DefaultInitAlloc<T>>;
 
+template <typename X>
+X* dupload_raw(const X* p, size_t count, cudaStream_t s) {
+    X* d = dalloc<X>(count);
+    if (count) CK(cudaMemcpyAsync(d, p, count * sizeof(X), cudaMemcpyHostToDevice, s));
+    return d;
+}
+
 template <typename X, typename Al>
 X* dupload(const std::vector<X, Al>& v, cudaStream_t s) {
     X* p = dalloc<X>(v.size());
@@ -468,8 +475,9 @@ struct gfors_ctx {
     bool maximize = false, integral = false, hasq = false;
     double c0 = 0.0;
     std::vector<int64_t> kptr, ktptr, qptr;
-    hvec<int32_t> kcol;
-    hvec<double> kval;
+    hvec<int32_t> kcol;  // canonical K on the host: filled by the load only when it permutes or negates
+    hvec<double> kval;   // rows, else on first use from the device copies (ensure_host_k)
+    bool khost = false;
     std::vector<int32_t> ktrow, qcol;
     std::vector<double> ktval, qval, ru;
     hvec<double> c;  // first touched by the parallel copy in the load
@@ -542,6 +550,7 @@ struct gfors_ctx {
     signed char* d_rsign = nullptr;
     DirPlan pd, pp;  // dual (rows of K), primal (rows of K') for the preprocessed precision
     DirPlan pdv[2], ppv[2];  // [0] fp32, [1] fp64 plans (row-block size differs)
+    bool plans64 = false;    // pdv[1], ppv[1] built (on the first fp64 Preprocess)
     bool push_dual_ok = false, push_primal_ok = false;  // push modes allowed by the matrix
     bool delta_dual = true;                             // delta push of the dual (option delta_dual)
     bool xskip = true;                                  // stationary-column skip (option xskip)
@@ -776,6 +785,30 @@ gfors_ctx::~gfors_ctx() {
     if (cap_stream) cudaStreamDestroy(cap_stream);
     if (cap_stream2) cudaStreamDestroy(cap_stream2);
     if (own_stream && stream) cudaStreamDestroy(stream);
+}
+
+// host copies of the canonical K (kcol, kval) from the device ones, for the host-side consumers
+// (relaxation checks, cover rows, TUReformulate) when the load did not need to make them
+void ensure_host_k(gfors_ctx* C) {
+    if (C->khost) return;
+    const long long nnz = C->nnz;
+    C->kcol.resize(nnz);
+    C->kval.resize(nnz);
+    if (nnz) {
+        CK(cudaStreamSynchronize(C->stream));
+        CK(cudaMemcpy(C->kcol.data(), C->d_kcol, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        if (C->kkind == KV_F64) {
+            CK(cudaMemcpy(C->kval.data(), C->d_kval, nnz * sizeof(double), cudaMemcpyDeviceToHost));
+        } else if (C->kkind == KV_I8) {
+            std::vector<signed char> a(nnz);
+            CK(cudaMemcpy(a.data(), C->d_kval, nnz, cudaMemcpyDeviceToHost));
+            for (long long p = 0; p < nnz; ++p) C->kval[p] = (double)a[p];
+        } else {  // one +-1 value per row
+            for (long long j = 0; j < C->m; ++j)
+                for (long long p = C->kptr[j]; p < C->kptr[j + 1]; ++p) C->kval[p] = (double)C->rsign[j];
+        }
+    }
+    C->khost = true;
 }
 
 #include "load_impl.inc"
@@ -1454,6 +1487,7 @@ void ensure_a3(gfors_ctx* C, long long a3n);
 
 // monotone relaxation (R26): every row acts as >= in the PDHG step / indicators; EvalBest unchanged
 void set_relax(gfors_ctx* C, int relax, int repair) {
+    if (relax) ensure_host_k(C);
     if (repair && !relax) input_error("params.repair: needs relax = 1");
     if (relax) {
         if (C->hasq) input_error("params.relax: the monotone relaxation needs Q = 0");
@@ -1488,6 +1522,7 @@ void set_complete(gfors_ctx* C, int complete, int W) {
     if (!complete) return;
     if (C->sharded) input_error("params.complete: not with the NCCL-sharded loop (winner regeneration)");
     if (C->n_cover < 0) {
+        ensure_host_k(C);
         std::vector<int> rows;
         for (long long j = 0; j < C->m1; ++j) {
             bool ok = C->ru[j] == 1.0 && C->kptr[j + 1] > C->kptr[j];
@@ -1751,6 +1786,11 @@ static void reset_push(gfors_ctx* C, cudaStream_t s) {
 // the product plans and push modes of the preprocessed precision (row-block size is per precision)
 static void select_plans(gfors_ctx* C) {
     const int v = C->precision == 64 ? 1 : 0;
+    if (v == 1 && !C->plans64) {
+        C->pdv[1] = plan_direction64(C->pdv[0], C->kptr, C->m, C->stream, C->owned);
+        C->ppv[1] = plan_direction64(C->ppv[0], C->ktptr, C->n, C->stream, C->owned);
+        C->plans64 = true;
+    }
     C->pd = C->pdv[v];
     C->pp = C->ppv[v];
     C->push_dual = C->push_dual_ok && C->pd.rb && C->pp.rb;
