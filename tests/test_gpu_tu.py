@@ -112,3 +112,58 @@ def test_tu_errors(gf):
     s.load(bad)
     with pytest.raises(gf.GforsError, match="not TU"):
         s.tu_reformulate([0, 1], [0, 1])
+
+
+def _canonical_pair(seed):
+    """The same canonical problem given two ways: A with its rows already canonical (GE rows first,
+    then EQ; no LE row), so the load keeps no host copy of K and TUReformulate downloads it from the
+    device (ensure_host_k); B with every GE row negated into an LE row, so the load copies and negates
+    on the host.  Integer values beyond +-1 (the int8 value class) and, for seed 1, a non-integer
+    coefficient (the fp64 class)."""
+    rng = np.random.default_rng(seed)
+    n = 12
+    K, r, sense, J, I = [], [], [], [], []
+    for k in range(3):
+        row = np.zeros(n)
+        row[k * 4:(k + 1) * 4] = 1.0
+        K.append(row); r.append(1.0); sense.append(0)
+        J.append(k); I.append(k * 4 + int(rng.integers(0, 4)))
+    ge = []
+    for _ in range(4):
+        row = np.zeros(n)
+        idx = rng.choice(n, size=5, replace=False)
+        row[idx] = rng.integers(1, 4, size=5) * rng.choice([-1, 1], size=5)
+        if seed == 1:
+            row[idx[0]] = 1.5
+        ge.append((row, float(rng.integers(-2, 3))))
+    c = rng.integers(-9, 10, size=n).astype(float)
+    # A: GE rows first, then the EQ rows
+    KA = [g[0] for g in ge] + K
+    rA = [g[1] for g in ge] + r
+    sA = [1] * len(ge) + sense
+    JA = [len(ge) + j for j in J]
+    # B: the GE rows as negated LE rows
+    KB = [-g[0] for g in ge] + K
+    rB = [-g[1] for g in ge] + r
+    sB = [-1] * len(ge) + sense
+    from tests.util import inst_from_dense
+    return inst_from_dense(KA, rA, sA, c), inst_from_dense(KB, rB, sB, c), JA, I
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_host_k_download_matches_host_copy(gf, seed):
+    """Host-side consumers see the same canonical K whether the load copied it (non-canonical input)
+    or downloads it on demand (canonical input): the TU-reduced problems evaluate bit-identically."""
+    A, B, J, I = _canonical_pair(seed)
+    res = []
+    for inst in (A, B):
+        s = gf.Solver(0)
+        s.load(inst)
+        s.tu_reformulate(J, I)
+        s.preprocess(precision=64)
+        p = G.p_vectors(s.n, 3)["unif"]
+        bits = O.sample(p, 5, 1, 0, 2)
+        res.append((s.n, s.m) + s.eval(bits))
+        s.close()
+    assert res[0][:2] == res[1][:2]
+    assert np.array_equal(res[0][2], res[1][2]) and np.array_equal(res[0][3], res[1][3])
