@@ -16,6 +16,7 @@
 #include <chrono>
 #include <climits>
 #include <map>
+#include <tuple>
 #include <mutex>
 #include <thread>
 #include <cub/cub.cuh>
@@ -346,6 +347,29 @@ static void smem_attr(const void* fn, size_t bytes) {
     if (bytes <= cur) return;
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     cur = bytes;
+}
+// one wave: the grid of a grid-stride kernel capped at its resident CTAs (occupancy x SMs), so no CTA
+// waits for a second wave — which matters most when the kernel's mode is switched off on the device
+// and every CTA only reads the mode and exits
+static int fit_grid(const void* fn, long long want, int block, size_t smem = 0) {
+    static std::mutex mu;
+    static std::map<std::tuple<const void*, int, int, size_t>, int> occ;
+    int dev = 0, sms = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    int per = 0;
+    {
+        std::lock_guard<std::mutex> g(mu);
+        auto it = occ.find({fn, dev, block, smem});
+        if (it != occ.end()) per = it->second;
+    }
+    if (!per) {
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, block, smem));
+        per = std::max(per, 1);
+        std::lock_guard<std::mutex> g(mu);
+        occ[{fn, dev, block, smem}] = per;
+    }
+    return (int)std::max<long long>(1, std::min<long long>(want, (long long)sms * per));
 }
 static void set_max_dyn_smem(const void* fn) {
     cudaFuncAttributes a;
@@ -1099,8 +1123,8 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
             if (C->push_dual) {
                 // sparse xbar: scatter the listed columns into the row accumulators, then the rows
                 auto push = [&](cudaStream_t q) {
-                    LAUNCH(C, q, KC_DUAL_PUSH, (k_push_scatter<T><<<grid_for(C->n), NT, 0, q>>>(csr_Kt(C), pl, st, ctrl, kint, j)));
-                    LAUNCH(C, q, KC_DUAL_PUSH, (k_push_rows<T><<<grid_for(C->m), NT, 0, q>>>(C->m, pl, st, g, rh, C->d_rsign, C->m1p,
+                    LAUNCH(C, q, KC_DUAL_PUSH, (k_push_scatter<T><<<fit_grid((const void*)k_push_scatter<T>, grid_for(C->n), NT), NT, 0, q>>>(csr_Kt(C), pl, st, ctrl, kint, j)));
+                    LAUNCH(C, q, KC_DUAL_PUSH, (k_push_rows<T><<<fit_grid((const void*)k_push_rows<T>, grid_for(C->m), NT), NT, 0, q>>>(C->m, pl, st, g, rh, C->d_rsign, C->m1p,
                                                                                       ctrl, kint, j, u_out)));
                 };
                 branch(C, s, [&](cudaStream_t q, cudaGraphConditionalHandle h, int a, int b) {
@@ -1154,15 +1178,19 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
                 });
             }
         } else if (C->pp.rb) {
-            const int grid = (int)std::min<long long>(C->pp.nblk, RB_GRID);
+            const long long want = std::min<long long>(C->pp.nblk, RB_GRID);
             if (C->hasq) {
-                KIND_SWITCH(tkind, LAUNCH(C, q, KC_PRIMAL,
-                    (k_primal_rb<T, KINDV, true><<<grid, RB_NT, 0, q>>>(csr_Kt(C), C->pp.blk_row, C->pp.nblk, Q, qs, st, cs,
-                                                                        ctrl, kint, j, pl, ppr))));
+                KIND_SWITCH(tkind, {
+                    const int grid = fit_grid((const void*)k_primal_rb<T, KINDV, true>, want, RB_NT);
+                    LAUNCH(C, q, KC_PRIMAL, (k_primal_rb<T, KINDV, true><<<grid, RB_NT, 0, q>>>(csr_Kt(C), C->pp.blk_row,
+                        C->pp.nblk, Q, qs, st, cs, ctrl, kint, j, pl, ppr)));
+                });
             } else {
-                KIND_SWITCH(tkind, LAUNCH(C, q, KC_PRIMAL,
-                    (k_primal_rb<T, KINDV, false><<<grid, RB_NT, 0, q>>>(csr_Kt(C), C->pp.blk_row, C->pp.nblk, Q, qs, st, cs,
-                                                                         ctrl, kint, j, pl, ppr))));
+                KIND_SWITCH(tkind, {
+                    const int grid = fit_grid((const void*)k_primal_rb<T, KINDV, false>, want, RB_NT);
+                    LAUNCH(C, q, KC_PRIMAL, (k_primal_rb<T, KINDV, false><<<grid, RB_NT, 0, q>>>(csr_Kt(C), C->pp.blk_row,
+                        C->pp.nblk, Q, qs, st, cs, ctrl, kint, j, pl, ppr)));
+                });
             }
         } else if (!C->pp.seg) {
             const int grid = grid_for(C->n * (long long)C->pp.sub);
@@ -1192,7 +1220,7 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
         LAUNCH(C, s, KC_PRIMAL_PUSH, (k_wlist<T><<<(int)std::min<long long>((C->m + 255) / 256, NUM_SMS_B200 * 4LL), NT, 0, s>>>(
                                           st, ppr, ctrl, kint, j)));
         auto push = [&](cudaStream_t q) {
-            LAUNCH(C, q, KC_PRIMAL_PUSH, (k_push_scatter_cols<T><<<grid_for(C->m * 32LL), NT, 0, q>>>(csr_K(C), ppr, st, ctrl, kint, j)));
+            LAUNCH(C, q, KC_PRIMAL_PUSH, (k_push_scatter_cols<T><<<fit_grid((const void*)k_push_scatter_cols<T>, grid_for(C->m * 32LL), NT), NT, 0, q>>>(csr_K(C), ppr, st, ctrl, kint, j)));
             if (C->hasq)
                 LAUNCH(C, q, KC_PRIMAL_COL, (k_primal_push<T, true><<<pp_grid<T>(C->n), NT, 0, q>>>(C->n, ppr, Q, qs, st, cs, ctrl, kint, j, pl,
                     csr_Kt(C), trig_push ? C->d_accv : nullptr, C->d_ones_cnt, C->d_trig_flag)));

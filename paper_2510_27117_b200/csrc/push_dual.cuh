@@ -21,9 +21,8 @@ namespace gfors {
 template <typename T>
 __global__ void __launch_bounds__(256) k_push_scatter(Csr Kt, PushList pl, State<T> s, const Ctrl* __restrict__ ctrl,
                                                       long long kint, long long j) {
-    const long long kk = iter_index(ctrl, kint, j);
-    const int par = (int)(kk & 1);
-    if (!push_mode(pl, par)) return;
+    const int par = cta_parity(ctrl, kint, j);
+    if (!cta_push_mode(pl, par)) return;
     const bool delta = pl_valid(pl, par);
     const T* __restrict__ xb = par ? s.xb[1] : s.xb[0];      // xbar_{k-1}
     const T* __restrict__ xbp = par ? s.xb[0] : s.xb[1];     // xbar_{k-2} (delta push only)
@@ -68,9 +67,8 @@ __global__ void __launch_bounds__(256) k_push_rows(long long m, PushList pl, Sta
                                                    const double* __restrict__ rh, const signed char* __restrict__ rsign,
                                                    long long m1, const Ctrl* __restrict__ ctrl, long long kint, long long j,
                                                    double* __restrict__ u_out) {
-    const long long kk = iter_index(ctrl, kint, j);
-    const int par = (int)(kk & 1);
-    if (!push_mode(pl, par)) return;
+    const int par = cta_parity(ctrl, kint, j);
+    if (!cta_push_mode(pl, par)) return;
     if (blockIdx.x == 0 && threadIdx.x == 0) { push_reset_next(pl, par); pl_set_valid(pl, par ^ 1, true); }
     const T* __restrict__ yin = par ? s.y[1] : s.y[0];
     T* __restrict__ yout = par ? s.y[0] : s.y[1];

@@ -55,6 +55,22 @@ __device__ __forceinline__ void push_reset_next(const PushList& pl, int par) {
 __device__ __forceinline__ bool push_mode(const PushList& pl, int par) {
     return pl.acc != nullptr && *(volatile unsigned*)pl_count(pl, par) <= pl.thr;
 }
+// iteration parity and the dual's mode read ONCE per CTA (thread 0) and broadcast through shared
+// memory: when every thread read the same control words, a launch whose mode is switched off (all
+// CTAs only read and exit) took ~8 us of same-address L2 requests.  Call at the top of the kernel
+// (contains __syncthreads).
+__device__ __forceinline__ int cta_parity(const Ctrl* ctrl, long long kint, long long j) {
+    __shared__ int s_par;
+    if (threadIdx.x == 0) s_par = (int)(((kint ? ctrl->blk * kint : 0) + j) & 1);
+    __syncthreads();
+    return s_par;
+}
+__device__ __forceinline__ bool cta_push_mode(const PushList& pl, int par) {
+    __shared__ int s_push;
+    if (threadIdx.x == 0) s_push = push_mode(pl, par) ? 1 : 0;
+    __syncthreads();
+    return s_push != 0;
+}
 
 // block-staged append of the pass's nonzero columns (one global atomic per CTA pass); enabled is
 // block-uniform.  s_list holds at most one entry per thread.
@@ -128,6 +144,13 @@ __device__ __forceinline__ PPMode pp_mode(const PushPrimal& pp, int par) {
         r.push = cnt <= pp.rthr;
     }
     return r;
+}
+// pp_mode read once per CTA (see cta_push_mode)
+__device__ __forceinline__ PPMode cta_pp_mode(const PushPrimal& pp, int par) {
+    __shared__ PPMode s_md;
+    if (threadIdx.x == 0) s_md = pp_mode(pp, par);
+    __syncthreads();
+    return s_md;
 }
 
 // the delta scatter of this iteration marks touched columns (xst = 0), so the push primal may skip

@@ -69,8 +69,8 @@ __global__ void __launch_bounds__(256) k_wlist(State<T> s, PushPrimal pp, const 
 template <typename T>
 __global__ void __launch_bounds__(256) k_push_scatter_cols(Csr K, PushPrimal pp, State<T> s, const Ctrl* __restrict__ ctrl,
                                                            long long kint, long long jj) {
-    const int par = (int)(iter_index(ctrl, kint, jj) & 1);
-    const PPMode md = pp_mode(pp, par);
+    const int par = cta_parity(ctrl, kint, jj);
+    const PPMode md = cta_pp_mode(pp, par);
     if (!md.push) return;
     const bool mark = pp_marking(pp, md);
     const double S = pow2(md.e);
@@ -154,9 +154,8 @@ __global__ void __launch_bounds__(256, OCC) k_primal_push(long long n, PushPrima
     __shared__ unsigned s_cnt, s_base;
     __shared__ int s_list[PP_LPASSES * 256 * PP_U];
     __shared__ bool s_en;
-    const long long kk = iter_index(ctrl, kint, j);
-    const int par = (int)(kk & 1);
-    const PPMode md = pp_mode(pp, par);
+    const int par = cta_parity(ctrl, kint, j);
+    const PPMode md = cta_pp_mode(pp, par);
     if (!md.push) return;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         // trigger iteration: also push x_k into the row accumulators of the indicator pass (k_trig_rows_push).
@@ -311,9 +310,11 @@ __global__ void __launch_bounds__(256) k_trig_rows_push(long long m, State<T> s,
                                                         unsigned char* __restrict__ ones_out, long long* __restrict__ accv,
                                                         unsigned* __restrict__ ones_cnt, unsigned* __restrict__ trig_flag) {
     __shared__ double sh[32];
-    if (*(volatile unsigned*)trig_flag == 0u) return;
-    const long long kk = iter_index(ctrl, kint, j);
-    const int par = (int)(kk & 1);
+    __shared__ int s_on;  // (read once per CTA, see cta_push_mode)
+    if (threadIdx.x == 0) s_on = *(volatile unsigned*)trig_flag != 0u;
+    __syncthreads();
+    if (!s_on) return;
+    const int par = cta_parity(ctrl, kint, j);
     const T* __restrict__ yprev = par ? s.y[1] : s.y[0];
     const T* __restrict__ ynew = par ? s.y[0] : s.y[1];
     const double tau2 = ctrl->tau2;

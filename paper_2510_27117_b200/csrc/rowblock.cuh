@@ -153,9 +153,8 @@ __global__ void __launch_bounds__(RB_NT, 8) k_dual_rb(Csr K, const int4* __restr
     constexpr int NZ = RB_NNZ_OF<T>;
     constexpr int U = NZ / RB_NT;
     __shared__ __align__(16) DualBuf<T> buf[2];
-    const long long kk = iter_index(ctrl, kint, j);
-    const int par = (int)(kk & 1);
-    if (push_mode(pl, par)) return;  // sparse xbar: k_push_scatter/k_push_rows do this iteration
+    const int par = cta_parity(ctrl, kint, j);
+    if (cta_push_mode(pl, par)) return;  // sparse xbar: k_push_scatter/k_push_rows do this iteration
     const bool clear_acc = pl.acc && pl_valid(pl, par);
     if (pl.acc && blockIdx.x == 0 && threadIdx.x == 0) { push_reset_next(pl, par); pl_set_valid(pl, par ^ 1, false); }
     const T* __restrict__ xb = par ? s.xb[1] : s.xb[0];
@@ -253,9 +252,8 @@ __global__ void __launch_bounds__(RB_NT, 6) k_primal_rb(Csr Kt, const long long*
     __shared__ unsigned s_cnt, s_base;
     __shared__ int s_list[RB_NT];
     __shared__ bool s_en, s_dd;
-    const long long kk = iter_index(ctrl, kint, j);
-    const int par = (int)(kk & 1);
-    if (pp_mode(pp, par).push) return;  // push-mode primal runs instead
+    const int par = cta_parity(ctrl, kint, j);
+    if (cta_pp_mode(pp, par).push) return;  // push-mode primal runs instead
     const bool clear_accx = pp_valid(pp, par);  // delta-push accumulators are stale after a gather
     if (pp.accx && blockIdx.x == 0 && threadIdx.x == 0) pp_set_next(pp, par, false, 0);
     const T* __restrict__ xin = par ? s.x[1] : s.x[0];
@@ -336,9 +334,11 @@ __global__ void __launch_bounds__(RB_NT) k_trig_rows_rb(Csr K, const long long* 
     constexpr int NZ = RB_NNZ_OF<T>;
     __shared__ __align__(16) T sv[2][NZ];
     __shared__ double sh[32];
-    if (trig_flag && *(volatile const unsigned*)trig_flag) return;  // x_k was pushed: k_trig_rows_push
-    const long long kk = iter_index(ctrl, kint, j);
-    const int par = (int)(kk & 1);
+    __shared__ int s_skip;  // (read once per CTA, see cta_push_mode)
+    if (threadIdx.x == 0) s_skip = (trig_flag && *(volatile const unsigned*)trig_flag) ? 1 : 0;
+    __syncthreads();
+    if (s_skip) return;  // x_k was pushed: k_trig_rows_push
+    const int par = cta_parity(ctrl, kint, j);
     const T* __restrict__ xk = par ? s.x[0] : s.x[1];
     const T* __restrict__ yprev = par ? s.y[1] : s.y[0];
     const T* __restrict__ ynew = par ? s.y[0] : s.y[1];
