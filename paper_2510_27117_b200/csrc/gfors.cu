@@ -1246,7 +1246,9 @@ void enqueue_trigger(gfors_ctx* C, cudaStream_t s, long long kint, long long j) 
     const double* rh = (const double*)C->d_rh;
     if (C->m > 0) {
         if (C->pd.rb) {
-            const int grid = (int)std::min<long long>(C->pd.nblk, (long long)C->nb1);
+            int grid = 1;
+            KIND_SWITCH(C->kkind, grid = fit_grid((const void*)k_trig_rows_rb<T, KINDV>,
+                                                  std::min<long long>(C->pd.nblk, (long long)C->nb1), RB_NT));
             auto gather = [&](cudaStream_t q) {
                 KIND_SWITCH(C->kkind, LAUNCH(C, q, KC_TRIGR,
                     (k_trig_rows_rb<T, KINDV><<<grid, RB_NT, 0, q>>>(csr_K(C), C->pd.blk_row, C->pd.nblk, st, g, rh,
