@@ -56,6 +56,14 @@ typedef struct {
      * record written straight into the gathered slots — then the same merge, winner regeneration and
      * halt agreement as the NCCL path; the result equals one rank with k_b*world. */
     int32_t loopback;
+    /* Optional device allocator, e.g. torch's caching allocator: alloc(bytes, alloc_ctx)
+     * returns device memory of `device` usable on `stream` (NULL = out of memory -> GFORS_E_OOM), free(p,
+     * alloc_ctx) takes back what alloc returned.  Every device buffer of this context then comes from it,
+     * allocated and freed inside this context's API calls (gfors_destroy included).  NULL: the library's
+     * private stream-ordered pool. */
+    void *(*alloc)(size_t bytes, void *alloc_ctx);
+    void (*free)(void *p, void *alloc_ctx);
+    void *alloc_ctx;
 } gfors_device_opts;
 
 /* Problem in USER form.  CSR K (m x n): k_rowptr[m+1] (nondecreasing, [0]=0),

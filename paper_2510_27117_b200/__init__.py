@@ -39,8 +39,32 @@ class GforsError(RuntimeError):
         self.code = code
 
 
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)
+FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p)
+
+
 class DeviceOpts(C.Structure):
-    _fields_ = [("device", I32), ("stream", P), ("rank", I32), ("world", I32), ("nccl_id", P), ("loopback", I32)]
+    _fields_ = [("device", I32), ("stream", P), ("rank", I32), ("world", I32), ("nccl_id", P), ("loopback", I32),
+                ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_ctx", P)]
+
+
+def torch_allocator(device: int, stream=None):
+    """(alloc, free) callbacks for gfors_device_opts backed by torch's caching allocator (the
+    library's device buffers then show up in torch.cuda.memory_allocated and are reused by torch after
+    the solver closes).  stream: the cudaStream_t the solver runs on (None: torch's current stream)."""
+    import torch
+
+    def _alloc(nbytes, _ctx):
+        try:
+            st = stream if stream is not None else torch.cuda.current_stream(device).cuda_stream
+            return torch.cuda.caching_allocator_alloc(int(nbytes), device, st)
+        except Exception:  # noqa: BLE001  (out of memory -> NULL -> GFORS_E_OOM)
+            return None
+
+    def _free(ptr, _ctx):
+        torch.cuda.caching_allocator_delete(ptr)
+
+    return ALLOC_FN(_alloc), FREE_FN(_free)
 
 
 class Problem(C.Structure):
@@ -161,10 +185,19 @@ class Solver:
     nccl_unique_id(), identical on all ranks) enables the in-loop incumbent exchange."""
 
     def __init__(self, device: int = 0, stream=None, rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
-                 loopback: bool = False, options: dict | None = None):
+                 loopback: bool = False, options: dict | None = None, allocator=None):
+        """allocator: None (the library's private pool), "torch" (torch's caching allocator) or an
+        (alloc, free) pair of ALLOC_FN / FREE_FN callbacks."""
         self._nccl_buf = (C.c_char * 128).from_buffer_copy(nccl_id) if nccl_id else None
+        if allocator == "torch":
+            import torch
+            if not stream:  # the solver's stream and the allocator's must agree (stream-ordered reuse)
+                stream = torch.cuda.current_stream(device).cuda_stream
+            allocator = torch_allocator(device, stream)
+        self._alloc_cb = allocator  # the callbacks must outlive the context
         opts = DeviceOpts(device, P(stream) if stream else None, rank, world,
-                          C.cast(self._nccl_buf, P) if nccl_id else None, int(bool(loopback)))
+                          C.cast(self._nccl_buf, P) if nccl_id else None, int(bool(loopback)),
+                          allocator[0] if allocator else ALLOC_FN(), allocator[1] if allocator else FREE_FN(), None)
         h = P()
         rc = _lib.gfors_create(C.byref(h), C.byref(opts))
         if rc != 0:

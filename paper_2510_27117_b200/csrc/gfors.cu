@@ -78,6 +78,19 @@ struct Err {
 // config-5 load varies 42-300 ms with plain cudaMalloc/cudaFree).  Allocation and free run on a
 // private non-blocking stream and are made synchronous (allocate + sync; device sync + free), so
 // the semantics are those of cudaMalloc/cudaFree for every caller stream.
+// optional caller allocator of the context whose API call runs on this thread (gfors_device_opts)
+struct AllocHooks {
+    void* (*alloc)(size_t, void*) = nullptr;
+    void (*free)(void*, void*) = nullptr;
+    void* ctx = nullptr;
+};
+static thread_local AllocHooks tls_hooks;
+struct HookScope {  // installs a context's hooks for the duration of one API call
+    AllocHooks prev;
+    explicit HookScope(const AllocHooks& h) : prev(tls_hooks) { tls_hooks = h; }
+    ~HookScope() { tls_hooks = prev; }
+};
+
 static cudaMemPool_t& pool_of(int dev) {
     static cudaMemPool_t pools[64] = {};
     return pools[dev];
@@ -123,6 +136,11 @@ template <typename X>
 X* dalloc(size_t count) {
     if (count == 0) count = 1;
     void* p = nullptr;
+    if (tls_hooks.alloc) {
+        p = tls_hooks.alloc(count * sizeof(X), tls_hooks.ctx);
+        if (!p) throw Err{GFORS_E_OOM, "device_opts.alloc returned NULL"};
+        return reinterpret_cast<X*>(p);
+    }
     cudaStream_t as = alloc_stream();
     if (as) {
         int dev = 0;
@@ -483,6 +501,7 @@ struct gfors_ctx {
     long long n = 0, m = 0, m1 = 0, m2 = 0, nnz = 0, qnnz = 0;
     long long m1p = 0;      // rows [0,m1p) are inequalities for the PDHG step (m under the relaxation, R26)
     bool repair = false;    // repair lanes before EvalBest (repair.cuh)
+    AllocHooks hooks;          // optional caller allocator (device_opts.alloc/free)
     bool kcan_pinned = false;  // d_kcol was uploaded straight from the caller's pinned K columns (load)
     bool complete = false;  // cover completion before EvalBest (cover.cuh)
     int* d_cover_rows = nullptr;      // eligible covering rows (prep-owned, built on first use)
@@ -736,6 +755,7 @@ struct gfors_ctx {
 // the free is ordered on the allocation stream before any later allocation from the pool.
 static void dfree(void* p) {
     if (!p) return;
+    if (tls_hooks.free) { tls_hooks.free(p, tls_hooks.ctx); return; }
     cudaStream_t as = alloc_stream();
     if (as) cudaFreeAsync(p, as); else cudaFree(p);
 }
@@ -2154,6 +2174,7 @@ static void do_run_t(gfors_ctx* C, const gfors_params* p, gfors_run_info* out) {
 // =============================================================================================
 #define API_BEGIN(C)                                 \
     if (!(C)) return GFORS_E_STATE;                  \
+    HookScope hook_scope_((C)->hooks);               \
     try {                                            \
         cudaSetDevice((C)->device);
 #define API_END(C)                                   \
@@ -2216,6 +2237,9 @@ gfors_status gfors_create(gfors_ctx** out, const gfors_device_opts* opts) {
     auto* C = new gfors_ctx();
     try {
         if (opts) { C->device = opts->device; C->rank = opts->rank; C->world = opts->world; }
+        if (opts && (!!opts->alloc != !!opts->free)) input_error("device_opts: alloc and free go together");
+        if (opts && opts->alloc) C->hooks = AllocHooks{opts->alloc, opts->free, opts->alloc_ctx};
+        HookScope hs(C->hooks);
         if (C->world < 1 || C->rank < 0 || C->rank >= C->world) input_error("device_opts: need 0 <= rank < world");
         if (opts && opts->loopback) {
             if (opts->nccl_id || C->rank != 0) input_error("device_opts.loopback: needs rank = 0 and nccl_id = NULL");
@@ -2349,7 +2373,11 @@ gfors_status gfors_best_incumbent(gfors_ctx* C, double* z, uint8_t* x, gfors_inc
 
 const char* gfors_last_error(const gfors_ctx* C) { return C ? C->err.c_str() : "null context"; }
 
-void gfors_destroy(gfors_ctx* C) { delete C; }
+void gfors_destroy(gfors_ctx* C) {
+    if (!C) return;
+    HookScope hs(C->hooks);  // the context's buffers go back to the allocator they came from
+    delete C;
+}
 
 gfors_status gfors_get_scaled(gfors_ctx* C, double* row_scale, double* r_scaled, double* c_scaled) {
     API_BEGIN(C)
