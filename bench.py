@@ -776,27 +776,29 @@ def run_gpu(args):
                 h2d += v.nbytes
             else:
                 host[k] = v
-        s2 = gf.Solver(local, stream=stream.cuda_stream, rank=rank, world=world,
-                       nccl_id=fresh_nccl_id() if world > 1 else None)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        s2.load(host)
-        ta = time.perf_counter()
-        s2.preprocess(precision=args.precision)
-        tb = time.perf_counter()
-        s2.run(max_iters=args.steps * args.k_int, **common)
-        tc = time.perf_counter()
-        z2, x2, _ = s2.best_incumbent()
-        torch.cuda.synchronize()
-        te = time.perf_counter() - t0
-        s2.close()
-        e2e_split = {"load_s": ta - t0, "preprocess_s": tb - ta, "run_s": tc - tb, "best_incumbent_s": t0 + te - tc}
+        reps = []
+        for _rep in range(3):  # three independent call chains; the median one is reported (host-side load varies)
+            s2 = gf.Solver(local, stream=stream.cuda_stream, rank=rank, world=world,
+                           nccl_id=fresh_nccl_id() if world > 1 else None)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            s2.load(host)
+            ta = time.perf_counter()
+            s2.preprocess(precision=args.precision)
+            tb = time.perf_counter()
+            s2.run(max_iters=args.steps * args.k_int, **common)
+            tc = time.perf_counter()
+            z2, x2, _ = s2.best_incumbent()
+            torch.cuda.synchronize()
+            te = time.perf_counter() - t0
+            s2.close()
+            reps.append((te, {"load_s": ta - t0, "preprocess_s": tb - ta, "run_s": tc - tb, "best_incumbent_s": t0 + te - tc}))
+        te, e2e_split = sorted(reps, key=lambda r: r[0])[1]
         e2e = {"value": args.steps * args.k_b * world / te, "unit": UNIT, "h2d_bytes_per_step": h2d / args.steps,
                "d2h_bytes_per_step": (meta["n"] + 64) / args.steps,
-               "note": "one gfors_load+preprocess+run(K blocks)+best_incumbent call chain from pinned host memory; "
-                       "instance bytes amortised over the K steps; the device leg before it is its warm-up (the library's "
-                       "device memory pool keeps the memory the closed solver released)", "seconds": te,
-               "split_s": e2e_split}
+               "note": "one gfors_load+preprocess+run(K blocks)+best_incumbent call chain from pinned host memory, "
+                       "a fresh solver each time; instance bytes amortised over the K steps; median of 3 chains",
+               "seconds": te, "split_s": e2e_split, "chains_s": [r[0] for r in reps]}
 
     # time-to-incumbent (BASELINE metric, third part): full solves of the small configs with the
     # default halting rule, %globaltimer stamp of the last improvement (Preprocess excluded)
