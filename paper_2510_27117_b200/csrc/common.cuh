@@ -3,10 +3,24 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <atomic>
 
 namespace gfors {
 
-constexpr int NUM_SMS_B200 = 148;  // B200 SM count: grids are sized in multiples of it
+constexpr int NUM_SMS_B200 = 148;  // B200 SM count (fallback only: grids use sm_count())
+
+// SM count of the current device, queried once per device: grids are sized in multiples of it
+inline int sm_count() {
+    static std::atomic<int> cache[64];
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= 64) return NUM_SMS_B200;
+    int v = cache[d].load(std::memory_order_relaxed);
+    if (!v) {
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d) != cudaSuccess || v <= 0) v = NUM_SMS_B200;
+        cache[d].store(v, std::memory_order_relaxed);
+    }
+    return v;
+}
 
 
 // Storage class of a sparse matrix's values (chosen at load).

@@ -48,7 +48,7 @@ using namespace gfors;
 namespace {
 
 constexpr int NT = 256;
-constexpr int RB_GRID = NUM_SMS_B200 * 8;
+inline int rb_grid() { return sm_count() * 8; }  // persistent row-block kernels: 8 CTAs per SM
 
 struct Err {
     gfors_status st;
@@ -181,7 +181,7 @@ X* dupload(const std::vector<X, Al>& v, cudaStream_t s) {
 int grid_for(long long work, int per_thread = 1) {
     long long b = (work / per_thread + NT - 1) / NT;
     if (b < 1) b = 1;
-    if (b > NUM_SMS_B200 * 8) b = NUM_SMS_B200 * 8;
+    if (b > sm_count() * 8) b = sm_count() * 8;
     return (int)b;
 }
 
@@ -288,7 +288,7 @@ DirPlan plan_direction(const std::vector<int64_t>& ptr, long long rows, cudaStre
     d.sub = pick_sub(mean);
     // long or few rows: fixed-length segments, one warp each (>= 8 warps per SM of work)
     const long long groups = rows;
-    d.seg = (maxlen > 4096) || (groups * 32 < (long long)NUM_SMS_B200 * 2048 && nnz > (long long)NUM_SMS_B200 * 1024);
+    d.seg = (maxlen > 4096) || (groups * 32 < (long long)sm_count() * 2048 && nnz > (long long)sm_count() * 1024);
     if (maxlen <= RB_NNZ32) {
         d.seg = false;
         d.rb = true;
@@ -306,7 +306,7 @@ DirPlan plan_direction(const std::vector<int64_t>& ptr, long long rows, cudaStre
     }
     if (d.seg) {
         long long L = 1024;
-        while (L > 128 && nnz / L < (long long)NUM_SMS_B200 * 16) L /= 2;
+        while (L > 128 && nnz / L < (long long)sm_count() * 16) L /= 2;
         d.seg_len = L;
         HostSeg h = make_segments(ptr, rows, L);
         d.ds.seg_start = dupload(h.seg_start, s);
@@ -1019,7 +1019,7 @@ void enqueue_qx(gfors_ctx* C, cudaStream_t s, QxSrc<TX> src, bool diff, double o
     }
     {
         const long long units = (n + QT_ROWS - 1) / QT_ROWS * nchunk;
-        const int grid = (int)std::min<long long>(units, NUM_SMS_B200 * 2LL);
+        const int grid = (int)std::min<long long>(units, sm_count() * 2LL);
         if (diff) smem_attr((const void*)k_qx_tma<TX, true>, qt_smem_bytes());
         else smem_attr((const void*)k_qx_tma<TX, false>, qt_smem_bytes());
         if (diff)
@@ -1120,7 +1120,7 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
     const double* rh = (const double*)C->d_rh;
     if (C->m > 0) {
         if (C->pd.rb) {
-            const int grid = (int)std::min<long long>(C->pd.nblk, RB_GRID);
+            const int grid = (int)std::min<long long>(C->pd.nblk, rb_grid());
             double* u_out = (kint == 0 || j == kint - 1) ? C->d_u : nullptr;
             auto gather = [&](cudaStream_t q) {
                 if (!C->rs_on) {
@@ -1134,7 +1134,7 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
                     if (!C->loopback && r != C->rank) continue;
                     const long long b0 = C->rs_blo[r], nb = C->rs_blo[r + 1] - b0;
                     if (nb <= 0) continue;
-                    const int gr = (int)std::min<long long>(nb, RB_GRID);
+                    const int gr = (int)std::min<long long>(nb, rb_grid());
                     KIND_SWITCH(C->kkind, LAUNCH(C, q, KC_DUAL,
                         (k_dual_rb<T, KINDV><<<gr, RB_NT, 0, q>>>(csr_K(C), C->pd.desc + b0, C->pd.ptr32, nb, st, g, rh,
                                                                   C->d_rsign, C->m1p, ctrl, kint, j, u_out, pl))));
@@ -1183,7 +1183,7 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
             const long long nwords = (C->m + 31) / 32;
             LAUNCH(C, q, KC_PRIMAL, (k_nzmask<T><<<grid_for(nwords * 32), NT, 0, q>>>(st.w, C->m, C->d_nzbits)));
             const size_t sm = sparse_primal_smem<T>(C->m);
-            const int grid = (int)std::min<long long>(C->sp_nblk, NUM_SMS_B200);
+            const int grid = (int)std::min<long long>(C->sp_nblk, (long long)sm_count());
             if (C->hasq) {
                 KIND_SWITCH(tkind, {
                     set_max_dyn_smem((const void*)k_primal_sparse<T, KINDV, true>);
@@ -1198,7 +1198,7 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
                 });
             }
         } else if (C->pp.rb) {
-            const long long want = std::min<long long>(C->pp.nblk, RB_GRID);
+            const long long want = std::min<long long>(C->pp.nblk, rb_grid());
             if (C->hasq) {
                 KIND_SWITCH(tkind, {
                     const int grid = fit_grid((const void*)k_primal_rb<T, KINDV, true>, want, RB_NT);
@@ -1237,7 +1237,7 @@ void enqueue_iter(gfors_ctx* C, cudaStream_t s, long long kint, long long j) {
     };
     if (C->push_primal) {
         // list the active duals (or the changed ones); the push kernels run iff the list is short
-        LAUNCH(C, s, KC_PRIMAL_PUSH, (k_wlist<T><<<(int)std::min<long long>((C->m + 255) / 256, NUM_SMS_B200 * 4LL), NT, 0, s>>>(
+        LAUNCH(C, s, KC_PRIMAL_PUSH, (k_wlist<T><<<(int)std::min<long long>((C->m + 255) / 256, sm_count() * 4LL), NT, 0, s>>>(
                                           st, ppr, ctrl, kint, j)));
         auto push = [&](cudaStream_t q) {
             LAUNCH(C, q, KC_PRIMAL_PUSH, (k_push_scatter_cols<T><<<fit_grid((const void*)k_push_scatter_cols<T>, grid_for(C->m * 32LL), NT), NT, 0, q>>>(csr_K(C), ppr, st, ctrl, kint, j)));

@@ -142,7 +142,7 @@ template <typename T>
 inline int pp_grid(long long n, int occ = 0) {
     const long long passes = (n + 256 * PP_U - 1) / (256 * PP_U);
     if (occ <= 0) occ = sizeof(T) == 4 ? PP_OCC32 : PP_OCC64;
-    return (int)std::max<long long>(1, std::min<long long>(passes, (long long)NUM_SMS_B200 * occ));
+    return (int)std::max<long long>(1, std::min<long long>(passes, (long long)sm_count() * occ));
 }
 
 template <typename T, bool HASQ, int OCC = (sizeof(T) == 4 ? PP_OCC32 : PP_OCC64)>
