@@ -270,7 +270,8 @@ def test_run_fp32_incumbent_feasible(gf):
         assert zg <= 1.25 * zb
 
 
-@pytest.mark.parametrize("case", ["tail", "short", "kr3", "kb1024", "maximize_mis", "no_constraints", "infeasible"])
+@pytest.mark.parametrize("case", ["tail", "short", "kr3", "kb1024", "kb512", "maximize_mis", "mis_kb1024", "no_constraints",
+                                  "infeasible"])
 def test_run_edge_cases(gf, case):
     kw = dict(max_iters=203)
     inst = G.SMALL["setcover"](9)
@@ -280,9 +281,14 @@ def test_run_edge_cases(gf, case):
         kw = dict(max_iters=100, k_r=3, k_int=7)
     elif case == "kb1024":
         kw = dict(max_iters=60, k_b=1024)
+    elif case == "kb512":  # 8-word feasibility units (one-plane rows, one thread per row and word)
+        kw = dict(max_iters=60, k_b=512)
     elif case == "maximize_mis":
         inst = G.max_independent_set(300, 0.02, 3, weighted=True)
         kw = dict(max_iters=500, sigma=0.5)
+    elif case == "mis_kb1024":  # 8-word units of two-plane packing rows (per-row lane groups)
+        inst = G.max_independent_set(300, 0.02, 3, weighted=True)
+        kw = dict(max_iters=300, sigma=0.5, k_b=1024)
     elif case == "no_constraints":
         inst = inst_from_dense([], [], [], np.random.default_rng(0).integers(-5, 6, 50).astype(float))
         kw = dict(max_iters=100)
