@@ -676,7 +676,7 @@ def run_gpu(args):
             if name not in pv:
                 continue
             row = {}
-            for kb in (64, 128, 1024, 4096):
+            for kb in (64, 128, 512, 1024, 4096):
                 s.sample_eval_timed(pv[name], 20251030, kb // 64, 1)  # warm-up: first launches load the kernels
                 ms_r = s.sample_eval_timed(pv[name], 20251030, kb // 64, 10)
                 row[str(kb)] = 10 * kb / (ms_r * 1e-3)
