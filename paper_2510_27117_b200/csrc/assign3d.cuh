@@ -35,8 +35,14 @@ __global__ void __launch_bounds__(256) k_a3_keys(const T* __restrict__ xa, const
         p = (((b + 1) * kint) & 1) ? xb2 : xa;  // x_k of the block (as k_sample)
     }
     for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < N; v += gridDim.x * (long long)blockDim.x) {
-        const double pv = (pfix ? pfix[v] : (double)p[v]) + 0.0;
-        keys[v] = ~(unsigned long long)__double_as_longlong(pv);
+        if (sizeof(T) == 4 && !pfix) {
+            // fp32 x_k: the 32-bit key ~bits(float) orders exactly as the fp64 one (a float converts to
+            // double exactly and monotonically), so the sort needs half the radix passes (end_bit 32)
+            keys[v] = (unsigned long long)(~__float_as_uint((float)p[v] + 0.0f));
+        } else {
+            const double pv = (pfix ? pfix[v] : (double)p[v]) + 0.0;
+            keys[v] = ~(unsigned long long)__double_as_longlong(pv);
+        }
         vals[v] = (int)v;
     }
 }

@@ -1663,7 +1663,8 @@ void enqueue_sample_a3(gfors_ctx* C, cudaStream_t s, const double* pfix, int W, 
                                                                    C->d_ctrl, kint, use_fixed, A.keys[0], A.vals[0])));
     if (!C->dry) {
         size_t bytes = A.tmp_bytes;
-        CK(cub::DeviceRadixSort::SortPairs(A.tmp, bytes, A.keys[0], A.keys[1], A.vals[0], A.vals[1], (int)N, 0, 64, s));
+        const int end_bit = (sizeof(T) == 4 && !pfix) ? 32 : 64;  // 32-bit keys for fp32 x_k (k_a3_keys)
+        CK(cub::DeviceRadixSort::SortPairs(A.tmp, bytes, A.keys[0], A.keys[1], A.vals[0], A.vals[1], (int)N, 0, end_bit, s));
     }
     // (the CUB radix-sort kernels are library launches: not counted in gfors_run_info.launches)
     const size_t gsm = a3_greedy_smem((int)A.n);
