@@ -1792,7 +1792,13 @@ static double power_iteration(gfors_ctx* C, bool isq, double tol, int max_iter) 
         } else if (isq) {
             k_spmv_rows<KV_F64><<<gc, NT, 0, s>>>(csr_Q(C), nullptr, nullptr, w, u);
         } else {
-            KIND_SWITCH(C->kkind, (k_spmv_cols<KINDV><<<gc, NT, 0, s>>>(csr_Kt(C), C->d_rsign, C->d_s, w, u)));
+            // w' once per row, then G lanes per column (G from the mean column length)
+            const int G = pick_sub(cols ? (double)C->nnz / (double)cols : 1.0);
+            const int gcg = grid_for(cols * (long long)G);
+            KIND_SWITCH(C->kkind, {
+                k_prescale<KINDV><<<grid_for(rows), NT, 0, s>>>(w, C->d_s, C->d_rsign, rows, C->d_tmp[3]);
+                SUB_SWITCH(G, (k_spmv_cols_g<KINDV, SUBV><<<gcg, NT, 0, s>>>(csr_Kt(C), C->d_tmp[3], u)));
+            });
         }
         CK(cudaGetLastError());
         const double nu = dev_norm(C, u, cols);

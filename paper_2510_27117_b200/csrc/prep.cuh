@@ -38,6 +38,38 @@ __global__ void __launch_bounds__(256) k_spmv_rows(Csr A, const signed char* __r
     }
 }
 
+// the per-row factor of the transposed product, once per row: w'_j = (w_j / s_j) * rsign_j (the same
+// operations, in the same order, as k_spmv_cols applies per nonzero: identical terms)
+template <int KIND>
+__global__ void __launch_bounds__(256) k_prescale(const double* __restrict__ w, const double* __restrict__ rowscale,
+                                                  const signed char* __restrict__ rsign, long long m,
+                                                  double* __restrict__ out) {
+    for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < m; j += gridDim.x * (long long)blockDim.x) {
+        double wj = w[j];
+        if (rowscale) wj /= rowscale[j];
+        if (KIND == KV_SIGN && rsign) wj *= (double)rsign[j];
+        out[j] = wj;
+    }
+}
+
+// u_i = sum_j val_ji * w'_j with G lanes per column (short columns: a whole warp per column left most
+// lanes idle); every lane of the warp runs the same trip count (the shuffles need all 32)
+template <int KIND, int G>
+__global__ void __launch_bounds__(256) k_spmv_cols_g(Csr At, const double* __restrict__ wp, double* __restrict__ u) {
+    constexpr int PER = 32 / G;  // columns per warp and trip
+    const int lane = threadIdx.x & 31, sub = lane & (G - 1);
+    const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = (gridDim.x * (long long)blockDim.x) >> 5;
+    for (long long i0 = warp * PER; i0 < At.rows; i0 += nwarps * PER) {
+        const long long i = i0 + lane / G;
+        double a = 0.0;
+        if (i < At.rows)
+            for (long long p = At.ptr[i] + sub; p < At.ptr[i + 1]; p += G) a += kval<KIND>(At.val, p) * wp[At.idx[p]];
+        for (int o = G >> 1; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o, G);
+        if (sub == 0 && i < At.rows) u[i] = a;
+    }
+}
+
 // transposed product through the explicit transpose CSR: u_i = sum_j val_ji * (w_j / s_j) * rsign_j
 template <int KIND>
 __global__ void __launch_bounds__(256) k_spmv_cols(Csr At, const signed char* __restrict__ rsign,
