@@ -502,6 +502,7 @@ struct gfors_ctx {
     long long m1p = 0;      // rows [0,m1p) are inequalities for the PDHG step (m under the relaxation, R26)
     bool repair = false;    // repair lanes before EvalBest (repair.cuh)
     AllocHooks hooks;          // optional caller allocator (device_opts.alloc/free)
+    long long maxrowdeg = 0;   // longest row of K (load)
     bool kcan_pinned = false;  // d_kcol was uploaded straight from the caller's pinned K columns (load)
     bool complete = false;  // cover completion before EvalBest (cover.cuh)
     int* d_cover_rows = nullptr;      // eligible covering rows (prep-owned, built on first use)
