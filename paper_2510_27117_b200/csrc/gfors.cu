@@ -278,12 +278,17 @@ int4* upload_desc(const std::vector<long long>& b, const std::vector<int64_t>& p
     return dd;
 }
 
+// int32 copy of a row-pointer array on the device (nnz < 2^31)
+__global__ void k_ptr32(const long long* __restrict__ p64, long long len, int* __restrict__ p32) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < len; i += gridDim.x * (long long)blockDim.x)
+        p32[i] = (int)p64[i];
+}
+
+// maxlen: the longest row (precomputed by the load); dptr64: the device copy of ptr
 DirPlan plan_direction(const std::vector<int64_t>& ptr, long long rows, cudaStream_t s,
-                       std::vector<void*>& owned) {
+                       std::vector<void*>& owned, long long maxlen, const long long* dptr64) {
     DirPlan d;
     const long long nnz = ptr[rows];
-    long long maxlen = 0;
-    for (long long r = 0; r < rows; ++r) maxlen = std::max<long long>(maxlen, ptr[r + 1] - ptr[r]);
     const double mean = rows ? (double)nnz / (double)rows : 0.0;
     d.sub = pick_sub(mean);
     // long or few rows: fixed-length segments, one warp each (>= 8 warps per SM of work)
@@ -300,9 +305,10 @@ DirPlan plan_direction(const std::vector<int64_t>& ptr, long long rows, cudaStre
         owned.push_back(d.blk_row);
         d.desc = upload_desc(b, ptr, s, owned);
         d.hblk = b;
-        std::vector<int> p32(ptr.begin(), ptr.begin() + rows + 1);
-        d.ptr32 = dupload(p32, s);
+        d.ptr32 = dalloc<int>(rows + 1);
         owned.push_back(d.ptr32);
+        k_ptr32<<<grid_for(rows + 1), NT, 0, s>>>(dptr64, rows + 1, d.ptr32);
+        CK(cudaGetLastError());
     }
     if (d.seg) {
         long long L = 1024;
@@ -503,6 +509,7 @@ struct gfors_ctx {
     bool repair = false;    // repair lanes before EvalBest (repair.cuh)
     AllocHooks hooks;          // optional caller allocator (device_opts.alloc/free)
     long long maxrowdeg = 0;   // longest row of K (load)
+    long long maxcoldeg_raw = 0;  // longest column of K (load)
     bool kcan_pinned = false;  // d_kcol was uploaded straight from the caller's pinned K columns (load)
     bool complete = false;  // cover completion before EvalBest (cover.cuh)
     int* d_cover_rows = nullptr;      // eligible covering rows (prep-owned, built on first use)
