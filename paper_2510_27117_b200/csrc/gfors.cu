@@ -19,6 +19,8 @@
 #include <tuple>
 #include <mutex>
 #include <thread>
+#include <condition_variable>
+#include <functional>
 #include <cub/cub.cuh>
 #include <cstdarg>
 #include <memory>
@@ -72,12 +74,14 @@ struct Err {
     throw Err{GFORS_E_INPUT, buf};
 }
 
-// Device memory comes from the device's default stream-ordered pool with an unbounded release
-// threshold: memory a closed solver frees stays mapped in the process, so the next load reuses it
-// instead of paying cudaMalloc's page mapping again (measured: the K upload + transpose phase of a
-// config-5 load varies 42-300 ms with plain cudaMalloc/cudaFree).  Allocation and free run on a
-// private non-blocking stream and are made synchronous (allocate + sync; device sync + free), so
-// the semantics are those of cudaMalloc/cudaFree for every caller stream.
+// Device memory comes from a PRIVATE stream-ordered pool per device (the device's default pool,
+// which other libraries share, is left untouched) with an unbounded release threshold: memory a
+// closed solver frees stays mapped while other solvers live, so the next load reuses it instead of
+// paying the page mapping again (measured: the K upload + transpose phase of a config-5 load varies
+// 42-300 ms with plain cudaMalloc/cudaFree); after the last solver it is trimmed to POOL_KEEP.
+// Allocation runs on a private non-blocking stream and is made synchronous (allocate + sync); frees
+// are stream-ordered on that stream after the owning context's stream is drained.  A caller
+// allocator (gfors_device_opts.alloc/free) replaces all of this for its context.
 // optional caller allocator of the context whose API call runs on this thread (gfors_device_opts)
 struct AllocHooks {
     void* (*alloc)(size_t, void*) = nullptr;
@@ -127,9 +131,12 @@ static int live_contexts(int dev, int delta) {
     return live[dev];
 }
 
-// after the last context of a device is destroyed its pool returns the memory to the system
+// after the last context of a device is destroyed its pool returns the memory above POOL_KEEP to the
+// system; up to POOL_KEEP stays mapped for the next solver of the process (re-mapping a config-5
+// solver's ~3 GB made its load take 0.13-1.05 s instead of 0.13 s)
+constexpr size_t POOL_KEEP = 4ull << 30;
 static void pool_trim(int dev) {
-    if (dev >= 0 && dev < 64 && pool_of(dev)) cudaMemPoolTrimTo(pool_of(dev), 0);
+    if (dev >= 0 && dev < 64 && pool_of(dev)) cudaMemPoolTrimTo(pool_of(dev), POOL_KEEP);
 }
 
 template <typename X>
