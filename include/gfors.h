@@ -216,6 +216,12 @@ const char *gfors_last_error(const gfors_ctx *ctx);
  * Unknown key: GFORS_E_INPUT. */
 gfors_status gfors_set_option(gfors_ctx *ctx, const char *key, int64_t value);
 void gfors_destroy(gfors_ctx *ctx);
+/* Device memory of destroyed contexts stays mapped in the library's private per-device pool, so the
+ * next context of the process reuses it without the driver's page mapping.  This
+ * returns the pool's memory on `device` to the system; GFORS_E_STATE while a context of the device is
+ * alive, GFORS_E_INPUT for a bad device.  Contexts with a caller allocator (gfors_device_opts.alloc)
+ * do not use the pool. */
+gfors_status gfors_release_memory(int32_t device);
 
 /* ---------------- hooks for parity tests and benchmarks (same library, host buffers) ------- */
 /* Preprocess results: row scale divisors s_j (m, canonical row order), and the scaled saddle

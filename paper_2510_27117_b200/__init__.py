@@ -134,6 +134,7 @@ EXPORTS = {
     "gfors_graph_note": (C.c_char_p, [P]),
     "gfors_set_option": (I32, [P, C.c_char_p, I64]),
     "gfors_sample_eval_timed": (I32, [P, P, U64, I64, I32, P]),
+    "gfors_release_memory": (I32, [I32]),
 }
 for _name, (_res, _args) in EXPORTS.items():
     _f = getattr(_lib, _name)
@@ -153,6 +154,13 @@ def default_params(**kw) -> Params:
             raise TypeError(f"unknown parameter {k!r}")
         setattr(p, k, v)
     return p
+
+
+def release_memory(device: int = 0):
+    """gfors_release_memory: return the library pool's memory on `device` (no solver of it alive)."""
+    rc = _lib.gfors_release_memory(int(device))
+    if rc != 0:
+        raise GforsError(rc, "gfors_release_memory: a solver of the device is alive, or a bad device")
 
 
 def merge_records(z, index, valid):

@@ -78,7 +78,7 @@ struct Err {
 // which other libraries share, is left untouched) with an unbounded release threshold: memory a
 // closed solver frees stays mapped while other solvers live, so the next load reuses it instead of
 // paying the page mapping again (measured: the K upload + transpose phase of a config-5 load varies
-// 42-300 ms with plain cudaMalloc/cudaFree); after the last solver it is trimmed to POOL_KEEP.
+// 42-300 ms with plain cudaMalloc/cudaFree); gfors_release_memory trims it on request.
 // Allocation runs on a private non-blocking stream and is made synchronous (allocate + sync); frees
 // are stream-ordered on that stream after the owning context's stream is drained.  A caller
 // allocator (gfors_device_opts.alloc/free) replaces all of this for its context.
@@ -131,12 +131,14 @@ static int live_contexts(int dev, int delta) {
     return live[dev];
 }
 
-// after the last context of a device is destroyed its pool returns the memory above POOL_KEEP to the
-// system; up to POOL_KEEP stays mapped for the next solver of the process (re-mapping a config-5
-// solver's ~3 GB made its load take 0.13-1.05 s instead of 0.13 s)
-constexpr size_t POOL_KEEP = 4ull << 30;
-static void pool_trim(int dev) {
-    if (dev >= 0 && dev < 64 && pool_of(dev)) cudaMemPoolTrimTo(pool_of(dev), POOL_KEEP);
+// The private pool keeps what it has mapped when solvers close: trimming it after the last solver and
+// re-mapping for the next one made a config-5 load take 0.12-2.3 s instead of a steady 0.11 s (the
+// driver's page mapping; measured with profiles/exp_e2e.py).  gfors_release_memory(device) returns the
+// pool's unused memory to the system on request.
+static void pool_release(int dev) {
+    if (dev < 0 || dev >= 64 || !pool_of(dev)) return;
+    cudaMemPoolTrimTo(pool_of(dev), 0);
+    cudaGetLastError();
 }
 
 template <typename X>
@@ -516,6 +518,7 @@ struct gfors_ctx {
     bool repair = false;    // repair lanes before EvalBest (repair.cuh)
     AllocHooks hooks;          // optional caller allocator (device_opts.alloc/free)
     long long maxrowdeg = 0;   // longest row of K (load)
+    double* kval_dev = nullptr;  // load-time only: the caller's values copied by the device validation
     long long maxcoldeg_raw = 0;  // longest column of K (load)
     bool kcan_pinned = false;  // d_kcol was uploaded straight from the caller's pinned K columns (load)
     bool complete = false;  // cover completion before EvalBest (cover.cuh)
@@ -833,13 +836,8 @@ gfors_ctx::~gfors_ctx() {
     if (stream) cudaStreamSynchronize(stream);
     free_prep();
     free_problem();
-    // the pool keeps freed memory while other contexts of the device live (fast reloads); the last
-    // one returns it to the system
-    if (counted && live_contexts(device, -1) == 0) {
-        cudaStream_t as = alloc_stream();
-        if (as) cudaStreamSynchronize(as);
-        pool_trim(device);
-    }
+    // the pool keeps the freed memory for the next solver (gfors_release_memory returns it)
+    if (counted) live_contexts(device, -1);
     if (comm) nccl().CommDestroy(comm);
     if (cap_stream) cudaStreamDestroy(cap_stream);
     if (cap_stream2) cudaStreamDestroy(cap_stream2);
@@ -2394,6 +2392,17 @@ gfors_status gfors_best_incumbent(gfors_ctx* C, double* z, uint8_t* x, gfors_inc
 }
 
 const char* gfors_last_error(const gfors_ctx* C) { return C ? C->err.c_str() : "null context"; }
+
+gfors_status gfors_release_memory(int32_t device) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) return GFORS_E_INPUT;
+    if (cudaSetDevice(device) != cudaSuccess) return GFORS_E_CUDA;
+    if (live_contexts(device, 0) > 0) return GFORS_E_STATE;
+    cudaStream_t as = alloc_stream();
+    if (as) cudaStreamSynchronize(as);
+    pool_release(device);
+    return GFORS_OK;
+}
 
 void gfors_destroy(gfors_ctx* C) {
     if (!C) return;

@@ -14,10 +14,9 @@ from gen import instances as G  # noqa: E402
 inst = G.make_config(5, 1)
 host = {k: (torch.from_numpy(np.ascontiguousarray(v)).pin_memory().numpy() if isinstance(v, np.ndarray) else v)
         for k, v in inst.items()}
-for rep in range(4):
+for rep in range(6):
     s = gf.Solver(0)
-    if rep == 3:
-        s.set_option("load_timing", 1)
+    s.set_option("load_timing", 1)
     torch.cuda.synchronize()
     t0 = time.perf_counter(); s.load(host); torch.cuda.synchronize(); t1 = time.perf_counter()
     sc = s.preprocess(precision=32); torch.cuda.synchronize(); t2 = time.perf_counter()

@@ -51,3 +51,15 @@ def test_allocator_failure_is_oom(gf):
     with pytest.raises(gf.GforsError, match="E_OOM"):
         s.load(G.make_config(1, 1))
     s.close()
+
+
+def test_release_memory(gf):
+    """gfors_release_memory: refused while a solver of the device lives, then returns the pool's memory."""
+    s = gf.Solver(0)
+    s.load(G.make_config(1, 1))
+    with pytest.raises(gf.GforsError):
+        gf.release_memory(0)
+    s.close()
+    gf.release_memory(0)
+    with pytest.raises(gf.GforsError):
+        gf.release_memory(99)
