@@ -277,6 +277,32 @@ def scaled_instance(cfg, seed, f):
     return G.make_config(cfg, seed)
 
 
+def oracle_small_configs(seed):
+    """the oracle as it stands (1 thread) on configs 1-4 — s per PDHG iteration
+    (sampling off; 1000 iterations each) and s per candidate (sampling + EvalBest of 128 candidates around
+    the final iterate)."""
+    from oracle import oracle as O
+    out = {}
+    for cfg, iters in ((1, 1000), (2, 1000), (3, 1000), (4, 1000)):
+        inst_c = make_instance(cfg, seed)
+        o = O.Oracle(inst_c)
+        o.preprocess(max_iter=50)
+        o.state_init()
+        tau = 0.99 ** 0.5
+        t0 = time.perf_counter()
+        for _ in range(iters):
+            o.step(1e-3, tau, tau)
+        t_it = (time.perf_counter() - t0) / iters
+        x, _, _ = o.get_state()
+        t0 = time.perf_counter()
+        bits = O.sample(np.clip(x, 0.0, 1.0), 20251030, 0, 0, 2)
+        o.eval(bits)
+        t_c = (time.perf_counter() - t0) / 128
+        out[f"config{cfg}"] = {"s_per_iteration": t_it, "iterations_timed": iters, "s_per_candidate": t_c,
+                               "candidates_timed": 128}
+    return out
+
+
 def run_reference(args):
     """Reference arm: the CPU oracle as it stands, on the host cores, same metric/unit/config.
     Each step runs one real oracle Alg. 1 block (k_int PDHG iterations + k_r*k_b candidates) on a
@@ -868,7 +894,7 @@ def run_gpu(args):
         ob = oracle_baseline(inst, args.k_int)
         cpu = {"value": ob["value"], "unit": UNIT, "cores": 1, "kind": "oracle", "sample": ob["sample"],
                "ms_per_block": ob["t_block"] * 1e3, "all_host_cores": ob["all_cores"], "cpu_model": ob["cpu_model"],
-               "host_cpu_count": os.cpu_count()}
+               "host_cpu_count": os.cpu_count(), "small_configs": oracle_small_configs(args.seed)}
 
     if rank == 0:
         line = {
