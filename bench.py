@@ -680,6 +680,19 @@ def run_gpu(args):
         l = steps_ms(100)
         pdhg_only = {"iters_1_100_per_s": 100 / (d * 1e-3), "iters_1001_1100_per_s": 100 / (l * 1e-3),
                      "how": "gfors_step hook (eager launches, rho = 1e-3 fixed, no sampling), CUDA events"}
+        # graph replay: one block of k_int = 1000 iterations (the loop graph, rho schedule,
+        # trigger pass once, one sampling round of 64 candidates), from x0, median of 3 runs
+        gms = []
+        for _ in range(4):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            s.run(max_iters=1000, k_int=1000, k_b=64, tol_primal=-1.0, tol_dual=-1.0, tol_binary=-1.0, stall_rel=-1.0)
+            b.record(stream)
+            torch.cuda.synchronize()
+            gms.append(a.elapsed_time(b))
+        pdhg_only["graph_iters_1_1000_per_s"] = 1000 / (statistics.median(gms[1:]) * 1e-3)
+        pdhg_only["graph_how"] = "one gfors_run of 1000 iterations with k_int = 1000 (one trigger pass and one 64-candidate round), from x0, median of 3 after one warm-up, CUDA events"
 
     # sampling-only candidates/s: RandSampleStep + EvalBest + argmin at fixed p, no
     # PDHG, per p-distribution (x_k of the blocks 1-K trajectory, U(0,1), 90/10 exact/uniform mix)
