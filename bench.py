@@ -856,6 +856,18 @@ def run_gpu(args):
                                    "found_iter": mc["found_iter"], "iters": info_c["iters"],
                                    "halt_reason": info_c["halt_reason"], "loop_s": info_c["elapsed_s"]}
             sc_.close()
+        # config 5 (the workload) under the same SPEC halting rule: its incumbent comes from Alg. 1's final
+        # round(x_k) once the penalised PDHG has converged (found_round = -1)
+        sc_ = gf.Solver(local, stream=stream.cuda_stream)
+        sc_.load(inst)
+        sc_.preprocess(precision=args.precision)
+        info_c = sc_.run(max_iters=200000, k_b=args.k_b)
+        zc, _, mc = sc_.best_incumbent(want_x=False)
+        tti["config5"] = {"z_best": zc if mc["has_incumbent"] else None,
+                          "time_to_incumbent_s": mc["found_time_s"] if mc["has_incumbent"] else None,
+                          "found_iter": mc["found_iter"], "found_round": mc["found_round"], "iters": info_c["iters"],
+                          "halt_reason": info_c["halt_reason"], "loop_s": info_c["elapsed_s"]}
+        sc_.close()
 
     # configs 2-4: their per-iteration working sets fit in the 126 MB L2, so the PDHG
     # step is judged against the measured L2 read bandwidth as well as HBM; iterations 1-100 from x0,
@@ -915,8 +927,12 @@ def run_gpu(args):
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32" if args.precision == 32 else "f64", "data": "synthetic",
             "pdhg_iters_per_s": iters_s,
-            "time_to_incumbent_s": inc["found_time_s"] if inc["has_incumbent"] else None,
-            "z_best": z if inc["has_incumbent"] else None,
+            # time-to-incumbent / z of config 5 solved under the SPEC halting rule (the timed run above
+            # disables halting and stops after K blocks, before any incumbent)
+            "time_to_incumbent_s": (tti or {}).get("config5", {}).get("time_to_incumbent_s"),
+            "z_best": (tti or {}).get("config5", {}).get("z_best"),
+            "time_to_incumbent_how": "config 5 solved with the SPEC halting defaults (time_to_incumbent_small_configs.config5); "
+                                     "the timed K-block run itself ends before the first incumbent",
             "config": {"workload": f"config{args.config}", "desc": "set cover n=5e6 cols, m=1e6 rows, row degree U{2..98}"
                        if args.config == 5 else f"BASELINE config {args.config}",
                        "n": meta["n"], "m": meta["m"], "nnz": meta["nnz"], "k_int": args.k_int, "k_r": 1,
