@@ -78,9 +78,14 @@ __global__ void __launch_bounds__(256) k_sample_thr(const T* __restrict__ xa, co
                                                     const double* __restrict__ pfix, long long n, int W,
                                                     const Ctrl* __restrict__ ctrl, long long kint, int use_fixed,
                                                     uint2* __restrict__ list, unsigned* __restrict__ cnt,
-                                                    uint64_t* __restrict__ X) {
+                                                    uint64_t* __restrict__ X, const double* __restrict__ c_int,
+                                                    unsigned long long* __restrict__ s1) {
+    // c_int != null (integral c): s1 += sum of c_i over the variables with p_i = 1 (their words are all
+    // ones, so k_obj_list adds this constant instead of streaming them)
     constexpr int PER = 4;  // variables per thread and chunk: one list atomic per 1024 variables
     __shared__ unsigned s_off[8], s_base;
+    __shared__ long long s_one[8];
+    long long one_sum = 0;
     const T* __restrict__ p = nullptr;
     if (!use_fixed) p = (((ctrl->blk + 1) * kint) & 1) ? xb2 : xa;  // x_k written by iteration (b+1)*kint - 1
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -96,7 +101,10 @@ __global__ void __launch_bounds__(256) k_sample_thr(const T* __restrict__ xa, co
                 pi = pi < 0.0 ? 0.0 : (pi > 1.0 ? 1.0 : pi);
                 const double Td = ceil(pi * 4294967296.0);
                 if (Td <= 0.0) { for (int w = 0; w < W; ++w) X[i * W + w] = 0ull; }
-                else if (Td >= 4294967296.0) { for (int w = 0; w < W; ++w) X[i * W + w] = ~0ull; }
+                else if (Td >= 4294967296.0) {
+                    for (int w = 0; w < W; ++w) X[i * W + w] = ~0ull;
+                    if (c_int) one_sum += (long long)c_int[i];
+                }
                 else t[k] = (uint32_t)Td;
             }
             bal[k] = __ballot_sync(0xffffffffu, t[k] != 0u);
@@ -118,6 +126,16 @@ __global__ void __launch_bounds__(256) k_sample_thr(const T* __restrict__ xa, co
         }
         __syncthreads();  // s_off / s_base reused by the next chunk
     }
+    if (c_int) {  // one integer atomic per CTA (exact, order-free)
+        for (int o = 16; o > 0; o >>= 1) one_sum += __shfl_xor_sync(0xffffffffu, one_sum, o);
+        if (lane == 0) s_one[wid] = one_sum;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            long long a = 0;
+            for (int w = 0; w < 8; ++w) a += s_one[w];
+            if (a) atomicAdd(s1, (unsigned long long)a);
+        }
+    }
 }
 
 // RandSampleStep pass 2 (Alg. 3, contract R10): the MSB-first compare decides a 64-lane word after a
@@ -134,7 +152,8 @@ constexpr int SMP_CTAS = 6;  // resident CTAs per SM of k_sample (grid = SMP_CTA
 __global__ void __launch_bounds__(256, SMP_CTAS) k_sample(const uint2* __restrict__ list, unsigned* __restrict__ cnt, int W,
                                                          long long word_off, const __grid_constant__ PhiloxKeys rk,
                                                          const Ctrl* __restrict__ ctrl, int r, int kr, unsigned round_fixed,
-                                                         int use_fixed, uint64_t* __restrict__ X) {
+                                                         int use_fixed, uint64_t* __restrict__ X,
+                                                         unsigned long long* __restrict__ s1) {
     const unsigned round = use_fixed ? round_fixed : (unsigned)(ctrl->blk * kr + r);
     const uint64_t pol = l2_policy_evict_last();  // the batch is gathered by the evaluator next
     const unsigned wbase = (unsigned)word_off;
@@ -191,7 +210,13 @@ __global__ void __launch_bounds__(256, SMP_CTAS) k_sample(const uint2* __restric
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
-        if (atomicAdd(cnt + 1, 1u) == gridDim.x - 1) { cnt[0] = 0u; cnt[1] = 0u; __threadfence(); }
+        if (atomicAdd(cnt + 1, 1u) == gridDim.x - 1) {
+            // the round's list length and p = 1 constant stay readable by k_obj_list (slots 2, 3 / s1[1])
+            cnt[2] = cnt[0];
+            if (s1) { s1[1] = s1[0]; s1[0] = 0ull; }
+            cnt[0] = 0u; cnt[1] = 0u;
+            __threadfence();
+        }
     }
 }
 
@@ -539,8 +564,11 @@ __global__ void __launch_bounds__(256) k_obj_planes(const double* __restrict__ c
 template <int WV>
 __global__ void __launch_bounds__(256) k_obj_bits(long long n, long long cpc, const unsigned* __restrict__ planes,
                                                   int NB, long long cmin, const uint64_t* __restrict__ X, int W,
-                                                  long long* __restrict__ zpart /*[gridDim.x][64W]*/) {
+                                                  long long* __restrict__ zpart /*[gridDim.x][64W]*/,
+                                                  const unsigned* __restrict__ list_cnt = nullptr, long long list_thr = 0) {
     __shared__ long long sacc[8][64 * WV];
+    // list_cnt: k_obj_list serves this round when the sampler's list is short (<= list_thr)
+    if (list_cnt && (long long)list_cnt[2] <= list_thr) return;
     const uint64_t pdem = l2_policy_evict_first();  // last reader of the batch: demote it in L2
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int w0 = blockIdx.y * WV;
@@ -600,6 +628,77 @@ __global__ void __launch_bounds__(256) k_obj_bits(long long n, long long cpc, co
     __syncthreads();
     if (threadIdx.x < 64 * WV) {
         long long t = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) t += sacc[k][threadIdx.x];
+        zpart[blockIdx.x * 64LL * W + 64LL * w0 + threadIdx.x] = t;
+    }
+}
+
+// The linear objective of a batch drawn by k_sample from its list: the words of the variables with
+// p = 0 are zero and those with p = 1 all ones, so  z_l = c0 + s1 + sum over the LISTED variables of
+// c_i x_il  (s1 = sum of c_i over p_i = 1, from k_sample_thr).  Chunks of 32 list entries per warp: the
+// coefficient planes of the chunk come from ballots of (c_i - cmin) bits, the batch words are gathered
+// by list index, then the same transposes and popcounts as k_obj_bits; gridDim.x partial rows, CTA 0's
+// row carries s1.  Cost scales with the list (the fractional variables) instead of n.
+template <int WV>
+__global__ void __launch_bounds__(256) k_obj_list(const uint2* __restrict__ list, const unsigned* __restrict__ cnt,
+                                                  const unsigned long long* __restrict__ s1, const double* __restrict__ c,
+                                                  int NB, long long cmin, const uint64_t* __restrict__ X, int W,
+                                                  long long* __restrict__ zpart /*[gridDim.x][64W]*/, long long list_thr) {
+    __shared__ long long sacc[8][64 * WV];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int w0 = blockIdx.y * WV;
+    const long long L = cnt[2];
+    if (L > list_thr) return;  // a long list: k_obj_bits streams every variable instead
+    const long long nch = (L + 31) / 32;
+    long long alo[WV], ahi[WV];
+#pragma unroll
+    for (int v = 0; v < WV; ++v) alo[v] = ahi[v] = 0;
+    for (long long ch = blockIdx.x * 8LL + wib; ch < nch; ch += gridDim.x * 8LL) {
+        const long long e = ch * 32 + lane;
+        uint64_t xw[WV];
+        long long cv = 0;
+        if (e < L) {
+            const unsigned i = __ldg(list + e).x;
+            if constexpr (WV == 2) {
+                const ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(X + (size_t)i * W + w0));
+                xw[0] = a.x; xw[1] = a.y;
+            } else {
+                xw[0] = __ldg(X + (size_t)i * W + w0);
+            }
+            cv = (long long)__ldg(c + i) - cmin;
+        } else {
+#pragma unroll
+            for (int v = 0; v < WV; ++v) xw[v] = 0ull;
+        }
+        unsigned tlo[WV], thi[WV];
+#pragma unroll
+        for (int v = 0; v < WV; ++v) {
+            tlo[v] = transpose32((unsigned)xw[v], lane);
+            thi[v] = transpose32((unsigned)(xw[v] >> 32), lane);
+        }
+        int slo[WV], shi[WV];
+#pragma unroll
+        for (int v = 0; v < WV; ++v) { slo[v] = 0; shi[v] = 0; }
+        for (int b = 0; b < NB; ++b) {
+            const unsigned pl = __ballot_sync(0xffffffffu, (cv >> b) & 1);
+#pragma unroll
+            for (int v = 0; v < WV; ++v) {
+                slo[v] += __popc(tlo[v] & pl) << b;
+                shi[v] += __popc(thi[v] & pl) << b;
+            }
+        }
+#pragma unroll
+        for (int v = 0; v < WV; ++v) {
+            alo[v] += (long long)slo[v] + cmin * __popc(tlo[v]);
+            ahi[v] += (long long)shi[v] + cmin * __popc(thi[v]);
+        }
+    }
+#pragma unroll
+    for (int v = 0; v < WV; ++v) { sacc[wib][64 * v + lane] = alo[v]; sacc[wib][64 * v + 32 + lane] = ahi[v]; }
+    __syncthreads();
+    if (threadIdx.x < 64 * WV) {
+        long long t = (blockIdx.x == 0) ? (long long)s1[1] : 0;
 #pragma unroll
         for (int k = 0; k < 8; ++k) t += sacc[k][threadIdx.x];
         zpart[blockIdx.x * 64LL * W + 64LL * w0 + threadIdx.x] = t;
