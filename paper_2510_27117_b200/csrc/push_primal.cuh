@@ -34,7 +34,8 @@ __global__ void __launch_bounds__(256) k_wlist(State<T> s, PushPrimal pp, const 
     const T* __restrict__ yold = par ? s.y[1] : s.y[0];
     double mx = 0.0;
     const long long m = pp.m;
-    const long long per = ((m + gridDim.x - 1) / gridDim.x + 255) / 256 * 256;
+    constexpr int WU = 4;  // rows per thread and pass (their loads in flight together)
+    const long long per = ((m + gridDim.x - 1) / gridDim.x + 256 * WU - 1) / (256 * WU) * (256 * WU);
     const long long r0 = blockIdx.x * per, r1 = min(m, r0 + per);
     if (threadIdx.x == 0) s_cnt = 0u;
     __syncthreads();
@@ -49,15 +50,22 @@ __global__ void __launch_bounds__(256) k_wlist(State<T> s, PushPrimal pp, const 
         if (threadIdx.x == 0) s_cnt = 0u;
         __syncthreads();
     };
-    for (long long b0 = r0; b0 < r1; b0 += 256) {  // block-uniform trip count
-        const long long j = b0 + threadIdx.x;
-        const double v = j < r1 ? (double)s.w[j] : 0.0;
-        mx = fmax(mx, fabs(v));
-        bool listed = v != 0.0;
-        if (delta) listed = j < r1 && ynew[j] != yold[j];
-        warp_append(listed, (int)j, &s_cnt, s_list);
+    for (long long b0 = r0; b0 < r1; b0 += 256 * WU) {  // block-uniform trip count
+        double v[WU];
+        bool listed[WU];
+#pragma unroll
+        for (int u = 0; u < WU; ++u) {
+            const long long j = b0 + u * 256 + threadIdx.x;
+            v[u] = j < r1 ? (double)s.w[j] : 0.0;
+            listed[u] = delta ? (j < r1 && ynew[j] != yold[j]) : v[u] != 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < WU; ++u) {
+            mx = fmax(mx, fabs(v[u]));
+            warp_append(listed[u], (int)(b0 + u * 256 + threadIdx.x), &s_cnt, s_list);
+        }
         __syncthreads();
-        if (s_cnt > WL_CAP - 256) flush();  // (block-uniform: read after the barrier)
+        if (s_cnt > WL_CAP - 256 * WU) flush();  // (block-uniform: read after the barrier)
     }
     flush();
     mx = block_max<256>(mx, sh);
