@@ -35,7 +35,7 @@ constexpr int RB_NNZ_OF = sizeof(T) == 8 ? RB_NNZ64 : RB_NNZ32;
 // cp.async.ca gathers (measured: dual 2.496 -> 2.470 ms per dense block against ld.global.cs)
 __device__ __forceinline__ int ldcs_i32(const int* p) {
     int v;
-    asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
+    asm("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
     return v;
 }
 
