@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(256) k_sample_thr(const T* __restrict__ xa, co
 // slowest word: a warp runs for the max over its lanes of the SUM of their trips (~33 words each on
 // config 5), not the sum over words of the max.  The last CTA to finish zeroes the list counter for
 // the next round.  Identical output to bernoulli_word.
-constexpr int SMP_CTAS = 6;  // resident CTAs per SM of k_sample (grid = SMP_CTAS x SMs: one wave)
+constexpr int SMP_CTAS = 5;  // resident CTAs per SM of k_sample (grid = SMP_CTAS x SMs: one wave)
 __global__ void __launch_bounds__(256, SMP_CTAS) k_sample(const uint2* __restrict__ list, unsigned* __restrict__ cnt, int W,
                                                          long long word_off, const __grid_constant__ PhiloxKeys rk,
                                                          const Ctrl* __restrict__ ctrl, int r, int kr, unsigned round_fixed,
